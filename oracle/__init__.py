@@ -1,0 +1,215 @@
+"""CPU oracle for the tile-centric mixed-precision GEMM (arxiv 2508.14848).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and the
+cpu_baseline / --impl reference legs of bench.py.  The product package
+(paper_2508_14848_b200) never imports it.  The arithmetic lives in
+gemm_mp_oracle.c (plain C, -ffp-contract=off); this file only marshals numpy
+arrays through ctypes.  Every definition is in DESIGN.md "Oracle definitions".
+"""
+import ctypes as ct
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "gemm_mp_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-shared", "-fPIC"]
+
+
+def build(force=False):
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", *CFLAGS, "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ct.CDLL(_LIB)
+        u64, i64, i32, dbl, vp = ct.c_uint64, ct.c_int64, ct.c_int32, ct.c_double, ct.c_void_p
+        L.orc_mix64.restype = u64; L.orc_mix64.argtypes = [u64]
+        L.orc_splitmix_output.restype = u64; L.orc_splitmix_output.argtypes = [u64, u64]
+        L.orc_uniform.restype = dbl; L.orc_uniform.argtypes = [u64]
+        L.orc_synth_block.restype = None
+        L.orc_synth_block.argtypes = [i64, i64, i32, u64, ct.c_int, ct.c_int, ct.c_int, u64,
+                                      i64, i64, i64, i64, vp, i64]
+        L.orc_encode.restype = ct.c_uint32; L.orc_encode.argtypes = [dbl, ct.c_int]
+        L.orc_decode.restype = dbl; L.orc_decode.argtypes = [ct.c_uint32, ct.c_int]
+        L.orc_encode_array.argtypes = [vp, i64, ct.c_int, vp]
+        L.orc_decode_array.argtypes = [vp, i64, ct.c_int, vp]
+        L.orc_scale_exp.restype = ct.c_int; L.orc_scale_exp.argtypes = [dbl, ct.c_int]
+        L.orc_cnorm.restype = dbl; L.orc_cnorm.argtypes = [vp, i64, i32]
+        L.orc_tile_stats.argtypes = [vp, i64, i64, i64, i32, vp, vp, vp]
+        L.orc_delta.restype = dbl; L.orc_delta.argtypes = [ct.c_int, i32]
+        L.orc_map_input.restype = ct.c_int
+        L.orc_map_input.argtypes = [i64, i64, i32, dbl, ct.c_uint32, vp, vp, vp, vp, vp]
+        L.orc_pack_tile.argtypes = [vp, i64, i32, ct.c_int, ct.c_int, ct.c_int, vp]
+        L.orc_shadow_tile.restype = ct.c_int
+        L.orc_shadow_tile.argtypes = [vp, i32, ct.c_int, ct.c_int, ct.c_int, vp]
+        L.orc_tile_gemm.argtypes = [ct.c_int, vp, vp, i32, vp]
+        L.orc_acc_init.argtypes = [i32, ct.c_int, dbl, vp, ct.c_int, vp]
+        L.orc_fold.argtypes = [i32, ct.c_int, dbl, ct.c_int, ct.c_int, vp, vp]
+        L.orc_finalize.restype = ct.c_int
+        L.orc_finalize.argtypes = [i32, ct.c_int, vp, vp, vp, i64]
+        L.orc_gemm_mp.restype = ct.c_int
+        L.orc_gemm_mp.argtypes = [vp, vp, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp]
+        L.orc_max_threads.restype = ct.c_int
+        L.orc_class_bytes.restype = ct.c_int; L.orc_class_bytes.argtypes = [ct.c_int]
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data_as(ct.c_void_p) if a is not None else None
+
+
+PAYLOAD_DTYPE = {0: np.uint64, 1: np.uint32, 2: np.uint16, 3: np.uint16, 4: np.uint8}
+CLASS_NAMES = ["FP64", "FP32", "FP16", "BF16", "E4M3"]
+
+
+# ---- O1 generator -----------------------------------------------------------
+def splitmix_output(seed, i):
+    return int(lib().orc_splitmix_output(seed, i))
+
+
+def synth_block(rows, cols, nb, seed, mode, E, s, tau, r0=0, nr=None, c0=0, nc=None):
+    nr = rows if nr is None else nr
+    nc = cols if nc is None else nc
+    out = np.empty((nr, nc), dtype=np.float64)
+    lib().orc_synth_block(rows, cols, nb, seed, mode, E, s, tau, r0, nr, c0, nc, _p(out), nc)
+    return out
+
+
+# ---- O2 converters ----------------------------------------------------------
+def encode(x, cls):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.empty(x.shape, dtype=np.uint32)
+    lib().orc_encode_array(_p(x), x.size, cls, _p(out))
+    return out
+
+
+def decode(bits, cls):
+    b = np.ascontiguousarray(bits, dtype=np.uint32)
+    out = np.empty(b.shape, dtype=np.float64)
+    lib().orc_decode_array(_p(b), b.size, cls, _p(out))
+    return out
+
+
+def scale_exp(maxabs, cls):
+    return int(lib().orc_scale_exp(float(maxabs), cls))
+
+
+def delta(cls, nb):
+    return float(lib().orc_delta(cls, nb))
+
+
+# ---- O4 norms / stats -------------------------------------------------------
+def cnorm(tile):
+    t = np.ascontiguousarray(tile, dtype=np.float64)
+    return float(lib().orc_cnorm(_p(t), t.shape[1], t.shape[0]))
+
+
+def tile_stats(X, nb):
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    mt, nt = X.shape[0] // nb, X.shape[1] // nb
+    S = np.empty(mt * nt); M = np.empty(mt * nt); F = np.empty(mt * nt, dtype=np.uint8)
+    lib().orc_tile_stats(_p(X), X.shape[1], mt, nt, nb, _p(S), _p(M), _p(F))
+    return S.reshape(mt, nt), M.reshape(mt, nt), F.reshape(mt, nt)
+
+
+# ---- O5 map of an input matrix --------------------------------------------
+def map_input(S, M, nb, tol, class_mask, finite=None):
+    S = np.ascontiguousarray(S, dtype=np.float64); M = np.ascontiguousarray(M, dtype=np.float64)
+    F = np.ones(S.shape, np.uint8) if finite is None else np.ascontiguousarray(finite, np.uint8)
+    code = np.empty(S.shape, np.uint8); scale = np.empty(S.shape, np.int16)
+    rc = lib().orc_map_input(S.shape[0], S.shape[1], nb, tol, class_mask, _p(S), _p(M), _p(F),
+                             _p(code), _p(scale))
+    return rc, code, scale
+
+
+# ---- O6 packing / shadows -------------------------------------------------
+def pack_tile(tile, cls, scale, kmajor_t=False):
+    t = np.ascontiguousarray(tile, dtype=np.float64)
+    nb = t.shape[0]
+    out = np.empty(nb * nb, dtype=PAYLOAD_DTYPE[cls])
+    lib().orc_pack_tile(_p(t), nb, nb, cls, scale, int(kmajor_t), _p(out))
+    return out
+
+
+def shadow_tile(payload, nb, frm, frm_scale, to):
+    out = np.empty(nb * nb, dtype=PAYLOAD_DTYPE[to])
+    p = np.ascontiguousarray(payload)
+    e = lib().orc_shadow_tile(_p(p), nb, frm, frm_scale, to, _p(out))
+    return out, int(e)
+
+
+def payload_values(payload, cls):
+    if cls == 0:
+        return np.ascontiguousarray(payload).view(np.float64).copy()
+    return decode(payload.astype(np.uint32), cls)
+
+
+# ---- O8 / O9 ----------------------------------------------------------------
+def tile_gemm(cls, a_payload, b_payload, nb):
+    P = np.empty(nb * nb, dtype=np.float64)
+    lib().orc_tile_gemm(cls, _p(np.ascontiguousarray(a_payload)),
+                        _p(np.ascontiguousarray(b_payload)), nb, _p(P))
+    return P.reshape(nb, nb)
+
+
+class _Desc(ct.Structure):
+    _fields_ = [("M", ct.c_int64), ("N", ct.c_int64), ("K", ct.c_int64), ("nb", ct.c_int32),
+                ("tol", ct.c_double), ("alpha", ct.c_double), ("beta", ct.c_double),
+                ("class_mask", ct.c_uint32),
+                ("a_map", ct.c_void_p), ("b_map", ct.c_void_p), ("c_map", ct.c_void_p)]
+
+
+class _Out(ct.Structure):
+    _fields_ = [("acode", ct.c_void_p), ("bcode", ct.c_void_p), ("ccode", ct.c_void_p),
+                ("ascale5", ct.c_void_p), ("bscale5", ct.c_void_p), ("cscale", ct.c_void_p),
+                ("cin_scale", ct.c_void_p),
+                ("SA", ct.c_void_p), ("MA", ct.c_void_p), ("SB", ct.c_void_p),
+                ("MB", ct.c_void_p), ("SC", ct.c_void_p), ("MC", ct.c_void_p),
+                ("threads", ct.c_int)]
+
+
+def gemm_mp(A, B, C, nb, tol, alpha=1.0, beta=0.0, class_mask=0b01111, ctiles=None,
+            a_map=None, b_map=None, c_map=None, Cout=None):
+    """Run the whole method (O1-O9).  Returns a dict with maps, scales and C.
+
+    ctiles: optional list of C tile indices i*nt+j to compute (sampled runs);
+    tiles not listed are left as in `Cout` (default: zeros)."""
+    A = np.ascontiguousarray(A, np.float64); B = np.ascontiguousarray(B, np.float64)
+    M, K = A.shape; K2, N = B.shape
+    assert K == K2
+    C = np.zeros((M, N)) if C is None else np.ascontiguousarray(C, np.float64)
+    mt, nt, kt = M // nb, N // nb, K // nb
+    maps = [None if m is None else np.ascontiguousarray(m, np.uint8) for m in (a_map, b_map, c_map)]
+    d = _Desc(M, N, K, nb, tol, alpha, beta, class_mask, *[_p(m) for m in maps])
+    o = dict(acode=np.zeros((mt, kt), np.uint8), bcode=np.zeros((kt, nt), np.uint8),
+             ccode=np.zeros((mt, nt), np.uint8), ascale5=np.zeros((mt, kt, 5), np.int16),
+             bscale5=np.zeros((kt, nt, 5), np.int16), cscale=np.zeros((mt, nt), np.int16),
+             cin_scale=np.zeros((mt, nt), np.int16),
+             SA=np.zeros((mt, kt)), MA=np.zeros((mt, kt)), SB=np.zeros((kt, nt)),
+             MB=np.zeros((kt, nt)), SC=np.zeros((mt, nt)), MC=np.zeros((mt, nt)))
+    out = _Out(*[_p(o[k]) for k in ["acode", "bcode", "ccode", "ascale5", "bscale5", "cscale",
+                                     "cin_scale", "SA", "MA", "SB", "MB", "SC", "MC"]], 0)
+    Cout = np.zeros((M, N)) if Cout is None else Cout
+    tl = None if ctiles is None else np.ascontiguousarray(ctiles, np.int64)
+    rc = lib().orc_gemm_mp(ct.byref(d), _p(A), K, _p(B), N, _p(C), N, _p(Cout), N, _p(tl),
+                           0 if tl is None else tl.size, ct.byref(out))
+    o["rc"] = rc
+    o["C"] = Cout
+    o["threads"] = out.threads
+    return o
+
+
+def max_threads():
+    return int(lib().orc_max_threads())
