@@ -1,0 +1,170 @@
+/*
+ * gemm_mp.h -- C ABI of the B200-native tile-centric mixed-precision GEMM
+ *
+ *     C <- alpha * A * B + beta * C
+ *
+ * of arxiv 2508.14848 ("Leveraging Hardware-Aware Computation in Mixed-Precision
+ * Matrix Multiply: A Tile-Centric Approach"), Algorithm 1:
+ * A (M x K), B (K x N) and C (M x N) are cut into nb x nb tiles (PAPER.md:145,
+ * 179); every tile of A, B and C carries its own precision (the #, $, * of
+ * PAPER.md:146), chosen here by a tile-norm criterion against a user tolerance
+ * (R1-R5); tiles are converted once into packed low-precision storage;
+ * each tile-GEMM runs at the lower precision of its two operands and is folded
+ * into C at C's tile precision; data moves between GPUs in the STORED precision
+ * and is converted at the receiver.  Multi-GPU: 2D block-cyclic
+ * over a P x Q grid "as square as possible" with a SUMMA schedule
+ * (PAPER.md:145).
+ *
+ * Conventions (all entry points):
+ *   - extern "C", no C++ types; every call returns gmp_status_t and never throws.
+ *     On error, gemm_mp_last_error() returns a thread-local message.
+ *   - Memory ownership: the CALLER owns all device memory (operands, scratch,
+ *     workspace), the CUDA stream and the NCCL communicator.  A plan owns host
+ *     metadata only (tile maps, job lists); gemm_mp_destroy frees it.
+ *   - Pointers named A, B, C, scratch, ws are DEVICE pointers; pointers named
+ *     host_* or the optional maps in gmp_desc_t are HOST pointers.
+ *   - Operand layout: binary64, row-major, leading dimension in elements.  On a
+ *     P x Q grid each rank passes ITS LOCAL tiles only, packed block-cyclically:
+ *     rank (p, q) = rank p*Q + q holds the tiles (i, l) of A with i = p mod P,
+ *     l = q mod Q at local tile position (i div P, l div Q); B tiles (l, j) with
+ *     l = p mod P, j = q mod Q; C tiles (i, j) with i = p mod P, j = q mod Q.
+ *     P = Q = 1 is the ordinary single-GPU layout.
+ *   - Asynchronous calls enqueue work on the given stream; asynchronous CUDA or
+ *     NCCL failures surface at the next call or at gemm_mp_sync.
+ */
+#ifndef GEMM_MP_H
+#define GEMM_MP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Precision classes, ordered by unit roundoff; the class
+ * of a tile-GEMM is max(code_A, code_B) = the lower of its operands' precisions
+ * (north_star; R6). */
+typedef enum { GMP_FP64 = 0, GMP_FP32 = 1, GMP_FP16 = 2, GMP_BF16 = 3, GMP_E4M3 = 4 } gmp_class_t;
+
+typedef enum {
+  GMP_OK = 0,
+  GMP_ERR_ARG = 1,           /* null/invalid argument, tol <= 0 or not finite, ld too small */
+  GMP_ERR_NOT_DIVISIBLE = 2, /* nb does not divide M, N or K, or nb is not a multiple of 128 */
+  GMP_ERR_MAP_SHAPE = 3,     /* explicit map holds a code > 4                                  */
+  GMP_ERR_NONFINITE = 4,     /* A, B (or C with beta != 0) holds a NaN or an infinity          */
+  GMP_ERR_GRID = 5,          /* P*Q, rank and communicator are inconsistent                    */
+  GMP_ERR_WORKSPACE = 6,     /* scratch or workspace smaller than the size query returned      */
+  GMP_ERR_STATE = 7,         /* call out of order (execute before convert, ...)                */
+  GMP_ERR_CUDA = 8,          /* a CUDA runtime/driver call failed                              */
+  GMP_ERR_NCCL = 9,          /* an NCCL call failed                                            */
+  GMP_ERR_UNSUPPORTED = 10   /* configuration outside what this build supports                 */
+} gmp_status_t;
+
+/* flags */
+#define GMP_FLAG_SIMT_ONLY 1u /* run classes 2..4 on the SIMT (binary32 FMA) kernel: cross-check only */
+
+typedef struct {
+  int64_t M, N, K;     /* global GEMM shape                                                    */
+  int32_t nb;          /* tile edge; multiple of 128 dividing M, N, K (PAPER.md:179 uses 1024/2048) */
+  double tol;          /* accuracy tolerance: ||C - C_fp64||_F <= tol (|a| ||A|| ||B|| + |b| ||C||) */
+  double alpha, beta;  /* GEMM scalars; beta == 0 means C is not read (BLAS convention)          */
+  uint32_t class_mask; /* bit c enables class c (gmp_class_t); FP64 always on; E4M3 opt-in        */
+  uint32_t flags;      /* GMP_FLAG_*                                                           */
+  int32_t P, Q, rank;  /* process grid and this rank (= p*Q + q); 1, 1, 0 on one GPU            */
+  /* optional explicit per-tile codes (host, row-major global tile grids: mt x kt, kt x nt,
+   * mt x nt) -- the paper's own "aD:bS" experiment mode.  NULL = criterion. */
+  const uint8_t *a_map, *b_map, *c_map;
+} gmp_desc_t;
+
+typedef struct gmp_plan_s *gmp_plan_t;
+
+/* Run statistics (gemm_mp_get_stats). Counts are global (identical on every rank)
+ * except the *_local fields. */
+typedef struct {
+  int64_t tiles_a[5], tiles_b[5], tiles_c[5]; /* tiles per stored class                  */
+  int64_t pairs[5];                           /* tile-GEMMs per pair class (global)      */
+  double flops[5];                            /* 2 nb^3 x pairs[c]                       */
+  int64_t pairs_local[5];                     /* tile-GEMMs this rank computes            */
+  int64_t shadows_local[5];                   /* shadow tiles this rank materialises      */
+  int64_t packed_bytes_local;                 /* packed A/B payload bytes stored locally  */
+  int64_t recv_bytes_local;                   /* SUMMA panel bytes this rank receives     */
+  int64_t workspace_bytes;
+  int32_t steps;                              /* SUMMA steps (K tiles / step depth)        */
+  int32_t launches_execute;                   /* kernels one gemm_mp_execute launches      */
+} gmp_stats_t;
+
+/* Device scratch needed by gemm_mp_plan (tile statistics + maps; KB-sized).     */
+gmp_status_t gemm_mp_scratch_size(const gmp_desc_t *desc, size_t *bytes);
+
+/* S1 + S2 of SURVEY 8(a): per-tile canonical sums of squares and maxabs of the
+ * local tiles (map-stats kernel), an all-reduce of the statistics over the grid
+ * (NCCL, P*Q > 1), the precision map / scale kernel, then ONE host
+ * synchronisation to read the maps back and size the packed arena.
+ * A, B (and C if beta != 0) must stay unchanged until gemm_mp_convert has
+ * completed on the stream.  nccl_comm: ncclComm_t of all P*Q ranks, NULL iff
+ * P*Q == 1.  Collective over the grid.  On success *out is a new plan.        */
+gmp_status_t gemm_mp_plan(const gmp_desc_t *desc, const double *A, int64_t lda, const double *B,
+                          int64_t ldb, const double *C, int64_t ldc, void *scratch,
+                          size_t scratch_bytes, void *nccl_comm, void *stream, gmp_plan_t *out);
+
+/* Device workspace for convert + execute: job tables, packed arenas (stored,
+ * shadows, SUMMA receive slots), W accumulators, packed C_in / C_out.          */
+gmp_status_t gemm_mp_workspace_size(gmp_plan_t plan, size_t *bytes);
+
+/* S3 + S5 (local tiles): convert-and-pack every local tile of A, B (and C_in)
+ * into its class with one RNE rounding and its power-of-two scale, then the
+ * receiver-side shadows needed by local tile-GEMMs.  Async on `stream`.  After
+ * completion A and B may be freed.  ws stays owned by the caller and must
+ * outlive every execute of this plan.                                          */
+gmp_status_t gemm_mp_convert(gmp_plan_t plan, void *ws, size_t ws_bytes, void *stream);
+
+/* S4 - S7: per SUMMA step, NCCL broadcasts of the step's A/B panels in stored
+ * precision (P*Q > 1) + shadows of received tiles on a comm stream, then one
+ * grouped tile-GEMM launch per precision class present, folding into the W
+ * accumulators; finally C-finalize writes the packed C and the binary64 user C
+ * (local layout, ldc).  Collective over the grid.  Async on `stream`; may be
+ * called repeatedly after one convert.                                          */
+gmp_status_t gemm_mp_execute(gmp_plan_t plan, double *C, int64_t ldc, void *stream);
+
+/* Waits for the plan's streams; returns the first asynchronous error.          */
+gmp_status_t gemm_mp_sync(gmp_plan_t plan);
+
+/* Global precision maps (host arrays, row-major tile grids) and STORED scales.
+ * Any pointer may be NULL.  C scales are the finalize scales of the last
+ * execute for local tiles (0 elsewhere).                                       */
+gmp_status_t gemm_mp_get_maps(gmp_plan_t plan, uint8_t *a, uint8_t *b, uint8_t *c, int16_t *a_scale,
+                              int16_t *b_scale, int16_t *c_scale);
+
+/* Copies one LOCAL tile's payload to host memory: which = 'A' or 'B' (class
+ * `cls` = the stored code or a materialised shadow class), 'C' (packed C_out of
+ * the last execute, cls = code), 'I' (packed C_in), 'W' (accumulator, binary64
+ * or binary32).  (ti, tj) are GLOBAL tile indices.  *bytes in: capacity, out:
+ * bytes written; *scale receives the tile's power-of-two scale.  Synchronous. */
+gmp_status_t gemm_mp_get_tile(gmp_plan_t plan, char which, int64_t ti, int64_t tj, int32_t cls,
+                              void *host_dst, size_t *bytes, int16_t *scale);
+
+gmp_status_t gemm_mp_get_stats(gmp_plan_t plan, gmp_stats_t *out);
+
+/* NCCL bootstrap helpers (the unique id travels over torch.distributed).      */
+gmp_status_t gemm_mp_nccl_unique_id(void *out128);
+gmp_status_t gemm_mp_nccl_comm_create(const void *id128, int nranks, int rank, void **comm);
+gmp_status_t gemm_mp_nccl_comm_destroy(void *comm);
+
+/* N1 synthetic generator (benchmark inputs): fills
+ * the local block-cyclic part of a rows x cols global matrix.  mode 0 uniform,
+ * 1 graded, 2 random.  Async.                                                  */
+gmp_status_t gemm_mp_synth(double *out, int64_t ld, int64_t rows, int64_t cols, int32_t nb,
+                           int32_t P, int32_t Q, int32_t p, int32_t q, uint64_t seed,
+                           uint64_t tau, int32_t mode, int32_t E, int32_t s, void *stream);
+
+/* Frees the plan's host metadata (NULL-safe).                                  */
+void gemm_mp_destroy(gmp_plan_t plan);
+
+/* Thread-local message of the last failing call on this thread.               */
+const char *gemm_mp_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GEMM_MP_H */

@@ -1,0 +1,216 @@
+"""Thin ctypes binding of include/gemm_mp.h -- argument marshalling only.
+
+Same names as the C ABI.  Every step of the method runs in libgemm_mp.so's CUDA
+kernels; there is no CPU or PyTorch fallback: if the library cannot be loaded
+the import fails loudly.  PyTorch is used by callers for device memory and
+streams only (pointers are passed as integers)."""
+import ctypes as ct
+import os
+import re
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgemm_mp.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "gemm_mp.h")
+
+GMP_FP64, GMP_FP32, GMP_FP16, GMP_BF16, GMP_E4M3 = range(5)
+CLASS_NAMES = ["FP64", "FP32", "FP16", "BF16", "E4M3"]
+CLASS_BYTES = [8, 4, 2, 2, 1]
+GMP_FLAG_SIMT_ONLY = 1
+STATUS = ["GMP_OK", "GMP_ERR_ARG", "GMP_ERR_NOT_DIVISIBLE", "GMP_ERR_MAP_SHAPE", "GMP_ERR_NONFINITE",
+          "GMP_ERR_GRID", "GMP_ERR_WORKSPACE", "GMP_ERR_STATE", "GMP_ERR_CUDA", "GMP_ERR_NCCL",
+          "GMP_ERR_UNSUPPORTED"]
+
+
+class GmpError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{STATUS[code] if 0 <= code < len(STATUS) else code}: {msg}")
+        self.code = code
+
+
+class gmp_desc_t(ct.Structure):
+    _fields_ = [("M", ct.c_int64), ("N", ct.c_int64), ("K", ct.c_int64), ("nb", ct.c_int32),
+                ("tol", ct.c_double), ("alpha", ct.c_double), ("beta", ct.c_double),
+                ("class_mask", ct.c_uint32), ("flags", ct.c_uint32),
+                ("P", ct.c_int32), ("Q", ct.c_int32), ("rank", ct.c_int32),
+                ("a_map", ct.c_void_p), ("b_map", ct.c_void_p), ("c_map", ct.c_void_p)]
+
+
+class gmp_stats_t(ct.Structure):
+    _fields_ = [("tiles_a", ct.c_int64 * 5), ("tiles_b", ct.c_int64 * 5), ("tiles_c", ct.c_int64 * 5),
+                ("pairs", ct.c_int64 * 5), ("flops", ct.c_double * 5), ("pairs_local", ct.c_int64 * 5),
+                ("shadows_local", ct.c_int64 * 5), ("packed_bytes_local", ct.c_int64),
+                ("recv_bytes_local", ct.c_int64), ("workspace_bytes", ct.c_int64),
+                ("steps", ct.c_int32), ("launches_execute", ct.c_int32)]
+
+    def as_dict(self):
+        d = {}
+        for name, _ in self._fields_:
+            v = getattr(self, name)
+            d[name] = list(v) if hasattr(v, "__len__") else v
+        return d
+
+
+_lib = None
+
+
+def lib():
+    """Loads libgemm_mp.so (raises if it is missing: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                              "(the CUDA path has no fallback)")
+        L = ct.CDLL(LIB_PATH)
+        vp, i64, i32, u64, st = ct.c_void_p, ct.c_int64, ct.c_int32, ct.c_uint64, ct.c_int
+        sig = {
+            "gemm_mp_scratch_size": [ct.POINTER(gmp_desc_t), ct.POINTER(ct.c_size_t)],
+            "gemm_mp_plan": [ct.POINTER(gmp_desc_t), vp, i64, vp, i64, vp, i64, vp, ct.c_size_t, vp, vp,
+                             ct.POINTER(vp)],
+            "gemm_mp_workspace_size": [vp, ct.POINTER(ct.c_size_t)],
+            "gemm_mp_convert": [vp, vp, ct.c_size_t, vp],
+            "gemm_mp_execute": [vp, vp, i64, vp],
+            "gemm_mp_sync": [vp],
+            "gemm_mp_get_maps": [vp, vp, vp, vp, vp, vp, vp],
+            "gemm_mp_get_tile": [vp, ct.c_char, i64, i64, i32, vp, ct.POINTER(ct.c_size_t),
+                                 ct.POINTER(ct.c_int16)],
+            "gemm_mp_get_stats": [vp, ct.POINTER(gmp_stats_t)],
+            "gemm_mp_nccl_unique_id": [vp],
+            "gemm_mp_nccl_comm_create": [vp, ct.c_int, ct.c_int, ct.POINTER(vp)],
+            "gemm_mp_nccl_comm_destroy": [vp],
+            "gemm_mp_synth": [vp, i64, i64, i64, i32, i32, i32, i32, i32, u64, u64, i32, i32, i32, vp],
+        }
+        for name, args in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = st
+        L.gemm_mp_destroy.argtypes = [vp]
+        L.gemm_mp_destroy.restype = None
+        L.gemm_mp_last_error.argtypes = []
+        L.gemm_mp_last_error.restype = ct.c_char_p
+        _lib = L
+    return _lib
+
+
+def header_symbols():
+    """Entry points declared in include/gemm_mp.h."""
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(gemm_mp_\w+)\s*\(", txt)))
+
+
+def _check(rc):
+    if rc != 0:
+        raise GmpError(rc, lib().gemm_mp_last_error().decode())
+
+
+def _ptr(x):
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    return x.data_ptr()
+
+
+def _stream(s):
+    if s is None:
+        return None
+    if isinstance(s, int):
+        return s
+    return s.cuda_stream
+
+
+def make_desc(M, N, K, nb, tol, alpha=1.0, beta=0.0, class_mask=0b01111, flags=0, P=1, Q=1, rank=0,
+              a_map=None, b_map=None, c_map=None):
+    """gmp_desc_t; explicit maps are numpy uint8 arrays kept alive on the struct."""
+    import numpy as np
+    maps = [None if m is None else np.ascontiguousarray(m, dtype=np.uint8) for m in (a_map, b_map, c_map)]
+    d = gmp_desc_t(M, N, K, nb, tol, alpha, beta, class_mask, flags, P, Q, rank,
+                   *[None if m is None else m.ctypes.data for m in maps])
+    d._keep = maps
+    return d
+
+
+def gemm_mp_scratch_size(desc):
+    n = ct.c_size_t()
+    _check(lib().gemm_mp_scratch_size(ct.byref(desc), ct.byref(n)))
+    return n.value
+
+
+def gemm_mp_plan(desc, A, lda, B, ldb, C, ldc, scratch, scratch_bytes, nccl_comm=None, stream=None):
+    h = ct.c_void_p()
+    _check(lib().gemm_mp_plan(ct.byref(desc), _ptr(A), lda, _ptr(B), ldb, _ptr(C), ldc, _ptr(scratch),
+                              scratch_bytes, nccl_comm, _stream(stream), ct.byref(h)))
+    return h.value
+
+
+def gemm_mp_workspace_size(plan):
+    n = ct.c_size_t()
+    _check(lib().gemm_mp_workspace_size(plan, ct.byref(n)))
+    return n.value
+
+
+def gemm_mp_convert(plan, ws, ws_bytes, stream=None):
+    _check(lib().gemm_mp_convert(plan, _ptr(ws), ws_bytes, _stream(stream)))
+
+
+def gemm_mp_execute(plan, C, ldc, stream=None):
+    _check(lib().gemm_mp_execute(plan, _ptr(C), ldc, _stream(stream)))
+
+
+def gemm_mp_sync(plan):
+    _check(lib().gemm_mp_sync(plan))
+
+
+def gemm_mp_get_maps(plan, mt, nt, kt):
+    import numpy as np
+    a = np.zeros((mt, kt), np.uint8); b = np.zeros((kt, nt), np.uint8); c = np.zeros((mt, nt), np.uint8)
+    as_ = np.zeros((mt, kt), np.int16); bs = np.zeros((kt, nt), np.int16); cs = np.zeros((mt, nt), np.int16)
+    _check(lib().gemm_mp_get_maps(plan, *[x.ctypes.data for x in (a, b, c, as_, bs, cs)]))
+    return dict(acode=a, bcode=b, ccode=c, ascale=as_, bscale=bs, cscale=cs)
+
+
+def gemm_mp_get_tile(plan, which, ti, tj, cls, nb):
+    import numpy as np
+    cap = nb * nb * 8
+    buf = np.empty(cap, np.uint8)
+    n = ct.c_size_t(cap)
+    sc = ct.c_int16()
+    _check(lib().gemm_mp_get_tile(plan, which.encode() if isinstance(which, str) else which, ti, tj, cls,
+                                  buf.ctypes.data, ct.byref(n), ct.byref(sc)))
+    return buf[:n.value].copy(), sc.value
+
+
+def gemm_mp_get_stats(plan):
+    s = gmp_stats_t()
+    _check(lib().gemm_mp_get_stats(plan, ct.byref(s)))
+    return s.as_dict()
+
+
+def gemm_mp_nccl_unique_id():
+    buf = (ct.c_char * 128)()
+    _check(lib().gemm_mp_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def gemm_mp_nccl_comm_create(uid, nranks, rank):
+    h = ct.c_void_p()
+    b = (ct.c_char * 128).from_buffer_copy(uid)
+    _check(lib().gemm_mp_nccl_comm_create(b, nranks, rank, ct.byref(h)))
+    return h.value
+
+
+def gemm_mp_nccl_comm_destroy(comm):
+    _check(lib().gemm_mp_nccl_comm_destroy(comm))
+
+
+def gemm_mp_synth(out, ld, rows, cols, nb, P, Q, p, q, seed, tau, mode, E, s, stream=None):
+    _check(lib().gemm_mp_synth(_ptr(out), ld, rows, cols, nb, P, Q, p, q, seed, tau, mode, E, s,
+                               _stream(stream)))
+
+
+def gemm_mp_destroy(plan):
+    if plan:
+        lib().gemm_mp_destroy(plan)
+
+
+def gemm_mp_last_error():
+    return lib().gemm_mp_last_error().decode()

@@ -1,0 +1,795 @@
+// gemm_mp_api.cu -- the C ABI (include/gemm_mp.h) of the B200-native tile-centric
+// mixed-precision GEMM: plan object, workspace layout, job lists, launches and
+// the SUMMA schedule over NCCL.  Every step of the method runs in the kernels of
+// gmp_*.cuh; the host only does bookkeeping (tile lists, offsets, launch order).
+#include "gemm_mp.h"
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <memory>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "gmp_common.cuh"
+#include "gmp_convert.cuh"
+#include "gmp_map.cuh"
+#include "gmp_simt.cuh"
+#include "gmp_tc.cuh"
+
+using namespace gmp;
+
+// ---------------------------------------------------------------------------
+// error handling
+// ---------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+static gmp_status_t fail(gmp_status_t s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+#define GMP_CUDA(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(GMP_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
+#define GMP_NCCL(call)                                                                   \
+  do {                                                                                   \
+    ncclResult_t r_ = (call);                                                            \
+    if (r_ != ncclSuccess)                                                               \
+      return fail(GMP_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_));     \
+  } while (0)
+#define GMP_TRY(call)                 \
+  do {                                \
+    gmp_status_t s_ = (call);         \
+    if (s_ != GMP_OK) return s_;      \
+  } while (0)
+
+static inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// ---------------------------------------------------------------------------
+// plan
+// ---------------------------------------------------------------------------
+struct Launch {
+  int step, cls, kind;  // kind 0: SIMT kernel, 1: tcgen05 kernel
+  int64_t ibeg, icount;
+};
+
+struct Bcast {           // one SUMMA broadcast of a stored tile in a step
+  int which;             // 0: A on the row communicator, 1: B on the column communicator
+  int root;              // root rank inside that communicator
+  int64_t off;           // byte offset of the payload slot (root: its stored tile)
+  int64_t bytes;
+};
+
+struct gmp_plan_s {
+  gmp_desc_t d{};
+  int64_t mt = 0, nt = 0, kt = 0, nA = 0, nB = 0, nC = 0;
+  int P = 1, Q = 1, p = 0, q = 0;
+  const double *A = nullptr, *B = nullptr, *C = nullptr;
+  int64_t lda = 0, ldb = 0, ldc = 0;
+  ncclComm_t world = nullptr, rowc = nullptr, colc = nullptr;
+  cudaStream_t comm_stream = nullptr;
+  std::vector<cudaEvent_t> step_ev;
+  // global maps (identical on every rank)
+  std::vector<uint8_t> codeA, codeB, codeC;
+  std::vector<int16_t> sA5, sB5, sCin, sCout;
+  // local tiles (global indices), C local position
+  std::vector<int64_t> locA, locB, locC;
+  // slots: [global tile][class] -> slot in that class's arena, -1 if absent
+  std::vector<int32_t> slotA5, slotB5;
+  int64_t arena_off[5] = {0}, arena_slots[5] = {0};
+  int64_t slot_bytes[5] = {0};
+  // tables
+  std::vector<PackJob> pack;
+  std::vector<ShadowJob> shadow_local;
+  std::vector<std::vector<ShadowJob>> shadow_step;   // receiver-side shadows per step
+  std::vector<std::vector<Bcast>> bcast_step;
+  std::vector<CTileDesc> ctd;
+  std::vector<WorkItem> items;
+  std::vector<PairDesc> pairs;
+  std::vector<Launch> launches;
+  std::vector<int64_t> shadow_step_off;   // element offset of each step's shadow jobs
+  // workspace layout (byte offsets)
+  int64_t off_pack = 0, off_shadow = 0, off_ctd = 0, off_items = 0, off_pairs = 0, off_maxbits = 0,
+          off_cscale = 0, off_tc = 0, ws_bytes = 0;
+  TcTables tc;
+  uint8_t* ws = nullptr;
+  bool converted = false;
+  bool executed = false;
+  gmp_stats_t st{};
+};
+
+extern "C" const char* gemm_mp_last_error(void) { return g_err.c_str(); }
+
+static gmp_status_t check_desc(const gmp_desc_t* d) {
+  if (!d) return fail(GMP_ERR_ARG, "desc is NULL");
+  if (d->nb <= 0 || d->M <= 0 || d->N <= 0 || d->K <= 0) return fail(GMP_ERR_ARG, "non-positive shape or nb");
+  if (d->nb % 128) return fail(GMP_ERR_NOT_DIVISIBLE, "nb must be a multiple of 128");
+  if (d->M % d->nb || d->N % d->nb || d->K % d->nb)
+    return fail(GMP_ERR_NOT_DIVISIBLE, "nb must divide M, N and K");
+  if (!(d->tol > 0.0) || !std::isfinite(d->tol)) return fail(GMP_ERR_ARG, "tol must be positive and finite");
+  if (!std::isfinite(d->alpha) || !std::isfinite(d->beta)) return fail(GMP_ERR_ARG, "alpha/beta not finite");
+  if (d->P < 1 || d->Q < 1 || d->rank < 0 || d->rank >= d->P * d->Q)
+    return fail(GMP_ERR_GRID, "invalid process grid / rank");
+  return GMP_OK;
+}
+
+// local tile counts of a block-cyclic dimension: tiles g with g % P == p
+static inline int64_t nloc(int64_t n, int P, int p) { return n > p ? (n - p + P - 1) / P : 0; }
+
+struct ScratchLayout {
+  int64_t S, F, codes, s5, scin, status, maps, jobs, total;
+};
+static ScratchLayout scratch_layout(const gmp_desc_t* d) {
+  const int64_t mt = d->M / d->nb, nt = d->N / d->nb, kt = d->K / d->nb;
+  const int64_t nA = mt * kt, nB = kt * nt, nC = mt * nt, n = nA + nB + nC;
+  ScratchLayout L{};
+  int64_t o = 0;
+  L.S = o; o = align_up(o + 2 * n * 8, 256);       // S then maxabs for A|B|C
+  L.F = o; o = align_up(o + n, 256);
+  L.codes = o; o = align_up(o + n, 256);
+  L.s5 = o; o = align_up(o + (nA + nB) * 5 * 2, 256);
+  L.scin = o; o = align_up(o + nC * 2, 256);
+  L.status = o; o = align_up(o + 16, 256);
+  L.maps = o; o = align_up(o + n, 256);
+  L.jobs = o; o = align_up(o + n * (int64_t)sizeof(StatsJob), 256);
+  L.total = o;
+  return L;
+}
+
+extern "C" gmp_status_t gemm_mp_scratch_size(const gmp_desc_t* desc, size_t* bytes) {
+  GMP_TRY(check_desc(desc));
+  if (!bytes) return fail(GMP_ERR_ARG, "bytes is NULL");
+  *bytes = (size_t)scratch_layout(desc).total;
+  return GMP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// host-side bookkeeping after the maps are known
+// ---------------------------------------------------------------------------
+static void build_tables(gmp_plan_s* pl) {
+  const gmp_desc_t& d = pl->d;
+  const int64_t nb = d.nb, nb2 = nb * nb, mt = pl->mt, nt = pl->nt, kt = pl->kt;
+  const int P = pl->P, Q = pl->Q, p = pl->p, q = pl->q;
+  const bool hasC = d.beta != 0.0;
+  for (int c = 0; c < 5; ++c) pl->slot_bytes[c] = nb2 * class_bytes(c);
+
+  // ---- which A/B tiles (and classes) this rank needs ----
+  std::vector<uint8_t> needA(pl->nA * 5, 0), needB(pl->nB * 5, 0);
+  int64_t pairs_cls[5] = {0}, pairs_loc[5] = {0};
+  for (int64_t i = 0; i < mt; ++i)
+    for (int64_t j = 0; j < nt; ++j)
+      for (int64_t l = 0; l < kt; ++l) {
+        const int ca = pl->codeA[i * kt + l], cb = pl->codeB[l * nt + j], c = std::max(ca, cb);
+        pairs_cls[c]++;
+        if (i % P != p || j % Q != q) continue;
+        pairs_loc[c]++;
+        needA[(i * kt + l) * 5 + ca] = 1;
+        needA[(i * kt + l) * 5 + c] = 1;
+        needB[(l * nt + j) * 5 + cb] = 1;
+        needB[(l * nt + j) * 5 + c] = 1;
+      }
+  // every A tile of this process row and B tile of this process column keeps a
+  // stored-precision slot: local tiles are broadcast roots, the others are
+  // received (every rank of a row/column takes part in the broadcast)
+  for (int64_t g = 0; g < pl->nA; ++g)
+    if ((g / kt) % P == p) needA[g * 5 + pl->codeA[g]] = 1;
+  for (int64_t g = 0; g < pl->nB; ++g)
+    if ((g % nt) % Q == q) needB[g * 5 + pl->codeB[g]] = 1;
+
+  // ---- arena slots ----
+  pl->slotA5.assign(pl->nA * 5, -1);
+  pl->slotB5.assign(pl->nB * 5, -1);
+  int64_t nslots[5] = {0};
+  for (int64_t g = 0; g < pl->nA; ++g)
+    for (int c = 0; c < 5; ++c)
+      if (needA[g * 5 + c]) pl->slotA5[g * 5 + c] = (int32_t)nslots[c]++;
+  for (int64_t g = 0; g < pl->nB; ++g)
+    for (int c = 0; c < 5; ++c)
+      if (needB[g * 5 + c]) pl->slotB5[g * 5 + c] = (int32_t)nslots[c]++;
+
+  // ---- local C tiles ----
+  const int64_t nCl = (int64_t)pl->locC.size();
+  pl->ctd.resize(nCl);
+
+  // ---- workspace layout ----
+  // tables are sized below; compute the rest first with a placeholder base
+  std::vector<int64_t> ctile_of_global(pl->nC, -1);
+  for (int64_t k = 0; k < nCl; ++k) ctile_of_global[pl->locC[k]] = k;
+
+  // ---- pack jobs (local A, B tiles; C_in) ----
+  pl->pack.clear();
+  auto arena = [&](int c, int32_t slot) { return pl->arena_off[c] + (int64_t)slot * pl->slot_bytes[c]; };
+
+  // ---- pairs / items per (step, class) ----
+  pl->pairs.clear();
+  pl->items.clear();
+  pl->launches.clear();
+  const int steps = (int)((kt + GMP_STEP_DEPTH - 1) / GMP_STEP_DEPTH);
+  struct Tmp { int64_t ct; int64_t pbeg, pcnt; };
+  // we need arena offsets before pairs: finish the layout first
+  int64_t o = 0;
+  const int64_t tables_guess = 0;
+  (void)tables_guess;
+  // count items to size tables
+  int64_t n_pairs = 0, n_items = 0;
+  for (int s = 0; s < steps; ++s)
+    for (int c = 4; c >= 0; --c)
+      for (int64_t k = 0; k < nCl; ++k) {
+        const int64_t g = pl->locC[k], i = g / nt, j = g % nt;
+        int64_t cnt = 0;
+        for (int64_t l = (int64_t)s * GMP_STEP_DEPTH; l < std::min<int64_t>(kt, (int64_t)(s + 1) * GMP_STEP_DEPTH); ++l)
+          if (std::max(pl->codeA[i * kt + l], pl->codeB[l * nt + j]) == c) ++cnt;
+        if (!cnt) continue;
+        n_pairs += cnt;
+        const bool tc = kTcAvailable && (c >= 2) && !(d.flags & GMP_FLAG_SIMT_ONLY);
+        n_items += tc ? tc_items_per_tile(nb) : (nb / 128) * (nb / simt_bn_rt(c));
+      }
+  const int64_t n_pack = (int64_t)pl->locA.size() + (int64_t)pl->locB.size() + (hasC ? nCl : 0);
+  int64_t n_shadow_local = 0, n_shadow_recv = 0;
+  for (int64_t g = 0; g < pl->nA; ++g)
+    for (int c = pl->codeA[g] + 1; c < 5; ++c)
+      if (needA[g * 5 + c]) ((g % kt) % Q == q ? n_shadow_local : n_shadow_recv)++;
+  for (int64_t g = 0; g < pl->nB; ++g)
+    for (int c = pl->codeB[g] + 1; c < 5; ++c)
+      if (needB[g * 5 + c]) ((g / nt) % P == p ? n_shadow_local : n_shadow_recv)++;
+
+  pl->off_pack = o; o = align_up(o + n_pack * (int64_t)sizeof(PackJob), 1024);
+  pl->off_shadow = o; o = align_up(o + (n_shadow_local + n_shadow_recv) * (int64_t)sizeof(ShadowJob), 1024);
+  pl->off_ctd = o; o = align_up(o + nCl * (int64_t)sizeof(CTileDesc), 1024);
+  pl->off_items = o; o = align_up(o + n_items * (int64_t)sizeof(WorkItem), 1024);
+  pl->off_pairs = o; o = align_up(o + n_pairs * (int64_t)sizeof(PairDesc), 1024);
+  pl->off_maxbits = o; o = align_up(o + nCl * 8, 1024);
+  pl->off_cscale = o; o = align_up(o + nCl * 2, 1024);
+  pl->off_tc = o; o = align_up(o + 1024, 1024);
+  for (int c = 0; c < 5; ++c) {
+    pl->arena_off[c] = o;
+    pl->arena_slots[c] = nslots[c];
+    o = align_up(o + nslots[c] * pl->slot_bytes[c], 1024);
+  }
+  for (int64_t k = 0; k < nCl; ++k) {
+    const int64_t g = pl->locC[k];
+    CTileDesc& t = pl->ctd[k];
+    t.code = pl->codeC[g];
+    t.cin_scale = hasC ? pl->sCin[g] : 0;
+    t.w_off = o; o = align_up(o + nb2 * (t.code == 0 ? 8 : 4), 1024);
+    if (hasC) { t.cin_off = o; o = align_up(o + nb2 * class_bytes(t.code), 1024); }
+    else t.cin_off = -1;
+    t.cout_off = o; o = align_up(o + nb2 * class_bytes(t.code), 1024);
+    const int64_t i = g / nt, j = g % nt;
+    t.user_off = -1;  // set at execute (depends on ldc)
+    t.pad = (int32_t)(((i / P) << 16) | (j / Q));  // local tile coordinates (il, jl)
+  }
+  pl->ws_bytes = o;
+
+  // ---- pack jobs ----
+  for (int64_t g : pl->locA) {
+    const int64_t i = g / kt, l = g % kt, il = i / P, ll = l / Q;
+    PackJob pj{};
+    pj.src = pl->A + il * nb * pl->lda + ll * nb;
+    pj.ld = pl->lda;
+    pj.cls = pl->codeA[g];
+    pj.scale = pl->sA5[g * 5 + pj.cls];
+    pj.transpose = 0;
+    pj.dst_off = arena(pj.cls, pl->slotA5[g * 5 + pj.cls]);
+    pl->pack.push_back(pj);
+  }
+  for (int64_t g : pl->locB) {
+    const int64_t l = g / nt, j = g % nt, ll = l / P, jl = j / Q;
+    PackJob pj{};
+    pj.src = pl->B + ll * nb * pl->ldb + jl * nb;
+    pj.ld = pl->ldb;
+    pj.cls = pl->codeB[g];
+    pj.scale = pl->sB5[g * 5 + pj.cls];
+    pj.transpose = 1;
+    pj.dst_off = arena(pj.cls, pl->slotB5[g * 5 + pj.cls]);
+    pl->pack.push_back(pj);
+  }
+  if (hasC)
+    for (int64_t k = 0; k < nCl; ++k) {
+      const int64_t g = pl->locC[k], i = g / nt, j = g % nt;
+      PackJob pj{};
+      pj.src = pl->C + (i / P) * nb * pl->ldc + (j / Q) * nb;
+      pj.ld = pl->ldc;
+      pj.cls = pl->codeC[g];
+      pj.scale = pl->sCin[g];
+      pj.transpose = 0;
+      pj.dst_off = pl->ctd[k].cin_off;
+      pl->pack.push_back(pj);
+    }
+
+  // ---- shadow jobs: local tiles now, received tiles per step ----
+  pl->shadow_local.clear();
+  pl->shadow_step.assign(steps, {});
+  auto add_shadows = [&](bool isB, int64_t g) {
+    const int code = isB ? pl->codeB[g] : pl->codeA[g];
+    const int16_t* s5 = (isB ? pl->sB5.data() : pl->sA5.data()) + g * 5;
+    const int32_t* sl = (isB ? pl->slotB5.data() : pl->slotA5.data()) + g * 5;
+    const bool local = isB ? ((g / nt) % P == p) : ((g % kt) % Q == q);
+    const int64_t l = isB ? g / nt : g % kt;
+    for (int c = code + 1; c < 5; ++c) {
+      if (sl[c] < 0) continue;
+      ShadowJob sj{};
+      sj.src_off = arena(code, sl[code]);
+      sj.dst_off = arena(c, sl[c]);
+      sj.from = (int16_t)code;
+      sj.to = (int16_t)c;
+      sj.d = (int16_t)(s5[c] - s5[code]);
+      if (local) pl->shadow_local.push_back(sj);
+      else pl->shadow_step[l / GMP_STEP_DEPTH].push_back(sj);
+    }
+  };
+  for (int64_t g = 0; g < pl->nA; ++g) add_shadows(false, g);
+  for (int64_t g = 0; g < pl->nB; ++g) add_shadows(true, g);
+  pl->shadow_step_off.assign(steps, 0);
+  {
+    int64_t acc = (int64_t)pl->shadow_local.size();
+    for (int s = 0; s < steps; ++s) { pl->shadow_step_off[s] = acc; acc += (int64_t)pl->shadow_step[s].size(); }
+  }
+
+  // ---- SUMMA broadcasts per step (stored bytes) ----
+  pl->bcast_step.assign(steps, {});
+  int64_t recv_bytes = 0;
+  if (P * Q > 1) {
+    for (int64_t l = 0; l < kt; ++l) {
+      const int s = (int)(l / GMP_STEP_DEPTH);
+      for (int64_t i = p; i < mt; i += P) {       // A(i,l) along process row p, root column l % Q
+        const int64_t g = i * kt + l;
+        const int c = pl->codeA[g];
+        Bcast b{0, (int)(l % Q), arena(c, pl->slotA5[g * 5 + c]), pl->slot_bytes[c]};
+        pl->bcast_step[s].push_back(b);
+        if ((int)(l % Q) != q) recv_bytes += b.bytes;
+      }
+      for (int64_t j = q; j < nt; j += Q) {       // B(l,j) along process column q, root row l % P
+        const int64_t g = l * nt + j;
+        const int c = pl->codeB[g];
+        Bcast b{1, (int)(l % P), arena(c, pl->slotB5[g * 5 + c]), pl->slot_bytes[c]};
+        pl->bcast_step[s].push_back(b);
+        if ((int)(l % P) != p) recv_bytes += b.bytes;
+      }
+    }
+  }
+
+  // ---- pairs and work items ----
+  for (int s = 0; s < steps; ++s) {
+    for (int c = 4; c >= 0; --c) {
+      const bool tc = kTcAvailable && (c >= 2) && !(d.flags & GMP_FLAG_SIMT_ONLY);
+      const int64_t ibeg = (int64_t)pl->items.size();
+      std::vector<WorkItem> its;
+      for (int64_t k = 0; k < nCl; ++k) {
+        const int64_t g = pl->locC[k], i = g / nt, j = g % nt;
+        const int64_t pbeg = (int64_t)pl->pairs.size();
+        for (int64_t l = (int64_t)s * GMP_STEP_DEPTH; l < std::min<int64_t>(kt, (int64_t)(s + 1) * GMP_STEP_DEPTH); ++l) {
+          const int ca = pl->codeA[i * kt + l], cb = pl->codeB[l * nt + j];
+          if (std::max(ca, cb) != c) continue;
+          PairDesc pd{};
+          pd.a_off = arena(c, pl->slotA5[(i * kt + l) * 5 + c]);
+          pd.b_off = arena(c, pl->slotB5[(l * nt + j) * 5 + c]);
+          pd.fexp = -(pl->sA5[(i * kt + l) * 5 + c] + pl->sB5[(l * nt + j) * 5 + c]);
+          pd.l = (int32_t)l;
+          pl->pairs.push_back(pd);
+        }
+        const int64_t pcnt = (int64_t)pl->pairs.size() - pbeg;
+        if (!pcnt) continue;
+        if (tc) {
+          tc_make_items(nb, (int32_t)k, (int32_t)pbeg, (int32_t)pcnt, its);
+        } else {
+          for (int64_t m0 = 0; m0 < nb; m0 += 128)
+            for (int64_t n0 = 0; n0 < nb; n0 += simt_bn_rt(c))
+              its.push_back(WorkItem{(int32_t)k, (int32_t)m0, (int32_t)n0, (int32_t)pbeg, (int32_t)pcnt, 0});
+        }
+      }
+      if (its.empty()) continue;
+      std::stable_sort(its.begin(), its.end(), [](const WorkItem& a, const WorkItem& b) { return a.pcnt > b.pcnt; });
+      pl->items.insert(pl->items.end(), its.begin(), its.end());
+      pl->launches.push_back(Launch{s, c, tc ? 1 : 0, ibeg, (int64_t)its.size()});
+    }
+  }
+
+  // ---- stats ----
+  gmp_stats_t& st = pl->st;
+  std::memset(&st, 0, sizeof st);
+  for (int64_t g = 0; g < pl->nA; ++g) st.tiles_a[pl->codeA[g]]++;
+  for (int64_t g = 0; g < pl->nB; ++g) st.tiles_b[pl->codeB[g]]++;
+  for (int64_t g = 0; g < pl->nC; ++g) st.tiles_c[pl->codeC[g]]++;
+  for (int c = 0; c < 5; ++c) {
+    st.pairs[c] = pairs_cls[c];
+    st.pairs_local[c] = pairs_loc[c];
+    st.flops[c] = 2.0 * (double)nb * (double)nb * (double)nb * (double)pairs_cls[c];
+  }
+  for (const auto& sj : pl->shadow_local) st.shadows_local[sj.to]++;
+  for (const auto& v : pl->shadow_step)
+    for (const auto& sj : v) st.shadows_local[sj.to]++;
+  for (const auto& pj : pl->pack) if (pj.dst_off >= pl->arena_off[0]) st.packed_bytes_local += nb2 * class_bytes(pj.cls);
+  st.recv_bytes_local = recv_bytes;
+  st.workspace_bytes = pl->ws_bytes;
+  st.steps = steps;
+  int nl = 2 + 1 + (int)pl->launches.size();  // maxabs memset is not a kernel: init, maxabs, finalize
+  for (int s = 0; s < steps; ++s) if (!pl->shadow_step[s].empty()) ++nl;
+  st.launches_execute = nl;
+}
+
+extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, int64_t lda, const double* B,
+                                     int64_t ldb, const double* C, int64_t ldc, void* scratch,
+                                     size_t scratch_bytes, void* nccl_comm, void* stream_, gmp_plan_t* out) {
+  GMP_TRY(check_desc(desc));
+  if (!out) return fail(GMP_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  const gmp_desc_t& d = *desc;
+  const int G = d.P * d.Q;
+  if ((G > 1) != (nccl_comm != nullptr)) return fail(GMP_ERR_GRID, "nccl_comm must be non-NULL iff P*Q > 1");
+  const ScratchLayout L = scratch_layout(desc);
+  if (!scratch || (int64_t)scratch_bytes < L.total) return fail(GMP_ERR_WORKSPACE, "scratch too small");
+  cudaStream_t stream = (cudaStream_t)stream_;
+  const int64_t nb = d.nb;
+  auto pl = new gmp_plan_s();
+  std::unique_ptr<gmp_plan_s> guard(pl);
+  pl->d = d;
+  pl->d.a_map = pl->d.b_map = pl->d.c_map = nullptr;
+  pl->mt = d.M / nb; pl->nt = d.N / nb; pl->kt = d.K / nb;
+  pl->nA = pl->mt * pl->kt; pl->nB = pl->kt * pl->nt; pl->nC = pl->mt * pl->nt;
+  pl->P = d.P; pl->Q = d.Q; pl->p = d.rank / d.Q; pl->q = d.rank % d.Q;
+  pl->A = A; pl->B = B; pl->C = C; pl->lda = lda; pl->ldb = ldb; pl->ldc = ldc;
+  const bool hasC = d.beta != 0.0;
+  const int64_t mtl = nloc(pl->mt, d.P, pl->p), ktlA = nloc(pl->kt, d.Q, pl->q);
+  const int64_t ktlB = nloc(pl->kt, d.P, pl->p), ntl = nloc(pl->nt, d.Q, pl->q);
+  if ((mtl * ktlA > 0 && (!A || lda < ktlA * nb)) || (ktlB * ntl > 0 && (!B || ldb < ntl * nb)) ||
+      (hasC && mtl * ntl > 0 && (!C || ldc < ntl * nb)))
+    return fail(GMP_ERR_ARG, "operand pointer NULL or leading dimension too small");
+  if (((uintptr_t)A | (uintptr_t)B | (uintptr_t)C) & 15 || (lda | ldb | (hasC ? ldc : 0)) & 1)
+    return fail(GMP_ERR_ARG, "operands must be 16-byte aligned with even leading dimensions");
+  auto chk_map = [&](const uint8_t* m, int64_t n) {
+    if (!m) return true;
+    for (int64_t t = 0; t < n; ++t) if (m[t] > 4) return false;
+    return true;
+  };
+  if (!chk_map(d.a_map, pl->nA) || !chk_map(d.b_map, pl->nB) || !chk_map(d.c_map, pl->nC))
+    return fail(GMP_ERR_MAP_SHAPE, "explicit map holds a code > 4");
+
+  for (int64_t i = pl->p; i < pl->mt; i += d.P)
+    for (int64_t l = pl->q; l < pl->kt; l += d.Q) pl->locA.push_back(i * pl->kt + l);
+  for (int64_t l = pl->p; l < pl->kt; l += d.P)
+    for (int64_t j = pl->q; j < pl->nt; j += d.Q) pl->locB.push_back(l * pl->nt + j);
+  for (int64_t i = pl->p; i < pl->mt; i += d.P)
+    for (int64_t j = pl->q; j < pl->nt; j += d.Q) pl->locC.push_back(i * pl->nt + j);
+
+  // ---- S1: stats of local tiles, written at their global index ----
+  uint8_t* sc = (uint8_t*)scratch;
+  const int64_t n = pl->nA + pl->nB + pl->nC;
+  double* S = (double*)(sc + L.S);
+  double* Mx = S + n;
+  uint8_t* F = sc + L.F;
+  GMP_CUDA(cudaMemsetAsync(sc + L.S, 0, 2 * n * 8, stream));
+  GMP_CUDA(cudaMemsetAsync(F, 0, n, stream));
+  std::vector<StatsJob> jobs;
+  for (int64_t g : pl->locA) {
+    const int64_t i = g / pl->kt, l = g % pl->kt;
+    jobs.push_back(StatsJob{A + (i / d.P) * nb * lda + (l / d.Q) * nb, lda, (int32_t)g});
+  }
+  for (int64_t g : pl->locB) {
+    const int64_t l = g / pl->nt, j = g % pl->nt;
+    jobs.push_back(StatsJob{B + (l / d.P) * nb * ldb + (j / d.Q) * nb, ldb, (int32_t)(pl->nA + g)});
+  }
+  if (hasC)
+    for (int64_t g : pl->locC) {
+      const int64_t i = g / pl->nt, j = g % pl->nt;
+      jobs.push_back(StatsJob{C + (i / d.P) * nb * ldc + (j / d.Q) * nb, ldc, (int32_t)(pl->nA + pl->nB + g)});
+    }
+  StatsJob* djobs = (StatsJob*)(sc + L.jobs);
+  if (!jobs.empty()) {
+    GMP_CUDA(cudaMemcpyAsync(djobs, jobs.data(), jobs.size() * sizeof(StatsJob), cudaMemcpyHostToDevice, stream));
+    k_tile_stats<<<(unsigned)jobs.size(), 256, 0, stream>>>(djobs, (int)nb, S, Mx, F);
+    GMP_CUDA(cudaGetLastError());
+  }
+  // ---- multi-GPU: every tile's stats owned by exactly one rank -> sum-allreduce is exact ----
+  if (G > 1) {
+    pl->world = (ncclComm_t)nccl_comm;
+    GMP_NCCL(ncclGroupStart());
+    GMP_NCCL(ncclAllReduce(S, S, 2 * n, ncclFloat64, ncclSum, pl->world, stream));
+    GMP_NCCL(ncclAllReduce(F, F, n, ncclUint8, ncclSum, pl->world, stream));
+    GMP_NCCL(ncclGroupEnd());
+  }
+  // ---- S2: map finalize ----
+  uint8_t* codes = sc + L.codes;
+  int16_t* s5 = (int16_t*)(sc + L.s5);
+  int16_t* scin = (int16_t*)(sc + L.scin);
+  int* status = (int*)(sc + L.status);
+  uint8_t* maps = sc + L.maps;
+  if (d.a_map) GMP_CUDA(cudaMemcpyAsync(maps, d.a_map, pl->nA, cudaMemcpyHostToDevice, stream));
+  if (d.b_map) GMP_CUDA(cudaMemcpyAsync(maps + pl->nA, d.b_map, pl->nB, cudaMemcpyHostToDevice, stream));
+  if (d.c_map) GMP_CUDA(cudaMemcpyAsync(maps + pl->nA + pl->nB, d.c_map, pl->nC, cudaMemcpyHostToDevice, stream));
+  FinalizeArgs fa{};
+  fa.mt = pl->mt; fa.nt = pl->nt; fa.kt = pl->kt; fa.nb = (int)nb;
+  fa.tol = d.tol; fa.alpha = d.alpha; fa.beta = d.beta; fa.mask = d.class_mask | 1u;
+  fa.explicit_a = d.a_map != nullptr; fa.explicit_b = d.b_map != nullptr; fa.explicit_c = d.c_map != nullptr;
+  fa.SA = S; fa.SB = S + pl->nA; fa.SC = S + pl->nA + pl->nB;
+  fa.MA = Mx; fa.MB = Mx + pl->nA; fa.MC = Mx + pl->nA + pl->nB;
+  fa.FA = F; fa.FB = F + pl->nA; fa.FC = F + pl->nA + pl->nB;
+  fa.mapA = maps; fa.mapB = maps + pl->nA; fa.mapC = maps + pl->nA + pl->nB;
+  fa.codeA = codes; fa.codeB = codes + pl->nA; fa.codeC = codes + pl->nA + pl->nB;
+  fa.scaleA5 = s5; fa.scaleB5 = s5 + pl->nA * 5; fa.scaleCin = scin; fa.status = status;
+  k_map_finalize<<<1, 1024, 0, stream>>>(fa);
+  GMP_CUDA(cudaGetLastError());
+  // ---- the one host synchronisation: read the maps back ----
+  pl->codeA.resize(pl->nA); pl->codeB.resize(pl->nB); pl->codeC.resize(pl->nC);
+  pl->sA5.resize(pl->nA * 5); pl->sB5.resize(pl->nB * 5); pl->sCin.resize(pl->nC); pl->sCout.assign(pl->nC, 0);
+  int h_status = 0;
+  GMP_CUDA(cudaMemcpyAsync(pl->codeA.data(), codes, pl->nA, cudaMemcpyDeviceToHost, stream));
+  GMP_CUDA(cudaMemcpyAsync(pl->codeB.data(), codes + pl->nA, pl->nB, cudaMemcpyDeviceToHost, stream));
+  GMP_CUDA(cudaMemcpyAsync(pl->codeC.data(), codes + pl->nA + pl->nB, pl->nC, cudaMemcpyDeviceToHost, stream));
+  GMP_CUDA(cudaMemcpyAsync(pl->sA5.data(), s5, pl->nA * 10, cudaMemcpyDeviceToHost, stream));
+  GMP_CUDA(cudaMemcpyAsync(pl->sB5.data(), s5 + pl->nA * 5, pl->nB * 10, cudaMemcpyDeviceToHost, stream));
+  GMP_CUDA(cudaMemcpyAsync(pl->sCin.data(), scin, pl->nC * 2, cudaMemcpyDeviceToHost, stream));
+  GMP_CUDA(cudaMemcpyAsync(&h_status, status, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  GMP_CUDA(cudaStreamSynchronize(stream));
+  if (h_status == 4) return fail(GMP_ERR_NONFINITE, "A, B or C holds a NaN or an infinity");
+  if (G > 1) {
+    GMP_NCCL(ncclCommSplit(pl->world, pl->p, pl->q, &pl->rowc, nullptr));
+    GMP_NCCL(ncclCommSplit(pl->world, pl->q, pl->p, &pl->colc, nullptr));
+    GMP_CUDA(cudaStreamCreateWithFlags(&pl->comm_stream, cudaStreamNonBlocking));
+  }
+  build_tables(pl);
+  pl->step_ev.resize(pl->st.steps);
+  for (auto& e : pl->step_ev) GMP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  *out = guard.release();
+  return GMP_OK;
+}
+
+extern "C" gmp_status_t gemm_mp_workspace_size(gmp_plan_t pl, size_t* bytes) {
+  if (!pl || !bytes) return fail(GMP_ERR_ARG, "NULL argument");
+  *bytes = (size_t)pl->ws_bytes;
+  return GMP_OK;
+}
+
+static int grid_for(int64_t n_elems, int per_thread) {
+  int64_t blocks = (n_elems / per_thread + 255) / 256;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 4));
+}
+
+extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_bytes, void* stream_) {
+  if (!pl) return fail(GMP_ERR_ARG, "plan is NULL");
+  if (!ws_ || (int64_t)ws_bytes < pl->ws_bytes) return fail(GMP_ERR_WORKSPACE, "workspace too small");
+  if ((uintptr_t)ws_ & 1023) return fail(GMP_ERR_ARG, "workspace must be 1024-byte aligned");
+  cudaStream_t stream = (cudaStream_t)stream_;
+  uint8_t* ws = (uint8_t*)ws_;
+  pl->ws = ws;
+  const int64_t nb = pl->d.nb;
+  // job tables
+  auto up = [&](int64_t off, const void* src, size_t bytes) -> gmp_status_t {
+    if (bytes) GMP_CUDA(cudaMemcpyAsync(ws + off, src, bytes, cudaMemcpyHostToDevice, stream));
+    return GMP_OK;
+  };
+  std::vector<ShadowJob> allsh = pl->shadow_local;
+  for (auto& v : pl->shadow_step) allsh.insert(allsh.end(), v.begin(), v.end());
+  GMP_TRY(up(pl->off_pack, pl->pack.data(), pl->pack.size() * sizeof(PackJob)));
+  GMP_TRY(up(pl->off_shadow, allsh.data(), allsh.size() * sizeof(ShadowJob)));
+  GMP_TRY(up(pl->off_items, pl->items.data(), pl->items.size() * sizeof(WorkItem)));
+  GMP_TRY(up(pl->off_pairs, pl->pairs.data(), pl->pairs.size() * sizeof(PairDesc)));
+  GMP_TRY(tc_prepare(pl->tc, ws, pl->arena_off, pl->arena_slots, (int)nb));
+  // S3 pack
+  if (!pl->pack.empty()) {
+    dim3 grid((unsigned)((nb / 64) * (nb / 64)), (unsigned)pl->pack.size());
+    k_pack<<<grid, 256, 0, stream>>>((const PackJob*)(ws + pl->off_pack), ws, (int)nb);
+    GMP_CUDA(cudaGetLastError());
+  }
+  // S5 shadows of local tiles
+  if (!pl->shadow_local.empty()) {
+    dim3 grid((unsigned)std::max<int64_t>(1, nb * nb / 8 / 256 / 4), (unsigned)pl->shadow_local.size());
+    k_shadow<<<grid, 256, 0, stream>>>((const ShadowJob*)(ws + pl->off_shadow), ws, nb * nb);
+    GMP_CUDA(cudaGetLastError());
+  }
+  pl->converted = true;
+  return GMP_OK;
+}
+
+extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ldc, void* stream_) {
+  if (!pl) return fail(GMP_ERR_ARG, "plan is NULL");
+  if (!pl->converted) return fail(GMP_ERR_STATE, "execute before convert");
+  const int64_t nb = pl->d.nb, nb2 = nb * nb;
+  const int64_t nCl = (int64_t)pl->locC.size();
+  const int64_t ntl = nloc(pl->nt, pl->Q, pl->q);
+  if (nCl > 0 && (!Cuser || ldc < ntl * nb)) return fail(GMP_ERR_ARG, "C NULL or ldc too small");
+  cudaStream_t stream = (cudaStream_t)stream_;
+  uint8_t* ws = pl->ws;
+  // C tile descriptors (user offsets depend on ldc)
+  for (auto& t : pl->ctd) {
+    const int64_t il = (uint32_t)t.pad >> 16, jl = t.pad & 0xFFFF;
+    t.user_off = il * nb * ldc + jl * nb;
+  }
+  if (nCl) GMP_CUDA(cudaMemcpyAsync(ws + pl->off_ctd, pl->ctd.data(), nCl * sizeof(CTileDesc), cudaMemcpyHostToDevice, stream));
+  const CTileDesc* dct = (const CTileDesc*)(ws + pl->off_ctd);
+  if (nCl) {
+    k_acc_init<<<dim3(grid_for(nb2, 1) / 4 + 1, (unsigned)nCl), 256, 0, stream>>>(dct, ws, nb2, pl->d.beta);
+    GMP_CUDA(cudaGetLastError());
+  }
+  const int steps = pl->st.steps;
+  const bool multi = pl->P * pl->Q > 1;
+  cudaEvent_t ready = nullptr;
+  if (multi) {
+    // comm stream starts after everything already queued on `stream` (convert, init)
+    GMP_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    GMP_CUDA(cudaEventRecord(ready, stream));
+    GMP_CUDA(cudaStreamWaitEvent(pl->comm_stream, ready, 0));
+    for (int s = 0; s < steps; ++s) {
+      GMP_NCCL(ncclGroupStart());
+      for (const Bcast& b : pl->bcast_step[s])
+        GMP_NCCL(ncclBroadcast(ws + b.off, ws + b.off, (size_t)b.bytes, ncclUint8, b.root,
+                               b.which == 0 ? pl->rowc : pl->colc, pl->comm_stream));
+      GMP_NCCL(ncclGroupEnd());
+      if (!pl->shadow_step[s].empty()) {
+        dim3 grid((unsigned)std::max<int64_t>(1, nb2 / 8 / 256 / 4), (unsigned)pl->shadow_step[s].size());
+        k_shadow<<<grid, 256, 0, pl->comm_stream>>>((const ShadowJob*)(ws + pl->off_shadow) + pl->shadow_step_off[s], ws, nb2);
+        GMP_CUDA(cudaGetLastError());
+      }
+      GMP_CUDA(cudaEventRecord(pl->step_ev[s], pl->comm_stream));
+    }
+  }
+  size_t li = 0;
+  for (int s = 0; s < steps; ++s) {
+    if (multi) GMP_CUDA(cudaStreamWaitEvent(stream, pl->step_ev[s], 0));
+    for (; li < pl->launches.size() && pl->launches[li].step == s; ++li) {
+      const Launch& L = pl->launches[li];
+      const WorkItem* it = (const WorkItem*)(ws + pl->off_items) + L.ibeg;
+      const PairDesc* pd = (const PairDesc*)(ws + pl->off_pairs);
+      if (L.kind == 1) {
+        GMP_TRY(tc_launch(pl->tc, L.cls, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, stream));
+      } else {
+        switch (L.cls) {
+#define GMP_L(C) case C: k_simt_class<C><<<(unsigned)L.icount, 256, 0, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha); break;
+          GMP_L(0) GMP_L(1) GMP_L(2) GMP_L(3) GMP_L(4)
+#undef GMP_L
+        }
+        GMP_CUDA(cudaGetLastError());
+      }
+    }
+  }
+  if (ready) cudaEventDestroy(ready);
+  if (nCl) {
+    unsigned long long* mb = (unsigned long long*)(ws + pl->off_maxbits);
+    GMP_CUDA(cudaMemsetAsync(mb, 0, nCl * 8, stream));
+    k_c_maxabs<<<dim3(grid_for(nb2, 4) / 8 + 1, (unsigned)nCl), 256, 0, stream>>>(dct, ws, nb2, mb);
+    GMP_CUDA(cudaGetLastError());
+    k_c_finalize<<<dim3(grid_for(nb2, 1) / 8 + 1, (unsigned)nCl), 256, 0, stream>>>(
+        dct, ws, mb, (int16_t*)(ws + pl->off_cscale), Cuser, ldc, (int)nb);
+    GMP_CUDA(cudaGetLastError());
+  }
+  pl->executed = true;
+  return GMP_OK;
+}
+
+extern "C" gmp_status_t gemm_mp_sync(gmp_plan_t pl) {
+  if (!pl) return fail(GMP_ERR_ARG, "plan is NULL");
+  GMP_CUDA(cudaDeviceSynchronize());
+  GMP_CUDA(cudaGetLastError());
+  if (pl->world) {
+    ncclResult_t ar = ncclSuccess;
+    GMP_NCCL(ncclCommGetAsyncError(pl->world, &ar));
+    if (ar != ncclSuccess) return fail(GMP_ERR_NCCL, std::string("async NCCL error: ") + ncclGetErrorString(ar));
+  }
+  return GMP_OK;
+}
+
+extern "C" gmp_status_t gemm_mp_get_maps(gmp_plan_t pl, uint8_t* a, uint8_t* b, uint8_t* c, int16_t* as,
+                                         int16_t* bs, int16_t* cs) {
+  if (!pl) return fail(GMP_ERR_ARG, "plan is NULL");
+  if (a) std::memcpy(a, pl->codeA.data(), pl->nA);
+  if (b) std::memcpy(b, pl->codeB.data(), pl->nB);
+  if (c) std::memcpy(c, pl->codeC.data(), pl->nC);
+  if (as) for (int64_t g = 0; g < pl->nA; ++g) as[g] = pl->sA5[g * 5 + pl->codeA[g]];
+  if (bs) for (int64_t g = 0; g < pl->nB; ++g) bs[g] = pl->sB5[g * 5 + pl->codeB[g]];
+  if (cs) {
+    std::fill(cs, cs + pl->nC, (int16_t)0);
+    if (pl->executed && !pl->locC.empty()) {
+      std::vector<int16_t> tmp(pl->locC.size());
+      GMP_CUDA(cudaDeviceSynchronize());
+      GMP_CUDA(cudaMemcpy(tmp.data(), pl->ws + pl->off_cscale, tmp.size() * 2, cudaMemcpyDeviceToHost));
+      for (size_t k = 0; k < tmp.size(); ++k) cs[pl->locC[k]] = tmp[k];
+    }
+  }
+  return GMP_OK;
+}
+
+extern "C" gmp_status_t gemm_mp_get_tile(gmp_plan_t pl, char which, int64_t ti, int64_t tj, int32_t cls,
+                                         void* dst, size_t* bytes, int16_t* scale) {
+  if (!pl || !dst || !bytes) return fail(GMP_ERR_ARG, "NULL argument");
+  if (!pl->converted) return fail(GMP_ERR_STATE, "no workspace yet (convert first)");
+  const int64_t nb2 = (int64_t)pl->d.nb * pl->d.nb;
+  int64_t off = -1, nbytes = 0;
+  int16_t sc = 0;
+  if (which == 'A' || which == 'B') {
+    const bool isB = which == 'B';
+    const int64_t rows = isB ? pl->kt : pl->mt, cols = isB ? pl->nt : pl->kt;
+    if (ti < 0 || tj < 0 || ti >= rows || tj >= cols || cls < 0 || cls > 4) return fail(GMP_ERR_ARG, "tile index out of range");
+    const int64_t g = ti * cols + tj;
+    const int32_t slot = (isB ? pl->slotB5 : pl->slotA5)[g * 5 + cls];
+    if (slot < 0) return fail(GMP_ERR_ARG, "representation not materialised on this rank");
+    off = pl->arena_off[cls] + slot * pl->slot_bytes[cls];
+    nbytes = pl->slot_bytes[cls];
+    sc = (isB ? pl->sB5 : pl->sA5)[g * 5 + cls];
+  } else if (which == 'C' || which == 'I' || which == 'W') {
+    if (ti < 0 || tj < 0 || ti >= pl->mt || tj >= pl->nt) return fail(GMP_ERR_ARG, "tile index out of range");
+    const int64_t g = ti * pl->nt + tj;
+    auto itc = std::find(pl->locC.begin(), pl->locC.end(), g);
+    if (itc == pl->locC.end()) return fail(GMP_ERR_ARG, "C tile is not local to this rank");
+    const CTileDesc& t = pl->ctd[itc - pl->locC.begin()];
+    if (which == 'W') { off = t.w_off; nbytes = nb2 * (t.code == 0 ? 8 : 4); }
+    else if (which == 'I') {
+      if (t.cin_off < 0) return fail(GMP_ERR_STATE, "beta == 0: no packed C_in");
+      off = t.cin_off; nbytes = nb2 * class_bytes(t.code); sc = t.cin_scale;
+    } else {
+      if (!pl->executed) return fail(GMP_ERR_STATE, "execute first");
+      off = t.cout_off; nbytes = nb2 * class_bytes(t.code);
+      GMP_CUDA(cudaDeviceSynchronize());
+      GMP_CUDA(cudaMemcpy(&sc, pl->ws + pl->off_cscale + 2 * (itc - pl->locC.begin()), 2, cudaMemcpyDeviceToHost));
+    }
+  } else {
+    return fail(GMP_ERR_ARG, "which must be A, B, C, I or W");
+  }
+  if ((int64_t)*bytes < nbytes) return fail(GMP_ERR_ARG, "host buffer too small");
+  GMP_CUDA(cudaDeviceSynchronize());
+  GMP_CUDA(cudaMemcpy(dst, pl->ws + off, nbytes, cudaMemcpyDeviceToHost));
+  *bytes = (size_t)nbytes;
+  if (scale) *scale = sc;
+  return GMP_OK;
+}
+
+extern "C" gmp_status_t gemm_mp_get_stats(gmp_plan_t pl, gmp_stats_t* out) {
+  if (!pl || !out) return fail(GMP_ERR_ARG, "NULL argument");
+  *out = pl->st;
+  return GMP_OK;
+}
+
+extern "C" gmp_status_t gemm_mp_nccl_unique_id(void* out128) {
+  if (!out128) return fail(GMP_ERR_ARG, "NULL argument");
+  ncclUniqueId id;
+  GMP_NCCL(ncclGetUniqueId(&id));
+  std::memcpy(out128, &id, sizeof id);
+  return GMP_OK;
+}
+
+extern "C" gmp_status_t gemm_mp_nccl_comm_create(const void* id128, int nranks, int rank, void** comm) {
+  if (!id128 || !comm) return fail(GMP_ERR_ARG, "NULL argument");
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof id);
+  ncclComm_t c = nullptr;
+  GMP_NCCL(ncclCommInitRank(&c, nranks, id, rank));
+  *comm = c;
+  return GMP_OK;
+}
+
+extern "C" gmp_status_t gemm_mp_nccl_comm_destroy(void* comm) {
+  if (comm) GMP_NCCL(ncclCommDestroy((ncclComm_t)comm));
+  return GMP_OK;
+}
+
+extern "C" gmp_status_t gemm_mp_synth(double* out, int64_t ld, int64_t rows, int64_t cols, int32_t nb, int32_t P,
+                                      int32_t Q, int32_t p, int32_t q, uint64_t seed, uint64_t tau, int32_t mode,
+                                      int32_t E, int32_t s, void* stream) {
+  if (!out || nb <= 0 || rows % nb || cols % nb || P < 1 || Q < 1) return fail(GMP_ERR_ARG, "bad synth arguments");
+  SynthArgs a{};
+  a.out = out; a.ld = ld;
+  a.lrows = nloc(rows / nb, P, p) * nb; a.lcols = nloc(cols / nb, Q, q) * nb;
+  a.grows = rows; a.gcols = cols; a.nb = nb; a.P = P; a.Q = Q; a.p0 = p; a.q0 = q;
+  a.seed = seed; a.tau = tau; a.mode = mode; a.E = E; a.s = s;
+  if (a.lrows * a.lcols == 0) return GMP_OK;
+  k_synth<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(a);
+  GMP_CUDA(cudaGetLastError());
+  return GMP_OK;
+}
+
+extern "C" void gemm_mp_destroy(gmp_plan_t pl) {
+  if (!pl) return;
+  for (auto& e : pl->step_ev) if (e) cudaEventDestroy(e);
+  if (pl->rowc) ncclCommDestroy(pl->rowc);
+  if (pl->colc) ncclCommDestroy(pl->colc);
+  if (pl->comm_stream) cudaStreamDestroy(pl->comm_stream);
+  tc_release(pl->tc);
+  delete pl;
+}

@@ -1,0 +1,282 @@
+// gmp_convert.cuh -- S3 convert-and-pack, S5 shadow convert, accumulator init,
+// S7 C-finalize and the N1 synthetic generator.
+//
+// All of these are HBM-bound streaming kernels: 16-byte vector loads, one RNE
+// rounding per element from binary64 (or from the decoded stored value for a
+// shadow, PAPER.md:148 receiver-side conversion), power-of-two scaling with
+// ldexp (exact).  Algorithmic bytes per element are listed in DESIGN.md.
+#pragma once
+#include "gmp_common.cuh"
+
+namespace gmp {
+
+// ---------------------------------------------------------------------------
+// S3 convert-and-pack: one job = one tile.  A and C tiles keep row-major order,
+// B tiles are written K-major (transposed) so that every tile-GEMM operand is
+// K-major.  64x64 sub-block per CTA.
+// ---------------------------------------------------------------------------
+struct PackJob {
+  const double* src;  // top-left element of the binary64 tile
+  int64_t ld;
+  int64_t dst_off;    // byte offset of the payload in the workspace
+  int16_t cls;
+  int16_t scale;
+  int16_t transpose;
+  int16_t pad;
+};
+
+template <int C>
+__device__ __forceinline__ void store8(uint8_t* dst, const double* v) {
+  // 8 consecutive payload elements of class C from 8 binary64 values
+  if constexpr (C == 0) {
+    double2* d = reinterpret_cast<double2*>(dst);
+    d[0] = make_double2(v[0], v[1]); d[1] = make_double2(v[2], v[3]);
+    d[2] = make_double2(v[4], v[5]); d[3] = make_double2(v[6], v[7]);
+  } else if constexpr (C == 1) {
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    d[0] = make_uint4(cvt_f32_rn(v[0]), cvt_f32_rn(v[1]), cvt_f32_rn(v[2]), cvt_f32_rn(v[3]));
+    d[1] = make_uint4(cvt_f32_rn(v[4]), cvt_f32_rn(v[5]), cvt_f32_rn(v[6]), cvt_f32_rn(v[7]));
+  } else if constexpr (C == 2 || C == 3) {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint16_t lo = (C == 2) ? cvt_f16_rn(v[2 * i]) : cvt_bf16_rn(v[2 * i]);
+      uint16_t hi = (C == 2) ? cvt_f16_rn(v[2 * i + 1]) : cvt_bf16_rn(v[2 * i + 1]);
+      w[i] = (uint32_t)lo | ((uint32_t)hi << 16);
+    }
+    *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+  } else {
+    uint32_t w[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      uint32_t lo = cvt_e4m3x2_rn(v[4 * i], v[4 * i + 1]);
+      uint32_t hi = cvt_e4m3x2_rn(v[4 * i + 2], v[4 * i + 3]);
+      w[i] = lo | (hi << 16);
+    }
+    *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+  }
+}
+
+template <int C>
+__device__ __forceinline__ void pack_block(const PackJob& j, uint8_t* ws, int nb, int r0, int c0,
+                                           double (*sm)[65]) {
+  const int t = threadIdx.x;
+  constexpr int B = class_bytes(C);
+  uint8_t* dst = ws + j.dst_off;
+  if (!j.transpose) {
+    // thread -> (row, 8-col group): 64 rows x 8 groups = 512 units, 2 per thread
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      int unit = t + u * 256;
+      int r = unit >> 3, g = unit & 7;
+      const double2* s = reinterpret_cast<const double2*>(j.src + (int64_t)(r0 + r) * j.ld + c0 + g * 8);
+      double v[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        double2 x = __ldg(s + i);
+        v[2 * i] = (C == 0) ? x.x : ldexp(x.x, j.scale);
+        v[2 * i + 1] = (C == 0) ? x.y : ldexp(x.y, j.scale);
+      }
+      store8<C>(dst + ((int64_t)(r0 + r) * nb + c0 + g * 8) * B, v);
+    }
+  } else {
+    // stage the 64x64 block in shared memory, write it transposed (K-major)
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      int unit = t + u * 256;           // 64 rows x 32 double2
+      int r = unit >> 5, q = unit & 31;
+      double2 x = __ldg(reinterpret_cast<const double2*>(j.src + (int64_t)(r0 + r) * j.ld + c0 + 2 * q));
+      sm[r][2 * q] = x.x;
+      sm[r][2 * q + 1] = x.y;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      int unit = t + u * 256;           // output row (= source col) x 8-k group
+      int oc = unit >> 3, g = unit & 7;
+      double v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        double x = sm[g * 8 + i][oc];
+        v[i] = (C == 0) ? x : ldexp(x, j.scale);
+      }
+      store8<C>(dst + ((int64_t)(c0 + oc) * nb + r0 + g * 8) * B, v);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_pack(const PackJob* __restrict__ jobs, uint8_t* ws, int nb) {
+  __shared__ double sm[64][65];
+  const PackJob j = jobs[blockIdx.y];
+  const int per = nb / 64;
+  const int r0 = (blockIdx.x / per) * 64, c0 = (blockIdx.x % per) * 64;
+  switch (j.cls) {
+    case 0: pack_block<0>(j, ws, nb, r0, c0, sm); break;
+    case 1: pack_block<1>(j, ws, nb, r0, c0, sm); break;
+    case 2: pack_block<2>(j, ws, nb, r0, c0, sm); break;
+    case 3: pack_block<3>(j, ws, nb, r0, c0, sm); break;
+    default: pack_block<4>(j, ws, nb, r0, c0, sm); break;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// S5 shadow convert (receiver-side, from the STORED payload):
+//   shadow = RN_to(decode_from(stored) * 2^d),  d = shadow scale - stored scale.
+// Layout is kept (A row-major, B K-major).  8 elements per thread-iteration.
+// ---------------------------------------------------------------------------
+struct ShadowJob {
+  int64_t src_off, dst_off;  // byte offsets in the workspace (or panel buffers)
+  int16_t from, to, d, pad;
+};
+
+template <int F, int T>
+__device__ __forceinline__ void shadow_run(const ShadowJob& j, uint8_t* ws, int64_t n) {
+  const uint8_t* src = ws + j.src_off;
+  uint8_t* dst = ws + j.dst_off;
+  for (int64_t e0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8; e0 < n;
+       e0 += (int64_t)gridDim.x * blockDim.x * 8) {
+    double v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = ldexp(payload_f64(src, e0 + i, F), j.d);
+    store8<T>(dst + e0 * class_bytes(T), v);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_shadow(const ShadowJob* __restrict__ jobs, uint8_t* ws, int64_t n) {
+  const ShadowJob j = jobs[blockIdx.y];
+  const int key = j.from * 8 + j.to;
+  switch (key) {
+#define GMP_SH(F, T) case F * 8 + T: shadow_run<F, T>(j, ws, n); break;
+    GMP_SH(0, 1) GMP_SH(0, 2) GMP_SH(0, 3) GMP_SH(0, 4)
+    GMP_SH(1, 2) GMP_SH(1, 3) GMP_SH(1, 4)
+    GMP_SH(2, 3) GMP_SH(2, 4)
+    GMP_SH(3, 4)
+#undef GMP_SH
+    default: break;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// accumulator init (O9):  W = beta == 0 ? 0 : RN_W(RN_W(beta) decode(C_in))
+// ---------------------------------------------------------------------------
+struct CTileDesc {
+  int64_t w_off;       // byte offset of the W accumulator (nb*nb of binary64 or binary32)
+  int64_t cin_off;     // byte offset of the packed C_in payload (beta != 0), -1 otherwise
+  int64_t cout_off;    // byte offset of the packed C_out payload
+  int64_t user_off;    // element offset of the tile's top-left in the user's C (local)
+  int16_t code;        // class of the C tile (W = binary64 iff code == 0)
+  int16_t cin_scale;
+  int32_t pad;
+};
+
+__global__ void __launch_bounds__(256) k_acc_init(const CTileDesc* __restrict__ ct, uint8_t* ws,
+                                                  int64_t n, double beta) {
+  const CTileDesc c = ct[blockIdx.y];
+  const float bf = __double2float_rn(beta);
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (c.code == 0) {
+      double x = (beta == 0.0) ? 0.0 : __dmul_rn(beta, payload_f64(ws + c.cin_off, e, 0));
+      reinterpret_cast<double*>(ws + c.w_off)[e] = x;
+    } else {
+      float x = 0.f;
+      if (beta != 0.0)
+        x = __double2float_rn(__dmul_rn((double)bf, ldexp(payload_f64(ws + c.cin_off, e, c.code), -c.cin_scale)));
+      reinterpret_cast<float*>(ws + c.w_off)[e] = x;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// S7 C-finalize: pass 1 maxabs(W) per tile (bit-pattern atomicMax on |x|),
+// pass 2 encode into the C class with the scale of maxabs, decode to user C.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_c_maxabs(const CTileDesc* __restrict__ ct, const uint8_t* ws,
+                                                  int64_t n, unsigned long long* maxbits) {
+  const CTileDesc c = ct[blockIdx.y];
+  double m = 0.0;
+  for (int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; e < n;
+       e += (int64_t)gridDim.x * blockDim.x * 4) {
+    if (c.code == 0) {
+      const double2* p = reinterpret_cast<const double2*>(ws + c.w_off) + e / 2;
+      double2 a = p[0], b = p[1];
+      m = fmax(m, fmax(fmax(fabs(a.x), fabs(a.y)), fmax(fabs(b.x), fabs(b.y))));
+    } else {
+      float4 a = reinterpret_cast<const float4*>(ws + c.w_off)[e / 4];
+      m = fmax(m, (double)fmaxf(fmaxf(fabsf(a.x), fabsf(a.y)), fmaxf(fabsf(a.z), fabsf(a.w))));
+    }
+  }
+  for (int off = 16; off >= 1; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(maxbits + blockIdx.y, (unsigned long long)__double_as_longlong(m));
+}
+
+__global__ void __launch_bounds__(256) k_c_finalize(const CTileDesc* __restrict__ ct, uint8_t* ws,
+                                                    const unsigned long long* maxbits, int16_t* cscale,
+                                                    double* cuser, int64_t ldc, int nb) {
+  const CTileDesc c = ct[blockIdx.y];
+  const double m = __longlong_as_double((long long)maxbits[blockIdx.y]);
+  const int e = scale_exp(m, c.code);
+  if (blockIdx.x == 0 && threadIdx.x == 0) cscale[blockIdx.y] = (int16_t)e;
+  const int64_t n = (int64_t)nb * nb;
+  uint8_t* pay = ws + c.cout_off;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double w = (c.code == 0) ? reinterpret_cast<const double*>(ws + c.w_off)[i]
+                             : (double)reinterpret_cast<const float*>(ws + c.w_off)[i];
+    double back;
+    if (c.code == 0) {
+      reinterpret_cast<double*>(pay)[i] = w;
+      back = w;
+    } else {
+      payload_store(pay, i, c.code, ldexp(w, e));
+      back = ldexp(payload_f64(pay, i, c.code), -e);
+    }
+    const int64_t r = i / nb, col = i - (i / nb) * nb;
+    cuser[c.user_off + r * ldc + col] = back;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// N1 synthetic generator (benchmark input only):
+// x(r,c) = v(r,c) 2^(s - e(r/nb, c/nb)); a local block-cyclic matrix holds the
+// global tiles (p0 + il*P, q0 + jl*Q).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+struct SynthArgs {
+  double* out;
+  int64_t ld, lrows, lcols;        // local matrix (lrows x lcols)
+  int64_t grows, gcols;            // global matrix
+  int nb, P, Q, p0, q0;
+  uint64_t seed, tau;
+  int mode, E, s;
+};
+
+__global__ void __launch_bounds__(256) k_synth(SynthArgs a) {
+  const int64_t mtg = a.grows / a.nb, ntg = a.gcols / a.nb;
+  const int64_t total = a.lrows * a.lcols;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lr = idx / a.lcols, lc = idx - (idx / a.lcols) * a.lcols;
+    const int64_t ti = a.p0 + (lr / a.nb) * a.P, tj = a.q0 + (lc / a.nb) * a.Q;
+    const int64_t gr = ti * a.nb + lr % a.nb, gc = tj * a.nb + lc % a.nb;
+    const uint64_t u = mix64(a.seed + ((uint64_t)(gr * a.gcols + gc) + 1ull) * 0x9E3779B97F4A7C15ull);
+    const double v = ((double)(u >> 11) * 0x1p-53) * 2.0 - 1.0;
+    int e = 0;
+    if (a.mode == 1) {
+      int64_t den = mtg + ntg - 2;
+      if (den < 1) den = 1;
+      e = (int)(((ti + tj) * (int64_t)a.E) / den);
+    } else if (a.mode == 2) {
+      const uint64_t w = mix64(a.tau + ((uint64_t)(ti * ntg + tj) + 1ull) * 0x9E3779B97F4A7C15ull);
+      e = (int)(w % (uint64_t)(a.E + 1));
+    }
+    a.out[lr * a.ld + lc] = ldexp(v, a.s - e);
+  }
+}
+
+}  // namespace gmp

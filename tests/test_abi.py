@@ -1,0 +1,43 @@
+"""CPU-side checks of the C-ABI library: it loads, exports every entry point the
+header declares, and validates arguments without touching a GPU."""
+import ctypes as ct
+
+import pytest
+
+from paper_2508_14848_b200 import binding as B
+
+
+def test_library_exports_every_header_symbol():
+    L = B.lib()
+    syms = B.header_symbols()
+    assert len(syms) >= 14
+    missing = [s for s in syms if not hasattr(L, s)]
+    assert not missing, missing
+
+
+@pytest.mark.parametrize("kw,code", [
+    (dict(M=1000, N=1024, K=1024, nb=128), "GMP_ERR_NOT_DIVISIBLE"),
+    (dict(M=1024, N=1024, K=1024, nb=96), "GMP_ERR_NOT_DIVISIBLE"),
+    (dict(M=1024, N=1024, K=1024, nb=128, tol=0.0), "GMP_ERR_ARG"),
+    (dict(M=1024, N=1024, K=1024, nb=128, tol=float("inf")), "GMP_ERR_ARG"),
+    (dict(M=1024, N=1024, K=1024, nb=128, P=2, Q=2, rank=4), "GMP_ERR_GRID"),
+])
+def test_scratch_size_validates(kw, code):
+    args = dict(tol=1e-6)
+    args.update(kw)
+    d = B.make_desc(**args)
+    with pytest.raises(B.GmpError) as e:
+        B.gemm_mp_scratch_size(d)
+    assert code in str(e.value)
+
+
+def test_scratch_size_is_small():
+    d = B.make_desc(65536, 65536, 65536, 2048, 1e-4)
+    n = B.gemm_mp_scratch_size(d)
+    assert 0 < n < 1 << 20
+
+
+def test_null_plan_is_rejected():
+    with pytest.raises(B.GmpError):
+        B.gemm_mp_workspace_size(None)
+    B.gemm_mp_destroy(None)  # NULL-safe

@@ -1,0 +1,134 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the same
+seeded inputs.  Maps, scales, packed payload bytes (stored and shadow) must be
+bit-exact; C must match the oracle's emulated result to 1e-13 (all-FP64) or
+4 u32 sqrt(K) (mixed; relative Frobenius), bitwise when every class runs on the
+SIMT kernels, and meet the user tolerance against cuBLAS DGEMM."""
+import numpy as np
+import pytest
+
+import gmp_inputs
+import oracle
+from gpu_harness import run_gpu, run_oracle, tol_metric
+from paper_2508_14848_b200 import binding as B
+
+pytestmark = pytest.mark.gpu
+
+U32 = 2.0 ** -24
+
+
+def _cases():
+    w1 = gmp_inputs.workload(1)
+    w1b = gmp_inputs.workload(1, "beta0")
+    return [
+        ("cfg1", w1),
+        ("cfg1_beta0", w1b),
+        ("e4m3_mix", gmp_inputs.small_workload(512, 384, 640, 128, 1e-2, mode="random", E=40, beta=0.5,
+                                               class_mask=0b11111, seed=41)),
+        ("bf16_mix", gmp_inputs.small_workload(768, 512, 512, 256, 1e-4, mode="random", E=32, beta=0.0, seed=42)),
+        ("nb384_graded", gmp_inputs.small_workload(768, 1152, 384, 384, 1e-6, mode="graded", E=20, beta=-1.5,
+                                                   seed=43)),
+        ("fp64_only", gmp_inputs.small_workload(512, 512, 512, 128, 1e-12, mode="random", E=10, beta=1.0,
+                                                class_mask=0b00001, seed=44)),
+    ]
+
+
+CASES = _cases()
+
+
+@pytest.fixture(scope="module", params=CASES, ids=[c[0] for c in CASES])
+def case(request):
+    name, w = request.param
+    A, Bm, C = w.matrices()
+    orc = run_oracle(A, Bm, C, w.nb, w.tol, w.alpha, w.beta, w.class_mask)
+    assert orc["rc"] == 0
+    g, (Cg, Cg2) = run_gpu(A, Bm, C, w.nb, w.tol, w.alpha, w.beta, w.class_mask, reps=2)
+    gs, (Cs,) = run_gpu(A, Bm, C, w.nb, w.tol, w.alpha, w.beta, w.class_mask, flags=B.GMP_FLAG_SIMT_ONLY)
+    return dict(name=name, w=w, A=A, B=Bm, C=C, orc=orc, g=g, Cg=Cg, Cg2=Cg2, gs=gs, Cs=Cs)
+
+
+def test_maps_bitwise(case):
+    m = case["g"].maps()
+    o = case["orc"]
+    assert np.array_equal(m["acode"], o["acode"])
+    assert np.array_equal(m["bcode"], o["bcode"])
+    assert np.array_equal(m["ccode"], o["ccode"])
+    amask = o["acode"][..., None] == np.arange(5)
+    bmask = o["bcode"][..., None] == np.arange(5)
+    assert np.array_equal(m["ascale"], (o["ascale5"] * amask).sum(-1))
+    assert np.array_equal(m["bscale"], (o["bscale5"] * bmask).sum(-1))
+
+
+def test_packed_bytes_bitwise(case):
+    """every stored and every materialised shadow payload, byte for byte"""
+    w, o, g = case["w"], case["orc"], case["g"]
+    nb = w.nb
+    checked = 0
+    for which, X, codes, s5, kmaj in [("A", case["A"], o["acode"], o["ascale5"], False),
+                                      ("B", case["B"], o["bcode"], o["bscale5"], True)]:
+        rows, cols = codes.shape
+        for ti in range(rows):
+            for tj in range(cols):
+                code = int(codes[ti, tj])
+                tile = X[ti * nb:(ti + 1) * nb, tj * nb:(tj + 1) * nb]
+                stored = oracle.pack_tile(tile, code, int(s5[ti, tj, code]), kmajor_t=kmaj)
+                got, sc = g.tile(which, ti, tj, code)
+                assert sc == s5[ti, tj, code]
+                assert np.array_equal(got, stored.view(np.uint8)), (which, ti, tj, code)
+                checked += 1
+                for c in range(code + 1, 5):
+                    try:
+                        got, sc = g.tile(which, ti, tj, c)
+                    except B.GmpError:
+                        continue  # not needed by any local tile-GEMM
+                    sh, e = oracle.shadow_tile(stored, nb, code, int(s5[ti, tj, code]), c)
+                    assert sc == e == s5[ti, tj, c]
+                    assert np.array_equal(got, sh.view(np.uint8)), (which, ti, tj, code, c)
+                    checked += 1
+    assert checked > 0
+
+
+def test_c_bitwise_on_simt_path(case):
+    """all classes on per-thread sequential-k kernels: C is the oracle's, bit for bit"""
+    assert np.array_equal(case["Cs"], case["orc"]["C"])
+
+
+def test_c_parity_product_path(case):
+    o, w = case["orc"], case["w"]
+    Co, Cg = o["C"], case["Cg"]
+    rel = np.linalg.norm(Cg - Co) / np.linalg.norm(Co)
+    allfp64 = (o["acode"] == 0).all() and (o["bcode"] == 0).all() and (o["ccode"] == 0).all()
+    bound = 1e-13 if allfp64 else 4 * U32 * np.sqrt(w.K)
+    assert rel <= bound, (rel, bound)
+
+
+def test_c_meets_tolerance(case):
+    w = case["w"]
+    assert tol_metric(case["Cg"], case["A"], case["B"], case["C"], w.alpha, w.beta) <= w.tol
+
+
+def test_repeat_execute_bitwise(case):
+    assert np.array_equal(case["Cg"], case["Cg2"])
+
+
+def test_packed_c_matches_oracle_finalize(case):
+    """packed C_out of each local tile = oracle finalize of the oracle's C (SIMT path)"""
+    o, w, gs = case["orc"], case["w"], case["gs"]
+    nb = w.nb
+    maps = gs.maps()
+    for ti in range(o["ccode"].shape[0]):
+        for tj in range(o["ccode"].shape[1]):
+            code = int(o["ccode"][ti, tj])
+            got, sc = gs.tile("C", ti, tj, code)
+            assert sc == o["cscale"][ti, tj] == maps["cscale"][ti, tj]
+            dec = oracle.payload_values(got.view(oracle.PAYLOAD_DTYPE[code]), code)
+            want = o["C"][ti * nb:(ti + 1) * nb, tj * nb:(tj + 1) * nb].ravel()
+            assert np.array_equal(np.ldexp(dec, -sc) if code else dec, want)
+
+
+def test_mixes_are_mixed():
+    """the synthetic recipes really produce the class mixes the configs name"""
+    w = gmp_inputs.workload(1)
+    A, Bm, C = w.matrices()
+    g, _ = run_gpu(A, Bm, C, w.nb, w.tol, w.alpha, w.beta, w.class_mask)
+    st = g.stats()
+    assert st["tiles_a"][0] > 0 and st["tiles_a"][1] > 0 and st["tiles_a"][2] > 0
