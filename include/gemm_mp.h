@@ -63,6 +63,7 @@ typedef enum {
 
 /* flags */
 #define GMP_FLAG_SIMT_ONLY 1u /* run classes 2..4 on the SIMT (binary32 FMA) kernel: cross-check only */
+#define GMP_FLAG_TIMING 2u    /* record CUDA events around each class launch of execute (stats.class_ms) */
 
 typedef struct {
   int64_t M, N, K;     /* global GEMM shape                                                    */
@@ -92,6 +93,10 @@ typedef struct {
   int64_t workspace_bytes;
   int32_t steps;                              /* SUMMA steps (K tiles / step depth)        */
   int32_t launches_execute;                   /* kernels one gemm_mp_execute launches      */
+  int32_t launches_plan, launches_convert;    /* kernels of gemm_mp_plan / gemm_mp_convert */
+  double class_ms[5];                         /* GMP_FLAG_TIMING: device ms of the class-c tile-GEMM
+                                                 launches of the last execute (waits for them) */
+  int32_t class_launches[5];                  /* launches per class in one execute             */
 } gmp_stats_t;
 
 /* Device scratch needed by gemm_mp_plan (tile statistics + maps; KB-sized).     */

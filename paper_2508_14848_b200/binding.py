@@ -16,6 +16,7 @@ GMP_FP64, GMP_FP32, GMP_FP16, GMP_BF16, GMP_E4M3 = range(5)
 CLASS_NAMES = ["FP64", "FP32", "FP16", "BF16", "E4M3"]
 CLASS_BYTES = [8, 4, 2, 2, 1]
 GMP_FLAG_SIMT_ONLY = 1
+GMP_FLAG_TIMING = 2
 STATUS = ["GMP_OK", "GMP_ERR_ARG", "GMP_ERR_NOT_DIVISIBLE", "GMP_ERR_MAP_SHAPE", "GMP_ERR_NONFINITE",
           "GMP_ERR_GRID", "GMP_ERR_WORKSPACE", "GMP_ERR_STATE", "GMP_ERR_CUDA", "GMP_ERR_NCCL",
           "GMP_ERR_UNSUPPORTED"]
@@ -40,7 +41,9 @@ class gmp_stats_t(ct.Structure):
                 ("pairs", ct.c_int64 * 5), ("flops", ct.c_double * 5), ("pairs_local", ct.c_int64 * 5),
                 ("shadows_local", ct.c_int64 * 5), ("packed_bytes_local", ct.c_int64),
                 ("recv_bytes_local", ct.c_int64), ("workspace_bytes", ct.c_int64),
-                ("steps", ct.c_int32), ("launches_execute", ct.c_int32)]
+                ("steps", ct.c_int32), ("launches_execute", ct.c_int32),
+                ("launches_plan", ct.c_int32), ("launches_convert", ct.c_int32),
+                ("class_ms", ct.c_double * 5), ("class_launches", ct.c_int32 * 5)]
 
     def as_dict(self):
         d = {}

@@ -100,6 +100,7 @@ struct gmp_plan_s {
   int64_t off_pack = 0, off_shadow = 0, off_ctd = 0, off_items = 0, off_pairs = 0, off_maxbits = 0,
           off_cscale = 0, off_tc = 0, ws_bytes = 0;
   TcTables tc;
+  std::vector<cudaEvent_t> launch_ev;    // GMP_FLAG_TIMING: start/stop per class launch
   uint8_t* ws = nullptr;
   bool converted = false;
   bool executed = false;
@@ -107,6 +108,29 @@ struct gmp_plan_s {
 };
 
 extern "C" const char* gemm_mp_last_error(void) { return g_err.c_str(); }
+
+// Row / column communicators are split once per (world communicator, grid) and
+// reused by every plan on it (ncclCommSplit is a collective costing milliseconds);
+// they are released by gemm_mp_nccl_comm_destroy of the world communicator.
+struct GridComms {
+  ncclComm_t world;
+  int P, Q;
+  ncclComm_t rowc, colc;
+  cudaStream_t comm_stream;
+};
+static std::vector<GridComms> g_grid_comms;
+
+static gmp_status_t grid_comms(ncclComm_t world, int P, int Q, int p, int q, GridComms* out) {
+  for (auto& g : g_grid_comms)
+    if (g.world == world && g.P == P && g.Q == Q) { *out = g; return GMP_OK; }
+  GridComms g{world, P, Q, nullptr, nullptr, nullptr};
+  GMP_NCCL(ncclCommSplit(world, p, q, &g.rowc, nullptr));
+  GMP_NCCL(ncclCommSplit(world, q, p, &g.colc, nullptr));
+  GMP_CUDA(cudaStreamCreateWithFlags(&g.comm_stream, cudaStreamNonBlocking));
+  g_grid_comms.push_back(g);
+  *out = g;
+  return GMP_OK;
+}
 
 static gmp_status_t check_desc(const gmp_desc_t* d) {
   if (!d) return fail(GMP_ERR_ARG, "desc is NULL");
@@ -374,6 +398,8 @@ static void build_tables(gmp_plan_s* pl) {
           pd.b_off = arena(c, pl->slotB5[(l * nt + j) * 5 + c]);
           pd.fexp = -(pl->sA5[(i * kt + l) * 5 + c] + pl->sB5[(l * nt + j) * 5 + c]);
           pd.l = (int32_t)l;
+          pd.a_slot = pl->slotA5[(i * kt + l) * 5 + c];
+          pd.b_slot = pl->slotB5[(l * nt + j) * 5 + c];
           pl->pairs.push_back(pd);
         }
         const int64_t pcnt = (int64_t)pl->pairs.size() - pbeg;
@@ -411,9 +437,12 @@ static void build_tables(gmp_plan_s* pl) {
   st.recv_bytes_local = recv_bytes;
   st.workspace_bytes = pl->ws_bytes;
   st.steps = steps;
-  int nl = 2 + 1 + (int)pl->launches.size();  // maxabs memset is not a kernel: init, maxabs, finalize
+  int nl = 3 + (int)pl->launches.size();  // acc init, tile-GEMM launches, maxabs, finalize
   for (int s = 0; s < steps; ++s) if (!pl->shadow_step[s].empty()) ++nl;
   st.launches_execute = nl;
+  st.launches_plan = 2;
+  st.launches_convert = (pl->pack.empty() ? 0 : 1) + (pl->shadow_local.empty() ? 0 : 1);
+  for (const Launch& L : pl->launches) st.class_launches[L.cls]++;
 }
 
 extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, int64_t lda, const double* B,
@@ -531,13 +560,19 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
   GMP_CUDA(cudaStreamSynchronize(stream));
   if (h_status == 4) return fail(GMP_ERR_NONFINITE, "A, B or C holds a NaN or an infinity");
   if (G > 1) {
-    GMP_NCCL(ncclCommSplit(pl->world, pl->p, pl->q, &pl->rowc, nullptr));
-    GMP_NCCL(ncclCommSplit(pl->world, pl->q, pl->p, &pl->colc, nullptr));
-    GMP_CUDA(cudaStreamCreateWithFlags(&pl->comm_stream, cudaStreamNonBlocking));
+    GridComms gc{};
+    GMP_TRY(grid_comms(pl->world, d.P, d.Q, pl->p, pl->q, &gc));
+    pl->rowc = gc.rowc;
+    pl->colc = gc.colc;
+    pl->comm_stream = gc.comm_stream;
   }
   build_tables(pl);
   pl->step_ev.resize(pl->st.steps);
   for (auto& e : pl->step_ev) GMP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  if (d.flags & GMP_FLAG_TIMING) {
+    pl->launch_ev.resize(2 * pl->launches.size());
+    for (auto& e : pl->launch_ev) GMP_CUDA(cudaEventCreate(&e));
+  }
   *out = guard.release();
   return GMP_OK;
 }
@@ -638,6 +673,7 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
       const Launch& L = pl->launches[li];
       const WorkItem* it = (const WorkItem*)(ws + pl->off_items) + L.ibeg;
       const PairDesc* pd = (const PairDesc*)(ws + pl->off_pairs);
+      if (!pl->launch_ev.empty()) GMP_CUDA(cudaEventRecord(pl->launch_ev[2 * li], stream));
       if (L.kind == 1) {
         GMP_TRY(tc_launch(pl->tc, L.cls, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, stream));
       } else {
@@ -648,6 +684,7 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
         }
         GMP_CUDA(cudaGetLastError());
       }
+      if (!pl->launch_ev.empty()) GMP_CUDA(cudaEventRecord(pl->launch_ev[2 * li + 1], stream));
     }
   }
   if (ready) cudaEventDestroy(ready);
@@ -742,6 +779,15 @@ extern "C" gmp_status_t gemm_mp_get_tile(gmp_plan_t pl, char which, int64_t ti, 
 
 extern "C" gmp_status_t gemm_mp_get_stats(gmp_plan_t pl, gmp_stats_t* out) {
   if (!pl || !out) return fail(GMP_ERR_ARG, "NULL argument");
+  for (int c = 0; c < 5; ++c) pl->st.class_ms[c] = 0.0;
+  if (pl->executed && !pl->launch_ev.empty()) {
+    for (size_t li = 0; li < pl->launches.size(); ++li) {
+      float ms = 0.f;
+      GMP_CUDA(cudaEventSynchronize(pl->launch_ev[2 * li + 1]));
+      GMP_CUDA(cudaEventElapsedTime(&ms, pl->launch_ev[2 * li], pl->launch_ev[2 * li + 1]));
+      pl->st.class_ms[pl->launches[li].cls] += ms;
+    }
+  }
   *out = pl->st;
   return GMP_OK;
 }
@@ -765,6 +811,17 @@ extern "C" gmp_status_t gemm_mp_nccl_comm_create(const void* id128, int nranks, 
 }
 
 extern "C" gmp_status_t gemm_mp_nccl_comm_destroy(void* comm) {
+  for (size_t k = 0; k < g_grid_comms.size();) {
+    GridComms& g = g_grid_comms[k];
+    if (g.world == (ncclComm_t)comm) {
+      ncclCommDestroy(g.rowc);
+      ncclCommDestroy(g.colc);
+      cudaStreamDestroy(g.comm_stream);
+      g_grid_comms.erase(g_grid_comms.begin() + k);
+    } else {
+      ++k;
+    }
+  }
   if (comm) GMP_NCCL(ncclCommDestroy((ncclComm_t)comm));
   return GMP_OK;
 }
@@ -787,9 +844,7 @@ extern "C" gmp_status_t gemm_mp_synth(double* out, int64_t ld, int64_t rows, int
 extern "C" void gemm_mp_destroy(gmp_plan_t pl) {
   if (!pl) return;
   for (auto& e : pl->step_ev) if (e) cudaEventDestroy(e);
-  if (pl->rowc) ncclCommDestroy(pl->rowc);
-  if (pl->colc) ncclCommDestroy(pl->colc);
-  if (pl->comm_stream) cudaStreamDestroy(pl->comm_stream);
+  for (auto& e : pl->launch_ev) if (e) cudaEventDestroy(e);
   tc_release(pl->tc);
   delete pl;
 }

@@ -34,6 +34,7 @@ struct PairDesc {
   int64_t a_off, b_off;  // byte offsets of the class-c payloads (A row-major, B K-major)
   int32_t fexp;          // -(eA + eB): fold factor alpha * 2^fexp
   int32_t l;             // global reduction tile index (bookkeeping)
+  int32_t a_slot, b_slot;  // slot indices in the class arena (TMA row = slot * nb)
 };
 
 template <int C> struct SimtCfg {

@@ -1,37 +1,352 @@
-// gmp_tc.cuh -- S6 grouped tile-GEMM for the FP16 / BF16 / E4M3 classes on the
-// 5th-generation tensor cores (tcgen05.mma, TMEM accumulators, TMA-fed shared
-// memory ring).  [bring-up stub: classes 2..4 run on gmp_simt.cuh until the
-// tcgen05 kernel lands]
+// gmp_tc.cuh -- S6 grouped tile-GEMM for the FP16 / BF16 / E4M3 precision
+// classes on the 5th-generation tensor cores.
+//
+// Persistent, warp-specialised kernel, one CTA per SM:
+//   warp 0      TMA producer: 128x128B (A) and BNx128B (B) boxes, SWIZZLE_128B,
+//               into a STAGES-deep shared-memory ring (mbarrier full/empty).
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//               (kind::f16 for FP16/BF16, kind::f8f6f4 for E4M3; M=128, N=BN,
+//               K=32 bytes per instruction), FP32 accumulation in TMEM,
+//               double-buffered accumulator (2 x BN columns) so the epilogue of
+//               pair p overlaps the MMAs of pair p+1.
+//   warps 2..5  epilogue: tcgen05.ld 32x32b, then the fold of DESIGN.md O9
+//               W = fma_W(RN_W(alpha 2^-(eA+eB)), P, W) into the W accumulator.
+// A work item is a 128 x BN sub-tile of one C tile with its ordered pair list
+// (l of the SUMMA step whose pair class is this launch's class); both operands
+// are K-major payloads in the class arena (A row-major, B transposed), one
+// 2-D TMA descriptor per arena: rows = slot*nb + r, cols = k.
+// Tensor-core accumulation order differs from the oracle's sequential sum: the
+// parity bound is 4 u32 sqrt(K); maps and bytes stay exact.
 #pragma once
+#include <cuda.h>
+
+#include <vector>
+
 #include "gmp_common.cuh"
 #include "gmp_simt.cuh"
 
 namespace gmp {
 
-constexpr bool kTcAvailable = false;
+constexpr bool kTcAvailable = true;
+constexpr int TC_BM = 128;
+constexpr int TC_STAGES = 4;
+constexpr int TC_THREADS = 192;
 
-struct TcTables {
-  int dummy = 0;
-};
+__host__ __device__ constexpr int tc_bn(int nb) { return (nb % 256 == 0) ? 256 : 128; }
 
-inline int64_t tc_items_per_tile(int64_t nb) { return (nb / 128) * (nb / 128); }
-
-inline void tc_make_items(int64_t nb, int32_t ctile, int32_t pbeg, int32_t pcnt, std::vector<WorkItem>& its) {
-  for (int64_t m0 = 0; m0 < nb; m0 += 128)
-    for (int64_t n0 = 0; n0 < nb; n0 += 128)
-      its.push_back(WorkItem{ctile, (int32_t)m0, (int32_t)n0, pbeg, pcnt, 0});
+// ---------------------------------------------------------------------------
+// PTX wrappers (sm_100a)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  const uint32_t a = smem_u32(b);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(b))
+               : "memory");
+}
+// K-major operand, SWIZZLE_128B canonical layout: 8-row x 128-byte atoms,
+// SBO = 1024 B between 8-row groups, LBO unused (1), version 1 (sm_100).
+__device__ __forceinline__ uint64_t sdesc_k_sw128(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// instruction descriptor: D = F32, A/B format, K-major both, N>>3, M>>4
+template <int C, int BN>
+__host__ __device__ constexpr uint32_t tc_idesc() {
+  constexpr uint32_t ab = (C == 3) ? 1u : 0u;   // kind::f16: F16 = 0, BF16 = 1; kind::f8f6f4: E4M3 = 0
+  return (1u << 4) | (ab << 7) | (ab << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
+}
+template <int C>
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  if constexpr (C == 4) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  }
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-inline gmp_status_t tc_prepare(TcTables&, uint8_t*, const int64_t*, const int64_t*, int) { return GMP_OK; }
+// ---------------------------------------------------------------------------
+// the kernel
+// ---------------------------------------------------------------------------
+template <int C, int BN>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+           const WorkItem* __restrict__ items, int nitems, const PairDesc* __restrict__ pairs,
+           const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha) {
+  constexpr int ESZ = (C == 4) ? 1 : 2;
+  constexpr int BK = 128 / ESZ;            // elements per 128-byte K block
+  constexpr int NMMA = 4;                  // 32-byte K per tcgen05.mma
+  constexpr int A_BYTES = TC_BM * 128, B_BYTES = BN * 128, STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr uint32_t TMEM_COLS = 2 * BN;
+  constexpr uint32_t IDESC = tc_idesc<C, BN>();
 
-inline gmp_status_t tc_launch(TcTables&, int cls, const WorkItem* it, int64_t n, const PairDesc* pd,
-                              const CTileDesc* ct, uint8_t* ws, int nb, double alpha, cudaStream_t s) {
-  switch (cls) {
-    case 2: k_simt_class<2><<<(unsigned)n, 256, 0, s>>>(it, pd, ct, ws, nb, alpha); break;
-    case 3: k_simt_class<3><<<(unsigned)n, 256, 0, s>>>(it, pd, ct, ws, nb, alpha); break;
-    default: k_simt_class<4><<<(unsigned)n, 256, 0, s>>>(it, pd, ct, ws, nb, alpha); break;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TC_STAGES * STAGE_BYTES);
+  uint64_t* empty = full + TC_STAGES;
+  uint64_t* tfull = empty + TC_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < TC_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
   }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int kblocks = nb / BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const WorkItem w = items[it];
+        for (int pi = 0; pi < w.pcnt; ++pi) {
+          const PairDesc pd = pairs[w.pbeg + pi];
+          const int arow = pd.a_slot * nb + w.m0, brow = pd.b_slot * nb + w.n0;
+          for (int kb = 0; kb < kblocks; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* sa = smem + stage * STAGE_BYTES;
+            mbar_expect_tx(&full[stage], STAGE_BYTES);
+            tma_load_2d(sa, &tmA, kb * BK, arow, &full[stage]);
+            tma_load_2d(sa + A_BYTES, &tmB, kb * BK, brow, &full[stage]);
+            if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const WorkItem w = items[it];
+        for (int pi = 0; pi < w.pcnt; ++pi) {
+          mbar_wait(&tempty[acc], acc_phase ^ 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+          for (int kb = 0; kb < kblocks; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+            const uint64_t ad = sdesc_k_sw128(sa), bd = sdesc_k_sw128(sa + A_BYTES);
+#pragma unroll
+            for (int k = 0; k < NMMA; ++k)
+              tc_mma<C>(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), IDESC, (kb | k) != 0);
+            tc_commit(&empty[stage]);
+            if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+          }
+          tc_commit(&tfull[acc]);
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+      }
+    }
+  } else {
+    // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 = tile rows
+    const int quarter = warp & 3;
+    const int rloc = quarter * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+      const WorkItem w = items[it];
+      const CTileDesc ct = ctiles[w.ctile];
+      const int64_t rowbase = (int64_t)(w.m0 + rloc) * nb + w.n0;
+      for (int pi = 0; pi < w.pcnt; ++pi) {
+        const PairDesc pd = pairs[w.pbeg + pi];
+        const double f64 = ldexp(alpha, pd.fexp);
+        const float f32 = __double2float_rn(f64);
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN);
+#pragma unroll 1
+        for (int ch = 0; ch < BN / 16; ++ch) {
+          uint32_t r[16];
+          tmem_ld16(tbase + ch * 16, r);
+          if (ct.code == 0) {
+            double2* wp = reinterpret_cast<double2*>(reinterpret_cast<double*>(ws + ct.w_off) + rowbase + ch * 16);
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              double2 x = wp[v];
+              x.x = __fma_rn(f64, (double)__uint_as_float(r[2 * v]), x.x);
+              x.y = __fma_rn(f64, (double)__uint_as_float(r[2 * v + 1]), x.y);
+              wp[v] = x;
+            }
+          } else {
+            float4* wp = reinterpret_cast<float4*>(reinterpret_cast<float*>(ws + ct.w_off) + rowbase + ch * 16);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              float4 x = wp[v];
+              x.x = __fmaf_rn(f32, __uint_as_float(r[4 * v + 0]), x.x);
+              x.y = __fmaf_rn(f32, __uint_as_float(r[4 * v + 1]), x.y);
+              x.z = __fmaf_rn(f32, __uint_as_float(r[4 * v + 2]), x.z);
+              x.w = __fmaf_rn(f32, __uint_as_float(r[4 * v + 3]), x.w);
+              wp[v] = x;
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+}
+
+template <int C, int BN>
+constexpr int tc_smem_bytes() {
+  return TC_STAGES * (TC_BM * 128 + BN * 128) + 1024 /*align*/ + 256 /*barriers*/;
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+struct TcTables {
+  CUtensorMap mapA[5], mapB[5];
+  bool ready[5] = {false, false, false, false, false};
+  int nb = 0;
+};
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline PFN_encodeTiled get_encode_tiled() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
+}
+
+inline int64_t tc_items_per_tile(int64_t nb) { return (nb / TC_BM) * (nb / tc_bn((int)nb)); }
+
+inline void tc_make_items(int64_t nb, int32_t ctile, int32_t pbeg, int32_t pcnt, std::vector<WorkItem>& its) {
+  const int bn = tc_bn((int)nb);
+  for (int64_t m0 = 0; m0 < nb; m0 += TC_BM)
+    for (int64_t n0 = 0; n0 < nb; n0 += bn) its.push_back(WorkItem{ctile, (int32_t)m0, (int32_t)n0, pbeg, pcnt, 0});
+}
+
+inline gmp_status_t tc_prepare(TcTables& t, uint8_t* ws, const int64_t* arena_off, const int64_t* arena_slots, int nb) {
+  t.nb = nb;
+  for (int c = 2; c <= 4; ++c) {
+    t.ready[c] = false;
+    if (arena_slots[c] == 0) continue;
+    PFN_encodeTiled enc = get_encode_tiled();
+    if (!enc) return GMP_ERR_CUDA;
+    const int esz = class_bytes(c);
+    cuuint64_t dims[2] = {(cuuint64_t)nb, (cuuint64_t)(arena_slots[c] * nb)};
+    cuuint64_t strides[1] = {(cuuint64_t)nb * esz};
+    cuuint32_t estr[2] = {1, 1};
+    const CUtensorMapDataType dt = (c == 4) ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16;
+    cuuint32_t boxA[2] = {(cuuint32_t)(128 / esz), (cuuint32_t)TC_BM};
+    cuuint32_t boxB[2] = {(cuuint32_t)(128 / esz), (cuuint32_t)tc_bn(nb)};
+    void* base = ws + arena_off[c];
+    if (enc(&t.mapA[c], dt, 2, base, dims, strides, boxA, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return GMP_ERR_CUDA;
+    if (enc(&t.mapB[c], dt, 2, base, dims, strides, boxB, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return GMP_ERR_CUDA;
+    t.ready[c] = true;
+  }
+  return GMP_OK;
+}
+
+template <int C, int BN>
+inline gmp_status_t tc_launch_t(TcTables& t, const WorkItem* it, int64_t n, const PairDesc* pd, const CTileDesc* ct,
+                                uint8_t* ws, int nb, double alpha, cudaStream_t s) {
+  constexpr int smem = tc_smem_bytes<C, BN>();
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_tc_class<C, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return GMP_ERR_CUDA;
+    attr = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::min<int64_t>(n, sms);
+  k_tc_class<C, BN><<<grid, TC_THREADS, smem, s>>>(t.mapA[C], t.mapB[C], it, (int)n, pd, ct, ws, nb, alpha);
   return cudaGetLastError() == cudaSuccess ? GMP_OK : GMP_ERR_CUDA;
+}
+
+inline gmp_status_t tc_launch(TcTables& t, int cls, const WorkItem* it, int64_t n, const PairDesc* pd,
+                              const CTileDesc* ct, uint8_t* ws, int nb, double alpha, cudaStream_t s) {
+  if (cls < 2 || cls > 4 || !t.ready[cls]) return GMP_ERR_STATE;
+  const bool wide = tc_bn(nb) == 256;
+  switch (cls) {
+    case 2: return wide ? tc_launch_t<2, 256>(t, it, n, pd, ct, ws, nb, alpha, s) : tc_launch_t<2, 128>(t, it, n, pd, ct, ws, nb, alpha, s);
+    case 3: return wide ? tc_launch_t<3, 256>(t, it, n, pd, ct, ws, nb, alpha, s) : tc_launch_t<3, 128>(t, it, n, pd, ct, ws, nb, alpha, s);
+    default: return wide ? tc_launch_t<4, 256>(t, it, n, pd, ct, ws, nb, alpha, s) : tc_launch_t<4, 128>(t, it, n, pd, ct, ws, nb, alpha, s);
+  }
 }
 
 inline void tc_release(TcTables&) {}
