@@ -1,0 +1,420 @@
+#!/usr/bin/env python3
+"""Benchmark of the tile-centric mixed-precision GEMM (arxiv 2508.14848) on B200.
+
+Contract (driver): python bench.py --gpus N --steps K --warmup W [--impl reference]
+prints ONE JSON line on rank 0.
+
+A "step" is one pass of the whole hot path over one GEMM of
+the workload: gemm_mp_plan (map-stats + map-finalize), gemm_mp_convert
+(convert-and-pack + shadows) and gemm_mp_execute (SUMMA broadcasts, grouped
+class tile-GEMMs with fold, C-finalize), inputs resident in HBM.  value =
+2 M N K / (device time per step, max over ranks): whole-job effective TFLOP/s.
+Default workload: BASELINE.json configs[1] (N=16384, nb=1024, tol 1e-8, FP64/FP32/
+FP16 mix).  For N > 1 the same GEMM is distributed 2D block-cyclic on a P x Q
+grid (strong scaling).  Inputs (2 GB per matrix) are far larger than L2.
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import gmp_inputs  # noqa: E402
+
+METRIC = "effective TFLOP/s (2MNK/t) and % of precision-mix roofline at 1/2/4/8 B200"
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+# Non-tensor pipes: FP32 FFMA 128 lanes/SM/clk, FP64 DFMA 64 lanes/SM/clk,
+# 148 SMs, 1965 MHz max clock (B200_PROFILING.md).  Tensor classes: measured BF16 peak
+# (MEASURED_PEAKS.json) x nominal ratio (FP16 = BF16, E4M3 = 2 x BF16).
+ALU_PEAK_TFLOPS = {0: 148 * 64 * 2 * 1.965e9 / 1e12, 1: 148 * 128 * 2 * 1.965e9 / 1e12}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="gemm_mp", choices=["gemm_mp", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--variant", default=None)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(PEAKS_FILE) as f:
+            p = json.load(f)
+        return p, "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+            "fallback (B200_PROFILING.md)"
+
+
+def class_peaks(peaks):
+    bf16 = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    return {0: ALU_PEAK_TFLOPS[0], 1: ALU_PEAK_TFLOPS[1], 2: bf16, 3: bf16, 4: 2 * bf16}
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvml) during the timed region
+# ---------------------------------------------------------------------------
+class Clocks:
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                try:
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except Exception:
+                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def start(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+
+    def stop(self):
+        if self.nv:
+            self._stop.set()
+            self.t.join()
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle baseline (rank 0, N = 1; and the --impl reference arm)
+# ---------------------------------------------------------------------------
+def oracle_pair_sample(w, mix, n_pairs, threads, seed=0):
+    """Times the oracle's tile-GEMM emulation + fold (O8-O9) on n_pairs
+    (A tile, B tile) pairs of workload w, classes drawn in the realised pair mix.
+    Returns (seconds, flops, classes)."""
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+    import oracle
+    L = oracle.lib()
+    nb = w.nb
+    mt, nt, kt = w.M // nb, w.N // nb, w.K // nb
+    rng = np.random.default_rng(seed)
+    tot = sum(mix)
+    counts = [int(round(n_pairs * m / tot)) for m in mix]
+    while sum(counts) < n_pairs:
+        counts[int(np.argmax(mix))] += 1
+    while sum(counts) > n_pairs:
+        counts[int(np.argmax(counts))] -= 1
+    classes = [c for c in range(5) for _ in range(counts[c])]
+    jobs = []
+    for c in classes:
+        i, j, l = int(rng.integers(mt)), int(rng.integers(nt)), int(rng.integers(kt))
+        At = gmp_inputs.synth_block(w.M, w.K, nb, w.a.seed, w.a.mode, w.a.E, w.a.s, w.a.tau, i * nb, nb, l * nb, nb)
+        Bt = gmp_inputs.synth_block(w.K, w.N, nb, w.b.seed, w.b.mode, w.b.E, w.b.s, w.b.tau, l * nb, nb, j * nb, nb)
+        ea = oracle.scale_exp(np.abs(At).max(), c)
+        eb = oracle.scale_exp(np.abs(Bt).max(), c)
+        jobs.append((c, oracle.pack_tile(At, c, ea), oracle.pack_tile(Bt, c, eb, kmajor_t=True), ea, eb))
+
+    def run(job):
+        import ctypes as ct
+        c, pa, pb, ea, eb = job
+        P = np.empty(nb * nb)
+        acc = np.zeros(nb * nb)
+        L.orc_tile_gemm(c, pa.ctypes.data_as(ct.c_void_p), pb.ctypes.data_as(ct.c_void_p), nb,
+                        P.ctypes.data_as(ct.c_void_p))
+        L.orc_fold(nb, 1, w.alpha, ea, eb, P.ctypes.data_as(ct.c_void_p), acc.ctypes.data_as(ct.c_void_p))
+        return float(acc[0])
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(run, jobs))
+    dt = time.perf_counter() - t0
+    return dt, 2.0 * nb ** 3 * len(jobs), classes
+
+
+def cpu_baseline(w, mix, threads=None):
+    import oracle
+    threads = threads or max(1, min(16, os.cpu_count() or 1))
+    n = threads
+    dt, fl, classes = oracle_pair_sample(w, mix, n, threads)
+    cls_count = {gmp_class_name(c): classes.count(c) for c in sorted(set(classes))}
+    return {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
+            "threads_available": oracle.max_threads(),
+            "sample": f"{n} tile-GEMM+fold pairs (nb={w.nb}) of {w.name} in its realised pair-class mix "
+                      f"{cls_count}, one pair per host thread, oracle O8-O9 as it stands; map/pack "
+                      f"phases excluded; wall {dt:.1f} s"}
+
+
+def gmp_class_name(c):
+    return ["FP64", "FP32", "FP16", "BF16", "E4M3"][c]
+
+
+def run_reference(a, w, rank):
+    """--impl reference: the oracle (the CPU reference of this tier) on the host cores."""
+    if rank != 0:
+        return
+    # realised mix of the workload is unknown without running the map; the reference arm
+    # uses the mix the GPU arm reports for cfg2 when available
+    mix = REFERENCE_MIX.get(a.config, [1, 1, 1, 0, 0])
+    threads = max(1, min(16, os.cpu_count() or 1))
+    for _ in range(a.warmup):
+        oracle_pair_sample(w, mix, threads, threads, seed=1)
+    times, fl = [], 0.0
+    for s in range(a.steps):
+        dt, fl, classes = oracle_pair_sample(w, mix, threads, threads, seed=100 + s)
+        times.append(dt)
+    tot = sum(times)
+    value = fl * a.steps / tot / 1e12
+    out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": a.gpus, "steps": a.steps,
+           "warmup": a.warmup, "ms_per_step": tot / a.steps * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32 (emulated classes)", "data": "synthetic",
+           "impl": "reference",
+           "config": {"workload": w.name, "M": w.M, "N": w.N, "K": w.K, "nb": w.nb, "tol": w.tol},
+           "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
+                            "sample": f"per step {threads} tile-GEMM+fold pairs (nb={w.nb}) of {w.name} "
+                                      f"in pair-class mix {mix}, one per host thread"},
+           "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# realised pair mixes (FP64, FP32, FP16, BF16, E4M3) measured by the GPU arm
+REFERENCE_MIX = {1: [5, 52, 7, 0, 0], 2: [916, 2029, 1151, 0, 0]}
+
+
+# ---------------------------------------------------------------------------
+# the GPU arm
+# ---------------------------------------------------------------------------
+def main():
+    a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    w = gmp_inputs.workload(a.config, a.variant)
+    if a.impl == "reference":
+        run_reference(a, w, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2508_14848_b200 import api
+    from paper_2508_14848_b200 import binding as B
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    G = world
+    if G > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    P, Q = api.default_grid(G)
+    p, q = rank // Q, rank % Q
+    stream = torch.cuda.current_stream(dev)
+
+    comm = None
+    if G > 1:
+        uid = B.gemm_mp_nccl_unique_id() if rank == 0 else bytes(128)
+        t = torch.frombuffer(bytearray(uid), dtype=torch.uint8).to(dev)
+        dist.broadcast(t, 0)
+        comm = B.gemm_mp_nccl_comm_create(bytes(t.cpu().numpy()), G, rank)
+
+    # ---- inputs: local block-cyclic parts, generated on the device (N1) ----
+    A = api.synth(w.M, w.K, w.nb, w.a, P, Q, p, q, device=dev)
+    Bm = api.synth(w.K, w.N, w.nb, w.b, P, Q, p, q, device=dev)
+    C = api.synth(w.M, w.N, w.nb, w.c, P, Q, p, q, device=dev) if w.beta != 0 else None
+    lr, lc = api.local_shape(w.M, w.N, w.nb, P, Q, p, q)
+    Cout = torch.empty((max(lr, 1), max(lc, 2)), dtype=torch.float64, device=dev)
+    ldc = Cout.stride(0)
+    torch.cuda.synchronize()
+
+    desc = B.make_desc(w.M, w.N, w.K, w.nb, w.tol, w.alpha, w.beta, w.class_mask, B.GMP_FLAG_TIMING, P, Q, rank)
+    nscr = B.gemm_mp_scratch_size(desc)
+    scratch = torch.empty(nscr, dtype=torch.uint8, device=dev)
+    ws_holder = {"t": None, "bytes": 0}
+
+    def ws_for(nbytes):
+        if ws_holder["bytes"] < nbytes:
+            ws_holder["t"] = None
+            torch.cuda.empty_cache()
+            t = torch.empty(nbytes + 1024, dtype=torch.uint8, device=dev)
+            off = (-t.data_ptr()) % 1024
+            ws_holder.update(t=t, base=t.data_ptr() + off, bytes=nbytes)
+        return ws_holder["base"]
+
+    def step(Ain, Bin, Cin, ev=None):
+        """one pass of the hot path: plan -> convert -> execute"""
+        if ev is not None:
+            ev[0].record(stream)
+        plan = B.gemm_mp_plan(desc, Ain, Ain.stride(0) if Ain.numel() else 1, Bin,
+                              Bin.stride(0) if Bin.numel() else 1, Cin, Cin.stride(0) if Cin is not None else 0,
+                              scratch, nscr, comm, stream)
+        if ev is not None:
+            ev[1].record(stream)
+        nws = B.gemm_mp_workspace_size(plan)
+        if nws > ws_holder["bytes"]:
+            raise RuntimeError("workspace grew inside the timed region")
+        B.gemm_mp_convert(plan, ws_holder["base"], nws, stream)
+        if ev is not None:
+            ev[2].record(stream)
+        B.gemm_mp_execute(plan, Cout, ldc, stream)
+        if ev is not None:
+            ev[3].record(stream)
+        return plan
+
+    # size the workspace once (outside the timed region)
+    p0 = B.gemm_mp_plan(desc, A, A.stride(0) if A.numel() else 1, Bm, Bm.stride(0) if Bm.numel() else 1, C,
+                        C.stride(0) if C is not None else 0, scratch, nscr, comm, stream)
+    ws_for(B.gemm_mp_workspace_size(p0))
+    st0 = B.gemm_mp_get_stats(p0)
+    B.gemm_mp_destroy(p0)
+
+    for _ in range(a.warmup):
+        B.gemm_mp_destroy(step(A, Bm, C))
+    torch.cuda.synchronize()
+
+    clocks = Clocks(local_rank)
+    plans, evs = [], []
+    if G > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for _ in range(a.steps):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        plans.append(step(A, Bm, C, ev))
+        evs.append(ev)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if G > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    elapsed = t_start.elapsed_time(t_end)  # ms, this rank
+    phase = [[e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3])] for e in evs]
+    stats = [B.gemm_mp_get_stats(pl) for pl in plans]
+    for pl in plans:
+        B.gemm_mp_destroy(pl)
+    if G > 1:
+        tt = torch.tensor([elapsed], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed = tt.item()
+    ms_step = elapsed / a.steps
+    value = w.flops / (ms_step * 1e-3) / 1e12
+
+    # ---- roofline of the dominant kernel (per-class device time, this rank) ----
+    peaks, peak_src = load_peaks()
+    cpk = class_peaks(peaks)
+    st = stats[-1]
+    class_ms = [statistics.mean(s["class_ms"][c] for s in stats) for c in range(5)]
+    dom = max(range(5), key=lambda c: class_ms[c])
+    flops_local = [2.0 * w.nb ** 3 * st["pairs_local"][c] for c in range(5)]
+    achieved = flops_local[dom] / (class_ms[dom] * 1e-3) / 1e12 if class_ms[dom] > 0 else 0.0
+    dom_peak = cpk[dom]
+    # precision-mix roofline: sum_c F_c / (G * Peak_c) vs the step time
+    t_roof_ms = sum(st["flops"][c] / (G * cpk[c] * 1e12) for c in range(5)) * 1e3
+    exec_ms = statistics.median(ph[2] for ph in phase)
+    launches = st["launches_plan"] + st["launches_convert"] + st["launches_execute"]
+
+    # ---- e2e: host (pinned) buffers, copies inside the timed region ----
+    hA = A.cpu().pin_memory()
+    hB = Bm.cpu().pin_memory()
+    hC = C.cpu().pin_memory() if C is not None else None
+    hOut = torch.empty(Cout.shape, dtype=torch.float64).pin_memory()
+    dA, dB = torch.empty_like(A), torch.empty_like(Bm)
+    dC = torch.empty_like(C) if C is not None else None
+    h2d = hA.numel() * 8 + hB.numel() * 8 + (hC.numel() * 8 if hC is not None else 0)
+    d2h = lr * lc * 8
+    e_times = []
+    for it in range(a.e2e_steps + 1):
+        if G > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        dA.copy_(hA, non_blocking=True)
+        dB.copy_(hB, non_blocking=True)
+        if dC is not None:
+            dC.copy_(hC, non_blocking=True)
+        pl = step(dA, dB, dC)
+        hOut.copy_(Cout, non_blocking=True)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        B.gemm_mp_destroy(pl)
+        if it > 0:
+            e_times.append(s0.elapsed_time(s1))
+    e2e_ms = statistics.mean(e_times)
+    if G > 1:
+        tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = tt.item()
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": G, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if G > 1 else "weak", "vs_baseline": None,
+            "dtype": "f64/f32/f16/bf16" + ("/e4m3" if w.class_mask & 16 else "") + " (per-tile classes)",
+            "data": "synthetic (counter-based SplitMix64, per-tile norm spread; DESIGN.md Input recipe)",
+            "config": {"workload": w.name, "M": w.M, "N": w.N, "K": w.K, "nb": w.nb, "tol": w.tol,
+                       "alpha": w.alpha, "beta": w.beta, "grid": f"{P}x{Q}", "parallelism": f"summa{P}x{Q}",
+                       "l2": "inputs (2+ GB per matrix) > 126 MB L2, no flush needed",
+                       "step": "plan+convert+execute (S1-S7)"},
+            "phases_ms": {"plan": statistics.median(ph[0] for ph in phase),
+                          "convert": statistics.median(ph[1] for ph in phase), "execute": exec_ms},
+            "execute_tflops": w.flops / (exec_ms * 1e-3) / 1e12,
+            "precision_mix_roofline": {"t_roof_ms": t_roof_ms, "frac_of_step": t_roof_ms / ms_step,
+                                       "frac_of_execute": t_roof_ms / exec_ms,
+                                       "class_peaks_tflops": {gmp_class_name(c): round(cpk[c], 1) for c in range(5)},
+                                       "peak_source": peak_src},
+            "mix": {"tiles_a": st["tiles_a"], "tiles_b": st["tiles_b"], "tiles_c": st["tiles_c"],
+                    "pairs": st["pairs"]},
+            "class_ms_rank0": class_ms,
+            "roofline": {"bound": "alu" if dom <= 1 else "tensor", "kernel": f"class {gmp_class_name(dom)} tile-GEMM",
+                         "achieved": achieved, "peak": dom_peak, "unit": "TFLOP/s",
+                         "frac": achieved / dom_peak if dom_peak else None, "traffic": None,
+                         "peak_source": ("derived: 148 SMs x " + ("64 DFMA" if dom == 0 else "128 FFMA") +
+                                         " lanes x 2 x 1965 MHz") if dom <= 1 else peak_src + " bf16 sustained"},
+            "e2e": {"value": w.flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches * a.steps,
+            "gpu_launches_per_step": launches,
+            "clocks": clk,
+        }
+        if G == 1 and not a.no_cpu_baseline:
+            mix = [st["pairs"][c] for c in range(5)]
+            out["cpu_baseline"] = cpu_baseline(w, mix)
+        print(json.dumps(out), flush=True)
+    if comm is not None:
+        dist.barrier()
+        B.gemm_mp_nccl_comm_destroy(comm)
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
