@@ -151,6 +151,23 @@ gmp_status_t gemm_mp_get_tile(gmp_plan_t plan, char which, int64_t ti, int64_t t
 
 gmp_status_t gemm_mp_get_stats(gmp_plan_t plan, gmp_stats_t *out);
 
+/* Host-only plan from given maps (no device work): the same tile lists, arena
+ * layout, work lists and SUMMA schedule as gemm_mp_plan builds after its map
+ * kernels.  acode/bcode/ccode: global code grids; ascale5/bscale5: [tile][5]
+ * class-c scales; cin_scale may be NULL.  For inspecting the schedule and the
+ * multi-rank bookkeeping without a GPU (convert/execute on it fail with
+ * GMP_ERR_STATE until a workspace is given).                                   */
+gmp_status_t gemm_mp_plan_host(const gmp_desc_t *desc, const uint8_t *acode, const uint8_t *bcode,
+                               const uint8_t *ccode, const int16_t *ascale5, const int16_t *bscale5,
+                               const int16_t *cin_scale, gmp_plan_t *out);
+
+/* SUMMA broadcasts of step `step` on this rank, 4 int64 per entry:
+ * {which (0 = A on the row communicator, 1 = B on the column communicator),
+ *  global tile index, root rank inside that communicator, payload bytes}.
+ * entries may be NULL to query the count *n.                                   */
+gmp_status_t gemm_mp_get_schedule(gmp_plan_t plan, int32_t step, int64_t *entries, int64_t cap,
+                                  int64_t *n);
+
 /* NCCL bootstrap helpers (the unique id travels over torch.distributed).      */
 gmp_status_t gemm_mp_nccl_unique_id(void *out128);
 gmp_status_t gemm_mp_nccl_comm_create(const void *id128, int nranks, int rank, void **comm);

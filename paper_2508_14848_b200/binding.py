@@ -81,6 +81,8 @@ def lib():
             "gemm_mp_nccl_comm_create": [vp, ct.c_int, ct.c_int, ct.POINTER(vp)],
             "gemm_mp_nccl_comm_destroy": [vp],
             "gemm_mp_synth": [vp, i64, i64, i64, i32, i32, i32, i32, i32, u64, u64, i32, i32, i32, vp],
+            "gemm_mp_plan_host": [ct.POINTER(gmp_desc_t), vp, vp, vp, vp, vp, vp, ct.POINTER(vp)],
+            "gemm_mp_get_schedule": [vp, i32, vp, i64, ct.POINTER(i64)],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -208,6 +210,28 @@ def gemm_mp_nccl_comm_destroy(comm):
 def gemm_mp_synth(out, ld, rows, cols, nb, P, Q, p, q, seed, tau, mode, E, s, stream=None):
     _check(lib().gemm_mp_synth(_ptr(out), ld, rows, cols, nb, P, Q, p, q, seed, tau, mode, E, s,
                                _stream(stream)))
+
+
+def gemm_mp_plan_host(desc, acode, bcode, ccode, ascale5, bscale5, cin_scale=None):
+    import numpy as np
+    arrs = [np.ascontiguousarray(acode, np.uint8), np.ascontiguousarray(bcode, np.uint8),
+            np.ascontiguousarray(ccode, np.uint8), np.ascontiguousarray(ascale5, np.int16),
+            np.ascontiguousarray(bscale5, np.int16),
+            None if cin_scale is None else np.ascontiguousarray(cin_scale, np.int16)]
+    h = ct.c_void_p()
+    _check(lib().gemm_mp_plan_host(ct.byref(desc), *[None if a is None else a.ctypes.data for a in arrs],
+                                   ct.byref(h)))
+    return h.value
+
+
+def gemm_mp_get_schedule(plan, step):
+    import numpy as np
+    n = ct.c_int64()
+    _check(lib().gemm_mp_get_schedule(plan, step, None, 0, ct.byref(n)))
+    out = np.zeros((n.value, 4), np.int64)
+    if n.value:
+        _check(lib().gemm_mp_get_schedule(plan, step, out.ctypes.data, n.value, ct.byref(n)))
+    return out
 
 
 def gemm_mp_destroy(plan):

@@ -57,13 +57,14 @@ static inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * 
 // plan
 // ---------------------------------------------------------------------------
 struct Launch {
-  int step, cls, kind;  // kind 0: SIMT kernel, 1: tcgen05 kernel
+  int step, cls, kind;  // kind 0: product SIMT/DMMA kernel, 1: tcgen05 kernel, 2: FP64 DFMA cross-check
   int64_t ibeg, icount;
 };
 
 struct Bcast {           // one SUMMA broadcast of a stored tile in a step
   int which;             // 0: A on the row communicator, 1: B on the column communicator
   int root;              // root rank inside that communicator
+  int64_t tile;          // global tile index (i*kt + l for A, l*nt + j for B)
   int64_t off;           // byte offset of the payload slot (root: its stored tile)
   int64_t bytes;
 };
@@ -367,14 +368,14 @@ static void build_tables(gmp_plan_s* pl) {
       for (int64_t i = p; i < mt; i += P) {       // A(i,l) along process row p, root column l % Q
         const int64_t g = i * kt + l;
         const int c = pl->codeA[g];
-        Bcast b{0, (int)(l % Q), arena(c, pl->slotA5[g * 5 + c]), pl->slot_bytes[c]};
+        Bcast b{0, (int)(l % Q), g, arena(c, pl->slotA5[g * 5 + c]), pl->slot_bytes[c]};
         pl->bcast_step[s].push_back(b);
         if ((int)(l % Q) != q) recv_bytes += b.bytes;
       }
       for (int64_t j = q; j < nt; j += Q) {       // B(l,j) along process column q, root row l % P
         const int64_t g = l * nt + j;
         const int c = pl->codeB[g];
-        Bcast b{1, (int)(l % P), arena(c, pl->slotB5[g * 5 + c]), pl->slot_bytes[c]};
+        Bcast b{1, (int)(l % P), g, arena(c, pl->slotB5[g * 5 + c]), pl->slot_bytes[c]};
         pl->bcast_step[s].push_back(b);
         if ((int)(l % P) != p) recv_bytes += b.bytes;
       }
@@ -415,7 +416,8 @@ static void build_tables(gmp_plan_s* pl) {
       if (its.empty()) continue;
       std::stable_sort(its.begin(), its.end(), [](const WorkItem& a, const WorkItem& b) { return a.pcnt > b.pcnt; });
       pl->items.insert(pl->items.end(), its.begin(), its.end());
-      pl->launches.push_back(Launch{s, c, tc ? 1 : 0, ibeg, (int64_t)its.size()});
+      const int kind = tc ? 1 : (c == 0 && (d.flags & GMP_FLAG_SIMT_ONLY)) ? 2 : 0;
+      pl->launches.push_back(Launch{s, c, kind, ibeg, (int64_t)its.size()});
     }
   }
 
@@ -443,6 +445,18 @@ static void build_tables(gmp_plan_s* pl) {
   st.launches_plan = 2;
   st.launches_convert = (pl->pack.empty() ? 0 : 1) + (pl->shadow_local.empty() ? 0 : 1);
   for (const Launch& L : pl->launches) st.class_launches[L.cls]++;
+}
+
+// 2D block-cyclic ownership: tile (i, j) of a grid lives on rank (i mod P, j mod Q)
+static void local_tiles(gmp_plan_s* pl) {
+  const int P = pl->P, Q = pl->Q;
+  pl->locA.clear(); pl->locB.clear(); pl->locC.clear();
+  for (int64_t i = pl->p; i < pl->mt; i += P)
+    for (int64_t l = pl->q; l < pl->kt; l += Q) pl->locA.push_back(i * pl->kt + l);
+  for (int64_t l = pl->p; l < pl->kt; l += P)
+    for (int64_t j = pl->q; j < pl->nt; j += Q) pl->locB.push_back(l * pl->nt + j);
+  for (int64_t i = pl->p; i < pl->mt; i += P)
+    for (int64_t j = pl->q; j < pl->nt; j += Q) pl->locC.push_back(i * pl->nt + j);
 }
 
 extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, int64_t lda, const double* B,
@@ -482,12 +496,7 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
   if (!chk_map(d.a_map, pl->nA) || !chk_map(d.b_map, pl->nB) || !chk_map(d.c_map, pl->nC))
     return fail(GMP_ERR_MAP_SHAPE, "explicit map holds a code > 4");
 
-  for (int64_t i = pl->p; i < pl->mt; i += d.P)
-    for (int64_t l = pl->q; l < pl->kt; l += d.Q) pl->locA.push_back(i * pl->kt + l);
-  for (int64_t l = pl->p; l < pl->kt; l += d.P)
-    for (int64_t j = pl->q; j < pl->nt; j += d.Q) pl->locB.push_back(l * pl->nt + j);
-  for (int64_t i = pl->p; i < pl->mt; i += d.P)
-    for (int64_t j = pl->q; j < pl->nt; j += d.Q) pl->locC.push_back(i * pl->nt + j);
+  local_tiles(pl);
 
   // ---- S1: stats of local tiles, written at their global index ----
   uint8_t* sc = (uint8_t*)scratch;
@@ -574,6 +583,55 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
     for (auto& e : pl->launch_ev) GMP_CUDA(cudaEventCreate(&e));
   }
   *out = guard.release();
+  return GMP_OK;
+}
+
+extern "C" gmp_status_t gemm_mp_plan_host(const gmp_desc_t* desc, const uint8_t* acode, const uint8_t* bcode,
+                                          const uint8_t* ccode, const int16_t* ascale5, const int16_t* bscale5,
+                                          const int16_t* cin_scale, gmp_plan_t* out) {
+  GMP_TRY(check_desc(desc));
+  if (!out || !acode || !bcode || !ccode || !ascale5 || !bscale5) return fail(GMP_ERR_ARG, "NULL argument");
+  *out = nullptr;
+  const gmp_desc_t& d = *desc;
+  auto pl = new gmp_plan_s();
+  std::unique_ptr<gmp_plan_s> guard(pl);
+  pl->d = d;
+  pl->d.a_map = pl->d.b_map = pl->d.c_map = nullptr;
+  pl->mt = d.M / d.nb; pl->nt = d.N / d.nb; pl->kt = d.K / d.nb;
+  pl->nA = pl->mt * pl->kt; pl->nB = pl->kt * pl->nt; pl->nC = pl->mt * pl->nt;
+  pl->P = d.P; pl->Q = d.Q; pl->p = d.rank / d.Q; pl->q = d.rank % d.Q;
+  for (int64_t t = 0; t < pl->nA; ++t) if (acode[t] > 4) return fail(GMP_ERR_MAP_SHAPE, "code > 4");
+  for (int64_t t = 0; t < pl->nB; ++t) if (bcode[t] > 4) return fail(GMP_ERR_MAP_SHAPE, "code > 4");
+  for (int64_t t = 0; t < pl->nC; ++t) if (ccode[t] > 4) return fail(GMP_ERR_MAP_SHAPE, "code > 4");
+  pl->codeA.assign(acode, acode + pl->nA);
+  pl->codeB.assign(bcode, bcode + pl->nB);
+  pl->codeC.assign(ccode, ccode + pl->nC);
+  pl->sA5.assign(ascale5, ascale5 + pl->nA * 5);
+  pl->sB5.assign(bscale5, bscale5 + pl->nB * 5);
+  pl->sCin.assign(pl->nC, 0);
+  if (cin_scale) pl->sCin.assign(cin_scale, cin_scale + pl->nC);
+  pl->sCout.assign(pl->nC, 0);
+  local_tiles(pl);
+  build_tables(pl);
+  *out = guard.release();
+  return GMP_OK;
+}
+
+extern "C" gmp_status_t gemm_mp_get_schedule(gmp_plan_t pl, int32_t step, int64_t* entries, int64_t cap,
+                                             int64_t* n) {
+  if (!pl || !n) return fail(GMP_ERR_ARG, "NULL argument");
+  if (step < 0 || step >= (int32_t)pl->bcast_step.size()) return fail(GMP_ERR_ARG, "step out of range");
+  const auto& v = pl->bcast_step[step];
+  *n = (int64_t)v.size();
+  if (entries) {
+    if (cap < (int64_t)v.size()) return fail(GMP_ERR_ARG, "entries buffer too small");
+    for (size_t k = 0; k < v.size(); ++k) {
+      entries[4 * k + 0] = v[k].which;
+      entries[4 * k + 1] = v[k].tile;
+      entries[4 * k + 2] = v[k].root;
+      entries[4 * k + 3] = v[k].bytes;
+    }
+  }
   return GMP_OK;
 }
 
@@ -679,8 +737,32 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
       } else {
         switch (L.cls) {
 #define GMP_L(C) case C: k_simt_class<C><<<(unsigned)L.icount, 256, 0, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha); break;
-          GMP_L(0) GMP_L(1) GMP_L(2) GMP_L(3) GMP_L(4)
+#define GMP_L2(C)                                                                                        \
+  case C: {                                                                                              \
+    static bool attr = false;                                                                            \
+    if (!attr) {                                                                                         \
+      GMP_CUDA(cudaFuncSetAttribute(k_simt2<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,             \
+                                    simt2_smem_bytes<C>()));                                             \
+      attr = true;                                                                                       \
+    }                                                                                                    \
+    k_simt2<C><<<(unsigned)L.icount, 256, simt2_smem_bytes<C>(), stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha); \
+  } break;
+          case 0:
+            if (L.kind == 2) {
+              k_simt_class<0><<<(unsigned)L.icount, 256, 0, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha);
+            } else {
+              static bool attr = false;
+              if (!attr) {
+                GMP_CUDA(cudaFuncSetAttribute(k_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, dmma_smem_bytes()));
+                attr = true;
+              }
+              k_dmma<<<(unsigned)L.icount, 256, dmma_smem_bytes(), stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha);
+            }
+            break;
+          case 1: k_ffma2<<<(unsigned)L.icount, 256, 0, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha); break;
+          GMP_L(2) GMP_L(3) GMP_L(4)
 #undef GMP_L
+#undef GMP_L2
         }
         GMP_CUDA(cudaGetLastError());
       }

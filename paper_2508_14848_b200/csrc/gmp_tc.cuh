@@ -9,8 +9,9 @@
 //               K=32 bytes per instruction), FP32 accumulation in TMEM,
 //               double-buffered accumulator (2 x BN columns) so the epilogue of
 //               pair p overlaps the MMAs of pair p+1.
-//   warps 2..5  epilogue: tcgen05.ld 32x32b, then the fold of DESIGN.md O9
-//               W = fma_W(RN_W(alpha 2^-(eA+eB)), P, W) into the W accumulator.
+//   warps 2..9  epilogue: tcgen05.ld 32x32b, then the fold of DESIGN.md O9
+//               W = fma_W(RN_W(alpha 2^-(eA+eB)), P, W); binary32 W rows stay in
+//               registers for the whole item (one W read/write per item).
 // A work item is a 128 x BN sub-tile of one C tile with its ordered pair list
 // (l of the SUMMA step whose pair class is this launch's class); both operands
 // are K-major payloads in the class arena (A row-major, B transposed), one
@@ -30,7 +31,8 @@ namespace gmp {
 constexpr bool kTcAvailable = true;
 constexpr int TC_BM = 128;
 constexpr int TC_STAGES = 4;
-constexpr int TC_THREADS = 192;
+constexpr int TC_THREADS = 320;   // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
+constexpr int TC_EPI_WARPS = 8;
 
 __host__ __device__ constexpr int tc_bn(int nb) { return (nb % 256 == 0) ? 256 : 128; }
 
@@ -100,14 +102,14 @@ __device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
   }
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t* r) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // ---------------------------------------------------------------------------
 // the kernel
@@ -135,7 +137,7 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < TC_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 4); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], TC_EPI_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
@@ -198,28 +200,63 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
       }
     }
   } else {
-    // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 = tile rows
-    const int quarter = warp & 3;
+    // epilogue: 8 warps; warp w reads TMEM lanes 32*(w%4)..+31 (= tile rows) and
+    // half (w-2)/4 of the BN columns.  binary32 W: the W row segment lives in
+    // registers for the whole item (one read + one write per item instead of
+    // per pair); binary64 W: read-modify-write per pair.
+    constexpr int HC = BN / 2;                  // columns per epilogue thread
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
     const int rloc = quarter * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
       const WorkItem w = items[it];
       const CTileDesc ct = ctiles[w.ctile];
-      const int64_t rowbase = (int64_t)(w.m0 + rloc) * nb + w.n0;
-      for (int pi = 0; pi < w.pcnt; ++pi) {
-        const PairDesc pd = pairs[w.pbeg + pi];
-        const double f64 = ldexp(alpha, pd.fexp);
-        const float f32 = __double2float_rn(f64);
-        mbar_wait(&tfull[acc], acc_phase);
-        tc_fence_after();
-        const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN);
+      const int64_t rowoff = (int64_t)(w.m0 + rloc) * nb + w.n0 + half * HC;
+      if (ct.code != 0) {
+        float* wrow = reinterpret_cast<float*>(ws + ct.w_off) + rowoff;
+        float accr[HC];
+#pragma unroll
+        for (int v = 0; v < HC / 4; ++v) {
+          float4 x = reinterpret_cast<const float4*>(wrow)[v];
+          accr[4 * v] = x.x; accr[4 * v + 1] = x.y; accr[4 * v + 2] = x.z; accr[4 * v + 3] = x.w;
+        }
+        for (int pi = 0; pi < w.pcnt; ++pi) {
+          const PairDesc pd = pairs[w.pbeg + pi];
+          const float f32 = __double2float_rn(ldexp(alpha, pd.fexp));
+          mbar_wait(&tfull[acc], acc_phase);
+          tc_fence_after();
+          const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + half * HC);
+#pragma unroll
+          for (int ch = 0; ch < HC / 16; ++ch) {
+            uint32_t r[16];
+            tmem_ld16_nowait(tbase + ch * 16, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int v = 0; v < 16; ++v) accr[ch * 16 + v] = __fmaf_rn(f32, __uint_as_float(r[v]), accr[ch * 16 + v]);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+#pragma unroll
+        for (int v = 0; v < HC / 4; ++v)
+          reinterpret_cast<float4*>(wrow)[v] = make_float4(accr[4 * v], accr[4 * v + 1], accr[4 * v + 2], accr[4 * v + 3]);
+      } else {
+        double* wrow = reinterpret_cast<double*>(ws + ct.w_off) + rowoff;
+        for (int pi = 0; pi < w.pcnt; ++pi) {
+          const PairDesc pd = pairs[w.pbeg + pi];
+          const double f64 = ldexp(alpha, pd.fexp);
+          mbar_wait(&tfull[acc], acc_phase);
+          tc_fence_after();
+          const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + half * HC);
 #pragma unroll 1
-        for (int ch = 0; ch < BN / 16; ++ch) {
-          uint32_t r[16];
-          tmem_ld16(tbase + ch * 16, r);
-          if (ct.code == 0) {
-            double2* wp = reinterpret_cast<double2*>(reinterpret_cast<double*>(ws + ct.w_off) + rowbase + ch * 16);
+          for (int ch = 0; ch < HC / 16; ++ch) {
+            uint32_t r[16];
+            tmem_ld16_nowait(tbase + ch * 16, r);
+            tmem_wait_ld();
+            double2* wp = reinterpret_cast<double2*>(wrow + ch * 16);
 #pragma unroll
             for (int v = 0; v < 8; ++v) {
               double2 x = wp[v];
@@ -227,23 +264,12 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
               x.y = __fma_rn(f64, (double)__uint_as_float(r[2 * v + 1]), x.y);
               wp[v] = x;
             }
-          } else {
-            float4* wp = reinterpret_cast<float4*>(reinterpret_cast<float*>(ws + ct.w_off) + rowbase + ch * 16);
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              float4 x = wp[v];
-              x.x = __fmaf_rn(f32, __uint_as_float(r[4 * v + 0]), x.x);
-              x.y = __fmaf_rn(f32, __uint_as_float(r[4 * v + 1]), x.y);
-              x.z = __fmaf_rn(f32, __uint_as_float(r[4 * v + 2]), x.z);
-              x.w = __fmaf_rn(f32, __uint_as_float(r[4 * v + 3]), x.w);
-              wp[v] = x;
-            }
           }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
   }
