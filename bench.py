@@ -142,7 +142,7 @@ def oracle_pair_sample(w, mix, n_pairs, threads, seed=0):
         Bt = gmp_inputs.synth_block(w.K, w.N, nb, w.b.seed, w.b.mode, w.b.E, w.b.s, w.b.tau, l * nb, nb, j * nb, nb)
         ea = oracle.scale_exp(np.abs(At).max(), c)
         eb = oracle.scale_exp(np.abs(Bt).max(), c)
-        jobs.append((c, oracle.pack_tile(At, c, ea), oracle.pack_tile(Bt, c, eb, kmajor_t=True), ea, eb))
+        jobs.append((c, oracle.pack_tile(At, c, ea, role="A"), oracle.pack_tile(Bt, c, eb, role="B"), ea, eb))
 
     def run(job):
         import ctypes as ct

@@ -52,7 +52,9 @@ def lib():
         L.orc_map_input.argtypes = [i64, i64, i32, dbl, ct.c_uint32, vp, vp, vp, vp, vp]
         L.orc_pack_tile.argtypes = [vp, i64, i32, ct.c_int, ct.c_int, ct.c_int, vp]
         L.orc_shadow_tile.restype = ct.c_int
-        L.orc_shadow_tile.argtypes = [vp, i32, ct.c_int, ct.c_int, ct.c_int, vp]
+        L.orc_shadow_tile.argtypes = [vp, i32, ct.c_int, ct.c_int, ct.c_int, ct.c_int, vp]
+        L.orc_layout_transposed.restype = ct.c_int
+        L.orc_layout_transposed.argtypes = [ct.c_int, ct.c_int]
         L.orc_tile_gemm.argtypes = [ct.c_int, vp, vp, i32, vp]
         L.orc_acc_init.argtypes = [i32, ct.c_int, dbl, vp, ct.c_int, vp]
         L.orc_fold.argtypes = [i32, ct.c_int, dbl, ct.c_int, ct.c_int, vp, vp]
@@ -135,18 +137,29 @@ def map_input(S, M, nb, tol, class_mask, finite=None):
 
 
 # ---- O6 packing / shadows -------------------------------------------------
-def pack_tile(tile, cls, scale, kmajor_t=False):
+ROLE = {"A": 0, "B": 1, "C": 2}
+
+
+def layout_transposed(role, cls):
+    """payload layout of a tile of matrix role ('A', 'B', 'C') at class cls (O6)"""
+    return bool(lib().orc_layout_transposed(ROLE.get(role, role), cls))
+
+
+def pack_tile(tile, cls, scale, transpose=False, role=None):
+    """payload of one tile; pass role='A'/'B'/'C' to use the library layout of O6"""
     t = np.ascontiguousarray(tile, dtype=np.float64)
     nb = t.shape[0]
+    if role is not None:
+        transpose = layout_transposed(role, cls)
     out = np.empty(nb * nb, dtype=PAYLOAD_DTYPE[cls])
-    lib().orc_pack_tile(_p(t), nb, nb, cls, scale, int(kmajor_t), _p(out))
+    lib().orc_pack_tile(_p(t), nb, nb, cls, scale, int(transpose), _p(out))
     return out
 
 
-def shadow_tile(payload, nb, frm, frm_scale, to):
+def shadow_tile(payload, nb, frm, frm_scale, to, role="A"):
     out = np.empty(nb * nb, dtype=PAYLOAD_DTYPE[to])
     p = np.ascontiguousarray(payload)
-    e = lib().orc_shadow_tile(_p(p), nb, frm, frm_scale, to, _p(out))
+    e = lib().orc_shadow_tile(_p(p), nb, ROLE.get(role, role), frm, frm_scale, to, _p(out))
     return out, int(e)
 
 

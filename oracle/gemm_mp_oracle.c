@@ -320,16 +320,27 @@ double orc_payload_value(const void *payload, int64_t idx, int cls) {
     return orc_decode(b, cls);
 }
 
-/* Stored payload of one tile: element (r,c) of the tile is RN_cls(x(r,c) 2^scale).
- * kmajor_t = 0: row-major (A and C tiles, payload[r*nb+c]);
- * kmajor_t = 1: transposed (B tiles, payload[c*nb+r], K contiguous). */
+/* Payload layout (O6 "Packed layout"): element (r,c) of a tile is at
+ * payload[r*nb + c] (not transposed) or payload[c*nb + r] (transposed).
+ *   FP64 / FP32 classes: MN-major operands -- A transposed (column-major), B not;
+ *   FP16 / BF16 / E4M3 classes: K-major operands -- A not transposed, B transposed;
+ *   C tiles (packed C_in / C_out): not transposed.
+ * role: 0 = A, 1 = B, 2 = C. */
+int orc_layout_transposed(int role, int cls) {
+    if (role == 2) return 0;
+    int mn_major = cls <= 1;
+    return role == 0 ? mn_major : !mn_major;
+}
+
+/* Stored payload of one tile: element (r,c) of the tile is RN_cls(x(r,c) 2^scale),
+ * written at the index given by `transpose` (see orc_layout_transposed). */
 void orc_pack_tile(const double *X, int64_t ld, int32_t nb, int cls, int scale,
-                   int kmajor_t, void *payload) {
+                   int transpose, void *payload) {
     for (int32_t r = 0; r < nb; ++r)
         for (int32_t c = 0; c < nb; ++c) {
             double x = X[(int64_t)r * ld + c];
             double y = (cls == 0) ? x : ldexp(x, scale);
-            int64_t idx = kmajor_t ? (int64_t)c * nb + r : (int64_t)r * nb + c;
+            int64_t idx = transpose ? (int64_t)c * nb + r : (int64_t)r * nb + c;
             orc_store_elem(payload, idx, cls, y);
         }
 }
@@ -337,7 +348,7 @@ void orc_pack_tile(const double *X, int64_t ld, int32_t nb, int cls, int scale,
 /* Shadow of a stored tile: decode the stored payload (class `from`, scale e_from),
  * take its maxabs, choose the class-`to` scale for the decoded tile, round once
  * from the decoded value.  Returns the shadow scale e_to = e_from + d. */
-int orc_shadow_tile(const void *payload, int32_t nb, int from, int from_scale, int to,
+int orc_shadow_tile(const void *payload, int32_t nb, int role, int from, int from_scale, int to,
                     void *out) {
     int64_t n = (int64_t)nb * nb;
     double m = 0.0;
@@ -348,8 +359,13 @@ int orc_shadow_tile(const void *payload, int32_t nb, int from, int from_scale, i
     /* decoded tile = w * 2^-from_scale; its scale for class `to` is
      * orc_scale_exp(m * 2^-from_scale, to) = from_scale + orc_scale_exp(m, to)  */
     int d = orc_scale_exp(m, to);
-    for (int64_t i = 0; i < n; ++i)
-        orc_store_elem(out, i, to, ldexp(orc_payload_value(payload, i, from), d));
+    int tf = orc_layout_transposed(role, from), tt = orc_layout_transposed(role, to);
+    for (int32_t r = 0; r < nb; ++r)
+        for (int32_t c = 0; c < nb; ++c) {
+            int64_t src = tf ? (int64_t)c * nb + r : (int64_t)r * nb + c;
+            int64_t dst = tt ? (int64_t)c * nb + r : (int64_t)r * nb + c;
+            orc_store_elem(out, dst, to, ldexp(orc_payload_value(payload, src, from), d));
+        }
     return from_scale + d;
 }
 
@@ -421,7 +437,8 @@ int orc_map_c(int64_t mt, int64_t nt, int64_t kt, int32_t nb, double tol, double
 
 /* ------------------------------------------------------------------------- */
 /* O8. Tile-GEMM emulation for pair class c (O8, R6, R8).            */
-/*   a: row-major nb x nb payload of class c; b: K-major (transposed) payload. */
+/*   a, b: class-c payloads of the A and B tiles in the layout of            */
+/*   orc_layout_transposed (read as a[r][p] and b[p][col]).                   */
 /*   P[r][col] = sum_p a[r][p] b[p][col], sequential p = 0..nb-1, from +0:    */
 /*     c = 0: binary64 fma;  c = 1: binary32 fmaf;                            */
 /*     c >= 2: binary32 acc + a*b (the product is exact in binary32).         */
@@ -431,10 +448,14 @@ void orc_tile_gemm(int cls, const void *a, const void *b, int32_t nb, double *P)
     int64_t n = (int64_t)nb * nb;
     double *av = (double *)malloc(sizeof(double) * n);
     double *bv = (double *)malloc(sizeof(double) * n);
-    for (int64_t i = 0; i < n; ++i) {
-        av[i] = orc_payload_value(a, i, cls);
-        bv[i] = orc_payload_value(b, i, cls);
-    }
+    int ta = orc_layout_transposed(0, cls), tb = orc_layout_transposed(1, cls);
+    for (int32_t r = 0; r < nb; ++r)         /* av[r*nb + p] = A(r,p), bv[col*nb + p] = B(p,col) */
+        for (int32_t p = 0; p < nb; ++p) {
+            av[(int64_t)r * nb + p] =
+                orc_payload_value(a, ta ? (int64_t)p * nb + r : (int64_t)r * nb + p, cls);
+            bv[(int64_t)r * nb + p] =
+                orc_payload_value(b, tb ? (int64_t)r * nb + p : (int64_t)p * nb + r, cls);
+        }
     for (int32_t r = 0; r < nb; ++r) {
         for (int32_t col = 0; col < nb; ++col) {
             const double *ar = av + (int64_t)r * nb;
@@ -607,10 +628,10 @@ int orc_gemm_mp(const orc_desc_t *d, const double *A, int64_t lda, const double 
         for (int c = 0; c < 5; ++c) s5[c] = 0;
         s5[code] = isB ? sb[tt] : sa[tt];
         pp[code] = malloc((size_t)tsz * ORC_FMT[code].bytes);
-        orc_pack_tile(tp, ld, nb, code, s5[code], isB, pp[code]);
+        orc_pack_tile(tp, ld, nb, code, s5[code], orc_layout_transposed(isB, code), pp[code]);
         for (int c = code + 1; c < 5; ++c) {
             void *dst = keep ? malloc((size_t)tsz * ORC_FMT[c].bytes) : tmp;
-            s5[c] = (int16_t)orc_shadow_tile(pp[code], nb, code, s5[code], c, dst);
+            s5[c] = (int16_t)orc_shadow_tile(pp[code], nb, isB, code, s5[code], c, dst);
             if (keep) pp[c] = dst;
         }
         if (!keep) { free(pp[code]); pp[code] = NULL; }

@@ -48,7 +48,7 @@ def test_cfg2_fullsize_sampled():
         code = int(o["acode"][ti, tj])
         got, sc = g.tile("A", ti, tj, code)
         ref = oracle.pack_tile(Ah[ti * nb:(ti + 1) * nb, tj * nb:(tj + 1) * nb], code,
-                               int(o["ascale5"][ti, tj, code]))
+                               int(o["ascale5"][ti, tj, code]), role="A")
         assert sc == o["ascale5"][ti, tj, code]
         assert np.array_equal(got, ref.view(np.uint8))
     Cg = out.cpu().numpy()

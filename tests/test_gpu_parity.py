@@ -70,7 +70,7 @@ def test_packed_bytes_bitwise(case):
             for tj in range(cols):
                 code = int(codes[ti, tj])
                 tile = X[ti * nb:(ti + 1) * nb, tj * nb:(tj + 1) * nb]
-                stored = oracle.pack_tile(tile, code, int(s5[ti, tj, code]), kmajor_t=kmaj)
+                stored = oracle.pack_tile(tile, code, int(s5[ti, tj, code]), role=which)
                 got, sc = g.tile(which, ti, tj, code)
                 assert sc == s5[ti, tj, code]
                 assert np.array_equal(got, stored.view(np.uint8)), (which, ti, tj, code)
@@ -80,7 +80,7 @@ def test_packed_bytes_bitwise(case):
                         got, sc = g.tile(which, ti, tj, c)
                     except B.GmpError:
                         continue  # not needed by any local tile-GEMM
-                    sh, e = oracle.shadow_tile(stored, nb, code, int(s5[ti, tj, code]), c)
+                    sh, e = oracle.shadow_tile(stored, nb, code, int(s5[ti, tj, code]), c, role=which)
                     assert sc == e == s5[ti, tj, c]
                     assert np.array_equal(got, sh.view(np.uint8)), (which, ti, tj, code, c)
                     checked += 1

@@ -16,7 +16,13 @@ FP64, FP32, FP16, BF16, E4M3 = range(5)
 
 
 def _payload(vals, cls, kmajor=False):
-    return oracle.pack_tile(vals, cls, 0, kmajor_t=kmajor)
+    """A operand (kmajor=False) or B operand (kmajor=True) payload in the O6 layout"""
+    return oracle.pack_tile(vals, cls, 0, role="B" if kmajor else "A")
+
+
+def _values(payload, cls, role, nb):
+    v = oracle.payload_values(payload, cls).reshape(nb, nb)
+    return v.T if oracle.layout_transposed(role, cls) else v
 
 
 def _fraction_tile_gemm(a, b, cls):
@@ -48,8 +54,8 @@ def test_tile_gemm_bitwise_vs_fraction_emulation(cls):
     b = rng.standard_normal((nb, nb)) * 3
     # make the operands exactly representable in the class first
     pa, pb = _payload(a, cls), _payload(b, cls, kmajor=True)
-    av = oracle.payload_values(pa, cls).reshape(nb, nb)
-    bv = oracle.payload_values(pb, cls).reshape(nb, nb).T
+    av = _values(pa, cls, "A", nb)
+    bv = _values(pb, cls, "B", nb)
     got = oracle.tile_gemm(cls, pa, pb, nb)
     want = _fraction_tile_gemm(av, bv, cls)
     assert np.array_equal(got, want)
@@ -63,8 +69,8 @@ def test_tile_gemm_gamma_bound(cls, u):
     scale = {FP16: 100.0, E4M3: 10.0}.get(cls, 1.0)
     pa = _payload(rng.standard_normal((nb, nb)) * scale, cls)
     pb = _payload(rng.standard_normal((nb, nb)) * scale, cls, kmajor=True)
-    av = oracle.payload_values(pa, cls).reshape(nb, nb)
-    bv = oracle.payload_values(pb, cls).reshape(nb, nb).T
+    av = _values(pa, cls, "A", nb)
+    bv = _values(pb, cls, "B", nb)
     got = oracle.tile_gemm(cls, pa, pb, nb)
     exact = [[sum(Fraction(float(av[r, p])) * Fraction(float(bv[p, c])) for p in range(nb))
               for c in range(0, nb, 7)] for r in range(0, nb, 5)]

@@ -169,13 +169,23 @@ def test_storage_error_bound(tol, mask, E):
     assert len(np.unique(code)) >= 2  # the recipe really mixes classes
 
 
-def test_pack_b_is_k_major():
+def test_pack_layouts():
+    """O6: FP64/FP32 operands MN-major (A column-major, B row-major), FP16/BF16/E4M3
+    operands K-major (A row-major, B column-major), C row-major."""
     rng = np.random.default_rng(4)
     t = rng.standard_normal((32, 32))
-    a = oracle.pack_tile(t, FP32, 0, kmajor_t=False).reshape(32, 32)
-    b = oracle.pack_tile(t, FP32, 0, kmajor_t=True).reshape(32, 32)
-    assert np.array_equal(a.T, b)
-    assert np.array_equal(a.view(np.float32), t.astype(np.float32))
+    plain = oracle.pack_tile(t, FP32, 0, transpose=False).reshape(32, 32)
+    trans = oracle.pack_tile(t, FP32, 0, transpose=True).reshape(32, 32)
+    assert np.array_equal(plain.T, trans)
+    assert np.array_equal(plain.view(np.float32), t.astype(np.float32))
+    assert np.array_equal(oracle.pack_tile(t, FP32, 0, role="A").reshape(32, 32), trans)
+    assert np.array_equal(oracle.pack_tile(t, FP32, 0, role="B").reshape(32, 32), plain)
+    assert np.array_equal(oracle.pack_tile(t, FP64, 0, role="A").reshape(32, 32), oracle.pack_tile(t, FP64, 0).reshape(32, 32).T)
+    for c in (FP16, BF16, E4M3):
+        p = oracle.pack_tile(t, c, 0).reshape(32, 32)
+        assert np.array_equal(oracle.pack_tile(t, c, 0, role="A").reshape(32, 32), p)
+        assert np.array_equal(oracle.pack_tile(t, c, 0, role="B").reshape(32, 32), p.T)
+    assert not oracle.layout_transposed("C", FP64) and not oracle.layout_transposed("C", FP16)
 
 
 def test_pack_fp64_is_copy():
@@ -184,18 +194,24 @@ def test_pack_fp64_is_copy():
     assert np.array_equal(p.view(np.float64).reshape(32, 32), t)
 
 
+@pytest.mark.parametrize("role", ["A", "B"])
 @pytest.mark.parametrize("frm,to", [(0, 1), (0, 2), (0, 4), (1, 2), (1, 3), (2, 3), (2, 4), (3, 4), (1, 4)])
-def test_shadow_is_receiver_side_rounding_of_stored(frm, to):
+def test_shadow_is_receiver_side_rounding_of_stored(frm, to, role):
     """Shadow = RN_to(decoded stored tile) with the scale chosen for the decoded
-    tile (R7): check against numpy/Fraction-free evaluation via the converters'
-    own pinned encode on the decoded values, and the scale definition."""
+    tile (R7), in the target class's layout: check against the pinned encoder
+    applied to the decoded tile and the scale definition."""
     nb = 32
     rng = np.random.default_rng(frm * 5 + to)
     t = rng.standard_normal((nb, nb)) * 2.0 ** -7
     e_from = oracle.scale_exp(np.abs(t).max(), frm)
-    stored = oracle.pack_tile(t, frm, e_from)
-    dec = np.ldexp(oracle.payload_values(stored, frm), -e_from)          # decoded tile
-    sh, e_to = oracle.shadow_tile(stored, nb, frm, e_from, to)
+    stored = oracle.pack_tile(t, frm, e_from, role=role)
+    vals = oracle.payload_values(stored, frm).reshape(nb, nb)
+    if oracle.layout_transposed(role, frm):
+        vals = vals.T
+    dec = np.ldexp(vals, -e_from)                                         # decoded tile (r, c)
+    sh, e_to = oracle.shadow_tile(stored, nb, frm, e_from, to, role=role)
     assert e_to == oracle.scale_exp(np.abs(dec).max(), to)
     want = oracle.encode(np.ldexp(dec, e_to), to)
-    assert np.array_equal(sh.astype(np.uint32), want)
+    if oracle.layout_transposed(role, to):
+        want = want.T
+    assert np.array_equal(sh.astype(np.uint32).reshape(nb, nb), want)

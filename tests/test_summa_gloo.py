@@ -58,12 +58,12 @@ def _worker(rank, G, port, q_out):
             if which == 0:
                 i, l = divmod(g, kt)
                 t = A[i * nb:(i + 1) * nb, l * nb:(l + 1) * nb]
-                c = int(o["acode"][i, l]); e = int(o["ascale5"][i, l, c]); km = False
+                c = int(o["acode"][i, l]); e = int(o["ascale5"][i, l, c]); role = "A"
             else:
                 l, j = divmod(g, nt)
                 t = Bm[l * nb:(l + 1) * nb, j * nb:(j + 1) * nb]
-                c = int(o["bcode"][l, j]); e = int(o["bscale5"][l, j, c]); km = True
-            return oracle.pack_tile(t, c, e, kmajor_t=km).view(np.uint8)
+                c = int(o["bcode"][l, j]); e = int(o["bscale5"][l, j, c]); role = "B"
+            return oracle.pack_tile(t, c, e, role=role).view(np.uint8)
 
         have = {}
         recv = 0
