@@ -53,6 +53,16 @@ static gmp_status_t fail(gmp_status_t s, const std::string& msg) {
 
 static inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
+// Packed layout (O6): FP64/FP32 operand payloads are MN-major (A tiles
+// column-major, B tiles row-major) for the outer-product SIMT/DMMA kernels;
+// FP16/BF16/E4M3 payloads are K-major (A row-major, B column-major) for the
+// tcgen05 descriptors.  role 0 = A, 1 = B.  Returns 1 if element (r,c) of the
+// tile is stored at c*nb + r.
+static inline int16_t layout_transposed(int role, int cls) {
+  const bool mn = cls <= 1;
+  return (int16_t)(role == 0 ? mn : !mn);
+}
+
 // ---------------------------------------------------------------------------
 // plan
 // ---------------------------------------------------------------------------
@@ -255,7 +265,7 @@ static void build_tables(gmp_plan_s* pl) {
         if (!cnt) continue;
         n_pairs += cnt;
         const bool tc = kTcAvailable && (c >= 2) && !(d.flags & GMP_FLAG_SIMT_ONLY);
-        n_items += tc ? tc_items_per_tile(nb) : (nb / 128) * (nb / simt_bn_rt(c));
+        n_items += tc ? tc_items_per_tile(nb) : (nb / 128) * (nb / mn_bn(c));
       }
   const int64_t n_pack = (int64_t)pl->locA.size() + (int64_t)pl->locB.size() + (hasC ? nCl : 0);
   int64_t n_shadow_local = 0, n_shadow_recv = 0;
@@ -302,7 +312,7 @@ static void build_tables(gmp_plan_s* pl) {
     pj.ld = pl->lda;
     pj.cls = pl->codeA[g];
     pj.scale = pl->sA5[g * 5 + pj.cls];
-    pj.transpose = 0;
+    pj.transpose = layout_transposed(0, pj.cls);
     pj.dst_off = arena(pj.cls, pl->slotA5[g * 5 + pj.cls]);
     pl->pack.push_back(pj);
   }
@@ -313,7 +323,7 @@ static void build_tables(gmp_plan_s* pl) {
     pj.ld = pl->ldb;
     pj.cls = pl->codeB[g];
     pj.scale = pl->sB5[g * 5 + pj.cls];
-    pj.transpose = 1;
+    pj.transpose = layout_transposed(1, pj.cls);
     pj.dst_off = arena(pj.cls, pl->slotB5[g * 5 + pj.cls]);
     pl->pack.push_back(pj);
   }
@@ -347,12 +357,16 @@ static void build_tables(gmp_plan_s* pl) {
       sj.from = (int16_t)code;
       sj.to = (int16_t)c;
       sj.d = (int16_t)(s5[c] - s5[code]);
+      sj.transpose = (int16_t)(layout_transposed(isB ? 1 : 0, code) != layout_transposed(isB ? 1 : 0, c));
       if (local) pl->shadow_local.push_back(sj);
       else pl->shadow_step[l / GMP_STEP_DEPTH].push_back(sj);
     }
   };
   for (int64_t g = 0; g < pl->nA; ++g) add_shadows(false, g);
   for (int64_t g = 0; g < pl->nB; ++g) add_shadows(true, g);
+  auto by_kind = [](const ShadowJob& a, const ShadowJob& b) { return a.transpose < b.transpose; };
+  std::stable_sort(pl->shadow_local.begin(), pl->shadow_local.end(), by_kind);
+  for (auto& v : pl->shadow_step) std::stable_sort(v.begin(), v.end(), by_kind);
   pl->shadow_step_off.assign(steps, 0);
   {
     int64_t acc = (int64_t)pl->shadow_local.size();
@@ -409,7 +423,7 @@ static void build_tables(gmp_plan_s* pl) {
           tc_make_items(nb, (int32_t)k, (int32_t)pbeg, (int32_t)pcnt, its);
         } else {
           for (int64_t m0 = 0; m0 < nb; m0 += 128)
-            for (int64_t n0 = 0; n0 < nb; n0 += simt_bn_rt(c))
+            for (int64_t n0 = 0; n0 < nb; n0 += mn_bn(c))
               its.push_back(WorkItem{(int32_t)k, (int32_t)m0, (int32_t)n0, (int32_t)pbeg, (int32_t)pcnt, 0});
         }
       }
@@ -440,10 +454,15 @@ static void build_tables(gmp_plan_s* pl) {
   st.workspace_bytes = pl->ws_bytes;
   st.steps = steps;
   int nl = 3 + (int)pl->launches.size();  // acc init, tile-GEMM launches, maxabs, finalize
-  for (int s = 0; s < steps; ++s) if (!pl->shadow_step[s].empty()) ++nl;
+  auto nsh = [](const std::vector<ShadowJob>& v) {
+    int64_t t = 0;
+    for (const auto& j : v) t += j.transpose;
+    return (t > 0 ? 1 : 0) + ((int64_t)v.size() - t > 0 ? 1 : 0);
+  };
+  for (int s = 0; s < steps; ++s) nl += nsh(pl->shadow_step[s]);
   st.launches_execute = nl;
   st.launches_plan = 2;
-  st.launches_convert = (pl->pack.empty() ? 0 : 1) + (pl->shadow_local.empty() ? 0 : 1);
+  st.launches_convert = (pl->pack.empty() ? 0 : 1) + nsh(pl->shadow_local);
   for (const Launch& L : pl->launches) st.class_launches[L.cls]++;
 }
 
@@ -641,6 +660,36 @@ extern "C" gmp_status_t gemm_mp_workspace_size(gmp_plan_t pl, size_t* bytes) {
   return GMP_OK;
 }
 
+// One launch for the layout-preserving shadows and one for the transposing ones;
+// the job list is ordered so that each kind is a contiguous range (build_tables).
+static gmp_status_t launch_shadows(const ShadowJob* djobs, const std::vector<ShadowJob>& jobs, uint8_t* ws, int nb,
+                                   cudaStream_t s) {
+  int64_t ntr = 0;
+  for (const auto& j : jobs) ntr += j.transpose;
+  const int64_t npl = (int64_t)jobs.size() - ntr;
+  if (npl) {
+    dim3 grid((unsigned)std::max<int64_t>(1, (int64_t)nb * nb / 8 / 256 / 4), (unsigned)npl);
+    k_shadow<<<grid, 256, 0, s>>>(djobs, ws, (int64_t)nb * nb);
+    GMP_CUDA(cudaGetLastError());
+  }
+  if (ntr) {
+    dim3 grid((unsigned)((nb / 64) * (nb / 64)), (unsigned)ntr);
+    k_shadow_t<<<grid, 256, 0, s>>>(djobs + npl, ws, nb);
+    GMP_CUDA(cudaGetLastError());
+  }
+  return GMP_OK;
+}
+
+template <typename K>
+static gmp_status_t set_smem_once(K kernel, int bytes) {
+  static std::vector<const void*> done;
+  const void* key = reinterpret_cast<const void*>(kernel);
+  for (const void* d : done) if (d == key) return GMP_OK;
+  GMP_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.push_back(key);
+  return GMP_OK;
+}
+
 static int grid_for(int64_t n_elems, int per_thread) {
   int64_t blocks = (n_elems / per_thread + 255) / 256;
   return (int)std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 4));
@@ -673,11 +722,7 @@ extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_byte
     GMP_CUDA(cudaGetLastError());
   }
   // S5 shadows of local tiles
-  if (!pl->shadow_local.empty()) {
-    dim3 grid((unsigned)std::max<int64_t>(1, nb * nb / 8 / 256 / 4), (unsigned)pl->shadow_local.size());
-    k_shadow<<<grid, 256, 0, stream>>>((const ShadowJob*)(ws + pl->off_shadow), ws, nb * nb);
-    GMP_CUDA(cudaGetLastError());
-  }
+  GMP_TRY(launch_shadows((const ShadowJob*)(ws + pl->off_shadow), pl->shadow_local, ws, (int)nb, stream));
   pl->converted = true;
   return GMP_OK;
 }
@@ -716,11 +761,8 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
         GMP_NCCL(ncclBroadcast(ws + b.off, ws + b.off, (size_t)b.bytes, ncclUint8, b.root,
                                b.which == 0 ? pl->rowc : pl->colc, pl->comm_stream));
       GMP_NCCL(ncclGroupEnd());
-      if (!pl->shadow_step[s].empty()) {
-        dim3 grid((unsigned)std::max<int64_t>(1, nb2 / 8 / 256 / 4), (unsigned)pl->shadow_step[s].size());
-        k_shadow<<<grid, 256, 0, pl->comm_stream>>>((const ShadowJob*)(ws + pl->off_shadow) + pl->shadow_step_off[s], ws, nb2);
-        GMP_CUDA(cudaGetLastError());
-      }
+      GMP_TRY(launch_shadows((const ShadowJob*)(ws + pl->off_shadow) + pl->shadow_step_off[s], pl->shadow_step[s],
+                             ws, (int)nb, pl->comm_stream));
       GMP_CUDA(cudaEventRecord(pl->step_ev[s], pl->comm_stream));
     }
   }
@@ -736,33 +778,24 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
         GMP_TRY(tc_launch(pl->tc, L.cls, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, stream));
       } else {
         switch (L.cls) {
-#define GMP_L(C) case C: k_simt_class<C><<<(unsigned)L.icount, 256, 0, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha); break;
-#define GMP_L2(C)                                                                                        \
-  case C: {                                                                                              \
-    static bool attr = false;                                                                            \
-    if (!attr) {                                                                                         \
-      GMP_CUDA(cudaFuncSetAttribute(k_simt2<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,             \
-                                    simt2_smem_bytes<C>()));                                             \
-      attr = true;                                                                                       \
-    }                                                                                                    \
-    k_simt2<C><<<(unsigned)L.icount, 256, simt2_smem_bytes<C>(), stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha); \
-  } break;
           case 0:
             if (L.kind == 2) {
-              k_simt_class<0><<<(unsigned)L.icount, 256, 0, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha);
+              GMP_TRY(set_smem_once(k_mn<double>, mn_smem_bytes<double>()));
+              k_mn<double><<<(unsigned)L.icount, 256, mn_smem_bytes<double>(), stream>>>(it, pd, dct, ws, (int)nb,
+                                                                                       pl->d.alpha);
             } else {
-              static bool attr = false;
-              if (!attr) {
-                GMP_CUDA(cudaFuncSetAttribute(k_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, dmma_smem_bytes()));
-                attr = true;
-              }
+              GMP_TRY(set_smem_once(k_dmma, dmma_smem_bytes()));
               k_dmma<<<(unsigned)L.icount, 256, dmma_smem_bytes(), stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha);
             }
             break;
-          case 1: k_ffma2<<<(unsigned)L.icount, 256, 0, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha); break;
-          GMP_L(2) GMP_L(3) GMP_L(4)
-#undef GMP_L
-#undef GMP_L2
+          case 1:
+            GMP_TRY(set_smem_once(k_mn<float>, mn_smem_bytes<float>()));
+            k_mn<float><<<(unsigned)L.icount, 256, mn_smem_bytes<float>(), stream>>>(it, pd, dct, ws, (int)nb,
+                                                                                   pl->d.alpha);
+            break;
+          case 2: k_simt_class<2><<<(unsigned)L.icount, 256, 0, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha); break;
+          case 3: k_simt_class<3><<<(unsigned)L.icount, 256, 0, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha); break;
+          default: k_simt_class<4><<<(unsigned)L.icount, 256, 0, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha); break;
         }
         GMP_CUDA(cudaGetLastError());
       }

@@ -11,9 +11,10 @@
 namespace gmp {
 
 // ---------------------------------------------------------------------------
-// S3 convert-and-pack: one job = one tile.  A and C tiles keep row-major order,
-// B tiles are written K-major (transposed) so that every tile-GEMM operand is
-// K-major.  64x64 sub-block per CTA.
+// S3 convert-and-pack: one job = one tile, 64x64 sub-block per CTA.  The job's
+// transpose flag follows the packed layout of DESIGN.md O6: FP64/FP32 operand
+// tiles MN-major (A transposed), FP16/BF16/E4M3 K-major (B transposed), C tiles
+// row-major.
 // ---------------------------------------------------------------------------
 struct PackJob {
   const double* src;  // top-left element of the binary64 tile
@@ -122,11 +123,13 @@ __global__ void __launch_bounds__(256) k_pack(const PackJob* __restrict__ jobs, 
 // ---------------------------------------------------------------------------
 // S5 shadow convert (receiver-side, from the STORED payload):
 //   shadow = RN_to(decode_from(stored) * 2^d),  d = shadow scale - stored scale.
-// Layout is kept (A row-major, B K-major).  8 elements per thread-iteration.
+// k_shadow keeps the layout (8 elements per thread-iteration); k_shadow_t
+// handles the MN-major -> K-major class changes.
 // ---------------------------------------------------------------------------
 struct ShadowJob {
   int64_t src_off, dst_off;  // byte offsets in the workspace (or panel buffers)
-  int16_t from, to, d, pad;
+  int16_t from, to, d;
+  int16_t transpose;         // 1: layout changes (MN-major FP64/FP32 -> K-major 16/8-bit)
 };
 
 template <int F, int T>
@@ -152,6 +155,46 @@ __global__ void __launch_bounds__(256) k_shadow(const ShadowJob* __restrict__ jo
     GMP_SH(2, 3) GMP_SH(2, 4)
     GMP_SH(3, 4)
 #undef GMP_SH
+    default: break;
+  }
+}
+
+// Transposing shadow (source MN-major class 0/1 -> target K-major class 2..4):
+// 64x64 blocks staged through shared memory, decoded exactly, scaled, rounded
+// once into the target class and written transposed.
+template <int F, int T>
+__device__ __forceinline__ void shadow_t_block(const ShadowJob& j, uint8_t* ws, int nb, int r0, int c0,
+                                               double (*sm)[65]) {
+  const int t = threadIdx.x;
+  const uint8_t* src = ws + j.src_off;
+  uint8_t* dst = ws + j.dst_off;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int unit = t + u * 256;  // 64 rows x 64 cols
+    const int r = unit >> 6, c = unit & 63;
+    sm[r][c] = ldexp(payload_f64(src, (int64_t)(r0 + r) * nb + c0 + c, F), j.d);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int unit = t + u * 256;  // output row (= source col) x 8-element group
+    const int oc = unit >> 3, gq = unit & 7;
+    double v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = sm[gq * 8 + i][oc];
+    store8<T>(dst + ((int64_t)(c0 + oc) * nb + r0 + gq * 8) * class_bytes(T), v);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_shadow_t(const ShadowJob* __restrict__ jobs, uint8_t* ws, int nb) {
+  __shared__ double sm[64][65];
+  const ShadowJob j = jobs[blockIdx.y];
+  const int per = nb / 64;
+  const int r0 = (blockIdx.x / per) * 64, c0 = (blockIdx.x % per) * 64;
+  switch (j.from * 8 + j.to) {
+#define GMP_ST(F, T) case F * 8 + T: shadow_t_block<F, T>(j, ws, nb, r0, c0, sm); break;
+    GMP_ST(0, 2) GMP_ST(0, 3) GMP_ST(0, 4) GMP_ST(1, 2) GMP_ST(1, 3) GMP_ST(1, 4)
+#undef GMP_ST
     default: break;
   }
 }

@@ -18,6 +18,8 @@
 // Classes 2..4 can also run here (payload decoded to binary32): that is the
 // bring-up / cross-check path; the product path for them is gmp_tc.cuh.
 #pragma once
+#include <type_traits>
+
 #include "gmp_common.cuh"
 #include "gmp_convert.cuh"
 
@@ -192,35 +194,8 @@ k_simt_class(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pa
 
 
 // ---------------------------------------------------------------------------
-// Product-path SIMT kernel for the FP64 and FP32 classes.
-// cp.async (LDGSTS) STAGES-deep ring of K-major slices: smem rows are the
-// payload rows themselves (row = m or n, BK contiguous k, padded to 144 B), so
-// the copy needs no transposition; the inner loop reads 4 (FP32) / 2 (FP64)
-// consecutive k of a row with one 128-bit LDS and runs them in increasing k,
-// keeping the per-thread sequential fma order of the oracle (O8).
-// Thread (tx, ty) owns rows ty + 16 i and columns tx + 16 j: A reads are
-// 2-address broadcasts, B reads hit 16 consecutive rows (conflict-free), the W
-// fold is 64-byte coalesced per half-warp.  The (pair, slice) sequence of an
-// item is one continuous pipeline, so the first slices of the next pair are in
-// flight while the current pair finishes and folds.
+// cp.async helpers
 // ---------------------------------------------------------------------------
-template <int C> struct Simt2Cfg;
-template <> struct Simt2Cfg<1> {
-  using T = float;
-  using V = float4;
-  static constexpr int BK = 32, BN = 128, TN = 8, VK = 4, STAGES = 4;
-};
-template <> struct Simt2Cfg<0> {
-  using T = double;
-  using V = double2;
-  static constexpr int BK = 16, BN = 64, TN = 4, VK = 2, STAGES = 4;
-};
-constexpr int SIMT2_ROWB = 144;  // bytes per smem row: 128 B of k + 16 B pad
-
-template <int C> constexpr int simt2_smem_bytes() {
-  return Simt2Cfg<C>::STAGES * (128 + Simt2Cfg<C>::BN) * SIMT2_ROWB;
-}
-
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
 }
@@ -228,126 +203,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int C>
-__global__ void __launch_bounds__(256, 1)
-k_simt2(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
-        const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha) {
-  using Cfg = Simt2Cfg<C>;
-  using T = typename Cfg::T;
-  using V = typename Cfg::V;
-  constexpr int BK = Cfg::BK, BN = Cfg::BN, TN = Cfg::TN, VK = Cfg::VK, ST = Cfg::STAGES;
-  constexpr int EB = sizeof(T);
-  constexpr int ROWS = 128 + BN;                 // A rows then B rows in one stage
-  constexpr int CHUNKS = ROWS * 8;               // 16-byte chunks per stage (128 B per row)
-  constexpr int CPT = CHUNKS / 256;              // chunks per thread
-  extern __shared__ __align__(16) uint8_t sm[];
-
-  const WorkItem it = items[blockIdx.x];
-  const CTileDesc ct = ctiles[it.ctile];
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const int nsl = nb / BK;
-  const int total = it.pcnt * nsl;
-  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
-
-  auto issue = [&](int g) {
-    if (g < total) {
-      const int pi = g / nsl, s = g - pi * nsl;
-      const PairDesc pd = pairs[it.pbeg + pi];
-      const uint32_t stg = sbase + (uint32_t)((g % ST) * ROWS * SIMT2_ROWB);
-#pragma unroll
-      for (int u = 0; u < CPT; ++u) {
-        const int c = tid + u * 256;
-        const int row = c >> 3, part = c & 7;
-        const uint8_t* src = (row < 128)
-            ? ws + pd.a_off + ((int64_t)(it.m0 + row) * nb + (int64_t)s * BK) * EB + part * 16
-            : ws + pd.b_off + ((int64_t)(it.n0 + row - 128) * nb + (int64_t)s * BK) * EB + part * 16;
-        cp_async16(stg + row * SIMT2_ROWB + part * 16, src);
-      }
-    }
-    cp_async_commit();
-  };
-
-#pragma unroll
-  for (int g = 0; g < ST - 1; ++g) issue(g);
-
-  T acc[8][TN];
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
-
-  for (int g = 0; g < total; ++g) {
-    cp_async_wait<ST - 2>();
-    __syncthreads();
-    issue(g + ST - 1);
-    const uint8_t* stg = sm + (g % ST) * ROWS * SIMT2_ROWB;
-    const uint8_t* As = stg;
-    const uint8_t* Bs = stg + 128 * SIMT2_ROWB;
-#pragma unroll
-    for (int kk = 0; kk < BK; kk += VK) {
-      V a[8], b[TN];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const V*>(As + (ty + 16 * i) * SIMT2_ROWB + kk * EB);
-#pragma unroll
-      for (int j = 0; j < TN; ++j) b[j] = *reinterpret_cast<const V*>(Bs + (tx + 16 * j) * SIMT2_ROWB + kk * EB);
-      if constexpr (VK == 4) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-          for (int j = 0; j < TN; ++j) {
-            acc[i][j] = __fmaf_rn(a[i].x, b[j].x, acc[i][j]);
-            acc[i][j] = __fmaf_rn(a[i].y, b[j].y, acc[i][j]);
-            acc[i][j] = __fmaf_rn(a[i].z, b[j].z, acc[i][j]);
-            acc[i][j] = __fmaf_rn(a[i].w, b[j].w, acc[i][j]);
-          }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-          for (int j = 0; j < TN; ++j) {
-            acc[i][j] = __fma_rn(a[i].x, b[j].x, acc[i][j]);
-            acc[i][j] = __fma_rn(a[i].y, b[j].y, acc[i][j]);
-          }
-      }
-    }
-    const int pi = g / nsl;
-    if (g - pi * nsl == nsl - 1) {
-      // ---- fold (DESIGN.md O9): W = fma_W(RN_W(alpha 2^fexp), RN_W(P), W) ----
-      const PairDesc pd = pairs[it.pbeg + pi];
-      const double f64 = ldexp(alpha, pd.fexp);
-      const float f32 = __double2float_rn(f64);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int64_t rb = (int64_t)(it.m0 + ty + 16 * i) * nb + it.n0 + tx;
-#pragma unroll
-        for (int j = 0; j < TN; ++j) {
-          if (ct.code == 0) {
-            double* w = reinterpret_cast<double*>(ws + ct.w_off) + rb + 16 * j;
-            *w = __fma_rn(f64, (double)acc[i][j], *w);
-          } else {
-            float* w = reinterpret_cast<float*>(ws + ct.w_off) + rb + 16 * j;
-            *w = __fmaf_rn(f32, to_f32(acc[i][j]), *w);
-          }
-          acc[i][j] = T(0);
-        }
-      }
-    }
-  }
-  cp_async_wait<0>();
-}
-
-
-// ---------------------------------------------------------------------------
-// Product-path FP32-class kernel: packed FFMA2 (fma.rn.f32x2, sm_100).
-// Blackwell's FP32 pipe reaches its 128 FMA/clk/SM only through the paired
-// FFMA2 (one instruction = two independent IEEE fma.rn on a register pair):
-// the outer product acc[i][j..j+1] += a[i] * (b[j], b[j+1]) uses a[i] as a
-// broadcast scalar operand, so every lane is still one fmaf in increasing k
-// and P stays bitwise the oracle's (O8).  128x128 sub-tile, 256 threads, 8x8
-// outputs per thread (32 float2 accumulators), BK = 16 slices staged through
-// registers into k-major shared memory (As[k][m]) for broadcast 128-bit LDS,
-// double buffered; the (pair, slice) sequence of an item is one pipeline.
-// ---------------------------------------------------------------------------
+// packed FFMA2: two independent IEEE fma.rn.f32 in one instruction, `a` broadcast
 __device__ __forceinline__ float2 ffma2_bcast(float a, float2 b, float2 c) {
   unsigned long long ra, rb, rc;
   asm("mov.b64 %0, {%1, %1};" : "=l"(ra) : "f"(a));
@@ -359,75 +215,122 @@ __device__ __forceinline__ float2 ffma2_bcast(float a, float2 b, float2 c) {
   return d;
 }
 
-__global__ void __launch_bounds__(256, 2)
-k_ffma2(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
-        const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha) {
-  constexpr int BK = 16, PADR = 132;
-  __shared__ __align__(16) float As[2][BK][PADR];
-  __shared__ __align__(16) float Bs[2][BK][PADR];
+// ---------------------------------------------------------------------------
+// FP32 / FP64 outer-product kernel over MN-major payloads (O6):
+// A tiles column-major, B tiles row-major, so a K-slice of a 128-row sub-tile
+// is BK contiguous rows of 128 elements -- copied verbatim by a STAGES-deep
+// cp.async ring into k-major shared memory As[k][m], Bs[k][n].
+//   float  (class 1): 128x128 sub-tile, 8x8 outputs per thread, packed FFMA2
+//                     (Blackwell's FP32 pipe reaches 128 FMA/clk/SM only through
+//                     it); a[i] is a broadcast scalar operand, every lane is one
+//                     fmaf in increasing k -> bitwise the oracle's O8.
+//   double (class 0): 128x64 sub-tile, 8x4 outputs per thread, DFMA; bitwise O8.
+//                     Cross-check kernel (GMP_FLAG_SIMT_ONLY); the product FP64
+//                     path is k_dmma.
+// The (pair, slice) sequence of an item is one continuous pipeline.
+// ---------------------------------------------------------------------------
+template <typename T> struct MnCfg;
+template <> struct MnCfg<float> { static constexpr int BN = 128, BK = 16, ST = 4; };
+template <> struct MnCfg<double> { static constexpr int BN = 64, BK = 16, ST = 4; };
+template <typename T> constexpr int mn_smem_bytes() {
+  return MnCfg<T>::ST * MnCfg<T>::BK * (128 + MnCfg<T>::BN) * (int)sizeof(T);
+}
+inline int mn_bn(int c) { return c == 0 ? 64 : 128; }
+
+template <typename T>
+__global__ void __launch_bounds__(256, 1)
+k_mn(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
+     const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha) {
+  constexpr int BN = MnCfg<T>::BN, BK = MnCfg<T>::BK, ST = MnCfg<T>::ST;
+  constexpr int ES = sizeof(T);
+  constexpr int ACH = 128 * ES / 16, BCH = BN * ES / 16;  // 16-byte chunks per smem row
+  constexpr int CHUNKS = BK * (ACH + BCH), CPT = CHUNKS / 256;
+  constexpr int STAGE = BK * (128 + BN) * ES;            // bytes
+  static_assert(CHUNKS % 256 == 0, "loader");
+  extern __shared__ __align__(16) uint8_t sm[];
   const WorkItem it = items[blockIdx.x];
   const CTileDesc ct = ctiles[it.ctile];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const int nsl = nb / BK;
   const int total = it.pcnt * nsl;
-  // loader: 128 rows x 16 k per operand = 512 float4, 2 per thread; a warp covers
-  // 32 consecutive rows at one k-quad, so the transposing STS are conflict-free
-  int lrow[2], lk[2];
-#pragma unroll
-  for (int u = 0; u < 2; ++u) { const int c = tid + 256 * u; lrow[u] = c & 127; lk[u] = (c >> 7) * 4; }
+  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
 
-  float4 ra[2], rb[2];
-  auto gload = [&](int g) {
-    const int pi = g / nsl, s = g - pi * nsl;
-    const PairDesc pd = pairs[it.pbeg + pi];
-    const float* Ag = reinterpret_cast<const float*>(ws + pd.a_off) + (int64_t)it.m0 * nb + s * BK;
-    const float* Bg = reinterpret_cast<const float*>(ws + pd.b_off) + (int64_t)it.n0 * nb + s * BK;
+  auto issue = [&](int g) {
+    if (g < total) {
+      const int pi = g / nsl, s = g - pi * nsl;
+      const PairDesc pd = pairs[it.pbeg + pi];
+      const uint8_t* Ag = ws + pd.a_off + ((int64_t)s * BK * nb + it.m0) * ES;
+      const uint8_t* Bg = ws + pd.b_off + ((int64_t)s * BK * nb + it.n0) * ES;
+      const uint32_t stg = sbase + (uint32_t)((g % ST) * STAGE);
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      ra[u] = __ldg(reinterpret_cast<const float4*>(Ag + (int64_t)lrow[u] * nb + lk[u]));
-      rb[u] = __ldg(reinterpret_cast<const float4*>(Bg + (int64_t)lrow[u] * nb + lk[u]));
+      for (int u = 0; u < CPT; ++u) {
+        const int c = tid + u * 256;
+        if (c < BK * ACH) {
+          const int k = c / ACH, ch = c - k * ACH;
+          cp_async16(stg + (k * 128) * ES + ch * 16, Ag + (int64_t)k * nb * ES + ch * 16);
+        } else {
+          const int c2 = c - BK * ACH, k = c2 / BCH, ch = c2 - k * BCH;
+          cp_async16(stg + (BK * 128 + k * BN) * ES + ch * 16, Bg + (int64_t)k * nb * ES + ch * 16);
+        }
+      }
     }
-  };
-  auto sstore = [&](int buf) {
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      As[buf][lk[u] + 0][lrow[u]] = ra[u].x; As[buf][lk[u] + 1][lrow[u]] = ra[u].y;
-      As[buf][lk[u] + 2][lrow[u]] = ra[u].z; As[buf][lk[u] + 3][lrow[u]] = ra[u].w;
-      Bs[buf][lk[u] + 0][lrow[u]] = rb[u].x; Bs[buf][lk[u] + 1][lrow[u]] = rb[u].y;
-      Bs[buf][lk[u] + 2][lrow[u]] = rb[u].z; Bs[buf][lk[u] + 3][lrow[u]] = rb[u].w;
-    }
+    cp_async_commit();
   };
 
-  float2 acc[8][4];
+#pragma unroll
+  for (int g = 0; g < ST - 1; ++g) issue(g);
+
+  constexpr int NJ = (sizeof(T) == 4) ? 4 : 4;  // float: 4 float2 pairs; double: 4 scalars
+  using Acc = typename std::conditional<sizeof(T) == 4, float2, double>::type;
+  Acc acc[8][NJ];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
+    for (int j = 0; j < NJ; ++j) {
+      if constexpr (sizeof(T) == 4) acc[i][j] = make_float2(0.f, 0.f);
+      else acc[i][j] = 0.0;
+    }
 
-  gload(0);
-  sstore(0);
-  __syncthreads();
   for (int g = 0; g < total; ++g) {
-    const int buf = g & 1;
-    if (g + 1 < total) gload(g + 1);
+    cp_async_wait<ST - 2>();
+    __syncthreads();
+    issue(g + ST - 1);
+    const T* As = reinterpret_cast<const T*>(sm + (g % ST) * STAGE);
+    const T* Bs = As + BK * 128;
 #pragma unroll
     for (int k = 0; k < BK; ++k) {
-      const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][k][ty * 4]);
-      const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][k][64 + ty * 4]);
-      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][k][tx * 4]);
-      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][k][64 + tx * 4]);
-      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const float2 b[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
-                           make_float2(b1.z, b1.w)};
+      T a[8];
+      if constexpr (sizeof(T) == 4) {
+        const float4 a0 = *reinterpret_cast<const float4*>(As + k * 128 + ty * 4);
+        const float4 a1 = *reinterpret_cast<const float4*>(As + k * 128 + 64 + ty * 4);
+        a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w; a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
+        const float4 b0 = *reinterpret_cast<const float4*>(Bs + k * BN + tx * 4);
+        const float4 b1 = *reinterpret_cast<const float4*>(Bs + k * BN + 64 + tx * 4);
+        const float2 b[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                             make_float2(b1.z, b1.w)};
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = ffma2_bcast(a[i], b[j], acc[i][j]);
+          for (int j = 0; j < 4; ++j) acc[i][j] = ffma2_bcast(a[i], b[j], acc[i][j]);
+      } else {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double2 x0 = *reinterpret_cast<const double2*>(As + k * 128 + h * 64 + ty * 4);
+          const double2 x1 = *reinterpret_cast<const double2*>(As + k * 128 + h * 64 + ty * 4 + 2);
+          a[h * 4 + 0] = x0.x; a[h * 4 + 1] = x0.y; a[h * 4 + 2] = x1.x; a[h * 4 + 3] = x1.y;
+        }
+        const double2 b0 = *reinterpret_cast<const double2*>(Bs + k * BN + tx * 2);
+        const double2 b1 = *reinterpret_cast<const double2*>(Bs + k * BN + 32 + tx * 2);
+        const double b[4] = {b0.x, b0.y, b1.x, b1.y};
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = __fma_rn(a[i], b[j], acc[i][j]);
+      }
     }
-    if (g + 1 < total) sstore(buf ^ 1);
     const int pi = g / nsl;
     if (g - pi * nsl == nsl - 1) {
-      // ---- fold (O9) ----
+      // ---- fold (DESIGN.md O9): W = fma_W(RN_W(alpha 2^fexp), RN_W(P), W) ----
       const PairDesc pd = pairs[it.pbeg + pi];
       const double f64 = ldexp(alpha, pd.fexp);
       const float f32 = __double2float_rn(f64);
@@ -435,43 +338,54 @@ k_ffma2(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
       for (int i = 0; i < 8; ++i) {
         const int r = it.m0 + (i >> 2) * 64 + ty * 4 + (i & 3);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int64_t e = (int64_t)r * nb + it.n0 + (j >> 1) * 64 + tx * 4 + (j & 1) * 2;
+        for (int j = 0; j < NJ; j += (sizeof(T) == 4 ? 1 : 2)) {
+          // float: pair j -> cols (j>>1)*64 + tx*4 + (j&1)*2 + {0,1}
+          // double: scalars j, j+1 -> cols (j>>1)*32 + tx*2 + {0,1}
+          const int col = (sizeof(T) == 4) ? (j >> 1) * 64 + tx * 4 + (j & 1) * 2 : (j >> 1) * 32 + tx * 2;
+          const int64_t e = (int64_t)r * nb + it.n0 + col;
+          double v0, v1;
+          if constexpr (sizeof(T) == 4) { v0 = acc[i][j].x; v1 = acc[i][j].y; }
+          else { v0 = acc[i][j]; v1 = acc[i][j + 1]; }
           if (ct.code == 0) {
             double2* w = reinterpret_cast<double2*>(reinterpret_cast<double*>(ws + ct.w_off) + e);
             double2 v = *w;
-            v.x = __fma_rn(f64, (double)acc[i][j].x, v.x);
-            v.y = __fma_rn(f64, (double)acc[i][j].y, v.y);
+            v.x = __fma_rn(f64, v0, v.x);
+            v.y = __fma_rn(f64, v1, v.y);
             *w = v;
           } else {
             float2* w = reinterpret_cast<float2*>(reinterpret_cast<float*>(ws + ct.w_off) + e);
             float2 v = *w;
-            v.x = __fmaf_rn(f32, acc[i][j].x, v.x);
-            v.y = __fmaf_rn(f32, acc[i][j].y, v.y);
+            v.x = __fmaf_rn(f32, __double2float_rn(v0), v.x);
+            v.y = __fmaf_rn(f32, __double2float_rn(v1), v.y);
             *w = v;
           }
-          acc[i][j] = make_float2(0.f, 0.f);
         }
       }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          if constexpr (sizeof(T) == 4) acc[i][j] = make_float2(0.f, 0.f);
+          else acc[i][j] = 0.0;
+        }
     }
-    __syncthreads();
   }
+  cp_async_wait<0>();
 }
-
 
 // ---------------------------------------------------------------------------
 // Product-path FP64-class kernel on the FP64 tensor pipe (DMMA, legacy
 // mma.sync.m16n8k16.row.col.f64 -- tcgen05 has no FP64 kind).
 // 128x64 sub-tile, 8 warps (4 x 2), warp tile 32x32 = 2 m16 x 4 n8 MMA tiles,
-// binary64 accumulation in registers; BK = 16 (one 128-byte row per operand
-// row) through a 4-stage cp.async ring whose 16-byte chunks are XOR-swizzled
-// by (row mod 8), which makes the m16n8k16 fragment loads conflict-free.
-// The accumulation order inside a DMMA is the hardware's; the parity bound is
+// binary64 accumulation in registers; MN-major payloads, BK = 16 k-rows per
+// stage through a 4-stage cp.async ring into As[k][m] / Bs[k][n] rows padded by
+// 64 bytes so the fragment loads (4 k-rows x 8 consecutive m) are conflict-free.
+// The accumulation order inside a DMMA is the hardware's: the parity bound is
 // the all-FP64 1e-13 relative Frobenius.
 // ---------------------------------------------------------------------------
-constexpr int DMMA_ST = 4;
-constexpr int DMMA_BN = 64;
-constexpr int dmma_smem_bytes() { return DMMA_ST * (128 + DMMA_BN) * 128; }
+constexpr int DMMA_ST = 4, DMMA_BN = 64, DMMA_BK = 16;
+constexpr int DMMA_AP = 128 + 8, DMMA_BP = DMMA_BN + 8;  // row pitches in doubles
+constexpr int dmma_smem_bytes() { return DMMA_ST * DMMA_BK * (DMMA_AP + DMMA_BP) * 8; }
 
 __device__ __forceinline__ void dmma16816(double (&c)[4], const double (&a)[8], const double (&b)[4]) {
   asm volatile(
@@ -485,14 +399,16 @@ __device__ __forceinline__ void dmma16816(double (&c)[4], const double (&a)[8], 
 __global__ void __launch_bounds__(256, 1)
 k_dmma(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
        const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha) {
-  constexpr int BK = 16, ROWS = 128 + DMMA_BN, ST = DMMA_ST;
-  constexpr int CPT = ROWS * 8 / 256;  // 16-byte chunks per thread per stage
+  constexpr int BK = DMMA_BK, ST = DMMA_ST, AP = DMMA_AP, BP = DMMA_BP;
+  constexpr int ACH = 64, BCH = DMMA_BN / 2;        // 16-byte chunks per k-row (A: 128 doubles, B: 64)
+  constexpr int CHUNKS = BK * (ACH + BCH), CPT = CHUNKS / 256;
+  constexpr int STAGE = BK * (AP + BP) * 8;
   extern __shared__ __align__(128) uint8_t sm[];
   const WorkItem it = items[blockIdx.x];
   const CTileDesc ct = ctiles[it.ctile];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;  // warp tile origin in the 128x64 sub-tile
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   const int nsl = nb / BK;
   const int total = it.pcnt * nsl;
   const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
@@ -501,26 +417,23 @@ k_dmma(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
     if (gi < total) {
       const int pi = gi / nsl, s = gi - pi * nsl;
       const PairDesc pd = pairs[it.pbeg + pi];
-      const uint32_t stg = sbase + (uint32_t)((gi % ST) * ROWS * 128);
+      const uint8_t* Ag = ws + pd.a_off + ((int64_t)s * BK * nb + it.m0) * 8;
+      const uint8_t* Bg = ws + pd.b_off + ((int64_t)s * BK * nb + it.n0) * 8;
+      const uint32_t stg = sbase + (uint32_t)((gi % ST) * STAGE);
 #pragma unroll
       for (int u = 0; u < CPT; ++u) {
         const int c = tid + u * 256;
-        const int row = c >> 3, ch = c & 7;
-        const uint8_t* src = (row < 128)
-            ? ws + pd.a_off + ((int64_t)(it.m0 + row) * nb + (int64_t)s * BK) * 8 + ch * 16
-            : ws + pd.b_off + ((int64_t)(it.n0 + row - 128) * nb + (int64_t)s * BK) * 8 + ch * 16;
-        cp_async16(stg + row * 128 + ((ch ^ (row & 7)) << 4), src);
+        if (c < BK * ACH) {
+          const int k = c / ACH, ch = c - k * ACH;
+          cp_async16(stg + k * AP * 8 + ch * 16, Ag + (int64_t)k * nb * 8 + ch * 16);
+        } else {
+          const int c2 = c - BK * ACH, k = c2 / BCH, ch = c2 - k * BCH;
+          cp_async16(stg + BK * AP * 8 + k * BP * 8 + ch * 16, Bg + (int64_t)k * nb * 8 + ch * 16);
+        }
       }
     }
     cp_async_commit();
   };
-  // element (row, k) of a stage sits at row*128 + ((k/2 ^ row%8) << 4) + (k%2)*8.  Every
-  // fragment row of this thread has row%8 == g and k = t + 4r, so the swizzled
-  // offsets are four per-thread constants: off[r] = (((t>>1) ^ g ^ 2r) << 4) + (t&1)*8.
-  int off[4];
-#pragma unroll
-  for (int r = 0; r < 4; ++r) off[r] = ((((t >> 1) ^ g) ^ (2 * r)) << 4) + ((t & 1) << 3);
-  const int abase = (wm + g) * 128, bbase = (128 + wn + g) * 128;
 
 #pragma unroll
   for (int gi = 0; gi < ST - 1; ++gi) issue(gi);
@@ -537,17 +450,17 @@ k_dmma(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
     cp_async_wait<ST - 2>();
     __syncthreads();
     issue(gi + ST - 1);
-    const uint8_t* stg = sm + (gi % ST) * ROWS * 128;
+    const double* As = reinterpret_cast<const double*>(sm + (gi % ST) * STAGE);
+    const double* Bs = As + BK * AP;
     double a[2][8], b[4][4];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
-        a[i][r] = *reinterpret_cast<const double*>(stg + abase + (i * 16 + 8 * (r & 1)) * 128 + off[r >> 1]);
+      for (int r = 0; r < 8; ++r) a[i][r] = As[(t + 4 * (r >> 1)) * AP + wm + i * 16 + g + 8 * (r & 1)];
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
-      for (int r = 0; r < 4; ++r) b[j][r] = *reinterpret_cast<const double*>(stg + bbase + j * 8 * 128 + off[r]);
+      for (int r = 0; r < 4; ++r) b[j][r] = Bs[(t + 4 * r) * BP + wn + j * 8 + g];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll

@@ -20,8 +20,12 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--flags", type=int, default=0)
     ap.add_argument("--mask", type=int, default=None)
+    ap.add_argument("--size", type=int, default=0, help="override M=N=K (keeps the config's recipe)")
     a = ap.parse_args()
     w = gmp_inputs.workload(a.cfg, a.variant)
+    if a.size:
+        import dataclasses
+        w = dataclasses.replace(w, M=a.size, N=a.size, K=a.size, name=w.name + f"_size{a.size}")
     dev = torch.device("cuda:0")
     t0 = time.time()
     A = api.synth(w.M, w.K, w.nb, w.a)
