@@ -238,7 +238,7 @@ template <typename T> constexpr int mn_smem_bytes() {
 inline int mn_bn(int c) { return c == 0 ? 64 : 128; }
 
 template <typename T>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 2 : 1)
 k_mn(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
      const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha) {
   constexpr int BN = MnCfg<T>::BN, BK = MnCfg<T>::BK, ST = MnCfg<T>::ST;
@@ -255,13 +255,18 @@ k_mn(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
   const int total = it.pcnt * nsl;
   const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
 
+  // producer cursor over the (pair, slice) sequence: no divisions in the loop
+  int ip = 0, is = 0, istage = 0;
+  const uint8_t *Ag = nullptr, *Bg = nullptr;
+  const int64_t slice_bytes = (int64_t)BK * nb * ES;
   auto issue = [&](int g) {
     if (g < total) {
-      const int pi = g / nsl, s = g - pi * nsl;
-      const PairDesc pd = pairs[it.pbeg + pi];
-      const uint8_t* Ag = ws + pd.a_off + ((int64_t)s * BK * nb + it.m0) * ES;
-      const uint8_t* Bg = ws + pd.b_off + ((int64_t)s * BK * nb + it.n0) * ES;
-      const uint32_t stg = sbase + (uint32_t)((g % ST) * STAGE);
+      if (is == 0) {
+        const PairDesc pd = pairs[it.pbeg + ip];
+        Ag = ws + pd.a_off + (int64_t)it.m0 * ES;
+        Bg = ws + pd.b_off + (int64_t)it.n0 * ES;
+      }
+      const uint32_t stg = sbase + (uint32_t)(istage * STAGE);
 #pragma unroll
       for (int u = 0; u < CPT; ++u) {
         const int c = tid + u * 256;
@@ -273,6 +278,10 @@ k_mn(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
           cp_async16(stg + (BK * 128 + k * BN) * ES + ch * 16, Bg + (int64_t)k * nb * ES + ch * 16);
         }
       }
+      Ag += slice_bytes;
+      Bg += slice_bytes;
+      if (++is == nsl) { is = 0; ++ip; }
+      if (++istage == ST) istage = 0;
     }
     cp_async_commit();
   };
@@ -291,11 +300,13 @@ k_mn(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
       else acc[i][j] = 0.0;
     }
 
+  int cstage = 0, cslice = 0, cpair = 0;
   for (int g = 0; g < total; ++g) {
     cp_async_wait<ST - 2>();
     __syncthreads();
     issue(g + ST - 1);
-    const T* As = reinterpret_cast<const T*>(sm + (g % ST) * STAGE);
+    const T* As = reinterpret_cast<const T*>(sm + cstage * STAGE);
+    if (++cstage == ST) cstage = 0;
     const T* Bs = As + BK * 128;
 #pragma unroll
     for (int k = 0; k < BK; ++k) {
@@ -328,8 +339,9 @@ k_mn(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
           for (int j = 0; j < 4; ++j) acc[i][j] = __fma_rn(a[i], b[j], acc[i][j]);
       }
     }
-    const int pi = g / nsl;
-    if (g - pi * nsl == nsl - 1) {
+    if (++cslice == nsl) {
+      cslice = 0;
+      const int pi = cpair++;
       // ---- fold (O9): W = fma_W(RN_W(alpha 2^fexp), RN_W(P), W) ----
       const PairDesc pd = pairs[it.pbeg + pi];
       const double f64 = ldexp(alpha, pd.fexp);
@@ -378,13 +390,14 @@ k_mn(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
 // mma.sync.m16n8k16.row.col.f64 -- tcgen05 has no FP64 kind).
 // 128x64 sub-tile, 8 warps (4 x 2), warp tile 32x32 = 2 m16 x 4 n8 MMA tiles,
 // binary64 accumulation in registers; MN-major payloads, BK = 16 k-rows per
-// stage through a 4-stage cp.async ring into As[k][m] / Bs[k][n] rows padded by
-// 64 bytes so the fragment loads (4 k-rows x 8 consecutive m) are conflict-free.
+// stage through a 4-stage cp.async ring into As[k][m] / Bs[k][n] rows whose
+// pitch is 32 B mod 128 B, so the fragment loads (per half-warp: 4 k-rows x 4
+// consecutive m) fall in four distinct 32-byte bank groups.
 // The accumulation order inside a DMMA is the hardware's: the parity bound is
 // the all-FP64 1e-13 relative Frobenius.
 // ---------------------------------------------------------------------------
 constexpr int DMMA_ST = 4, DMMA_BN = 64, DMMA_BK = 16;
-constexpr int DMMA_AP = 128 + 8, DMMA_BP = DMMA_BN + 8;  // row pitches in doubles
+constexpr int DMMA_AP = 128 + 4, DMMA_BP = DMMA_BN + 4;  // row pitches in doubles (= 32 B mod 128 B)
 constexpr int dmma_smem_bytes() { return DMMA_ST * DMMA_BK * (DMMA_AP + DMMA_BP) * 8; }
 
 __device__ __forceinline__ void dmma16816(double (&c)[4], const double (&a)[8], const double (&b)[4]) {
