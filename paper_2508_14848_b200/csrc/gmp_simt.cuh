@@ -389,7 +389,7 @@ k_mn(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
 // Product-path FP64-class kernel on the FP64 tensor pipe (DMMA, legacy
 // mma.sync.m16n8k16.row.col.f64 -- tcgen05 has no FP64 kind).
 // 128x64 sub-tile, 8 warps (4 x 2), warp tile 32x32 = 2 m16 x 4 n8 MMA tiles,
-// binary64 accumulation in registers; MN-major payloads, BK = 16 k-rows per
+// binary64 accumulation in registers, 2 CTAs per SM; MN-major payloads, BK = 16 k-rows per
 // stage through a 4-stage cp.async ring into As[k][m] / Bs[k][n] rows whose
 // pitch is 32 B mod 128 B, so the fragment loads (per half-warp: 4 k-rows x 4
 // consecutive m) fall in four distinct 32-byte bank groups.
@@ -401,7 +401,7 @@ constexpr int DMMA_AP = 128 + 4, DMMA_BP = DMMA_BN + 4;  // row pitches in doubl
 constexpr int dmma_smem_bytes() { return DMMA_ST * DMMA_BK * (DMMA_AP + DMMA_BP) * 8; }
 
 __device__ __forceinline__ void dmma16816(double (&c)[4], const double (&a)[8], const double (&b)[4]) {
-  asm volatile(
+  asm(
       "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, "
       "{%12,%13,%14,%15}, {%0,%1,%2,%3};"
       : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
@@ -409,7 +409,7 @@ __device__ __forceinline__ void dmma16816(double (&c)[4], const double (&a)[8], 
         "d"(b[1]), "d"(b[2]), "d"(b[3]));
 }
 
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, 2)
 k_dmma(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
        const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha) {
   constexpr int BK = DMMA_BK, ST = DMMA_ST, AP = DMMA_AP, BP = DMMA_BP;
@@ -465,19 +465,19 @@ k_dmma(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
     issue(gi + ST - 1);
     const double* As = reinterpret_cast<const double*>(sm + (gi % ST) * STAGE);
     const double* Bs = As + BK * AP;
-    double a[2][8], b[4][4];
+    double a[2][8];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
       for (int r = 0; r < 8; ++r) a[i][r] = As[(t + 4 * (r >> 1)) * AP + wm + i * 16 + g + 8 * (r & 1)];
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < 4; ++j) {
+      double b[4];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) b[j][r] = Bs[(t + 4 * r) * BP + wn + j * 8 + g];
+      for (int r = 0; r < 4; ++r) b[r] = Bs[(t + 4 * r) * BP + wn + j * 8 + g];
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) dmma16816(acc[i][j], a[i], b[j]);
+      for (int i = 0; i < 2; ++i) dmma16816(acc[i][j], a[i], b);
+    }
     const int pi = gi / nsl;
     if (gi - pi * nsl == nsl - 1) {
       // ---- fold (O9) ----

@@ -33,7 +33,7 @@ def main():
     C = api.synth(w.M, w.N, w.nb, w.c) if w.beta != 0 else None
     torch.cuda.synchronize()
     mask = w.class_mask if a.mask is None else a.mask
-    desc = B.make_desc(w.M, w.N, w.K, w.nb, w.tol, w.alpha, w.beta, mask, a.flags)
+    desc = B.make_desc(w.M, w.N, w.K, w.nb, w.tol, w.alpha, w.beta, mask, a.flags | B.GMP_FLAG_TIMING)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
     ev[0].record()
     g = api.GemmMP(desc, A, Bm, C)
@@ -54,7 +54,10 @@ def main():
     print(json.dumps(dict(cfg=w.name, plan_ms=ev[0].elapsed_time(ev[1]), convert_ms=ev[1].elapsed_time(ev[2]),
                           first_exec_ms=ev[2].elapsed_time(ev[3]), exec_ms=times, tflops=w.flops / best / 1e9,
                           tiles_a=st["tiles_a"], tiles_b=st["tiles_b"], tiles_c=st["tiles_c"],
-                          pairs=st["pairs"], launches=st["launches_execute"], ws_gb=st["workspace_bytes"] / 1e9)))
+                          pairs=st["pairs"], launches=st["launches_execute"], ws_gb=st["workspace_bytes"] / 1e9,
+                          class_ms=[round(x, 3) for x in st["class_ms"]],
+                          class_tflops=[round(st["flops"][c] / (st["class_ms"][c] * 1e-3) / 1e12, 1) if st["class_ms"][c] else 0
+                                        for c in range(5)])))
 
 
 if __name__ == "__main__":
