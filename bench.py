@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--variant", default=None)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (cfg3+ on one GPU)")
+    ap.add_argument("--size", type=int, default=0, help="override M=N=K (keeps the config's recipe)")
     return ap.parse_args()
 
 
@@ -210,6 +212,47 @@ def run_reference(a, w, rank):
 REFERENCE_MIX = {1: [5, 52, 7, 0, 0], 2: [916, 2029, 1151, 0, 0]}
 
 
+def run_e2e(a, A, Bm, C, Cout, lr, lc, G, dev, stream, step, w):
+    """The same step through the public API from pinned HOST buffers: H2D copies of
+    A, B (C), plan/convert/execute, D2H of the result, all inside the timed region."""
+    import torch
+    import torch.distributed as dist
+    from paper_2508_14848_b200 import binding as B
+    hA = A.cpu().pin_memory()
+    hB = Bm.cpu().pin_memory()
+    hC = C.cpu().pin_memory() if C is not None else None
+    hOut = torch.empty(Cout.shape, dtype=torch.float64).pin_memory()
+    dA, dB = torch.empty_like(A), torch.empty_like(Bm)
+    dC = torch.empty_like(C) if C is not None else None
+    h2d = hA.numel() * 8 + hB.numel() * 8 + (hC.numel() * 8 if hC is not None else 0)
+    d2h = lr * lc * 8
+    e_times = []
+    for it in range(a.e2e_steps + 1):
+        if G > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        dA.copy_(hA, non_blocking=True)
+        dB.copy_(hB, non_blocking=True)
+        if dC is not None:
+            dC.copy_(hC, non_blocking=True)
+        pl = step(dA, dB, dC)
+        hOut.copy_(Cout, non_blocking=True)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        B.gemm_mp_destroy(pl)
+        if it > 0:
+            e_times.append(s0.elapsed_time(s1))
+    e2e_ms = statistics.mean(e_times)
+    if G > 1:
+        tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = tt.item()
+    return {"value": w.flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+
+
 # ---------------------------------------------------------------------------
 # the GPU arm
 # ---------------------------------------------------------------------------
@@ -219,6 +262,9 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     w = gmp_inputs.workload(a.config, a.variant)
+    if a.size:
+        import dataclasses
+        w = dataclasses.replace(w, M=a.size, N=a.size, K=a.size, name=w.name + f"_size{a.size}")
     if a.impl == "reference":
         run_reference(a, w, rank)
         return
@@ -342,37 +388,10 @@ def main():
     launches = st["launches_plan"] + st["launches_convert"] + st["launches_execute"]
 
     # ---- e2e: host (pinned) buffers, copies inside the timed region ----
-    hA = A.cpu().pin_memory()
-    hB = Bm.cpu().pin_memory()
-    hC = C.cpu().pin_memory() if C is not None else None
-    hOut = torch.empty(Cout.shape, dtype=torch.float64).pin_memory()
-    dA, dB = torch.empty_like(A), torch.empty_like(Bm)
-    dC = torch.empty_like(C) if C is not None else None
-    h2d = hA.numel() * 8 + hB.numel() * 8 + (hC.numel() * 8 if hC is not None else 0)
-    d2h = lr * lc * 8
-    e_times = []
-    for it in range(a.e2e_steps + 1):
-        if G > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s0.record(stream)
-        dA.copy_(hA, non_blocking=True)
-        dB.copy_(hB, non_blocking=True)
-        if dC is not None:
-            dC.copy_(hC, non_blocking=True)
-        pl = step(dA, dB, dC)
-        hOut.copy_(Cout, non_blocking=True)
-        s1.record(stream)
-        torch.cuda.synchronize()
-        B.gemm_mp_destroy(pl)
-        if it > 0:
-            e_times.append(s0.elapsed_time(s1))
-    e2e_ms = statistics.mean(e_times)
-    if G > 1:
-        tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = tt.item()
+    e2e = None
+    if not a.no_e2e:
+        e2e = run_e2e(a, A, Bm, C, Cout, lr, lc, G, dev, stream, step, w)
+
 
     if rank == 0:
         out = {
@@ -400,8 +419,7 @@ def main():
                          "frac": achieved / dom_peak if dom_peak else None, "traffic": None,
                          "peak_source": ("derived: 148 SMs x " + ("64 DFMA" if dom == 0 else "128 FFMA") +
                                          " lanes x 2 x 1965 MHz") if dom <= 1 else peak_src + " bf16 sustained"},
-            "e2e": {"value": w.flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "e2e": e2e,
             "gpu_launches": launches * a.steps,
             "gpu_launches_per_step": launches,
             "clocks": clk,

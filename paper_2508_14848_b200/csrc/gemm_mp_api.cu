@@ -265,7 +265,7 @@ static void build_tables(gmp_plan_s* pl) {
         if (!cnt) continue;
         n_pairs += cnt;
         const bool tc = kTcAvailable && (c >= 2) && !(d.flags & GMP_FLAG_SIMT_ONLY);
-        n_items += tc ? tc_items_per_tile(nb) : (nb / 128) * (nb / mn_bn(c));
+        n_items += 1;
       }
   const int64_t n_pack = (int64_t)pl->locA.size() + (int64_t)pl->locB.size() + (hasC ? nCl : 0);
   int64_t n_shadow_local = 0, n_shadow_recv = 0;
@@ -419,19 +419,15 @@ static void build_tables(gmp_plan_s* pl) {
         }
         const int64_t pcnt = (int64_t)pl->pairs.size() - pbeg;
         if (!pcnt) continue;
-        if (tc) {
-          tc_make_items(nb, (int32_t)k, (int32_t)pbeg, (int32_t)pcnt, its);
-        } else {
-          for (int64_t m0 = 0; m0 < nb; m0 += 128)
-            for (int64_t n0 = 0; n0 < nb; n0 += mn_bn(c))
-              its.push_back(WorkItem{(int32_t)k, (int32_t)m0, (int32_t)n0, (int32_t)pbeg, (int32_t)pcnt, 0});
-        }
+        its.push_back(WorkItem{(int32_t)k, 0, 0, (int32_t)pbeg, (int32_t)pcnt, 0});
       }
       if (its.empty()) continue;
       std::stable_sort(its.begin(), its.end(), [](const WorkItem& a, const WorkItem& b) { return a.pcnt > b.pcnt; });
       pl->items.insert(pl->items.end(), its.begin(), its.end());
       const int kind = tc ? 1 : (c == 0 && (d.flags & GMP_FLAG_SIMT_ONLY)) ? 2 : 0;
-      pl->launches.push_back(Launch{s, c, kind, ibeg, (int64_t)its.size()});
+      // flat launch size: items x sub-tiles of the class kernel's CTA tile
+      const int bn = tc ? tc_bn((int)nb) : mn_bn(c);
+      pl->launches.push_back(Launch{s, c, kind, ibeg, (int64_t)its.size() * subtiles_per_item((int)nb, bn)});
     }
   }
 

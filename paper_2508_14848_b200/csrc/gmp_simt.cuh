@@ -27,10 +27,24 @@ namespace gmp {
 
 struct WorkItem {
   int32_t ctile;       // index into the CTileDesc array
-  int32_t m0, n0;      // sub-tile origin inside the C tile
+  int32_t m0, n0;      // sub-tile origin inside the C tile (filled by expand_item)
   int32_t pbeg, pcnt;  // range in the PairDesc list
   int32_t pad;
 };
+
+// The host lists one WorkItem per (C tile, pair list); a launch covers
+// items x S sub-tiles (S = (nb/128) * (nb/bn)).  Flat index -> item + sub-tile,
+// consecutive flat indices walk the n-blocks of one 128-row band (A panel reuse).
+__device__ __forceinline__ WorkItem expand_item(const WorkItem* __restrict__ items, int64_t flat, int nb, int bn) {
+  const int nbn = nb / bn, S = (nb / 128) * nbn;
+  const int64_t idx = flat / S;
+  const int sub = (int)(flat - idx * S);
+  WorkItem w = items[idx];
+  w.m0 = (sub / nbn) * 128;
+  w.n0 = (sub - (sub / nbn) * nbn) * bn;
+  return w;
+}
+__host__ __device__ inline int64_t subtiles_per_item(int nb, int bn) { return (int64_t)(nb / 128) * (nb / bn); }
 
 struct PairDesc {
   int64_t a_off, b_off;  // byte offsets of the class-c payloads (A row-major, B K-major)
@@ -103,7 +117,7 @@ k_simt_class(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pa
   __shared__ __align__(16) T As[2][BK][BM + PAD];
   __shared__ __align__(16) T Bs[2][BK][BN + PAD];
 
-  const WorkItem it = items[blockIdx.x];
+  const WorkItem it = expand_item(items, blockIdx.x, nb, BN);
   const CTileDesc ct = ctiles[it.ctile];
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
@@ -248,7 +262,7 @@ k_mn(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
   constexpr int STAGE = BK * (128 + BN) * ES;            // bytes
   static_assert(CHUNKS % 256 == 0, "loader");
   extern __shared__ __align__(16) uint8_t sm[];
-  const WorkItem it = items[blockIdx.x];
+  const WorkItem it = expand_item(items, blockIdx.x, nb, BN);
   const CTileDesc ct = ctiles[it.ctile];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const int nsl = nb / BK;
@@ -417,7 +431,7 @@ k_dmma(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
   constexpr int CHUNKS = BK * (ACH + BCH), CPT = CHUNKS / 256;
   constexpr int STAGE = BK * (AP + BP) * 8;
   extern __shared__ __align__(128) uint8_t sm[];
-  const WorkItem it = items[blockIdx.x];
+  const WorkItem it = expand_item(items, blockIdx.x, nb, DMMA_BN);
   const CTileDesc ct = ctiles[it.ctile];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;

@@ -117,7 +117,7 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 template <int C, int BN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-           const WorkItem* __restrict__ items, int nitems, const PairDesc* __restrict__ pairs,
+           const WorkItem* __restrict__ items, int64_t nitems, const PairDesc* __restrict__ pairs,
            const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha) {
   constexpr int ESZ = (C == 4) ? 1 : 2;
   constexpr int BK = 128 / ESZ;            // elements per 128-byte K block
@@ -157,8 +157,8 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-        const WorkItem w = items[it];
+      for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const WorkItem w = expand_item(items, it, nb, BN);
         for (int pi = 0; pi < w.pcnt; ++pi) {
           const PairDesc pd = pairs[w.pbeg + pi];
           const int arow = pd.a_slot * nb + w.m0, brow = pd.b_slot * nb + w.n0;
@@ -177,8 +177,8 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
     if (lane == 0) {
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
-      for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-        const WorkItem w = items[it];
+      for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const WorkItem w = expand_item(items, it, nb, BN);
         for (int pi = 0; pi < w.pcnt; ++pi) {
           mbar_wait(&tempty[acc], acc_phase ^ 1);
           tc_fence_after();
@@ -209,8 +209,8 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
     const int rloc = quarter * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-      const WorkItem w = items[it];
+    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+      const WorkItem w = expand_item(items, it, nb, BN);
       const CTileDesc ct = ctiles[w.ctile];
       const int64_t rowoff = (int64_t)(w.m0 + rloc) * nb + w.n0 + half * HC;
       if (ct.code != 0) {
@@ -310,13 +310,6 @@ inline PFN_encodeTiled get_encode_tiled() {
   return fn;
 }
 
-inline int64_t tc_items_per_tile(int64_t nb) { return (nb / TC_BM) * (nb / tc_bn((int)nb)); }
-
-inline void tc_make_items(int64_t nb, int32_t ctile, int32_t pbeg, int32_t pcnt, std::vector<WorkItem>& its) {
-  const int bn = tc_bn((int)nb);
-  for (int64_t m0 = 0; m0 < nb; m0 += TC_BM)
-    for (int64_t n0 = 0; n0 < nb; n0 += bn) its.push_back(WorkItem{ctile, (int32_t)m0, (int32_t)n0, pbeg, pcnt, 0});
-}
 
 inline gmp_status_t tc_prepare(TcTables& t, uint8_t* ws, const int64_t* arena_off, const int64_t* arena_slots, int nb) {
   t.nb = nb;
@@ -360,7 +353,7 @@ inline gmp_status_t tc_launch_t(TcTables& t, const WorkItem* it, int64_t n, cons
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)std::min<int64_t>(n, sms);
-  k_tc_class<C, BN><<<grid, TC_THREADS, smem, s>>>(t.mapA[C], t.mapB[C], it, (int)n, pd, ct, ws, nb, alpha);
+  k_tc_class<C, BN><<<grid, TC_THREADS, smem, s>>>(t.mapA[C], t.mapB[C], it, n, pd, ct, ws, nb, alpha);
   return cudaGetLastError() == cudaSuccess ? GMP_OK : GMP_ERR_CUDA;
 }
 
