@@ -59,9 +59,13 @@ def load_peaks():
             "fallback (B200_PROFILING.md)"
 
 
-def class_peaks(peaks):
+def class_peaks(peaks, fp32_on_tensor=True):
+    """Peak of the hardware path each class runs on.  FP32 class: by default the
+    tensor pipe with nine BF16 MMAs per FP32 product (BF16 peak / 9); with
+    GMP_FLAG_FP32_FFMA the FP32 pipe (FFMA2)."""
     bf16 = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
-    return {0: ALU_PEAK_TFLOPS[0], 1: ALU_PEAK_TFLOPS[1], 2: bf16, 3: bf16, 4: 2 * bf16}
+    fp32 = bf16 / 9.0 if fp32_on_tensor else ALU_PEAK_TFLOPS[1]
+    return {0: ALU_PEAK_TFLOPS[0], 1: fp32, 2: bf16, 3: bf16, 4: 2 * bf16}
 
 
 # ---------------------------------------------------------------------------
@@ -414,11 +418,14 @@ def main():
             "mix": {"tiles_a": st["tiles_a"], "tiles_b": st["tiles_b"], "tiles_c": st["tiles_c"],
                     "pairs": st["pairs"]},
             "class_ms_rank0": class_ms,
-            "roofline": {"bound": "alu" if dom <= 1 else "tensor", "kernel": f"class {gmp_class_name(dom)} tile-GEMM",
+            "roofline": {"bound": "tensor", "kernel": f"class {gmp_class_name(dom)} tile-GEMM",
                          "achieved": achieved, "peak": dom_peak, "unit": "TFLOP/s",
                          "frac": achieved / dom_peak if dom_peak else None, "traffic": None,
-                         "peak_source": ("derived: 148 SMs x " + ("64 DFMA" if dom == 0 else "128 FFMA") +
-                                         " lanes x 2 x 1965 MHz") if dom <= 1 else peak_src + " bf16 sustained"},
+                         "peak_source": ("derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz (DMMA = DFMA nominal)"
+                                         if dom == 0 else
+                                         peak_src + " bf16 sustained / 9 (FP32 class = 9 BF16 MMAs per product)"
+                                         if dom == 1 else peak_src + " bf16 sustained" +
+                                         (" x 2 (E4M3)" if dom == 4 else ""))},
             "e2e": e2e,
             "gpu_launches": launches * a.steps,
             "gpu_launches_per_step": launches,

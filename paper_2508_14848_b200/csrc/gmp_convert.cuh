@@ -200,6 +200,51 @@ __global__ void __launch_bounds__(256) k_shadow_t(const ShadowJob* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------
+// FP32 class on the tensor pipe: exact 3-way BF16 split of an FP32 payload
+// (MN-major) into three K-major BF16 parts, x = x0 + x1 + x2 with
+// x0 = RN_bf16(x), x1 = RN_bf16(x - x0), x2 = x - x0 - x1 (both differences
+// are exact in binary32, x2 has at most 8 significant bits).  Receiver-side:
+// made from the stored (or shadow) FP32 payload.  64x64 blocks, transposed.
+// ---------------------------------------------------------------------------
+struct SplitJob {
+  int64_t src_off;   // FP32 payload (MN-major)
+  int64_t dst_off;   // 3 consecutive nb x nb BF16 parts (K-major)
+};
+
+__global__ void __launch_bounds__(256) k_split(const SplitJob* __restrict__ jobs, uint8_t* ws, int nb) {
+  __shared__ float sm[64][65];
+  const SplitJob j = jobs[blockIdx.y];
+  const int per = nb / 64;
+  const int r0 = (blockIdx.x / per) * 64, c0 = (blockIdx.x % per) * 64;
+  const float* src = reinterpret_cast<const float*>(ws + j.src_off);
+  uint16_t* dst = reinterpret_cast<uint16_t*>(ws + j.dst_off);
+  const int64_t part = (int64_t)nb * nb;
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int unit = t + u * 256;
+    const int r = unit >> 6, c = unit & 63;
+    sm[r][c] = src[(int64_t)(r0 + r) * nb + c0 + c];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int unit = t + u * 256;
+    const int oc = unit >> 6, orr = unit & 63;   // output row oc (= source col), element orr
+    const float x = sm[orr][oc];
+    const uint16_t h0 = cvt_bf16_rn((double)x);
+    const float r1 = __fsub_rn(x, bf16_to_f32(h0));
+    const uint16_t h1 = cvt_bf16_rn((double)r1);
+    const float r2 = __fsub_rn(r1, bf16_to_f32(h1));
+    const uint16_t h2 = cvt_bf16_rn((double)r2);
+    const int64_t o = (int64_t)(c0 + oc) * nb + r0 + orr;
+    dst[o] = h0;
+    dst[part + o] = h1;
+    dst[2 * part + o] = h2;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // accumulator init (O9):  W = beta == 0 ? 0 : RN_W(RN_W(beta) decode(C_in))
 // ---------------------------------------------------------------------------
 struct CTileDesc {

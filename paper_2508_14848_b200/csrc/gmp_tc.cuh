@@ -114,29 +114,39 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
+// C = 2, 3, 4: FP16 / BF16 / E4M3 classes, NP = 1 operand part.
+// C = 5: the FP32 class on the tensor pipe ("BF16x9"): each FP32 operand tile is
+// split exactly into three BF16 parts x = x0 + x1 + x2 (k_split, receiver-side
+// from the stored FP32 payload), NP = 3, and all nine part products -- each
+// exact in the FP32 accumulator's inputs -- are accumulated per K block,
+// smallest terms first; binary32 inputs, exact products, binary32 accumulation.
+template <int C> constexpr int tc_np() { return C == 5 ? 3 : 1; }
+template <int C> constexpr int tc_stages() { return C == 5 ? 2 : TC_STAGES; }
+
 template <int C, int BN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const WorkItem* __restrict__ items, int64_t nitems, const PairDesc* __restrict__ pairs,
            const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha) {
+  constexpr int NP = tc_np<C>(), ST = tc_stages<C>();
   constexpr int ESZ = (C == 4) ? 1 : 2;
   constexpr int BK = 128 / ESZ;            // elements per 128-byte K block
   constexpr int NMMA = 4;                  // 32-byte K per tcgen05.mma
-  constexpr int A_BYTES = TC_BM * 128, B_BYTES = BN * 128, STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr int A_BYTES = TC_BM * 128, B_BYTES = BN * 128, STAGE_BYTES = NP * (A_BYTES + B_BYTES);
   constexpr uint32_t TMEM_COLS = 2 * BN;
-  constexpr uint32_t IDESC = tc_idesc<C, BN>();
+  constexpr uint32_t IDESC = tc_idesc<(C == 5 ? 3 : C), BN>();
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TC_STAGES * STAGE_BYTES);
-  uint64_t* empty = full + TC_STAGES;
-  uint64_t* tfull = empty + TC_STAGES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * STAGE_BYTES);
+  uint64_t* empty = full + ST;
+  uint64_t* tfull = empty + ST;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < TC_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < ST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], TC_EPI_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
@@ -161,14 +171,17 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
         const WorkItem w = expand_item(items, it, nb, BN);
         for (int pi = 0; pi < w.pcnt; ++pi) {
           const PairDesc pd = pairs[w.pbeg + pi];
-          const int arow = pd.a_slot * nb + w.m0, brow = pd.b_slot * nb + w.n0;
           for (int kb = 0; kb < kblocks; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* sa = smem + stage * STAGE_BYTES;
             mbar_expect_tx(&full[stage], STAGE_BYTES);
-            tma_load_2d(sa, &tmA, kb * BK, arow, &full[stage]);
-            tma_load_2d(sa + A_BYTES, &tmB, kb * BK, brow, &full[stage]);
-            if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+              tma_load_2d(sa + p * A_BYTES, &tmA, kb * BK, (pd.a_slot * NP + p) * nb + w.m0, &full[stage]);
+              tma_load_2d(sa + NP * A_BYTES + p * B_BYTES, &tmB, kb * BK, (pd.b_slot * NP + p) * nb + w.n0,
+                          &full[stage]);
+            }
+            if (++stage == ST) { stage = 0; phase ^= 1; }
           }
         }
       }
@@ -187,12 +200,19 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
             mbar_wait(&full[stage], phase);
             tc_fence_after();
             const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
-            const uint64_t ad = sdesc_k_sw128(sa), bd = sdesc_k_sw128(sa + A_BYTES);
 #pragma unroll
-            for (int k = 0; k < NMMA; ++k)
-              tc_mma<C>(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), IDESC, (kb | k) != 0);
+            for (int t = 0; t < NP * NP; ++t) {
+              // terms (i, j) by decreasing i + j: the smallest part products first
+              constexpr int TI[9] = {2, 2, 1, 2, 1, 0, 1, 0, 0}, TJ[9] = {2, 1, 2, 0, 1, 2, 0, 1, 0};
+              const int ti = (NP == 1) ? 0 : TI[t], tj = (NP == 1) ? 0 : TJ[t];
+              const uint64_t ad = sdesc_k_sw128(sa + ti * A_BYTES);
+              const uint64_t bd = sdesc_k_sw128(sa + NP * A_BYTES + tj * B_BYTES);
+#pragma unroll
+              for (int k = 0; k < NMMA; ++k)
+                tc_mma<C>(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), IDESC, (kb | t | k) != 0);
+            }
             tc_commit(&empty[stage]);
-            if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+            if (++stage == ST) { stage = 0; phase ^= 1; }
           }
           tc_commit(&tfull[acc]);
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
@@ -282,15 +302,15 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
 
 template <int C, int BN>
 constexpr int tc_smem_bytes() {
-  return TC_STAGES * (TC_BM * 128 + BN * 128) + 1024 /*align*/ + 256 /*barriers*/;
+  return tc_stages<C>() * tc_np<C>() * (TC_BM * 128 + BN * 128) + 1024 /*align*/ + 256 /*barriers*/;
 }
 
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 struct TcTables {
-  CUtensorMap mapA[5], mapB[5];
-  bool ready[5] = {false, false, false, false, false};
+  CUtensorMap mapA[6], mapB[6];   // classes 2..4 and 5 = FP32 split (BF16 parts)
+  bool ready[6] = {false, false, false, false, false, false};
   int nb = 0;
 };
 
@@ -311,20 +331,23 @@ inline PFN_encodeTiled get_encode_tiled() {
 }
 
 
+// arena_off / arena_slots have 6 entries; arena 5 holds FP32 splits (3 BF16 parts per slot)
 inline gmp_status_t tc_prepare(TcTables& t, uint8_t* ws, const int64_t* arena_off, const int64_t* arena_slots, int nb) {
   t.nb = nb;
-  for (int c = 2; c <= 4; ++c) {
+  for (int c = 2; c <= 5; ++c) {
     t.ready[c] = false;
     if (arena_slots[c] == 0) continue;
     PFN_encodeTiled enc = get_encode_tiled();
     if (!enc) return GMP_ERR_CUDA;
-    const int esz = class_bytes(c);
-    cuuint64_t dims[2] = {(cuuint64_t)nb, (cuuint64_t)(arena_slots[c] * nb)};
+    const int esz = (c == 4) ? 1 : 2;
+    const int64_t rows = arena_slots[c] * (c == 5 ? 3 : 1) * nb;
+    cuuint64_t dims[2] = {(cuuint64_t)nb, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)nb * esz};
     cuuint32_t estr[2] = {1, 1};
     const CUtensorMapDataType dt = (c == 4) ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16;
+    const int bn = (c == 5) ? 128 : tc_bn(nb);
     cuuint32_t boxA[2] = {(cuuint32_t)(128 / esz), (cuuint32_t)TC_BM};
-    cuuint32_t boxB[2] = {(cuuint32_t)(128 / esz), (cuuint32_t)tc_bn(nb)};
+    cuuint32_t boxB[2] = {(cuuint32_t)(128 / esz), (cuuint32_t)bn};
     void* base = ws + arena_off[c];
     if (enc(&t.mapA[c], dt, 2, base, dims, strides, boxA, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -357,14 +380,16 @@ inline gmp_status_t tc_launch_t(TcTables& t, const WorkItem* it, int64_t n, cons
   return cudaGetLastError() == cudaSuccess ? GMP_OK : GMP_ERR_CUDA;
 }
 
+// cls: 2..4 for the 16/8-bit classes, 5 for the FP32 class on the tensor pipe
 inline gmp_status_t tc_launch(TcTables& t, int cls, const WorkItem* it, int64_t n, const PairDesc* pd,
                               const CTileDesc* ct, uint8_t* ws, int nb, double alpha, cudaStream_t s) {
-  if (cls < 2 || cls > 4 || !t.ready[cls]) return GMP_ERR_STATE;
+  if (cls < 2 || cls > 5 || !t.ready[cls]) return GMP_ERR_STATE;
   const bool wide = tc_bn(nb) == 256;
   switch (cls) {
     case 2: return wide ? tc_launch_t<2, 256>(t, it, n, pd, ct, ws, nb, alpha, s) : tc_launch_t<2, 128>(t, it, n, pd, ct, ws, nb, alpha, s);
     case 3: return wide ? tc_launch_t<3, 256>(t, it, n, pd, ct, ws, nb, alpha, s) : tc_launch_t<3, 128>(t, it, n, pd, ct, ws, nb, alpha, s);
-    default: return wide ? tc_launch_t<4, 256>(t, it, n, pd, ct, ws, nb, alpha, s) : tc_launch_t<4, 128>(t, it, n, pd, ct, ws, nb, alpha, s);
+    case 4: return wide ? tc_launch_t<4, 256>(t, it, n, pd, ct, ws, nb, alpha, s) : tc_launch_t<4, 128>(t, it, n, pd, ct, ws, nb, alpha, s);
+    default: return tc_launch_t<5, 128>(t, it, n, pd, ct, ws, nb, alpha, s);
   }
 }
 

@@ -62,10 +62,46 @@ def test_explicit_maps_match_oracle():
     rng = np.random.default_rng(0)
     maps = tuple(rng.integers(0, 2, (4, 4)).astype(np.uint8) for _ in range(3))
     o = run_oracle(A, Bm, C, 128, 1e-6, 1.0, 1.0, 0b00011, maps=maps)
-    g, (out,) = run_gpu(A, Bm, C, 128, 1e-6, 1.0, 1.0, 0b00011, maps=maps)
+    # FP32 class on the FP32 pipe (FFMA2): bitwise the oracle (FP64 class on DMMA: 1e-13)
+    g, (out,) = run_gpu(A, Bm, C, 128, 1e-6, 1.0, 1.0, 0b00011, flags=B.GMP_FLAG_FP32_FFMA, maps=maps)
     m = g.maps()
     assert np.array_equal(m["acode"], maps[0]) and np.array_equal(m["ccode"], maps[2])
-    assert np.array_equal(out, o["C"])  # FP64/FP32 classes run on sequential-k kernels: bitwise
+    assert np.linalg.norm(out - o["C"]) / np.linalg.norm(o["C"]) <= 1e-13
+    g2, (out2,) = run_gpu(A, Bm, C, 128, 1e-6, 1.0, 1.0, 0b00011, flags=B.GMP_FLAG_SIMT_ONLY, maps=maps)
+    assert np.array_equal(out2, o["C"])  # FP64 DFMA + FP32 FFMA2: bitwise
+    # default: FP32 class on the tensor pipe (exact BF16x3 split, FP32 accumulation)
+    g3, (out3,) = run_gpu(A, Bm, C, 128, 1e-6, 1.0, 1.0, 0b00011, maps=maps)
+    assert np.linalg.norm(out3 - o["C"]) / np.linalg.norm(o["C"]) <= 4 * 2.0 ** -24 * np.sqrt(512)
+
+
+def test_fp32_split_parts_are_exact():
+    """The tensor-pipe FP32 class consumes x = x0 + x1 + x2 (three BF16 parts,
+    K-major): the parts must reproduce every FP32 operand value exactly."""
+    w = gmp_inputs.small_workload(512, 512, 512, 128, 1e-5, mode="random", E=10, beta=0.0, seed=21)
+    A, Bm, C = w.matrices()
+    g, _ = run_gpu(A, Bm, None, 128, w.tol, 1.0, 0.0, w.class_mask)
+    o = run_oracle(A, Bm, None, 128, w.tol, 1.0, 0.0, w.class_mask)
+    nb = 128
+    checked = 0
+    for which, X, codes, s5 in [("A", A, o["acode"], o["ascale5"]), ("B", Bm, o["bcode"], o["bscale5"])]:
+        for ti in range(codes.shape[0]):
+            for tj in range(codes.shape[1]):
+                try:
+                    parts, sc = g.tile(which, ti, tj, 5)
+                except B.GmpError:
+                    continue
+                code = int(codes[ti, tj])
+                tile = X[ti * nb:(ti + 1) * nb, tj * nb:(tj + 1) * nb]
+                stored = oracle.pack_tile(tile, code, int(s5[ti, tj, code]), role=which)
+                f32 = stored if code == 1 else oracle.shadow_tile(stored, nb, code, int(s5[ti, tj, code]), 1, role=which)[0]
+                v = oracle.payload_values(f32, 1).reshape(nb, nb)     # MN-major payload
+                want = v.T                                            # K-major view
+                pv = [oracle.decode(parts.view(np.uint16)[k * nb * nb:(k + 1) * nb * nb].astype(np.uint32), 3)
+                      .reshape(nb, nb) for k in range(3)]
+                assert np.array_equal(pv[0] + pv[1] + pv[2], want)
+                assert np.all(np.abs(pv[1]) <= np.abs(pv[0]) * 2.0 ** -8 + 1e-300)
+                checked += 1
+    assert checked > 0
 
 
 def test_rectangular_many_tiles_sampled_vs_oracle():
