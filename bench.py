@@ -393,7 +393,7 @@ def main():
 
     # ---- e2e: host (pinned) buffers, copies inside the timed region ----
     e2e = None
-    if not a.no_e2e:
+    if not a.no_e2e and a.e2e_steps > 0:
         e2e = run_e2e(a, A, Bm, C, Cout, lr, lc, G, dev, stream, step, w)
 
 
