@@ -59,13 +59,16 @@ def load_peaks():
             "fallback (B200_PROFILING.md)"
 
 
-def class_peaks(peaks, fp32_on_tensor=True):
-    """Peak of the hardware path each class runs on.  FP32 class: by default the
-    tensor pipe with nine BF16 MMAs per FP32 product (BF16 peak / 9); with
+def class_peaks(peaks, fp32_on_tensor=True, fp64_on_int8=False):
+    """Peak of the hardware path each class runs on.
+    FP64 class: DMMA on the FP64 pipe (148 SMs x 64 FMA/clk x 2 x 1965 MHz); with
+    the experimental GMP_FLAG_FP64_INT8 the INT8 tensor pipe (2 x BF16 / 28).
+    FP32 class: by default nine BF16 MMAs per product (BF16 / 9); with
     GMP_FLAG_FP32_FFMA the FP32 pipe (FFMA2)."""
     bf16 = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    fp64 = 2 * bf16 / 28.0 if fp64_on_int8 else ALU_PEAK_TFLOPS[0]
     fp32 = bf16 / 9.0 if fp32_on_tensor else ALU_PEAK_TFLOPS[1]
-    return {0: ALU_PEAK_TFLOPS[0], 1: fp32, 2: bf16, 3: bf16, 4: 2 * bf16}
+    return {0: fp64, 1: fp32, 2: bf16, 3: bf16, 4: 2 * bf16}
 
 
 # ---------------------------------------------------------------------------

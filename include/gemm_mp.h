@@ -64,6 +64,8 @@ typedef enum {
 /* flags */
 #define GMP_FLAG_SIMT_ONLY 1u /* run classes 2..4 on the SIMT (binary32 FMA) kernel: cross-check only */
 #define GMP_FLAG_TIMING 2u    /* record CUDA events around each class launch of execute (stats.class_ms) */
+#define GMP_FLAG_FP64_INT8 8u /* experimental: FP64 class on the INT8 tensor pipe (7 exact int8 digits
+                                 per element, 28 tcgen05 kind::i8 MMAs) instead of DMMA (default)    */
 #define GMP_FLAG_FP32_FFMA 4u /* FP32 class on the FP32 pipe (packed FFMA2, bitwise O8) instead of the
                                  default tensor-pipe path (exact BF16x3 split, nine BF16 MMAs per block) */
 
@@ -145,7 +147,8 @@ gmp_status_t gemm_mp_get_maps(gmp_plan_t plan, uint8_t *a, uint8_t *b, uint8_t *
 
 /* Copies one LOCAL tile's payload to host memory: which = 'A' or 'B' (class
  * `cls` = the stored code or a materialised shadow class; cls = 5: the three
- * K-major BF16 parts of the FP32 class's tensor-pipe split), 'C' (packed C_out of
+ * K-major BF16 parts of the FP32 class's tensor-pipe split; cls = 6: the seven
+ * int8 digit planes of the FP64 class's INT8 path), 'C' (packed C_out of
  * the last execute, cls = code), 'I' (packed C_in), 'W' (accumulator, binary64
  * or binary32).  (ti, tj) are GLOBAL tile indices.  *bytes in: capacity, out:
  * bytes written; *scale receives the tile's power-of-two scale.  Synchronous. */

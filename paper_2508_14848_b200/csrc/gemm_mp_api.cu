@@ -21,6 +21,7 @@
 #include "gmp_map.cuh"
 #include "gmp_simt.cuh"
 #include "gmp_tc.cuh"
+#include "gmp_ozaki.cuh"
 
 using namespace gmp;
 
@@ -67,7 +68,8 @@ static inline int16_t layout_transposed(int role, int cls) {
 // plan
 // ---------------------------------------------------------------------------
 struct Launch {
-  int step, cls, kind;  // kind 0: SIMT/DMMA kernel, 1: tcgen05, 2: FP64 DFMA cross-check, 3: FP32 on tcgen05 (BF16x9)
+  int step, cls, kind;  // kind 0: SIMT/DMMA kernel, 1: tcgen05, 2: FP64 DFMA cross-check, 3: FP32 on tcgen05
+                        // (BF16x9), 4: FP64 on the INT8 tensor pipe (Ozaki digits)
   int64_t ibeg, icount;
 };
 
@@ -95,10 +97,17 @@ struct gmp_plan_s {
   std::vector<int64_t> locA, locB, locC;
   // slots: [global tile][class] -> slot in that class's arena, -1 if absent
   std::vector<int32_t> slotA5, slotB5;
-  int64_t arena_off[6] = {0}, arena_slots[6] = {0};   // 0..4 classes, 5 = FP32 BF16x3 splits
-  int64_t slot_bytes[6] = {0};
+  int64_t arena_off[7] = {0}, arena_slots[7] = {0};   // 0..4 classes, 5 = FP32 BF16x3 splits,
+  int64_t slot_bytes[7] = {0};                          // 6 = FP64 int8 digit planes (Ozaki)
   std::vector<int32_t> splitA, splitB;                  // [global tile] -> split slot, -1 if absent
+  std::vector<int32_t> sliceA, sliceB;                  // [global tile] -> digit slot, -1 if absent
   bool fp32_tc = false;                                 // FP32 class on the tensor pipe (default)
+  bool fp64_tc = false;                                 // FP64 class on the INT8 tensor pipe (opt-in)
+  std::vector<SliceJob> slice_local;
+  std::vector<std::vector<SliceJob>> slice_step;
+  std::vector<int64_t> slice_step_off;
+  int64_t off_slice = 0, off_oexp = 0;
+  OzTables oz;
   std::vector<SplitJob> split_local;
   std::vector<std::vector<SplitJob>> split_step;
   std::vector<int64_t> split_step_off;
@@ -202,10 +211,12 @@ static void build_tables(gmp_plan_s* pl) {
   const bool hasC = d.beta != 0.0;
   for (int c = 0; c < 5; ++c) pl->slot_bytes[c] = nb2 * class_bytes(c);
   pl->slot_bytes[5] = 3 * nb2 * 2;
+  pl->slot_bytes[6] = OZ_NS * nb2;
   pl->fp32_tc = kTcAvailable && !(d.flags & (GMP_FLAG_SIMT_ONLY | GMP_FLAG_FP32_FFMA));
+  pl->fp64_tc = kTcAvailable && (d.flags & GMP_FLAG_FP64_INT8) && !(d.flags & GMP_FLAG_SIMT_ONLY);
 
   // ---- which A/B tiles (and classes) this rank needs ----
-  std::vector<uint8_t> needSA(pl->nA, 0), needSB(pl->nB, 0);
+  std::vector<uint8_t> needSA(pl->nA, 0), needSB(pl->nB, 0), needOA(pl->nA, 0), needOB(pl->nB, 0);
   std::vector<uint8_t> needA(pl->nA * 5, 0), needB(pl->nB * 5, 0);
   int64_t pairs_cls[5] = {0}, pairs_loc[5] = {0};
   for (int64_t i = 0; i < mt; ++i)
@@ -220,6 +231,7 @@ static void build_tables(gmp_plan_s* pl) {
         needB[(l * nt + j) * 5 + cb] = 1;
         needB[(l * nt + j) * 5 + c] = 1;
         if (c == 1 && pl->fp32_tc) { needSA[i * kt + l] = 1; needSB[l * nt + j] = 1; }
+        if (c == 0 && pl->fp64_tc) { needOA[i * kt + l] = 1; needOB[l * nt + j] = 1; }
       }
   // every A tile of this process row and B tile of this process column keeps a
   // stored-precision slot: local tiles are broadcast roots, the others are
@@ -244,6 +256,11 @@ static void build_tables(gmp_plan_s* pl) {
   pl->splitB.assign(pl->nB, -1);
   for (int64_t g = 0; g < pl->nA; ++g) if (needSA[g]) pl->splitA[g] = (int32_t)nsplit++;
   for (int64_t g = 0; g < pl->nB; ++g) if (needSB[g]) pl->splitB[g] = (int32_t)nsplit++;
+  int64_t nslice = 0;
+  pl->sliceA.assign(pl->nA, -1);
+  pl->sliceB.assign(pl->nB, -1);
+  for (int64_t g = 0; g < pl->nA; ++g) if (needOA[g]) pl->sliceA[g] = (int32_t)nslice++;
+  for (int64_t g = 0; g < pl->nB; ++g) if (needOB[g]) pl->sliceB[g] = (int32_t)nslice++;
 
   // ---- local C tiles ----
   const int64_t nCl = (int64_t)pl->locC.size();
@@ -293,6 +310,8 @@ static void build_tables(gmp_plan_s* pl) {
 
   pl->off_pack = o; o = align_up(o + n_pack * (int64_t)sizeof(PackJob), 1024);
   pl->off_split = o; o = align_up(o + nsplit * (int64_t)sizeof(SplitJob), 1024);
+  pl->off_slice = o; o = align_up(o + nslice * (int64_t)sizeof(SliceJob), 1024);
+  pl->off_oexp = o; o = align_up(o + nslice * nb * 2, 1024);
   pl->off_shadow = o; o = align_up(o + (n_shadow_local + n_shadow_recv) * (int64_t)sizeof(ShadowJob), 1024);
   pl->off_ctd = o; o = align_up(o + nCl * (int64_t)sizeof(CTileDesc), 1024);
   pl->off_items = o; o = align_up(o + n_items * (int64_t)sizeof(WorkItem), 1024);
@@ -308,6 +327,9 @@ static void build_tables(gmp_plan_s* pl) {
   pl->arena_off[5] = o;
   pl->arena_slots[5] = nsplit;
   o = align_up(o + nsplit * pl->slot_bytes[5], 1024);
+  pl->arena_off[6] = o;
+  pl->arena_slots[6] = nslice;
+  o = align_up(o + nslice * pl->slot_bytes[6], 1024);
   for (int64_t k = 0; k < nCl; ++k) {
     const int64_t g = pl->locC[k];
     CTileDesc& t = pl->ctd[k];
@@ -401,6 +423,26 @@ static void build_tables(gmp_plan_s* pl) {
   };
   for (int64_t g = 0; g < pl->nA; ++g) add_split(false, g);
   for (int64_t g = 0; g < pl->nB; ++g) add_split(true, g);
+  // ---- FP64-class digit planes (receiver-side, from the stored binary64 payload) ----
+  pl->slice_local.clear();
+  pl->slice_step.assign(steps, {});
+  auto add_slice = [&](bool isB, int64_t g) {
+    const int32_t sl = (isB ? pl->sliceB : pl->sliceA)[g];
+    if (sl < 0) return;
+    const int32_t src = (isB ? pl->slotB5 : pl->slotA5)[g * 5 + 0];
+    SliceJob sj{arena(0, src), pl->arena_off[6] + (int64_t)sl * pl->slot_bytes[6], pl->off_oexp + (int64_t)sl * nb * 2};
+    const bool local = isB ? ((g / nt) % P == p) : ((g % kt) % Q == q);
+    const int64_t l = isB ? g / nt : g % kt;
+    if (local) pl->slice_local.push_back(sj);
+    else pl->slice_step[l / GMP_STEP_DEPTH].push_back(sj);
+  };
+  for (int64_t g = 0; g < pl->nA; ++g) add_slice(false, g);
+  for (int64_t g = 0; g < pl->nB; ++g) add_slice(true, g);
+  pl->slice_step_off.assign(steps, 0);
+  {
+    int64_t acc = (int64_t)pl->slice_local.size();
+    for (int s = 0; s < steps; ++s) { pl->slice_step_off[s] = acc; acc += (int64_t)pl->slice_step[s].size(); }
+  }
   pl->split_step_off.assign(steps, 0);
   {
     int64_t acc = (int64_t)pl->split_local.size();
@@ -454,6 +496,12 @@ static void build_tables(gmp_plan_s* pl) {
           pd.l = (int32_t)l;
           pd.a_slot = pl->slotA5[(i * kt + l) * 5 + c];
           pd.b_slot = pl->slotB5[(l * nt + j) * 5 + c];
+          if (c == 0 && pl->fp64_tc) {   // operands are the int8 digit planes
+            pd.a_slot = pl->sliceA[i * kt + l];
+            pd.b_slot = pl->sliceB[l * nt + j];
+            pd.a_off = pl->arena_off[6] + (int64_t)pd.a_slot * pl->slot_bytes[6];
+            pd.b_off = pl->arena_off[6] + (int64_t)pd.b_slot * pl->slot_bytes[6];
+          }
           if (c == 1 && pl->fp32_tc) {   // operands are the BF16x3 splits
             pd.a_slot = pl->splitA[i * kt + l];
             pd.b_slot = pl->splitB[l * nt + j];
@@ -469,10 +517,10 @@ static void build_tables(gmp_plan_s* pl) {
       if (its.empty()) continue;
       std::stable_sort(its.begin(), its.end(), [](const WorkItem& a, const WorkItem& b) { return a.pcnt > b.pcnt; });
       pl->items.insert(pl->items.end(), its.begin(), its.end());
-      const bool split = (c == 1 && pl->fp32_tc);
-      const int kind = split ? 3 : tc ? 1 : (c == 0 && (d.flags & GMP_FLAG_SIMT_ONLY)) ? 2 : 0;
+      const bool split = (c == 1 && pl->fp32_tc), ozaki = (c == 0 && pl->fp64_tc);
+      const int kind = ozaki ? 4 : split ? 3 : tc ? 1 : (c == 0 && (d.flags & GMP_FLAG_SIMT_ONLY)) ? 2 : 0;
       // flat launch size: items x sub-tiles of the class kernel's CTA tile
-      const int bn = split ? 128 : tc ? tc_bn((int)nb) : mn_bn(c);
+      const int bn = ozaki ? OZ_BN : split ? 128 : tc ? tc_bn((int)nb) : mn_bn(c);
       pl->launches.push_back(Launch{s, c, kind, ibeg, (int64_t)its.size() * subtiles_per_item((int)nb, bn)});
     }
   }
@@ -501,10 +549,12 @@ static void build_tables(gmp_plan_s* pl) {
     for (const auto& j : v) t += j.transpose;
     return (t > 0 ? 1 : 0) + ((int64_t)v.size() - t > 0 ? 1 : 0);
   };
-  for (int s = 0; s < steps; ++s) nl += nsh(pl->shadow_step[s]) + (pl->split_step[s].empty() ? 0 : 1);
+  for (int s = 0; s < steps; ++s)
+    nl += nsh(pl->shadow_step[s]) + (pl->split_step[s].empty() ? 0 : 1) + (pl->slice_step[s].empty() ? 0 : 1);
   st.launches_execute = nl;
   st.launches_plan = 2;
-  st.launches_convert = (pl->pack.empty() ? 0 : 1) + nsh(pl->shadow_local) + (pl->split_local.empty() ? 0 : 1);
+  st.launches_convert = (pl->pack.empty() ? 0 : 1) + nsh(pl->shadow_local) + (pl->split_local.empty() ? 0 : 1) +
+                        (pl->slice_local.empty() ? 0 : 1);
   for (const Launch& L : pl->launches) st.class_launches[L.cls]++;
 }
 
@@ -760,7 +810,12 @@ extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_byte
     std::vector<SplitJob> allsp = pl->split_local;
     for (auto& v : pl->split_step) allsp.insert(allsp.end(), v.begin(), v.end());
     GMP_TRY(up(pl->off_split, allsp.data(), allsp.size() * sizeof(SplitJob)));
+    std::vector<SliceJob> allsl = pl->slice_local;
+    for (auto& v : pl->slice_step) allsl.insert(allsl.end(), v.begin(), v.end());
+    GMP_TRY(up(pl->off_slice, allsl.data(), allsl.size() * sizeof(SliceJob)));
   }
+  if (oz_prepare(pl->oz, ws, pl->arena_off[6], pl->arena_slots[6], (int)nb) != GMP_OK)
+    return fail(GMP_ERR_CUDA, "cuTensorMapEncodeTiled (digit arena) failed");
   GMP_TRY(tc_prepare(pl->tc, ws, pl->arena_off, pl->arena_slots, (int)nb));
   // S3 pack
   if (!pl->pack.empty()) {
@@ -773,6 +828,11 @@ extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_byte
   if (!pl->split_local.empty()) {
     k_split<<<dim3((unsigned)((nb / 64) * (nb / 64)), (unsigned)pl->split_local.size()), 256, 0, stream>>>(
         (const SplitJob*)(ws + pl->off_split), ws, (int)nb);
+    GMP_CUDA(cudaGetLastError());
+  }
+  if (!pl->slice_local.empty()) {
+    k_slice64<<<dim3((unsigned)(nb / 64), (unsigned)pl->slice_local.size()), 256, 0, stream>>>(
+        (const SliceJob*)(ws + pl->off_slice), ws, (int)nb);
     GMP_CUDA(cudaGetLastError());
   }
   pl->converted = true;
@@ -820,6 +880,11 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
                   pl->comm_stream>>>((const SplitJob*)(ws + pl->off_split) + pl->split_step_off[s], ws, (int)nb);
         GMP_CUDA(cudaGetLastError());
       }
+      if (!pl->slice_step[s].empty()) {
+        k_slice64<<<dim3((unsigned)(nb / 64), (unsigned)pl->slice_step[s].size()), 256, 0, pl->comm_stream>>>(
+            (const SliceJob*)(ws + pl->off_slice) + pl->slice_step_off[s], ws, (int)nb);
+        GMP_CUDA(cudaGetLastError());
+      }
       GMP_CUDA(cudaEventRecord(pl->step_ev[s], pl->comm_stream));
     }
   }
@@ -831,7 +896,10 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
       const WorkItem* it = (const WorkItem*)(ws + pl->off_items) + L.ibeg;
       const PairDesc* pd = (const PairDesc*)(ws + pl->off_pairs);
       if (!pl->launch_ev.empty()) GMP_CUDA(cudaEventRecord(pl->launch_ev[2 * li], stream));
-      if (L.kind == 1 || L.kind == 3) {
+      if (L.kind == 4) {
+        if (oz_launch(pl->oz, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, pl->off_oexp, stream) != GMP_OK)
+          return fail(GMP_ERR_CUDA, std::string("k_tc_fp64 launch: ") + cudaGetErrorString(cudaGetLastError()));
+      } else if (L.kind == 1 || L.kind == 3) {
         GMP_TRY(tc_launch(pl->tc, L.kind == 3 ? 5 : L.cls, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, stream));
       } else {
         switch (L.cls) {
@@ -915,13 +983,14 @@ extern "C" gmp_status_t gemm_mp_get_tile(gmp_plan_t pl, char which, int64_t ti, 
   if (which == 'A' || which == 'B') {
     const bool isB = which == 'B';
     const int64_t rows = isB ? pl->kt : pl->mt, cols = isB ? pl->nt : pl->kt;
-    if (ti < 0 || tj < 0 || ti >= rows || tj >= cols || cls < 0 || cls > 5) return fail(GMP_ERR_ARG, "tile index out of range");
+    if (ti < 0 || tj < 0 || ti >= rows || tj >= cols || cls < 0 || cls > 6) return fail(GMP_ERR_ARG, "tile index out of range");
     const int64_t g = ti * cols + tj;
-    const int32_t slot = (cls == 5) ? (isB ? pl->splitB : pl->splitA)[g] : (isB ? pl->slotB5 : pl->slotA5)[g * 5 + cls];
+    const int32_t slot = (cls == 6) ? (isB ? pl->sliceB : pl->sliceA)[g]
+                       : (cls == 5) ? (isB ? pl->splitB : pl->splitA)[g] : (isB ? pl->slotB5 : pl->slotA5)[g * 5 + cls];
     if (slot < 0) return fail(GMP_ERR_ARG, "representation not materialised on this rank");
     off = pl->arena_off[cls] + slot * pl->slot_bytes[cls];
     nbytes = pl->slot_bytes[cls];
-    sc = (isB ? pl->sB5 : pl->sA5)[g * 5 + (cls == 5 ? 1 : cls)];
+    sc = (cls == 6) ? 0 : (isB ? pl->sB5 : pl->sA5)[g * 5 + (cls == 5 ? 1 : cls)];
   } else if (which == 'C' || which == 'I' || which == 'W') {
     if (ti < 0 || tj < 0 || ti >= pl->mt || tj >= pl->nt) return fail(GMP_ERR_ARG, "tile index out of range");
     const int64_t g = ti * pl->nt + tj;

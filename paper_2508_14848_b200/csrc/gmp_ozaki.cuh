@@ -1,0 +1,334 @@
+// gmp_ozaki.cuh -- EXPERIMENTAL: the FP64 class on the INT8 tensor pipe (Ozaki-
+// style error-free slicing + tcgen05.mma kind::i8), opt-in with
+// GMP_FLAG_FP64_INT8 (the product FP64 path is k_dmma).  Correct (tested to the
+// 1e-13 FP64 parity bound) but currently ~3x slower than DMMA on B200: the
+// seven 32-byte-wide digit planes per operand make every TMA box a stream of
+// 32-byte row segments (1344 per stage) and the seven int32 diagonal
+// accumulators cap N at 64, so the tensor pipe idles (ncu: 7 % active, 56 % L2
+// hit).  DESIGN.md section 10 lists the layout change this needs.
+//
+// Slicing (k_slice64, receiver-side from the stored binary64 payload): for each
+// K-major operand row r (A: tile row, B: tile column) with e_r the frexp
+// exponent of max_k |x(r,k)| (all |x| 2^-e_r < 1), the normalised value
+// a = x 2^-e_r is cut into NS = 7 signed 8-bit digits by exact truncation:
+//     t = a 2^7 ; q_i = trunc(t) in [-127, 127] ; a = t - q_i   (all exact in binary64)
+// so x = 2^e_r (sum_i q_i 2^-7i + rho), |rho| < 2^-49.
+// Product: P(r,c) = 2^(e_r + f_c) sum_{d=2..8} 2^-7d S_d(r,c),
+//          S_d = sum_{i+j=d} Q^A_i Q^B_j^T   (exact int32: <= 7 * 127^2 * nb < 2^31)
+// -- 28 int8 MMAs per K block (terms i + j <= NS + 1), the dropped terms and rho
+// are below 2^-48 of |A||B| row/column scales: binary64-level normwise accuracy
+// (parity bound 1e-13).  The seven diagonal accumulators
+// live in TMEM (7 x 64 int32 columns); the epilogue combines them in binary64,
+// smallest first, applies the two power-of-two row/column scales and folds
+// (O9).
+#pragma once
+#include "gmp_tc.cuh"
+
+namespace gmp {
+
+constexpr int OZ_NS = 7;              // int8 digits per element
+constexpr int OZ_BN = 64;             // N of the MMA tile (7 x 64 TMEM columns)
+constexpr int OZ_BK = 32;             // bytes (= int8 elements) of K per stage: one MMA per term
+constexpr int OZ_STAGES = 4;
+constexpr int OZ_THREADS = 320;       // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
+
+// ---------------------------------------------------------------------------
+// slicing kernel: one job = one tile (MN-major binary64 payload -> NS K-major
+// int8 digit planes + nb row exponents).  One CTA per 64 output rows.
+// ---------------------------------------------------------------------------
+struct SliceJob {
+  int64_t src_off;   // binary64 payload (MN-major: element (r, k) at k*nb + r)
+  int64_t dst_off;   // NS planes of nb x nb int8, K-major (element (r, k) at r*nb + k)
+  int64_t exp_off;   // nb int16 row exponents
+};
+
+__global__ void __launch_bounds__(256) k_slice64(const SliceJob* __restrict__ jobs, uint8_t* ws, int nb) {
+  __shared__ double sm[64][65];
+  __shared__ int sexp[64];
+  __shared__ double smax[4][64];
+  const SliceJob j = jobs[blockIdx.y];
+  const int r0 = blockIdx.x * 64;
+  const double* src = reinterpret_cast<const double*>(ws + j.src_off);
+  int8_t* dst = reinterpret_cast<int8_t*>(ws + j.dst_off);
+  const int t = threadIdx.x, rr = t & 63, kq = t >> 6;   // 64 rows x 4 k-lanes
+  // pass 1: row maxima over k (coalesced: 64 consecutive r per k)
+  double m = 0.0;
+  for (int k = kq; k < nb; k += 4) m = fmax(m, fabs(src[(int64_t)k * nb + r0 + rr]));
+  smax[kq][rr] = m;
+  __syncthreads();
+  if (t < 64) {
+    const double mx = fmax(fmax(smax[0][t], smax[1][t]), fmax(smax[2][t], smax[3][t]));
+    int e = 0;
+    if (mx > 0.0) frexp(mx, &e);            // mx in [2^(e-1), 2^e)
+    sexp[t] = e;
+    reinterpret_cast<int16_t*>(ws + j.exp_off)[r0 + t] = (int16_t)e;
+  }
+  __syncthreads();
+  const int64_t plane = (int64_t)nb * nb;
+  // pass 2: 64 x 64 blocks, transpose through shared memory, digits per element
+  for (int k0 = 0; k0 < nb; k0 += 64) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int unit = t + u * 256;
+      const int kk = unit >> 6, r = unit & 63;
+      sm[kk][r] = src[(int64_t)(k0 + kk) * nb + r0 + r];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      // thread -> (row r, 4 consecutive k)
+      const int unit = t + u * 256;
+      const int r = unit >> 4, kk0 = (unit & 15) * 4;
+      int8_t q[OZ_NS][4];
+#pragma unroll
+      for (int e4 = 0; e4 < 4; ++e4) {
+        double a = ldexp(sm[kk0 + e4][r], -sexp[r]);
+#pragma unroll
+        for (int i = 0; i < OZ_NS; ++i) {
+          const double tt = a * 128.0;        // exact
+          const double qi = trunc(tt);        // |qi| <= 127
+          q[i][e4] = (int8_t)qi;
+          a = tt - qi;                        // exact
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < OZ_NS; ++i) {
+        const uint32_t w = (uint32_t)(uint8_t)q[i][0] | ((uint32_t)(uint8_t)q[i][1] << 8) |
+                           ((uint32_t)(uint8_t)q[i][2] << 16) | ((uint32_t)(uint8_t)q[i][3] << 24);
+        *reinterpret_cast<uint32_t*>(dst + i * plane + (int64_t)(r0 + r) * nb + k0 + kk0) = w;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// INT8 tcgen05 kernel
+// ---------------------------------------------------------------------------
+// K-major SWIZZLE_32B canonical layout: 8-row x 32-byte atoms, SBO = 256 B.
+__device__ __forceinline__ uint64_t sdesc_k_sw32(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(256 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)6 << 61);
+}
+// D = S32 (c_format 2), A/B signed int8 (format 1), K-major, N = 64, M = 128
+constexpr uint32_t oz_idesc() {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
+}
+__device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+constexpr int oz_smem_bytes() {
+  return OZ_STAGES * OZ_NS * (TC_BM + OZ_BN) * OZ_BK + 1024 + 256;
+}
+
+__global__ void __launch_bounds__(OZ_THREADS, 1)
+k_tc_fp64(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+          const WorkItem* __restrict__ items, int64_t nitems, const PairDesc* __restrict__ pairs,
+          const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha,
+          int64_t exp_off) {
+  constexpr int A_BYTES = TC_BM * OZ_BK, B_BYTES = OZ_BN * OZ_BK;
+  constexpr int STAGE_BYTES = OZ_NS * (A_BYTES + B_BYTES);
+  constexpr uint32_t TMEM_COLS = 512;
+  constexpr uint32_t IDESC = oz_idesc();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OZ_STAGES * STAGE_BYTES);
+  uint64_t* empty = full + OZ_STAGES;
+  uint64_t* tfull = empty + OZ_STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  const int16_t* __restrict__ exps = reinterpret_cast<const int16_t*>(ws + exp_off);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < OZ_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, TC_EPI_WARPS);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int kblocks = nb / OZ_BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const WorkItem w = expand_item(items, it, nb, OZ_BN);
+        for (int pi = 0; pi < w.pcnt; ++pi) {
+          const PairDesc pd = pairs[w.pbeg + pi];
+          for (int kb = 0; kb < kblocks; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* sa = smem + stage * STAGE_BYTES;
+            mbar_expect_tx(&full[stage], STAGE_BYTES);
+#pragma unroll
+            for (int p = 0; p < OZ_NS; ++p) {
+              tma_load_2d(sa + p * A_BYTES, &tmA, kb * OZ_BK, (pd.a_slot * OZ_NS + p) * nb + w.m0, &full[stage]);
+              tma_load_2d(sa + OZ_NS * A_BYTES + p * B_BYTES, &tmB, kb * OZ_BK, (pd.b_slot * OZ_NS + p) * nb + w.n0,
+                          &full[stage]);
+            }
+            if (++stage == OZ_STAGES) { stage = 0; phase ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const WorkItem w = expand_item(items, it, nb, OZ_BN);
+        for (int pi = 0; pi < w.pcnt; ++pi) {
+          mbar_wait(tempty, acc_phase ^ 1);
+          tc_fence_after();
+          for (int kb = 0; kb < kblocks; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+            // diagonal d = i + j (digits 1-based): accumulator column block d - 2
+#pragma unroll
+            for (int d = OZ_NS + 1; d >= 2; --d) {
+              const uint32_t d_tmem = tmem_base + (uint32_t)((d - 2) * OZ_BN);
+#pragma unroll
+              for (int i = 1; i < d; ++i) {
+                const int j = d - i;
+                const uint64_t ad = sdesc_k_sw32(sa + (i - 1) * A_BYTES);
+                const uint64_t bd = sdesc_k_sw32(sa + OZ_NS * A_BYTES + (j - 1) * B_BYTES);
+                tc_mma_i8(d_tmem, ad, bd, IDESC, (kb != 0 || i != 1) ? 1u : 0u);
+              }
+            }
+            tc_commit(&empty[stage]);
+            if (++stage == OZ_STAGES) { stage = 0; phase ^= 1; }
+          }
+          tc_commit(tfull);
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // epilogue: warp w reads TMEM lanes 32*(w%4)..+31 (tile rows) and half (w-2)/4
+    // of the 64 columns (32 each, two 16-column chunks)
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    const int rloc = quarter * 32 + lane;
+    uint32_t acc_phase = 0;
+    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+      const WorkItem w = expand_item(items, it, nb, OZ_BN);
+      const CTileDesc ct = ctiles[w.ctile];
+      const int64_t rowoff = (int64_t)(w.m0 + rloc) * nb + w.n0 + half * 32;
+      for (int pi = 0; pi < w.pcnt; ++pi) {
+        const PairDesc pd = pairs[w.pbeg + pi];
+        const double f64 = ldexp(alpha, pd.fexp);
+        const float f32 = __double2float_rn(f64);
+        const int er = exps[(int64_t)pd.a_slot * nb + w.m0 + rloc];
+        const int16_t* fcol = exps + (int64_t)pd.b_slot * nb + w.n0 + half * 32;
+        mbar_wait(tfull, acc_phase);
+        tc_fence_after();
+        const uint32_t tq = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(half * 32);
+#pragma unroll 1
+        for (int ch = 0; ch < 2; ++ch) {
+          double p[16];
+#pragma unroll
+          for (int v = 0; v < 16; ++v) p[v] = 0.0;
+#pragma unroll
+          for (int d = OZ_NS + 1; d >= 2; --d) {      // smallest diagonal first
+            uint32_t r[16];
+            tmem_ld16_nowait(tq + (uint32_t)((d - 2) * OZ_BN + ch * 16), r);
+            tmem_wait_ld();
+            const double sc = ldexp(1.0, -7 * d);
+#pragma unroll
+            for (int v = 0; v < 16; ++v) p[v] = __fma_rn((double)(int32_t)r[v], sc, p[v]);
+          }
+          if (ct.code == 0) {
+            double* wp = reinterpret_cast<double*>(ws + ct.w_off) + rowoff + ch * 16;
+#pragma unroll
+            for (int v = 0; v < 16; v += 2) {
+              double2 x = *reinterpret_cast<double2*>(wp + v);
+              x.x = __fma_rn(f64, ldexp(p[v], er + fcol[ch * 16 + v]), x.x);
+              x.y = __fma_rn(f64, ldexp(p[v + 1], er + fcol[ch * 16 + v + 1]), x.y);
+              *reinterpret_cast<double2*>(wp + v) = x;
+            }
+          } else {
+            float* wp = reinterpret_cast<float*>(ws + ct.w_off) + rowoff + ch * 16;
+#pragma unroll
+            for (int v = 0; v < 16; v += 2) {
+              float2 x = *reinterpret_cast<float2*>(wp + v);
+              x.x = __fmaf_rn(f32, __double2float_rn(ldexp(p[v], er + fcol[ch * 16 + v])), x.x);
+              x.y = __fmaf_rn(f32, __double2float_rn(ldexp(p[v + 1], er + fcol[ch * 16 + v + 1])), x.y);
+              *reinterpret_cast<float2*>(wp + v) = x;
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty);
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+}
+
+// host: TMA maps over the digit arena (rows = slot * NS * nb + plane * nb + r)
+struct OzTables {
+  CUtensorMap mapA, mapB;
+  bool ready = false;
+};
+
+inline gmp_status_t oz_prepare(OzTables& t, uint8_t* ws, int64_t arena_off, int64_t slots, int nb) {
+  t.ready = false;
+  if (slots == 0) return GMP_OK;
+  PFN_encodeTiled enc = get_encode_tiled();
+  if (!enc) return GMP_ERR_CUDA;
+  cuuint64_t dims[2] = {(cuuint64_t)nb, (cuuint64_t)(slots * OZ_NS * nb)};
+  cuuint64_t strides[1] = {(cuuint64_t)nb};
+  cuuint32_t estr[2] = {1, 1};
+  cuuint32_t boxA[2] = {(cuuint32_t)OZ_BK, (cuuint32_t)TC_BM};
+  cuuint32_t boxB[2] = {(cuuint32_t)OZ_BK, (cuuint32_t)OZ_BN};
+  if (enc(&t.mapA, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, ws + arena_off, dims, strides, boxA, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return GMP_ERR_CUDA;
+  if (enc(&t.mapB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, ws + arena_off, dims, strides, boxB, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return GMP_ERR_CUDA;
+  t.ready = true;
+  return GMP_OK;
+}
+
+inline gmp_status_t oz_launch(OzTables& t, const WorkItem* it, int64_t n, const PairDesc* pd, const CTileDesc* ct,
+                              uint8_t* ws, int nb, double alpha, int64_t exp_off, cudaStream_t s) {
+  if (!t.ready) return GMP_ERR_STATE;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_tc_fp64, cudaFuncAttributeMaxDynamicSharedMemorySize, oz_smem_bytes()) != cudaSuccess)
+      return GMP_ERR_CUDA;
+    attr = true;
+  }
+  // one CTA per (item, sub-tile), scheduled in flat order: the CTAs of one C
+  // tile run together and walk its pair list in step (L2 reuse of the planes)
+  const int grid = (int)n;
+  k_tc_fp64<<<grid, OZ_THREADS, oz_smem_bytes(), s>>>(t.mapA, t.mapB, it, n, pd, ct, ws, nb, alpha, exp_off);
+  return cudaGetLastError() == cudaSuccess ? GMP_OK : GMP_ERR_CUDA;
+}
+
+}  // namespace gmp

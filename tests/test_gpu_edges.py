@@ -114,3 +114,32 @@ def test_rectangular_many_tiles_sampled_vs_oracle():
         i, j = divmod(t, 4)
         sl = (slice(i * 128, (i + 1) * 128), slice(j * 128, (j + 1) * 128))
         assert np.array_equal(out[sl], o["C"][sl])
+
+
+def test_fp64_digit_planes_reconstruct():
+    """FP64 class on the (experimental, opt-in) INT8 tensor pipe: the seven int8 digit planes of every
+    sliced operand satisfy x = 2^e_r (sum_i q_i 2^-7i + rho), |rho| < 2^-49, |q| <= 127
+    (checked against the oracle-packed binary64 payload, K-major view)."""
+    w = gmp_inputs.small_workload(512, 512, 512, 128, 1e-12, mode="random", E=12, beta=0.0,
+                                  class_mask=0b00001, seed=31)
+    A, Bm, C = w.matrices()
+    g, (out,) = run_gpu(A, Bm, None, 128, w.tol, 1.0, 0.0, w.class_mask, flags=B.GMP_FLAG_FP64_INT8)
+    nb = 128
+    checked = 0
+    for which, X in [("A", A), ("B", Bm)]:
+        for ti in range(4):
+            for tj in range(4):
+                planes, _ = g.tile(which, ti, tj, 6)
+                q = planes.view(np.int8).reshape(7, nb, nb).astype(np.float64)
+                tile = X[ti * nb:(ti + 1) * nb, tj * nb:(tj + 1) * nb]
+                kmaj = tile if which == "A" else tile.T          # rows = output rows / cols, K contiguous
+                rowmax = np.abs(kmaj).max(axis=1)
+                _, e = np.frexp(rowmax)
+                rec = sum(q[i] * 2.0 ** (-7 * (i + 1)) for i in range(7))
+                rec = np.ldexp(rec, e[:, None])
+                assert np.all(np.abs(q) <= 127)
+                assert np.all(np.abs(rec - kmaj) <= np.ldexp(1.0, e - 49)[:, None])
+                checked += 1
+    assert checked == 32
+    o = run_oracle(A, Bm, None, 128, w.tol, 1.0, 0.0, w.class_mask)
+    assert np.linalg.norm(out - o["C"]) / np.linalg.norm(o["C"]) <= 1e-13
