@@ -71,6 +71,7 @@ struct Launch {
   int step, cls, kind;  // kind 0: SIMT/DMMA kernel, 1: tcgen05, 2: FP64 DFMA cross-check, 3: FP32 on tcgen05
                         // (BF16x9), 4: FP64 on the INT8 tensor pipe (Ozaki digits)
   int64_t ibeg, icount;
+  int bn;  // N of the class kernel's CTA tile
 };
 
 struct Bcast {           // one SUMMA broadcast of a stored tile in a step
@@ -519,9 +520,14 @@ static void build_tables(gmp_plan_s* pl) {
       pl->items.insert(pl->items.end(), its.begin(), its.end());
       const bool split = (c == 1 && pl->fp32_tc), ozaki = (c == 0 && pl->fp64_tc);
       const int kind = ozaki ? 4 : split ? 3 : tc ? 1 : (c == 0 && (d.flags & GMP_FLAG_SIMT_ONLY)) ? 2 : 0;
+      // tcgen05 launches that fold into binary64 W keep the accumulator rows in
+      // registers, which needs BN = 128
+      bool w64 = false;
+      for (const WorkItem& wi : its) w64 = w64 || pl->ctd[wi.ctile].code == 0;
+      const int tcbn = (w64 ? 128 : tc_bn((int)nb));
       // flat launch size: items x sub-tiles of the class kernel's CTA tile
-      const int bn = ozaki ? OZ_BN : split ? 128 : tc ? tc_bn((int)nb) : mn_bn(c);
-      pl->launches.push_back(Launch{s, c, kind, ibeg, (int64_t)its.size() * subtiles_per_item((int)nb, bn)});
+      const int bn = ozaki ? OZ_BN : split ? 128 : tc ? tcbn : mn_bn(c);
+      pl->launches.push_back(Launch{s, c, kind, ibeg, (int64_t)its.size() * subtiles_per_item((int)nb, bn), bn});
     }
   }
 
@@ -900,7 +906,8 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
         if (oz_launch(pl->oz, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, pl->off_oexp, stream) != GMP_OK)
           return fail(GMP_ERR_CUDA, std::string("k_tc_fp64 launch: ") + cudaGetErrorString(cudaGetLastError()));
       } else if (L.kind == 1 || L.kind == 3) {
-        GMP_TRY(tc_launch(pl->tc, L.kind == 3 ? 5 : L.cls, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, stream));
+        GMP_TRY(tc_launch(pl->tc, L.kind == 3 ? 5 : L.cls, L.bn, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha,
+                          stream));
       } else {
         switch (L.cls) {
           case 0:

@@ -263,7 +263,41 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
 #pragma unroll
         for (int v = 0; v < HC / 4; ++v)
           reinterpret_cast<float4*>(wrow)[v] = make_float4(accr[4 * v], accr[4 * v + 1], accr[4 * v + 2], accr[4 * v + 3]);
+      } else if constexpr (HC <= 64) {
+        // binary64 W, BN <= 128: the W row segment lives in registers for the item
+        double* wrow = reinterpret_cast<double*>(ws + ct.w_off) + rowoff;
+        double accd[HC];
+#pragma unroll
+        for (int v = 0; v < HC / 2; ++v) {
+          const double2 x = reinterpret_cast<const double2*>(wrow)[v];
+          accd[2 * v] = x.x; accd[2 * v + 1] = x.y;
+        }
+        for (int pi = 0; pi < w.pcnt; ++pi) {
+          const PairDesc pd = pairs[w.pbeg + pi];
+          const double f64 = ldexp(alpha, pd.fexp);
+          mbar_wait(&tfull[acc], acc_phase);
+          tc_fence_after();
+          const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + half * HC);
+#pragma unroll
+          for (int ch = 0; ch < HC / 16; ++ch) {
+            uint32_t r[16];
+            tmem_ld16_nowait(tbase + ch * 16, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int v = 0; v < 16; ++v)
+              accd[ch * 16 + v] = __fma_rn(f64, (double)__uint_as_float(r[v]), accd[ch * 16 + v]);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+#pragma unroll
+        for (int v = 0; v < HC / 2; ++v)
+          reinterpret_cast<double2*>(wrow)[v] = make_double2(accd[2 * v], accd[2 * v + 1]);
       } else {
+        // binary64 W with BN = 256: read-modify-write per pair (the host prefers
+        // BN = 128 for launches that hold binary64 accumulators)
         double* wrow = reinterpret_cast<double*>(ws + ct.w_off) + rowoff;
         for (int pi = 0; pi < w.pcnt; ++pi) {
           const PairDesc pd = pairs[w.pbeg + pi];
@@ -309,7 +343,8 @@ constexpr int tc_smem_bytes() {
 // host side
 // ---------------------------------------------------------------------------
 struct TcTables {
-  CUtensorMap mapA[6], mapB[6];   // classes 2..4 and 5 = FP32 split (BF16 parts)
+  CUtensorMap mapA[6], mapB[6];   // classes 2..4 and 5 = FP32 split (BF16 parts); B box rows = tc_bn(nb)
+  CUtensorMap mapB128[6];         // B box of 128 rows (launches with binary64 W)
   bool ready[6] = {false, false, false, false, false, false};
   int nb = 0;
 };
@@ -357,6 +392,11 @@ inline gmp_status_t tc_prepare(TcTables& t, uint8_t* ws, const int64_t* arena_of
             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return GMP_ERR_CUDA;
+    cuuint32_t boxB128[2] = {(cuuint32_t)(128 / esz), 128u};
+    if (enc(&t.mapB128[c], dt, 2, base, dims, strides, boxB128, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return GMP_ERR_CUDA;
     t.ready[c] = true;
   }
   return GMP_OK;
@@ -376,15 +416,17 @@ inline gmp_status_t tc_launch_t(TcTables& t, const WorkItem* it, int64_t n, cons
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)std::min<int64_t>(n, sms);
-  k_tc_class<C, BN><<<grid, TC_THREADS, smem, s>>>(t.mapA[C], t.mapB[C], it, n, pd, ct, ws, nb, alpha);
+  k_tc_class<C, BN><<<grid, TC_THREADS, smem, s>>>(t.mapA[C], BN == 128 ? t.mapB128[C] : t.mapB[C], it, n, pd, ct, ws,
+                                                    nb, alpha);
   return cudaGetLastError() == cudaSuccess ? GMP_OK : GMP_ERR_CUDA;
 }
 
-// cls: 2..4 for the 16/8-bit classes, 5 for the FP32 class on the tensor pipe
-inline gmp_status_t tc_launch(TcTables& t, int cls, const WorkItem* it, int64_t n, const PairDesc* pd,
+// cls: 2..4 for the 16/8-bit classes, 5 for the FP32 class on the tensor pipe;
+// bn: 256 or 128 (tc_bn_for(): 128 when the launch folds into binary64 W)
+inline gmp_status_t tc_launch(TcTables& t, int cls, int bn, const WorkItem* it, int64_t n, const PairDesc* pd,
                               const CTileDesc* ct, uint8_t* ws, int nb, double alpha, cudaStream_t s) {
   if (cls < 2 || cls > 5 || !t.ready[cls]) return GMP_ERR_STATE;
-  const bool wide = tc_bn(nb) == 256;
+  const bool wide = bn == 256;
   switch (cls) {
     case 2: return wide ? tc_launch_t<2, 256>(t, it, n, pd, ct, ws, nb, alpha, s) : tc_launch_t<2, 128>(t, it, n, pd, ct, ws, nb, alpha, s);
     case 3: return wide ? tc_launch_t<3, 256>(t, it, n, pd, ct, ws, nb, alpha, s) : tc_launch_t<3, 128>(t, it, n, pd, ct, ws, nb, alpha, s);
