@@ -916,8 +916,9 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
               k_mn<double><<<(unsigned)L.icount, 256, mn_smem_bytes<double>(), stream>>>(it, pd, dct, ws, (int)nb,
                                                                                        pl->d.alpha);
             } else {
-              GMP_TRY(set_smem_once(k_dmma, dmma_smem_bytes()));
-              k_dmma<<<(unsigned)L.icount, 256, dmma_smem_bytes(), stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha);
+              GMP_TRY(set_smem_once(k_dmma<DMMA_WN>, dmma_smem_bytes()));
+              k_dmma<DMMA_WN><<<(unsigned)L.icount, 256, dmma_smem_bytes(), stream>>>(it, pd, dct, ws, (int)nb,
+                                                                                      pl->d.alpha);
             }
             break;
           case 1:

@@ -410,9 +410,17 @@ k_mn(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
 // The accumulation order inside a DMMA is the hardware's: the parity bound is
 // the all-FP64 1e-13 relative Frobenius.
 // ---------------------------------------------------------------------------
-constexpr int DMMA_ST = 4, DMMA_BN = 64, DMMA_BK = 16;
-constexpr int DMMA_AP = 128 + 4, DMMA_BP = DMMA_BN + 4;  // row pitches in doubles (= 32 B mod 128 B)
-constexpr int dmma_smem_bytes() { return DMMA_ST * DMMA_BK * (DMMA_AP + DMMA_BP) * 8; }
+constexpr int DMMA_ST = 4, DMMA_BK = 16;
+template <int WN> struct DmmaCfg {
+  static constexpr int BN = 2 * WN;                 // 8 warps = 4 (m) x 2 (n), warp tile 32 x WN
+  static constexpr int AP = 128 + 4, BP = BN + 4;   // row pitches in doubles (= 32 B mod 128 B)
+  static constexpr int SMEM = DMMA_ST * DMMA_BK * (AP + BP) * 8;
+  static constexpr int MINB = (WN == 32) ? 2 : 1;
+};
+constexpr int DMMA_WN = 32;                         // product configuration (128 x 64 sub-tiles; 32 x 64 warp
+                                                    // tiles at 1 CTA/SM measured 9 % slower)
+constexpr int DMMA_BN = DmmaCfg<DMMA_WN>::BN;
+constexpr int dmma_smem_bytes() { return DmmaCfg<DMMA_WN>::SMEM; }
 
 __device__ __forceinline__ void dmma16816(double (&c)[4], const double (&a)[8], const double (&b)[4]) {
   asm(
@@ -423,30 +431,38 @@ __device__ __forceinline__ void dmma16816(double (&c)[4], const double (&a)[8], 
         "d"(b[1]), "d"(b[2]), "d"(b[3]));
 }
 
-__global__ void __launch_bounds__(256, 2)
+template <int WN>
+__global__ void __launch_bounds__(256, DmmaCfg<WN>::MINB)
 k_dmma(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
        const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha) {
-  constexpr int BK = DMMA_BK, ST = DMMA_ST, AP = DMMA_AP, BP = DMMA_BP;
-  constexpr int ACH = 64, BCH = DMMA_BN / 2;        // 16-byte chunks per k-row (A: 128 doubles, B: 64)
+  using Cfg = DmmaCfg<WN>;
+  constexpr int BK = DMMA_BK, ST = DMMA_ST, AP = Cfg::AP, BP = Cfg::BP, BN = Cfg::BN, NJ = WN / 8;
+  constexpr int ACH = 64, BCH = BN / 2;             // 16-byte chunks per k-row (A: 128 doubles, B: BN)
   constexpr int CHUNKS = BK * (ACH + BCH), CPT = CHUNKS / 256;
   constexpr int STAGE = BK * (AP + BP) * 8;
+  static_assert(CHUNKS % 256 == 0, "loader");
   extern __shared__ __align__(128) uint8_t sm[];
-  const WorkItem it = expand_item(items, blockIdx.x, nb, DMMA_BN);
+  const WorkItem it = expand_item(items, blockIdx.x, nb, BN);
   const CTileDesc ct = ctiles[it.ctile];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * WN;
   const int nsl = nb / BK;
   const int total = it.pcnt * nsl;
   const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
 
+  // producer cursor over the (pair, slice) sequence (no divisions in the loop)
+  int ip = 0, is = 0, istage = 0;
+  const uint8_t *Ag = nullptr, *Bg = nullptr;
+  const int64_t slice_bytes = (int64_t)BK * nb * 8;
   auto issue = [&](int gi) {
     if (gi < total) {
-      const int pi = gi / nsl, s = gi - pi * nsl;
-      const PairDesc pd = pairs[it.pbeg + pi];
-      const uint8_t* Ag = ws + pd.a_off + ((int64_t)s * BK * nb + it.m0) * 8;
-      const uint8_t* Bg = ws + pd.b_off + ((int64_t)s * BK * nb + it.n0) * 8;
-      const uint32_t stg = sbase + (uint32_t)((gi % ST) * STAGE);
+      if (is == 0) {
+        const PairDesc pd = pairs[it.pbeg + ip];
+        Ag = ws + pd.a_off + (int64_t)it.m0 * 8;
+        Bg = ws + pd.b_off + (int64_t)it.n0 * 8;
+      }
+      const uint32_t stg = sbase + (uint32_t)(istage * STAGE);
 #pragma unroll
       for (int u = 0; u < CPT; ++u) {
         const int c = tid + u * 256;
@@ -458,6 +474,10 @@ k_dmma(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
           cp_async16(stg + BK * AP * 8 + k * BP * 8 + ch * 16, Bg + (int64_t)k * nb * 8 + ch * 16);
         }
       }
+      Ag += slice_bytes;
+      Bg += slice_bytes;
+      if (++is == nsl) { is = 0; ++ip; }
+      if (++istage == ST) istage = 0;
     }
     cp_async_commit();
   };
@@ -465,43 +485,45 @@ k_dmma(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
 #pragma unroll
   for (int gi = 0; gi < ST - 1; ++gi) issue(gi);
 
-  double acc[2][4][4];
+  double acc[2][NJ][4];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < NJ; ++j)
 #pragma unroll
       for (int v = 0; v < 4; ++v) acc[i][j][v] = 0.0;
 
+  int cstage = 0, cslice = 0, cpair = 0;
   for (int gi = 0; gi < total; ++gi) {
     cp_async_wait<ST - 2>();
     __syncthreads();
     issue(gi + ST - 1);
-    const double* As = reinterpret_cast<const double*>(sm + (gi % ST) * STAGE);
+    const double* As = reinterpret_cast<const double*>(sm + cstage * STAGE);
     const double* Bs = As + BK * AP;
+    if (++cstage == ST) cstage = 0;
     double a[2][8];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
       for (int r = 0; r < 8; ++r) a[i][r] = As[(t + 4 * (r >> 1)) * AP + wm + i * 16 + g + 8 * (r & 1)];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < NJ; ++j) {
       double b[4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) b[r] = Bs[(t + 4 * r) * BP + wn + j * 8 + g];
 #pragma unroll
       for (int i = 0; i < 2; ++i) dmma16816(acc[i][j], a[i], b);
     }
-    const int pi = gi / nsl;
-    if (gi - pi * nsl == nsl - 1) {
+    if (++cslice == nsl) {
+      cslice = 0;
       // ---- fold (O9) ----
-      const PairDesc pd = pairs[it.pbeg + pi];
+      const PairDesc pd = pairs[it.pbeg + cpair++];
       const double f64 = ldexp(alpha, pd.fexp);
       const float f32 = __double2float_rn(f64);
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < NJ; ++j)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int r = it.m0 + wm + i * 16 + g + 8 * h;
