@@ -392,6 +392,15 @@ def main():
     # precision-mix roofline: sum_c F_c / (G * Peak_c) vs the step time
     t_roof_ms = sum(st["flops"][c] / (G * cpk[c] * 1e12) for c in range(5)) * 1e3
     exec_ms = statistics.median(ph[2] for ph in phase)
+    # DRAM traffic per launch of the dominant kernel from the committed ncu capture
+    traffic = None
+    try:
+        kname = {0: "k_dmma<32>", 1: "k_tc_class<5, 128>", 2: "k_tc_class<2, 128>", 3: "k_tc_class<3, 256>",
+                 4: "k_tc_class<4, 256>"}[dom]
+        with open(os.path.join(ROOT, "profiles", "traffic_r01.json")) as f:
+            traffic = json.load(f)["kernels"].get(kname)
+    except Exception:
+        traffic = None
     launches = st["launches_plan"] + st["launches_convert"] + st["launches_execute"]
 
     # ---- e2e: host (pinned) buffers, copies inside the timed region ----
@@ -423,7 +432,9 @@ def main():
             "class_ms_rank0": class_ms,
             "roofline": {"bound": "tensor", "kernel": f"class {gmp_class_name(dom)} tile-GEMM",
                          "achieved": achieved, "peak": dom_peak, "unit": "TFLOP/s",
-                         "frac": achieved / dom_peak if dom_peak else None, "traffic": None,
+                         "frac": achieved / dom_peak if dom_peak else None, "traffic": traffic,
+                         "traffic_unit": "bytes per launch (ncu dram read+write, profiles/traffic_r01.json)",
+                         "launches_timed": st["class_launches"][dom],
                          "peak_source": ("derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz (DMMA = DFMA nominal)"
                                          if dom == 0 else
                                          peak_src + " bf16 sustained / 9 (FP32 class = 9 BF16 MMAs per product)"
