@@ -41,3 +41,21 @@ def test_null_plan_is_rejected():
     with pytest.raises(B.GmpError):
         B.gemm_mp_workspace_size(None)
     B.gemm_mp_destroy(None)  # NULL-safe
+
+
+@pytest.mark.parametrize("kw", [dict(M=0, N=128, K=128), dict(M=128, N=-128, K=128), dict(M=128, N=128, K=0)])
+def test_empty_or_negative_shapes_rejected(kw):
+    d = B.make_desc(nb=128, tol=1e-6, **kw)
+    with pytest.raises(B.GmpError) as e:
+        B.gemm_mp_scratch_size(d)
+    assert "GMP_ERR_ARG" in str(e.value)
+
+
+def test_host_plan_rejects_bad_codes():
+    import numpy as np
+    d = B.make_desc(256, 256, 256, 128, 1e-6)
+    bad = np.full((2, 2), 7, np.uint8)
+    z = np.zeros((2, 2, 5), np.int16)
+    with pytest.raises(B.GmpError) as e:
+        B.gemm_mp_plan_host(d, bad, bad, bad, z, z)
+    assert "GMP_ERR_MAP_SHAPE" in str(e.value)

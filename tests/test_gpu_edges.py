@@ -143,3 +143,18 @@ def test_fp64_digit_planes_reconstruct():
     assert checked == 32
     o = run_oracle(A, Bm, None, 128, w.tol, 1.0, 0.0, w.class_mask)
     assert np.linalg.norm(out - o["C"]) / np.linalg.norm(o["C"]) <= 1e-13
+
+
+@pytest.mark.parametrize("nb,mask,tol", [(128, 0b01111, 1e-6), (256, 0b11111, 1e-1), (128, 0b00001, 1e-12)])
+def test_single_tile(nb, mask, tol):
+    """degenerate grid: M = N = K = nb (one tile each, one SUMMA step, one pair)"""
+    w = gmp_inputs.small_workload(nb, nb, nb, nb, tol, mode="uniform", E=0, beta=0.25, class_mask=mask, seed=61)
+    A, Bm, C = w.matrices()
+    o = run_oracle(A, Bm, C, nb, tol, 1.0, 0.25, mask)
+    g, (out,) = run_gpu(A, Bm, C, nb, tol, 1.0, 0.25, mask)
+    m = g.maps()
+    assert np.array_equal(m["acode"], o["acode"]) and np.array_equal(m["ccode"], o["ccode"])
+    gs, (outs,) = run_gpu(A, Bm, C, nb, tol, 1.0, 0.25, mask, flags=B.GMP_FLAG_SIMT_ONLY)
+    assert np.array_equal(outs, o["C"])
+    bound = 1e-13 if mask == 1 else 4 * 2.0 ** -24 * np.sqrt(nb)
+    assert np.linalg.norm(out - o["C"]) / np.linalg.norm(o["C"]) <= bound
