@@ -27,9 +27,7 @@
 namespace gmp {
 
 constexpr int OZ_NS = 7;              // int8 digits per element
-constexpr int OZ_BN = 64;             // N of the MMA tile (7 x 64 TMEM columns)
-constexpr int OZ_BK = 32;             // bytes (= int8 elements) of K per stage: one MMA per term
-constexpr int OZ_STAGES = 4;
+constexpr int OZ_BN = 128;            // N of the MMA tile (= OZ2_BN)
 constexpr int OZ_THREADS = 320;       // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
 
 // ---------------------------------------------------------------------------
@@ -103,16 +101,22 @@ __global__ void __launch_bounds__(256) k_slice64(const SliceJob* __restrict__ jo
 }
 
 // ---------------------------------------------------------------------------
-// INT8 tcgen05 kernel
+// INT8 tcgen05 kernel.  M = 128, N = 128, 64-byte K blocks (SWIZZLE_64B), the
+// seven diagonals in two passes over K so that at most four int32 accumulators
+// (4 x 128 TMEM columns) are live: pass 0 = diagonals 2..5 (digits 1..4,
+// 10 terms), pass 1 = diagonals 6..8 (digits 1..7, 18 terms).  Each pass folds
+// its binary64 partial product into W (O9; the two partials differ in
+// magnitude by 2^-28, so folding twice changes W by less than 1 ulp).
 // ---------------------------------------------------------------------------
-// K-major SWIZZLE_32B canonical layout: 8-row x 32-byte atoms, SBO = 256 B.
-__device__ __forceinline__ uint64_t sdesc_k_sw32(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(256 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)6 << 61);
+constexpr int OZ2_BN = 128, OZ2_BK = 64, OZ2_STAGES = 2;
+// K-major SWIZZLE_64B canonical layout: 8-row x 64-byte atoms, SBO = 512 B.
+__device__ __forceinline__ uint64_t sdesc_k_sw64(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
 }
-// D = S32 (c_format 2), A/B signed int8 (format 1), K-major, N = 64, M = 128
+// D = S32 (c_format 2), A/B signed int8 (format 1), K-major, N = 128, M = 128
 constexpr uint32_t oz_idesc() {
-  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ2_BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
 }
 __device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                           uint32_t accumulate) {
@@ -122,31 +126,29 @@ __device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint64_t adesc, uint6
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
-constexpr int oz_smem_bytes() {
-  return OZ_STAGES * OZ_NS * (TC_BM + OZ_BN) * OZ_BK + 1024 + 256;
-}
+constexpr int OZ2_PLANE_A = TC_BM * OZ2_BK, OZ2_PLANE_B = OZ2_BN * OZ2_BK;   // 8 KB each
+constexpr int OZ2_STAGE = OZ_NS * (OZ2_PLANE_A + OZ2_PLANE_B);                 // 112 KB
+constexpr int oz_smem_bytes() { return OZ2_STAGES * OZ2_STAGE + 1024 + 256; }
 
 __global__ void __launch_bounds__(OZ_THREADS, 1)
 k_tc_fp64(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
           const WorkItem* __restrict__ items, int64_t nitems, const PairDesc* __restrict__ pairs,
           const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha,
           int64_t exp_off) {
-  constexpr int A_BYTES = TC_BM * OZ_BK, B_BYTES = OZ_BN * OZ_BK;
-  constexpr int STAGE_BYTES = OZ_NS * (A_BYTES + B_BYTES);
   constexpr uint32_t TMEM_COLS = 512;
   constexpr uint32_t IDESC = oz_idesc();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OZ_STAGES * STAGE_BYTES);
-  uint64_t* empty = full + OZ_STAGES;
-  uint64_t* tfull = empty + OZ_STAGES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OZ2_STAGES * OZ2_STAGE);
+  uint64_t* empty = full + OZ2_STAGES;
+  uint64_t* tfull = empty + OZ2_STAGES;
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
   const int16_t* __restrict__ exps = reinterpret_cast<const int16_t*>(ws + exp_off);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < OZ_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < OZ2_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(tfull, 1);
     mbar_init(tempty, TC_EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -162,27 +164,29 @@ k_tc_fp64(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int kblocks = nb / OZ_BK;
+  const int kblocks = nb / OZ2_BK;
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
-        const WorkItem w = expand_item(items, it, nb, OZ_BN);
+        const WorkItem w = expand_item(items, it, nb, OZ2_BN);
         for (int pi = 0; pi < w.pcnt; ++pi) {
           const PairDesc pd = pairs[w.pbeg + pi];
-          for (int kb = 0; kb < kblocks; ++kb) {
-            mbar_wait(&empty[stage], phase ^ 1);
-            uint8_t* sa = smem + stage * STAGE_BYTES;
-            mbar_expect_tx(&full[stage], STAGE_BYTES);
-#pragma unroll
-            for (int p = 0; p < OZ_NS; ++p) {
-              tma_load_2d(sa + p * A_BYTES, &tmA, kb * OZ_BK, (pd.a_slot * OZ_NS + p) * nb + w.m0, &full[stage]);
-              tma_load_2d(sa + OZ_NS * A_BYTES + p * B_BYTES, &tmB, kb * OZ_BK, (pd.b_slot * OZ_NS + p) * nb + w.n0,
-                          &full[stage]);
+          for (int pass = 0; pass < 2; ++pass) {
+            const int npl = pass ? OZ_NS : 4;
+            for (int kb = 0; kb < kblocks; ++kb) {
+              mbar_wait(&empty[stage], phase ^ 1);
+              uint8_t* sa = smem + stage * OZ2_STAGE;
+              mbar_expect_tx(&full[stage], (uint32_t)(npl * (OZ2_PLANE_A + OZ2_PLANE_B)));
+              for (int p = 0; p < npl; ++p) {
+                tma_load_2d(sa + p * OZ2_PLANE_A, &tmA, kb * OZ2_BK, (pd.a_slot * OZ_NS + p) * nb + w.m0, &full[stage]);
+                tma_load_2d(sa + OZ_NS * OZ2_PLANE_A + p * OZ2_PLANE_B, &tmB, kb * OZ2_BK,
+                            (pd.b_slot * OZ_NS + p) * nb + w.n0, &full[stage]);
+              }
+              if (++stage == OZ2_STAGES) { stage = 0; phase ^= 1; }
             }
-            if (++stage == OZ_STAGES) { stage = 0; phase ^= 1; }
           }
         }
       }
@@ -192,91 +196,100 @@ k_tc_fp64(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       int stage = 0;
       uint32_t phase = 0, acc_phase = 0;
       for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
-        const WorkItem w = expand_item(items, it, nb, OZ_BN);
+        const WorkItem w = expand_item(items, it, nb, OZ2_BN);
         for (int pi = 0; pi < w.pcnt; ++pi) {
-          mbar_wait(tempty, acc_phase ^ 1);
-          tc_fence_after();
-          for (int kb = 0; kb < kblocks; ++kb) {
-            mbar_wait(&full[stage], phase);
+          for (int pass = 0; pass < 2; ++pass) {
+            const int dlo = pass ? 6 : 2, dhi = pass ? OZ_NS + 1 : 5;
+            mbar_wait(tempty, acc_phase ^ 1);
             tc_fence_after();
-            const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
-            // diagonal d = i + j (digits 1-based): accumulator column block d - 2
+            for (int kb = 0; kb < kblocks; ++kb) {
+              mbar_wait(&full[stage], phase);
+              tc_fence_after();
+              const uint32_t sa = smem_u32(smem + stage * OZ2_STAGE);
+              for (int d = dhi; d >= dlo; --d) {           // smallest diagonal first
+                const uint32_t d_tmem = tmem_base + (uint32_t)((d - dlo) * OZ2_BN);
+                for (int i = 1; i < d; ++i) {
+                  const int j = d - i;
+                  if (i > OZ_NS || j > OZ_NS) continue;
+                  const uint64_t ad = sdesc_k_sw64(sa + (i - 1) * OZ2_PLANE_A);
+                  const uint64_t bd = sdesc_k_sw64(sa + OZ_NS * OZ2_PLANE_A + (j - 1) * OZ2_PLANE_B);
+                  const bool first = (kb == 0) && (i == 1 || (d - (OZ_NS) > 1 && i == d - OZ_NS));
 #pragma unroll
-            for (int d = OZ_NS + 1; d >= 2; --d) {
-              const uint32_t d_tmem = tmem_base + (uint32_t)((d - 2) * OZ_BN);
-#pragma unroll
-              for (int i = 1; i < d; ++i) {
-                const int j = d - i;
-                const uint64_t ad = sdesc_k_sw32(sa + (i - 1) * A_BYTES);
-                const uint64_t bd = sdesc_k_sw32(sa + OZ_NS * A_BYTES + (j - 1) * B_BYTES);
-                tc_mma_i8(d_tmem, ad, bd, IDESC, (kb != 0 || i != 1) ? 1u : 0u);
+                  for (int k = 0; k < OZ2_BK / 32; ++k)
+                    tc_mma_i8(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), IDESC,
+                              (first && k == 0) ? 0u : 1u);
+                }
               }
+              tc_commit(&empty[stage]);
+              if (++stage == OZ2_STAGES) { stage = 0; phase ^= 1; }
             }
-            tc_commit(&empty[stage]);
-            if (++stage == OZ_STAGES) { stage = 0; phase ^= 1; }
+            tc_commit(tfull);
+            acc_phase ^= 1;
           }
-          tc_commit(tfull);
-          acc_phase ^= 1;
         }
       }
     }
   } else {
     // epilogue: warp w reads TMEM lanes 32*(w%4)..+31 (tile rows) and half (w-2)/4
-    // of the 64 columns (32 each, two 16-column chunks)
+    // of the 128 columns (64 each, four 16-column chunks)
     const int quarter = warp & 3, half = (warp - 2) >> 2;
     const int rloc = quarter * 32 + lane;
     uint32_t acc_phase = 0;
     for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
-      const WorkItem w = expand_item(items, it, nb, OZ_BN);
+      const WorkItem w = expand_item(items, it, nb, OZ2_BN);
       const CTileDesc ct = ctiles[w.ctile];
-      const int64_t rowoff = (int64_t)(w.m0 + rloc) * nb + w.n0 + half * 32;
+      const int64_t rowoff = (int64_t)(w.m0 + rloc) * nb + w.n0 + half * 64;
       for (int pi = 0; pi < w.pcnt; ++pi) {
         const PairDesc pd = pairs[w.pbeg + pi];
         const double f64 = ldexp(alpha, pd.fexp);
         const float f32 = __double2float_rn(f64);
         const int er = exps[(int64_t)pd.a_slot * nb + w.m0 + rloc];
-        const int16_t* fcol = exps + (int64_t)pd.b_slot * nb + w.n0 + half * 32;
-        mbar_wait(tfull, acc_phase);
-        tc_fence_after();
-        const uint32_t tq = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(half * 32);
+        const int16_t* fcol = exps + (int64_t)pd.b_slot * nb + w.n0 + half * 64;
+        for (int pass = 0; pass < 2; ++pass) {
+          const int dlo = pass ? 6 : 2, dhi = pass ? OZ_NS + 1 : 5;
+          mbar_wait(tfull, acc_phase);
+          tc_fence_after();
+          const uint32_t tq = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(half * 64);
 #pragma unroll 1
-        for (int ch = 0; ch < 2; ++ch) {
-          double p[16];
+          for (int ch = 0; ch < 4; ++ch) {
+            double p[16];
 #pragma unroll
-          for (int v = 0; v < 16; ++v) p[v] = 0.0;
+            for (int v = 0; v < 16; ++v) p[v] = 0.0;
+            for (int d = dhi; d >= dlo; --d) {             // smallest diagonal first
+              uint32_t r[16];
+              tmem_ld16_nowait(tq + (uint32_t)((d - dlo) * OZ2_BN + ch * 16), r);
+              tmem_wait_ld();
+              const double sc = __longlong_as_double((long long)(1023 - 7 * d) << 52);   // 2^-7d
 #pragma unroll
-          for (int d = OZ_NS + 1; d >= 2; --d) {      // smallest diagonal first
-            uint32_t r[16];
-            tmem_ld16_nowait(tq + (uint32_t)((d - 2) * OZ_BN + ch * 16), r);
-            tmem_wait_ld();
-            const double sc = ldexp(1.0, -7 * d);
-#pragma unroll
-            for (int v = 0; v < 16; ++v) p[v] = __fma_rn((double)(int32_t)r[v], sc, p[v]);
-          }
-          if (ct.code == 0) {
-            double* wp = reinterpret_cast<double*>(ws + ct.w_off) + rowoff + ch * 16;
-#pragma unroll
-            for (int v = 0; v < 16; v += 2) {
-              double2 x = *reinterpret_cast<double2*>(wp + v);
-              x.x = __fma_rn(f64, ldexp(p[v], er + fcol[ch * 16 + v]), x.x);
-              x.y = __fma_rn(f64, ldexp(p[v + 1], er + fcol[ch * 16 + v + 1]), x.y);
-              *reinterpret_cast<double2*>(wp + v) = x;
+              for (int v = 0; v < 16; ++v) p[v] = __fma_rn((double)(int32_t)r[v], sc, p[v]);
             }
-          } else {
-            float* wp = reinterpret_cast<float*>(ws + ct.w_off) + rowoff + ch * 16;
+            // 2^(e_r + f_c) as exact power-of-two factors (ldexp keeps the rare
+            // out-of-range exponents correct)
+            if (ct.code == 0) {
+              double* wp = reinterpret_cast<double*>(ws + ct.w_off) + rowoff + ch * 16;
 #pragma unroll
-            for (int v = 0; v < 16; v += 2) {
-              float2 x = *reinterpret_cast<float2*>(wp + v);
-              x.x = __fmaf_rn(f32, __double2float_rn(ldexp(p[v], er + fcol[ch * 16 + v])), x.x);
-              x.y = __fmaf_rn(f32, __double2float_rn(ldexp(p[v + 1], er + fcol[ch * 16 + v + 1])), x.y);
-              *reinterpret_cast<float2*>(wp + v) = x;
+              for (int v = 0; v < 16; v += 2) {
+                double2 x = *reinterpret_cast<double2*>(wp + v);
+                x.x = __fma_rn(f64, ldexp(p[v], er + fcol[ch * 16 + v]), x.x);
+                x.y = __fma_rn(f64, ldexp(p[v + 1], er + fcol[ch * 16 + v + 1]), x.y);
+                *reinterpret_cast<double2*>(wp + v) = x;
+              }
+            } else {
+              float* wp = reinterpret_cast<float*>(ws + ct.w_off) + rowoff + ch * 16;
+#pragma unroll
+              for (int v = 0; v < 16; v += 2) {
+                float2 x = *reinterpret_cast<float2*>(wp + v);
+                x.x = __fmaf_rn(f32, __double2float_rn(ldexp(p[v], er + fcol[ch * 16 + v])), x.x);
+                x.y = __fmaf_rn(f32, __double2float_rn(ldexp(p[v + 1], er + fcol[ch * 16 + v + 1])), x.y);
+                *reinterpret_cast<float2*>(wp + v) = x;
+              }
             }
           }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(tempty);
+          acc_phase ^= 1;
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(tempty);
-        acc_phase ^= 1;
       }
     }
   }
@@ -301,14 +314,14 @@ inline gmp_status_t oz_prepare(OzTables& t, uint8_t* ws, int64_t arena_off, int6
   cuuint64_t dims[2] = {(cuuint64_t)nb, (cuuint64_t)(slots * OZ_NS * nb)};
   cuuint64_t strides[1] = {(cuuint64_t)nb};
   cuuint32_t estr[2] = {1, 1};
-  cuuint32_t boxA[2] = {(cuuint32_t)OZ_BK, (cuuint32_t)TC_BM};
-  cuuint32_t boxB[2] = {(cuuint32_t)OZ_BK, (cuuint32_t)OZ_BN};
+  cuuint32_t boxA[2] = {(cuuint32_t)OZ2_BK, (cuuint32_t)TC_BM};
+  cuuint32_t boxB[2] = {(cuuint32_t)OZ2_BK, (cuuint32_t)OZ2_BN};
   if (enc(&t.mapA, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, ws + arena_off, dims, strides, boxA, estr,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return GMP_ERR_CUDA;
   if (enc(&t.mapB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, ws + arena_off, dims, strides, boxB, estr,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return GMP_ERR_CUDA;
   t.ready = true;
