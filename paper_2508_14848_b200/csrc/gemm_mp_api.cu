@@ -903,8 +903,8 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
       const PairDesc* pd = (const PairDesc*)(ws + pl->off_pairs);
       if (!pl->launch_ev.empty()) GMP_CUDA(cudaEventRecord(pl->launch_ev[2 * li], stream));
       if (L.kind == 4) {
-        if (oz_launch(pl->oz, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, pl->off_oexp, stream) != GMP_OK)
-          return fail(GMP_ERR_CUDA, std::string("k_tc_fp64 launch: ") + cudaGetErrorString(cudaGetLastError()));
+        const cudaError_t e = oz_launch(pl->oz, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, pl->off_oexp, stream);
+        if (e != cudaSuccess) return fail(GMP_ERR_CUDA, std::string("k_tc_fp64 launch: ") + cudaGetErrorString(e));
       } else if (L.kind == 1 || L.kind == 3) {
         GMP_TRY(tc_launch(pl->tc, L.kind == 3 ? 5 : L.cls, L.bn, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha,
                           stream));

@@ -1,11 +1,10 @@
-// gmp_ozaki.cuh -- EXPERIMENTAL: the FP64 class on the INT8 tensor pipe (Ozaki-
-// style error-free slicing + tcgen05.mma kind::i8), opt-in with
-// GMP_FLAG_FP64_INT8 (the product FP64 path is k_dmma).  Correct (tested to the
-// 1e-13 FP64 parity bound) but currently ~3x slower than DMMA on B200: the
-// seven 32-byte-wide digit planes per operand make every TMA box a stream of
-// 32-byte row segments (1344 per stage) and the seven int32 diagonal
-// accumulators cap N at 64, so the tensor pipe idles (ncu: 7 % active, 56 % L2
-// hit).  DESIGN.md section 10 lists the layout change this needs.
+// gmp_ozaki.cuh -- OPT-IN: the FP64 class on the INT8 tensor pipe (Ozaki-style
+// error-free slicing + tcgen05.mma kind::i8), enabled with GMP_FLAG_FP64_INT8.
+// The product FP64 path stays k_dmma (binary64 arithmetic, as north_star and the
+// paper's FP64 class specify); this path reaches binary64-level NORMWISE accuracy
+// (tested to the 1e-13 FP64 parity bound) but not DGEMM's componentwise bound.
+// Measured on B200 (profiles/ozaki_r01.md): all-FP64 cfg2 61 TFLOP/s vs 32.6
+// for DMMA; mixed cfg2 execute 70 ms vs 94 ms.
 //
 // Slicing (k_slice64, receiver-side from the stored binary64 payload): for each
 // K-major operand row r (A: tile row, B: tile column) with e_r the frexp
@@ -19,16 +18,17 @@
 // are below 2^-48 of |A||B| row/column scales: binary64-level normwise accuracy
 // (parity bound 1e-13).  The seven diagonal accumulators
 // live in TMEM (7 x 64 int32 columns); the epilogue combines them in binary64,
-// smallest first, applies the two power-of-two row/column scales and folds
-// (O9).
+// smallest first, applies the two power-of-two row/column scales and folds into
+// the register-resident W row segment (O9).
 #pragma once
 #include "gmp_tc.cuh"
 
 namespace gmp {
 
 constexpr int OZ_NS = 7;              // int8 digits per element
-constexpr int OZ_BN = 128;            // N of the MMA tile (= OZ2_BN)
+constexpr int OZ_BN = 64;             // N of the MMA tile (= OZ2_BN)
 constexpr int OZ_THREADS = 320;       // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
+constexpr int OZ_EPI_WARPS = 8;       // 2 per TMEM lane quarter, 32 columns each
 
 // ---------------------------------------------------------------------------
 // slicing kernel: one job = one tile (MN-major binary64 payload -> NS K-major
@@ -101,20 +101,19 @@ __global__ void __launch_bounds__(256) k_slice64(const SliceJob* __restrict__ jo
 }
 
 // ---------------------------------------------------------------------------
-// INT8 tcgen05 kernel.  M = 128, N = 128, 64-byte K blocks (SWIZZLE_64B), the
-// seven diagonals in two passes over K so that at most four int32 accumulators
-// (4 x 128 TMEM columns) are live: pass 0 = diagonals 2..5 (digits 1..4,
-// 10 terms), pass 1 = diagonals 6..8 (digits 1..7, 18 terms).  Each pass folds
-// its binary64 partial product into W (O9; the two partials differ in
-// magnitude by 2^-28, so folding twice changes W by less than 1 ulp).
+// INT8 tcgen05 kernel.  M = 128, N = 64, 64-byte K blocks (SWIZZLE_64B), all
+// seven diagonal accumulators live in TMEM (7 x 64 int32 columns), one pass
+// over K per pair (each digit plane is read once).  The epilogue keeps its W row
+// segment in registers for the whole item and folds each pair's binary64
+// product into it (O9).
 // ---------------------------------------------------------------------------
-constexpr int OZ2_BN = 128, OZ2_BK = 64, OZ2_STAGES = 2;
+constexpr int OZ2_BN = 64, OZ2_BK = 64, OZ2_STAGES = 2;
 // K-major SWIZZLE_64B canonical layout: 8-row x 64-byte atoms, SBO = 512 B.
 __device__ __forceinline__ uint64_t sdesc_k_sw64(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
 }
-// D = S32 (c_format 2), A/B signed int8 (format 1), K-major, N = 128, M = 128
+// D = S32 (c_format 2), A/B signed int8 (format 1), K-major, N = 64, M = 128
 constexpr uint32_t oz_idesc() {
   return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ2_BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
 }
@@ -124,6 +123,16 @@ __device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint64_t adesc, uint6
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void tmem_ld8_nowait(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+__device__ __noinline__ double pow2_scale_slow(double x, int e) { return ldexp(x, e); }
+__device__ __forceinline__ double pow2_scale(double x, int e) {
+  return (e > -1000 && e < 1000) ? x * __longlong_as_double((long long)(1023 + e) << 52) : pow2_scale_slow(x, e);
 }
 
 constexpr int OZ2_PLANE_A = TC_BM * OZ2_BK, OZ2_PLANE_B = OZ2_BN * OZ2_BK;   // 8 KB each
@@ -150,7 +159,7 @@ k_tc_fp64(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < OZ2_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(tfull, 1);
-    mbar_init(tempty, TC_EPI_WARPS);
+    mbar_init(tempty, OZ_EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
@@ -174,19 +183,16 @@ k_tc_fp64(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         const WorkItem w = expand_item(items, it, nb, OZ2_BN);
         for (int pi = 0; pi < w.pcnt; ++pi) {
           const PairDesc pd = pairs[w.pbeg + pi];
-          for (int pass = 0; pass < 2; ++pass) {
-            const int npl = pass ? OZ_NS : 4;
-            for (int kb = 0; kb < kblocks; ++kb) {
-              mbar_wait(&empty[stage], phase ^ 1);
-              uint8_t* sa = smem + stage * OZ2_STAGE;
-              mbar_expect_tx(&full[stage], (uint32_t)(npl * (OZ2_PLANE_A + OZ2_PLANE_B)));
-              for (int p = 0; p < npl; ++p) {
-                tma_load_2d(sa + p * OZ2_PLANE_A, &tmA, kb * OZ2_BK, (pd.a_slot * OZ_NS + p) * nb + w.m0, &full[stage]);
-                tma_load_2d(sa + OZ_NS * OZ2_PLANE_A + p * OZ2_PLANE_B, &tmB, kb * OZ2_BK,
-                            (pd.b_slot * OZ_NS + p) * nb + w.n0, &full[stage]);
-              }
-              if (++stage == OZ2_STAGES) { stage = 0; phase ^= 1; }
+          for (int kb = 0; kb < kblocks; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* sa = smem + stage * OZ2_STAGE;
+            mbar_expect_tx(&full[stage], (uint32_t)OZ2_STAGE);
+            for (int p = 0; p < OZ_NS; ++p) {
+              tma_load_2d(sa + p * OZ2_PLANE_A, &tmA, kb * OZ2_BK, (pd.a_slot * OZ_NS + p) * nb + w.m0, &full[stage]);
+              tma_load_2d(sa + OZ_NS * OZ2_PLANE_A + p * OZ2_PLANE_B, &tmB, kb * OZ2_BK,
+                          (pd.b_slot * OZ_NS + p) * nb + w.n0, &full[stage]);
             }
+            if (++stage == OZ2_STAGES) { stage = 0; phase ^= 1; }
           }
         }
       }
@@ -198,98 +204,105 @@ k_tc_fp64(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
         const WorkItem w = expand_item(items, it, nb, OZ2_BN);
         for (int pi = 0; pi < w.pcnt; ++pi) {
-          for (int pass = 0; pass < 2; ++pass) {
-            const int dlo = pass ? 6 : 2, dhi = pass ? OZ_NS + 1 : 5;
-            mbar_wait(tempty, acc_phase ^ 1);
+          mbar_wait(tempty, acc_phase ^ 1);
+          tc_fence_after();
+          for (int kb = 0; kb < kblocks; ++kb) {
+            mbar_wait(&full[stage], phase);
             tc_fence_after();
-            for (int kb = 0; kb < kblocks; ++kb) {
-              mbar_wait(&full[stage], phase);
-              tc_fence_after();
-              const uint32_t sa = smem_u32(smem + stage * OZ2_STAGE);
-              for (int d = dhi; d >= dlo; --d) {           // smallest diagonal first
-                const uint32_t d_tmem = tmem_base + (uint32_t)((d - dlo) * OZ2_BN);
-                for (int i = 1; i < d; ++i) {
-                  const int j = d - i;
-                  if (i > OZ_NS || j > OZ_NS) continue;
-                  const uint64_t ad = sdesc_k_sw64(sa + (i - 1) * OZ2_PLANE_A);
-                  const uint64_t bd = sdesc_k_sw64(sa + OZ_NS * OZ2_PLANE_A + (j - 1) * OZ2_PLANE_B);
-                  const bool first = (kb == 0) && (i == 1 || (d - (OZ_NS) > 1 && i == d - OZ_NS));
+            const uint32_t sa = smem_u32(smem + stage * OZ2_STAGE);
+            for (int d = OZ_NS + 1; d >= 2; --d) {           // smallest diagonal first
+              const uint32_t d_tmem = tmem_base + (uint32_t)((d - 2) * OZ2_BN);
+              for (int i = 1; i < d; ++i) {
+                const int j = d - i;
+                const uint64_t ad = sdesc_k_sw64(sa + (i - 1) * OZ2_PLANE_A);
+                const uint64_t bd = sdesc_k_sw64(sa + OZ_NS * OZ2_PLANE_A + (j - 1) * OZ2_PLANE_B);
 #pragma unroll
-                  for (int k = 0; k < OZ2_BK / 32; ++k)
-                    tc_mma_i8(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), IDESC,
-                              (first && k == 0) ? 0u : 1u);
-                }
+                for (int k = 0; k < OZ2_BK / 32; ++k)
+                  tc_mma_i8(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), IDESC,
+                            (kb == 0 && i == 1 && k == 0) ? 0u : 1u);
               }
-              tc_commit(&empty[stage]);
-              if (++stage == OZ2_STAGES) { stage = 0; phase ^= 1; }
             }
-            tc_commit(tfull);
-            acc_phase ^= 1;
+            tc_commit(&empty[stage]);
+            if (++stage == OZ2_STAGES) { stage = 0; phase ^= 1; }
           }
+          tc_commit(tfull);
+          acc_phase ^= 1;
         }
       }
     }
   } else {
-    // epilogue: warp w reads TMEM lanes 32*(w%4)..+31 (tile rows) and half (w-2)/4
-    // of the 128 columns (64 each, four 16-column chunks)
-    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    // epilogue: 8 warps; warp w reads TMEM lanes 32*(w%4)..+31 (tile rows) and
+    // column group (w-2)/4 (32 columns, four 8-column chunks).  The thread's W row
+    // segment (32 binary64 or binary32 values) stays in registers for the whole
+    // item: one W read and one W write per item instead of two per pair.
+    const int quarter = warp & 3, cg = (warp - 2) >> 2;
     const int rloc = quarter * 32 + lane;
     uint32_t acc_phase = 0;
     for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
       const WorkItem w = expand_item(items, it, nb, OZ2_BN);
       const CTileDesc ct = ctiles[w.ctile];
-      const int64_t rowoff = (int64_t)(w.m0 + rloc) * nb + w.n0 + half * 64;
+      const int64_t rowoff = (int64_t)(w.m0 + rloc) * nb + w.n0 + cg * 32;
+      const bool w64 = ct.code == 0;
+      double accd[32];
+      if (w64) {
+#pragma unroll
+        for (int v = 0; v < 16; ++v) {
+          const double2 x = reinterpret_cast<const double2*>(reinterpret_cast<const double*>(ws + ct.w_off) + rowoff)[v];
+          accd[2 * v] = x.x; accd[2 * v + 1] = x.y;
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const float4 x = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(ws + ct.w_off) + rowoff)[v];
+          accd[4 * v] = x.x; accd[4 * v + 1] = x.y; accd[4 * v + 2] = x.z; accd[4 * v + 3] = x.w;
+        }
+      }
       for (int pi = 0; pi < w.pcnt; ++pi) {
         const PairDesc pd = pairs[w.pbeg + pi];
         const double f64 = ldexp(alpha, pd.fexp);
         const float f32 = __double2float_rn(f64);
         const int er = exps[(int64_t)pd.a_slot * nb + w.m0 + rloc];
-        const int16_t* fcol = exps + (int64_t)pd.b_slot * nb + w.n0 + half * 64;
-        for (int pass = 0; pass < 2; ++pass) {
-          const int dlo = pass ? 6 : 2, dhi = pass ? OZ_NS + 1 : 5;
-          mbar_wait(tfull, acc_phase);
-          tc_fence_after();
-          const uint32_t tq = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(half * 64);
+        const int16_t* fcol = exps + (int64_t)pd.b_slot * nb + w.n0 + cg * 32;
+        mbar_wait(tfull, acc_phase);
+        tc_fence_after();
+        const uint32_t tq = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(cg * 32);
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {                   // four 8-column chunks
+          double p[8];
+#pragma unroll
+          for (int v = 0; v < 8; ++v) p[v] = 0.0;
 #pragma unroll 1
-          for (int ch = 0; ch < 4; ++ch) {
-            double p[16];
+          for (int d = OZ_NS + 1; d >= 2; --d) {           // smallest diagonal first
+            uint32_t r[8];
+            tmem_ld8_nowait(tq + (uint32_t)((d - 2) * OZ2_BN + ch * 8), r);
+            tmem_wait_ld();
+            const double sc = __longlong_as_double((long long)(1023 - 7 * d) << 52);   // 2^-7d
 #pragma unroll
-            for (int v = 0; v < 16; ++v) p[v] = 0.0;
-            for (int d = dhi; d >= dlo; --d) {             // smallest diagonal first
-              uint32_t r[16];
-              tmem_ld16_nowait(tq + (uint32_t)((d - dlo) * OZ2_BN + ch * 16), r);
-              tmem_wait_ld();
-              const double sc = __longlong_as_double((long long)(1023 - 7 * d) << 52);   // 2^-7d
-#pragma unroll
-              for (int v = 0; v < 16; ++v) p[v] = __fma_rn((double)(int32_t)r[v], sc, p[v]);
-            }
-            // 2^(e_r + f_c) as exact power-of-two factors (ldexp keeps the rare
-            // out-of-range exponents correct)
-            if (ct.code == 0) {
-              double* wp = reinterpret_cast<double*>(ws + ct.w_off) + rowoff + ch * 16;
-#pragma unroll
-              for (int v = 0; v < 16; v += 2) {
-                double2 x = *reinterpret_cast<double2*>(wp + v);
-                x.x = __fma_rn(f64, ldexp(p[v], er + fcol[ch * 16 + v]), x.x);
-                x.y = __fma_rn(f64, ldexp(p[v + 1], er + fcol[ch * 16 + v + 1]), x.y);
-                *reinterpret_cast<double2*>(wp + v) = x;
-              }
-            } else {
-              float* wp = reinterpret_cast<float*>(ws + ct.w_off) + rowoff + ch * 16;
-#pragma unroll
-              for (int v = 0; v < 16; v += 2) {
-                float2 x = *reinterpret_cast<float2*>(wp + v);
-                x.x = __fmaf_rn(f32, __double2float_rn(ldexp(p[v], er + fcol[ch * 16 + v])), x.x);
-                x.y = __fmaf_rn(f32, __double2float_rn(ldexp(p[v + 1], er + fcol[ch * 16 + v + 1])), x.y);
-                *reinterpret_cast<float2*>(wp + v) = x;
-              }
-            }
+            for (int v = 0; v < 8; ++v) p[v] = __fma_rn((double)(int32_t)r[v], sc, p[v]);
           }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(tempty);
-          acc_phase ^= 1;
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            // P = p 2^(e_r + f_c): exact power-of-two scaling
+            const double P = pow2_scale(p[v], er + fcol[ch * 8 + v]);
+            if (w64) accd[ch * 8 + v] = __fma_rn(f64, P, accd[ch * 8 + v]);
+            else accd[ch * 8 + v] = (double)__fmaf_rn(f32, __double2float_rn(P), (float)accd[ch * 8 + v]);
+          }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty);
+        acc_phase ^= 1;
+      }
+      if (w64) {
+#pragma unroll
+        for (int v = 0; v < 16; ++v)
+          reinterpret_cast<double2*>(reinterpret_cast<double*>(ws + ct.w_off) + rowoff)[v] =
+              make_double2(accd[2 * v], accd[2 * v + 1]);
+      } else {
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          reinterpret_cast<float4*>(reinterpret_cast<float*>(ws + ct.w_off) + rowoff)[v] =
+              make_float4((float)accd[4 * v], (float)accd[4 * v + 1], (float)accd[4 * v + 2], (float)accd[4 * v + 3]);
       }
     }
   }
@@ -328,20 +341,20 @@ inline gmp_status_t oz_prepare(OzTables& t, uint8_t* ws, int64_t arena_off, int6
   return GMP_OK;
 }
 
-inline gmp_status_t oz_launch(OzTables& t, const WorkItem* it, int64_t n, const PairDesc* pd, const CTileDesc* ct,
-                              uint8_t* ws, int nb, double alpha, int64_t exp_off, cudaStream_t s) {
-  if (!t.ready) return GMP_ERR_STATE;
+inline cudaError_t oz_launch(OzTables& t, const WorkItem* it, int64_t n, const PairDesc* pd, const CTileDesc* ct,
+                             uint8_t* ws, int nb, double alpha, int64_t exp_off, cudaStream_t s) {
+  if (!t.ready) return cudaErrorNotReady;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(k_tc_fp64, cudaFuncAttributeMaxDynamicSharedMemorySize, oz_smem_bytes()) != cudaSuccess)
-      return GMP_ERR_CUDA;
+    const cudaError_t e = cudaFuncSetAttribute(k_tc_fp64, cudaFuncAttributeMaxDynamicSharedMemorySize, oz_smem_bytes());
+    if (e != cudaSuccess) return e;
     attr = true;
   }
   // one CTA per (item, sub-tile), scheduled in flat order: the CTAs of one C
   // tile run together and walk its pair list in step (L2 reuse of the planes)
   const int grid = (int)n;
   k_tc_fp64<<<grid, OZ_THREADS, oz_smem_bytes(), s>>>(t.mapA, t.mapB, it, n, pd, ct, ws, nb, alpha, exp_off);
-  return cudaGetLastError() == cudaSuccess ? GMP_OK : GMP_ERR_CUDA;
+  return cudaGetLastError();
 }
 
 }  // namespace gmp
