@@ -398,7 +398,10 @@ def main():
         kname = {0: "k_dmma<32>", 1: "k_tc_class<5, 128>", 2: "k_tc_class<2, 128>", 3: "k_tc_class<3, 256>",
                  4: "k_tc_class<4, 256>"}[dom]
         with open(os.path.join(ROOT, "profiles", "traffic_r01.json")) as f:
-            traffic = json.load(f)["kernels"].get(kname)
+            tr = json.load(f)
+        # per-launch bytes only describe the captured launch configuration
+        if tr.get("workload") == w.name and tr.get("n_gpus") == G:
+            traffic = tr["kernels"].get(kname)
     except Exception:
         traffic = None
     launches = st["launches_plan"] + st["launches_convert"] + st["launches_execute"]
