@@ -58,9 +58,15 @@ __device__ __forceinline__ void store8(uint8_t* dst, const double* v) {
   }
 }
 
+// 64x64 binary64 staging block, XOR-swizzled instead of padded: element (r, c)
+// lives at r*64 + (c ^ 2*((r >> 3) & 7)).  Row-wise double2 writes stay
+// contiguous, and the transposed reads (8 row groups x 2 columns per half-warp)
+// hit 16 distinct 8-byte bank pairs.
+__device__ __forceinline__ int sw64(int r, int c) { return r * 64 + (c ^ (((r >> 3) & 7) << 1)); }
+
 template <int C>
 __device__ __forceinline__ void pack_block(const PackJob& j, uint8_t* ws, int nb, int r0, int c0,
-                                           double (*sm)[65]) {
+                                           double* sm) {
   const int t = threadIdx.x;
   constexpr int B = class_bytes(C);
   uint8_t* dst = ws + j.dst_off;
@@ -86,9 +92,8 @@ __device__ __forceinline__ void pack_block(const PackJob& j, uint8_t* ws, int nb
     for (int u = 0; u < 8; ++u) {
       int unit = t + u * 256;           // 64 rows x 32 double2
       int r = unit >> 5, q = unit & 31;
-      double2 x = __ldg(reinterpret_cast<const double2*>(j.src + (int64_t)(r0 + r) * j.ld + c0 + 2 * q));
-      sm[r][2 * q] = x.x;
-      sm[r][2 * q + 1] = x.y;
+      const double2 x = __ldg(reinterpret_cast<const double2*>(j.src + (int64_t)(r0 + r) * j.ld + c0 + 2 * q));
+      *reinterpret_cast<double2*>(sm + sw64(r, 2 * q)) = x;
     }
     __syncthreads();
 #pragma unroll
@@ -98,7 +103,7 @@ __device__ __forceinline__ void pack_block(const PackJob& j, uint8_t* ws, int nb
       double v[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        double x = sm[g * 8 + i][oc];
+        const double x = sm[sw64(g * 8 + i, oc)];
         v[i] = (C == 0) ? x : ldexp(x, j.scale);
       }
       store8<C>(dst + ((int64_t)(c0 + oc) * nb + r0 + g * 8) * B, v);
@@ -107,7 +112,7 @@ __device__ __forceinline__ void pack_block(const PackJob& j, uint8_t* ws, int nb
 }
 
 __global__ void __launch_bounds__(256) k_pack(const PackJob* __restrict__ jobs, uint8_t* ws, int nb) {
-  __shared__ double sm[64][65];
+  __shared__ __align__(16) double sm[64 * 64];
   const PackJob j = jobs[blockIdx.y];
   const int per = nb / 64;
   const int r0 = (blockIdx.x / per) * 64, c0 = (blockIdx.x % per) * 64;
@@ -164,7 +169,7 @@ __global__ void __launch_bounds__(256) k_shadow(const ShadowJob* __restrict__ jo
 // once into the target class and written transposed.
 template <int F, int T>
 __device__ __forceinline__ void shadow_t_block(const ShadowJob& j, uint8_t* ws, int nb, int r0, int c0,
-                                               double (*sm)[65]) {
+                                               double* sm) {
   const int t = threadIdx.x;
   const uint8_t* src = ws + j.src_off;
   uint8_t* dst = ws + j.dst_off;
@@ -172,7 +177,7 @@ __device__ __forceinline__ void shadow_t_block(const ShadowJob& j, uint8_t* ws, 
   for (int u = 0; u < 16; ++u) {
     const int unit = t + u * 256;  // 64 rows x 64 cols
     const int r = unit >> 6, c = unit & 63;
-    sm[r][c] = ldexp(payload_f64(src, (int64_t)(r0 + r) * nb + c0 + c, F), j.d);
+    sm[sw64(r, c)] = ldexp(payload_f64(src, (int64_t)(r0 + r) * nb + c0 + c, F), j.d);
   }
   __syncthreads();
 #pragma unroll
@@ -181,13 +186,13 @@ __device__ __forceinline__ void shadow_t_block(const ShadowJob& j, uint8_t* ws, 
     const int oc = unit >> 3, gq = unit & 7;
     double v[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = sm[gq * 8 + i][oc];
+    for (int i = 0; i < 8; ++i) v[i] = sm[sw64(gq * 8 + i, oc)];
     store8<T>(dst + ((int64_t)(c0 + oc) * nb + r0 + gq * 8) * class_bytes(T), v);
   }
 }
 
 __global__ void __launch_bounds__(256) k_shadow_t(const ShadowJob* __restrict__ jobs, uint8_t* ws, int nb) {
-  __shared__ double sm[64][65];
+  __shared__ __align__(16) double sm[64 * 64];
   const ShadowJob j = jobs[blockIdx.y];
   const int per = nb / 64;
   const int r0 = (blockIdx.x / per) * 64, c0 = (blockIdx.x % per) * 64;
@@ -212,35 +217,46 @@ struct SplitJob {
 };
 
 __global__ void __launch_bounds__(256) k_split(const SplitJob* __restrict__ jobs, uint8_t* ws, int nb) {
-  __shared__ float sm[64][65];
+  // 64x64 binary32 block, element (r, c) at r*64 + (c ^ 4*((r >> 3) & 7)):
+  // row-wise writes and the transposed 8-row reads are both conflict-free
+  __shared__ float sm[64 * 64];
   const SplitJob j = jobs[blockIdx.y];
   const int per = nb / 64;
   const int r0 = (blockIdx.x / per) * 64, c0 = (blockIdx.x % per) * 64;
   const float* src = reinterpret_cast<const float*>(ws + j.src_off);
-  uint16_t* dst = reinterpret_cast<uint16_t*>(ws + j.dst_off);
-  const int64_t part = (int64_t)nb * nb;
+  uint8_t* dst = ws + j.dst_off;
+  const int64_t part = (int64_t)nb * nb * 2;   // bytes per BF16 part
   const int t = threadIdx.x;
 #pragma unroll
-  for (int u = 0; u < 16; ++u) {
-    const int unit = t + u * 256;
-    const int r = unit >> 6, c = unit & 63;
-    sm[r][c] = src[(int64_t)(r0 + r) * nb + c0 + c];
+  for (int u = 0; u < 4; ++u) {
+    const int unit = t + u * 256;              // 64 rows x 16 float4
+    const int r = unit >> 4, q = unit & 15;
+    const float4 x = *reinterpret_cast<const float4*>(src + (int64_t)(r0 + r) * nb + c0 + 4 * q);
+    *reinterpret_cast<float4*>(sm + r * 64 + ((4 * q) ^ (((r >> 3) & 7) << 2))) = x;
   }
   __syncthreads();
 #pragma unroll
-  for (int u = 0; u < 16; ++u) {
+  for (int u = 0; u < 2; ++u) {
     const int unit = t + u * 256;
-    const int oc = unit >> 6, orr = unit & 63;   // output row oc (= source col), element orr
-    const float x = sm[orr][oc];
-    const uint16_t h0 = cvt_bf16_rn((double)x);
-    const float r1 = __fsub_rn(x, bf16_to_f32(h0));
-    const uint16_t h1 = cvt_bf16_rn((double)r1);
-    const float r2 = __fsub_rn(r1, bf16_to_f32(h1));
-    const uint16_t h2 = cvt_bf16_rn((double)r2);
-    const int64_t o = (int64_t)(c0 + oc) * nb + r0 + orr;
-    dst[o] = h0;
-    dst[part + o] = h1;
-    dst[2 * part + o] = h2;
+    const int oc = unit >> 3, g = unit & 7;    // output row oc (= source col), elements 8g..8g+7
+    uint32_t w0[4], w1[4], w2[4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = g * 8 + i;
+      const float x = sm[r * 64 + (oc ^ (g << 2))];
+      const uint16_t h0 = cvt_bf16_rn((double)x);
+      const float r1 = __fsub_rn(x, bf16_to_f32(h0));
+      const uint16_t h1 = cvt_bf16_rn((double)r1);
+      const float r2 = __fsub_rn(r1, bf16_to_f32(h1));
+      const uint16_t h2 = cvt_bf16_rn((double)r2);
+      const int sh = (i & 1) * 16;
+      if (sh == 0) { w0[i >> 1] = h0; w1[i >> 1] = h1; w2[i >> 1] = h2; }
+      else { w0[i >> 1] |= (uint32_t)h0 << 16; w1[i >> 1] |= (uint32_t)h1 << 16; w2[i >> 1] |= (uint32_t)h2 << 16; }
+    }
+    const int64_t o = ((int64_t)(c0 + oc) * nb + r0 + g * 8) * 2;
+    *reinterpret_cast<uint4*>(dst + o) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+    *reinterpret_cast<uint4*>(dst + part + o) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+    *reinterpret_cast<uint4*>(dst + 2 * part + o) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
   }
 }
 
