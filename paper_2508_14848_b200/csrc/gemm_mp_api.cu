@@ -339,7 +339,8 @@ static void build_tables(gmp_plan_s* pl) {
     t.w_off = o; o = align_up(o + nb2 * (t.code == 0 ? 8 : 4), 1024);
     if (hasC) { t.cin_off = o; o = align_up(o + nb2 * class_bytes(t.code), 1024); }
     else t.cin_off = -1;
-    t.cout_off = o; o = align_up(o + nb2 * class_bytes(t.code), 1024);
+    if (t.code == 0) t.cout_off = t.w_off;   // binary64 W is the FP64 C_out payload
+    else { t.cout_off = o; o = align_up(o + nb2 * class_bytes(t.code), 1024); }
     const int64_t i = g / nt, j = g % nt;
     t.user_off = -1;  // set at execute (depends on ldc)
     t.pad = (int32_t)(((i / P) << 16) | (j / Q));  // local tile coordinates (il, jl)
@@ -916,9 +917,21 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
               k_mn<double><<<(unsigned)L.icount, 256, mn_smem_bytes<double>(), stream>>>(it, pd, dct, ws, (int)nb,
                                                                                        pl->d.alpha);
             } else {
-              GMP_TRY(set_smem_once(k_dmma<DMMA_WN>, dmma_smem_bytes()));
-              k_dmma<DMMA_WN><<<(unsigned)L.icount, 256, dmma_smem_bytes(), stream>>>(it, pd, dct, ws, (int)nb,
-                                                                                      pl->d.alpha);
+              // experiment knob (unset = product configuration BK 16 x 4 stages)
+              static const int dv = getenv("GMP_DMMA_VARIANT") ? atoi(getenv("GMP_DMMA_VARIANT")) : 0;
+              if (dv == 1) {
+                using V = DmmaCfg<DMMA_WN, 32, 2>;
+                GMP_TRY(set_smem_once(k_dmma<DMMA_WN, 32, 2>, V::SMEM));
+                k_dmma<DMMA_WN, 32, 2><<<(unsigned)L.icount, 256, V::SMEM, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha);
+              } else if (dv == 2) {
+                using V = DmmaCfg<DMMA_WN, 16, 3>;
+                GMP_TRY(set_smem_once(k_dmma<DMMA_WN, 16, 3>, V::SMEM));
+                k_dmma<DMMA_WN, 16, 3><<<(unsigned)L.icount, 256, V::SMEM, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha);
+              } else {
+                using V = DmmaCfg<DMMA_WN>;
+                GMP_TRY(set_smem_once(k_dmma<DMMA_WN>, V::SMEM));
+                k_dmma<DMMA_WN><<<(unsigned)L.icount, 256, V::SMEM, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha);
+              }
             }
             break;
           case 1:
@@ -941,7 +954,7 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
     GMP_CUDA(cudaMemsetAsync(mb, 0, nCl * 8, stream));
     k_c_maxabs<<<dim3(grid_for(nb2, 4) / 8 + 1, (unsigned)nCl), 256, 0, stream>>>(dct, ws, nb2, mb);
     GMP_CUDA(cudaGetLastError());
-    k_c_finalize<<<dim3(grid_for(nb2, 1) / 8 + 1, (unsigned)nCl), 256, 0, stream>>>(
+    k_c_finalize<<<dim3((unsigned)(nb / FIN_ROWS), (unsigned)nCl), 256, 0, stream>>>(
         dct, ws, mb, (int16_t*)(ws + pl->off_cscale), Cuser, ldc, (int)nb);
     GMP_CUDA(cudaGetLastError());
   }

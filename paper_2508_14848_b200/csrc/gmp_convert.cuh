@@ -298,22 +298,22 @@ __global__ void __launch_bounds__(256) k_acc_init(const CTileDesc* __restrict__ 
 __global__ void __launch_bounds__(256) k_c_maxabs(const CTileDesc* __restrict__ ct, const uint8_t* ws,
                                                   int64_t n, unsigned long long* maxbits) {
   const CTileDesc c = ct[blockIdx.y];
-  double m = 0.0;
+  if (c.code == 0) return;                      // FP64 C tiles carry no scale
+  float m = 0.f;
   for (int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; e < n;
        e += (int64_t)gridDim.x * blockDim.x * 4) {
-    if (c.code == 0) {
-      const double2* p = reinterpret_cast<const double2*>(ws + c.w_off) + e / 2;
-      double2 a = p[0], b = p[1];
-      m = fmax(m, fmax(fmax(fabs(a.x), fabs(a.y)), fmax(fabs(b.x), fabs(b.y))));
-    } else {
-      float4 a = reinterpret_cast<const float4*>(ws + c.w_off)[e / 4];
-      m = fmax(m, (double)fmaxf(fmaxf(fabsf(a.x), fabsf(a.y)), fmaxf(fabsf(a.z), fabsf(a.w))));
-    }
+    const float4 a = reinterpret_cast<const float4*>(ws + c.w_off)[e / 4];
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(a.x), fabsf(a.y)), fmaxf(fabsf(a.z), fabsf(a.w))));
   }
-  for (int off = 16; off >= 1; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
-  if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(maxbits + blockIdx.y, (unsigned long long)__double_as_longlong(m));
+  for (int off = 16; off >= 1; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0 && m > 0.f)
+    atomicMax(maxbits + blockIdx.y, (unsigned long long)__double_as_longlong((double)m));
 }
 
+// one CTA per FP_ROWS rows of a C tile, threads along the row (coalesced user C
+// stores).  FP64 C tiles: the packed C_out IS the binary64 W (plan aliases
+// cout_off = w_off), so only the user's C is written.
+constexpr int FIN_ROWS = 4;
 __global__ void __launch_bounds__(256) k_c_finalize(const CTileDesc* __restrict__ ct, uint8_t* ws,
                                                     const unsigned long long* maxbits, int16_t* cscale,
                                                     double* cuser, int64_t ldc, int nb) {
@@ -321,22 +321,21 @@ __global__ void __launch_bounds__(256) k_c_finalize(const CTileDesc* __restrict_
   const double m = __longlong_as_double((long long)maxbits[blockIdx.y]);
   const int e = scale_exp(m, c.code);
   if (blockIdx.x == 0 && threadIdx.x == 0) cscale[blockIdx.y] = (int16_t)e;
-  const int64_t n = (int64_t)nb * nb;
   uint8_t* pay = ws + c.cout_off;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    double w = (c.code == 0) ? reinterpret_cast<const double*>(ws + c.w_off)[i]
-                             : (double)reinterpret_cast<const float*>(ws + c.w_off)[i];
-    double back;
+  for (int rr = 0; rr < FIN_ROWS; ++rr) {
+    const int64_t r = (int64_t)blockIdx.x * FIN_ROWS + rr;
+    double* urow = cuser + c.user_off + r * ldc;
     if (c.code == 0) {
-      reinterpret_cast<double*>(pay)[i] = w;
-      back = w;
+      const double* wrow = reinterpret_cast<const double*>(ws + c.w_off) + r * nb;
+      for (int col = threadIdx.x; col < nb; col += blockDim.x) urow[col] = wrow[col];
     } else {
-      payload_store(pay, i, c.code, ldexp(w, e));
-      back = ldexp(payload_f64(pay, i, c.code), -e);
+      const float* wrow = reinterpret_cast<const float*>(ws + c.w_off) + r * nb;
+      for (int col = threadIdx.x; col < nb; col += blockDim.x) {
+        const int64_t i = r * nb + col;
+        payload_store(pay, i, c.code, ldexp((double)wrow[col], e));
+        urow[col] = ldexp(payload_f64(pay, i, c.code), -e);
+      }
     }
-    const int64_t r = i / nb, col = i - (i / nb) * nb;
-    cuser[c.user_off + r * ldc + col] = back;
   }
 }
 

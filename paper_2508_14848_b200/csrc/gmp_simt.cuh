@@ -410,17 +410,16 @@ k_mn(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
 // The accumulation order inside a DMMA is the hardware's: the parity bound is
 // the all-FP64 1e-13 relative Frobenius.
 // ---------------------------------------------------------------------------
-constexpr int DMMA_ST = 4, DMMA_BK = 16;
-template <int WN> struct DmmaCfg {
+template <int WN, int BK_ = 16, int ST_ = 4> struct DmmaCfg {
+  static constexpr int BK = BK_, ST = ST_;          // k-rows per stage (multiple of 16), ring depth
   static constexpr int BN = 2 * WN;                 // 8 warps = 4 (m) x 2 (n), warp tile 32 x WN
   static constexpr int AP = 128 + 4, BP = BN + 4;   // row pitches in doubles (= 32 B mod 128 B)
-  static constexpr int SMEM = DMMA_ST * DMMA_BK * (AP + BP) * 8;
+  static constexpr int SMEM = ST * BK * (AP + BP) * 8;
   static constexpr int MINB = (WN == 32) ? 2 : 1;
 };
 constexpr int DMMA_WN = 32;                         // product configuration (128 x 64 sub-tiles; 32 x 64 warp
                                                     // tiles at 1 CTA/SM measured 9 % slower)
 constexpr int DMMA_BN = DmmaCfg<DMMA_WN>::BN;
-constexpr int dmma_smem_bytes() { return DmmaCfg<DMMA_WN>::SMEM; }
 
 __device__ __forceinline__ void dmma16816(double (&c)[4], const double (&a)[8], const double (&b)[4]) {
   asm(
@@ -431,12 +430,12 @@ __device__ __forceinline__ void dmma16816(double (&c)[4], const double (&a)[8], 
         "d"(b[1]), "d"(b[2]), "d"(b[3]));
 }
 
-template <int WN>
+template <int WN, int BK_ = 16, int ST_ = 4>
 __global__ void __launch_bounds__(256, DmmaCfg<WN>::MINB)
 k_dmma(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
        const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha) {
-  using Cfg = DmmaCfg<WN>;
-  constexpr int BK = DMMA_BK, ST = DMMA_ST, AP = Cfg::AP, BP = Cfg::BP, BN = Cfg::BN, NJ = WN / 8;
+  using Cfg = DmmaCfg<WN, BK_, ST_>;
+  constexpr int BK = Cfg::BK, ST = Cfg::ST, AP = Cfg::AP, BP = Cfg::BP, BN = Cfg::BN, NJ = WN / 8;
   constexpr int ACH = 64, BCH = BN / 2;             // 16-byte chunks per k-row (A: 128 doubles, B: BN)
   constexpr int CHUNKS = BK * (ACH + BCH), CPT = CHUNKS / 256;
   constexpr int STAGE = BK * (AP + BP) * 8;
@@ -501,23 +500,29 @@ k_dmma(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
     const double* As = reinterpret_cast<const double*>(sm + cstage * STAGE);
     const double* Bs = As + BK * AP;
     if (++cstage == ST) cstage = 0;
-    double a[2][8];
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+    for (int kk = 0; kk < BK; kk += 16) {
+      double a[2][8];
 #pragma unroll
-      for (int r = 0; r < 8; ++r) a[i][r] = As[(t + 4 * (r >> 1)) * AP + wm + i * 16 + g + 8 * (r & 1)];
+      for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) {
-      double b[4];
+        for (int r = 0; r < 8; ++r) a[i][r] = As[(kk + t + 4 * (r >> 1)) * AP + wm + i * 16 + g + 8 * (r & 1)];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) b[r] = Bs[(t + 4 * r) * BP + wn + j * 8 + g];
+      for (int j = 0; j < NJ; ++j) {
+        double b[4];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) dmma16816(acc[i][j], a[i], b);
+        for (int r = 0; r < 4; ++r) b[r] = Bs[(kk + t + 4 * r) * BP + wn + j * 8 + g];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) dmma16816(acc[i][j], a[i], b);
+      }
     }
     if (++cslice == nsl) {
       cslice = 0;
-      // ---- fold (O9) ----
+      // ---- fold (O9, R25): consecutive pairs with the same fold
+      // factor (every FP64-class pair: eA = eB = 0) keep accumulating in the
+      // DMMA registers; W is read and written once per run of equal factors ----
       const PairDesc pd = pairs[it.pbeg + cpair++];
+      if (cpair < it.pcnt && pairs[it.pbeg + cpair].fexp == pd.fexp) continue;
       const double f64 = ldexp(alpha, pd.fexp);
       const float f32 = __double2float_rn(f64);
 #pragma unroll
