@@ -88,12 +88,16 @@ __device__ __forceinline__ void pack_block(const PackJob& j, uint8_t* ws, int nb
     }
   } else {
     // stage the 64x64 block in shared memory, write it transposed (K-major)
+    double2 x[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      int unit = t + u * 256;           // 64 rows x 32 double2
-      int r = unit >> 5, q = unit & 31;
-      const double2 x = __ldg(reinterpret_cast<const double2*>(j.src + (int64_t)(r0 + r) * j.ld + c0 + 2 * q));
-      *reinterpret_cast<double2*>(sm + sw64(r, 2 * q)) = x;
+      const int unit = t + u * 256;     // 64 rows x 32 double2
+      x[u] = __ldg(reinterpret_cast<const double2*>(j.src + (int64_t)(r0 + (unit >> 5)) * j.ld + c0 + 2 * (unit & 31)));
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int unit = t + u * 256;
+      *reinterpret_cast<double2*>(sm + sw64(unit >> 5, 2 * (unit & 31))) = x[u];
     }
     __syncthreads();
 #pragma unroll
@@ -173,11 +177,19 @@ __device__ __forceinline__ void shadow_t_block(const ShadowJob& j, uint8_t* ws, 
   const int t = threadIdx.x;
   const uint8_t* src = ws + j.src_off;
   uint8_t* dst = ws + j.dst_off;
+  // all 16 loads first: a global load through a generic pointer may alias the
+  // shared block, so interleaving them with the shared stores would serialise
+  double x[16];
 #pragma unroll
   for (int u = 0; u < 16; ++u) {
     const int unit = t + u * 256;  // 64 rows x 64 cols
     const int r = unit >> 6, c = unit & 63;
-    sm[sw64(r, c)] = ldexp(payload_f64(src, (int64_t)(r0 + r) * nb + c0 + c, F), j.d);
+    x[u] = payload_f64(src, (int64_t)(r0 + r) * nb + c0 + c, F);
+  }
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int unit = t + u * 256;
+    sm[sw64(unit >> 6, unit & 63)] = ldexp(x[u], j.d);
   }
   __syncthreads();
 #pragma unroll
@@ -227,12 +239,17 @@ __global__ void __launch_bounds__(256) k_split(const SplitJob* __restrict__ jobs
   uint8_t* dst = ws + j.dst_off;
   const int64_t part = (int64_t)nb * nb * 2;   // bytes per BF16 part
   const int t = threadIdx.x;
+  float4 x[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int unit = t + u * 256;              // 64 rows x 16 float4
+    x[u] = *reinterpret_cast<const float4*>(src + (int64_t)(r0 + (unit >> 4)) * nb + c0 + 4 * (unit & 15));
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int unit = t + u * 256;
     const int r = unit >> 4, q = unit & 15;
-    const float4 x = *reinterpret_cast<const float4*>(src + (int64_t)(r0 + r) * nb + c0 + 4 * q);
-    *reinterpret_cast<float4*>(sm + r * 64 + ((4 * q) ^ (((r >> 3) & 7) << 2))) = x;
+    *reinterpret_cast<float4*>(sm + r * 64 + ((4 * q) ^ (((r >> 3) & 7) << 2))) = x[u];
   }
   __syncthreads();
 #pragma unroll
