@@ -402,13 +402,13 @@ def main():
     # DRAM traffic per launch of the dominant kernel from the committed ncu capture
     traffic = None
     try:
-        kname = {0: "k_dmma<32>", 1: "k_tc_class<5, 128>", 2: "k_tc_class<2, 128>", 3: "k_tc_class<3, 256>",
-                 4: "k_tc_class<4, 256>"}[dom]
+        kpref = {0: "k_dmma<", 1: "k_tc_class<5,", 2: "k_tc_class<2,", 3: "k_tc_class<3,", 4: "k_tc_class<4,"}[dom]
         with open(os.path.join(ROOT, "profiles", "traffic_r01.json")) as f:
             tr = json.load(f)
         # per-launch bytes only describe the captured launch configuration
         if tr.get("workload") == w.name and tr.get("n_gpus") == G:
-            traffic = tr["kernels"].get(kname)
+            hits = [v for k, v in tr["kernels"].items() if k.startswith(kpref)]
+            traffic = sum(hits) / len(hits) if hits else None
     except Exception:
         traffic = None
     launches = st["launches_plan"] + st["launches_convert"] + st["launches_execute"]

@@ -2,6 +2,7 @@
 
 usage: python tools/ncu_summary.py full <report.ncu-rep> <out.md>
        python tools/ncu_summary.py launches <launches.csv> <out.md>
+       python tools/ncu_summary.py traffic <report.ncu-rep> <out.json> <workload> <n_gpus>
 """
 import csv
 import io
@@ -51,6 +52,30 @@ def full(rep, out):
     open(out, "w").write("\n".join(lines) + "\n")
 
 
+def traffic(rep, out, workload, n_gpus):
+    """bytes per launch (dram read + write, mean over the captured launches) per kernel"""
+    import json
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    hdr, units, data = rows[0], rows[1], rows[2:]
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    acc = {}
+    for r in data:
+        name = re.sub(r"^void ", "", r[hdr.index("Kernel Name")])
+        name = re.sub(r"\(.*", "", name) if not name.startswith("k_tc_class<") and not name.startswith("k_dmma<") \
+            else re.sub(r"\(.*", "", name.replace("gmp::", ""))
+        name = name.replace("gmp::", "")
+        tot = 0.0
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = hdr.index(k)
+            tot += float(r[i]) * scale.get(units[i], 1.0)
+        acc.setdefault(name, []).append(tot)
+    d = {"source": rep + " (ncu --set full)", "workload": workload, "n_gpus": int(n_gpus),
+         "unit": "bytes per launch (dram read + write), mean over captured launches",
+         "kernels": {k: sum(v) / len(v) for k, v in acc.items()}}
+    json.dump(d, open(out, "w"), indent=1)
+
+
 def launches(path, out):
     rows = [r for r in csv.reader(open(path)) if len(r) > 5]
     hdr = rows[0]
@@ -75,4 +100,4 @@ def launches(path, out):
 
 
 if __name__ == "__main__":
-    {"full": full, "launches": launches}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    {"full": full, "launches": launches, "traffic": traffic}[sys.argv[1]](*sys.argv[2:])
