@@ -24,6 +24,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
+import bench  # noqa: E402  (Clocks sampler)
 import gmp_inputs  # noqa: E402
 from paper_2508_14848_b200 import api  # noqa: E402
 from paper_2508_14848_b200 import binding as B  # noqa: E402
@@ -64,11 +65,14 @@ def run(w, reps, mask=None, flags=0, explicit=None, label=None):
     ev[3].record()
     torch.cuda.synchronize()
     times, cms = [], []
+    clk = bench.Clocks(torch.cuda.current_device())
+    clk.start()
     for _ in range(reps):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record(); g.execute(out); e.record(); e.synchronize()
         times.append(s.elapsed_time(e))
         cms.append(g.stats()["class_ms"])
+    clocks = clk.stop()
     st = g.stats()
     best = min(times)
     pk = peaks()
@@ -85,7 +89,7 @@ def run(w, reps, mask=None, flags=0, explicit=None, label=None):
                class_tflops={NAMES[c]: round(st["flops"][c] / (cls_ms[c] * 1e-3) / 1e12, 1)
                              for c in range(5) if st["pairs"][c] and cls_ms[c] > 0},
                t_roof_ms=t_roof, roof_frac_exec=t_roof / best,
-               peaks_tflops={NAMES[c]: round(pk[c], 1) for c in range(5)})
+               peaks_tflops={NAMES[c]: round(pk[c], 1) for c in range(5)}, clocks=clocks)
     g.close()
     del A, Bm, C, out
     torch.cuda.empty_cache()
