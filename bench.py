@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (cfg3+ on one GPU)")
     ap.add_argument("--size", type=int, default=0, help="override M=N=K (keeps the config's recipe)")
+    ap.add_argument("--sender", action="store_true",
+                    help="GMP_FLAG_SENDER_SIDE: hybrid sender-side conversion of SUMMA panels (NEXT-2)")
     return ap.parse_args()
 
 
@@ -308,7 +310,8 @@ def main():
     ldc = Cout.stride(0)
     torch.cuda.synchronize()
 
-    desc = B.make_desc(w.M, w.N, w.K, w.nb, w.tol, w.alpha, w.beta, w.class_mask, B.GMP_FLAG_TIMING, P, Q, rank)
+    flags = B.GMP_FLAG_TIMING | (B.GMP_FLAG_SENDER_SIDE if a.sender else 0)
+    desc = B.make_desc(w.M, w.N, w.K, w.nb, w.tol, w.alpha, w.beta, w.class_mask, flags, P, Q, rank)
     nscr = B.gemm_mp_scratch_size(desc)
     scratch = torch.empty(nscr, dtype=torch.uint8, device=dev)
     ws_holder = {"t": None, "bytes": 0}
@@ -423,13 +426,15 @@ def main():
         out = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": G, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong" if G > 1 else "weak", "vs_baseline": None,
+            "scaling": "strong", "vs_baseline": None,
             "dtype": "f64/f32/f16/bf16" + ("/e4m3" if w.class_mask & 16 else "") + " (per-tile classes)",
             "data": "synthetic (counter-based SplitMix64, per-tile norm spread; DESIGN.md Input recipe)",
             "config": {"workload": w.name, "M": w.M, "N": w.N, "K": w.K, "nb": w.nb, "tol": w.tol,
                        "alpha": w.alpha, "beta": w.beta, "grid": f"{P}x{Q}", "parallelism": f"summa{P}x{Q}",
                        "l2": "inputs (2+ GB per matrix) > 126 MB L2, no flush needed",
-                       "step": "plan+convert+execute (S1-S7)"},
+                       "step": "plan+convert+execute (S1-S7)",
+                       "conversion": "sender-side hybrid (NEXT-2)" if a.sender else "receiver-side (PAPER.md:148)"},
+            "nvlink_recv_bytes_rank0": st["recv_bytes_local"],
             "phases_ms": {"plan": statistics.median(ph[0] for ph in phase),
                           "convert": statistics.median(ph[1] for ph in phase), "execute": exec_ms},
             "execute_tflops": w.flops / (exec_ms * 1e-3) / 1e12,

@@ -68,6 +68,14 @@ typedef enum {
                                  per element, 28 tcgen05 kind::i8 MMAs) instead of DMMA (default)    */
 #define GMP_FLAG_FP32_FFMA 4u /* FP32 class on the FP32 pipe (packed FFMA2, bitwise O8) instead of the
                                  default tensor-pipe path (exact BF16x3 split, nine BF16 MMAs per block) */
+#define GMP_FLAG_SENDER_SIDE 16u /* SURVEY 8(f) NEXT-2, hybrid conversion (PAPER.md:148 defers it): a
+                                 SUMMA panel tile whose receivers in its process row (A) / column (B)
+                                 together need a set of classes S whose payloads are smaller than the
+                                 stored one is broadcast as those |S| payloads, converted at the SENDER
+                                 from its stored payload (RN_c(decode(stored)), the same bytes a
+                                 receiver would make); otherwise the stored payload is sent.  Maps,
+                                 packed bytes and C are bit-identical to the default receiver-side
+                                 mode; only the bytes on NVLink (stats.recv_bytes_local) change.     */
 
 typedef struct {
   int64_t M, N, K;     /* global GEMM shape                                                    */
@@ -167,10 +175,12 @@ gmp_status_t gemm_mp_plan_host(const gmp_desc_t *desc, const uint8_t *acode, con
                                const uint8_t *ccode, const int16_t *ascale5, const int16_t *bscale5,
                                const int16_t *cin_scale, gmp_plan_t *out);
 
-/* SUMMA broadcasts of step `step` on this rank, 4 int64 per entry:
+/* SUMMA broadcasts of step `step` on this rank, 5 int64 per entry:
  * {which (0 = A on the row communicator, 1 = B on the column communicator),
- *  global tile index, root rank inside that communicator, payload bytes}.
- * entries may be NULL to query the count *n.                                   */
+ *  global tile index, class of the payload on the wire (the stored class, or a
+ *  shadow class under GMP_FLAG_SENDER_SIDE), root rank inside that
+ *  communicator, payload bytes}.  entries may be NULL to query the count *n;
+ *  cap counts entries (5 int64 each).                                          */
 gmp_status_t gemm_mp_get_schedule(gmp_plan_t plan, int32_t step, int64_t *entries, int64_t cap,
                                   int64_t *n);
 

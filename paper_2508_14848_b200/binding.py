@@ -19,6 +19,7 @@ GMP_FLAG_SIMT_ONLY = 1
 GMP_FLAG_TIMING = 2
 GMP_FLAG_FP32_FFMA = 4
 GMP_FLAG_FP64_INT8 = 8
+GMP_FLAG_SENDER_SIDE = 16
 STATUS = ["GMP_OK", "GMP_ERR_ARG", "GMP_ERR_NOT_DIVISIBLE", "GMP_ERR_MAP_SHAPE", "GMP_ERR_NONFINITE",
           "GMP_ERR_GRID", "GMP_ERR_WORKSPACE", "GMP_ERR_STATE", "GMP_ERR_CUDA", "GMP_ERR_NCCL",
           "GMP_ERR_UNSUPPORTED"]
@@ -230,7 +231,7 @@ def gemm_mp_get_schedule(plan, step):
     import numpy as np
     n = ct.c_int64()
     _check(lib().gemm_mp_get_schedule(plan, step, None, 0, ct.byref(n)))
-    out = np.zeros((n.value, 4), np.int64)
+    out = np.zeros((n.value, 5), np.int64)
     if n.value:
         _check(lib().gemm_mp_get_schedule(plan, step, out.ctypes.data, n.value, ct.byref(n)))
     return out

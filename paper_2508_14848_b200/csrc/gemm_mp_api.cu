@@ -74,10 +74,11 @@ struct Launch {
   int bn;  // N of the class kernel's CTA tile
 };
 
-struct Bcast {           // one SUMMA broadcast of a stored tile in a step
+struct Bcast {           // one SUMMA broadcast of a panel tile payload in a step
   int which;             // 0: A on the row communicator, 1: B on the column communicator
   int root;              // root rank inside that communicator
   int64_t tile;          // global tile index (i*kt + l for A, l*nt + j for B)
+  int cls;               // class of the payload (stored class, or a sender-side shadow class)
   int64_t off;           // byte offset of the payload slot (root: its stored tile)
   int64_t bytes;
 };
@@ -98,6 +99,7 @@ struct gmp_plan_s {
   std::vector<int64_t> locA, locB, locC;
   // slots: [global tile][class] -> slot in that class's arena, -1 if absent
   std::vector<int32_t> slotA5, slotB5;
+  std::vector<uint8_t> wireA, wireB;     // per panel tile: bitmask of classes broadcast (GMP_FLAG_SENDER_SIDE)
   int64_t arena_off[7] = {0}, arena_slots[7] = {0};   // 0..4 classes, 5 = FP32 BF16x3 splits,
   int64_t slot_bytes[7] = {0};                          // 6 = FP64 int8 digit planes (Ozaki)
   std::vector<int32_t> splitA, splitB;                  // [global tile] -> split slot, -1 if absent
@@ -234,13 +236,55 @@ static void build_tables(gmp_plan_s* pl) {
         if (c == 1 && pl->fp32_tc) { needSA[i * kt + l] = 1; needSB[l * nt + j] = 1; }
         if (c == 0 && pl->fp64_tc) { needOA[i * kt + l] = 1; needOB[l * nt + j] = 1; }
       }
-  // every A tile of this process row and B tile of this process column keeps a
-  // stored-precision slot: local tiles are broadcast roots, the others are
-  // received (every rank of a row/column takes part in the broadcast)
-  for (int64_t g = 0; g < pl->nA; ++g)
-    if ((g / kt) % P == p) needA[g * 5 + pl->codeA[g]] = 1;
-  for (int64_t g = 0; g < pl->nB; ++g)
-    if ((g % nt) % Q == q) needB[g * 5 + pl->codeB[g]] = 1;
+  // ---- wire classes of every panel tile of this process row (A) / column (B) ----
+  // receiver-side (default): the stored class.  GMP_FLAG_SENDER_SIDE
+  // (hybrid, NEXT-2): the union S of the pair classes the receiving ranks of the
+  // row / column need, when those payloads are smaller than the stored one.
+  // Computed from the global maps only, so every rank of a row/column agrees.
+  const bool sender = (d.flags & GMP_FLAG_SENDER_SIDE) && P * Q > 1;
+  pl->wireA.assign(pl->nA, 0);
+  pl->wireB.assign(pl->nB, 0);
+  for (int64_t g = 0; g < pl->nA; ++g) {
+    const int64_t i = g / kt, l = g % kt;
+    if (i % P != p) continue;
+    const int code = pl->codeA[g];
+    uint8_t set = 0;
+    if (sender)
+      for (int64_t j = 0; j < nt; ++j)
+        if ((int)(j % Q) != (int)(l % Q)) set |= (uint8_t)(1u << std::max(code, (int)pl->codeB[l * nt + j]));
+    int64_t sb = 0;
+    for (int c = 0; c < 5; ++c) if (set >> c & 1) sb += pl->slot_bytes[c];
+    pl->wireA[g] = (set && sb < pl->slot_bytes[code]) ? set : (uint8_t)(1u << code);
+  }
+  for (int64_t g = 0; g < pl->nB; ++g) {
+    const int64_t l = g / nt, j = g % nt;
+    if (j % Q != q) continue;
+    const int code = pl->codeB[g];
+    uint8_t set = 0;
+    if (sender)
+      for (int64_t i = 0; i < mt; ++i)
+        if ((int)(i % P) != (int)(l % P)) set |= (uint8_t)(1u << std::max(code, (int)pl->codeA[i * kt + l]));
+    int64_t sb = 0;
+    for (int c = 0; c < 5; ++c) if (set >> c & 1) sb += pl->slot_bytes[c];
+    pl->wireB[g] = (set && sb < pl->slot_bytes[code]) ? set : (uint8_t)(1u << code);
+  }
+  // every panel tile of this process row / column holds slots for its wire
+  // classes (roots send them, the others receive); a receiver of a tile sent
+  // sender-side gets every class it needs on the wire and keeps no stored copy
+  for (int64_t g = 0; g < pl->nA; ++g) {
+    if ((g / kt) % P != p) continue;
+    const bool root = (int)((g % kt) % Q) == q;
+    if (!root && pl->wireA[g] != (1u << pl->codeA[g]))
+      for (int c = 0; c < 5; ++c) needA[g * 5 + c] = 0;
+    for (int c = 0; c < 5; ++c) if (pl->wireA[g] >> c & 1) needA[g * 5 + c] = 1;
+  }
+  for (int64_t g = 0; g < pl->nB; ++g) {
+    if ((g % nt) % Q != q) continue;
+    const bool root = (int)((g / nt) % P) == p;
+    if (!root && pl->wireB[g] != (1u << pl->codeB[g]))
+      for (int c = 0; c < 5; ++c) needB[g * 5 + c] = 0;
+    for (int c = 0; c < 5; ++c) if (pl->wireB[g] >> c & 1) needB[g * 5 + c] = 1;
+  }
 
   // ---- arena slots ----
   pl->slotA5.assign(pl->nA * 5, -1);
@@ -392,6 +436,8 @@ static void build_tables(gmp_plan_s* pl) {
     const int32_t* sl = (isB ? pl->slotB5.data() : pl->slotA5.data()) + g * 5;
     const bool local = isB ? ((g / nt) % P == p) : ((g % kt) % Q == q);
     const int64_t l = isB ? g / nt : g % kt;
+    const uint8_t wire = (isB ? pl->wireB : pl->wireA)[g];
+    if (!local && wire && wire != (1u << code)) return;   // every needed class arrives on the wire
     for (int c = code + 1; c < 5; ++c) {
       if (sl[c] < 0) continue;
       ShadowJob sj{};
@@ -464,17 +510,21 @@ static void build_tables(gmp_plan_s* pl) {
       const int s = (int)(l / GMP_STEP_DEPTH);
       for (int64_t i = p; i < mt; i += P) {       // A(i,l) along process row p, root column l % Q
         const int64_t g = i * kt + l;
-        const int c = pl->codeA[g];
-        Bcast b{0, (int)(l % Q), g, arena(c, pl->slotA5[g * 5 + c]), pl->slot_bytes[c]};
-        pl->bcast_step[s].push_back(b);
-        if ((int)(l % Q) != q) recv_bytes += b.bytes;
+        for (int c = 0; c < 5; ++c) {
+          if (!(pl->wireA[g] >> c & 1)) continue;
+          Bcast b{0, (int)(l % Q), g, c, arena(c, pl->slotA5[g * 5 + c]), pl->slot_bytes[c]};
+          pl->bcast_step[s].push_back(b);
+          if ((int)(l % Q) != q) recv_bytes += b.bytes;
+        }
       }
       for (int64_t j = q; j < nt; j += Q) {       // B(l,j) along process column q, root row l % P
         const int64_t g = l * nt + j;
-        const int c = pl->codeB[g];
-        Bcast b{1, (int)(l % P), g, arena(c, pl->slotB5[g * 5 + c]), pl->slot_bytes[c]};
-        pl->bcast_step[s].push_back(b);
-        if ((int)(l % P) != p) recv_bytes += b.bytes;
+        for (int c = 0; c < 5; ++c) {
+          if (!(pl->wireB[g] >> c & 1)) continue;
+          Bcast b{1, (int)(l % P), g, c, arena(c, pl->slotB5[g * 5 + c]), pl->slot_bytes[c]};
+          pl->bcast_step[s].push_back(b);
+          if ((int)(l % P) != p) recv_bytes += b.bytes;
+        }
       }
     }
   }
@@ -744,10 +794,11 @@ extern "C" gmp_status_t gemm_mp_get_schedule(gmp_plan_t pl, int32_t step, int64_
   if (entries) {
     if (cap < (int64_t)v.size()) return fail(GMP_ERR_ARG, "entries buffer too small");
     for (size_t k = 0; k < v.size(); ++k) {
-      entries[4 * k + 0] = v[k].which;
-      entries[4 * k + 1] = v[k].tile;
-      entries[4 * k + 2] = v[k].root;
-      entries[4 * k + 3] = v[k].bytes;
+      entries[5 * k + 0] = v[k].which;
+      entries[5 * k + 1] = v[k].tile;
+      entries[5 * k + 2] = v[k].cls;
+      entries[5 * k + 3] = v[k].root;
+      entries[5 * k + 4] = v[k].bytes;
     }
   }
   return GMP_OK;

@@ -4,9 +4,11 @@ Every rank builds the library's host-side plan (gemm_mp_plan_host) from the
 same oracle maps, executes ITS SUMMA schedule with torch.distributed (gloo)
 broadcasts of oracle-packed stored payloads on the row / column groups, and
 checks (1) every tile-GEMM operand it needs arrives bit-exact in its stored
-precision, (2) its received bytes equal the library's count and
-the closed form, (3) the local tile-GEMMs of all ranks partition
-the global pair set.  The GPU run of the same schedule over NCCL is
+precision -- or, under GMP_FLAG_SENDER_SIDE,
+as the oracle's shadows of the stored payload in every class a receiver needs --
+(2) its received bytes equal the library's count and the closed form (SURVEY
+8(e); for the hybrid mode the cheaper of stored vs union-of-needed-classes per
+tile), (3) the local tile-GEMMs of all ranks partition the global pair set.  The GPU run of the same schedule over NCCL is
 tools/multi_gpu_check.py."""
 import os
 import socket
@@ -28,7 +30,13 @@ def _free_port():
     return p
 
 
-def _worker(rank, G, port, q_out):
+def _wire(code, partner_codes):
+    """hybrid rule: the union of pair classes the receivers need, if cheaper than the stored payload"""
+    S = {max(code, int(c)) for c in partner_codes}
+    return S if S and sum(BY[c] for c in S) < BY[code] else {code}
+
+
+def _worker(rank, G, port, q_out, sender=False):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
@@ -48,7 +56,8 @@ def _worker(rank, G, port, q_out):
         mt, kt, nt = o["acode"].shape[0], o["acode"].shape[1], o["bcode"].shape[1]
         P, Q = api.default_grid(G)
         p, q = rank // Q, rank % Q
-        desc = B.make_desc(w.M, w.N, w.K, nb, w.tol, w.alpha, 0.0, w.class_mask, 0, P, Q, rank)
+        flags = B.GMP_FLAG_SENDER_SIDE if sender else 0
+        desc = B.make_desc(w.M, w.N, w.K, nb, w.tol, w.alpha, 0.0, w.class_mask, flags, P, Q, rank)
         plan = B.gemm_mp_plan_host(desc, o["acode"], o["bcode"], o["ccode"], o["ascale5"], o["bscale5"])
         st = B.gemm_mp_get_stats(plan)
         rows = [dist.new_group([pp * Q + qq for qq in range(Q)]) for pp in range(P)]
@@ -63,7 +72,13 @@ def _worker(rank, G, port, q_out):
                 l, j = divmod(g, nt)
                 t = Bm[l * nb:(l + 1) * nb, j * nb:(j + 1) * nb]
                 c = int(o["bcode"][l, j]); e = int(o["bscale5"][l, j, c]); role = "B"
-            return oracle.pack_tile(t, c, e, role=role).view(np.uint8)
+            return oracle.pack_tile(t, c, e, role=role), c, e, role
+
+        def payload(which, g, cls):
+            p0, c, e, role = stored(which, g)
+            if cls == c:
+                return p0.view(np.uint8)
+            return oracle.shadow_tile(p0, nb, c, e, cls, role=role)[0].view(np.uint8)
 
         have = {}
         recv = 0
@@ -71,35 +86,51 @@ def _worker(rank, G, port, q_out):
         for s in range(st["steps"]):
             sched = B.gemm_mp_get_schedule(plan, s)
             works, bufs = [], []
-            for which, g, root, nbytes in sched:
+            for which, g, cls, root, nbytes in sched:
                 grp = rows[p] if which == 0 else cols[q]
                 root_global = p * Q + root if which == 0 else root * Q + q
                 if root_global == rank:
-                    buf = torch.from_numpy(stored(which, g).copy())
+                    buf = torch.from_numpy(payload(which, g, cls).copy())
+                    have.setdefault((which, int(g)), set()).add(stored(which, g)[1])   # the root owns the tile
                 else:
                     buf = torch.zeros(int(nbytes), dtype=torch.uint8)
                     recv += int(nbytes)
                 if buf.numel() != nbytes:
                     errs.append(f"size of tile {which}:{g}")
                 works.append(dist.broadcast(buf, root_global, group=grp, async_op=True))
-                bufs.append((which, int(g), buf))
+                bufs.append((which, int(g), int(cls), buf))
             for wk in works:
                 wk.wait()
-            for which, g, buf in bufs:
-                if not np.array_equal(buf.numpy(), stored(which, g)):
-                    errs.append(f"payload mismatch {which}:{g}")
-                have[(which, g)] = True
-        # every operand of every local tile-GEMM is present
+            for which, g, cls, buf in bufs:
+                if not np.array_equal(buf.numpy(), payload(which, g, cls)):
+                    errs.append(f"payload mismatch {which}:{g}:{cls}")
+                have.setdefault((which, g), set()).add(cls)
+        # every operand of every local tile-GEMM is present: its pair class, or the
+        # stored class (receiver-side conversion)
         pairs_local = 0
         for i in range(p, mt, P):
             for j in range(q, nt, Q):
                 for l in range(kt):
                     pairs_local += 1
-                    if (0, i * kt + l) not in have or (1, l * nt + j) not in have:
+                    ca, cb = int(o["acode"][i, l]), int(o["bcode"][l, j])
+                    c = max(ca, cb)
+                    ha, hb = have.get((0, i * kt + l), set()), have.get((1, l * nt + j), set())
+                    if not (c in ha or ca in ha) or not (c in hb or cb in hb):
                         errs.append(f"missing operand for C({i},{j}) l={l}")
-        closed = sum(nb * nb * BY[o["acode"][i, l]] for i in range(p, mt, P) for l in range(kt) if l % Q != q) + \
+        if sender:
+            closed = sum(nb * nb * sum(BY[c] for c in _wire(int(o["acode"][i, l]),
+                                                            [o["bcode"][l, j] for j in range(nt) if j % Q != l % Q]))
+                         for i in range(p, mt, P) for l in range(kt) if l % Q != q) + \
+                sum(nb * nb * sum(BY[c] for c in _wire(int(o["bcode"][l, j]),
+                                                       [o["acode"][i, l] for i in range(mt) if i % P != l % P]))
+                    for j in range(q, nt, Q) for l in range(kt) if l % P != p)
+        else:
+            closed = sum(nb * nb * BY[o["acode"][i, l]] for i in range(p, mt, P) for l in range(kt) if l % Q != q) + \
+                sum(nb * nb * BY[o["bcode"][l, j]] for j in range(q, nt, Q) for l in range(kt) if l % P != p)
+        stored_bytes = sum(nb * nb * BY[o["acode"][i, l]] for i in range(p, mt, P) for l in range(kt) if l % Q != q) + \
             sum(nb * nb * BY[o["bcode"][l, j]] for j in range(q, nt, Q) for l in range(kt) if l % P != p)
         q_out.put(dict(rank=rank, errs=errs, recv=recv, recv_lib=st["recv_bytes_local"], closed=closed,
+                       stored_bytes=stored_bytes,
                        pairs_local=sum(st["pairs_local"]), pairs_count=pairs_local, pairs_total=sum(st["pairs"]),
                        grid=(P, Q)))
         B.gemm_mp_destroy(plan)
@@ -107,12 +138,13 @@ def _worker(rank, G, port, q_out):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("sender", [False, True])
 @pytest.mark.parametrize("G", [2, 4])
-def test_summa_schedule_over_gloo(G):
+def test_summa_schedule_over_gloo(G, sender):
     ctx = mp.get_context("spawn")
     qo = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, G, port, qo)) for r in range(G)]
+    procs = [ctx.Process(target=_worker, args=(r, G, port, qo, sender)) for r in range(G)]
     for pr in procs:
         pr.start()
     res = [qo.get(timeout=300) for _ in range(G)]
@@ -123,10 +155,15 @@ def test_summa_schedule_over_gloo(G):
     for r in res:
         assert not r["errs"], r["errs"][:5]
         assert r["recv"] == r["recv_lib"] == r["closed"], r
+        assert r["recv"] <= r["stored_bytes"]
+        if not sender:
+            assert r["recv"] == r["stored_bytes"]
         assert r["pairs_local"] == r["pairs_count"]
         tot += r["pairs_local"]
     assert tot == res[0]["pairs_total"]
     assert any(r["recv"] > 0 for r in res)
+    if sender:   # the E4M3-enabled random workload has tiles whose receivers need less than stored
+        assert sum(r["recv"] for r in res) < sum(r["stored_bytes"] for r in res)
 
 
 def test_spec_closed_form_128_bytes():

@@ -39,6 +39,7 @@ def main():
     import argparse
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg", default="small")
+    ap.add_argument("--sender", action="store_true", help="GMP_FLAG_SENDER_SIDE (hybrid conversion, NEXT-2)")
     a = ap.parse_args()
     rank, G = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     lr_ = int(os.environ.get("LOCAL_RANK", rank))
@@ -60,7 +61,8 @@ def main():
     A = api.synth(w.M, w.K, w.nb, w.a, P, Q, p, q, device=dev)
     Bm = api.synth(w.K, w.N, w.nb, w.b, P, Q, p, q, device=dev)
     C = api.synth(w.M, w.N, w.nb, w.c, P, Q, p, q, device=dev) if w.beta != 0 else None
-    desc = B.make_desc(w.M, w.N, w.K, w.nb, w.tol, w.alpha, w.beta, w.class_mask, 0, P, Q, rank)
+    flags = B.GMP_FLAG_SENDER_SIDE if a.sender else 0
+    desc = B.make_desc(w.M, w.N, w.K, w.nb, w.tol, w.alpha, w.beta, w.class_mask, flags, P, Q, rank)
     g = api.GemmMP.__new__(api.GemmMP)
     # distributed plan (GemmMP handles buffers; pass the comm)
     g.__init__(desc, A, Bm, C, nccl_comm=comm, device=dev)
@@ -75,9 +77,15 @@ def main():
     ok = True
     msgs = []
     want_recv = closed_form_recv(maps["acode"], maps["bcode"], w.nb, P, Q, p, q)
-    if st["recv_bytes_local"] != want_recv:
+    if a.sender:   # hybrid: never more than the stored bytes (the gloo test checks the exact rule)
+        if st["recv_bytes_local"] > want_recv:
+            ok = False
+            msgs.append(f"rank {rank}: sender-side recv bytes {st['recv_bytes_local']} > stored {want_recv}")
+    elif st["recv_bytes_local"] != want_recv:
         ok = False
         msgs.append(f"rank {rank}: recv bytes {st['recv_bytes_local']} != closed form {want_recv}")
+    recv_all = [None] * G
+    dist.all_gather_object(recv_all, (st["recv_bytes_local"], want_recv))
     # gather local C tiles on rank 0
     outs = [None] * G
     dist.all_gather_object(outs, (p, q, out.cpu().numpy()))
@@ -109,7 +117,9 @@ def main():
                 diff = np.nanmax(np.abs(F[np.ix_(rr, cc)] - loc))
                 msgs.append(f"C of rank ({pp},{qq}) differs from 1-GPU (max |d| {diff})")
         print(json.dumps({"ok": ok, "G": G, "grid": f"{P}x{Q}", "workload": w.name, "msgs": msgs,
-                          "recv_bytes_rank0": st["recv_bytes_local"], "pairs": st["pairs"]}), flush=True)
+                          "mode": "sender-side (hybrid)" if a.sender else "receiver-side",
+                          "recv_bytes_rank0": st["recv_bytes_local"], "recv_bytes_all": sum(r[0] for r in recv_all),
+                          "stored_bytes_all": sum(r[1] for r in recv_all), "pairs": st["pairs"]}), flush=True)
     flag = torch.tensor([0 if ok else 1], device=dev)
     dist.all_reduce(flag)
     g.close()
