@@ -396,6 +396,11 @@ def main():
     st = stats[-1]
     class_ms = [statistics.mean(s["class_ms"][c] for s in stats) for c in range(5)]
     dom = max(range(5), key=lambda c: class_ms[c])
+    # precision-induced load imbalance: per-rank tile-GEMM device time
+    busy = [sum(class_ms)]
+    if G > 1:
+        busy = [None] * G
+        dist.all_gather_object(busy, sum(class_ms))
     flops_local = [2.0 * w.nb ** 3 * st["pairs_local"][c] for c in range(5)]
     achieved = flops_local[dom] / (class_ms[dom] * 1e-3) / 1e12 if class_ms[dom] > 0 else 0.0
     dom_peak = cpk[dom]
@@ -445,6 +450,8 @@ def main():
             "mix": {"tiles_a": st["tiles_a"], "tiles_b": st["tiles_b"], "tiles_c": st["tiles_c"],
                     "pairs": st["pairs"]},
             "class_ms_rank0": class_ms,
+            "tile_gemm_ms_per_rank": busy,
+            "imbalance": max(busy) / (sum(busy) / len(busy)) if sum(busy) > 0 else None,
             "roofline": {"bound": "tensor", "kernel": f"class {gmp_class_name(dom)} tile-GEMM",
                          "achieved": achieved, "peak": dom_peak, "unit": "TFLOP/s",
                          "frac": achieved / dom_peak if dom_peak else None, "traffic": traffic,
