@@ -97,3 +97,103 @@ def gemm_mp(A, B_, C=None, nb=128, tol=1e-6, alpha=1.0, beta=0.0, class_mask=0b0
     out = torch.empty((M, N), dtype=torch.float64, device=A.device) if out is None else out
     g.execute(out)
     return out, g
+
+
+class HostPipeline:
+    """A stream of GEMMs whose operands and results live in (pinned) HOST memory.
+
+    Each step k copies its A, B (C) to the device, runs plan -> convert ->
+    execute, and copies its C back.  Device operand and result buffers are
+    double-buffered, and the copies run on their own streams, so the H2D of step
+    k+1 and the D2H of step k-1 overlap the compute of step k (PCIe is full
+    duplex).  Only copies and stream/event ordering happen here; every step of
+    the method runs in the library's kernels.
+
+    `desc` fixes the shape (every step reuses it); `comm` is the NCCL
+    communicator for P*Q > 1.  Host tensors must be pinned for the copies to be
+    asynchronous."""
+
+    def __init__(self, desc, local_a, local_b, local_c, local_out, device, comm=None):
+        self.desc, self.device, self.comm = desc, device, comm
+        self.compute = torch.cuda.current_stream(device)
+        self.h2d = torch.cuda.Stream(device)
+        self.d2h = torch.cuda.Stream(device)
+        mk = lambda shp: [torch.empty(shp, dtype=torch.float64, device=device) for _ in range(2)]  # noqa: E731
+        self.dA, self.dB = mk(local_a), mk(local_b)
+        self.dC = mk(local_c) if desc.beta != 0.0 else [None, None]
+        self.dOut = mk(local_out)
+        self.nscr = B.gemm_mp_scratch_size(desc)
+        self.scratch = torch.empty(self.nscr, dtype=torch.uint8, device=device)
+        self.ws, self.ws_bytes = None, 0
+        self.plans = []
+
+    def _ensure_ws(self, nbytes):
+        if nbytes > self.ws_bytes:
+            raw = torch.empty(nbytes + 1024, dtype=torch.uint8, device=self.device)
+            off = (-raw.data_ptr()) % 1024
+            self._ws_raw, self.ws, self.ws_bytes = raw, raw[off:off + nbytes], nbytes
+
+    def reserve(self, hA, hB, hC=None):
+        """Size the workspace outside any timed region (one plan on the first inputs)."""
+        self.dA[0].copy_(hA)
+        self.dB[0].copy_(hB)
+        if hC is not None:
+            self.dC[0].copy_(hC)
+        pl = B.gemm_mp_plan(self.desc, self.dA[0], self.dA[0].stride(0), self.dB[0], self.dB[0].stride(0),
+                            self.dC[0], self.dC[0].stride(0) if self.dC[0] is not None else 0,
+                            self.scratch, self.nscr, self.comm, self.compute)
+        self._ensure_ws(B.gemm_mp_workspace_size(pl))
+        B.gemm_mp_destroy(pl)
+        torch.cuda.synchronize(self.device)
+
+    def run(self, hA, hB, hC, hOut):
+        """Process len(hA) steps: hOut[k] <- alpha hA[k] hB[k] + beta hC[k] (host tensors)."""
+        K = len(hA)
+        h2d_done = [torch.cuda.Event() for _ in range(K)]
+        convert_done = [torch.cuda.Event() for _ in range(K)]
+        exec_done = [torch.cuda.Event() for _ in range(K)]
+        d2h_done = [torch.cuda.Event() for _ in range(K)]
+
+        def enqueue_h2d(k):
+            b = k % 2
+            with torch.cuda.stream(self.h2d):
+                if k >= 2:
+                    self.h2d.wait_event(convert_done[k - 2])   # buffers b free once step k-2 is packed
+                self.dA[b].copy_(hA[k], non_blocking=True)
+                self.dB[b].copy_(hB[k], non_blocking=True)
+                if self.dC[b] is not None:
+                    self.dC[b].copy_(hC[k], non_blocking=True)
+                h2d_done[k].record(self.h2d)
+
+        enqueue_h2d(0)
+        for k in range(K):
+            b = k % 2
+            if k + 1 < K:
+                enqueue_h2d(k + 1)                              # before plan's host sync
+            self.compute.wait_event(h2d_done[k])
+            dC = self.dC[b]
+            pl = B.gemm_mp_plan(self.desc, self.dA[b], self.dA[b].stride(0), self.dB[b], self.dB[b].stride(0),
+                                dC, dC.stride(0) if dC is not None else 0, self.scratch, self.nscr, self.comm,
+                                self.compute)
+            self.plans.append(pl)
+            nws = B.gemm_mp_workspace_size(pl)
+            if nws > self.ws_bytes:
+                raise RuntimeError("HostPipeline: workspace larger than reserved (call reserve first)")
+            B.gemm_mp_convert(pl, self.ws, nws, self.compute)
+            convert_done[k].record(self.compute)
+            if k >= 2:
+                self.compute.wait_event(d2h_done[k - 2])        # result buffer b read back
+            B.gemm_mp_execute(pl, self.dOut[b], self.dOut[b].stride(0), self.compute)
+            exec_done[k].record(self.compute)
+            with torch.cuda.stream(self.d2h):
+                self.d2h.wait_event(exec_done[k])
+                hOut[k].copy_(self.dOut[b], non_blocking=True)
+                d2h_done[k].record(self.d2h)
+        self.compute.wait_event(d2h_done[K - 1])
+        self.compute.wait_stream(self.h2d)
+
+    def close(self):
+        torch.cuda.synchronize(self.device)
+        for pl in self.plans:
+            B.gemm_mp_destroy(pl)
+        self.plans = []
