@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <memory>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -53,6 +54,93 @@ static gmp_status_t fail(gmp_status_t s, const std::string& msg) {
   } while (0)
 
 static inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// ---------------------------------------------------------------------------
+// metadata transfers without the copy engines
+// ---------------------------------------------------------------------------
+// The host tables (KB-MB: job lists, pairs, items, tile codes) move through
+// mapped pinned host memory that a kernel reads (H2D) or writes (D2H) over PCIe,
+// so they never queue behind a caller's multi-GB cudaMemcpyAsync on a copy
+// engine -- api.HostPipeline overlaps exactly such copies with plan / convert /
+// execute.  Stages come from a process-wide grow-only pool; one is reusable
+// once the event recorded after its last kernel has completed.
+namespace {
+struct Stage {
+  uint8_t* h = nullptr;   // host (mapped, pinned)
+  uint8_t* d = nullptr;   // device alias
+  size_t cap = 0;
+  cudaEvent_t done = nullptr;
+  int dev = -1;
+  bool busy = false;
+};
+std::mutex g_stage_mu;
+std::vector<Stage*> g_stages;
+
+__global__ void k_xfer(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t n) {
+  // 16-byte chunks (src/dst 16-byte aligned), byte tail
+  const int64_t n16 = n >> 4;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = t; i < n16; i += stride)
+    reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+  for (int64_t i = (n16 << 4) + t; i < n; i += stride) dst[i] = src[i];
+}
+}  // namespace
+
+static Stage* stage_acquire(size_t bytes) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(g_stage_mu);
+  for (Stage* s : g_stages)
+    if (!s->busy && s->dev == dev && s->cap >= bytes && cudaEventQuery(s->done) == cudaSuccess) {
+      s->busy = true;
+      return s;
+    }
+  Stage* s = new Stage;
+  s->cap = (size_t)align_up((int64_t)std::max<size_t>(bytes, (size_t)1 << 20), 1 << 20);
+  if (cudaHostAlloc((void**)&s->h, s->cap, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
+      cudaHostGetDevicePointer((void**)&s->d, s->h, 0) != cudaSuccess ||
+      cudaEventCreateWithFlags(&s->done, cudaEventDisableTiming) != cudaSuccess) {
+    delete s;
+    return nullptr;
+  }
+  s->dev = dev;
+  s->busy = true;
+  g_stages.push_back(s);
+  return s;
+}
+
+static void stage_release(Stage* s, cudaStream_t stream) {
+  cudaEventRecord(s->done, stream);
+  std::lock_guard<std::mutex> lk(g_stage_mu);
+  s->busy = false;
+}
+
+static int xfer_grid(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n / 16 + 255) / 256, 148)); }
+
+// batch of host -> device table uploads through one stage
+struct Upload {
+  struct Item { const void* src; uint8_t* dst; int64_t bytes; };
+  std::vector<Item> items;
+  void add(uint8_t* dst, const void* src, int64_t bytes) { if (bytes > 0) items.push_back({src, dst, bytes}); }
+  gmp_status_t run(cudaStream_t stream) {
+    if (items.empty()) return GMP_OK;
+    int64_t total = 0;
+    for (const Item& it : items) total += align_up(it.bytes, 16);
+    Stage* st = stage_acquire((size_t)total);
+    if (!st) return fail(GMP_ERR_CUDA, "pinned staging buffer allocation failed");
+    int64_t o = 0;
+    for (const Item& it : items) {
+      std::memcpy(st->h + o, it.src, (size_t)it.bytes);
+      k_xfer<<<xfer_grid(it.bytes), 256, 0, stream>>>(st->d + o, it.dst, it.bytes);
+      o += align_up(it.bytes, 16);
+    }
+    const cudaError_t e = cudaGetLastError();
+    stage_release(st, stream);
+    items.clear();
+    if (e != cudaSuccess) return fail(GMP_ERR_CUDA, std::string("k_xfer: ") + cudaGetErrorString(e));
+    return GMP_OK;
+  }
+};
 
 // Packed layout (O6): FP64/FP32 operand payloads are MN-major (A tiles
 // column-major, B tiles row-major) for the outer-product SIMT/DMMA kernels;
@@ -690,7 +778,9 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
     }
   StatsJob* djobs = (StatsJob*)(sc + L.jobs);
   if (!jobs.empty()) {
-    GMP_CUDA(cudaMemcpyAsync(djobs, jobs.data(), jobs.size() * sizeof(StatsJob), cudaMemcpyHostToDevice, stream));
+    Upload up;
+    up.add((uint8_t*)djobs, jobs.data(), (int64_t)(jobs.size() * sizeof(StatsJob)));
+    GMP_TRY(up.run(stream));
     k_tile_stats<<<(unsigned)jobs.size(), 256, 0, stream>>>(djobs, (int)nb, S, Mx, F);
     GMP_CUDA(cudaGetLastError());
   }
@@ -708,9 +798,13 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
   int16_t* scin = (int16_t*)(sc + L.scin);
   int* status = (int*)(sc + L.status);
   uint8_t* maps = sc + L.maps;
-  if (d.a_map) GMP_CUDA(cudaMemcpyAsync(maps, d.a_map, pl->nA, cudaMemcpyHostToDevice, stream));
-  if (d.b_map) GMP_CUDA(cudaMemcpyAsync(maps + pl->nA, d.b_map, pl->nB, cudaMemcpyHostToDevice, stream));
-  if (d.c_map) GMP_CUDA(cudaMemcpyAsync(maps + pl->nA + pl->nB, d.c_map, pl->nC, cudaMemcpyHostToDevice, stream));
+  {
+    Upload up;
+    if (d.a_map) up.add(maps, d.a_map, pl->nA);
+    if (d.b_map) up.add(maps + pl->nA, d.b_map, pl->nB);
+    if (d.c_map) up.add(maps + pl->nA + pl->nB, d.c_map, pl->nC);
+    GMP_TRY(up.run(stream));
+  }
   FinalizeArgs fa{};
   fa.mt = pl->mt; fa.nt = pl->nt; fa.kt = pl->kt; fa.nb = (int)nb;
   fa.tol = d.tol; fa.alpha = d.alpha; fa.beta = d.beta; fa.mask = d.class_mask | 1u;
@@ -727,14 +821,33 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
   pl->codeA.resize(pl->nA); pl->codeB.resize(pl->nB); pl->codeC.resize(pl->nC);
   pl->sA5.resize(pl->nA * 5); pl->sB5.resize(pl->nB * 5); pl->sCin.resize(pl->nC); pl->sCout.assign(pl->nC, 0);
   int h_status = 0;
-  GMP_CUDA(cudaMemcpyAsync(pl->codeA.data(), codes, pl->nA, cudaMemcpyDeviceToHost, stream));
-  GMP_CUDA(cudaMemcpyAsync(pl->codeB.data(), codes + pl->nA, pl->nB, cudaMemcpyDeviceToHost, stream));
-  GMP_CUDA(cudaMemcpyAsync(pl->codeC.data(), codes + pl->nA + pl->nB, pl->nC, cudaMemcpyDeviceToHost, stream));
-  GMP_CUDA(cudaMemcpyAsync(pl->sA5.data(), s5, pl->nA * 10, cudaMemcpyDeviceToHost, stream));
-  GMP_CUDA(cudaMemcpyAsync(pl->sB5.data(), s5 + pl->nA * 5, pl->nB * 10, cudaMemcpyDeviceToHost, stream));
-  GMP_CUDA(cudaMemcpyAsync(pl->sCin.data(), scin, pl->nC * 2, cudaMemcpyDeviceToHost, stream));
-  GMP_CUDA(cudaMemcpyAsync(&h_status, status, sizeof(int), cudaMemcpyDeviceToHost, stream));
-  GMP_CUDA(cudaStreamSynchronize(stream));
+  {
+    // codes, scales and status -> mapped host memory by a kernel, then the sync
+    const int64_t nall = pl->nA + pl->nB + pl->nC;
+    const int64_t o_s5 = align_up(nall, 16), o_scin = o_s5 + align_up((pl->nA + pl->nB) * 10, 16),
+                  o_st = o_scin + align_up(pl->nC * 2, 16), total = o_st + 16;
+    Stage* st = stage_acquire((size_t)total);
+    if (!st) return fail(GMP_ERR_CUDA, "pinned staging buffer allocation failed");
+    k_xfer<<<xfer_grid(nall), 256, 0, stream>>>(codes, st->d, nall);
+    k_xfer<<<xfer_grid((pl->nA + pl->nB) * 10), 256, 0, stream>>>((const uint8_t*)s5, st->d + o_s5,
+                                                                 (pl->nA + pl->nB) * 10);
+    k_xfer<<<xfer_grid(pl->nC * 2), 256, 0, stream>>>((const uint8_t*)scin, st->d + o_scin, pl->nC * 2);
+    k_xfer<<<1, 32, 0, stream>>>((const uint8_t*)status, st->d + o_st, (int64_t)sizeof(int));
+    const cudaError_t e1 = cudaGetLastError();
+    const cudaError_t e2 = cudaStreamSynchronize(stream);
+    if (e1 == cudaSuccess && e2 == cudaSuccess) {
+      std::memcpy(pl->codeA.data(), st->h, pl->nA);
+      std::memcpy(pl->codeB.data(), st->h + pl->nA, pl->nB);
+      std::memcpy(pl->codeC.data(), st->h + pl->nA + pl->nB, pl->nC);
+      std::memcpy(pl->sA5.data(), st->h + o_s5, pl->nA * 10);
+      std::memcpy(pl->sB5.data(), st->h + o_s5 + pl->nA * 10, pl->nB * 10);
+      std::memcpy(pl->sCin.data(), st->h + o_scin, pl->nC * 2);
+      std::memcpy(&h_status, st->h + o_st, sizeof(int));
+    }
+    stage_release(st, stream);
+    GMP_CUDA(e1);
+    GMP_CUDA(e2);
+  }
   if (h_status == 4) return fail(GMP_ERR_NONFINITE, "A, B or C holds a NaN or an infinity");
   if (G > 1) {
     GridComms gc{};
@@ -854,24 +967,20 @@ extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_byte
   pl->ws = ws;
   const int64_t nb = pl->d.nb;
   // job tables
-  auto up = [&](int64_t off, const void* src, size_t bytes) -> gmp_status_t {
-    if (bytes) GMP_CUDA(cudaMemcpyAsync(ws + off, src, bytes, cudaMemcpyHostToDevice, stream));
-    return GMP_OK;
-  };
+  Upload tables;
   std::vector<ShadowJob> allsh = pl->shadow_local;
   for (auto& v : pl->shadow_step) allsh.insert(allsh.end(), v.begin(), v.end());
-  GMP_TRY(up(pl->off_pack, pl->pack.data(), pl->pack.size() * sizeof(PackJob)));
-  GMP_TRY(up(pl->off_shadow, allsh.data(), allsh.size() * sizeof(ShadowJob)));
-  GMP_TRY(up(pl->off_items, pl->items.data(), pl->items.size() * sizeof(WorkItem)));
-  GMP_TRY(up(pl->off_pairs, pl->pairs.data(), pl->pairs.size() * sizeof(PairDesc)));
-  {
-    std::vector<SplitJob> allsp = pl->split_local;
-    for (auto& v : pl->split_step) allsp.insert(allsp.end(), v.begin(), v.end());
-    GMP_TRY(up(pl->off_split, allsp.data(), allsp.size() * sizeof(SplitJob)));
-    std::vector<SliceJob> allsl = pl->slice_local;
-    for (auto& v : pl->slice_step) allsl.insert(allsl.end(), v.begin(), v.end());
-    GMP_TRY(up(pl->off_slice, allsl.data(), allsl.size() * sizeof(SliceJob)));
-  }
+  std::vector<SplitJob> allsp = pl->split_local;
+  for (auto& v : pl->split_step) allsp.insert(allsp.end(), v.begin(), v.end());
+  std::vector<SliceJob> allsl = pl->slice_local;
+  for (auto& v : pl->slice_step) allsl.insert(allsl.end(), v.begin(), v.end());
+  tables.add(ws + pl->off_pack, pl->pack.data(), (int64_t)(pl->pack.size() * sizeof(PackJob)));
+  tables.add(ws + pl->off_shadow, allsh.data(), (int64_t)(allsh.size() * sizeof(ShadowJob)));
+  tables.add(ws + pl->off_items, pl->items.data(), (int64_t)(pl->items.size() * sizeof(WorkItem)));
+  tables.add(ws + pl->off_pairs, pl->pairs.data(), (int64_t)(pl->pairs.size() * sizeof(PairDesc)));
+  tables.add(ws + pl->off_split, allsp.data(), (int64_t)(allsp.size() * sizeof(SplitJob)));
+  tables.add(ws + pl->off_slice, allsl.data(), (int64_t)(allsl.size() * sizeof(SliceJob)));
+  GMP_TRY(tables.run(stream));
   if (oz_prepare(pl->oz, ws, pl->arena_off[6], pl->arena_slots[6], (int)nb) != GMP_OK)
     return fail(GMP_ERR_CUDA, "cuTensorMapEncodeTiled (digit arena) failed");
   GMP_TRY(tc_prepare(pl->tc, ws, pl->arena_off, pl->arena_slots, (int)nb));
@@ -911,7 +1020,11 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
     const int64_t il = (uint32_t)t.pad >> 16, jl = t.pad & 0xFFFF;
     t.user_off = il * nb * ldc + jl * nb;
   }
-  if (nCl) GMP_CUDA(cudaMemcpyAsync(ws + pl->off_ctd, pl->ctd.data(), nCl * sizeof(CTileDesc), cudaMemcpyHostToDevice, stream));
+  {
+    Upload up;
+    up.add(ws + pl->off_ctd, pl->ctd.data(), (int64_t)(nCl * sizeof(CTileDesc)));
+    GMP_TRY(up.run(stream));
+  }
   const CTileDesc* dct = (const CTileDesc*)(ws + pl->off_ctd);
   if (nCl) {
     k_acc_init<<<dim3(grid_for(nb2, 1) / 4 + 1, (unsigned)nCl), 256, 0, stream>>>(dct, ws, nb2, pl->d.beta);
