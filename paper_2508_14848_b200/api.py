@@ -178,7 +178,10 @@ class HostPipeline:
             self.plans.append(pl)
             nws = B.gemm_mp_workspace_size(pl)
             if nws > self.ws_bytes:
-                raise RuntimeError("HostPipeline: workspace larger than reserved (call reserve first)")
+                # another input's maps need more slots: grow (torch's allocator frees the
+                # old block in stream order, and every use of it is on this stream)
+                with torch.cuda.stream(self.compute):
+                    self._ensure_ws(nws)
             B.gemm_mp_convert(pl, self.ws, nws, self.compute)
             convert_done[k].record(self.compute)
             if k >= 2:
