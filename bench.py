@@ -80,7 +80,7 @@ def class_peaks(peaks, fp32_on_tensor=True, fp64_on_int8=False, figure="bf16_tfl
 # ---------------------------------------------------------------------------
 class Clocks:
     def __init__(self, index):
-        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.samples, self.reasons, self.max_mhz, self.power = [], set(), None, []
         self._stop = threading.Event()
         try:
             import pynvml
@@ -104,6 +104,10 @@ class Clocks:
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
                 try:
+                    self.power.append(nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
+                except Exception:
+                    pass
+                try:
                     r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 except Exception:
                     r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
@@ -124,7 +128,8 @@ class Clocks:
             self._stop.set()
             self.t.join()
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
-                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "power_w_median": statistics.median(self.power) if self.power else None}
 
 
 # ---------------------------------------------------------------------------
