@@ -23,6 +23,7 @@
 #include "gmp_simt.cuh"
 #include "gmp_tc.cuh"
 #include "gmp_ozaki.cuh"
+#include "gmp_tc2.cuh"
 
 using namespace gmp;
 
@@ -157,7 +158,8 @@ static inline int16_t layout_transposed(int role, int cls) {
 // ---------------------------------------------------------------------------
 struct Launch {
   int step, cls, kind;  // kind 0: SIMT/DMMA kernel, 1: tcgen05, 2: FP64 DFMA cross-check, 3: FP32 on tcgen05
-                        // (BF16x9), 4: FP64 on the INT8 tensor pipe (Ozaki digits)
+                        // (BF16x9), 4: FP64 on the INT8 tensor pipe (Ozaki digits), 5: tcgen05 on an SM
+                        // pair (cta_group::2, 256 x 256 sub-tiles)
   int64_t ibeg, icount;
   int bn;  // N of the class kernel's CTA tile
 };
@@ -664,6 +666,15 @@ static void build_tables(gmp_plan_s* pl) {
       bool w64 = false;
       for (const WorkItem& wi : its) w64 = w64 || pl->ctd[wi.ctile].code == 0;
       const int tcbn = (w64 ? 128 : tc_bn((int)nb));
+      // 16-bit / 8-bit classes folding into binary32 W on 256-multiple tiles run on
+      // SM pairs (k_tc2_class, cta_group::2); GMP_TC2=0 in the environment keeps
+      // them on the 1-SM kernel (A/B measurements)
+      static const bool tc2_env = !(getenv("GMP_TC2") && atoi(getenv("GMP_TC2")) == 0);
+      const bool pair = tc && !w64 && c >= 2 && (nb % 256 == 0) && tc2_env;
+      if (pair) {
+        pl->launches.push_back(Launch{s, c, 5, ibeg, (int64_t)its.size() * tc2_subtiles_per_item((int)nb), TC2_BN});
+        continue;
+      }
       // flat launch size: items x sub-tiles of the class kernel's CTA tile
       const int bn = ozaki ? OZ_BN : split ? 128 : tc ? tcbn : mn_bn(c);
       pl->launches.push_back(Launch{s, c, kind, ibeg, (int64_t)its.size() * subtiles_per_item((int)nb, bn), bn});
@@ -1070,6 +1081,8 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
       if (L.kind == 4) {
         const cudaError_t e = oz_launch(pl->oz, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, pl->off_oexp, stream);
         if (e != cudaSuccess) return fail(GMP_ERR_CUDA, std::string("k_tc_fp64 launch: ") + cudaGetErrorString(e));
+      } else if (L.kind == 5) {
+        GMP_TRY(tc2_launch(pl->tc, L.cls, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, stream));
       } else if (L.kind == 1 || L.kind == 3) {
         GMP_TRY(tc_launch(pl->tc, L.kind == 3 ? 5 : L.cls, L.bn, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha,
                           stream));

@@ -29,6 +29,9 @@ def _cases():
                                                    seed=43)),
         ("fp64_only", gmp_inputs.small_workload(512, 512, 512, 128, 1e-12, mode="random", E=10, beta=1.0,
                                                 class_mask=0b00001, seed=44)),
+        # nb = 512: 2 x 2 sub-tiles of 256 x 256 per C tile on the SM-pair kernel (k_tc2_class)
+        ("pairs_nb512", gmp_inputs.small_workload(1024, 1536, 1536, 512, 1e-2, mode="random", E=24, beta=0.75,
+                                                  class_mask=0b11111, seed=45)),
     ]
 
 
