@@ -68,6 +68,10 @@ typedef enum {
                                  per element, 28 tcgen05 kind::i8 MMAs) instead of DMMA (default)    */
 #define GMP_FLAG_FP32_FFMA 4u /* FP32 class on the FP32 pipe (packed FFMA2, bitwise O8) instead of the
                                  default tensor-pipe path (exact BF16x3 split, nine BF16 MMAs per block) */
+#define GMP_FLAG_TC_PAIR 32u /* FP16/BF16/E4M3 launches whose C tiles fold into binary32 W and whose
+                                 nb is a multiple of 256 run on SM pairs (tcgen05 cta_group::2, 256 x 256
+                                 sub-tiles, half the B bytes per SM).  Opt-in: under the board power
+                                 cap it measured 4-8 % slower than the 1-SM kernel    */
 #define GMP_FLAG_SENDER_SIDE 16u /* SURVEY 8(f) NEXT-2, hybrid conversion (PAPER.md:148 defers it): a
                                  SUMMA panel tile whose receivers in its process row (A) / column (B)
                                  together need a set of classes S whose payloads are smaller than the

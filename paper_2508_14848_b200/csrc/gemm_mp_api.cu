@@ -666,11 +666,9 @@ static void build_tables(gmp_plan_s* pl) {
       bool w64 = false;
       for (const WorkItem& wi : its) w64 = w64 || pl->ctd[wi.ctile].code == 0;
       const int tcbn = (w64 ? 128 : tc_bn((int)nb));
-      // 16-bit / 8-bit classes folding into binary32 W on 256-multiple tiles run on
-      // SM pairs (k_tc2_class, cta_group::2); GMP_TC2=0 in the environment keeps
-      // them on the 1-SM kernel (A/B measurements)
-      static const bool tc2_env = !(getenv("GMP_TC2") && atoi(getenv("GMP_TC2")) == 0);
-      const bool pair = tc && !w64 && c >= 2 && (nb % 256 == 0) && tc2_env;
+      // GMP_FLAG_TC_PAIR: 16-bit / 8-bit classes folding into binary32 W on
+      // 256-multiple tiles run on SM pairs (k_tc2_class, cta_group::2)
+      const bool pair = tc && !w64 && c >= 2 && (nb % 256 == 0) && (d.flags & GMP_FLAG_TC_PAIR);
       if (pair) {
         pl->launches.push_back(Launch{s, c, 5, ibeg, (int64_t)its.size() * tc2_subtiles_per_item((int)nb), TC2_BN});
         continue;

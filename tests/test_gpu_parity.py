@@ -29,9 +29,12 @@ def _cases():
                                                    seed=43)),
         ("fp64_only", gmp_inputs.small_workload(512, 512, 512, 128, 1e-12, mode="random", E=10, beta=1.0,
                                                 class_mask=0b00001, seed=44)),
-        # nb = 512: 2 x 2 sub-tiles of 256 x 256 per C tile on the SM-pair kernel (k_tc2_class)
+        # nb = 512 with GMP_FLAG_TC_PAIR: 2 x 2 sub-tiles of 256 x 256 per C tile on the
+        # SM-pair kernel (k_tc2_class); the plain nb = 512 run covers the 1-SM kernel
         ("pairs_nb512", gmp_inputs.small_workload(1024, 1536, 1536, 512, 1e-2, mode="random", E=24, beta=0.75,
-                                                  class_mask=0b11111, seed=45)),
+                                                  class_mask=0b11111, seed=45), B.GMP_FLAG_TC_PAIR),
+        ("nb512", gmp_inputs.small_workload(1024, 1536, 1536, 512, 1e-2, mode="random", E=24, beta=0.75,
+                                            class_mask=0b11111, seed=45)),
     ]
 
 
@@ -40,11 +43,12 @@ CASES = _cases()
 
 @pytest.fixture(scope="module", params=CASES, ids=[c[0] for c in CASES])
 def case(request):
-    name, w = request.param
+    name, w = request.param[:2]
+    flags = request.param[2] if len(request.param) > 2 else 0
     A, Bm, C = w.matrices()
     orc = run_oracle(A, Bm, C, w.nb, w.tol, w.alpha, w.beta, w.class_mask)
     assert orc["rc"] == 0
-    g, (Cg, Cg2) = run_gpu(A, Bm, C, w.nb, w.tol, w.alpha, w.beta, w.class_mask, reps=2)
+    g, (Cg, Cg2) = run_gpu(A, Bm, C, w.nb, w.tol, w.alpha, w.beta, w.class_mask, flags=flags, reps=2)
     gs, (Cs,) = run_gpu(A, Bm, C, w.nb, w.tol, w.alpha, w.beta, w.class_mask, flags=B.GMP_FLAG_SIMT_ONLY)
     return dict(name=name, w=w, A=A, B=Bm, C=C, orc=orc, g=g, Cg=Cg, Cg2=Cg2, gs=gs, Cs=Cs)
 
