@@ -72,6 +72,9 @@ typedef enum {
                                  nb is a multiple of 256 run on SM pairs (tcgen05 cta_group::2, 256 x 256
                                  sub-tiles, half the B bytes per SM).  Opt-in: under the board power
                                  cap it measured 4-8 % slower than the 1-SM kernel    */
+#define GMP_FLAG_TC_MCAST 64u /* same launches as GMP_FLAG_TC_PAIR, but each SM keeps its own 1-SM MMA
+                                 (M = 128) and only the B box is split and multicast across a 2-CTA
+                                 cluster (a third fewer L2->SM bytes, no cross-SM operand reads)     */
 #define GMP_FLAG_SENDER_SIDE 16u /* SURVEY 8(f) NEXT-2, hybrid conversion (PAPER.md:148 defers it): a
                                  SUMMA panel tile whose receivers in its process row (A) / column (B)
                                  together need a set of classes S whose payloads are smaller than the

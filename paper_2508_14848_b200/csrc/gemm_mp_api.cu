@@ -159,7 +159,8 @@ static inline int16_t layout_transposed(int role, int cls) {
 struct Launch {
   int step, cls, kind;  // kind 0: SIMT/DMMA kernel, 1: tcgen05, 2: FP64 DFMA cross-check, 3: FP32 on tcgen05
                         // (BF16x9), 4: FP64 on the INT8 tensor pipe (Ozaki digits), 5: tcgen05 on an SM
-                        // pair (cta_group::2, 256 x 256 sub-tiles)
+                        // pair (cta_group::2, 256 x 256 sub-tiles), 6: 1-SM tcgen05 with B multicast
+                        // across a 2-CTA cluster
   int64_t ibeg, icount;
   int bn;  // N of the class kernel's CTA tile
 };
@@ -669,8 +670,10 @@ static void build_tables(gmp_plan_s* pl) {
       // GMP_FLAG_TC_PAIR: 16-bit / 8-bit classes folding into binary32 W on
       // 256-multiple tiles run on SM pairs (k_tc2_class, cta_group::2)
       const bool pair = tc && !w64 && c >= 2 && (nb % 256 == 0) && (d.flags & GMP_FLAG_TC_PAIR);
-      if (pair) {
-        pl->launches.push_back(Launch{s, c, 5, ibeg, (int64_t)its.size() * tc2_subtiles_per_item((int)nb), TC2_BN});
+      const bool mcast = tc && !w64 && c >= 2 && (nb % 256 == 0) && (d.flags & GMP_FLAG_TC_MCAST) && !pair;
+      if (pair || mcast) {
+        pl->launches.push_back(Launch{s, c, pair ? 5 : 6, ibeg, (int64_t)its.size() * tc2_subtiles_per_item((int)nb),
+                                      TC2_BN});
         continue;
       }
       // flat launch size: items x sub-tiles of the class kernel's CTA tile
@@ -1081,6 +1084,8 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
         if (e != cudaSuccess) return fail(GMP_ERR_CUDA, std::string("k_tc_fp64 launch: ") + cudaGetErrorString(e));
       } else if (L.kind == 5) {
         GMP_TRY(tc2_launch(pl->tc, L.cls, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, stream));
+      } else if (L.kind == 6) {
+        GMP_TRY(tcmc_launch(pl->tc, L.cls, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, stream));
       } else if (L.kind == 1 || L.kind == 3) {
         GMP_TRY(tc_launch(pl->tc, L.kind == 3 ? 5 : L.cls, L.bn, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha,
                           stream));

@@ -35,6 +35,8 @@ def _cases():
                                                   class_mask=0b11111, seed=45), B.GMP_FLAG_TC_PAIR),
         ("nb512", gmp_inputs.small_workload(1024, 1536, 1536, 512, 1e-2, mode="random", E=24, beta=0.75,
                                             class_mask=0b11111, seed=45)),
+        ("mcast_nb512", gmp_inputs.small_workload(1024, 1536, 1536, 512, 1e-2, mode="random", E=24, beta=0.75,
+                                                  class_mask=0b11111, seed=45), B.GMP_FLAG_TC_MCAST),
     ]
 
 
