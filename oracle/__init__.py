@@ -72,8 +72,9 @@ def _p(a):
     return a.ctypes.data_as(ct.c_void_p) if a is not None else None
 
 
-PAYLOAD_DTYPE = {0: np.uint64, 1: np.uint32, 2: np.uint16, 3: np.uint16, 4: np.uint8}
-CLASS_NAMES = ["FP64", "FP32", "FP16", "BF16", "E4M3"]
+PAYLOAD_DTYPE = {0: np.uint64, 1: np.uint32, 2: np.uint16, 3: np.uint16, 4: np.uint8, 5: np.uint8}
+CLASS_NAMES = ["FP64", "FP32", "FP16", "BF16", "E4M3", "E5M2"]
+NCLS = len(CLASS_NAMES)
 
 
 # ---- O1 generator -----------------------------------------------------------
@@ -207,8 +208,8 @@ def gemm_mp(A, B, C, nb, tol, alpha=1.0, beta=0.0, class_mask=0b01111, ctiles=No
     maps = [None if m is None else np.ascontiguousarray(m, np.uint8) for m in (a_map, b_map, c_map)]
     d = _Desc(M, N, K, nb, tol, alpha, beta, class_mask, *[_p(m) for m in maps])
     o = dict(acode=np.zeros((mt, kt), np.uint8), bcode=np.zeros((kt, nt), np.uint8),
-             ccode=np.zeros((mt, nt), np.uint8), ascale5=np.zeros((mt, kt, 5), np.int16),
-             bscale5=np.zeros((kt, nt, 5), np.int16), cscale=np.zeros((mt, nt), np.int16),
+             ccode=np.zeros((mt, nt), np.uint8), ascale5=np.zeros((mt, kt, NCLS), np.int16),
+             bscale5=np.zeros((kt, nt, NCLS), np.int16), cscale=np.zeros((mt, nt), np.int16),
              cin_scale=np.zeros((mt, nt), np.int16),
              SA=np.zeros((mt, kt)), MA=np.zeros((mt, kt)), SB=np.zeros((kt, nt)),
              MB=np.zeros((kt, nt)), SC=np.zeros((mt, nt)), MC=np.zeros((mt, nt)))

@@ -87,7 +87,9 @@ void orc_synth_block(int64_t rows, int64_t cols, int32_t nb, uint64_t seed, int 
 
 /* ------------------------------------------------------------------------- */
 /* O2. Number formats and round-to-nearest-even from binary64 (O2).  */
-/*     Class codes: 0 FP64, 1 FP32, 2 FP16, 3 BF16, 4 E4M3 (OCP "FN").          */
+/*     Class codes: 0 FP64, 1 FP32, 2 FP16, 3 BF16, 4 E4M3 (OCP "FN"),         */
+/*     5 E5M2 (OCP, IEEE-like inf/NaN).  Codes are ordered by */
+/*     unit roundoff, so a pair's class is max(code_A, code_B).                   */
 /* ------------------------------------------------------------------------- */
 typedef struct {
     int p;          /* fraction (trailing significand) bits          */
@@ -102,12 +104,14 @@ typedef struct {
     int bytes;
 } orc_fmt_t;
 
-static const orc_fmt_t ORC_FMT[5] = {
+#define ORC_NCLS 6
+static const orc_fmt_t ORC_FMT[ORC_NCLS] = {
     /* FP64 */ {52, 11, 1023, -1022, 0x1.fffffffffffffp+1023, 0, 0x1p-53, 0x1p-1074, 0.0, 8},
     /* FP32 */ {23, 8, 127, -126, 0x1.fffffep+127, 0, 0x1p-24, 0x1p-149, 1.0, 4},
     /* FP16 */ {10, 5, 15, -14, 65504.0, 0, 0x1p-11, 0x1p-24, 65504.0, 2},
     /* BF16 */ {7, 8, 127, -126, 0x1.fep+127, 0, 0x1p-8, 0x1p-133, 1.0, 2},
     /* E4M3 */ {3, 4, 7, -6, 448.0, 1, 0x1p-4, 0x1p-9, 448.0, 1},
+    /* E5M2 */ {2, 5, 15, -14, 57344.0, 0, 0x1p-3, 0x1p-16, 57344.0, 1},
 };
 
 int orc_class_bytes(int cls) { return ORC_FMT[cls].bytes; }
@@ -255,9 +259,10 @@ void orc_tile_stats(const double *X, int64_t ld, int64_t mt, int64_t nt, int32_t
 
 /* ------------------------------------------------------------------------- */
 /* O5. Precision map for an input matrix A or B (O5, readings R1-R5, */
-/*     R13, R14).  Ladder: E4M3, BF16, FP16, FP32, FP64; first eligible wins.   */
+/*     R13, R14).  Ladder: E5M2, E4M3, BF16, FP16, FP32, FP64 (enabled classes;  */
+/*     lowest precision first); first eligible wins.                           */
 /* ------------------------------------------------------------------------- */
-static const int ORC_LADDER[5] = {4, 3, 2, 1, 0};
+static const int ORC_LADDER[ORC_NCLS] = {5, 4, 3, 2, 1, 0};
 
 /* delta_k = u_k + sqrt(nb) * u_acc(k); u_acc = u64 for FP64, u32 otherwise */
 double orc_delta(int cls, int32_t nb) {
@@ -282,7 +287,7 @@ int orc_map_input(int64_t mt, int64_t nt, int32_t nb, double tol, uint32_t class
     for (int64_t t = 0; t < ntiles; ++t) {
         int chosen = 0;
         if (!isinf(SX)) {
-            for (int li = 0; li < 5; ++li) {
+            for (int li = 0; li < ORC_NCLS; ++li) {
                 int k = ORC_LADDER[li];
                 if (!(mask & (1u << k))) continue;
                 if (k == 0) { chosen = 0; break; }
@@ -306,7 +311,7 @@ static void orc_store_elem(void *payload, int64_t idx, int cls, double x) {
     if (cls == 0) { ((double *)payload)[idx] = x; return; }
     uint32_t b = orc_encode(x, cls);
     if (cls == 1) ((uint32_t *)payload)[idx] = b;
-    else if (cls == 4) ((uint8_t *)payload)[idx] = (uint8_t)b;
+    else if (cls >= 4) ((uint8_t *)payload)[idx] = (uint8_t)b;
     else ((uint16_t *)payload)[idx] = (uint16_t)b;
 }
 
@@ -315,7 +320,7 @@ double orc_payload_value(const void *payload, int64_t idx, int cls) {
     if (cls == 0) return ((const double *)payload)[idx];
     uint32_t b;
     if (cls == 1) b = ((const uint32_t *)payload)[idx];
-    else if (cls == 4) b = ((const uint8_t *)payload)[idx];
+    else if (cls >= 4) b = ((const uint8_t *)payload)[idx];
     else b = ((const uint16_t *)payload)[idx];
     return orc_decode(b, cls);
 }
@@ -323,7 +328,7 @@ double orc_payload_value(const void *payload, int64_t idx, int cls) {
 /* Payload layout (O6 "Packed layout"): element (r,c) of a tile is at
  * payload[r*nb + c] (not transposed) or payload[c*nb + r] (transposed).
  *   FP64 / FP32 classes: MN-major operands -- A transposed (column-major), B not;
- *   FP16 / BF16 / E4M3 classes: K-major operands -- A not transposed, B transposed;
+ *   FP16 / BF16 / E4M3 / E5M2 classes: K-major operands -- A not transposed, B transposed;
  *   C tiles (packed C_in / C_out): not transposed.
  * role: 0 = A, 1 = B, 2 = C. */
 int orc_layout_transposed(int role, int cls) {
@@ -371,7 +376,7 @@ int orc_shadow_tile(const void *payload, int32_t nb, int role, int from, int fro
 
 /* ------------------------------------------------------------------------- */
 /* O7. Precision map for C (output estimate; O7, R9, R23).          */
-/* ascale/bscale: [tile][5] class-c scales of A and B tiles (stored or shadow)*/
+/* ascale/bscale: [tile][6] class-c scales of A and B tiles (stored or shadow)*/
 /* for every c >= code; entries for c < code are ignored.                      */
 /* ------------------------------------------------------------------------- */
 int orc_map_c(int64_t mt, int64_t nt, int64_t kt, int32_t nb, double tol, double alpha,
@@ -405,7 +410,7 @@ int orc_map_c(int64_t mt, int64_t nt, int64_t kt, int32_t nb, double tol, double
             double sc = (beta != 0.0) ? SC[i * nt + j] : 0.0;
             double nhat = (aa * RA) * QB + ab * sqrt(sc);
             int chosen = 0;
-            for (int li = 0; li < 5; ++li) {
+            for (int li = 0; li < ORC_NCLS; ++li) {
                 int k = ORC_LADDER[li];
                 if (!(mask & (1u << k))) continue;
                 if (k == 0) { chosen = 0; break; }
@@ -423,7 +428,7 @@ int orc_map_c(int64_t mt, int64_t nt, int64_t kt, int32_t nb, double tol, double
                 for (int64_t l = 0; ok && l < kt; ++l) {
                     int ca = acode[i * kt + l], cb = bcode[l * nt + j];
                     int c = ca > cb ? ca : cb;
-                    int ea = ascale[(i * kt + l) * 5 + c], eb = bscale[(l * nt + j) * 5 + c];
+                    int ea = ascale[(i * kt + l) * ORC_NCLS + c], eb = bscale[(l * nt + j) * ORC_NCLS + c];
                     double fct = ldexp(alpha, -(ea + eb));
                     if (fct != 0.0 && !(fabs(fct) >= 0x1p-126 && fabs(fct) <= 0x1p100)) ok = 0;
                 }
@@ -546,7 +551,7 @@ typedef struct {
 typedef struct {
     /* outputs sized by the caller: mt*kt, kt*nt, mt*nt */
     uint8_t *acode, *bcode, *ccode;
-    int16_t *ascale5, *bscale5;   /* [tile][5]: class-c scale for c >= code, else 0 */
+    int16_t *ascale5, *bscale5;   /* [tile][ORC_NCLS]: class-c scale for c >= code, else 0 */
     int16_t *cscale;              /* finalize scale of each computed C tile        */
     int16_t *cin_scale;           /* scale of packed C_in (beta != 0)              */
     double *SA, *MA, *SB, *MB, *SC, *MC;
@@ -610,8 +615,8 @@ int orc_gemm_mp(const orc_desc_t *d, const double *A, int64_t lda, const double 
             }
         }
     }
-    void **Ap = calloc((size_t)nA * 5, sizeof(void *));
-    void **Bp = calloc((size_t)nB * 5, sizeof(void *));
+    void **Ap = calloc((size_t)nA * ORC_NCLS, sizeof(void *));
+    void **Bp = calloc((size_t)nB * ORC_NCLS, sizeof(void *));
 #pragma omp parallel for schedule(dynamic)
     for (int64_t t = 0; t < nA + nB; ++t) {
         int isB = t >= nA;
@@ -622,14 +627,14 @@ int orc_gemm_mp(const orc_desc_t *d, const double *A, int64_t lda, const double 
         const double *tp = X + (tt / ncols) * nb * ld + (tt % ncols) * nb;
         int code = isB ? o->bcode[tt] : o->acode[tt];
         int keep = isB ? needB[tt] : needA[tt];
-        int16_t *s5 = isB ? o->bscale5 + tt * 5 : o->ascale5 + tt * 5;
-        void **pp = isB ? Bp + tt * 5 : Ap + tt * 5;
+        int16_t *s5 = isB ? o->bscale5 + tt * ORC_NCLS : o->ascale5 + tt * ORC_NCLS;
+        void **pp = isB ? Bp + tt * ORC_NCLS : Ap + tt * ORC_NCLS;
         void *tmp = malloc((size_t)tsz * 8);
-        for (int c = 0; c < 5; ++c) s5[c] = 0;
+        for (int c = 0; c < ORC_NCLS; ++c) s5[c] = 0;
         s5[code] = isB ? sb[tt] : sa[tt];
         pp[code] = malloc((size_t)tsz * ORC_FMT[code].bytes);
         orc_pack_tile(tp, ld, nb, code, s5[code], orc_layout_transposed(isB, code), pp[code]);
-        for (int c = code + 1; c < 5; ++c) {
+        for (int c = code + 1; c < ORC_NCLS; ++c) {
             void *dst = keep ? malloc((size_t)tsz * ORC_FMT[c].bytes) : tmp;
             s5[c] = (int16_t)orc_shadow_tile(pp[code], nb, isB, code, s5[code], c, dst);
             if (keep) pp[c] = dst;
@@ -677,10 +682,10 @@ int orc_gemm_mp(const orc_desc_t *d, const double *A, int64_t lda, const double 
                         for (int64_t l = s0; l < s1; ++l) {
                             int ca = o->acode[i * kt + l], cb = o->bcode[l * nt + j];
                             if ((ca > cb ? ca : cb) != c) continue;
-                            orc_tile_gemm(c, Ap[(i * kt + l) * 5 + c], Bp[(l * nt + j) * 5 + c],
+                            orc_tile_gemm(c, Ap[(i * kt + l) * ORC_NCLS + c], Bp[(l * nt + j) * ORC_NCLS + c],
                                           nb, P);
-                            orc_fold(nb, codec, d->alpha, o->ascale5[(i * kt + l) * 5 + c],
-                                     o->bscale5[(l * nt + j) * 5 + c], P, acc);
+                            orc_fold(nb, codec, d->alpha, o->ascale5[(i * kt + l) * ORC_NCLS + c],
+                                     o->bscale5[(l * nt + j) * ORC_NCLS + c], P, acc);
                         }
                     }
                 }
@@ -691,8 +696,8 @@ int orc_gemm_mp(const orc_desc_t *d, const double *A, int64_t lda, const double 
         }
         o->threads = nthreads;
     }
-    for (int64_t t = 0; t < nA * 5; ++t) free(Ap[t]);
-    for (int64_t t = 0; t < nB * 5; ++t) free(Bp[t]);
+    for (int64_t t = 0; t < nA * ORC_NCLS; ++t) free(Ap[t]);
+    for (int64_t t = 0; t < nB * ORC_NCLS; ++t) free(Bp[t]);
     free(Ap); free(Bp); free(fA); free(fB); free(fC); free(sa); free(sb);
     return rc;
 }

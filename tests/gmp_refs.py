@@ -42,6 +42,22 @@ def e4m3_values():
     return np.arange(256, dtype=np.uint32), np.array(vals)
 
 
+def e5m2_values():
+    """OCP FP8 E5M2: bias 15, IEEE-like (S.11111.00 = inf, S.11111.xx = NaN), max 57344."""
+    vals = []
+    for b in range(256):
+        s = -1.0 if b & 0x80 else 1.0
+        e = (b >> 2) & 0x1F
+        m = b & 3
+        if e == 31:
+            vals.append(s * np.inf if m == 0 else np.nan)
+        elif e == 0:
+            vals.append(s * m * 2.0 ** -16)
+        else:
+            vals.append(s * (1 + m / 4) * 2.0 ** (e - 15))
+    return np.arange(256, dtype=np.uint32), np.array(vals)
+
+
 class NearestEven:
     """Round-to-nearest, ties to the pattern with even last bit, over a value set."""
 

@@ -11,7 +11,7 @@ import pytest
 import oracle
 import gmp_refs as refs
 
-FP32, FP16, BF16, E4M3 = 1, 2, 3, 4
+FP32, FP16, BF16, E4M3, E5M2 = 1, 2, 3, 4, 5
 
 
 def _midpoint_probe(vals):
@@ -51,7 +51,7 @@ def test_bf16_decode_exhaustive():
 def _check_nearest_even(cls, bits, vals, x, sat):
     ne = refs.NearestEven(bits, vals, None)
     got = oracle.encode(x, cls)
-    sign_shift = {BF16: 15, E4M3: 7}[cls]
+    sign_shift = {BF16: 15, E4M3: 7, E5M2: 7}[cls]
     for xi, gi in zip(x, got):
         r = ne.round_abs(Fraction(abs(float(xi))))
         if r is None:
@@ -102,6 +102,51 @@ def test_e4m3_encode_exhaustive_nearest_even_satfinite():
     assert oracle.encode(np.array([-1e30]), E4M3)[0] == 0xFE
 
 
+def test_e5m2_decode_all_256_vs_torch_float8():
+    """E5M2: every pattern against torch.float8_e5m2 (a library
+    decoder) and against the enumeration of the OCP format in tests/gmp_refs.py"""
+    import torch
+    bits, vals = refs.e5m2_values()
+    lib = torch.arange(256, dtype=torch.int32).to(torch.uint8).view(torch.float8_e5m2).to(torch.float64).numpy()
+    got = oracle.decode(bits, E5M2)
+    for ref in (vals, lib):
+        assert np.array_equal(np.isnan(got), np.isnan(ref))
+        ok = ~np.isnan(ref)
+        assert np.array_equal(got[ok], ref[ok])
+    assert np.nanmax(got[np.isfinite(got)]) == 57344.0 and got[0x01] == 2.0 ** -16 and got[0x7C] == np.inf
+
+
+def test_e5m2_encode_exhaustive_nearest_even():
+    bits, vals = refs.e5m2_values()
+    fin = np.isfinite(vals)
+    x = _midpoint_probe(vals[fin])
+    x = np.concatenate([x, [2.0 ** -17, np.nextafter(2.0 ** -17, 1), 3 * 2.0 ** -18, 1 + 2 ** -3 + 2 ** -40]])
+    _check_nearest_even(E5M2, bits[fin], vals[fin], x, sat=False)
+
+
+def test_e5m2_encode_vs_torch_float8():
+    """float32-representable probes (random, midpoints, midpoints +- 1 ulp32) against
+    torch's float32 -> float8_e5m2 conversion (round to nearest even)"""
+    import torch
+    _, vals = refs.e5m2_values()
+    v = np.unique(vals[np.isfinite(vals) & (vals >= 0)]).astype(np.float32)
+    mids = ((v[:-1].astype(np.float64) + v[1:]) / 2).astype(np.float32)    # exact in binary32
+    rng = np.random.default_rng(5)
+    rnd = (rng.standard_normal(20000) * np.exp2(rng.integers(-18, 16, 20000))).astype(np.float32)
+    x = np.concatenate([v, mids, np.nextafter(mids, np.float32(np.inf)), np.nextafter(mids, np.float32(0)), rnd])
+    x = np.concatenate([x, -x])
+    x = x[np.abs(x) <= 57344.0]
+    want = torch.from_numpy(x).to(torch.float8_e5m2).view(torch.uint8).numpy().astype(np.uint32)
+    got = oracle.encode(x.astype(np.float64), E5M2)
+    assert np.array_equal(got, want)
+
+
+def test_e5m2_overflow_is_infinity():
+    # IEEE-like: RN beyond 57344 (ties at 61440 go to the even 2^16) is +-inf
+    got = oracle.encode(np.array([57344.0, 61439.99, 61440.0, 1e9, -1e9]), E5M2)
+    assert list(got) == [0x7B, 0x7B, 0x7C, 0x7C, 0xFC]
+
+
 def test_fp32_encode_vs_hardware_cast():
     rng = np.random.default_rng(1)
     x = np.concatenate([
@@ -129,7 +174,7 @@ def test_fp32_roundtrip_identity():
     assert np.array_equal(back, f)
 
 
-@pytest.mark.parametrize("cls,omega", [(FP32, 1.0), (FP16, 65504.0), (BF16, 1.0), (E4M3, 448.0)])
+@pytest.mark.parametrize("cls,omega", [(FP32, 1.0), (FP16, 65504.0), (BF16, 1.0), (E4M3, 448.0), (E5M2, 57344.0)])
 def test_scale_exp_definition(cls, omega):
     """e = largest integer with maxabs*2^e <= Omega' (checked from the definition
     with exact power-of-two scaling), on edges, subnormals and random values."""
@@ -150,4 +195,5 @@ def test_scale_exp_closed_forms():
         m, E = np.frexp(x)
         assert oracle.scale_exp(x, FP16) == (16 - E if m <= 0.99951171875 else 15 - E)
         assert oracle.scale_exp(x, E4M3) == (9 - E if m <= 0.875 else 8 - E)
+        assert oracle.scale_exp(x, E5M2) == (16 - E if m <= 0.875 else 15 - E)   # 57344 = 0.875 2^16
         assert oracle.scale_exp(x, FP32) == (1 - E if m == 0.5 else -E)

@@ -12,7 +12,7 @@ import gmp_inputs
 import oracle
 import gmp_refs as refs
 
-FP64, FP32, FP16, BF16, E4M3 = range(5)
+FP64, FP32, FP16, BF16, E4M3, E5M2 = range(6)
 
 
 def _payload(vals, cls, kmajor=False):
@@ -46,7 +46,7 @@ def _fraction_tile_gemm(a, b, cls):
     return P
 
 
-@pytest.mark.parametrize("cls", [FP64, FP32, FP16, BF16, E4M3])
+@pytest.mark.parametrize("cls", [FP64, FP32, FP16, BF16, E4M3, E5M2])
 def test_tile_gemm_bitwise_vs_fraction_emulation(cls):
     nb = 8
     rng = np.random.default_rng(10 + cls)
@@ -62,11 +62,11 @@ def test_tile_gemm_bitwise_vs_fraction_emulation(cls):
 
 
 @pytest.mark.parametrize("cls,u", [(FP64, 2.0 ** -53), (FP32, 2.0 ** -24), (FP16, 2.0 ** -24),
-                                   (BF16, 2.0 ** -24), (E4M3, 2.0 ** -24)])
+                                   (BF16, 2.0 ** -24), (E4M3, 2.0 ** -24), (E5M2, 2.0 ** -24)])
 def test_tile_gemm_gamma_bound(cls, u):
     nb = 64
     rng = np.random.default_rng(20 + cls)
-    scale = {FP16: 100.0, E4M3: 10.0}.get(cls, 1.0)
+    scale = {FP16: 100.0, E4M3: 10.0, E5M2: 100.0}.get(cls, 1.0)
     pa = _payload(rng.standard_normal((nb, nb)) * scale, cls)
     pb = _payload(rng.standard_normal((nb, nb)) * scale, cls, kmajor=True)
     av = _values(pa, cls, "A", nb)
@@ -142,7 +142,7 @@ def test_cfg1_meets_tolerance_and_mixes_classes(variant):
 
 
 @pytest.mark.parametrize("tol,mask,E", [(1e-3, 0b11111, 30), (1e-2, 0b11111, 40), (1e-5, 0b01111, 22),
-                                        (1e-9, 0b01111, 22)])
+                                        (1e-9, 0b01111, 22), (1e-2, 0b111111, 40), (0.1, 0b111111, 48)])
 def test_small_workloads_meet_tolerance(tol, mask, E):
     w = gmp_inputs.small_workload(256, 192, 320, 64, tol, mode="random", E=E, beta=0.5,
                                   class_mask=mask, seed=E)

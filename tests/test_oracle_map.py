@@ -13,9 +13,10 @@ import pytest
 import gmp_inputs
 import oracle
 
-FP64, FP32, FP16, BF16, E4M3 = range(5)
+FP64, FP32, FP16, BF16, E4M3, E5M2 = range(6)
 ALL = 0b11111
 NOE4 = 0b01111
+ALL6 = 0b111111   # with E5M2
 
 
 @pytest.mark.parametrize("nb,k", [(32, 0), (128, -3), (64, 5), (256, -40)])
@@ -68,6 +69,10 @@ def _const_grid(vals, nb):
     (0.3, 0b00111, FP16),   # BF16/E4M3 disabled
     (0.3, 0b00011, FP32),
     (0.3, 0b00001, FP64),
+    # delta_E5M2 (nb=128) = 2^-3 + sqrt(128) 2^-24 = 0.1250007: eligible iff tol/4 >= it
+    (0.3, ALL6, E4M3),      # eps 0.075 < delta_E5M2
+    (0.6, ALL6, E5M2),      # eps 0.15
+    (0.6, 0b101111, E5M2),  # E4M3 off, E5M2 on
 ])
 def test_map_equal_constant_tiles_closed_form(tol, mask, want):
     nb = 128
@@ -105,6 +110,28 @@ def test_map_hand_built_grid():
     # E4M3 448 -> 2^8 * 2^-k scale
     assert scale[0, 0] == 0 and scale[0, 1] == 5 + 15 and scale[0, 3] == 9
     assert scale[1, 2] == 20 + 8 and scale[3, 3] == 0
+
+
+def test_map_hand_built_grid_with_e5m2():
+    """The grid above with E5M2 enabled: delta_E5M2 = 2^-3 + sqrt(32) 2^-24 -> r <= 2.5e-4 /
+    (4 * 0.125) = 5.0e-4.  Only the 2^-20 tiles (r ~ 9.5e-7) and the zero tile (first enabled
+    ladder class) move from E4M3 to E5M2; their E5M2 scale targets 57344 = 0.875 2^16
+    (value 2^-20 -> e = 20 + 15)."""
+    v = np.array([[1.0, 2 ** -5, 2 ** -5, 2 ** -9],
+                  [2 ** -5, 2 ** -9, 2 ** -20, 2 ** -20],
+                  [2 ** -5, 2 ** -9, 2 ** -20, 2 ** -9],
+                  [2 ** -20, 2 ** -20, 2 ** -9, 0.0]])
+    nb = 32
+    X = _const_grid(v, nb)
+    S, M, F = oracle.tile_stats(X, nb)
+    rc, code, scale = oracle.map_input(S, M, nb, 1e-3, ALL6, F)
+    want = np.array([[FP32, FP16, FP16, BF16],
+                     [FP16, BF16, E5M2, E5M2],
+                     [FP16, BF16, E5M2, BF16],
+                     [E5M2, E5M2, BF16, E5M2]])
+    assert rc == 0
+    assert np.array_equal(code, want), code
+    assert scale[1, 2] == 20 + 15 and scale[3, 3] == 0
 
 
 def test_map_all_zero_matrix():
@@ -195,7 +222,8 @@ def test_pack_fp64_is_copy():
 
 
 @pytest.mark.parametrize("role", ["A", "B"])
-@pytest.mark.parametrize("frm,to", [(0, 1), (0, 2), (0, 4), (1, 2), (1, 3), (2, 3), (2, 4), (3, 4), (1, 4)])
+@pytest.mark.parametrize("frm,to", [(0, 1), (0, 2), (0, 4), (1, 2), (1, 3), (2, 3), (2, 4), (3, 4), (1, 4),
+                                    (0, 5), (1, 5), (2, 5), (3, 5), (4, 5)])
 def test_shadow_is_receiver_side_rounding_of_stored(frm, to, role):
     """Shadow = RN_to(decoded stored tile) with the scale chosen for the decoded
     tile (R7), in the target class's layout: check against the pinned encoder
