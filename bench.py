@@ -61,6 +61,9 @@ def load_peaks():
             "fallback (B200_PROFILING.md)"
 
 
+NCLS = 6   # FP64, FP32, FP16, BF16, E4M3, E5M2 (include/gemm_mp.h gmp_class_t)
+
+
 def class_peaks(peaks, fp32_on_tensor=True, fp64_on_int8=False, figure="bf16_tflops_sustained"):
     """Peak of the hardware path each class runs on.
     `figure` picks the measured BF16 number: the burst one when the timed
@@ -72,7 +75,7 @@ def class_peaks(peaks, fp32_on_tensor=True, fp64_on_int8=False, figure="bf16_tfl
     bf16 = peaks.get(figure, peaks.get("bf16_tflops"))
     fp64 = 2 * bf16 / 28.0 if fp64_on_int8 else ALU_PEAK_TFLOPS[0]
     fp32 = bf16 / 9.0 if fp32_on_tensor else ALU_PEAK_TFLOPS[1]
-    return {0: fp64, 1: fp32, 2: bf16, 3: bf16, 4: 2 * bf16}
+    return {0: fp64, 1: fp32, 2: bf16, 3: bf16, 4: 2 * bf16, 5: 2 * bf16}
 
 
 # ---------------------------------------------------------------------------
@@ -152,7 +155,7 @@ def oracle_pair_sample(w, mix, n_pairs, threads, seed=0):
         counts[int(np.argmax(mix))] += 1
     while sum(counts) > n_pairs:
         counts[int(np.argmax(counts))] -= 1
-    classes = [c for c in range(5) for _ in range(counts[c])]
+    classes = [c for c in range(len(counts)) for _ in range(counts[c])]
     jobs = []
     for c in classes:
         i, j, l = int(rng.integers(mt)), int(rng.integers(nt)), int(rng.integers(kt))
@@ -193,7 +196,7 @@ def cpu_baseline(w, mix, threads=None):
 
 
 def gmp_class_name(c):
-    return ["FP64", "FP32", "FP16", "BF16", "E4M3"][c]
+    return ["FP64", "FP32", "FP16", "BF16", "E4M3", "E5M2"][c]
 
 
 def run_reference(a, w, rank):
@@ -406,23 +409,24 @@ def main():
     fig_name = "bf16 burst" if hot else "bf16 sustained"
     cpk = class_peaks(peaks, figure=figure)
     st = stats[-1]
-    class_ms = [statistics.mean(s["class_ms"][c] for s in stats) for c in range(5)]
-    dom = max(range(5), key=lambda c: class_ms[c])
+    class_ms = [statistics.mean(s["class_ms"][c] for s in stats) for c in range(NCLS)]
+    dom = max(range(NCLS), key=lambda c: class_ms[c])
     # precision-induced load imbalance: per-rank tile-GEMM device time
     busy = [sum(class_ms)]
     if G > 1:
         busy = [None] * G
         dist.all_gather_object(busy, sum(class_ms))
-    flops_local = [2.0 * w.nb ** 3 * st["pairs_local"][c] for c in range(5)]
+    flops_local = [2.0 * w.nb ** 3 * st["pairs_local"][c] for c in range(NCLS)]
     achieved = flops_local[dom] / (class_ms[dom] * 1e-3) / 1e12 if class_ms[dom] > 0 else 0.0
     dom_peak = cpk[dom]
     # precision-mix roofline: sum_c F_c / (G * Peak_c) vs the step time
-    t_roof_ms = sum(st["flops"][c] / (G * cpk[c] * 1e12) for c in range(5)) * 1e3
+    t_roof_ms = sum(st["flops"][c] / (G * cpk[c] * 1e12) for c in range(NCLS)) * 1e3
     exec_ms = statistics.median(ph[2] for ph in phase)
     # DRAM traffic per launch of the dominant kernel from the committed ncu capture
     traffic = None
     try:
-        kpref = {0: "k_dmma<", 1: "k_tc_class<5,", 2: "k_tc_class<2,", 3: "k_tc_class<3,", 4: "k_tc_class<4,"}[dom]
+        kpref = {0: "k_dmma<", 1: "k_tc_class<9,", 2: "k_tc_class<2,", 3: "k_tc_class<3,", 4: "k_tc_class<4,",
+                 5: "k_tc_class<5,"}[dom]
         with open(os.path.join(ROOT, "profiles", "traffic_r01.json")) as f:
             tr = json.load(f)
         # per-launch bytes only describe the captured launch configuration
@@ -457,7 +461,7 @@ def main():
             "execute_tflops": w.flops / (exec_ms * 1e-3) / 1e12,
             "precision_mix_roofline": {"t_roof_ms": t_roof_ms, "frac_of_step": t_roof_ms / ms_step,
                                        "frac_of_execute": t_roof_ms / exec_ms,
-                                       "class_peaks_tflops": {gmp_class_name(c): round(cpk[c], 1) for c in range(5)},
+                                       "class_peaks_tflops": {gmp_class_name(c): round(cpk[c], 1) for c in range(NCLS)},
                                        "peak_source": peak_src + " " + fig_name},
             "mix": {"tiles_a": st["tiles_a"], "tiles_b": st["tiles_b"], "tiles_c": st["tiles_c"],
                     "pairs": st["pairs"]},
@@ -473,14 +477,14 @@ def main():
                                          if dom == 0 else
                                          peak_src + " " + fig_name + " / 9 (FP32 class = 9 BF16 MMAs per product)"
                                          if dom == 1 else peak_src + " " + fig_name +
-                                         (" x 2 (E4M3)" if dom == 4 else ""))},
+                                         (" x 2 (FP8)" if dom >= 4 else ""))},
             "e2e": e2e,
             "gpu_launches": launches * a.steps,
             "gpu_launches_per_step": launches,
             "clocks": clk,
         }
         if G == 1 and not a.no_cpu_baseline:
-            mix = [st["pairs"][c] for c in range(5)]
+            mix = [st["pairs"][c] for c in range(NCLS)]
             out["cpu_baseline"] = cpu_baseline(w, mix)
         print(json.dumps(out), flush=True)
     if comm is not None:

@@ -45,7 +45,8 @@ extern "C" {
 /* Precision classes, ordered by unit roundoff; the class
  * of a tile-GEMM is max(code_A, code_B) = the lower of its operands' precisions
  * (north_star; R6). */
-typedef enum { GMP_FP64 = 0, GMP_FP32 = 1, GMP_FP16 = 2, GMP_BF16 = 3, GMP_E4M3 = 4 } gmp_class_t;
+typedef enum { GMP_FP64 = 0, GMP_FP32 = 1, GMP_FP16 = 2, GMP_BF16 = 3, GMP_E4M3 = 4, GMP_E5M2 = 5 } gmp_class_t;
+#define GMP_NCLASS_ABI 6   /* classes; ordered by unit roundoff, so a pair's class is max(code_A, code_B) */
 
 typedef enum {
   GMP_OK = 0,
@@ -89,7 +90,7 @@ typedef struct {
   int32_t nb;          /* tile edge; multiple of 128 dividing M, N, K (PAPER.md:179 uses 1024/2048) */
   double tol;          /* accuracy tolerance: ||C - C_fp64||_F <= tol (|a| ||A|| ||B|| + |b| ||C||) */
   double alpha, beta;  /* GEMM scalars; beta == 0 means C is not read (BLAS convention)          */
-  uint32_t class_mask; /* bit c enables class c (gmp_class_t); FP64 always on; E4M3 opt-in        */
+  uint32_t class_mask; /* bit c enables class c (gmp_class_t); FP64 always on; E4M3/E5M2 opt-in   */
   uint32_t flags;      /* GMP_FLAG_*                                                           */
   int32_t P, Q, rank;  /* process grid and this rank (= p*Q + q); 1, 1, 0 on one GPU            */
   /* optional explicit per-tile codes (host, row-major global tile grids: mt x kt, kt x nt,
@@ -102,20 +103,20 @@ typedef struct gmp_plan_s *gmp_plan_t;
 /* Run statistics (gemm_mp_get_stats). Counts are global (identical on every rank)
  * except the *_local fields. */
 typedef struct {
-  int64_t tiles_a[5], tiles_b[5], tiles_c[5]; /* tiles per stored class                  */
-  int64_t pairs[5];                           /* tile-GEMMs per pair class (global)      */
-  double flops[5];                            /* 2 nb^3 x pairs[c]                       */
-  int64_t pairs_local[5];                     /* tile-GEMMs this rank computes            */
-  int64_t shadows_local[5];                   /* shadow tiles this rank materialises      */
+  int64_t tiles_a[6], tiles_b[6], tiles_c[6]; /* tiles per stored class                  */
+  int64_t pairs[6];                           /* tile-GEMMs per pair class (global)      */
+  double flops[6];                            /* 2 nb^3 x pairs[c]                       */
+  int64_t pairs_local[6];                     /* tile-GEMMs this rank computes            */
+  int64_t shadows_local[6];                   /* shadow tiles this rank materialises      */
   int64_t packed_bytes_local;                 /* packed A/B payload bytes stored locally  */
   int64_t recv_bytes_local;                   /* SUMMA panel bytes this rank receives     */
   int64_t workspace_bytes;
   int32_t steps;                              /* SUMMA steps (K tiles / step depth)        */
   int32_t launches_execute;                   /* kernels one gemm_mp_execute launches      */
   int32_t launches_plan, launches_convert;    /* kernels of gemm_mp_plan / gemm_mp_convert */
-  double class_ms[5];                         /* GMP_FLAG_TIMING: device ms of the class-c tile-GEMM
+  double class_ms[6];                         /* GMP_FLAG_TIMING: device ms of the class-c tile-GEMM
                                                  launches of the last execute (waits for them) */
-  int32_t class_launches[5];                  /* launches per class in one execute             */
+  int32_t class_launches[6];                  /* launches per class in one execute             */
 } gmp_stats_t;
 
 /* Device scratch needed by gemm_mp_plan (tile statistics + maps; KB-sized).     */
@@ -161,9 +162,9 @@ gmp_status_t gemm_mp_get_maps(gmp_plan_t plan, uint8_t *a, uint8_t *b, uint8_t *
                               int16_t *b_scale, int16_t *c_scale);
 
 /* Copies one LOCAL tile's payload to host memory: which = 'A' or 'B' (class
- * `cls` = the stored code or a materialised shadow class; cls = 5: the three
- * K-major BF16 parts of the FP32 class's tensor-pipe split; cls = 6: the seven
- * int8 digit planes of the FP64 class's INT8 path), 'C' (packed C_out of
+ * `cls` = the stored code or a materialised shadow class (0..5); cls = 6: the
+ * three K-major BF16 parts of the FP32 class's tensor-pipe split; cls = 7: the
+ * seven int8 digit planes of the FP64 class's INT8 path), 'C' (packed C_out of
  * the last execute, cls = code), 'I' (packed C_in), 'W' (accumulator, binary64
  * or binary32).  (ti, tj) are GLOBAL tile indices.  *bytes in: capacity, out:
  * bytes written; *scale receives the tile's power-of-two scale.  Synchronous. */
@@ -174,7 +175,7 @@ gmp_status_t gemm_mp_get_stats(gmp_plan_t plan, gmp_stats_t *out);
 
 /* Host-only plan from given maps (no device work): the same tile lists, arena
  * layout, work lists and SUMMA schedule as gemm_mp_plan builds after its map
- * kernels.  acode/bcode/ccode: global code grids; ascale5/bscale5: [tile][5]
+ * kernels.  acode/bcode/ccode: global code grids; ascale5/bscale5: [tile][6]
  * class-c scales; cin_scale may be NULL.  For inspecting the schedule and the
  * multi-rank bookkeeping without a GPU (convert/execute on it fail with
  * GMP_ERR_STATE until a workspace is given).                                   */

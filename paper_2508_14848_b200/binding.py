@@ -12,8 +12,10 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgemm_mp.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "gemm_mp.h")
 
-GMP_FP64, GMP_FP32, GMP_FP16, GMP_BF16, GMP_E4M3 = range(5)
-CLASS_NAMES = ["FP64", "FP32", "FP16", "BF16", "E4M3"]
+GMP_FP64, GMP_FP32, GMP_FP16, GMP_BF16, GMP_E4M3, GMP_E5M2 = range(6)
+CLASS_NAMES = ["FP64", "FP32", "FP16", "BF16", "E4M3", "E5M2"]
+NCLS = len(CLASS_NAMES)
+TILE_SPLIT, TILE_DIGITS = NCLS, NCLS + 1   # gemm_mp_get_tile cls of the FP32 splits / FP64 digit planes
 CLASS_BYTES = [8, 4, 2, 2, 1]
 GMP_FLAG_SIMT_ONLY = 1
 GMP_FLAG_TIMING = 2
@@ -42,13 +44,13 @@ class gmp_desc_t(ct.Structure):
 
 
 class gmp_stats_t(ct.Structure):
-    _fields_ = [("tiles_a", ct.c_int64 * 5), ("tiles_b", ct.c_int64 * 5), ("tiles_c", ct.c_int64 * 5),
-                ("pairs", ct.c_int64 * 5), ("flops", ct.c_double * 5), ("pairs_local", ct.c_int64 * 5),
-                ("shadows_local", ct.c_int64 * 5), ("packed_bytes_local", ct.c_int64),
+    _fields_ = [("tiles_a", ct.c_int64 * 6), ("tiles_b", ct.c_int64 * 6), ("tiles_c", ct.c_int64 * 6),
+                ("pairs", ct.c_int64 * 6), ("flops", ct.c_double * 6), ("pairs_local", ct.c_int64 * 6),
+                ("shadows_local", ct.c_int64 * 6), ("packed_bytes_local", ct.c_int64),
                 ("recv_bytes_local", ct.c_int64), ("workspace_bytes", ct.c_int64),
                 ("steps", ct.c_int32), ("launches_execute", ct.c_int32),
                 ("launches_plan", ct.c_int32), ("launches_convert", ct.c_int32),
-                ("class_ms", ct.c_double * 5), ("class_launches", ct.c_int32 * 5)]
+                ("class_ms", ct.c_double * 6), ("class_launches", ct.c_int32 * 6)]
 
     def as_dict(self):
         d = {}

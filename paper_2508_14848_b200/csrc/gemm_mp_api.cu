@@ -55,6 +55,7 @@ static gmp_status_t fail(gmp_status_t s, const std::string& msg) {
   } while (0)
 
 static inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+constexpr int NC = GMP_NCLASS;   // precision classes 0..5 (gmp_class_t)
 
 // ---------------------------------------------------------------------------
 // metadata transfers without the copy engines
@@ -191,8 +192,8 @@ struct gmp_plan_s {
   // slots: [global tile][class] -> slot in that class's arena, -1 if absent
   std::vector<int32_t> slotA5, slotB5;
   std::vector<uint8_t> wireA, wireB;     // per panel tile: bitmask of classes broadcast (GMP_FLAG_SENDER_SIDE)
-  int64_t arena_off[7] = {0}, arena_slots[7] = {0};   // 0..4 classes, 5 = FP32 BF16x3 splits,
-  int64_t slot_bytes[7] = {0};                          // 6 = FP64 int8 digit planes (Ozaki)
+  int64_t arena_off[GMP_NARENA] = {0}, arena_slots[GMP_NARENA] = {0};   // 0..5 classes, GMP_AR_SPLIT = FP32
+  int64_t slot_bytes[GMP_NARENA] = {0};   // BF16x3 splits, GMP_AR_SLICE = FP64 int8 digit planes (Ozaki)
   std::vector<int32_t> splitA, splitB;                  // [global tile] -> split slot, -1 if absent
   std::vector<int32_t> sliceA, sliceB;                  // [global tile] -> digit slot, -1 if absent
   bool fp32_tc = false;                                 // FP32 class on the tensor pipe (default)
@@ -279,7 +280,7 @@ static ScratchLayout scratch_layout(const gmp_desc_t* d) {
   L.S = o; o = align_up(o + 2 * n * 8, 256);       // S then maxabs for A|B|C
   L.F = o; o = align_up(o + n, 256);
   L.codes = o; o = align_up(o + n, 256);
-  L.s5 = o; o = align_up(o + (nA + nB) * 5 * 2, 256);
+  L.s5 = o; o = align_up(o + (nA + nB) * NC * 2, 256);
   L.scin = o; o = align_up(o + nC * 2, 256);
   L.status = o; o = align_up(o + 16, 256);
   L.maps = o; o = align_up(o + n, 256);
@@ -303,16 +304,16 @@ static void build_tables(gmp_plan_s* pl) {
   const int64_t nb = d.nb, nb2 = nb * nb, mt = pl->mt, nt = pl->nt, kt = pl->kt;
   const int P = pl->P, Q = pl->Q, p = pl->p, q = pl->q;
   const bool hasC = d.beta != 0.0;
-  for (int c = 0; c < 5; ++c) pl->slot_bytes[c] = nb2 * class_bytes(c);
-  pl->slot_bytes[5] = 3 * nb2 * 2;
-  pl->slot_bytes[6] = OZ_NS * nb2;
+  for (int c = 0; c < NC; ++c) pl->slot_bytes[c] = nb2 * class_bytes(c);
+  pl->slot_bytes[GMP_AR_SPLIT] = 3 * nb2 * 2;
+  pl->slot_bytes[GMP_AR_SLICE] = OZ_NS * nb2;
   pl->fp32_tc = kTcAvailable && !(d.flags & (GMP_FLAG_SIMT_ONLY | GMP_FLAG_FP32_FFMA));
   pl->fp64_tc = kTcAvailable && (d.flags & GMP_FLAG_FP64_INT8) && !(d.flags & GMP_FLAG_SIMT_ONLY);
 
   // ---- which A/B tiles (and classes) this rank needs ----
   std::vector<uint8_t> needSA(pl->nA, 0), needSB(pl->nB, 0), needOA(pl->nA, 0), needOB(pl->nB, 0);
-  std::vector<uint8_t> needA(pl->nA * 5, 0), needB(pl->nB * 5, 0);
-  int64_t pairs_cls[5] = {0}, pairs_loc[5] = {0};
+  std::vector<uint8_t> needA(pl->nA * NC, 0), needB(pl->nB * NC, 0);
+  int64_t pairs_cls[NC] = {0}, pairs_loc[NC] = {0};
   for (int64_t i = 0; i < mt; ++i)
     for (int64_t j = 0; j < nt; ++j)
       for (int64_t l = 0; l < kt; ++l) {
@@ -320,10 +321,10 @@ static void build_tables(gmp_plan_s* pl) {
         pairs_cls[c]++;
         if (i % P != p || j % Q != q) continue;
         pairs_loc[c]++;
-        needA[(i * kt + l) * 5 + ca] = 1;
-        needA[(i * kt + l) * 5 + c] = 1;
-        needB[(l * nt + j) * 5 + cb] = 1;
-        needB[(l * nt + j) * 5 + c] = 1;
+        needA[(i * kt + l) * NC + ca] = 1;
+        needA[(i * kt + l) * NC + c] = 1;
+        needB[(l * nt + j) * NC + cb] = 1;
+        needB[(l * nt + j) * NC + c] = 1;
         if (c == 1 && pl->fp32_tc) { needSA[i * kt + l] = 1; needSB[l * nt + j] = 1; }
         if (c == 0 && pl->fp64_tc) { needOA[i * kt + l] = 1; needOB[l * nt + j] = 1; }
       }
@@ -344,7 +345,7 @@ static void build_tables(gmp_plan_s* pl) {
       for (int64_t j = 0; j < nt; ++j)
         if ((int)(j % Q) != (int)(l % Q)) set |= (uint8_t)(1u << std::max(code, (int)pl->codeB[l * nt + j]));
     int64_t sb = 0;
-    for (int c = 0; c < 5; ++c) if (set >> c & 1) sb += pl->slot_bytes[c];
+    for (int c = 0; c < NC; ++c) if (set >> c & 1) sb += pl->slot_bytes[c];
     pl->wireA[g] = (set && sb < pl->slot_bytes[code]) ? set : (uint8_t)(1u << code);
   }
   for (int64_t g = 0; g < pl->nB; ++g) {
@@ -356,7 +357,7 @@ static void build_tables(gmp_plan_s* pl) {
       for (int64_t i = 0; i < mt; ++i)
         if ((int)(i % P) != (int)(l % P)) set |= (uint8_t)(1u << std::max(code, (int)pl->codeA[i * kt + l]));
     int64_t sb = 0;
-    for (int c = 0; c < 5; ++c) if (set >> c & 1) sb += pl->slot_bytes[c];
+    for (int c = 0; c < NC; ++c) if (set >> c & 1) sb += pl->slot_bytes[c];
     pl->wireB[g] = (set && sb < pl->slot_bytes[code]) ? set : (uint8_t)(1u << code);
   }
   // every panel tile of this process row / column holds slots for its wire
@@ -366,27 +367,27 @@ static void build_tables(gmp_plan_s* pl) {
     if ((g / kt) % P != p) continue;
     const bool root = (int)((g % kt) % Q) == q;
     if (!root && pl->wireA[g] != (1u << pl->codeA[g]))
-      for (int c = 0; c < 5; ++c) needA[g * 5 + c] = 0;
-    for (int c = 0; c < 5; ++c) if (pl->wireA[g] >> c & 1) needA[g * 5 + c] = 1;
+      for (int c = 0; c < NC; ++c) needA[g * NC + c] = 0;
+    for (int c = 0; c < NC; ++c) if (pl->wireA[g] >> c & 1) needA[g * NC + c] = 1;
   }
   for (int64_t g = 0; g < pl->nB; ++g) {
     if ((g % nt) % Q != q) continue;
     const bool root = (int)((g / nt) % P) == p;
     if (!root && pl->wireB[g] != (1u << pl->codeB[g]))
-      for (int c = 0; c < 5; ++c) needB[g * 5 + c] = 0;
-    for (int c = 0; c < 5; ++c) if (pl->wireB[g] >> c & 1) needB[g * 5 + c] = 1;
+      for (int c = 0; c < NC; ++c) needB[g * NC + c] = 0;
+    for (int c = 0; c < NC; ++c) if (pl->wireB[g] >> c & 1) needB[g * NC + c] = 1;
   }
 
   // ---- arena slots ----
-  pl->slotA5.assign(pl->nA * 5, -1);
-  pl->slotB5.assign(pl->nB * 5, -1);
-  int64_t nslots[5] = {0};
+  pl->slotA5.assign(pl->nA * NC, -1);
+  pl->slotB5.assign(pl->nB * NC, -1);
+  int64_t nslots[NC] = {0};
   for (int64_t g = 0; g < pl->nA; ++g)
-    for (int c = 0; c < 5; ++c)
-      if (needA[g * 5 + c]) pl->slotA5[g * 5 + c] = (int32_t)nslots[c]++;
+    for (int c = 0; c < NC; ++c)
+      if (needA[g * NC + c]) pl->slotA5[g * NC + c] = (int32_t)nslots[c]++;
   for (int64_t g = 0; g < pl->nB; ++g)
-    for (int c = 0; c < 5; ++c)
-      if (needB[g * 5 + c]) pl->slotB5[g * 5 + c] = (int32_t)nslots[c]++;
+    for (int c = 0; c < NC; ++c)
+      if (needB[g * NC + c]) pl->slotB5[g * NC + c] = (int32_t)nslots[c]++;
   int64_t nsplit = 0;
   pl->splitA.assign(pl->nA, -1);
   pl->splitB.assign(pl->nB, -1);
@@ -424,7 +425,7 @@ static void build_tables(gmp_plan_s* pl) {
   // count items to size tables
   int64_t n_pairs = 0, n_items = 0;
   for (int s = 0; s < steps; ++s)
-    for (int c = 4; c >= 0; --c)
+    for (int c = NC - 1; c >= 0; --c)
       for (int64_t k = 0; k < nCl; ++k) {
         const int64_t g = pl->locC[k], i = g / nt, j = g % nt;
         int64_t cnt = 0;
@@ -438,11 +439,11 @@ static void build_tables(gmp_plan_s* pl) {
   const int64_t n_pack = (int64_t)pl->locA.size() + (int64_t)pl->locB.size() + (hasC ? nCl : 0);
   int64_t n_shadow_local = 0, n_shadow_recv = 0;
   for (int64_t g = 0; g < pl->nA; ++g)
-    for (int c = pl->codeA[g] + 1; c < 5; ++c)
-      if (needA[g * 5 + c]) ((g % kt) % Q == q ? n_shadow_local : n_shadow_recv)++;
+    for (int c = pl->codeA[g] + 1; c < NC; ++c)
+      if (needA[g * NC + c]) ((g % kt) % Q == q ? n_shadow_local : n_shadow_recv)++;
   for (int64_t g = 0; g < pl->nB; ++g)
-    for (int c = pl->codeB[g] + 1; c < 5; ++c)
-      if (needB[g * 5 + c]) ((g / nt) % P == p ? n_shadow_local : n_shadow_recv)++;
+    for (int c = pl->codeB[g] + 1; c < NC; ++c)
+      if (needB[g * NC + c]) ((g / nt) % P == p ? n_shadow_local : n_shadow_recv)++;
 
   pl->off_pack = o; o = align_up(o + n_pack * (int64_t)sizeof(PackJob), 1024);
   pl->off_split = o; o = align_up(o + nsplit * (int64_t)sizeof(SplitJob), 1024);
@@ -455,17 +456,17 @@ static void build_tables(gmp_plan_s* pl) {
   pl->off_maxbits = o; o = align_up(o + nCl * 8, 1024);
   pl->off_cscale = o; o = align_up(o + nCl * 2, 1024);
   pl->off_tc = o; o = align_up(o + 1024, 1024);
-  for (int c = 0; c < 5; ++c) {
+  for (int c = 0; c < NC; ++c) {
     pl->arena_off[c] = o;
     pl->arena_slots[c] = nslots[c];
     o = align_up(o + nslots[c] * pl->slot_bytes[c], 1024);
   }
-  pl->arena_off[5] = o;
-  pl->arena_slots[5] = nsplit;
-  o = align_up(o + nsplit * pl->slot_bytes[5], 1024);
-  pl->arena_off[6] = o;
-  pl->arena_slots[6] = nslice;
-  o = align_up(o + nslice * pl->slot_bytes[6], 1024);
+  pl->arena_off[GMP_AR_SPLIT] = o;
+  pl->arena_slots[GMP_AR_SPLIT] = nsplit;
+  o = align_up(o + nsplit * pl->slot_bytes[GMP_AR_SPLIT], 1024);
+  pl->arena_off[GMP_AR_SLICE] = o;
+  pl->arena_slots[GMP_AR_SLICE] = nslice;
+  o = align_up(o + nslice * pl->slot_bytes[GMP_AR_SLICE], 1024);
   for (int64_t k = 0; k < nCl; ++k) {
     const int64_t g = pl->locC[k];
     CTileDesc& t = pl->ctd[k];
@@ -489,9 +490,9 @@ static void build_tables(gmp_plan_s* pl) {
     pj.src = pl->A + il * nb * pl->lda + ll * nb;
     pj.ld = pl->lda;
     pj.cls = pl->codeA[g];
-    pj.scale = pl->sA5[g * 5 + pj.cls];
+    pj.scale = pl->sA5[g * NC + pj.cls];
     pj.transpose = layout_transposed(0, pj.cls);
-    pj.dst_off = arena(pj.cls, pl->slotA5[g * 5 + pj.cls]);
+    pj.dst_off = arena(pj.cls, pl->slotA5[g * NC + pj.cls]);
     pl->pack.push_back(pj);
   }
   for (int64_t g : pl->locB) {
@@ -500,9 +501,9 @@ static void build_tables(gmp_plan_s* pl) {
     pj.src = pl->B + ll * nb * pl->ldb + jl * nb;
     pj.ld = pl->ldb;
     pj.cls = pl->codeB[g];
-    pj.scale = pl->sB5[g * 5 + pj.cls];
+    pj.scale = pl->sB5[g * NC + pj.cls];
     pj.transpose = layout_transposed(1, pj.cls);
-    pj.dst_off = arena(pj.cls, pl->slotB5[g * 5 + pj.cls]);
+    pj.dst_off = arena(pj.cls, pl->slotB5[g * NC + pj.cls]);
     pl->pack.push_back(pj);
   }
   if (hasC)
@@ -523,13 +524,13 @@ static void build_tables(gmp_plan_s* pl) {
   pl->shadow_step.assign(steps, {});
   auto add_shadows = [&](bool isB, int64_t g) {
     const int code = isB ? pl->codeB[g] : pl->codeA[g];
-    const int16_t* s5 = (isB ? pl->sB5.data() : pl->sA5.data()) + g * 5;
-    const int32_t* sl = (isB ? pl->slotB5.data() : pl->slotA5.data()) + g * 5;
+    const int16_t* s5 = (isB ? pl->sB5.data() : pl->sA5.data()) + g * NC;
+    const int32_t* sl = (isB ? pl->slotB5.data() : pl->slotA5.data()) + g * NC;
     const bool local = isB ? ((g / nt) % P == p) : ((g % kt) % Q == q);
     const int64_t l = isB ? g / nt : g % kt;
     const uint8_t wire = (isB ? pl->wireB : pl->wireA)[g];
     if (!local && wire && wire != (1u << code)) return;   // every needed class arrives on the wire
-    for (int c = code + 1; c < 5; ++c) {
+    for (int c = code + 1; c < NC; ++c) {
       if (sl[c] < 0) continue;
       ShadowJob sj{};
       sj.src_off = arena(code, sl[code]);
@@ -553,8 +554,8 @@ static void build_tables(gmp_plan_s* pl) {
   auto add_split = [&](bool isB, int64_t g) {
     const int32_t sl = (isB ? pl->splitB : pl->splitA)[g];
     if (sl < 0) return;
-    const int32_t src = (isB ? pl->slotB5 : pl->slotA5)[g * 5 + 1];
-    SplitJob sj{arena(1, src), pl->arena_off[5] + (int64_t)sl * pl->slot_bytes[5]};
+    const int32_t src = (isB ? pl->slotB5 : pl->slotA5)[g * NC + 1];
+    SplitJob sj{arena(1, src), pl->arena_off[GMP_AR_SPLIT] + (int64_t)sl * pl->slot_bytes[GMP_AR_SPLIT]};
     const bool local = isB ? ((g / nt) % P == p) : ((g % kt) % Q == q);
     const int64_t l = isB ? g / nt : g % kt;
     if (local) pl->split_local.push_back(sj);
@@ -568,8 +569,9 @@ static void build_tables(gmp_plan_s* pl) {
   auto add_slice = [&](bool isB, int64_t g) {
     const int32_t sl = (isB ? pl->sliceB : pl->sliceA)[g];
     if (sl < 0) return;
-    const int32_t src = (isB ? pl->slotB5 : pl->slotA5)[g * 5 + 0];
-    SliceJob sj{arena(0, src), pl->arena_off[6] + (int64_t)sl * pl->slot_bytes[6], pl->off_oexp + (int64_t)sl * nb * 2};
+    const int32_t src = (isB ? pl->slotB5 : pl->slotA5)[g * NC + 0];
+    SliceJob sj{arena(0, src), pl->arena_off[GMP_AR_SLICE] + (int64_t)sl * pl->slot_bytes[GMP_AR_SLICE],
+                pl->off_oexp + (int64_t)sl * nb * 2};
     const bool local = isB ? ((g / nt) % P == p) : ((g % kt) % Q == q);
     const int64_t l = isB ? g / nt : g % kt;
     if (local) pl->slice_local.push_back(sj);
@@ -601,18 +603,18 @@ static void build_tables(gmp_plan_s* pl) {
       const int s = (int)(l / GMP_STEP_DEPTH);
       for (int64_t i = p; i < mt; i += P) {       // A(i,l) along process row p, root column l % Q
         const int64_t g = i * kt + l;
-        for (int c = 0; c < 5; ++c) {
+        for (int c = 0; c < NC; ++c) {
           if (!(pl->wireA[g] >> c & 1)) continue;
-          Bcast b{0, (int)(l % Q), g, c, arena(c, pl->slotA5[g * 5 + c]), pl->slot_bytes[c]};
+          Bcast b{0, (int)(l % Q), g, c, arena(c, pl->slotA5[g * NC + c]), pl->slot_bytes[c]};
           pl->bcast_step[s].push_back(b);
           if ((int)(l % Q) != q) recv_bytes += b.bytes;
         }
       }
       for (int64_t j = q; j < nt; j += Q) {       // B(l,j) along process column q, root row l % P
         const int64_t g = l * nt + j;
-        for (int c = 0; c < 5; ++c) {
+        for (int c = 0; c < NC; ++c) {
           if (!(pl->wireB[g] >> c & 1)) continue;
-          Bcast b{1, (int)(l % P), g, c, arena(c, pl->slotB5[g * 5 + c]), pl->slot_bytes[c]};
+          Bcast b{1, (int)(l % P), g, c, arena(c, pl->slotB5[g * NC + c]), pl->slot_bytes[c]};
           pl->bcast_step[s].push_back(b);
           if ((int)(l % P) != p) recv_bytes += b.bytes;
         }
@@ -622,7 +624,7 @@ static void build_tables(gmp_plan_s* pl) {
 
   // ---- pairs and work items ----
   for (int s = 0; s < steps; ++s) {
-    for (int c = 4; c >= 0; --c) {
+    for (int c = NC - 1; c >= 0; --c) {
       const bool tc = kTcAvailable && (c >= 2) && !(d.flags & GMP_FLAG_SIMT_ONLY);
       const int64_t ibeg = (int64_t)pl->items.size();
       std::vector<WorkItem> its;
@@ -633,23 +635,23 @@ static void build_tables(gmp_plan_s* pl) {
           const int ca = pl->codeA[i * kt + l], cb = pl->codeB[l * nt + j];
           if (std::max(ca, cb) != c) continue;
           PairDesc pd{};
-          pd.a_off = arena(c, pl->slotA5[(i * kt + l) * 5 + c]);
-          pd.b_off = arena(c, pl->slotB5[(l * nt + j) * 5 + c]);
-          pd.fexp = -(pl->sA5[(i * kt + l) * 5 + c] + pl->sB5[(l * nt + j) * 5 + c]);
+          pd.a_off = arena(c, pl->slotA5[(i * kt + l) * NC + c]);
+          pd.b_off = arena(c, pl->slotB5[(l * nt + j) * NC + c]);
+          pd.fexp = -(pl->sA5[(i * kt + l) * NC + c] + pl->sB5[(l * nt + j) * NC + c]);
           pd.l = (int32_t)l;
-          pd.a_slot = pl->slotA5[(i * kt + l) * 5 + c];
-          pd.b_slot = pl->slotB5[(l * nt + j) * 5 + c];
+          pd.a_slot = pl->slotA5[(i * kt + l) * NC + c];
+          pd.b_slot = pl->slotB5[(l * nt + j) * NC + c];
           if (c == 0 && pl->fp64_tc) {   // operands are the int8 digit planes
             pd.a_slot = pl->sliceA[i * kt + l];
             pd.b_slot = pl->sliceB[l * nt + j];
-            pd.a_off = pl->arena_off[6] + (int64_t)pd.a_slot * pl->slot_bytes[6];
-            pd.b_off = pl->arena_off[6] + (int64_t)pd.b_slot * pl->slot_bytes[6];
+            pd.a_off = pl->arena_off[GMP_AR_SLICE] + (int64_t)pd.a_slot * pl->slot_bytes[GMP_AR_SLICE];
+            pd.b_off = pl->arena_off[GMP_AR_SLICE] + (int64_t)pd.b_slot * pl->slot_bytes[GMP_AR_SLICE];
           }
           if (c == 1 && pl->fp32_tc) {   // operands are the BF16x3 splits
             pd.a_slot = pl->splitA[i * kt + l];
             pd.b_slot = pl->splitB[l * nt + j];
-            pd.a_off = pl->arena_off[5] + (int64_t)pd.a_slot * pl->slot_bytes[5];
-            pd.b_off = pl->arena_off[5] + (int64_t)pd.b_slot * pl->slot_bytes[5];
+            pd.a_off = pl->arena_off[GMP_AR_SPLIT] + (int64_t)pd.a_slot * pl->slot_bytes[GMP_AR_SPLIT];
+            pd.b_off = pl->arena_off[GMP_AR_SPLIT] + (int64_t)pd.b_slot * pl->slot_bytes[GMP_AR_SPLIT];
           }
           pl->pairs.push_back(pd);
         }
@@ -688,7 +690,7 @@ static void build_tables(gmp_plan_s* pl) {
   for (int64_t g = 0; g < pl->nA; ++g) st.tiles_a[pl->codeA[g]]++;
   for (int64_t g = 0; g < pl->nB; ++g) st.tiles_b[pl->codeB[g]]++;
   for (int64_t g = 0; g < pl->nC; ++g) st.tiles_c[pl->codeC[g]]++;
-  for (int c = 0; c < 5; ++c) {
+  for (int c = 0; c < NC; ++c) {
     st.pairs[c] = pairs_cls[c];
     st.pairs_local[c] = pairs_loc[c];
     st.flops[c] = 2.0 * (double)nb * (double)nb * (double)nb * (double)pairs_cls[c];
@@ -758,11 +760,11 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
     return fail(GMP_ERR_ARG, "operands must be 16-byte aligned with even leading dimensions");
   auto chk_map = [&](const uint8_t* m, int64_t n) {
     if (!m) return true;
-    for (int64_t t = 0; t < n; ++t) if (m[t] > 4) return false;
+    for (int64_t t = 0; t < n; ++t) if (m[t] >= NC) return false;
     return true;
   };
   if (!chk_map(d.a_map, pl->nA) || !chk_map(d.b_map, pl->nB) || !chk_map(d.c_map, pl->nC))
-    return fail(GMP_ERR_MAP_SHAPE, "explicit map holds a code > 4");
+    return fail(GMP_ERR_MAP_SHAPE, "explicit map holds a code > 5");
 
   local_tiles(pl);
 
@@ -826,12 +828,12 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
   fa.FA = F; fa.FB = F + pl->nA; fa.FC = F + pl->nA + pl->nB;
   fa.mapA = maps; fa.mapB = maps + pl->nA; fa.mapC = maps + pl->nA + pl->nB;
   fa.codeA = codes; fa.codeB = codes + pl->nA; fa.codeC = codes + pl->nA + pl->nB;
-  fa.scaleA5 = s5; fa.scaleB5 = s5 + pl->nA * 5; fa.scaleCin = scin; fa.status = status;
+  fa.scaleA5 = s5; fa.scaleB5 = s5 + pl->nA * NC; fa.scaleCin = scin; fa.status = status;
   k_map_finalize<<<1, 1024, 0, stream>>>(fa);
   GMP_CUDA(cudaGetLastError());
   // ---- the one host synchronisation: read the maps back ----
   pl->codeA.resize(pl->nA); pl->codeB.resize(pl->nB); pl->codeC.resize(pl->nC);
-  pl->sA5.resize(pl->nA * 5); pl->sB5.resize(pl->nB * 5); pl->sCin.resize(pl->nC); pl->sCout.assign(pl->nC, 0);
+  pl->sA5.resize(pl->nA * NC); pl->sB5.resize(pl->nB * NC); pl->sCin.resize(pl->nC); pl->sCout.assign(pl->nC, 0);
   int h_status = 0;
   {
     // codes, scales and status -> mapped host memory by a kernel, then the sync
@@ -893,14 +895,14 @@ extern "C" gmp_status_t gemm_mp_plan_host(const gmp_desc_t* desc, const uint8_t*
   pl->mt = d.M / d.nb; pl->nt = d.N / d.nb; pl->kt = d.K / d.nb;
   pl->nA = pl->mt * pl->kt; pl->nB = pl->kt * pl->nt; pl->nC = pl->mt * pl->nt;
   pl->P = d.P; pl->Q = d.Q; pl->p = d.rank / d.Q; pl->q = d.rank % d.Q;
-  for (int64_t t = 0; t < pl->nA; ++t) if (acode[t] > 4) return fail(GMP_ERR_MAP_SHAPE, "code > 4");
-  for (int64_t t = 0; t < pl->nB; ++t) if (bcode[t] > 4) return fail(GMP_ERR_MAP_SHAPE, "code > 4");
-  for (int64_t t = 0; t < pl->nC; ++t) if (ccode[t] > 4) return fail(GMP_ERR_MAP_SHAPE, "code > 4");
+  for (int64_t t = 0; t < pl->nA; ++t) if (acode[t] >= NC) return fail(GMP_ERR_MAP_SHAPE, "code > 5");
+  for (int64_t t = 0; t < pl->nB; ++t) if (bcode[t] >= NC) return fail(GMP_ERR_MAP_SHAPE, "code > 5");
+  for (int64_t t = 0; t < pl->nC; ++t) if (ccode[t] >= NC) return fail(GMP_ERR_MAP_SHAPE, "code > 5");
   pl->codeA.assign(acode, acode + pl->nA);
   pl->codeB.assign(bcode, bcode + pl->nB);
   pl->codeC.assign(ccode, ccode + pl->nC);
-  pl->sA5.assign(ascale5, ascale5 + pl->nA * 5);
-  pl->sB5.assign(bscale5, bscale5 + pl->nB * 5);
+  pl->sA5.assign(ascale5, ascale5 + pl->nA * NC);
+  pl->sB5.assign(bscale5, bscale5 + pl->nB * NC);
   pl->sCin.assign(pl->nC, 0);
   if (cin_scale) pl->sCin.assign(cin_scale, cin_scale + pl->nC);
   pl->sCout.assign(pl->nC, 0);
@@ -993,7 +995,7 @@ extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_byte
   tables.add(ws + pl->off_split, allsp.data(), (int64_t)(allsp.size() * sizeof(SplitJob)));
   tables.add(ws + pl->off_slice, allsl.data(), (int64_t)(allsl.size() * sizeof(SliceJob)));
   GMP_TRY(tables.run(stream));
-  if (oz_prepare(pl->oz, ws, pl->arena_off[6], pl->arena_slots[6], (int)nb) != GMP_OK)
+  if (oz_prepare(pl->oz, ws, pl->arena_off[GMP_AR_SLICE], pl->arena_slots[GMP_AR_SLICE], (int)nb) != GMP_OK)
     return fail(GMP_ERR_CUDA, "cuTensorMapEncodeTiled (digit arena) failed");
   GMP_TRY(tc_prepare(pl->tc, ws, pl->arena_off, pl->arena_slots, (int)nb));
   // S3 pack
@@ -1087,7 +1089,7 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
       } else if (L.kind == 6) {
         GMP_TRY(tcmc_launch(pl->tc, L.cls, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, stream));
       } else if (L.kind == 1 || L.kind == 3) {
-        GMP_TRY(tc_launch(pl->tc, L.kind == 3 ? 5 : L.cls, L.bn, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha,
+        GMP_TRY(tc_launch(pl->tc, L.kind == 3 ? TC_SPLIT : L.cls, L.bn, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha,
                           stream));
       } else {
         switch (L.cls) {
@@ -1121,7 +1123,8 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
             break;
           case 2: k_simt_class<2><<<(unsigned)L.icount, 256, 0, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha); break;
           case 3: k_simt_class<3><<<(unsigned)L.icount, 256, 0, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha); break;
-          default: k_simt_class<4><<<(unsigned)L.icount, 256, 0, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha); break;
+          case 4: k_simt_class<4><<<(unsigned)L.icount, 256, 0, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha); break;
+          default: k_simt_class<5><<<(unsigned)L.icount, 256, 0, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha); break;
         }
         GMP_CUDA(cudaGetLastError());
       }
@@ -1160,8 +1163,8 @@ extern "C" gmp_status_t gemm_mp_get_maps(gmp_plan_t pl, uint8_t* a, uint8_t* b, 
   if (a) std::memcpy(a, pl->codeA.data(), pl->nA);
   if (b) std::memcpy(b, pl->codeB.data(), pl->nB);
   if (c) std::memcpy(c, pl->codeC.data(), pl->nC);
-  if (as) for (int64_t g = 0; g < pl->nA; ++g) as[g] = pl->sA5[g * 5 + pl->codeA[g]];
-  if (bs) for (int64_t g = 0; g < pl->nB; ++g) bs[g] = pl->sB5[g * 5 + pl->codeB[g]];
+  if (as) for (int64_t g = 0; g < pl->nA; ++g) as[g] = pl->sA5[g * NC + pl->codeA[g]];
+  if (bs) for (int64_t g = 0; g < pl->nB; ++g) bs[g] = pl->sB5[g * NC + pl->codeB[g]];
   if (cs) {
     std::fill(cs, cs + pl->nC, (int16_t)0);
     if (pl->executed && !pl->locC.empty()) {
@@ -1184,14 +1187,16 @@ extern "C" gmp_status_t gemm_mp_get_tile(gmp_plan_t pl, char which, int64_t ti, 
   if (which == 'A' || which == 'B') {
     const bool isB = which == 'B';
     const int64_t rows = isB ? pl->kt : pl->mt, cols = isB ? pl->nt : pl->kt;
-    if (ti < 0 || tj < 0 || ti >= rows || tj >= cols || cls < 0 || cls > 6) return fail(GMP_ERR_ARG, "tile index out of range");
+    if (ti < 0 || tj < 0 || ti >= rows || tj >= cols || cls < 0 || cls >= GMP_NARENA)
+      return fail(GMP_ERR_ARG, "tile index out of range");
     const int64_t g = ti * cols + tj;
-    const int32_t slot = (cls == 6) ? (isB ? pl->sliceB : pl->sliceA)[g]
-                       : (cls == 5) ? (isB ? pl->splitB : pl->splitA)[g] : (isB ? pl->slotB5 : pl->slotA5)[g * 5 + cls];
+    const int32_t slot = (cls == GMP_AR_SLICE) ? (isB ? pl->sliceB : pl->sliceA)[g]
+                       : (cls == GMP_AR_SPLIT) ? (isB ? pl->splitB : pl->splitA)[g]
+                                               : (isB ? pl->slotB5 : pl->slotA5)[g * NC + cls];
     if (slot < 0) return fail(GMP_ERR_ARG, "representation not materialised on this rank");
     off = pl->arena_off[cls] + slot * pl->slot_bytes[cls];
     nbytes = pl->slot_bytes[cls];
-    sc = (cls == 6) ? 0 : (isB ? pl->sB5 : pl->sA5)[g * 5 + (cls == 5 ? 1 : cls)];
+    sc = (cls == GMP_AR_SLICE) ? 0 : (isB ? pl->sB5 : pl->sA5)[g * NC + (cls == GMP_AR_SPLIT ? 1 : cls)];
   } else if (which == 'C' || which == 'I' || which == 'W') {
     if (ti < 0 || tj < 0 || ti >= pl->mt || tj >= pl->nt) return fail(GMP_ERR_ARG, "tile index out of range");
     const int64_t g = ti * pl->nt + tj;
@@ -1221,7 +1226,7 @@ extern "C" gmp_status_t gemm_mp_get_tile(gmp_plan_t pl, char which, int64_t ti, 
 
 extern "C" gmp_status_t gemm_mp_get_stats(gmp_plan_t pl, gmp_stats_t* out) {
   if (!pl || !out) return fail(GMP_ERR_ARG, "NULL argument");
-  for (int c = 0; c < 5; ++c) pl->st.class_ms[c] = 0.0;
+  for (int c = 0; c < NC; ++c) pl->st.class_ms[c] = 0.0;
   if (pl->executed && !pl->launch_ev.empty()) {
     for (size_t li = 0; li < pl->launches.size(); ++li) {
       float ms = 0.f;

@@ -1,34 +1,40 @@
 // gmp_common.cuh -- device-side number formats and exact helpers for the
 // tile-centric mixed-precision GEMM (arxiv 2508.14848).  sm_100a only.
 //
-// Class codes: 0 FP64, 1 FP32, 2 FP16, 3 BF16, 4 E4M3 (OCP FN).
+// Class codes: 0 FP64, 1 FP32, 2 FP16, 3 BF16, 4 E4M3 (OCP FN),
+// 5 E5M2 (OCP).  Ordered by unit roundoff: pair class = max.
 // Every conversion from binary64 is ONE round-to-nearest-even (PAPER.md:148
 // receiver-side conversion; R11): hardware cvt.rn for FP32/FP16/BF16,
-// round-to-odd into binary32 followed by cvt.rn.satfinite for E4M3.
+// round-to-odd into binary32 followed by cvt.rn.satfinite for E4M3 / E5M2 (the
+// per-tile scale keeps every value <= Omega', so satfinite never triggers).
 // No code here is shared with oracle/ (which re-derives everything from the
 // format definitions in plain C).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
 
-#define GMP_NCLASS 5
+#define GMP_NCLASS 6
+// workspace arenas: one per class, then the FP32 BF16x3 splits and the FP64 int8 digits
+#define GMP_AR_SPLIT (GMP_NCLASS)
+#define GMP_AR_SLICE (GMP_NCLASS + 1)
+#define GMP_NARENA (GMP_NCLASS + 2)
 #define GMP_STEP_DEPTH 8  // SUMMA step depth D (R15): fold order is G-independent
 
 namespace gmp {
 
 __host__ __device__ constexpr int class_bytes(int c) {
-  return c == 0 ? 8 : c == 1 ? 4 : c == 4 ? 1 : 2;
+  return c == 0 ? 8 : c == 1 ? 4 : c >= 4 ? 1 : 2;
 }
 
 // unit roundoff u_k, smallest subnormal eta_k, scale target Omega'_k (R10)
 __host__ __device__ inline double class_u(int c) {
-  return c == 0 ? 0x1p-53 : c == 1 ? 0x1p-24 : c == 2 ? 0x1p-11 : c == 3 ? 0x1p-8 : 0x1p-4;
+  return c == 0 ? 0x1p-53 : c == 1 ? 0x1p-24 : c == 2 ? 0x1p-11 : c == 3 ? 0x1p-8 : c == 4 ? 0x1p-4 : 0x1p-3;
 }
 __host__ __device__ inline double class_eta(int c) {
-  return c == 0 ? 0x1p-1074 : c == 1 ? 0x1p-149 : c == 2 ? 0x1p-24 : c == 3 ? 0x1p-133 : 0x1p-9;
+  return c == 0 ? 0x1p-1074 : c == 1 ? 0x1p-149 : c == 2 ? 0x1p-24 : c == 3 ? 0x1p-133 : c == 4 ? 0x1p-9 : 0x1p-16;
 }
 __host__ __device__ inline double class_omega(int c) {
-  return c == 2 ? 65504.0 : c == 4 ? 448.0 : 1.0;
+  return c == 2 ? 65504.0 : c == 4 ? 448.0 : c == 5 ? 57344.0 : 1.0;
 }
 
 // ---- binary64 -> class bits, one RNE rounding --------------------------------
@@ -64,6 +70,15 @@ __device__ __forceinline__ uint16_t cvt_e4m3x2_rn(double lo, double hi) {
 __device__ __forceinline__ uint8_t cvt_e4m3_rn(double x) {
   return (uint8_t)(cvt_e4m3x2_rn(x, 0.0) & 0xFF);
 }
+__device__ __forceinline__ uint16_t cvt_e5m2x2_rn(double lo, double hi) {
+  uint16_t r;
+  float flo = rto_f32(lo), fhi = rto_f32(hi);
+  asm("cvt.rn.satfinite.e5m2x2.f32 %0, %1, %2;" : "=h"(r) : "f"(fhi), "f"(flo));
+  return r;
+}
+__device__ __forceinline__ uint8_t cvt_e5m2_rn(double x) {
+  return (uint8_t)(cvt_e5m2x2_rn(x, 0.0) & 0xFF);
+}
 
 // ---- class bits -> exact binary64 / binary32 ----------------------------------
 __device__ __forceinline__ float f16_to_f32(uint16_t h) {
@@ -80,6 +95,12 @@ __device__ __forceinline__ float e4m3_to_f32(uint8_t b) {
   asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"(in));
   return f16_to_f32((uint16_t)(h2 & 0xFFFF));
 }
+__device__ __forceinline__ float e5m2_to_f32(uint8_t b) {
+  uint32_t h2;
+  uint16_t in = b;
+  asm("cvt.rn.f16x2.e5m2x2 %0, %1;" : "=r"(h2) : "h"(in));
+  return f16_to_f32((uint16_t)(h2 & 0xFFFF));
+}
 // value of element i of a payload of class c, as binary32 (exact for c >= 1)
 template <int C>
 __device__ __forceinline__ float payload_f32(const void* p, int64_t i) {
@@ -87,6 +108,7 @@ __device__ __forceinline__ float payload_f32(const void* p, int64_t i) {
   if constexpr (C == 2) return f16_to_f32(reinterpret_cast<const uint16_t*>(p)[i]);
   if constexpr (C == 3) return bf16_to_f32(reinterpret_cast<const uint16_t*>(p)[i]);
   if constexpr (C == 4) return e4m3_to_f32(reinterpret_cast<const uint8_t*>(p)[i]);
+  if constexpr (C == 5) return e5m2_to_f32(reinterpret_cast<const uint8_t*>(p)[i]);
   return 0.f;
 }
 __device__ __forceinline__ double payload_f64(const void* p, int64_t i, int c) {
@@ -95,7 +117,8 @@ __device__ __forceinline__ double payload_f64(const void* p, int64_t i, int c) {
     case 1: return (double)reinterpret_cast<const float*>(p)[i];
     case 2: return (double)f16_to_f32(reinterpret_cast<const uint16_t*>(p)[i]);
     case 3: return (double)bf16_to_f32(reinterpret_cast<const uint16_t*>(p)[i]);
-    default: return (double)e4m3_to_f32(reinterpret_cast<const uint8_t*>(p)[i]);
+    case 4: return (double)e4m3_to_f32(reinterpret_cast<const uint8_t*>(p)[i]);
+    default: return (double)e5m2_to_f32(reinterpret_cast<const uint8_t*>(p)[i]);
   }
 }
 // store RN_c(x) as element i of a payload of class c
@@ -105,7 +128,8 @@ __device__ __forceinline__ void payload_store(void* p, int64_t i, int c, double 
     case 1: reinterpret_cast<uint32_t*>(p)[i] = cvt_f32_rn(x); break;
     case 2: reinterpret_cast<uint16_t*>(p)[i] = cvt_f16_rn(x); break;
     case 3: reinterpret_cast<uint16_t*>(p)[i] = cvt_bf16_rn(x); break;
-    default: reinterpret_cast<uint8_t*>(p)[i] = cvt_e4m3_rn(x); break;
+    case 4: reinterpret_cast<uint8_t*>(p)[i] = cvt_e4m3_rn(x); break;
+    default: reinterpret_cast<uint8_t*>(p)[i] = cvt_e5m2_rn(x); break;
   }
 }
 // RN_c(x) as an exact binary64 value (used for the analytic shadow scale)
@@ -115,7 +139,8 @@ __device__ __forceinline__ double round_to_class(double x, int c) {
     case 1: return (double)__uint_as_float(cvt_f32_rn(x));
     case 2: return (double)f16_to_f32(cvt_f16_rn(x));
     case 3: return (double)bf16_to_f32(cvt_bf16_rn(x));
-    default: return (double)e4m3_to_f32(cvt_e4m3_rn(x));
+    case 4: return (double)e4m3_to_f32(cvt_e4m3_rn(x));
+    default: return (double)e5m2_to_f32(cvt_e5m2_rn(x));
   }
 }
 

@@ -50,8 +50,8 @@ __device__ __forceinline__ void store8(uint8_t* dst, const double* v) {
     uint32_t w[2];
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
-      uint32_t lo = cvt_e4m3x2_rn(v[4 * i], v[4 * i + 1]);
-      uint32_t hi = cvt_e4m3x2_rn(v[4 * i + 2], v[4 * i + 3]);
+      uint32_t lo = (C == 4) ? cvt_e4m3x2_rn(v[4 * i], v[4 * i + 1]) : cvt_e5m2x2_rn(v[4 * i], v[4 * i + 1]);
+      uint32_t hi = (C == 4) ? cvt_e4m3x2_rn(v[4 * i + 2], v[4 * i + 3]) : cvt_e5m2x2_rn(v[4 * i + 2], v[4 * i + 3]);
       w[i] = lo | (hi << 16);
     }
     *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
@@ -125,7 +125,8 @@ __global__ void __launch_bounds__(256) k_pack(const PackJob* __restrict__ jobs, 
     case 1: pack_block<1>(j, ws, nb, r0, c0, sm); break;
     case 2: pack_block<2>(j, ws, nb, r0, c0, sm); break;
     case 3: pack_block<3>(j, ws, nb, r0, c0, sm); break;
-    default: pack_block<4>(j, ws, nb, r0, c0, sm); break;
+    case 4: pack_block<4>(j, ws, nb, r0, c0, sm); break;
+    default: pack_block<5>(j, ws, nb, r0, c0, sm); break;
   }
 }
 
@@ -159,10 +160,11 @@ __global__ void __launch_bounds__(256) k_shadow(const ShadowJob* __restrict__ jo
   const int key = j.from * 8 + j.to;
   switch (key) {
 #define GMP_SH(F, T) case F * 8 + T: shadow_run<F, T>(j, ws, n); break;
-    GMP_SH(0, 1) GMP_SH(0, 2) GMP_SH(0, 3) GMP_SH(0, 4)
-    GMP_SH(1, 2) GMP_SH(1, 3) GMP_SH(1, 4)
-    GMP_SH(2, 3) GMP_SH(2, 4)
-    GMP_SH(3, 4)
+    GMP_SH(0, 1) GMP_SH(0, 2) GMP_SH(0, 3) GMP_SH(0, 4) GMP_SH(0, 5)
+    GMP_SH(1, 2) GMP_SH(1, 3) GMP_SH(1, 4) GMP_SH(1, 5)
+    GMP_SH(2, 3) GMP_SH(2, 4) GMP_SH(2, 5)
+    GMP_SH(3, 4) GMP_SH(3, 5)
+    GMP_SH(4, 5)
 #undef GMP_SH
     default: break;
   }
@@ -210,7 +212,7 @@ __global__ void __launch_bounds__(256) k_shadow_t(const ShadowJob* __restrict__ 
   const int r0 = (blockIdx.x / per) * 64, c0 = (blockIdx.x % per) * 64;
   switch (j.from * 8 + j.to) {
 #define GMP_ST(F, T) case F * 8 + T: shadow_t_block<F, T>(j, ws, nb, r0, c0, sm); break;
-    GMP_ST(0, 2) GMP_ST(0, 3) GMP_ST(0, 4) GMP_ST(1, 2) GMP_ST(1, 3) GMP_ST(1, 4)
+    GMP_ST(0, 2) GMP_ST(0, 3) GMP_ST(0, 4) GMP_ST(0, 5) GMP_ST(1, 2) GMP_ST(1, 3) GMP_ST(1, 4) GMP_ST(1, 5)
 #undef GMP_ST
     default: break;
   }

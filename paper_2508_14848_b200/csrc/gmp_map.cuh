@@ -91,7 +91,7 @@ struct FinalizeArgs {
   const uint8_t *mapA, *mapB, *mapC;   // explicit maps (device) or null
   // outputs
   uint8_t *codeA, *codeB, *codeC;
-  int16_t *scaleA5, *scaleB5;          // [tile][5], class-c scale for c >= code
+  int16_t *scaleA5, *scaleB5;          // [tile][GMP_NCLASS], class-c scale for c >= code
   int16_t *scaleCin;                   // packed C_in scale (beta != 0)
   int* status;                         // 0 ok, 4 non-finite
 };
@@ -148,10 +148,10 @@ __global__ void __launch_bounds__(1024) k_map_finalize(FinalizeArgs a) {
     const int expl = isB ? a.explicit_b : a.explicit_a;
     if (expl) {
       chosen = (isB ? a.mapB : a.mapA)[tt];
-      if (chosen > 4 || !(mask & (1u << chosen))) chosen = 0;
+      if (chosen >= GMP_NCLASS || !(mask & (1u << chosen))) chosen = 0;
     } else if (!isinf(SX)) {
       const double rhs = __ddiv_rn(__dmul_rn(eps, __dsqrt_rn(SX)), __dsqrt_rn(ntiles));
-      for (int kk = 4; kk >= 1; --kk) {        // ladder E4M3, BF16, FP16, FP32 (then FP64)
+      for (int kk = GMP_NCLASS - 1; kk >= 1; --kk) {   // ladder E5M2, E4M3, BF16, FP16, FP32 (then FP64)
         if (!(mask & (1u << kk))) continue;
         if (M == 0.0) { chosen = kk; break; }
         const int e = scale_exp(M, kk);
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(1024) k_map_finalize(FinalizeArgs a) {
     }
     const int e = scale_exp(M, chosen);
     (isB ? a.codeB : a.codeA)[tt] = (uint8_t)chosen;
-    fill_scales5(M, chosen, e, (isB ? a.scaleB5 : a.scaleA5) + tt * 5);
+    fill_scales5(M, chosen, e, (isB ? a.scaleB5 : a.scaleA5) + tt * GMP_NCLASS);
   }
   __syncthreads();
   // ---- C tiles (O7) ----
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(1024) k_map_finalize(FinalizeArgs a) {
     int chosen = 0;
     if (a.explicit_c) {
       chosen = a.mapC[ct];
-      if (chosen > 4 || !(mask & (1u << chosen))) chosen = 0;
+      if (chosen >= GMP_NCLASS || !(mask & (1u << chosen))) chosen = 0;
     } else {
       double RA = 0.0, QB = 0.0;
       for (int64_t l = 0; l < a.kt; ++l) RA = __dadd_rn(RA, a.SA[i * a.kt + l]);
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(1024) k_map_finalize(FinalizeArgs a) {
       QB = __dsqrt_rn(QB);
       const double sc = hasC ? a.SC[ct] : 0.0;
       const double nhat = __dadd_rn(__dmul_rn(__dmul_rn(aa, RA), QB), __dmul_rn(ab, __dsqrt_rn(sc)));
-      for (int k = 4; k >= 1; --k) {
+      for (int k = GMP_NCLASS - 1; k >= 1; --k) {
         if (!(mask & (1u << k))) continue;
         const double dC = __dadd_rn(__dadd_rn(class_u(k), __dmul_rn(sqkt, 0x1p-24)),
                                     __ddiv_rn(__dmul_rn((double)a.nb, class_eta(k)), class_omega(k)));
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(1024) k_map_finalize(FinalizeArgs a) {
         for (int64_t l = 0; ok && l < a.kt; ++l) {
           const int ca = a.codeA[i * a.kt + l], cb = a.codeB[l * a.nt + j];
           const int c = ca > cb ? ca : cb;
-          const int ea = a.scaleA5[(i * a.kt + l) * 5 + c], eb = a.scaleB5[(l * a.nt + j) * 5 + c];
+          const int ea = a.scaleA5[(i * a.kt + l) * GMP_NCLASS + c], eb = a.scaleB5[(l * a.nt + j) * GMP_NCLASS + c];
           const double f = ldexp(a.alpha, -(ea + eb));
           if (f != 0.0 && !(fabs(f) >= 0x1p-126 && fabs(f) <= 0x1p100)) ok = false;
         }

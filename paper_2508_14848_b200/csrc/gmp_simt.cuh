@@ -83,7 +83,7 @@ __device__ __forceinline__ void ld4(const uint8_t* p, T* v) {
   } else {
     uint32_t a = __ldg(reinterpret_cast<const uint32_t*>(p));
 #pragma unroll
-    for (int i = 0; i < 4; ++i) v[i] = e4m3_to_f32((uint8_t)(a >> (8 * i)));
+    for (int i = 0; i < 4; ++i) v[i] = (C == 4) ? e4m3_to_f32((uint8_t)(a >> (8 * i))) : e5m2_to_f32((uint8_t)(a >> (8 * i)));
   }
 }
 

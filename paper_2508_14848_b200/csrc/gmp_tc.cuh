@@ -84,13 +84,13 @@ __device__ __forceinline__ uint64_t sdesc_k_sw128(uint32_t saddr) {
 // instruction descriptor: D = F32, A/B format, K-major both, N>>3, M>>4
 template <int C, int BN>
 __host__ __device__ constexpr uint32_t tc_idesc() {
-  constexpr uint32_t ab = (C == 3) ? 1u : 0u;   // kind::f16: F16 = 0, BF16 = 1; kind::f8f6f4: E4M3 = 0
+  constexpr uint32_t ab = (C == 3 || C == 5) ? 1u : 0u;   // kind::f16: F16 0, BF16 1; kind::f8f6f4: E4M3 0, E5M2 1
   return (1u << 4) | (ab << 7) | (ab << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
 }
 template <int C>
 __device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                        uint32_t accumulate) {
-  if constexpr (C == 4) {
+  if constexpr (C == 4 || C == 5) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
@@ -114,14 +114,16 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
-// C = 2, 3, 4: FP16 / BF16 / E4M3 classes, NP = 1 operand part.
-// C = 5: the FP32 class on the tensor pipe ("BF16x9"): each FP32 operand tile is
+// C = 2, 3, 4, 5: FP16 / BF16 / E4M3 / E5M2 classes, NP = 1 operand part.
+// C = TC_SPLIT: the FP32 class on the tensor pipe ("BF16x9"): each FP32 operand tile is
 // split exactly into three BF16 parts x = x0 + x1 + x2 (k_split, receiver-side
 // from the stored FP32 payload), NP = 3, and all nine part products -- each
 // exact in the FP32 accumulator's inputs -- are accumulated per K block,
 // smallest terms first; binary32 inputs, exact products, binary32 accumulation.
-template <int C> constexpr int tc_np() { return C == 5 ? 3 : 1; }
-template <int C> constexpr int tc_stages() { return C == 5 ? 2 : TC_STAGES; }
+constexpr int TC_SPLIT = 9;   // template id of the FP32-class (BF16x9) kernel; its maps are arena GMP_AR_SPLIT
+template <int C> constexpr int tc_np() { return C == TC_SPLIT ? 3 : 1; }
+template <int C> constexpr int tc_stages() { return C == TC_SPLIT ? 2 : TC_STAGES; }
+template <int C> constexpr int tc_map_index() { return C == TC_SPLIT ? GMP_AR_SPLIT : C; }
 
 template <int C, int BN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -129,12 +131,12 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
            const WorkItem* __restrict__ items, int64_t nitems, const PairDesc* __restrict__ pairs,
            const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha) {
   constexpr int NP = tc_np<C>(), ST = tc_stages<C>();
-  constexpr int ESZ = (C == 4) ? 1 : 2;
+  constexpr int ESZ = (C == 4 || C == 5) ? 1 : 2;
   constexpr int BK = 128 / ESZ;            // elements per 128-byte K block
   constexpr int NMMA = 4;                  // 32-byte K per tcgen05.mma
   constexpr int A_BYTES = TC_BM * 128, B_BYTES = BN * 128, STAGE_BYTES = NP * (A_BYTES + B_BYTES);
   constexpr uint32_t TMEM_COLS = 2 * BN;
-  constexpr uint32_t IDESC = tc_idesc<(C == 5 ? 3 : C), BN>();
+  constexpr uint32_t IDESC = tc_idesc<(C == TC_SPLIT ? 3 : C), BN>();
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -343,9 +345,10 @@ constexpr int tc_smem_bytes() {
 // host side
 // ---------------------------------------------------------------------------
 struct TcTables {
-  CUtensorMap mapA[6], mapB[6];   // classes 2..4 and 5 = FP32 split (BF16 parts); B box rows = tc_bn(nb)
-  CUtensorMap mapB128[6];         // B box of 128 rows (launches with binary64 W)
-  bool ready[6] = {false, false, false, false, false, false};
+  CUtensorMap mapA[GMP_NARENA], mapB[GMP_NARENA];   // classes 2..5 and GMP_AR_SPLIT (FP32 BF16 parts);
+                                                    // B box rows = tc_bn(nb)
+  CUtensorMap mapB128[GMP_NARENA];                  // B box of 128 rows (launches with binary64 W)
+  bool ready[GMP_NARENA] = {};
   int nb = 0;
 };
 
@@ -366,21 +369,23 @@ inline PFN_encodeTiled get_encode_tiled() {
 }
 
 
-// arena_off / arena_slots have 6 entries; arena 5 holds FP32 splits (3 BF16 parts per slot)
+// arena_off / arena_slots have GMP_NARENA entries; arena GMP_AR_SPLIT holds FP32
+// splits (3 BF16 parts per slot)
 inline gmp_status_t tc_prepare(TcTables& t, uint8_t* ws, const int64_t* arena_off, const int64_t* arena_slots, int nb) {
   t.nb = nb;
-  for (int c = 2; c <= 5; ++c) {
+  for (int c = 2; c <= GMP_AR_SPLIT; ++c) {
     t.ready[c] = false;
     if (arena_slots[c] == 0) continue;
     PFN_encodeTiled enc = get_encode_tiled();
     if (!enc) return GMP_ERR_CUDA;
-    const int esz = (c == 4) ? 1 : 2;
-    const int64_t rows = arena_slots[c] * (c == 5 ? 3 : 1) * nb;
+    const bool split = c == GMP_AR_SPLIT;
+    const int esz = (c == 4 || c == 5) ? 1 : 2;
+    const int64_t rows = arena_slots[c] * (split ? 3 : 1) * nb;
     cuuint64_t dims[2] = {(cuuint64_t)nb, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)nb * esz};
     cuuint32_t estr[2] = {1, 1};
-    const CUtensorMapDataType dt = (c == 4) ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16;
-    const int bn = (c == 5) ? 128 : tc_bn(nb);
+    const CUtensorMapDataType dt = (esz == 1) ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16;
+    const int bn = split ? 128 : tc_bn(nb);
     cuuint32_t boxA[2] = {(cuuint32_t)(128 / esz), (cuuint32_t)TC_BM};
     cuuint32_t boxB[2] = {(cuuint32_t)(128 / esz), (cuuint32_t)bn};
     void* base = ws + arena_off[c];
@@ -416,22 +421,25 @@ inline gmp_status_t tc_launch_t(TcTables& t, const WorkItem* it, int64_t n, cons
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)std::min<int64_t>(n, sms);
-  k_tc_class<C, BN><<<grid, TC_THREADS, smem, s>>>(t.mapA[C], BN == 128 ? t.mapB128[C] : t.mapB[C], it, n, pd, ct, ws,
-                                                    nb, alpha);
+  constexpr int mi = tc_map_index<C>();
+  k_tc_class<C, BN><<<grid, TC_THREADS, smem, s>>>(t.mapA[mi], BN == 128 ? t.mapB128[mi] : t.mapB[mi], it, n, pd, ct,
+                                                    ws, nb, alpha);
   return cudaGetLastError() == cudaSuccess ? GMP_OK : GMP_ERR_CUDA;
 }
 
-// cls: 2..4 for the 16/8-bit classes, 5 for the FP32 class on the tensor pipe;
-// bn: 256 or 128 (tc_bn_for(): 128 when the launch folds into binary64 W)
+// cls: 2..5 for the 16/8-bit classes, TC_SPLIT for the FP32 class on the tensor
+// pipe; bn: 256 or 128 (128 when the launch folds into binary64 W)
 inline gmp_status_t tc_launch(TcTables& t, int cls, int bn, const WorkItem* it, int64_t n, const PairDesc* pd,
                               const CTileDesc* ct, uint8_t* ws, int nb, double alpha, cudaStream_t s) {
-  if (cls < 2 || cls > 5 || !t.ready[cls]) return GMP_ERR_STATE;
+  const int mi = (cls == TC_SPLIT) ? GMP_AR_SPLIT : cls;
+  if (!((cls >= 2 && cls <= 5) || cls == TC_SPLIT) || !t.ready[mi]) return GMP_ERR_STATE;
   const bool wide = bn == 256;
   switch (cls) {
     case 2: return wide ? tc_launch_t<2, 256>(t, it, n, pd, ct, ws, nb, alpha, s) : tc_launch_t<2, 128>(t, it, n, pd, ct, ws, nb, alpha, s);
     case 3: return wide ? tc_launch_t<3, 256>(t, it, n, pd, ct, ws, nb, alpha, s) : tc_launch_t<3, 128>(t, it, n, pd, ct, ws, nb, alpha, s);
     case 4: return wide ? tc_launch_t<4, 256>(t, it, n, pd, ct, ws, nb, alpha, s) : tc_launch_t<4, 128>(t, it, n, pd, ct, ws, nb, alpha, s);
-    default: return tc_launch_t<5, 128>(t, it, n, pd, ct, ws, nb, alpha, s);
+    case 5: return wide ? tc_launch_t<5, 256>(t, it, n, pd, ct, ws, nb, alpha, s) : tc_launch_t<5, 128>(t, it, n, pd, ct, ws, nb, alpha, s);
+    default: return tc_launch_t<TC_SPLIT, 128>(t, it, n, pd, ct, ws, nb, alpha, s);
   }
 }
 

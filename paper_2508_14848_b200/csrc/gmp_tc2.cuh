@@ -57,7 +57,7 @@ __device__ __forceinline__ void mbar_arrive_cta0(uint64_t* b) {
 template <int C>
 __device__ __forceinline__ void tc2_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                         uint32_t accumulate) {
-  if constexpr (C == 4) {
+  if constexpr (C == 4 || C == 5) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
@@ -72,7 +72,7 @@ __device__ __forceinline__ void tc2_mma(uint32_t d_tmem, uint64_t adesc, uint64_
 // D = F32, A/B format, K-major, N = 256, M = 256 (the pair)
 template <int C>
 __host__ __device__ constexpr uint32_t tc2_idesc() {
-  constexpr uint32_t ab = (C == 3) ? 1u : 0u;
+  constexpr uint32_t ab = (C == 3 || C == 5) ? 1u : 0u;
   return (1u << 4) | (ab << 7) | (ab << 10) | ((uint32_t)(TC2_BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
 }
 __host__ __device__ inline int64_t tc2_subtiles_per_item(int nb) { return (int64_t)(nb / 256) * (nb / 256); }
@@ -82,7 +82,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 k_tc2_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
             const WorkItem* __restrict__ items, int64_t nitems, const PairDesc* __restrict__ pairs,
             const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha) {
-  constexpr int ESZ = (C == 4) ? 1 : 2;
+  constexpr int ESZ = (C == 4 || C == 5) ? 1 : 2;
   constexpr int BK = 128 / ESZ;                  // elements per 128-byte K block
   constexpr int NMMA = 4;                        // 32-byte K per tcgen05.mma
   constexpr int A_BYTES = 128 * 128, B_BYTES = 128 * 128, STAGE_BYTES = A_BYTES + B_BYTES;
@@ -256,7 +256,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 k_tcmc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
              const WorkItem* __restrict__ items, int64_t nitems, const PairDesc* __restrict__ pairs,
              const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha) {
-  constexpr int ESZ = (C == 4) ? 1 : 2;
+  constexpr int ESZ = (C == 4 || C == 5) ? 1 : 2;
   constexpr int BK = 128 / ESZ;
   constexpr int NMMA = 4;
   constexpr int BN = TC2_BN;
@@ -420,11 +420,12 @@ inline gmp_status_t tcmc_launch_t(TcTables& t, const WorkItem* it, int64_t n, co
 
 inline gmp_status_t tcmc_launch(TcTables& t, int cls, const WorkItem* it, int64_t n, const PairDesc* pd,
                                 const CTileDesc* ct, uint8_t* ws, int nb, double alpha, cudaStream_t s) {
-  if (cls < 2 || cls > 4 || !t.ready[cls]) return GMP_ERR_STATE;
+  if (cls < 2 || cls > 5 || !t.ready[cls]) return GMP_ERR_STATE;
   switch (cls) {
     case 2: return tcmc_launch_t<2>(t, it, n, pd, ct, ws, nb, alpha, s);
     case 3: return tcmc_launch_t<3>(t, it, n, pd, ct, ws, nb, alpha, s);
-    default: return tcmc_launch_t<4>(t, it, n, pd, ct, ws, nb, alpha, s);
+    case 4: return tcmc_launch_t<4>(t, it, n, pd, ct, ws, nb, alpha, s);
+    default: return tcmc_launch_t<5>(t, it, n, pd, ct, ws, nb, alpha, s);
   }
 }
 
@@ -452,11 +453,12 @@ inline gmp_status_t tc2_launch_t(TcTables& t, const WorkItem* it, int64_t n, con
 // cls: 2..4; n = items x tc2_subtiles_per_item(nb)
 inline gmp_status_t tc2_launch(TcTables& t, int cls, const WorkItem* it, int64_t n, const PairDesc* pd,
                                const CTileDesc* ct, uint8_t* ws, int nb, double alpha, cudaStream_t s) {
-  if (cls < 2 || cls > 4 || !t.ready[cls]) return GMP_ERR_STATE;
+  if (cls < 2 || cls > 5 || !t.ready[cls]) return GMP_ERR_STATE;
   switch (cls) {
     case 2: return tc2_launch_t<2>(t, it, n, pd, ct, ws, nb, alpha, s);
     case 3: return tc2_launch_t<3>(t, it, n, pd, ct, ws, nb, alpha, s);
-    default: return tc2_launch_t<4>(t, it, n, pd, ct, ws, nb, alpha, s);
+    case 4: return tc2_launch_t<4>(t, it, n, pd, ct, ws, nb, alpha, s);
+    default: return tc2_launch_t<5>(t, it, n, pd, ct, ws, nb, alpha, s);
   }
 }
 

@@ -44,8 +44,8 @@ def tol_metric(Cmp, A, Bm, C, alpha, beta):
     return num / den
 
 
-U_CLASS = [2.0 ** -53, 2.0 ** -24, 2.0 ** -11, 2.0 ** -8, 2.0 ** -4]
-ETA_CLASS = [2.0 ** -1074, 2.0 ** -149, 2.0 ** -24, 2.0 ** -133, 2.0 ** -9]
+U_CLASS = [2.0 ** -53, 2.0 ** -24, 2.0 ** -11, 2.0 ** -8, 2.0 ** -4, 2.0 ** -3]
+ETA_CLASS = [2.0 ** -1074, 2.0 ** -149, 2.0 ** -24, 2.0 ** -133, 2.0 ** -9, 2.0 ** -16]
 
 
 def c_parity(Cg, Co, ccode, cscale, nb, K, allfp64):

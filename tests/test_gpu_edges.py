@@ -87,7 +87,7 @@ def test_fp32_split_parts_are_exact():
         for ti in range(codes.shape[0]):
             for tj in range(codes.shape[1]):
                 try:
-                    parts, sc = g.tile(which, ti, tj, 5)
+                    parts, sc = g.tile(which, ti, tj, B.TILE_SPLIT)
                 except B.GmpError:
                     continue
                 code = int(codes[ti, tj])
@@ -129,7 +129,7 @@ def test_fp64_digit_planes_reconstruct():
     for which, X in [("A", A), ("B", Bm)]:
         for ti in range(4):
             for tj in range(4):
-                planes, _ = g.tile(which, ti, tj, 6)
+                planes, _ = g.tile(which, ti, tj, B.TILE_DIGITS)
                 q = planes.view(np.int8).reshape(7, nb, nb).astype(np.float64)
                 tile = X[ti * nb:(ti + 1) * nb, tj * nb:(tj + 1) * nb]
                 kmaj = tile if which == "A" else tile.T          # rows = output rows / cols, K contiguous
@@ -145,7 +145,8 @@ def test_fp64_digit_planes_reconstruct():
     assert np.linalg.norm(out - o["C"]) / np.linalg.norm(o["C"]) <= 1e-13
 
 
-@pytest.mark.parametrize("nb,mask,tol", [(128, 0b01111, 1e-6), (256, 0b11111, 1e-1), (128, 0b00001, 1e-12)])
+@pytest.mark.parametrize("nb,mask,tol", [(128, 0b01111, 1e-6), (256, 0b11111, 1e-1), (128, 0b00001, 1e-12),
+                                         (256, 0b111111, 0.5)])
 def test_single_tile(nb, mask, tol):
     """degenerate grid: M = N = K = nb (one tile each, one SUMMA step, one pair)"""
     w = gmp_inputs.small_workload(nb, nb, nb, nb, tol, mode="uniform", E=0, beta=0.25, class_mask=mask, seed=61)

@@ -29,6 +29,12 @@ def _cases():
                                                    seed=43)),
         ("fp64_only", gmp_inputs.small_workload(512, 512, 512, 128, 1e-12, mode="random", E=10, beta=1.0,
                                                 class_mask=0b00001, seed=44)),
+        # E5M2 enabled: E5M2 tiles, E5M2 shadows of every class, E5M2 pairs on
+        # tcgen05 kind::f8f6f4, E5M2 C tiles
+        ("e5m2_mix", gmp_inputs.small_workload(512, 384, 640, 128, 1e-1, mode="random", E=48, beta=0.5,
+                                               class_mask=0b111111, seed=46)),
+        ("e5m2_nb256", gmp_inputs.small_workload(768, 512, 1024, 256, 2e-2, mode="random", E=40, beta=0.0,
+                                                 class_mask=0b111111, seed=47)),
         # nb = 512 with GMP_FLAG_TC_PAIR: 2 x 2 sub-tiles of 256 x 256 per C tile on the
         # SM-pair kernel (k_tc2_class); the plain nb = 512 run covers the 1-SM kernel
         ("pairs_nb512", gmp_inputs.small_workload(1024, 1536, 1536, 512, 1e-2, mode="random", E=24, beta=0.75,
@@ -61,8 +67,8 @@ def test_maps_bitwise(case):
     assert np.array_equal(m["acode"], o["acode"])
     assert np.array_equal(m["bcode"], o["bcode"])
     assert np.array_equal(m["ccode"], o["ccode"])
-    amask = o["acode"][..., None] == np.arange(5)
-    bmask = o["bcode"][..., None] == np.arange(5)
+    amask = o["acode"][..., None] == np.arange(B.NCLS)
+    bmask = o["bcode"][..., None] == np.arange(B.NCLS)
     assert np.array_equal(m["ascale"], (o["ascale5"] * amask).sum(-1))
     assert np.array_equal(m["bscale"], (o["bscale5"] * bmask).sum(-1))
 

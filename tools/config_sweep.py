@@ -29,7 +29,7 @@ import gmp_inputs  # noqa: E402
 from paper_2508_14848_b200 import api  # noqa: E402
 from paper_2508_14848_b200 import binding as B  # noqa: E402
 
-NAMES = ["FP64", "FP32", "FP16", "BF16", "E4M3"]
+NAMES = ["FP64", "FP32", "FP16", "BF16", "E4M3", "E5M2"]
 
 
 def peaks():
@@ -38,7 +38,7 @@ def peaks():
     except Exception:
         p = {"bf16_tflops": 1590.0}
     bf16 = p.get("bf16_tflops", 1590.0)
-    return [37.22496, bf16 / 9.0, bf16, bf16, 2 * bf16]
+    return [37.22496, bf16 / 9.0, bf16, bf16, 2 * bf16, 2 * bf16]
 
 
 def run(w, reps, mask=None, flags=0, explicit=None, label=None):
@@ -76,20 +76,20 @@ def run(w, reps, mask=None, flags=0, explicit=None, label=None):
     st = g.stats()
     best = min(times)
     pk = peaks()
-    t_roof = sum(st["flops"][c] / (pk[c] * 1e12) for c in range(5)) * 1e3
-    cls_ms = [min(x[c] for x in cms) for c in range(5)]
+    t_roof = sum(st["flops"][c] / (pk[c] * 1e12) for c in range(len(NAMES))) * 1e3
+    cls_ms = [min(x[c] for x in cms) for c in range(len(NAMES))]
     res = dict(run=label or w.name, M=w.M, N=w.N, K=w.K, nb=w.nb, tol=w.tol,
                plan_ms=ev[0].elapsed_time(ev[1]), convert_ms=ev[1].elapsed_time(ev[2]),
                exec_ms_best=best, exec_ms=times, tflops_exec=w.flops / best / 1e9,
                tflops_step=w.flops / (best + ev[0].elapsed_time(ev[2])) / 1e9,
-               pairs={NAMES[c]: st["pairs"][c] for c in range(5)},
-               tiles_a={NAMES[c]: st["tiles_a"][c] for c in range(5)},
-               tiles_c={NAMES[c]: st["tiles_c"][c] for c in range(5)},
-               class_ms={NAMES[c]: round(cls_ms[c], 3) for c in range(5) if st["pairs"][c]},
+               pairs={NAMES[c]: st["pairs"][c] for c in range(len(NAMES))},
+               tiles_a={NAMES[c]: st["tiles_a"][c] for c in range(len(NAMES))},
+               tiles_c={NAMES[c]: st["tiles_c"][c] for c in range(len(NAMES))},
+               class_ms={NAMES[c]: round(cls_ms[c], 3) for c in range(len(NAMES)) if st["pairs"][c]},
                class_tflops={NAMES[c]: round(st["flops"][c] / (cls_ms[c] * 1e-3) / 1e12, 1)
-                             for c in range(5) if st["pairs"][c] and cls_ms[c] > 0},
+                             for c in range(len(NAMES)) if st["pairs"][c] and cls_ms[c] > 0},
                t_roof_ms=t_roof, roof_frac_exec=t_roof / best,
-               peaks_tflops={NAMES[c]: round(pk[c], 1) for c in range(5)}, clocks=clocks)
+               peaks_tflops={NAMES[c]: round(pk[c], 1) for c in range(len(NAMES))}, clocks=clocks)
     g.close()
     del A, Bm, C, out
     torch.cuda.empty_cache()

@@ -57,7 +57,7 @@ def main():
                           pairs=st["pairs"], launches=st["launches_execute"], ws_gb=st["workspace_bytes"] / 1e9,
                           class_ms=[round(x, 3) for x in st["class_ms"]],
                           class_tflops=[round(st["flops"][c] / (st["class_ms"][c] * 1e-3) / 1e12, 1) if st["class_ms"][c] else 0
-                                        for c in range(5)])))
+                                        for c in range(len(st["class_ms"]))])))
 
 
 if __name__ == "__main__":
