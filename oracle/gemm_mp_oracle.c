@@ -678,7 +678,7 @@ int orc_gemm_mp(const orc_desc_t *d, const double *A, int64_t lda, const double 
                 orc_acc_init(nb, codec, d->beta, cin, cins, acc);
                 for (int64_t s0 = 0; s0 < kt; s0 += ORC_STEP_DEPTH) {
                     int64_t s1 = s0 + ORC_STEP_DEPTH < kt ? s0 + ORC_STEP_DEPTH : kt;
-                    for (int c = 4; c >= 0; --c) {
+                    for (int c = ORC_NCLS - 1; c >= 0; --c) {
                         for (int64_t l = s0; l < s1; ++l) {
                             int ca = o->acode[i * kt + l], cb = o->bcode[l * nt + j];
                             if ((ca > cb ? ca : cb) != c) continue;

@@ -838,13 +838,13 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
   {
     // codes, scales and status -> mapped host memory by a kernel, then the sync
     const int64_t nall = pl->nA + pl->nB + pl->nC;
-    const int64_t o_s5 = align_up(nall, 16), o_scin = o_s5 + align_up((pl->nA + pl->nB) * 10, 16),
+    const int64_t o_s5 = align_up(nall, 16), o_scin = o_s5 + align_up((pl->nA + pl->nB) * NC * 2, 16),
                   o_st = o_scin + align_up(pl->nC * 2, 16), total = o_st + 16;
     Stage* st = stage_acquire((size_t)total);
     if (!st) return fail(GMP_ERR_CUDA, "pinned staging buffer allocation failed");
     k_xfer<<<xfer_grid(nall), 256, 0, stream>>>(codes, st->d, nall);
-    k_xfer<<<xfer_grid((pl->nA + pl->nB) * 10), 256, 0, stream>>>((const uint8_t*)s5, st->d + o_s5,
-                                                                 (pl->nA + pl->nB) * 10);
+    k_xfer<<<xfer_grid((pl->nA + pl->nB) * NC * 2), 256, 0, stream>>>((const uint8_t*)s5, st->d + o_s5,
+                                                                 (pl->nA + pl->nB) * NC * 2);
     k_xfer<<<xfer_grid(pl->nC * 2), 256, 0, stream>>>((const uint8_t*)scin, st->d + o_scin, pl->nC * 2);
     k_xfer<<<1, 32, 0, stream>>>((const uint8_t*)status, st->d + o_st, (int64_t)sizeof(int));
     const cudaError_t e1 = cudaGetLastError();
@@ -853,8 +853,8 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
       std::memcpy(pl->codeA.data(), st->h, pl->nA);
       std::memcpy(pl->codeB.data(), st->h + pl->nA, pl->nB);
       std::memcpy(pl->codeC.data(), st->h + pl->nA + pl->nB, pl->nC);
-      std::memcpy(pl->sA5.data(), st->h + o_s5, pl->nA * 10);
-      std::memcpy(pl->sB5.data(), st->h + o_s5 + pl->nA * 10, pl->nB * 10);
+      std::memcpy(pl->sA5.data(), st->h + o_s5, pl->nA * NC * 2);
+      std::memcpy(pl->sB5.data(), st->h + o_s5 + pl->nA * NC * 2, pl->nB * NC * 2);
       std::memcpy(pl->sCin.data(), st->h + o_scin, pl->nC * 2);
       std::memcpy(&h_status, st->h + o_st, sizeof(int));
     }

@@ -184,3 +184,27 @@ def test_explicit_maps_paper_mode():
     o = oracle.gemm_mp(A, B, C, 32, 1e-6, 1.0, 1.0, 0b00011, a_map=amap, b_map=bmap, c_map=cmap)
     assert np.array_equal(o["acode"], amap) and np.array_equal(o["ccode"], cmap)
     assert _tol_metric(o["C"], A, B, C, 1.0, 1.0) < 1e-6
+
+
+@pytest.mark.parametrize("cls", [FP64, FP32, FP16, BF16, E4M3, E5M2])
+def test_every_pair_class_contributes(cls):
+    """All tiles of A, B, C mapped to one class (explicit maps), non-negative data
+    (no cancellation, so ||A B|| ~ ||A|| ||B||): C must match alpha A B + beta C
+    relative to itself within that class's storage + accumulation error -- a class
+    that the fold skipped leaves C = beta C_in (relative error ~1) -- and, for the
+    16/8-bit classes, show that class's rounding (the class path really ran)."""
+    nb = 32
+    w = gmp_inputs.small_workload(96, 64, 128, nb, 1e-6, mode="uniform", E=0, beta=0.5, seed=11)
+    A, B, C = (np.abs(x) for x in w.matrices())
+    mt, nt, kt = 3, 2, 4
+    maps = dict(a_map=np.full((mt, kt), cls, np.uint8), b_map=np.full((kt, nt), cls, np.uint8),
+                c_map=np.full((mt, nt), cls, np.uint8))
+    o = oracle.gemm_mp(A, B, C, nb, 1e-6, 1.0, 0.5, 0b111111, **maps)
+    assert o["rc"] == 0 and (o["acode"] == cls).all() and (o["ccode"] == cls).all()
+    ref = A @ B + 0.5 * C
+    err = np.linalg.norm(o["C"] - ref) / np.linalg.norm(ref)
+    u = [2.0 ** -53, 2.0 ** -24, 2.0 ** -11, 2.0 ** -8, 2.0 ** -4, 2.0 ** -3][cls]
+    # storage of A, B, C_in and the final C each <= u relative (no cancellation), accumulation <= K u32
+    assert err <= 4 * u + 128 * 2.0 ** -24 + 1e-15, err
+    if cls >= FP16:
+        assert err > 1e-2 * u   # the class's rounding is visible: the class path really ran
