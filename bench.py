@@ -217,7 +217,7 @@ def run_reference(a, w, rank):
     value = fl * a.steps / tot / 1e12
     out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": a.gpus, "steps": a.steps,
            "warmup": a.warmup, "ms_per_step": tot / a.steps * 1e3, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32 (emulated classes)", "data": "synthetic",
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64/f32 (emulated classes)", "data": "synthetic",
            "impl": "reference",
            "config": {"workload": w.name, "M": w.M, "N": w.N, "K": w.K, "nb": w.nb, "tol": w.tol},
            "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
