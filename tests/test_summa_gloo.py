@@ -19,7 +19,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-BY = [8, 4, 2, 2, 1]
+BY = [8, 4, 2, 2, 1, 1]
 
 
 def _free_port():
@@ -50,7 +50,7 @@ def _worker(rank, G, port, q_out, sender=False):
     try:
         nb = 64 if False else 128
         w = gmp_inputs.small_workload(5 * nb, 3 * nb, 9 * nb, nb, 1e-4, mode="random", E=32, beta=0.0,
-                                      class_mask=0b11111, seed=9)
+                                      class_mask=0b111111, seed=9)
         A, Bm, C = w.matrices()
         o = oracle.gemm_mp(A, Bm, None, nb, w.tol, w.alpha, 0.0, w.class_mask, ctiles=[])
         mt, kt, nt = o["acode"].shape[0], o["acode"].shape[1], o["bcode"].shape[1]

@@ -22,7 +22,7 @@ from paper_2508_14848_b200 import binding as B  # noqa: E402
 def closed_form_recv(acode, bcode, nb, P, Q, p, q):
     mt, kt = acode.shape
     nt = bcode.shape[1]
-    by = [8, 4, 2, 2, 1]
+    by = [8, 4, 2, 2, 1, 1]
     tot = 0
     for i in range(p, mt, P):
         for l in range(kt):
@@ -48,7 +48,7 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     if a.cfg == "small":
         w = gmp_inputs.small_workload(2048, 1536, 2560, 256, 1e-4, mode="random", E=32, beta=0.75, seed=5,
-                                      class_mask=0b11111)
+                                      class_mask=0b111111)
     else:
         w = gmp_inputs.workload(int(a.cfg))
     P, Q = api.default_grid(G)
