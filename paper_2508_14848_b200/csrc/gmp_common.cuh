@@ -144,6 +144,16 @@ __device__ __forceinline__ double round_to_class(double x, int c) {
   }
 }
 
+// x * 2^e with one rounding (exact unless the result under/overflows), as ldexp:
+// when 2^e is a normal binary64 the product IS ldexp(x, e) (multiplication by a
+// power of two rounds once, like scalbn), built from the exponent bits instead of
+// the library's branchy loop (measured: the per-pair ldexp of the fold was a
+// quarter of the stall samples of the FP16-class epilogue).
+__device__ __forceinline__ double ldexp_fast(double x, int e) {
+  if (e >= -1022 && e <= 1023) return __dmul_rn(x, __longlong_as_double((long long)(1023 + e) << 52));
+  return ldexp(x, e);
+}
+
 // RN_32 of a binary64 tile-GEMM result (class 0 folded into a binary32 W)
 __device__ __forceinline__ float to_f32(float x) { return x; }
 __device__ __forceinline__ float to_f32(double x) { return __double2float_rn(x); }

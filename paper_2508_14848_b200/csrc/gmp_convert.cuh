@@ -81,8 +81,8 @@ __device__ __forceinline__ void pack_block(const PackJob& j, uint8_t* ws, int nb
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         double2 x = __ldg(s + i);
-        v[2 * i] = (C == 0) ? x.x : ldexp(x.x, j.scale);
-        v[2 * i + 1] = (C == 0) ? x.y : ldexp(x.y, j.scale);
+        v[2 * i] = (C == 0) ? x.x : ldexp_fast(x.x, j.scale);
+        v[2 * i + 1] = (C == 0) ? x.y : ldexp_fast(x.y, j.scale);
       }
       store8<C>(dst + ((int64_t)(r0 + r) * nb + c0 + g * 8) * B, v);
     }
@@ -108,7 +108,7 @@ __device__ __forceinline__ void pack_block(const PackJob& j, uint8_t* ws, int nb
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const double x = sm[sw64(g * 8 + i, oc)];
-        v[i] = (C == 0) ? x : ldexp(x, j.scale);
+        v[i] = (C == 0) ? x : ldexp_fast(x, j.scale);
       }
       store8<C>(dst + ((int64_t)(c0 + oc) * nb + r0 + g * 8) * B, v);
     }
@@ -150,7 +150,7 @@ __device__ __forceinline__ void shadow_run(const ShadowJob& j, uint8_t* ws, int6
        e0 += (int64_t)gridDim.x * blockDim.x * 8) {
     double v[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = ldexp(payload_f64(src, e0 + i, F), j.d);
+    for (int i = 0; i < 8; ++i) v[i] = ldexp_fast(payload_f64(src, e0 + i, F), j.d);
     store8<T>(dst + e0 * class_bytes(T), v);
   }
 }
@@ -191,7 +191,7 @@ __device__ __forceinline__ void shadow_t_block(const ShadowJob& j, uint8_t* ws, 
 #pragma unroll
   for (int u = 0; u < 16; ++u) {
     const int unit = t + u * 256;
-    sm[sw64(unit >> 6, unit & 63)] = ldexp(x[u], j.d);
+    sm[sw64(unit >> 6, unit & 63)] = ldexp_fast(x[u], j.d);
   }
   __syncthreads();
 #pragma unroll
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(256) k_acc_init(const CTileDesc* __restrict__ 
     } else {
       float x = 0.f;
       if (beta != 0.0)
-        x = __double2float_rn(__dmul_rn((double)bf, ldexp(payload_f64(ws + c.cin_off, e, c.code), -c.cin_scale)));
+        x = __double2float_rn(__dmul_rn((double)bf, ldexp_fast(payload_f64(ws + c.cin_off, e, c.code), -c.cin_scale)));
       reinterpret_cast<float*>(ws + c.w_off)[e] = x;
     }
   }
@@ -351,8 +351,8 @@ __global__ void __launch_bounds__(256) k_c_finalize(const CTileDesc* __restrict_
       const float* wrow = reinterpret_cast<const float*>(ws + c.w_off) + r * nb;
       for (int col = threadIdx.x; col < nb; col += blockDim.x) {
         const int64_t i = r * nb + col;
-        payload_store(pay, i, c.code, ldexp((double)wrow[col], e));
-        urow[col] = ldexp(payload_f64(pay, i, c.code), -e);
+        payload_store(pay, i, c.code, ldexp_fast((double)wrow[col], e));
+        urow[col] = ldexp_fast(payload_f64(pay, i, c.code), -e);
       }
     }
   }
@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(256) k_synth(SynthArgs a) {
       const uint64_t w = mix64(a.tau + ((uint64_t)(ti * ntg + tj) + 1ull) * 0x9E3779B97F4A7C15ull);
       e = (int)(w % (uint64_t)(a.E + 1));
     }
-    a.out[lr * a.ld + lc] = ldexp(v, a.s - e);
+    a.out[lr * a.ld + lc] = ldexp_fast(v, a.s - e);
   }
 }
 

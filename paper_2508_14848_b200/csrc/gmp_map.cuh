@@ -106,7 +106,7 @@ __device__ __forceinline__ double delta_in(int k, int nb) {
 // shadow scale = e_code + scale_exp(RN_code(maxabs 2^e_code), c)  (max of the
 // decoded payload, by monotonicity of RN; O6)
 __device__ void fill_scales5(double maxabs, int code, int e_code, int16_t* s5) {
-  double pm = (code == 0) ? maxabs : round_to_class(ldexp(maxabs, e_code), code);
+  double pm = (code == 0) ? maxabs : round_to_class(ldexp_fast(maxabs, e_code), code);
   for (int c = 0; c < GMP_NCLASS; ++c)
     s5[c] = (c < code) ? 0 : (c == code) ? (int16_t)e_code : (int16_t)(e_code + scale_exp(pm, c));
 }
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(1024) k_map_finalize(FinalizeArgs a) {
         if (M == 0.0) { chosen = kk; break; }
         const int e = scale_exp(M, kk);
         const double lhs = __dadd_rn(__dmul_rn(delta_in(kk, a.nb), __dsqrt_rn(S)),
-                                     __dmul_rn((double)a.nb, ldexp(class_eta(kk), -e - 1)));
+                                     __dmul_rn((double)a.nb, ldexp_fast(class_eta(kk), -e - 1)));
         if (lhs <= rhs) { chosen = kk; break; }
       }
     }
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(1024) k_map_finalize(FinalizeArgs a) {
           const int ca = a.codeA[i * a.kt + l], cb = a.codeB[l * a.nt + j];
           const int c = ca > cb ? ca : cb;
           const int ea = a.scaleA5[(i * a.kt + l) * GMP_NCLASS + c], eb = a.scaleB5[(l * a.nt + j) * GMP_NCLASS + c];
-          const double f = ldexp(a.alpha, -(ea + eb));
+          const double f = ldexp_fast(a.alpha, -(ea + eb));
           if (f != 0.0 && !(fabs(f) >= 0x1p-126 && fabs(f) <= 0x1p100)) ok = false;
         }
         if (!ok) chosen = 0;

@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(256) k_slice64(const SliceJob* __restrict__ jo
       int8_t q[OZ_NS][4];
 #pragma unroll
       for (int e4 = 0; e4 < 4; ++e4) {
-        double a = ldexp(sm[kk0 + e4][r], -sexp[r]);
+        double a = ldexp_fast(sm[kk0 + e4][r], -sexp[r]);
 #pragma unroll
         for (int i = 0; i < OZ_NS; ++i) {
           const double tt = a * 128.0;        // exact
@@ -259,7 +259,7 @@ k_tc_fp64(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       }
       for (int pi = 0; pi < w.pcnt; ++pi) {
         const PairDesc pd = pairs[w.pbeg + pi];
-        const double f64 = ldexp(alpha, pd.fexp);
+        const double f64 = ldexp_fast(alpha, pd.fexp);
         const float f32 = __double2float_rn(f64);
         const int er = exps[(int64_t)pd.a_slot * nb + w.m0 + rloc];
         const int16_t* fcol = exps + (int64_t)pd.b_slot * nb + w.n0 + cg * 32;

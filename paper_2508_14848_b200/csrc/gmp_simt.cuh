@@ -174,7 +174,7 @@ k_simt_class(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pa
       __syncthreads();
     }
     // ---- fold (O9): W = fma_W(RN_W(alpha 2^fexp), RN_W(P), W) ----
-    const double f64 = ldexp(alpha, pd.fexp);
+    const double f64 = ldexp_fast(alpha, pd.fexp);
     const float f32 = __double2float_rn(f64);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -358,7 +358,7 @@ k_mn(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
       const int pi = cpair++;
       // ---- fold (O9): W = fma_W(RN_W(alpha 2^fexp), RN_W(P), W) ----
       const PairDesc pd = pairs[it.pbeg + pi];
-      const double f64 = ldexp(alpha, pd.fexp);
+      const double f64 = ldexp_fast(alpha, pd.fexp);
       const float f32 = __double2float_rn(f64);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -523,7 +523,7 @@ k_dmma(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
       // DMMA registers; W is read and written once per run of equal factors ----
       const PairDesc pd = pairs[it.pbeg + cpair++];
       if (cpair < it.pcnt && pairs[it.pbeg + cpair].fexp == pd.fexp) continue;
-      const double f64 = ldexp(alpha, pd.fexp);
+      const double f64 = ldexp_fast(alpha, pd.fexp);
       const float f32 = __double2float_rn(f64);
 #pragma unroll
       for (int i = 0; i < 2; ++i)

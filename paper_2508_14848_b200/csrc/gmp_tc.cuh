@@ -245,7 +245,7 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
         }
         for (int pi = 0; pi < w.pcnt; ++pi) {
           const PairDesc pd = pairs[w.pbeg + pi];
-          const float f32 = __double2float_rn(ldexp(alpha, pd.fexp));
+          const float f32 = __double2float_rn(ldexp_fast(alpha, pd.fexp));
           mbar_wait(&tfull[acc], acc_phase);
           tc_fence_after();
           const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + half * HC);
@@ -276,7 +276,7 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
         }
         for (int pi = 0; pi < w.pcnt; ++pi) {
           const PairDesc pd = pairs[w.pbeg + pi];
-          const double f64 = ldexp(alpha, pd.fexp);
+          const double f64 = ldexp_fast(alpha, pd.fexp);
           mbar_wait(&tfull[acc], acc_phase);
           tc_fence_after();
           const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + half * HC);
@@ -303,7 +303,7 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
         double* wrow = reinterpret_cast<double*>(ws + ct.w_off) + rowoff;
         for (int pi = 0; pi < w.pcnt; ++pi) {
           const PairDesc pd = pairs[w.pbeg + pi];
-          const double f64 = ldexp(alpha, pd.fexp);
+          const double f64 = ldexp_fast(alpha, pd.fexp);
           mbar_wait(&tfull[acc], acc_phase);
           tc_fence_after();
           const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + half * HC);

@@ -197,7 +197,7 @@ k_tc2_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       }
       for (int pi = 0; pi < w.pcnt; ++pi) {
         const PairDesc pd = pairs[w.pbeg + pi];
-        const float f32 = __double2float_rn(ldexp(alpha, pd.fexp));
+        const float f32 = __double2float_rn(ldexp_fast(alpha, pd.fexp));
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * TC2_BN + half * HC);
@@ -368,7 +368,7 @@ k_tcmc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       }
       for (int pi = 0; pi < w.pcnt; ++pi) {
         const PairDesc pd = pairs[w.pbeg + pi];
-        const float f32 = __double2float_rn(ldexp(alpha, pd.fexp));
+        const float f32 = __double2float_rn(ldexp_fast(alpha, pd.fexp));
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + half * HC);
