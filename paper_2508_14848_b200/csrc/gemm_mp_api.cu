@@ -1099,21 +1099,10 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
               k_mn<double><<<(unsigned)L.icount, 256, mn_smem_bytes<double>(), stream>>>(it, pd, dct, ws, (int)nb,
                                                                                        pl->d.alpha);
             } else {
-              // experiment knob (unset = product configuration BK 16 x 4 stages)
-              static const int dv = getenv("GMP_DMMA_VARIANT") ? atoi(getenv("GMP_DMMA_VARIANT")) : 0;
-              if (dv == 1) {
-                using V = DmmaCfg<DMMA_WN, 32, 2>;
-                GMP_TRY(set_smem_once(k_dmma<DMMA_WN, 32, 2>, V::SMEM));
-                k_dmma<DMMA_WN, 32, 2><<<(unsigned)L.icount, 256, V::SMEM, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha);
-              } else if (dv == 2) {
-                using V = DmmaCfg<DMMA_WN, 16, 3>;
-                GMP_TRY(set_smem_once(k_dmma<DMMA_WN, 16, 3>, V::SMEM));
-                k_dmma<DMMA_WN, 16, 3><<<(unsigned)L.icount, 256, V::SMEM, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha);
-              } else {
-                using V = DmmaCfg<DMMA_WN>;
-                GMP_TRY(set_smem_once(k_dmma<DMMA_WN>, V::SMEM));
-                k_dmma<DMMA_WN><<<(unsigned)L.icount, 256, V::SMEM, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha);
-              }
+              // BK = 16 x 4 stages (BK 32 x 2 and 16 x 3 measured equal, profiles/dmma_peak_r01.md)
+              using V = DmmaCfg<DMMA_WN>;
+              GMP_TRY(set_smem_once(k_dmma<DMMA_WN>, V::SMEM));
+              k_dmma<DMMA_WN><<<(unsigned)L.icount, 256, V::SMEM, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha);
             }
             break;
           case 1:
