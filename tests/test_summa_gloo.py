@@ -138,8 +138,7 @@ def _worker(rank, G, port, q_out, sender=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("sender", [False, True])
-@pytest.mark.parametrize("G", [2, 4])
+@pytest.mark.parametrize("G,sender", [(2, False), (4, False), (2, True), (4, True), (8, False)])
 def test_summa_schedule_over_gloo(G, sender):
     ctx = mp.get_context("spawn")
     qo = ctx.Queue()
