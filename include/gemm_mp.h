@@ -52,7 +52,7 @@ typedef enum {
   GMP_OK = 0,
   GMP_ERR_ARG = 1,           /* null/invalid argument, tol <= 0 or not finite, ld too small */
   GMP_ERR_NOT_DIVISIBLE = 2, /* nb does not divide M, N or K, or nb is not a multiple of 128 */
-  GMP_ERR_MAP_SHAPE = 3,     /* explicit map holds a code > 4                                  */
+  GMP_ERR_MAP_SHAPE = 3,     /* explicit map holds a code > 5                                  */
   GMP_ERR_NONFINITE = 4,     /* A, B (or C with beta != 0) holds a NaN or an infinity          */
   GMP_ERR_GRID = 5,          /* P*Q, rank and communicator are inconsistent                    */
   GMP_ERR_WORKSPACE = 6,     /* scratch or workspace smaller than the size query returned      */
@@ -138,14 +138,18 @@ gmp_status_t gemm_mp_plan(const gmp_desc_t *desc, const double *A, int64_t lda, 
 gmp_status_t gemm_mp_workspace_size(gmp_plan_t plan, size_t *bytes);
 
 /* S3 + S5 (local tiles): convert-and-pack every local tile of A, B (and C_in)
- * into its class with one RNE rounding and its power-of-two scale, then the
- * receiver-side shadows needed by local tile-GEMMs.  Async on `stream`.  After
+ * into its class with one RNE rounding and its power-of-two scale (PAPER.md:148,
+ * DESIGN.md O3/O6), then the receiver-side shadows needed by local tile-GEMMs
+ * (and, under GMP_FLAG_SENDER_SIDE, the shadows this rank sends).  Host tables
+ * reach the device through pinned staging read by a kernel, never through a
+ * copy engine.  ws must be 1024-byte aligned.  Async on `stream`.  After
  * completion A and B may be freed.  ws stays owned by the caller and must
  * outlive every execute of this plan.                                          */
 gmp_status_t gemm_mp_convert(gmp_plan_t plan, void *ws, size_t ws_bytes, void *stream);
 
 /* S4 - S7: per SUMMA step, NCCL broadcasts of the step's A/B panels in stored
- * precision (P*Q > 1) + shadows of received tiles on a comm stream, then one
+ * precision (P*Q > 1; or their needed shadow classes under GMP_FLAG_SENDER_SIDE)
+ * + shadows of received tiles on a comm stream, then one
  * grouped tile-GEMM launch per precision class present, folding into the W
  * accumulators; finally C-finalize writes the packed C and the binary64 user C
  * (local layout, ldc).  Collective over the grid.  Async on `stream`; may be
