@@ -9,7 +9,7 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgemm_mp.so")
+LIB_PATH = os.environ.get("GMP_LIB_PATH") or os.path.join(_HERE, "libgemm_mp.so")   # override: A/B builds
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "gemm_mp.h")
 
 GMP_FP64, GMP_FP32, GMP_FP16, GMP_BF16, GMP_E4M3, GMP_E5M2 = range(6)
