@@ -679,7 +679,7 @@ static void build_tables(gmp_plan_s* pl) {
         continue;
       }
       // flat launch size: items x sub-tiles of the class kernel's CTA tile
-      const int bn = ozaki ? OZ_BN : split ? 128 : tc ? tcbn : mn_bn(c);
+      const int bn = ozaki ? OZ_BN : split ? 128 : tc ? tcbn : (c == 0 && kind == 0) ? DMMA_BN : mn_bn(c);
       pl->launches.push_back(Launch{s, c, kind, ibeg, (int64_t)its.size() * subtiles_per_item((int)nb, bn), bn});
     }
   }
@@ -1100,9 +1100,10 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
                                                                                        pl->d.alpha);
             } else {
               // BK = 16 x 4 stages (BK 32 x 2 and 16 x 3 measured equal, profiles/dmma_peak_r01.md)
-              using V = DmmaCfg<DMMA_WN>;
-              GMP_TRY(set_smem_once(k_dmma<DMMA_WN>, V::SMEM));
-              k_dmma<DMMA_WN><<<(unsigned)L.icount, 256, V::SMEM, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha);
+              using V = DmmaProduct;
+              GMP_TRY(set_smem_once(k_dmma<DMMA_WN, 16, 4, DMMA_WGN>, V::SMEM));
+              k_dmma<DMMA_WN, 16, 4, DMMA_WGN><<<(unsigned)L.icount, V::THREADS, V::SMEM, stream>>>(it, pd, dct, ws,
+                                                                                                (int)nb, pl->d.alpha);
             }
             break;
           case 1:

@@ -410,16 +410,21 @@ k_mn(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
 // The accumulation order inside a DMMA is the hardware's: the parity bound is
 // the all-FP64 1e-13 relative Frobenius.
 // ---------------------------------------------------------------------------
-template <int WN, int BK_ = 16, int ST_ = 4> struct DmmaCfg {
+template <int WN, int BK_ = 16, int ST_ = 4, int WGN_ = 2> struct DmmaCfg {
   static constexpr int BK = BK_, ST = ST_;          // k-rows per stage (multiple of 16), ring depth
-  static constexpr int BN = 2 * WN;                 // 8 warps = 4 (m) x 2 (n), warp tile 32 x WN
+  static constexpr int WGN = WGN_;                  // warp columns: 4 (m) x WGN (n) warps, warp tile 32 x WN
+  static constexpr int BN = WGN * WN;
+  static constexpr int THREADS = 4 * WGN * 32;
   static constexpr int AP = 128 + 4, BP = BN + 4;   // row pitches in doubles (= 32 B mod 128 B)
   static constexpr int SMEM = ST * BK * (AP + BP) * 8;
-  static constexpr int MINB = (WN == 32) ? 2 : 1;
+  static constexpr int MINB = (THREADS == 256 && WN == 32) ? 2 : 1;
 };
-constexpr int DMMA_WN = 32;                         // product configuration (128 x 64 sub-tiles; 32 x 64 warp
-                                                    // tiles at 1 CTA/SM measured 9 % slower)
-constexpr int DMMA_BN = DmmaCfg<DMMA_WN>::BN;
+// product: 128 x 64 sub-tiles, 8 warps of 32 x 32, 2 CTAs/SM.  Measured alternatives
+// (profiles/dmma_peak_r01.md): 32 x 64 warp tiles at 1 CTA/SM 9 % slower; 128 x 128
+// sub-tiles with 16 warps (WGN = 4) at 1 CTA/SM 8 % slower (one barrier for all warps).
+constexpr int DMMA_WN = 32, DMMA_WGN = 2;
+using DmmaProduct = DmmaCfg<DMMA_WN, 16, 4, DMMA_WGN>;
+constexpr int DMMA_BN = DmmaProduct::BN;
 
 __device__ __forceinline__ void dmma16816(double (&c)[4], const double (&a)[8], const double (&b)[4]) {
   asm(
@@ -430,22 +435,23 @@ __device__ __forceinline__ void dmma16816(double (&c)[4], const double (&a)[8], 
         "d"(b[1]), "d"(b[2]), "d"(b[3]));
 }
 
-template <int WN, int BK_ = 16, int ST_ = 4>
-__global__ void __launch_bounds__(256, DmmaCfg<WN>::MINB)
+template <int WN, int BK_ = 16, int ST_ = 4, int WGN_ = 2>
+__global__ void __launch_bounds__(DmmaCfg<WN, BK_, ST_, WGN_>::THREADS, DmmaCfg<WN, BK_, ST_, WGN_>::MINB)
 k_dmma(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
        const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha) {
-  using Cfg = DmmaCfg<WN, BK_, ST_>;
+  using Cfg = DmmaCfg<WN, BK_, ST_, WGN_>;
   constexpr int BK = Cfg::BK, ST = Cfg::ST, AP = Cfg::AP, BP = Cfg::BP, BN = Cfg::BN, NJ = WN / 8;
+  constexpr int NT = Cfg::THREADS, WGN = Cfg::WGN;
   constexpr int ACH = 64, BCH = BN / 2;             // 16-byte chunks per k-row (A: 128 doubles, B: BN)
-  constexpr int CHUNKS = BK * (ACH + BCH), CPT = CHUNKS / 256;
+  constexpr int CHUNKS = BK * (ACH + BCH), CPT = CHUNKS / NT;
   constexpr int STAGE = BK * (AP + BP) * 8;
-  static_assert(CHUNKS % 256 == 0, "loader");
+  static_assert(CHUNKS % NT == 0, "loader");
   extern __shared__ __align__(128) uint8_t sm[];
   const WorkItem it = expand_item(items, blockIdx.x, nb, BN);
   const CTileDesc ct = ctiles[it.ctile];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * WN;
+  const int wm = (warp / WGN) * 32, wn = (warp % WGN) * WN;
   const int nsl = nb / BK;
   const int total = it.pcnt * nsl;
   const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
@@ -464,7 +470,7 @@ k_dmma(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
       const uint32_t stg = sbase + (uint32_t)(istage * STAGE);
 #pragma unroll
       for (int u = 0; u < CPT; ++u) {
-        const int c = tid + u * 256;
+        const int c = tid + u * NT;
         if (c < BK * ACH) {
           const int k = c / ACH, ch = c - k * ACH;
           cp_async16(stg + k * AP * 8 + ch * 16, Ag + (int64_t)k * nb * 8 + ch * 16);
