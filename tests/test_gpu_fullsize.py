@@ -64,3 +64,73 @@ def test_cfg2_fullsize_sampled():
         den = abs(w.alpha) * np.linalg.norm(Ah) * np.linalg.norm(Bh) + abs(w.beta) * np.linalg.norm(Ch)
         assert np.linalg.norm(cg - ref) / den <= w.tol
     g.close()
+
+
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_n65536_fullsize_properties(cfg):
+    """BASELINE configs[2]/[3] (N=65536, nb=2048) at full size on one GPU, as bench.py
+    --config 3/4 runs them.  The oracle cannot redo a 65536^3 GEMM, so properties
+    that hold at any size are checked: (1) every stored scale is the oracle's scale
+    definition (O3) of the tile's maxabs; (2) sampled tiles satisfy the criterion for
+    their class and fail it for the next-lower-precision enabled class (O5, norms in
+    binary64 by torch, a 1e-9 band around the threshold is skipped); (3) two sampled
+    row panels of C meet the tolerance against a cuBLAS DGEMM of those panels, with
+    the global normaliser; (4) repeated executes are bitwise identical."""
+    w = gmp_inputs.workload(cfg)
+    nb = w.nb
+    mt, nt, kt = w.M // nb, w.N // nb, w.K // nb
+    dev = torch.device("cuda:0")
+    torch.cuda.empty_cache()
+    A = api.synth(w.M, w.K, nb, w.a, device=dev)
+    Bm = api.synth(w.K, w.N, nb, w.b, device=dev)
+    desc = B.make_desc(w.M, w.N, w.K, nb, w.tol, w.alpha, w.beta, w.class_mask)
+    g = api.GemmMP(desc, A, Bm, None)
+    g.convert()
+    out = torch.empty(w.M, w.N, dtype=torch.float64, device=dev)
+    g.execute(out)
+    g.sync()
+    m = g.maps()
+    st = g.stats()
+    assert sum(st["pairs"]) == mt * nt * kt
+    enabled = {c for c in range(6) if (w.class_mask | 1) >> c & 1}
+    assert set(np.unique(m["acode"])) <= enabled and set(np.unique(m["bcode"])) <= enabled
+    rng = np.random.default_rng(cfg)
+    tiles = [(int(rng.integers(mt)), int(rng.integers(kt))) for _ in range(12)]
+    SX = float((A * A).sum())
+    rhs = (w.tol / 4.0) * np.sqrt(SX) / np.sqrt(mt * kt)
+    u = [2.0 ** -53, 2.0 ** -24, 2.0 ** -11, 2.0 ** -8, 2.0 ** -4, 2.0 ** -3]
+    eta = [2.0 ** -1074, 2.0 ** -149, 2.0 ** -24, 2.0 ** -133, 2.0 ** -9, 2.0 ** -16]
+    ladder = [c for c in (5, 4, 3, 2, 1) if c in enabled]
+
+    def lhs(k, S, mx):
+        e = oracle.scale_exp(mx, k)
+        return (u[k] + np.sqrt(nb) * 2.0 ** -24) * np.sqrt(S) + nb * np.ldexp(eta[k], -e - 1)
+
+    for (ti, tl) in tiles:
+        t = A[ti * nb:(ti + 1) * nb, tl * nb:(tl + 1) * nb]
+        mx = float(t.abs().max())
+        S = float((t * t).sum())
+        code = int(m["acode"][ti, tl])
+        assert int(m["ascale"][ti, tl]) == oracle.scale_exp(mx, code)          # (1)
+        if code != 0:                                                           # (2) eligible
+            assert lhs(code, S, mx) <= rhs * (1 + 1e-9)
+        for k in ladder:                                                        # lower classes rejected
+            if k == code:
+                break
+            assert lhs(k, S, mx) >= rhs * (1 - 1e-9), (ti, tl, k, code)
+    nA = float(torch.linalg.norm(A))
+    nB = float(torch.linalg.norm(Bm))
+    den = abs(w.alpha) * nA * nB
+    for i in (0, mt - 1):                                                       # (3)
+        rows = slice(i * nb, (i + 1) * nb)
+        ref = w.alpha * (A[rows, :] @ Bm)
+        err = float(torch.linalg.norm(out[rows, :] - ref))
+        assert err / den <= w.tol, (i, err / den)
+        del ref
+    first = out.clone()
+    g.execute(out)                                                              # (4)
+    g.sync()
+    assert torch.equal(first, out)
+    g.close()
+    del A, Bm, out, first
+    torch.cuda.empty_cache()
