@@ -184,6 +184,8 @@ struct gmp_plan_s {
   ncclComm_t world = nullptr, rowc = nullptr, colc = nullptr;
   cudaStream_t comm_stream = nullptr;
   std::vector<cudaEvent_t> step_ev;
+  cudaEvent_t packed_ev = nullptr;   // convert: local stored tiles (and sender shadows) are packed
+  bool step0_issued = false;         // convert pre-issued SUMMA step 0 (first execute skips it)
   // global maps (identical on every rank)
   std::vector<uint8_t> codeA, codeB, codeC;
   std::vector<int16_t> sA5, sB5, sCin, sCout;
@@ -972,6 +974,32 @@ static int grid_for(int64_t n_elems, int per_thread) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 4));
 }
 
+// SUMMA step s on the comm stream: grouped broadcasts of the step's panel tiles,
+// then the receiver-side shadows / splits / digit slices of the received tiles;
+// step_ev[s] gates the step's class launches on the compute stream.
+static gmp_status_t issue_comm_step(gmp_plan_s* pl, uint8_t* ws, int s) {
+  const int64_t nb = pl->d.nb;
+  GMP_NCCL(ncclGroupStart());
+  for (const Bcast& b : pl->bcast_step[s])
+    GMP_NCCL(ncclBroadcast(ws + b.off, ws + b.off, (size_t)b.bytes, ncclUint8, b.root,
+                           b.which == 0 ? pl->rowc : pl->colc, pl->comm_stream));
+  GMP_NCCL(ncclGroupEnd());
+  GMP_TRY(launch_shadows((const ShadowJob*)(ws + pl->off_shadow) + pl->shadow_step_off[s], pl->shadow_step[s], ws,
+                         (int)nb, pl->comm_stream));
+  if (!pl->split_step[s].empty()) {
+    k_split<<<dim3((unsigned)((nb / 64) * (nb / 64)), (unsigned)pl->split_step[s].size()), 256, 0,
+              pl->comm_stream>>>((const SplitJob*)(ws + pl->off_split) + pl->split_step_off[s], ws, (int)nb);
+    GMP_CUDA(cudaGetLastError());
+  }
+  if (!pl->slice_step[s].empty()) {
+    k_slice64<<<dim3((unsigned)(nb / 64), (unsigned)pl->slice_step[s].size()), 256, 0, pl->comm_stream>>>(
+        (const SliceJob*)(ws + pl->off_slice) + pl->slice_step_off[s], ws, (int)nb);
+    GMP_CUDA(cudaGetLastError());
+  }
+  GMP_CUDA(cudaEventRecord(pl->step_ev[s], pl->comm_stream));
+  return GMP_OK;
+}
+
 extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_bytes, void* stream_) {
   if (!pl) return fail(GMP_ERR_ARG, "plan is NULL");
   if (!ws_ || (int64_t)ws_bytes < pl->ws_bytes) return fail(GMP_ERR_WORKSPACE, "workspace too small");
@@ -1006,6 +1034,16 @@ extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_byte
   }
   // S5 shadows of local tiles
   GMP_TRY(launch_shadows((const ShadowJob*)(ws + pl->off_shadow), pl->shadow_local, ws, (int)nb, stream));
+  // multi-GPU: SUMMA step 0 starts as soon as this rank's panel tiles are packed,
+  // overlapping the rest of convert (splits, digit slices) and the accumulator init
+  pl->step0_issued = false;
+  if (pl->P * pl->Q > 1 && pl->st.steps > 0) {
+    if (!pl->packed_ev) GMP_CUDA(cudaEventCreateWithFlags(&pl->packed_ev, cudaEventDisableTiming));
+    GMP_CUDA(cudaEventRecord(pl->packed_ev, stream));
+    GMP_CUDA(cudaStreamWaitEvent(pl->comm_stream, pl->packed_ev, 0));
+    GMP_TRY(issue_comm_step(pl, ws, 0));
+    pl->step0_issued = true;
+  }
   if (!pl->split_local.empty()) {
     k_split<<<dim3((unsigned)((nb / 64) * (nb / 64)), (unsigned)pl->split_local.size()), 256, 0, stream>>>(
         (const SplitJob*)(ws + pl->off_split), ws, (int)nb);
@@ -1048,30 +1086,20 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
   const bool multi = pl->P * pl->Q > 1;
   cudaEvent_t ready = nullptr;
   if (multi) {
-    // comm stream starts after everything already queued on `stream` (convert, init)
-    GMP_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-    GMP_CUDA(cudaEventRecord(ready, stream));
-    GMP_CUDA(cudaStreamWaitEvent(pl->comm_stream, ready, 0));
-    for (int s = 0; s < steps; ++s) {
-      GMP_NCCL(ncclGroupStart());
-      for (const Bcast& b : pl->bcast_step[s])
-        GMP_NCCL(ncclBroadcast(ws + b.off, ws + b.off, (size_t)b.bytes, ncclUint8, b.root,
-                               b.which == 0 ? pl->rowc : pl->colc, pl->comm_stream));
-      GMP_NCCL(ncclGroupEnd());
-      GMP_TRY(launch_shadows((const ShadowJob*)(ws + pl->off_shadow) + pl->shadow_step_off[s], pl->shadow_step[s],
-                             ws, (int)nb, pl->comm_stream));
-      if (!pl->split_step[s].empty()) {
-        k_split<<<dim3((unsigned)((nb / 64) * (nb / 64)), (unsigned)pl->split_step[s].size()), 256, 0,
-                  pl->comm_stream>>>((const SplitJob*)(ws + pl->off_split) + pl->split_step_off[s], ws, (int)nb);
-        GMP_CUDA(cudaGetLastError());
-      }
-      if (!pl->slice_step[s].empty()) {
-        k_slice64<<<dim3((unsigned)(nb / 64), (unsigned)pl->slice_step[s].size()), 256, 0, pl->comm_stream>>>(
-            (const SliceJob*)(ws + pl->off_slice) + pl->slice_step_off[s], ws, (int)nb);
-        GMP_CUDA(cudaGetLastError());
-      }
-      GMP_CUDA(cudaEventRecord(pl->step_ev[s], pl->comm_stream));
+    int s0 = 0;
+    if (pl->step0_issued) {
+      // first execute after convert: step 0 is already in flight (issued by convert
+      // once the panel tiles were packed); later steps queue behind it
+      s0 = 1;
+      pl->step0_issued = false;
+    } else {
+      // repeated execute: the comm stream starts after everything queued on
+      // `stream` (the previous execute still reads the receive slots)
+      GMP_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+      GMP_CUDA(cudaEventRecord(ready, stream));
+      GMP_CUDA(cudaStreamWaitEvent(pl->comm_stream, ready, 0));
     }
+    for (int s = s0; s < steps; ++s) GMP_TRY(issue_comm_step(pl, ws, s));
   }
   size_t li = 0;
   for (int s = 0; s < steps; ++s) {
@@ -1281,6 +1309,7 @@ extern "C" gmp_status_t gemm_mp_synth(double* out, int64_t ld, int64_t rows, int
 extern "C" void gemm_mp_destroy(gmp_plan_t pl) {
   if (!pl) return;
   for (auto& e : pl->step_ev) if (e) cudaEventDestroy(e);
+  if (pl->packed_ev) cudaEventDestroy(pl->packed_ev);
   for (auto& e : pl->launch_ev) if (e) cudaEventDestroy(e);
   tc_release(pl->tc);
   delete pl;
