@@ -24,18 +24,18 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("sender", [False, True])
-@pytest.mark.parametrize("G", [2, 4])
-def test_summa_bitwise_vs_single_gpu(G, sender):
+@pytest.mark.parametrize("G,sender,cfg", [(2, False, "small"), (2, True, "small"), (4, False, "small"),
+                                          (4, True, "small"), (2, False, "uneven"), (4, True, "uneven")])
+def test_summa_bitwise_vs_single_gpu(G, sender, cfg):
     if torch.cuda.device_count() < G:
         pytest.skip(f"needs {G} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={G}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(ROOT, "tools", "multi_gpu_check.py")] + (["--sender"] if sender else [])
+           os.path.join(ROOT, "tools", "multi_gpu_check.py"), "--cfg", cfg] + (["--sender"] if sender else [])
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
     res = json.loads(line)
     assert res["ok"], res["msgs"]
-    if sender:   # the E4M3-enabled random workload has panel tiles sent cheaper than stored
+    if sender and cfg == "small":   # the FP8-enabled random workload has panel tiles sent cheaper than stored
         assert res["recv_bytes_all"] < res["stored_bytes_all"], res

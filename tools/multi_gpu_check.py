@@ -49,6 +49,9 @@ def main():
     if a.cfg == "small":
         w = gmp_inputs.small_workload(2048, 1536, 2560, 256, 1e-4, mode="random", E=32, beta=0.75, seed=5,
                                       class_mask=0b111111)
+    elif a.cfg == "uneven":   # tile grids that do not divide by P or Q (5 x 3 x 7 tiles of 256)
+        w = gmp_inputs.small_workload(1280, 768, 1792, 256, 1e-3, mode="graded", E=24, beta=-0.5, seed=6,
+                                      class_mask=0b111111)
     else:
         w = gmp_inputs.workload(int(a.cfg))
     P, Q = api.default_grid(G)
