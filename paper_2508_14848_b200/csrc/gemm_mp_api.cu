@@ -961,11 +961,7 @@ static gmp_status_t launch_shadows(const ShadowJob* djobs, const std::vector<Sha
 
 template <typename K>
 static gmp_status_t set_smem_once(K kernel, int bytes) {
-  static std::vector<const void*> done;
-  const void* key = reinterpret_cast<const void*>(kernel);
-  for (const void* d : done) if (d == key) return GMP_OK;
-  GMP_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  done.push_back(key);
+  GMP_CUDA(ensure_max_smem(kernel, bytes));
   return GMP_OK;
 }
 

@@ -13,6 +13,10 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <mutex>
+#include <utility>
+#include <vector>
+
 #define GMP_NCLASS 6
 // workspace arenas: one per class, then the FP32 BF16x3 splits and the FP64 int8 digits
 #define GMP_AR_SPLIT (GMP_NCLASS)
@@ -167,6 +171,24 @@ __device__ __forceinline__ int scale_exp(double maxabs, int c) {
   double m = frexp(maxabs, &E);
   double mo = frexp(class_omega(c), &Eo);
   return (m <= mo) ? (Eo - E) : (Eo - 1 - E);
+}
+
+// Opt a kernel into `bytes` of dynamic shared memory once per (kernel, device):
+// the attribute is per device, so a process driving several GPUs sets it on each.
+template <class K>
+inline cudaError_t ensure_max_smem(K kernel, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const void* key = reinterpret_cast<const void*>(kernel);
+  std::lock_guard<std::mutex> lk(mu);
+  for (const auto& d : done)
+    if (d.first == key && d.second == dev) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.emplace_back(key, dev);
+  return e;
 }
 
 }  // namespace gmp

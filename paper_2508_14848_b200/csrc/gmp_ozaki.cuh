@@ -344,11 +344,9 @@ inline gmp_status_t oz_prepare(OzTables& t, uint8_t* ws, int64_t arena_off, int6
 inline cudaError_t oz_launch(OzTables& t, const WorkItem* it, int64_t n, const PairDesc* pd, const CTileDesc* ct,
                              uint8_t* ws, int nb, double alpha, int64_t exp_off, cudaStream_t s) {
   if (!t.ready) return cudaErrorNotReady;
-  static bool attr = false;
-  if (!attr) {
-    const cudaError_t e = cudaFuncSetAttribute(k_tc_fp64, cudaFuncAttributeMaxDynamicSharedMemorySize, oz_smem_bytes());
+  {
+    const cudaError_t e = ensure_max_smem(k_tc_fp64, oz_smem_bytes());
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   // one CTA per (item, sub-tile), scheduled in flat order: the CTAs of one C
   // tile run together and walk its pair list in step (L2 reuse of the planes)

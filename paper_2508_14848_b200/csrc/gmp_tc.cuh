@@ -411,12 +411,7 @@ template <int C, int BN>
 inline gmp_status_t tc_launch_t(TcTables& t, const WorkItem* it, int64_t n, const PairDesc* pd, const CTileDesc* ct,
                                 uint8_t* ws, int nb, double alpha, cudaStream_t s) {
   constexpr int smem = tc_smem_bytes<C, BN>();
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(k_tc_class<C, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-      return GMP_ERR_CUDA;
-    attr = true;
-  }
+  if (ensure_max_smem(k_tc_class<C, BN>, smem) != cudaSuccess) return GMP_ERR_CUDA;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -403,12 +403,7 @@ template <int C>
 inline gmp_status_t tcmc_launch_t(TcTables& t, const WorkItem* it, int64_t n, const PairDesc* pd, const CTileDesc* ct,
                                   uint8_t* ws, int nb, double alpha, cudaStream_t s) {
   constexpr int smem = tcmc_smem_bytes();
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(k_tcmc_class<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-      return GMP_ERR_CUDA;
-    attr = true;
-  }
+  if (ensure_max_smem(k_tcmc_class<C>, smem) != cudaSuccess) return GMP_ERR_CUDA;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -435,12 +430,7 @@ template <int C>
 inline gmp_status_t tc2_launch_t(TcTables& t, const WorkItem* it, int64_t n, const PairDesc* pd, const CTileDesc* ct,
                                  uint8_t* ws, int nb, double alpha, cudaStream_t s) {
   constexpr int smem = tc2_smem_bytes();
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(k_tc2_class<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-      return GMP_ERR_CUDA;
-    attr = true;
-  }
+  if (ensure_max_smem(k_tc2_class<C>, smem) != cudaSuccess) return GMP_ERR_CUDA;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
