@@ -242,8 +242,10 @@ struct GridComms {
   cudaStream_t comm_stream;
 };
 static std::vector<GridComms> g_grid_comms;
+static std::mutex g_grid_mu;   // plans may be built from several host threads
 
 static gmp_status_t grid_comms(ncclComm_t world, int P, int Q, int p, int q, GridComms* out) {
+  std::lock_guard<std::mutex> lk(g_grid_mu);
   for (auto& g : g_grid_comms)
     if (g.world == world && g.P == P && g.Q == Q) { *out = g; return GMP_OK; }
   GridComms g{world, P, Q, nullptr, nullptr, nullptr};
@@ -1272,6 +1274,7 @@ extern "C" gmp_status_t gemm_mp_nccl_comm_create(const void* id128, int nranks, 
 }
 
 extern "C" gmp_status_t gemm_mp_nccl_comm_destroy(void* comm) {
+  std::lock_guard<std::mutex> lk(g_grid_mu);
   for (size_t k = 0; k < g_grid_comms.size();) {
     GridComms& g = g_grid_comms[k];
     if (g.world == (ncclComm_t)comm) {
