@@ -420,7 +420,16 @@ def main():
     achieved = flops_local[dom] / (class_ms[dom] * 1e-3) / 1e12 if class_ms[dom] > 0 else 0.0
     dom_peak = cpk[dom]
     # precision-mix roofline: sum_c F_c / (G * Peak_c) vs the step time
-    t_roof_ms = sum(st["flops"][c] / (G * cpk[c] * 1e12) for c in range(NCLS)) * 1e3
+    t_comp_ms = sum(st["flops"][c] / (G * cpk[c] * 1e12) for c in range(NCLS)) * 1e3
+    # T_roof = max(sum_c F_c / (G Peak_c), max_rank B_recv / BW_link);
+    # BW_link = the NVLink 5 datasheet 900 GB/s per direction (not measured here)
+    recv_max = st["recv_bytes_local"]
+    if G > 1:
+        rb = torch.tensor([float(st["recv_bytes_local"])], dtype=torch.float64, device=dev)
+        dist.all_reduce(rb, op=dist.ReduceOp.MAX)
+        recv_max = int(rb.item())
+    t_link_ms = recv_max / 900e9 * 1e3
+    t_roof_ms = max(t_comp_ms, t_link_ms)
     exec_ms = statistics.median(ph[2] for ph in phase)
     # DRAM traffic per launch of the dominant kernel from the committed ncu capture
     traffic = None
@@ -459,7 +468,9 @@ def main():
             "phases_ms": {"plan": statistics.median(ph[0] for ph in phase),
                           "convert": statistics.median(ph[1] for ph in phase), "execute": exec_ms},
             "execute_tflops": w.flops / (exec_ms * 1e-3) / 1e12,
-            "precision_mix_roofline": {"t_roof_ms": t_roof_ms, "frac_of_step": t_roof_ms / ms_step,
+            "precision_mix_roofline": {"t_roof_ms": t_roof_ms, "t_compute_ms": t_comp_ms, "t_link_ms": t_link_ms,
+                                       "link_gbs": 900.0, "recv_bytes_max_rank": recv_max,
+                                       "frac_of_step": t_roof_ms / ms_step,
                                        "frac_of_execute": t_roof_ms / exec_ms,
                                        "class_peaks_tflops": {gmp_class_name(c): round(cpk[c], 1) for c in range(NCLS)},
                                        "peak_source": peak_src + " " + fig_name},
