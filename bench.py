@@ -449,7 +449,10 @@ def main():
     # ---- e2e: host (pinned) buffers, copies inside the timed region ----
     e2e = None
     if not a.no_e2e and a.e2e_steps > 0:
-        e2e = run_e2e(a, A, Bm, C, Cout, lr, lc, G, dev, stream, desc, comm, w)
+        try:
+            e2e = run_e2e(a, A, Bm, C, Cout, lr, lc, G, dev, stream, desc, comm, w)
+        except Exception as ex:  # the device-timed line must still be printed
+            e2e = {"error": f"{type(ex).__name__}: {str(ex)[:200]}"}
 
 
     if rank == 0:
@@ -496,7 +499,10 @@ def main():
         }
         if G == 1 and not a.no_cpu_baseline:
             mix = [st["pairs"][c] for c in range(NCLS)]
-            out["cpu_baseline"] = cpu_baseline(w, mix)
+            try:
+                out["cpu_baseline"] = cpu_baseline(w, mix)
+            except Exception as ex:
+                out["cpu_baseline"] = {"error": f"{type(ex).__name__}: {str(ex)[:200]}", "kind": "oracle"}
         print(json.dumps(out), flush=True)
     if comm is not None:
         dist.barrier()
