@@ -186,6 +186,8 @@ struct gmp_plan_s {
   std::vector<cudaEvent_t> step_ev;
   cudaEvent_t packed_ev = nullptr;   // convert: local stored tiles (and sender shadows) are packed
   bool step0_issued = false;         // convert pre-issued SUMMA step 0 (first execute skips it)
+  bool panels_valid = false;         // every SUMMA step has been issued since the last convert: the
+                                     // receive slots (and their shadows / splits) stay valid
   // global maps (identical on every rank)
   std::vector<uint8_t> codeA, codeB, codeC;
   std::vector<int16_t> sA5, sB5, sCin, sCout;
@@ -1035,6 +1037,7 @@ extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_byte
   // multi-GPU: SUMMA step 0 starts as soon as this rank's panel tiles are packed,
   // overlapping the rest of convert (splits, digit slices) and the accumulator init
   pl->step0_issued = false;
+  pl->panels_valid = false;
   if (pl->P * pl->Q > 1 && pl->st.steps > 0) {
     if (!pl->packed_ev) GMP_CUDA(cudaEventCreateWithFlags(&pl->packed_ev, cudaEventDisableTiming));
     GMP_CUDA(cudaEventRecord(pl->packed_ev, stream));
@@ -1083,7 +1086,7 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
   const int steps = pl->st.steps;
   const bool multi = pl->P * pl->Q > 1;
   cudaEvent_t ready = nullptr;
-  if (multi) {
+  if (multi && !pl->panels_valid) {
     int s0 = 0;
     if (pl->step0_issued) {
       // first execute after convert: step 0 is already in flight (issued by convert
@@ -1091,13 +1094,16 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
       s0 = 1;
       pl->step0_issued = false;
     } else {
-      // repeated execute: the comm stream starts after everything queued on
-      // `stream` (the previous execute still reads the receive slots)
+      // the comm stream starts after everything queued on `stream`
       GMP_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
       GMP_CUDA(cudaEventRecord(ready, stream));
       GMP_CUDA(cudaStreamWaitEvent(pl->comm_stream, ready, 0));
     }
     for (int s = s0; s < steps; ++s) GMP_TRY(issue_comm_step(pl, ws, s));
+    // A and B payloads are fixed after convert and every remote tile owns its
+    // receive slot, so a repeated execute reuses the received panels (no SUMMA
+    // traffic); the step events below are the ones of this issuance
+    pl->panels_valid = true;
   }
   size_t li = 0;
   for (int s = 0; s < steps; ++s) {
