@@ -43,6 +43,9 @@ def _cases():
                                             class_mask=0b11111, seed=45)),
         ("mcast_nb512", gmp_inputs.small_workload(1024, 1536, 1536, 512, 1e-2, mode="random", E=24, beta=0.75,
                                                   class_mask=0b11111, seed=45), B.GMP_FLAG_TC_MCAST),
+        ("pairs_e5m2_nb512", gmp_inputs.small_workload(1024, 1024, 1536, 512, 5e-2, mode="random", E=32,
+                                                       beta=0.0, class_mask=0b111111, seed=48),
+         B.GMP_FLAG_TC_PAIR),
     ]
 
 
