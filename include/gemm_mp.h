@@ -90,7 +90,8 @@ typedef struct {
   int32_t nb;          /* tile edge; multiple of 128 dividing M, N, K (PAPER.md:179 uses 1024/2048) */
   double tol;          /* accuracy tolerance: ||C - C_fp64||_F <= tol (|a| ||A|| ||B|| + |b| ||C||) */
   double alpha, beta;  /* GEMM scalars; beta == 0 means C is not read (BLAS convention)          */
-  uint32_t class_mask; /* bit c enables class c (gmp_class_t); FP64 always on; E4M3/E5M2 opt-in   */
+  uint32_t class_mask; /* bit c enables class c (gmp_class_t); FP64 always on; E4M3/E5M2 opt-in;
+                          bits above 5 are ignored                                           */
   uint32_t flags;      /* GMP_FLAG_*                                                           */
   int32_t P, Q, rank;  /* process grid and this rank (= p*Q + q); 1, 1, 0 on one GPU            */
   /* optional explicit per-tile codes (host, row-major global tile grids: mt x kt, kt x nt,
