@@ -208,3 +208,28 @@ def test_every_pair_class_contributes(cls):
     assert err <= 4 * u + 128 * 2.0 ** -24 + 1e-15, err
     if cls >= FP16:
         assert err > 1e-2 * u   # the class's rounding is visible: the class path really ran
+
+
+@pytest.mark.parametrize("k,mask", [(1, 0b000011), (2, 0b000111), (3, 0b001111), (4, 0b011111), (5, 0b111111)])
+def test_c_map_closed_form_equal_tiles(k, mask):
+    """O7 on equal constant tiles (mt = nt = kt = 4, beta = 0): R_i = 2a, Q_j = 2b, so
+    n_hat = 4ab for every C tile while N_hat = 16ab and NT_C = 4 -- the C tile takes
+    class k iff d_k = u_k + sqrt(kt) u32 + nb eta_k / Omega'_k <= tol / 2.  Just above
+    the threshold of the lowest enabled class the map is that class; just below, the
+    next class up (FP64 below FP32's)."""
+    nb = 32
+    u = [2.0 ** -53, 2.0 ** -24, 2.0 ** -11, 2.0 ** -8, 2.0 ** -4, 2.0 ** -3][k]
+    eta = [0, 2.0 ** -149, 2.0 ** -24, 2.0 ** -133, 2.0 ** -9, 2.0 ** -16][k]
+    omega = [0, 1.0, 65504.0, 1.0, 448.0, 57344.0][k]
+    dk = u + 2.0 * 2.0 ** -24 + nb * eta / omega
+    A = np.full((4 * nb, 4 * nb), 0.75)
+    Bm = np.full((4 * nb, 4 * nb), -1.25)
+    # A/B maps forced to FP64 so only the C criterion is exercised
+    amap = np.zeros((4, 4), np.uint8)
+    for tol, want_k in [(2 * dk * (1 + 1e-6), True), (2 * dk * (1 - 1e-6), False)]:
+        o = oracle.gemm_mp(A, Bm, None, nb, tol, 1.0, 0.0, mask, a_map=amap, b_map=amap, ctiles=[])
+        assert o["rc"] == 0
+        if want_k:
+            assert (o["ccode"] == k).all(), (k, tol, o["ccode"])
+        else:
+            assert (o["ccode"] < k).all(), (k, tol, o["ccode"])
