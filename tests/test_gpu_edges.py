@@ -159,3 +159,24 @@ def test_single_tile(nb, mask, tol):
     assert np.array_equal(outs, o["C"])
     ok, rel = c_parity(out, o["C"], o["ccode"], o["cscale"], nb, nb, mask == 1)
     assert ok, rel
+
+
+@pytest.mark.parametrize("k,mask", [(1, 0b000011), (2, 0b000111), (3, 0b001111), (4, 0b011111), (5, 0b111111)])
+def test_c_map_at_the_threshold_matches_oracle(k, mask):
+    """Equal constant tiles put every C tile exactly at its class threshold
+    (d_k = tol / 2, tests/test_oracle_gemm.py::test_c_map_closed_form_equal_tiles);
+    at the threshold and 1e-6 either side the GPU's C map is the oracle's, bit for bit
+    (same evaluation order of the criterion)."""
+    nb = 128
+    u = [2.0 ** -53, 2.0 ** -24, 2.0 ** -11, 2.0 ** -8, 2.0 ** -4, 2.0 ** -3][k]
+    eta = [0, 2.0 ** -149, 2.0 ** -24, 2.0 ** -133, 2.0 ** -9, 2.0 ** -16][k]
+    omega = [0, 1.0, 65504.0, 1.0, 448.0, 57344.0][k]
+    dk = u + 2.0 * 2.0 ** -24 + nb * eta / omega
+    A = np.full((4 * nb, 4 * nb), 0.75)
+    Bm = np.full((4 * nb, 4 * nb), -1.25)
+    amap = np.zeros((4, 4), np.uint8)
+    for tol in (2 * dk * (1 + 1e-6), 2 * dk, 2 * dk * (1 - 1e-6)):
+        o = run_oracle(A, Bm, None, nb, tol, 1.0, 0.0, mask, maps=(amap, amap, None), ctiles=[])
+        g, _ = run_gpu(A, Bm, None, nb, tol, 1.0, 0.0, mask, maps=(amap, amap, None))
+        assert np.array_equal(g.maps()["ccode"], o["ccode"]), (k, tol)
+        g.close()
