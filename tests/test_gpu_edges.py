@@ -180,3 +180,22 @@ def test_c_map_at_the_threshold_matches_oracle(k, mask):
         g, _ = run_gpu(A, Bm, None, nb, tol, 1.0, 0.0, mask, maps=(amap, amap, None))
         assert np.array_equal(g.maps()["ccode"], o["ccode"]), (k, tol)
         g.close()
+
+
+@pytest.mark.parametrize("k,mask", [(1, 0b000011), (2, 0b000111), (3, 0b001111), (4, 0b011111), (5, 0b111111)])
+def test_ab_map_at_the_threshold_matches_oracle(k, mask):
+    """Equal constant tiles: ||X_ij|| / ||X|| = 1/NT, so an A/B tile takes class k iff
+    delta_k (+ its underflow term) <= tol / 4.  At tol = 4 delta_k and 1e-6 either
+    side the GPU's A and B maps are the oracle's, bit for bit."""
+    nb = 128
+    u = [2.0 ** -53, 2.0 ** -24, 2.0 ** -11, 2.0 ** -8, 2.0 ** -4, 2.0 ** -3][k]
+    dk = u + np.sqrt(nb) * 2.0 ** -24
+    A = np.full((3 * nb, 4 * nb), 0.75)
+    Bm = np.full((4 * nb, 2 * nb), -1.25)
+    for tol in (4 * dk * (1 + 1e-6), 4 * dk, 4 * dk * (1 - 1e-6)):
+        o = run_oracle(A, Bm, None, nb, tol, 1.0, 0.0, mask, ctiles=[])
+        g, _ = run_gpu(A, Bm, None, nb, tol, 1.0, 0.0, mask)
+        m = g.maps()
+        assert np.array_equal(m["acode"], o["acode"]) and np.array_equal(m["bcode"], o["bcode"]), (k, tol)
+        assert np.array_equal(m["ccode"], o["ccode"]), (k, tol)
+        g.close()
