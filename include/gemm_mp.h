@@ -76,6 +76,15 @@ typedef enum {
 #define GMP_FLAG_TC_MCAST 64u /* same launches as GMP_FLAG_TC_PAIR, but each SM keeps its own 1-SM MMA
                                  (M = 128) and only the B box is split and multicast across a 2-CTA
                                  cluster (a third fewer L2->SM bytes, no cross-SM operand reads)     */
+#define GMP_FLAG_TC_FUSED 128u /* opt-in: when the FP32 class runs on the tensor pipe and every tensor
+                                 class of a SUMMA step runs 128 x 128 sub-tiles (binary64 W, or nb
+                                 not a multiple of 256), the step's tensor classes share one launch
+                                 (k_tc_fused): per C sub-tile their pairs run in the fold order
+                                 (class 5 .. 1, l increasing) with one W read and write instead of
+                                 one per class; C is bit-identical.  Measured 3-10 % slower than the
+                                 per-class launches on cfg2 (the 16-bit pairs at 128 x 128 are bound
+                                 by L2->SM bandwidth, not by W traffic).  stats.class_ms
+                                 splits the launch's time by the classes' MMA issue cycles.       */
 #define GMP_FLAG_SENDER_SIDE 16u /* SURVEY 8(f) NEXT-2, hybrid conversion (PAPER.md:148 defers it): a
                                  SUMMA panel tile whose receivers in its process row (A) / column (B)
                                  together need a set of classes S whose payloads are smaller than the

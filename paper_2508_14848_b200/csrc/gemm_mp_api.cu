@@ -24,6 +24,7 @@
 #include "gmp_tc.cuh"
 #include "gmp_ozaki.cuh"
 #include "gmp_tc2.cuh"
+#include "gmp_tcf.cuh"
 
 using namespace gmp;
 
@@ -161,9 +162,13 @@ struct Launch {
   int step, cls, kind;  // kind 0: SIMT/DMMA kernel, 1: tcgen05, 2: FP64 DFMA cross-check, 3: FP32 on tcgen05
                         // (BF16x9), 4: FP64 on the INT8 tensor pipe (Ozaki digits), 5: tcgen05 on an SM
                         // pair (cta_group::2, 256 x 256 sub-tiles), 6: 1-SM tcgen05 with B multicast
-                        // across a 2-CTA cluster
+                        // across a 2-CTA cluster, 7: every tensor class of the step in one
+                        // launch (k_tc_fused; cls = 1, the classes are in `present`)
   int64_t ibeg, icount;
   int bn;  // N of the class kernel's CTA tile
+  unsigned present = 0;  // kind 7: bit c set for each class c with pairs in the launch
+  double share[GMP_NCLASS] = {};  // kind 7: estimated share of the launch time per class
+                                  // (MMA issue cycles; GMP_FLAG_TIMING attribution)
 };
 
 struct Bcast {           // one SUMMA broadcast of a panel tile payload in a step
@@ -439,7 +444,6 @@ static void build_tables(gmp_plan_s* pl) {
           if (std::max(pl->codeA[i * kt + l], pl->codeB[l * nt + j]) == c) ++cnt;
         if (!cnt) continue;
         n_pairs += cnt;
-        const bool tc = kTcAvailable && (c >= 2) && !(d.flags & GMP_FLAG_SIMT_ONLY);
         n_items += 1;
       }
   const int64_t n_pack = (int64_t)pl->locA.size() + (int64_t)pl->locB.size() + (hasC ? nCl : 0);
@@ -629,38 +633,102 @@ static void build_tables(gmp_plan_s* pl) {
   }
 
   // ---- pairs and work items ----
+  // pairs of class c for local C tile k in SUMMA step s, l increasing (fold order O9)
+  auto add_pairs = [&](int s, int c, int64_t k) {
+    const int64_t g = pl->locC[k], i = g / nt, j = g % nt;
+    for (int64_t l = (int64_t)s * GMP_STEP_DEPTH; l < std::min<int64_t>(kt, (int64_t)(s + 1) * GMP_STEP_DEPTH); ++l) {
+      const int ca = pl->codeA[i * kt + l], cb = pl->codeB[l * nt + j];
+      if (std::max(ca, cb) != c) continue;
+      PairDesc pd{};
+      pd.a_off = arena(c, pl->slotA5[(i * kt + l) * NC + c]);
+      pd.b_off = arena(c, pl->slotB5[(l * nt + j) * NC + c]);
+      pd.fexp = -(pl->sA5[(i * kt + l) * NC + c] + pl->sB5[(l * nt + j) * NC + c]);
+      pd.l = (int32_t)l;
+      pd.a_slot = pl->slotA5[(i * kt + l) * NC + c];
+      pd.b_slot = pl->slotB5[(l * nt + j) * NC + c];
+      if (c == 0 && pl->fp64_tc) {   // operands are the int8 digit planes
+        pd.a_slot = pl->sliceA[i * kt + l];
+        pd.b_slot = pl->sliceB[l * nt + j];
+        pd.a_off = pl->arena_off[GMP_AR_SLICE] + (int64_t)pd.a_slot * pl->slot_bytes[GMP_AR_SLICE];
+        pd.b_off = pl->arena_off[GMP_AR_SLICE] + (int64_t)pd.b_slot * pl->slot_bytes[GMP_AR_SLICE];
+      }
+      if (c == 1 && pl->fp32_tc) {   // operands are the BF16x3 splits
+        pd.a_slot = pl->splitA[i * kt + l];
+        pd.b_slot = pl->splitB[l * nt + j];
+        pd.a_off = pl->arena_off[GMP_AR_SPLIT] + (int64_t)pd.a_slot * pl->slot_bytes[GMP_AR_SPLIT];
+        pd.b_off = pl->arena_off[GMP_AR_SPLIT] + (int64_t)pd.b_slot * pl->slot_bytes[GMP_AR_SPLIT];
+      }
+      pd.cls = c;
+      pl->pairs.push_back(pd);
+    }
+  };
+  const bool tc_on = kTcAvailable && !(d.flags & GMP_FLAG_SIMT_ONLY);
   for (int s = 0; s < steps; ++s) {
+    // GMP_FLAG_TC_FUSED: one launch for every tensor-core class of the step
+    // (k_tc_fused, gmp_tcf.cuh) when the FP32 class runs on the tensor pipe, at
+    // least two tensor classes have pairs, and each of them would run at BN = 128
+    // anyway (binary64 W in the launch, or nb not a multiple of 256): W is then
+    // read and written once per step for all of them instead of once per class.
+    bool fuse = tc_on && pl->fp32_tc && (d.flags & GMP_FLAG_TC_FUSED);
+    unsigned present = 0;
+    if (fuse) {
+      bool w64c[NC] = {};
+      for (int64_t k = 0; k < nCl; ++k) {
+        const int64_t g = pl->locC[k], i = g / nt, j = g % nt;
+        for (int64_t l = (int64_t)s * GMP_STEP_DEPTH; l < std::min<int64_t>(kt, (int64_t)(s + 1) * GMP_STEP_DEPTH); ++l) {
+          const int c = std::max(pl->codeA[i * kt + l], pl->codeB[l * nt + j]);
+          present |= 1u << c;
+          w64c[c] = w64c[c] || pl->ctd[k].code == 0;
+        }
+      }
+      present &= 0x3Eu;   // classes 1..5
+      int ncls = 0;
+      for (int c = 1; c < NC; ++c) {
+        if (!(present >> c & 1)) continue;
+        ++ncls;
+        if (c >= 2 && !w64c[c] && tc_bn((int)nb) != 128) fuse = false;
+      }
+      fuse = fuse && ncls >= 2;
+    }
+    if (fuse) {
+      const int64_t ibeg = (int64_t)pl->items.size();
+      std::vector<WorkItem> its;
+      std::vector<int64_t> cost;
+      for (int64_t k = 0; k < nCl; ++k) {
+        const int64_t pbeg = (int64_t)pl->pairs.size();
+        for (int c = NC - 1; c >= 1; --c) add_pairs(s, c, k);
+        const int64_t pcnt = (int64_t)pl->pairs.size() - pbeg;
+        if (!pcnt) continue;
+        int64_t w = 0;   // MMA issue cycles per K: BF16x9 36, 16-bit 4, 8-bit 1 (half the blocks, twice the rate)
+        for (int64_t q = pbeg; q < pbeg + pcnt; ++q) w += pl->pairs[q].cls == 1 ? 36 : pl->pairs[q].cls >= 4 ? 1 : 4;
+        its.push_back(WorkItem{(int32_t)k, 0, 0, (int32_t)pbeg, (int32_t)pcnt, 0});
+        cost.push_back(w);
+      }
+      std::vector<size_t> ord(its.size());
+      for (size_t q = 0; q < ord.size(); ++q) ord[q] = q;
+      std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return cost[a] > cost[b]; });
+      for (size_t q : ord) pl->items.push_back(its[q]);
+      Launch L{s, 1, 7, ibeg, (int64_t)its.size() * subtiles_per_item((int)nb, TCF_BN), TCF_BN};
+      L.present = present;
+      double tot = 0.0;
+      for (const WorkItem& wi : its)
+        for (int64_t q = wi.pbeg; q < wi.pbeg + wi.pcnt; ++q) {
+          const int c = pl->pairs[q].cls;
+          const double w = c == 1 ? 36.0 : c >= 4 ? 1.0 : 4.0;
+          L.share[c] += w;
+          tot += w;
+        }
+      for (int c = 0; c < NC; ++c) L.share[c] = tot > 0 ? L.share[c] / tot : 0.0;
+      pl->launches.push_back(L);
+    }
     for (int c = NC - 1; c >= 0; --c) {
-      const bool tc = kTcAvailable && (c >= 2) && !(d.flags & GMP_FLAG_SIMT_ONLY);
+      if (fuse && c >= 1) continue;
+      const bool tc = tc_on && (c >= 2);
       const int64_t ibeg = (int64_t)pl->items.size();
       std::vector<WorkItem> its;
       for (int64_t k = 0; k < nCl; ++k) {
-        const int64_t g = pl->locC[k], i = g / nt, j = g % nt;
         const int64_t pbeg = (int64_t)pl->pairs.size();
-        for (int64_t l = (int64_t)s * GMP_STEP_DEPTH; l < std::min<int64_t>(kt, (int64_t)(s + 1) * GMP_STEP_DEPTH); ++l) {
-          const int ca = pl->codeA[i * kt + l], cb = pl->codeB[l * nt + j];
-          if (std::max(ca, cb) != c) continue;
-          PairDesc pd{};
-          pd.a_off = arena(c, pl->slotA5[(i * kt + l) * NC + c]);
-          pd.b_off = arena(c, pl->slotB5[(l * nt + j) * NC + c]);
-          pd.fexp = -(pl->sA5[(i * kt + l) * NC + c] + pl->sB5[(l * nt + j) * NC + c]);
-          pd.l = (int32_t)l;
-          pd.a_slot = pl->slotA5[(i * kt + l) * NC + c];
-          pd.b_slot = pl->slotB5[(l * nt + j) * NC + c];
-          if (c == 0 && pl->fp64_tc) {   // operands are the int8 digit planes
-            pd.a_slot = pl->sliceA[i * kt + l];
-            pd.b_slot = pl->sliceB[l * nt + j];
-            pd.a_off = pl->arena_off[GMP_AR_SLICE] + (int64_t)pd.a_slot * pl->slot_bytes[GMP_AR_SLICE];
-            pd.b_off = pl->arena_off[GMP_AR_SLICE] + (int64_t)pd.b_slot * pl->slot_bytes[GMP_AR_SLICE];
-          }
-          if (c == 1 && pl->fp32_tc) {   // operands are the BF16x3 splits
-            pd.a_slot = pl->splitA[i * kt + l];
-            pd.b_slot = pl->splitB[l * nt + j];
-            pd.a_off = pl->arena_off[GMP_AR_SPLIT] + (int64_t)pd.a_slot * pl->slot_bytes[GMP_AR_SPLIT];
-            pd.b_off = pl->arena_off[GMP_AR_SPLIT] + (int64_t)pd.b_slot * pl->slot_bytes[GMP_AR_SPLIT];
-          }
-          pl->pairs.push_back(pd);
-        }
+        add_pairs(s, c, k);
         const int64_t pcnt = (int64_t)pl->pairs.size() - pbeg;
         if (!pcnt) continue;
         its.push_back(WorkItem{(int32_t)k, 0, 0, (int32_t)pbeg, (int32_t)pcnt, 0});
@@ -720,7 +788,13 @@ static void build_tables(gmp_plan_s* pl) {
   st.launches_plan = 2;
   st.launches_convert = (pl->pack.empty() ? 0 : 1) + nsh(pl->shadow_local) + (pl->split_local.empty() ? 0 : 1) +
                         (pl->slice_local.empty() ? 0 : 1);
-  for (const Launch& L : pl->launches) st.class_launches[L.cls]++;
+  for (const Launch& L : pl->launches) {
+    if (L.kind == 7) {
+      for (int c = 0; c < NC; ++c) st.class_launches[c] += (int32_t)(L.present >> c & 1);
+    } else {
+      st.class_launches[L.cls]++;
+    }
+  }
 }
 
 // 2D block-cyclic ownership: tile (i, j) of a grid lives on rank (i mod P, j mod Q)
@@ -1120,6 +1194,8 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
         GMP_TRY(tc2_launch(pl->tc, L.cls, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, stream));
       } else if (L.kind == 6) {
         GMP_TRY(tcmc_launch(pl->tc, L.cls, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, stream));
+      } else if (L.kind == 7) {
+        GMP_TRY(tcf_launch(pl->tc, L.present, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, stream));
       } else if (L.kind == 1 || L.kind == 3) {
         GMP_TRY(tc_launch(pl->tc, L.kind == 3 ? TC_SPLIT : L.cls, L.bn, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha,
                           stream));
@@ -1254,7 +1330,12 @@ extern "C" gmp_status_t gemm_mp_get_stats(gmp_plan_t pl, gmp_stats_t* out) {
       float ms = 0.f;
       GMP_CUDA(cudaEventSynchronize(pl->launch_ev[2 * li + 1]));
       GMP_CUDA(cudaEventElapsedTime(&ms, pl->launch_ev[2 * li], pl->launch_ev[2 * li + 1]));
-      pl->st.class_ms[pl->launches[li].cls] += ms;
+      const Launch& L = pl->launches[li];
+      if (L.kind == 7) {
+        for (int c = 0; c < NC; ++c) pl->st.class_ms[c] += ms * L.share[c];
+      } else {
+        pl->st.class_ms[L.cls] += ms;
+      }
     }
   }
   *out = pl->st;

@@ -51,6 +51,8 @@ struct PairDesc {
   int32_t fexp;          // -(eA + eB): fold factor alpha * 2^fexp
   int32_t l;             // global reduction tile index (bookkeeping)
   int32_t a_slot, b_slot;  // slot indices in the class arena (TMA row = slot * nb)
+  int32_t cls;             // pair class (k_tc_fused: selects the operand arena and the MMA kind)
+  int32_t pad;
 };
 
 template <int C> struct SimtCfg {

@@ -111,6 +111,121 @@ __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t* r) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// Epilogue warps 2..9 of the 1-SM tcgen05 kernels (k_tc_class, k_tc_fused): per
+// pair, read the FP32 product from TMEM and fold it into W (O9).
+template <int BN>
+__device__ __forceinline__ void tc_epilogue(const WorkItem* __restrict__ items, int64_t nitems,
+                                            const PairDesc* __restrict__ pairs, const CTileDesc* __restrict__ ctiles,
+                                            uint8_t* __restrict__ ws, int nb, double alpha, uint32_t tmem_base,
+                                            uint64_t* tfull, uint64_t* tempty, int warp, int lane) {
+  // epilogue: 8 warps; warp w reads TMEM lanes 32*(w%4)..+31 (= tile rows) and
+  // half (w-2)/4 of the BN columns.  binary32 W: the W row segment lives in
+  // registers for the whole item (one read + one write per item instead of
+  // per pair); binary64 W: read-modify-write per pair.
+  constexpr int HC = BN / 2;                  // columns per epilogue thread
+  const int quarter = warp & 3, half = (warp - 2) >> 2;
+  const int rloc = quarter * 32 + lane;
+  int acc = 0;
+  uint32_t acc_phase = 0;
+  for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const WorkItem w = expand_item(items, it, nb, BN);
+    const CTileDesc ct = ctiles[w.ctile];
+    const int64_t rowoff = (int64_t)(w.m0 + rloc) * nb + w.n0 + half * HC;
+    if (ct.code != 0) {
+      float* wrow = reinterpret_cast<float*>(ws + ct.w_off) + rowoff;
+      float accr[HC];
+#pragma unroll
+      for (int v = 0; v < HC / 4; ++v) {
+        float4 x = reinterpret_cast<const float4*>(wrow)[v];
+        accr[4 * v] = x.x; accr[4 * v + 1] = x.y; accr[4 * v + 2] = x.z; accr[4 * v + 3] = x.w;
+      }
+      for (int pi = 0; pi < w.pcnt; ++pi) {
+        const PairDesc pd = pairs[w.pbeg + pi];
+        const float f32 = __double2float_rn(ldexp_fast(alpha, pd.fexp));
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + half * HC);
+#pragma unroll
+        for (int ch = 0; ch < HC / 16; ++ch) {
+          uint32_t r[16];
+          tmem_ld16_nowait(tbase + ch * 16, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int v = 0; v < 16; ++v) accr[ch * 16 + v] = __fmaf_rn(f32, __uint_as_float(r[v]), accr[ch * 16 + v]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+#pragma unroll
+      for (int v = 0; v < HC / 4; ++v)
+        reinterpret_cast<float4*>(wrow)[v] = make_float4(accr[4 * v], accr[4 * v + 1], accr[4 * v + 2], accr[4 * v + 3]);
+    } else if constexpr (HC <= 64) {
+      // binary64 W, BN <= 128: the W row segment lives in registers for the item
+      double* wrow = reinterpret_cast<double*>(ws + ct.w_off) + rowoff;
+      double accd[HC];
+#pragma unroll
+      for (int v = 0; v < HC / 2; ++v) {
+        const double2 x = reinterpret_cast<const double2*>(wrow)[v];
+        accd[2 * v] = x.x; accd[2 * v + 1] = x.y;
+      }
+      for (int pi = 0; pi < w.pcnt; ++pi) {
+        const PairDesc pd = pairs[w.pbeg + pi];
+        const double f64 = ldexp_fast(alpha, pd.fexp);
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + half * HC);
+#pragma unroll
+        for (int ch = 0; ch < HC / 16; ++ch) {
+          uint32_t r[16];
+          tmem_ld16_nowait(tbase + ch * 16, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int v = 0; v < 16; ++v)
+            accd[ch * 16 + v] = __fma_rn(f64, (double)__uint_as_float(r[v]), accd[ch * 16 + v]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+#pragma unroll
+      for (int v = 0; v < HC / 2; ++v)
+        reinterpret_cast<double2*>(wrow)[v] = make_double2(accd[2 * v], accd[2 * v + 1]);
+    } else {
+      // binary64 W with BN = 256: read-modify-write per pair (the host prefers
+      // BN = 128 for launches that hold binary64 accumulators)
+      double* wrow = reinterpret_cast<double*>(ws + ct.w_off) + rowoff;
+      for (int pi = 0; pi < w.pcnt; ++pi) {
+        const PairDesc pd = pairs[w.pbeg + pi];
+        const double f64 = ldexp_fast(alpha, pd.fexp);
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + half * HC);
+#pragma unroll 1
+        for (int ch = 0; ch < HC / 16; ++ch) {
+          uint32_t r[16];
+          tmem_ld16_nowait(tbase + ch * 16, r);
+          tmem_wait_ld();
+          double2* wp = reinterpret_cast<double2*>(wrow + ch * 16);
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            double2 x = wp[v];
+            x.x = __fma_rn(f64, (double)__uint_as_float(r[2 * v]), x.x);
+            x.y = __fma_rn(f64, (double)__uint_as_float(r[2 * v + 1]), x.y);
+            wp[v] = x;
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
@@ -222,112 +337,7 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
       }
     }
   } else {
-    // epilogue: 8 warps; warp w reads TMEM lanes 32*(w%4)..+31 (= tile rows) and
-    // half (w-2)/4 of the BN columns.  binary32 W: the W row segment lives in
-    // registers for the whole item (one read + one write per item instead of
-    // per pair); binary64 W: read-modify-write per pair.
-    constexpr int HC = BN / 2;                  // columns per epilogue thread
-    const int quarter = warp & 3, half = (warp - 2) >> 2;
-    const int rloc = quarter * 32 + lane;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
-      const WorkItem w = expand_item(items, it, nb, BN);
-      const CTileDesc ct = ctiles[w.ctile];
-      const int64_t rowoff = (int64_t)(w.m0 + rloc) * nb + w.n0 + half * HC;
-      if (ct.code != 0) {
-        float* wrow = reinterpret_cast<float*>(ws + ct.w_off) + rowoff;
-        float accr[HC];
-#pragma unroll
-        for (int v = 0; v < HC / 4; ++v) {
-          float4 x = reinterpret_cast<const float4*>(wrow)[v];
-          accr[4 * v] = x.x; accr[4 * v + 1] = x.y; accr[4 * v + 2] = x.z; accr[4 * v + 3] = x.w;
-        }
-        for (int pi = 0; pi < w.pcnt; ++pi) {
-          const PairDesc pd = pairs[w.pbeg + pi];
-          const float f32 = __double2float_rn(ldexp_fast(alpha, pd.fexp));
-          mbar_wait(&tfull[acc], acc_phase);
-          tc_fence_after();
-          const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + half * HC);
-#pragma unroll
-          for (int ch = 0; ch < HC / 16; ++ch) {
-            uint32_t r[16];
-            tmem_ld16_nowait(tbase + ch * 16, r);
-            tmem_wait_ld();
-#pragma unroll
-            for (int v = 0; v < 16; ++v) accr[ch * 16 + v] = __fmaf_rn(f32, __uint_as_float(r[v]), accr[ch * 16 + v]);
-          }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
-          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-        }
-#pragma unroll
-        for (int v = 0; v < HC / 4; ++v)
-          reinterpret_cast<float4*>(wrow)[v] = make_float4(accr[4 * v], accr[4 * v + 1], accr[4 * v + 2], accr[4 * v + 3]);
-      } else if constexpr (HC <= 64) {
-        // binary64 W, BN <= 128: the W row segment lives in registers for the item
-        double* wrow = reinterpret_cast<double*>(ws + ct.w_off) + rowoff;
-        double accd[HC];
-#pragma unroll
-        for (int v = 0; v < HC / 2; ++v) {
-          const double2 x = reinterpret_cast<const double2*>(wrow)[v];
-          accd[2 * v] = x.x; accd[2 * v + 1] = x.y;
-        }
-        for (int pi = 0; pi < w.pcnt; ++pi) {
-          const PairDesc pd = pairs[w.pbeg + pi];
-          const double f64 = ldexp_fast(alpha, pd.fexp);
-          mbar_wait(&tfull[acc], acc_phase);
-          tc_fence_after();
-          const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + half * HC);
-#pragma unroll
-          for (int ch = 0; ch < HC / 16; ++ch) {
-            uint32_t r[16];
-            tmem_ld16_nowait(tbase + ch * 16, r);
-            tmem_wait_ld();
-#pragma unroll
-            for (int v = 0; v < 16; ++v)
-              accd[ch * 16 + v] = __fma_rn(f64, (double)__uint_as_float(r[v]), accd[ch * 16 + v]);
-          }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
-          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-        }
-#pragma unroll
-        for (int v = 0; v < HC / 2; ++v)
-          reinterpret_cast<double2*>(wrow)[v] = make_double2(accd[2 * v], accd[2 * v + 1]);
-      } else {
-        // binary64 W with BN = 256: read-modify-write per pair (the host prefers
-        // BN = 128 for launches that hold binary64 accumulators)
-        double* wrow = reinterpret_cast<double*>(ws + ct.w_off) + rowoff;
-        for (int pi = 0; pi < w.pcnt; ++pi) {
-          const PairDesc pd = pairs[w.pbeg + pi];
-          const double f64 = ldexp_fast(alpha, pd.fexp);
-          mbar_wait(&tfull[acc], acc_phase);
-          tc_fence_after();
-          const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + half * HC);
-#pragma unroll 1
-          for (int ch = 0; ch < HC / 16; ++ch) {
-            uint32_t r[16];
-            tmem_ld16_nowait(tbase + ch * 16, r);
-            tmem_wait_ld();
-            double2* wp = reinterpret_cast<double2*>(wrow + ch * 16);
-#pragma unroll
-            for (int v = 0; v < 8; ++v) {
-              double2 x = wp[v];
-              x.x = __fma_rn(f64, (double)__uint_as_float(r[2 * v]), x.x);
-              x.y = __fma_rn(f64, (double)__uint_as_float(r[2 * v + 1]), x.y);
-              wp[v] = x;
-            }
-          }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
-          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-        }
-      }
-    }
+    tc_epilogue<BN>(items, nitems, pairs, ctiles, ws, nb, alpha, tmem_base, tfull, tempty, warp, lane);
   }
   tc_fence_before();
   __syncthreads();

@@ -61,7 +61,9 @@ def case(request):
     assert orc["rc"] == 0
     g, (Cg, Cg2) = run_gpu(A, Bm, C, w.nb, w.tol, w.alpha, w.beta, w.class_mask, flags=flags, reps=2)
     gs, (Cs,) = run_gpu(A, Bm, C, w.nb, w.tol, w.alpha, w.beta, w.class_mask, flags=B.GMP_FLAG_SIMT_ONLY)
-    return dict(name=name, w=w, A=A, B=Bm, C=C, orc=orc, g=g, Cg=Cg, Cg2=Cg2, gs=gs, Cs=Cs)
+    gp, (Cp,) = run_gpu(A, Bm, C, w.nb, w.tol, w.alpha, w.beta, w.class_mask,
+                        flags=flags | B.GMP_FLAG_TC_FUSED)
+    return dict(name=name, w=w, A=A, B=Bm, C=C, orc=orc, g=g, Cg=Cg, Cg2=Cg2, gs=gs, Cs=Cs, gp=gp, Cp=Cp)
 
 
 def test_maps_bitwise(case):
@@ -117,6 +119,13 @@ def test_c_parity_product_path(case):
     assert ok, rel
 
 
+def test_fused_launch_equals_per_class_launches(case):
+    """k_tc_fused (GMP_FLAG_TC_FUSED: all tensor classes of a step in one launch) runs the
+    same pairs with the same arithmetic in the same fold order as the default one
+    k_tc_class launch per class: C is bit-identical"""
+    assert np.array_equal(case["Cg"], case["Cp"])
+
+
 def test_c_meets_tolerance(case):
     w = case["w"]
     assert tol_metric(case["Cg"], case["A"], case["B"], case["C"], w.alpha, w.beta) <= w.tol
@@ -148,3 +157,15 @@ def test_mixes_are_mixed():
     g, _ = run_gpu(A, Bm, C, w.nb, w.tol, w.alpha, w.beta, w.class_mask)
     st = g.stats()
     assert st["tiles_a"][0] > 0 and st["tiles_a"][1] > 0 and st["tiles_a"][2] > 0
+
+
+def test_fused_launch_is_used():
+    """cfg1 (nb = 128: every tensor class runs 128 x 128 sub-tiles) has FP32, FP16 and BF16
+    pairs in each step, so GMP_FLAG_TC_FUSED launches fewer kernels than the per-class plan"""
+    w = gmp_inputs.workload(1)
+    A, Bm, C = w.matrices()
+    g, _ = run_gpu(A, Bm, C, w.nb, w.tol, w.alpha, w.beta, w.class_mask, flags=B.GMP_FLAG_TC_FUSED)
+    gp, _ = run_gpu(A, Bm, C, w.nb, w.tol, w.alpha, w.beta, w.class_mask)
+    st, sp = g.stats(), gp.stats()
+    assert sum(1 for c in range(1, 6) if st["pairs"][c]) >= 2
+    assert st["launches_execute"] < sp["launches_execute"]
