@@ -263,7 +263,7 @@ k_mn(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
   constexpr int CHUNKS = BK * (ACH + BCH), CPT = CHUNKS / 256;
   constexpr int STAGE = BK * (128 + BN) * ES;            // bytes
   static_assert(CHUNKS % 256 == 0, "loader");
-  extern __shared__ __align__(16) uint8_t sm[];
+  extern __shared__ __align__(128) uint8_t sm[];
   const WorkItem it = expand_item(items, blockIdx.x, nb, BN);
   const CTileDesc ct = ctiles[it.ctile];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
