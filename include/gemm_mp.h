@@ -207,7 +207,11 @@ gmp_status_t gemm_mp_plan_host(const gmp_desc_t *desc, const uint8_t *acode, con
 gmp_status_t gemm_mp_get_schedule(gmp_plan_t plan, int32_t step, int64_t *entries, int64_t cap,
                                   int64_t *n);
 
-/* NCCL bootstrap helpers (the unique id travels over torch.distributed).      */
+/* NCCL bootstrap helpers (the unique id travels over torch.distributed).
+ * The first plan on a world communicator splits it into the SUMMA row and
+ * column communicators (cached); environment variables GMP_NCCL_MAX_CTAS and
+ * GMP_NCCL_CTA_POLICY, when set, go into their ncclConfig_t (maxCTAs,
+ * CTAPolicy).  Default: NCCL's own (profiles/nccl_cta_r01.md).                 */
 gmp_status_t gemm_mp_nccl_unique_id(void *out128);
 gmp_status_t gemm_mp_nccl_comm_create(const void *id128, int nranks, int rank, void **comm);
 gmp_status_t gemm_mp_nccl_comm_destroy(void *comm);

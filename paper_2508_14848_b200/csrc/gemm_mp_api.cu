@@ -256,8 +256,11 @@ static gmp_status_t grid_comms(ncclComm_t world, int P, int Q, int p, int q, Gri
   for (auto& g : g_grid_comms)
     if (g.world == world && g.P == P && g.Q == Q) { *out = g; return GMP_OK; }
   GridComms g{world, P, Q, nullptr, nullptr, nullptr};
-  GMP_NCCL(ncclCommSplit(world, p, q, &g.rowc, nullptr));
-  GMP_NCCL(ncclCommSplit(world, q, p, &g.colc, nullptr));
+  ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+  if (const char* e = getenv("GMP_NCCL_MAX_CTAS")) cfg.maxCTAs = atoi(e);
+  if (const char* e = getenv("GMP_NCCL_CTA_POLICY")) cfg.CTAPolicy = atoi(e);
+  GMP_NCCL(ncclCommSplit(world, p, q, &g.rowc, &cfg));
+  GMP_NCCL(ncclCommSplit(world, q, p, &g.colc, &cfg));
   GMP_CUDA(cudaStreamCreateWithFlags(&g.comm_stream, cudaStreamNonBlocking));
   g_grid_comms.push_back(g);
   *out = g;
