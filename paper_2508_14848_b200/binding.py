@@ -226,6 +226,12 @@ def gemm_mp_plan_host(desc, acode, bcode, ccode, ascale5, bscale5, cin_scale=Non
             np.ascontiguousarray(ccode, np.uint8), np.ascontiguousarray(ascale5, np.int16),
             np.ascontiguousarray(bscale5, np.int16),
             None if cin_scale is None else np.ascontiguousarray(cin_scale, np.int16)]
+    # the library reads NCLS scales per tile and one C_in scale per C tile
+    for codes, sc, name in ((arrs[0], arrs[3], "ascale5"), (arrs[1], arrs[4], "bscale5")):
+        if sc.size != codes.size * NCLS:
+            raise ValueError(f"{name} must hold {NCLS} int16 per tile ({codes.size * NCLS}), got {sc.size}")
+    if arrs[5] is not None and arrs[5].size != arrs[2].size:
+        raise ValueError("cin_scale must hold one int16 per C tile")
     h = ct.c_void_p()
     _check(lib().gemm_mp_plan_host(ct.byref(desc), *[None if a is None else a.ctypes.data for a in arrs],
                                    ct.byref(h)))

@@ -431,11 +431,8 @@ static void build_tables(gmp_plan_s* pl) {
   pl->items.clear();
   pl->launches.clear();
   const int steps = (int)((kt + GMP_STEP_DEPTH - 1) / GMP_STEP_DEPTH);
-  struct Tmp { int64_t ct; int64_t pbeg, pcnt; };
-  // we need arena offsets before pairs: finish the layout first
+  // arena offsets are needed before the pairs: finish the layout first
   int64_t o = 0;
-  const int64_t tables_guess = 0;
-  (void)tables_guess;
   // count items to size tables
   int64_t n_pairs = 0, n_items = 0;
   for (int s = 0; s < steps; ++s)

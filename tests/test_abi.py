@@ -55,7 +55,43 @@ def test_host_plan_rejects_bad_codes():
     import numpy as np
     d = B.make_desc(256, 256, 256, 128, 1e-6)
     bad = np.full((2, 2), 7, np.uint8)
-    z = np.zeros((2, 2, 5), np.int16)
+    z = np.zeros((2, 2, 6), np.int16)
     with pytest.raises(B.GmpError) as e:
         B.gemm_mp_plan_host(d, bad, bad, bad, z, z)
     assert "GMP_ERR_MAP_SHAPE" in str(e.value)
+
+
+def test_host_plan_checks_scale_array_sizes():
+    """the binding refuses scale arrays shorter than NCLS entries per tile (the library
+    would read past them)"""
+    import numpy as np
+    d = B.make_desc(256, 256, 256, 128, 1e-6)
+    c = np.zeros((2, 2), np.uint8)
+    with pytest.raises(ValueError):
+        B.gemm_mp_plan_host(d, c, c, c, np.zeros((2, 2, 5), np.int16), np.zeros((2, 2, 6), np.int16))
+    pl = B.gemm_mp_plan_host(d, c, c, c, np.zeros((2, 2, 6), np.int16), np.zeros((2, 2, 6), np.int16))
+    B.gemm_mp_destroy(pl)
+
+
+def test_fused_tensor_launch_plan():
+    """GMP_FLAG_TC_FUSED (host plan only): with FP32 and FP16 pairs in each SUMMA step
+    and nb = 128, the step's tensor classes share one launch; the FP64 class keeps its
+    own; the per-class launch counts still name every class present"""
+    import numpy as np
+    nb, t = 128, 4
+    d0 = B.make_desc(t * nb, t * nb, t * nb, nb, 1e-6, 1.0, 0.0, 0b00111)
+    d1 = B.make_desc(t * nb, t * nb, t * nb, nb, 1e-6, 1.0, 0.0, 0b00111, B.GMP_FLAG_TC_FUSED)
+    ac = np.array([[0, 1, 2, 1]] * t, np.uint8)     # per l: FP64, FP32, FP16, FP32 pairs
+    bc = np.zeros((t, t), np.uint8)
+    bc[1:, :] = 1
+    cc = np.zeros((t, t), np.uint8)
+    z = np.zeros((t, t, 6), np.int16)
+    st = []
+    for d in (d0, d1):
+        pl = B.gemm_mp_plan_host(d, ac, bc, cc, z, z)
+        st.append(B.gemm_mp_get_stats(pl))
+        B.gemm_mp_destroy(pl)
+    sep, fus = st
+    assert sep["pairs"][:3] == fus["pairs"][:3] == [t * t, 2 * t * t, t * t]
+    assert fus["launches_execute"] == sep["launches_execute"] - 1          # one step, FP32 + FP16 fused
+    assert list(fus["class_launches"][:3]) == list(sep["class_launches"][:3]) == [1, 1, 1]
