@@ -164,7 +164,9 @@ gmp_status_t gemm_mp_convert(gmp_plan_t plan, void *ws, size_t ws_bytes, void *s
  * accumulators; finally C-finalize writes the packed C and the binary64 user C
  * (local layout, ldc).  Collective over the grid.  Async on `stream`; may be
  * called repeatedly after one convert (a repeated execute reuses the received
- * panels: no SUMMA traffic).                                                   */
+ * panels: no SUMMA traffic).  The C tile descriptors are uploaded only when ldc
+ * or the workspace changed, so on one GPU a repeated execute with the same
+ * arguments issues kernels only and may be captured into a CUDA graph.         */
 gmp_status_t gemm_mp_execute(gmp_plan_t plan, double *C, int64_t ldc, void *stream);
 
 /* Waits for the plan's streams; returns the first asynchronous error.          */

@@ -46,8 +46,11 @@ class GemmMP:
     def convert(self):
         B.gemm_mp_convert(self.plan, self.ws, self.ws_bytes, self.stream)
 
-    def execute(self, C):
-        B.gemm_mp_execute(self.plan, C, C.stride(0), self.stream)
+    def execute(self, C, stream=None):
+        """C <- alpha A B + beta C_in on `stream` (default: the plan's).  A repeated execute
+        with the same C and workspace issues kernels only, so it can be captured into a
+        CUDA graph (torch.cuda.graph) after one warm-up execute."""
+        B.gemm_mp_execute(self.plan, C, C.stride(0), stream or self.stream)
 
     def maps(self):
         return B.gemm_mp_get_maps(self.plan, self.mt, self.nt, self.kt)

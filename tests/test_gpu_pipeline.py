@@ -39,3 +39,34 @@ def test_host_pipeline_matches_single_runs(beta):
     pipe.close()
     for k in range(steps):
         assert np.array_equal(hOut[k].numpy(), want[k]), f"step {k}"
+
+
+@pytest.mark.parametrize("flags", [0, B.GMP_FLAG_TC_FUSED])
+def test_execute_replays_from_a_cuda_graph(flags):
+    """after one warm-up execute, gemm_mp_execute issues kernels only (the C tile
+    descriptors are already on the device), so a captured execute replays to the
+    same C, bit for bit, as often as it is launched"""
+    w = gmp_inputs.small_workload(512, 768, 1024, 128, 1e-5, mode="random", E=24, beta=0.5, seed=77,
+                                  class_mask=0b11111)
+    A, Bm, C = w.matrices()
+    dev = torch.device("cuda:0")
+    desc = B.make_desc(w.M, w.N, w.K, w.nb, w.tol, w.alpha, w.beta, w.class_mask, flags)
+    g = api.GemmMP(desc, torch.from_numpy(A).to(dev), torch.from_numpy(Bm).to(dev), torch.from_numpy(C).to(dev))
+    g.convert()
+    out = torch.empty(w.M, w.N, dtype=torch.float64, device=dev)
+    g.execute(out)
+    g.sync()
+    ref = out.clone()
+    graph = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(graph, stream=side):
+            g.execute(out, stream=side)
+    torch.cuda.synchronize()
+    for _ in range(3):
+        out.fill_(float("nan"))
+        graph.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
+    g.close()
