@@ -30,17 +30,30 @@ __global__ void __launch_bounds__(256) k_tile_stats(const StatsJob* __restrict__
   const int64_t n = (int64_t)nb * nb;
   double a0 = 0.0, a1 = 0.0, mx = 0.0;
   bool fin = true;
-  constexpr int U = 8;
-  int64_t q = 2 * t;
-  // canonical order: w = 0,1,2,...; loads are batched U at a time, the fma
-  // chain of each slot stays in increasing w.
-  for (; q + (int64_t)(U - 1) * 512 < n; q += (int64_t)U * 512) {
+  // canonical order: w = 0,1,2,...; loads are batched U at a time (U x 16 B in
+  // flight per thread: one CTA per tile must keep enough bytes in flight when a
+  // rank holds few tiles), the fma chain of each slot stays in increasing w.
+  // Element q = 2t + 512 w sits at row q / nb, column q % nb; both advance by a
+  // constant per w (dr rows + dc columns, one carry).
+#ifndef GMP_STATS_U
+#define GMP_STATS_U 16
+#endif
+  constexpr int U = GMP_STATS_U;
+  const int dr = 512 / nb, dc = 512 % nb;
+  int r = (2 * t) / nb, c = (2 * t) % nb;
+  auto step = [&] {
+    r += dr;
+    c += dc;
+    if (c >= nb) { c -= nb; ++r; }
+  };
+  const int64_t nw = n / 512;            // chain length per slot (nb^2 is a multiple of 512)
+  int64_t w = 0;
+  for (; w + U <= nw; w += U) {
     double2 v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      int64_t qq = q + (int64_t)u * 512;
-      int64_t r = qq / nb, c = qq - r * nb;
-      v[u] = __ldg(reinterpret_cast<const double2*>(j.base + r * j.ld + c));
+      v[u] = __ldg(reinterpret_cast<const double2*>(j.base + (int64_t)r * j.ld + c));
+      step();
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -51,9 +64,9 @@ __global__ void __launch_bounds__(256) k_tile_stats(const StatsJob* __restrict__
       mx = fmax(mx, fmax(m0, m1));
     }
   }
-  for (; q < n; q += 512) {
-    int64_t r = q / nb, c = q - r * nb;
-    double2 v = __ldg(reinterpret_cast<const double2*>(j.base + r * j.ld + c));
+  for (; w < nw; ++w) {
+    double2 v = __ldg(reinterpret_cast<const double2*>(j.base + (int64_t)r * j.ld + c));
+    step();
     a0 = __fma_rn(v.x, v.x, a0);
     a1 = __fma_rn(v.y, v.y, a1);
     double m0 = fabs(v.x), m1 = fabs(v.y);
