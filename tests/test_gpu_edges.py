@@ -199,3 +199,29 @@ def test_ab_map_at_the_threshold_matches_oracle(k, mask):
         assert np.array_equal(m["acode"], o["acode"]) and np.array_equal(m["bcode"], o["bcode"]), (k, tol)
         assert np.array_equal(m["ccode"], o["ccode"]), (k, tol)
         g.close()
+
+
+def test_extreme_exponents_match_oracle():
+    """A's sum of squares overflows binary64 (|a| ~ 2^520: S_A = inf, every A tile FP64 by
+    O5's rule), B's entries are tiny (~2^-520, per-tile scales far from 0) and their
+    product is O(1): maps and scales equal the oracle's bit for bit, C meets the parity
+    bound against the oracle"""
+    rng = np.random.default_rng(5)
+    nb = 128
+    A = np.ldexp(rng.uniform(-1, 1, (256, 384)), 520)
+    Bm = np.ldexp(rng.uniform(-1, 1, (384, 256)), -520)
+    Bm[:128, :128] = np.ldexp(Bm[:128, :128], -30)        # a wider spread of tile norms in B
+    C = rng.uniform(-1, 1, (256, 256))
+    tol, alpha, beta, mask = 1e-6, 1.0, 0.5, 0b01111
+    assert np.isinf((A * A).sum())
+    o = run_oracle(A, Bm, C, nb, tol, alpha, beta, mask)
+    assert o["rc"] == 0 and (o["acode"] == 0).all()
+    g, (out,) = run_gpu(A, Bm, C, nb, tol, alpha, beta, mask)
+    m = g.maps()
+    for k in ("acode", "bcode", "ccode"):
+        assert np.array_equal(m[k], o[k]), k
+    assert np.array_equal(m["bscale"], np.take_along_axis(o["bscale5"], o["bcode"][..., None].astype(np.int64),
+                                                          axis=2)[..., 0])
+    allfp64 = (o["bcode"] == 0).all() and (o["ccode"] == 0).all()
+    ok, rel = c_parity(out, o["C"], o["ccode"], o["cscale"], nb, 384, allfp64)
+    assert ok, rel
