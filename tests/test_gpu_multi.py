@@ -24,14 +24,18 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("G,sender,cfg", [(2, False, "small"), (2, True, "small"), (4, False, "small"),
-                                          (4, True, "small"), (2, False, "uneven"), (4, True, "uneven")])
-def test_summa_bitwise_vs_single_gpu(G, sender, cfg):
+# grids 1x4 / 4x1: a 4-member row (column) communicator, as in the 2x4 grid of 8 GPUs
+@pytest.mark.parametrize("G,sender,cfg,grid", [(2, False, "small", None), (2, True, "small", None),
+                                               (4, False, "small", None), (4, True, "small", None),
+                                               (2, False, "uneven", None), (4, True, "uneven", None),
+                                               (4, False, "small", "1x4"), (4, True, "uneven", "4x1")])
+def test_summa_bitwise_vs_single_gpu(G, sender, cfg, grid):
     if torch.cuda.device_count() < G:
         pytest.skip(f"needs {G} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={G}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(ROOT, "tools", "multi_gpu_check.py"), "--cfg", cfg] + (["--sender"] if sender else [])
+           os.path.join(ROOT, "tools", "multi_gpu_check.py"), "--cfg", cfg] + (["--sender"] if sender else []) + \
+        (["--grid", grid] if grid else [])
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]

@@ -40,6 +40,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg", default="small")
     ap.add_argument("--sender", action="store_true", help="GMP_FLAG_SENDER_SIDE (hybrid conversion, NEXT-2)")
+    ap.add_argument("--grid", default=None, help="PxQ process grid (default: api.default_grid)")
     a = ap.parse_args()
     rank, G = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     lr_ = int(os.environ.get("LOCAL_RANK", rank))
@@ -54,7 +55,8 @@ def main():
                                       class_mask=0b111111)
     else:
         w = gmp_inputs.workload(int(a.cfg))
-    P, Q = api.default_grid(G)
+    P, Q = api.default_grid(G) if a.grid is None else tuple(int(v) for v in a.grid.split("x"))
+    assert P * Q == G, (P, Q, G)
     p, q = rank // Q, rank % Q
     uid = B.gemm_mp_nccl_unique_id() if rank == 0 else bytes(128)
     t = torch.frombuffer(bytearray(uid), dtype=torch.uint8).to(dev)
