@@ -82,8 +82,8 @@ typedef enum {
                                  (k_tc_fused): per C sub-tile their pairs run in the fold order
                                  (class 5 .. 1, l increasing) with one W read and write instead of
                                  one per class; C is bit-identical.  Measured 3-10 % slower than the
-                                 per-class launches on cfg2 (the 16-bit pairs at 128 x 128 are bound
-                                 by L2->SM bandwidth, not by W traffic).  stats.class_ms
+                                 per-class launches on cfg2 (the 16-bit pairs at 128 x 128 are limited
+                                 by their operand feed, not by W traffic).  stats.class_ms
                                  splits the launch's time by the classes' MMA issue cycles.       */
 #define GMP_FLAG_SENDER_SIDE 16u /* SURVEY 8(f) NEXT-2, hybrid conversion (PAPER.md:148 defers it): a
                                  SUMMA panel tile whose receivers in its process row (A) / column (B)

@@ -15,8 +15,8 @@
 // Opt-in (GMP_FLAG_TC_FUSED).  Measured on cfg2 (profiles/tc_fused_r01.md): the
 // saved W traffic is real (1.8 GB less DRAM written per step) but the launch takes
 // ~10 % more cycles than the two per-class launches it replaces -- the 16-bit
-// pairs at 128 x 128 need ~118 B/clk/SM of operands against an L2->SM ceiling of
-// ~43 B/clk/SM, so they are L2-bound in either form, and inside the fused
+// pairs at 128 x 128 need ~118 B/clk/SM of operands (the full-chip L2 averages
+// ~43 B/clk/SM), so W traffic is not what limits them, and inside the fused
 // launch they also slow the FP32 class's pipeline (tensor pipe 72.6 % vs 88.3 %).
 //
 // Warp roles as k_tc_class (warp 0 TMA, warp 1 TMEM alloc + MMA issue, warps 2..9
