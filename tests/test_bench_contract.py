@@ -31,6 +31,25 @@ def test_reference_arm_prints_the_contract_line():
     assert out["config"]["workload"].startswith("cfg1")
 
 
+def test_reference_arm_under_torchrun_prints_once():
+    """the driver launches the reference arm like the GPU arm for N > 1: rank 0 alone
+    runs the oracle and prints the line, the other ranks exit 0 without work"""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                        "--impl", "reference", "--gpus", "2", "--config", "1", "--steps", "1", "--warmup", "0"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    out = json.loads(lines[0])
+    assert out["impl"] == "reference" and out["n_gpus"] == 2 and out["value"] > 0
+
+
 @pytest.mark.gpu
 def test_gpu_arm_prints_the_contract_line():
     torch = pytest.importorskip("torch")
