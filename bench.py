@@ -236,7 +236,7 @@ def run_e2e(a, A, Bm, C, Cout, lr, lc, G, dev, stream, desc, comm, w):
     (api.HostPipeline): every step copies its A, B (C) host->device, runs plan ->
     convert -> execute, and reads its C back device->host, all inside the timed
     region; the copies of neighbouring steps overlap this step's compute
-    (double-buffered device operands, full-duplex PCIe).  Time = first H2D to
+    (triple-buffered device operands, full-duplex PCIe).  Time = first H2D to
     last D2H, fill and drain included, / steps."""
     import torch
     import torch.distributed as dist

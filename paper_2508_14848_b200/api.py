@@ -107,23 +107,26 @@ class HostPipeline:
 
     Each step k copies its A, B (C) to the device, runs plan -> convert ->
     execute, and copies its C back.  Device operand and result buffers are
-    double-buffered, and the copies run on their own streams, so the H2D of step
-    k+1 and the D2H of step k-1 overlap the compute of step k (PCIe is full
-    duplex).  Only copies and stream/event ordering happen here; every step of
+    `nbuf`-fold buffered (3 by default), and the copies run on their own streams,
+    so the H2D of the next steps and the D2H of the previous ones overlap the
+    compute of step k (PCIe is full duplex).  Only copies and stream/event ordering happen here; every step of
     the method runs in the library's kernels.
 
     `desc` fixes the shape (every step reuses it); `comm` is the NCCL
     communicator for P*Q > 1.  Host tensors must be pinned for the copies to be
     asynchronous."""
 
-    def __init__(self, desc, local_a, local_b, local_c, local_out, device, comm=None):
+    def __init__(self, desc, local_a, local_b, local_c, local_out, device, comm=None, nbuf=3):
         self.desc, self.device, self.comm = desc, device, comm
         self.compute = torch.cuda.current_stream(device)
         self.h2d = torch.cuda.Stream(device)
         self.d2h = torch.cuda.Stream(device)
-        mk = lambda shp: [torch.empty(shp, dtype=torch.float64, device=device) for _ in range(2)]  # noqa: E731
+        # nbuf device copies of the operands and results: the H2D of step k+nbuf-1
+        # only waits for step k-1's convert, so copies run nbuf-1 steps ahead
+        self.nbuf = nbuf
+        mk = lambda shp: [torch.empty(shp, dtype=torch.float64, device=device) for _ in range(nbuf)]  # noqa: E731
         self.dA, self.dB = mk(local_a), mk(local_b)
-        self.dC = mk(local_c) if desc.beta != 0.0 else [None, None]
+        self.dC = mk(local_c) if desc.beta != 0.0 else [None] * nbuf
         self.dOut = mk(local_out)
         self.nscr = B.gemm_mp_scratch_size(desc)
         self.scratch = torch.empty(self.nscr, dtype=torch.uint8, device=device)
@@ -152,27 +155,33 @@ class HostPipeline:
     def run(self, hA, hB, hC, hOut):
         """Process len(hA) steps: hOut[k] <- alpha hA[k] hB[k] + beta hC[k] (host tensors)."""
         K = len(hA)
-        h2d_done = [torch.cuda.Event() for _ in range(K)]
-        convert_done = [torch.cuda.Event() for _ in range(K)]
-        exec_done = [torch.cuda.Event() for _ in range(K)]
-        d2h_done = [torch.cuda.Event() for _ in range(K)]
+        timed = getattr(self, "record_timeline", False)   # dev aid: keep timing events of the last run
+        h2d_done = [torch.cuda.Event(enable_timing=timed) for _ in range(K)]
+        convert_done = [torch.cuda.Event(enable_timing=timed) for _ in range(K)]
+        exec_done = [torch.cuda.Event(enable_timing=timed) for _ in range(K)]
+        d2h_done = [torch.cuda.Event(enable_timing=timed) for _ in range(K)]
+        if timed:
+            self.timeline = (h2d_done, convert_done, exec_done, d2h_done)
+
+        nbuf = self.nbuf
 
         def enqueue_h2d(k):
-            b = k % 2
+            b = k % nbuf
             with torch.cuda.stream(self.h2d):
-                if k >= 2:
-                    self.h2d.wait_event(convert_done[k - 2])   # buffers b free once step k-2 is packed
+                if k >= nbuf:
+                    self.h2d.wait_event(convert_done[k - nbuf])   # buffers b free once step k-nbuf is packed
                 self.dA[b].copy_(hA[k], non_blocking=True)
                 self.dB[b].copy_(hB[k], non_blocking=True)
                 if self.dC[b] is not None:
                     self.dC[b].copy_(hC[k], non_blocking=True)
                 h2d_done[k].record(self.h2d)
 
-        enqueue_h2d(0)
+        for k in range(min(nbuf - 1, K)):
+            enqueue_h2d(k)
         for k in range(K):
-            b = k % 2
-            if k + 1 < K:
-                enqueue_h2d(k + 1)                              # before plan's host sync
+            b = k % nbuf
+            if k + nbuf - 1 < K:
+                enqueue_h2d(k + nbuf - 1)                       # before plan's host sync
             self.compute.wait_event(h2d_done[k])
             dC = self.dC[b]
             pl = B.gemm_mp_plan(self.desc, self.dA[b], self.dA[b].stride(0), self.dB[b], self.dB[b].stride(0),
@@ -187,8 +196,8 @@ class HostPipeline:
                     self._ensure_ws(nws)
             B.gemm_mp_convert(pl, self.ws, nws, self.compute)
             convert_done[k].record(self.compute)
-            if k >= 2:
-                self.compute.wait_event(d2h_done[k - 2])        # result buffer b read back
+            if k >= nbuf:
+                self.compute.wait_event(d2h_done[k - nbuf])     # result buffer b read back
             B.gemm_mp_execute(pl, self.dOut[b], self.dOut[b].stride(0), self.compute)
             exec_done[k].record(self.compute)
             with torch.cuda.stream(self.d2h):

@@ -1,6 +1,6 @@
 """api.HostPipeline (host-buffer GEMM stream, bench.py's e2e leg): every step's
 host result equals the result of the same GEMM run on its own, for a stream of
-DIFFERENT inputs, so the double buffering never mixes steps up; and the
+DIFFERENT inputs, so the multi-buffering never mixes steps up; and the
 library's table staging (mapped pinned memory, k_xfer) holds up while large
 copies occupy the copy engines."""
 import numpy as np
@@ -15,10 +15,10 @@ from paper_2508_14848_b200 import binding as B
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("beta", [0.0, 0.5])
-def test_host_pipeline_matches_single_runs(beta):
+@pytest.mark.parametrize("beta,nbuf", [(0.0, 3), (0.5, 3), (0.5, 2)])
+def test_host_pipeline_matches_single_runs(beta, nbuf):
     M, N, K, nb = 768, 512, 1024, 128
-    steps = 5
+    steps = 6
     hA, hB, hC, want = [], [], [], []
     for k in range(steps):
         w = gmp_inputs.small_workload(M, N, K, nb, 1e-5, mode="random", E=20, beta=beta, seed=40 + k,
@@ -31,7 +31,7 @@ def test_host_pipeline_matches_single_runs(beta):
         want.append(out)
     desc = B.make_desc(M, N, K, nb, 1e-5, 1.0, beta, 0b11111)
     dev = torch.device("cuda:0")
-    pipe = api.HostPipeline(desc, (M, K), (K, N), (M, N) if beta != 0.0 else None, (M, N), dev)
+    pipe = api.HostPipeline(desc, (M, K), (K, N), (M, N) if beta != 0.0 else None, (M, N), dev, nbuf=nbuf)
     pipe.reserve(hA[0], hB[0], hC[0])
     hOut = [torch.full((M, N), float("nan"), dtype=torch.float64).pin_memory() for _ in range(steps)]
     pipe.run(hA, hB, hC, hOut)
