@@ -227,6 +227,9 @@ struct gmp_plan_s {
   std::vector<WorkItem> items;
   std::vector<PairDesc> pairs;
   std::vector<Launch> launches;
+  std::vector<int32_t> acc_init_idx;      // local C tiles whose W0 k_acc_init writes (the others: their
+                                          // first tile-GEMM launch, WorkItem.pad bit 0)
+  int64_t off_accinit = 0;
   std::vector<int64_t> shadow_step_off;   // element offset of each step's shadow jobs
   // workspace layout (byte offsets)
   int64_t off_pack = 0, off_shadow = 0, off_ctd = 0, off_items = 0, off_pairs = 0, off_maxbits = 0,
@@ -466,6 +469,7 @@ static void build_tables(gmp_plan_s* pl) {
   pl->off_items = o; o = align_up(o + n_items * (int64_t)sizeof(WorkItem), 1024);
   pl->off_pairs = o; o = align_up(o + n_pairs * (int64_t)sizeof(PairDesc), 1024);
   pl->off_maxbits = o; o = align_up(o + nCl * 8, 1024);
+  pl->off_accinit = o; o = align_up(o + nCl * 4, 1024);
   pl->off_cscale = o; o = align_up(o + nCl * 2, 1024);
   pl->off_tc = o; o = align_up(o + 1024, 1024);
   for (int c = 0; c < NC; ++c) {
@@ -760,6 +764,30 @@ static void build_tables(gmp_plan_s* pl) {
     }
   }
 
+  // ---- W0 (O9): the first launch of SUMMA step 0 that touches a local C tile starts
+  // its W from C_in when its kernel can (k_tc_class incl. the FP32 split, k_tc_fused:
+  // the W rows are loaded once per item there); the other tiles get W0 from
+  // k_acc_init ----
+  pl->acc_init_idx.clear();
+  {
+    std::vector<uint8_t> done(nCl, 0);
+    for (size_t li = 0; li < pl->launches.size(); ++li) {
+      const Launch& L = pl->launches[li];
+      if (L.step != 0) break;
+      const int64_t iend = li + 1 < pl->launches.size() ? pl->launches[li + 1].ibeg : (int64_t)pl->items.size();
+      const bool can = L.kind == 1 || L.kind == 3 || L.kind == 7;
+      for (int64_t q = L.ibeg; q < iend; ++q) {
+        WorkItem& wi = pl->items[q];
+        if (done[wi.ctile]) continue;
+        done[wi.ctile] = 1;
+        if (can) wi.pad |= 1;
+        else pl->acc_init_idx.push_back(wi.ctile);
+      }
+    }
+    for (int64_t k = 0; k < nCl; ++k)
+      if (!done[k]) pl->acc_init_idx.push_back((int32_t)k);
+  }
+
   // ---- stats ----
   gmp_stats_t& st = pl->st;
   std::memset(&st, 0, sizeof st);
@@ -778,7 +806,7 @@ static void build_tables(gmp_plan_s* pl) {
   st.recv_bytes_local = recv_bytes;
   st.workspace_bytes = pl->ws_bytes;
   st.steps = steps;
-  int nl = 3 + (int)pl->launches.size();  // acc init, tile-GEMM launches, maxabs, finalize
+  int nl = (pl->acc_init_idx.empty() ? 2 : 3) + (int)pl->launches.size();  // [acc init], tile-GEMMs, maxabs, finalize
   auto nsh = [](const std::vector<ShadowJob>& v) {
     int64_t t = 0;
     for (const auto& j : v) t += j.transpose;
@@ -1094,6 +1122,7 @@ extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_byte
   std::vector<SliceJob> allsl = pl->slice_local;
   for (auto& v : pl->slice_step) allsl.insert(allsl.end(), v.begin(), v.end());
   tables.add(ws + pl->off_pack, pl->pack.data(), (int64_t)(pl->pack.size() * sizeof(PackJob)));
+  tables.add(ws + pl->off_accinit, (const uint8_t*)pl->acc_init_idx.data(), (int64_t)(pl->acc_init_idx.size() * 4));
   tables.add(ws + pl->off_shadow, allsh.data(), (int64_t)(allsh.size() * sizeof(ShadowJob)));
   tables.add(ws + pl->off_items, pl->items.data(), (int64_t)(pl->items.size() * sizeof(WorkItem)));
   tables.add(ws + pl->off_pairs, pl->pairs.data(), (int64_t)(pl->pairs.size() * sizeof(PairDesc)));
@@ -1161,8 +1190,9 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
     pl->ctd_ws = ws;
   }
   const CTileDesc* dct = (const CTileDesc*)(ws + pl->off_ctd);
-  if (nCl) {
-    k_acc_init<<<dim3(grid_for(nb2, 1) / 4 + 1, (unsigned)nCl), 256, 0, stream>>>(dct, ws, nb2, pl->d.beta);
+  if (!pl->acc_init_idx.empty()) {
+    k_acc_init<<<dim3(grid_for(nb2, 1) / 4 + 1, (unsigned)pl->acc_init_idx.size()), 256, 0, stream>>>(
+        dct, (const int32_t*)(ws + pl->off_accinit), ws, nb2, pl->d.beta);
     GMP_CUDA(cudaGetLastError());
   }
   const int steps = pl->st.steps;
@@ -1203,10 +1233,10 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
       } else if (L.kind == 6) {
         GMP_TRY(tcmc_launch(pl->tc, L.cls, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, stream));
       } else if (L.kind == 7) {
-        GMP_TRY(tcf_launch(pl->tc, L.present, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, stream));
+        GMP_TRY(tcf_launch(pl->tc, L.present, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, pl->d.beta, stream));
       } else if (L.kind == 1 || L.kind == 3) {
         GMP_TRY(tc_launch(pl->tc, L.kind == 3 ? TC_SPLIT : L.cls, L.bn, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha,
-                          stream));
+                          pl->d.beta, stream));
       } else {
         switch (L.cls) {
           case 0:

@@ -292,21 +292,25 @@ struct CTileDesc {
   int32_t pad;
 };
 
-__global__ void __launch_bounds__(256) k_acc_init(const CTileDesc* __restrict__ ct, uint8_t* ws,
-                                                  int64_t n, double beta) {
-  const CTileDesc c = ct[blockIdx.y];
+// W0 of element e of a C tile (binary64 W for code 0, binary32 otherwise)
+__device__ __forceinline__ double w0_f64(const CTileDesc& c, const uint8_t* ws, int64_t e, double beta) {
+  return (beta == 0.0) ? 0.0 : __dmul_rn(beta, payload_f64(ws + c.cin_off, e, 0));
+}
+__device__ __forceinline__ float w0_f32(const CTileDesc& c, const uint8_t* ws, int64_t e, double beta) {
+  if (beta == 0.0) return 0.f;
   const float bf = __double2float_rn(beta);
+  return __double2float_rn(__dmul_rn((double)bf, ldexp_fast(payload_f64(ws + c.cin_off, e, c.code), -c.cin_scale)));
+}
+
+// W0 of the C tiles listed in idx (the tiles whose first tile-GEMM launch does not
+// initialise W itself; WorkItem.pad bit 0 marks the items that do)
+__global__ void __launch_bounds__(256) k_acc_init(const CTileDesc* __restrict__ ct, const int32_t* __restrict__ idx,
+                                                  uint8_t* ws, int64_t n, double beta) {
+  const CTileDesc c = ct[idx[blockIdx.y]];
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
-    if (c.code == 0) {
-      double x = (beta == 0.0) ? 0.0 : __dmul_rn(beta, payload_f64(ws + c.cin_off, e, 0));
-      reinterpret_cast<double*>(ws + c.w_off)[e] = x;
-    } else {
-      float x = 0.f;
-      if (beta != 0.0)
-        x = __double2float_rn(__dmul_rn((double)bf, ldexp_fast(payload_f64(ws + c.cin_off, e, c.code), -c.cin_scale)));
-      reinterpret_cast<float*>(ws + c.w_off)[e] = x;
-    }
+    if (c.code == 0) reinterpret_cast<double*>(ws + c.w_off)[e] = w0_f64(c, ws, e, beta);
+    else reinterpret_cast<float*>(ws + c.w_off)[e] = w0_f32(c, ws, e, beta);
   }
 }
 

@@ -116,8 +116,9 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 template <int BN>
 __device__ __forceinline__ void tc_epilogue(const WorkItem* __restrict__ items, int64_t nitems,
                                             const PairDesc* __restrict__ pairs, const CTileDesc* __restrict__ ctiles,
-                                            uint8_t* __restrict__ ws, int nb, double alpha, uint32_t tmem_base,
-                                            uint64_t* tfull, uint64_t* tempty, int warp, int lane) {
+                                            uint8_t* __restrict__ ws, int nb, double alpha, double beta,
+                                            uint32_t tmem_base, uint64_t* tfull, uint64_t* tempty, int warp,
+                                            int lane) {
   // epilogue: 8 warps; warp w reads TMEM lanes 32*(w%4)..+31 (= tile rows) and
   // half (w-2)/4 of the BN columns.  binary32 W: the W row segment lives in
   // registers for the whole item (one read + one write per item instead of
@@ -134,10 +135,15 @@ __device__ __forceinline__ void tc_epilogue(const WorkItem* __restrict__ items, 
     if (ct.code != 0) {
       float* wrow = reinterpret_cast<float*>(ws + ct.w_off) + rowoff;
       float accr[HC];
+      if (w.pad & 1) {   // first tile-GEMM launch of this C tile: W0 from C_in (O9)
 #pragma unroll
-      for (int v = 0; v < HC / 4; ++v) {
-        float4 x = reinterpret_cast<const float4*>(wrow)[v];
-        accr[4 * v] = x.x; accr[4 * v + 1] = x.y; accr[4 * v + 2] = x.z; accr[4 * v + 3] = x.w;
+        for (int v = 0; v < HC; ++v) accr[v] = w0_f32(ct, ws, rowoff + v, beta);
+      } else {
+#pragma unroll
+        for (int v = 0; v < HC / 4; ++v) {
+          float4 x = reinterpret_cast<const float4*>(wrow)[v];
+          accr[4 * v] = x.x; accr[4 * v + 1] = x.y; accr[4 * v + 2] = x.z; accr[4 * v + 3] = x.w;
+        }
       }
       for (int pi = 0; pi < w.pcnt; ++pi) {
         const PairDesc pd = pairs[w.pbeg + pi];
@@ -165,10 +171,15 @@ __device__ __forceinline__ void tc_epilogue(const WorkItem* __restrict__ items, 
       // binary64 W, BN <= 128: the W row segment lives in registers for the item
       double* wrow = reinterpret_cast<double*>(ws + ct.w_off) + rowoff;
       double accd[HC];
+      if (w.pad & 1) {   // first tile-GEMM launch of this C tile: W0 from C_in (O9)
 #pragma unroll
-      for (int v = 0; v < HC / 2; ++v) {
-        const double2 x = reinterpret_cast<const double2*>(wrow)[v];
-        accd[2 * v] = x.x; accd[2 * v + 1] = x.y;
+        for (int v = 0; v < HC; ++v) accd[v] = w0_f64(ct, ws, rowoff + v, beta);
+      } else {
+#pragma unroll
+        for (int v = 0; v < HC / 2; ++v) {
+          const double2 x = reinterpret_cast<const double2*>(wrow)[v];
+          accd[2 * v] = x.x; accd[2 * v + 1] = x.y;
+        }
       }
       for (int pi = 0; pi < w.pcnt; ++pi) {
         const PairDesc pd = pairs[w.pbeg + pi];
@@ -244,7 +255,7 @@ template <int C, int BN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const WorkItem* __restrict__ items, int64_t nitems, const PairDesc* __restrict__ pairs,
-           const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha) {
+           const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha, double beta) {
   constexpr int NP = tc_np<C>(), ST = tc_stages<C>();
   constexpr int ESZ = (C == 4 || C == 5) ? 1 : 2;
   constexpr int BK = 128 / ESZ;            // elements per 128-byte K block
@@ -337,7 +348,7 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
       }
     }
   } else {
-    tc_epilogue<BN>(items, nitems, pairs, ctiles, ws, nb, alpha, tmem_base, tfull, tempty, warp, lane);
+    tc_epilogue<BN>(items, nitems, pairs, ctiles, ws, nb, alpha, beta, tmem_base, tfull, tempty, warp, lane);
   }
   tc_fence_before();
   __syncthreads();
@@ -419,7 +430,7 @@ inline gmp_status_t tc_prepare(TcTables& t, uint8_t* ws, const int64_t* arena_of
 
 template <int C, int BN>
 inline gmp_status_t tc_launch_t(TcTables& t, const WorkItem* it, int64_t n, const PairDesc* pd, const CTileDesc* ct,
-                                uint8_t* ws, int nb, double alpha, cudaStream_t s) {
+                                uint8_t* ws, int nb, double alpha, double beta, cudaStream_t s) {
   constexpr int smem = tc_smem_bytes<C, BN>();
   if (ensure_max_smem(k_tc_class<C, BN>, smem) != cudaSuccess) return GMP_ERR_CUDA;
   int dev = 0, sms = 148;
@@ -428,23 +439,23 @@ inline gmp_status_t tc_launch_t(TcTables& t, const WorkItem* it, int64_t n, cons
   const int grid = (int)std::min<int64_t>(n, sms);
   constexpr int mi = tc_map_index<C>();
   k_tc_class<C, BN><<<grid, TC_THREADS, smem, s>>>(t.mapA[mi], BN == 128 ? t.mapB128[mi] : t.mapB[mi], it, n, pd, ct,
-                                                    ws, nb, alpha);
+                                                    ws, nb, alpha, beta);
   return cudaGetLastError() == cudaSuccess ? GMP_OK : GMP_ERR_CUDA;
 }
 
 // cls: 2..5 for the 16/8-bit classes, TC_SPLIT for the FP32 class on the tensor
 // pipe; bn: 256 or 128 (128 when the launch folds into binary64 W)
 inline gmp_status_t tc_launch(TcTables& t, int cls, int bn, const WorkItem* it, int64_t n, const PairDesc* pd,
-                              const CTileDesc* ct, uint8_t* ws, int nb, double alpha, cudaStream_t s) {
+                              const CTileDesc* ct, uint8_t* ws, int nb, double alpha, double beta, cudaStream_t s) {
   const int mi = (cls == TC_SPLIT) ? GMP_AR_SPLIT : cls;
   if (!((cls >= 2 && cls <= 5) || cls == TC_SPLIT) || !t.ready[mi]) return GMP_ERR_STATE;
   const bool wide = bn == 256;
   switch (cls) {
-    case 2: return wide ? tc_launch_t<2, 256>(t, it, n, pd, ct, ws, nb, alpha, s) : tc_launch_t<2, 128>(t, it, n, pd, ct, ws, nb, alpha, s);
-    case 3: return wide ? tc_launch_t<3, 256>(t, it, n, pd, ct, ws, nb, alpha, s) : tc_launch_t<3, 128>(t, it, n, pd, ct, ws, nb, alpha, s);
-    case 4: return wide ? tc_launch_t<4, 256>(t, it, n, pd, ct, ws, nb, alpha, s) : tc_launch_t<4, 128>(t, it, n, pd, ct, ws, nb, alpha, s);
-    case 5: return wide ? tc_launch_t<5, 256>(t, it, n, pd, ct, ws, nb, alpha, s) : tc_launch_t<5, 128>(t, it, n, pd, ct, ws, nb, alpha, s);
-    default: return tc_launch_t<TC_SPLIT, 128>(t, it, n, pd, ct, ws, nb, alpha, s);
+    case 2: return wide ? tc_launch_t<2, 256>(t, it, n, pd, ct, ws, nb, alpha, beta, s) : tc_launch_t<2, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, s);
+    case 3: return wide ? tc_launch_t<3, 256>(t, it, n, pd, ct, ws, nb, alpha, beta, s) : tc_launch_t<3, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, s);
+    case 4: return wide ? tc_launch_t<4, 256>(t, it, n, pd, ct, ws, nb, alpha, beta, s) : tc_launch_t<4, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, s);
+    case 5: return wide ? tc_launch_t<5, 256>(t, it, n, pd, ct, ws, nb, alpha, beta, s) : tc_launch_t<5, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, s);
+    default: return tc_launch_t<TC_SPLIT, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, s);
   }
 }
 

@@ -56,7 +56,7 @@ struct TcfRing {
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_tc_fused(const __grid_constant__ TcfMaps maps, const WorkItem* __restrict__ items, int64_t nitems,
            const PairDesc* __restrict__ pairs, const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb,
-           double alpha) {
+           double alpha, double beta) {
   constexpr int BN = TCF_BN, NMMA = 4;
   constexpr uint32_t TMEM_COLS = 2 * BN;
   extern __shared__ uint8_t smem_raw[];
@@ -168,7 +168,7 @@ k_tc_fused(const __grid_constant__ TcfMaps maps, const WorkItem* __restrict__ it
       }
     }
   } else {
-    tc_epilogue<BN>(items, nitems, pairs, ctiles, ws, nb, alpha, tmem_base, tfull, tempty, warp, lane);
+    tc_epilogue<BN>(items, nitems, pairs, ctiles, ws, nb, alpha, beta, tmem_base, tfull, tempty, warp, lane);
   }
   tc_fence_before();
   __syncthreads();
@@ -181,7 +181,7 @@ constexpr int tcf_smem_bytes() { return TCF_SLOTS * TCF_SLOT + 1024 /*align*/ + 
 
 // cls_present: bit c set when the launch holds class-c pairs (c = 1 means the split arena)
 inline gmp_status_t tcf_launch(TcTables& t, unsigned cls_present, const WorkItem* it, int64_t n, const PairDesc* pd,
-                               const CTileDesc* ct, uint8_t* ws, int nb, double alpha, cudaStream_t s) {
+                               const CTileDesc* ct, uint8_t* ws, int nb, double alpha, double beta, cudaStream_t s) {
   TcfMaps m;
   std::memset(&m, 0, sizeof m);
   for (int c = 1; c <= 5; ++c) {
@@ -197,7 +197,7 @@ inline gmp_status_t tcf_launch(TcTables& t, unsigned cls_present, const WorkItem
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)std::min<int64_t>(n, sms);
-  k_tc_fused<<<grid, TC_THREADS, smem, s>>>(m, it, n, pd, ct, ws, nb, alpha);
+  k_tc_fused<<<grid, TC_THREADS, smem, s>>>(m, it, n, pd, ct, ws, nb, alpha, beta);
   return cudaGetLastError() == cudaSuccess ? GMP_OK : GMP_ERR_CUDA;
 }
 
