@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--impl", default="gemm_mp", choices=["gemm_mp", "reference"])
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--variant", default=None)
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (cfg3+ on one GPU)")
     ap.add_argument("--size", type=int, default=0, help="override M=N=K (keeps the config's recipe)")
