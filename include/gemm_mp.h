@@ -190,12 +190,23 @@ gmp_status_t gemm_mp_get_tile(gmp_plan_t plan, char which, int64_t ti, int64_t t
 
 gmp_status_t gemm_mp_get_stats(gmp_plan_t plan, gmp_stats_t *out);
 
+/* Debug export of S1 (O4): the GLOBAL per-tile statistics
+ * the map kernel used, as read back at gemm_mp_plan's one synchronisation --
+ * S = the canonical CNORM sum of squares, maxabs, finite flag (1 = no NaN/Inf) --
+ * for which = 'A' (mt x kt), 'B' (kt x nt) or 'C' (mt x nt; zeros when beta == 0),
+ * row-major tile grids.  On P*Q > 1 these are the all-reduced statistics
+ * (identical on every rank).  Host arrays, any may be NULL.  GMP_ERR_STATE on a
+ * gemm_mp_plan_host plan (no statistics were computed).                         */
+gmp_status_t gemm_mp_get_tile_stats(gmp_plan_t plan, char which, double *S, double *maxabs,
+                                    uint8_t *finite);
+
 /* Host-only plan from given maps (no device work): the same tile lists, arena
  * layout, work lists and SUMMA schedule as gemm_mp_plan builds after its map
  * kernels.  acode/bcode/ccode: global code grids; ascale5/bscale5: [tile][6]
  * class-c scales; cin_scale may be NULL.  For inspecting the schedule and the
- * multi-rank bookkeeping without a GPU (convert/execute on it fail with
- * GMP_ERR_STATE until a workspace is given).                                   */
+ * multi-rank bookkeeping without a GPU: it holds no operands, statistics or
+ * communicators, so gemm_mp_convert / gemm_mp_execute / gemm_mp_get_tile_stats
+ * on it fail with GMP_ERR_STATE.                                               */
 gmp_status_t gemm_mp_plan_host(const gmp_desc_t *desc, const uint8_t *acode, const uint8_t *bcode,
                                const uint8_t *ccode, const int16_t *ascale5, const int16_t *bscale5,
                                const int16_t *cin_scale, gmp_plan_t *out);

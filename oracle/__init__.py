@@ -191,12 +191,14 @@ class _Out(ct.Structure):
                 ("cin_scale", ct.c_void_p),
                 ("SA", ct.c_void_p), ("MA", ct.c_void_p), ("SB", ct.c_void_p),
                 ("MB", ct.c_void_p), ("SC", ct.c_void_p), ("MC", ct.c_void_p),
-                ("threads", ct.c_int)]
+                ("threads", ct.c_int), ("W", ct.c_void_p), ("ldw", ct.c_int64)]
 
 
 def gemm_mp(A, B, C, nb, tol, alpha=1.0, beta=0.0, class_mask=0b01111, ctiles=None,
-            a_map=None, b_map=None, c_map=None, Cout=None):
-    """Run the whole method (O1-O9).  Returns a dict with maps, scales and C.
+            a_map=None, b_map=None, c_map=None, Cout=None, want_w=True):
+    """Run the whole method (O1-O9).  Returns a dict with maps, scales and C, and
+    (want_w) "W": the final W accumulator of every computed C tile (binary64 array
+    holding the exact binary64 / binary32 W values, SURVEY 8(c) C6 debug export).
 
     ctiles: optional list of C tile indices i*nt+j to compute (sampled runs);
     tiles not listed are left as in `Cout` (default: zeros)."""
@@ -213,17 +215,30 @@ def gemm_mp(A, B, C, nb, tol, alpha=1.0, beta=0.0, class_mask=0b01111, ctiles=No
              cin_scale=np.zeros((mt, nt), np.int16),
              SA=np.zeros((mt, kt)), MA=np.zeros((mt, kt)), SB=np.zeros((kt, nt)),
              MB=np.zeros((kt, nt)), SC=np.zeros((mt, nt)), MC=np.zeros((mt, nt)))
+    W = np.zeros((M, N)) if want_w else None
     out = _Out(*[_p(o[k]) for k in ["acode", "bcode", "ccode", "ascale5", "bscale5", "cscale",
-                                     "cin_scale", "SA", "MA", "SB", "MB", "SC", "MC"]], 0)
+                                     "cin_scale", "SA", "MA", "SB", "MB", "SC", "MC"]], 0, _p(W), N)
     Cout = np.zeros((M, N)) if Cout is None else Cout
     tl = None if ctiles is None else np.ascontiguousarray(ctiles, np.int64)
     rc = lib().orc_gemm_mp(ct.byref(d), _p(A), K, _p(B), N, _p(C), N, _p(Cout), N, _p(tl),
                            0 if tl is None else tl.size, ct.byref(out))
     o["rc"] = rc
     o["C"] = Cout
+    o["W"] = W
     o["threads"] = out.threads
     return o
 
 
 def max_threads():
     return int(lib().orc_max_threads())
+
+
+def finalize(acc, code):
+    """O9 finalize of one C tile's W accumulator (binary64 array of exact W values):
+    returns (packed payload, user binary64 tile, scale)."""
+    a = np.ascontiguousarray(acc, dtype=np.float64)
+    nb = a.shape[0]
+    pay = np.empty(nb * nb, dtype=PAYLOAD_DTYPE[code])
+    user = np.empty((nb, nb), dtype=np.float64)
+    e = lib().orc_finalize(nb, code, _p(a), _p(pay), _p(user), nb)
+    return pay, user, int(e)

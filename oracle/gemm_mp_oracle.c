@@ -383,7 +383,7 @@ int orc_map_c(int64_t mt, int64_t nt, int64_t kt, int32_t nb, double tol, double
               double beta, uint32_t class_mask, const double *SA, const double *SB,
               const double *SC, const uint8_t *finiteC, const uint8_t *acode,
               const int16_t *ascale, const uint8_t *bcode, const int16_t *bscale,
-              uint8_t *code) {
+              uint8_t *code, const uint8_t *cmap) {
     if (beta != 0.0)
         for (int64_t t = 0; t < mt * nt; ++t)
             if (!finiteC[t]) return 1;
@@ -410,15 +410,21 @@ int orc_map_c(int64_t mt, int64_t nt, int64_t kt, int32_t nb, double tol, double
             double sc = (beta != 0.0) ? SC[i * nt + j] : 0.0;
             double nhat = (aa * RA) * QB + ab * sqrt(sc);
             int chosen = 0;
-            for (int li = 0; li < ORC_NCLS; ++li) {
-                int k = ORC_LADDER[li];
-                if (!(mask & (1u << k))) continue;
-                if (k == 0) { chosen = 0; break; }
-                double dC = (ORC_FMT[k].u + sqkt * 0x1p-24) +
-                            ((double)nb * ORC_FMT[k].eta) / ORC_FMT[k].omega_s;
-                if (dC * nhat <= rhs) { chosen = k; break; }
+            if (cmap) {                   /* explicit map (R19): the code, if enabled */
+                chosen = cmap[i * nt + j];
+                if (!(mask & (1u << chosen))) chosen = 0;
+            } else {
+                for (int li = 0; li < ORC_NCLS; ++li) {
+                    int k = ORC_LADDER[li];
+                    if (!(mask & (1u << k))) continue;
+                    if (k == 0) { chosen = 0; break; }
+                    double dC = (ORC_FMT[k].u + sqkt * 0x1p-24) +
+                                ((double)nb * ORC_FMT[k].eta) / ORC_FMT[k].omega_s;
+                    if (dC * nhat <= rhs) { chosen = k; break; }
+                }
             }
-            /* R23: FP32 accumulator range guards */
+            /* R23: FP32 accumulator range guards -- for explicit codes too: a binary32
+             * W cannot hold an output or fold factor outside its range */
             if (chosen != 0) {
                 int ok = (nhat <= 0x1p100);
                 if (beta != 0.0) {
@@ -556,6 +562,10 @@ typedef struct {
     int16_t *cin_scale;           /* scale of packed C_in (beta != 0)              */
     double *SA, *MA, *SB, *MB, *SC, *MC;
     int threads;
+    /* optional debug export: the final W accumulator of every
+     * computed C tile, exact W values as binary64, row-major with leading dim ldw */
+    double *W;
+    int64_t ldw;
 } orc_out_t;
 
 /* Apply an explicit map (R19, NEXT-1): codes given, scales from the rule. */
@@ -643,14 +653,9 @@ int orc_gemm_mp(const orc_desc_t *d, const double *A, int64_t lda, const double 
         free(tmp);
     }
     free(needA); free(needB);
-    if (d->c_map) {
-        int16_t *tmp = malloc(sizeof(int16_t) * nC);
-        orc_explicit_map(nC, d->c_map, d->class_mask, o->MC, o->ccode, tmp);
-        free(tmp);
-    } else {
-        rc = orc_map_c(mt, nt, kt, nb, d->tol, d->alpha, d->beta, d->class_mask, o->SA,
-                       o->SB, o->SC, fC, o->acode, o->ascale5, o->bcode, o->bscale5, o->ccode);
-    }
+    rc = orc_map_c(mt, nt, kt, nb, d->tol, d->alpha, d->beta, d->class_mask, o->SA,
+                   o->SB, o->SC, fC, o->acode, o->ascale5, o->bcode, o->bscale5, o->ccode,
+                   d->c_map);
     if (!rc) {
         int64_t nlist = ctiles ? n_ctiles : nC;
         int nthreads = 1;
@@ -689,6 +694,9 @@ int orc_gemm_mp(const orc_desc_t *d, const double *A, int64_t lda, const double 
                         }
                     }
                 }
+                if (o->W)
+                    for (int64_t r = 0; r < nb; ++r)
+                        memcpy(o->W + (i * nb + r) * o->ldw + j * nb, acc + r * nb, sizeof(double) * nb);
                 int e = orc_finalize(nb, codec, acc, cpay, Cout + i * nb * ldo + j * nb, ldo);
                 if (o->cscale) o->cscale[ct] = (int16_t)e;
             }

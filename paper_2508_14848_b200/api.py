@@ -58,6 +58,11 @@ class GemmMP:
     def stats(self):
         return B.gemm_mp_get_stats(self.plan)
 
+    def tile_stats(self, which):
+        """global per-tile (S, maxabs, finite) grids of 'A', 'B' or 'C' (S1 debug export)"""
+        rows, cols = {"A": (self.mt, self.kt), "B": (self.kt, self.nt), "C": (self.mt, self.nt)}[which]
+        return B.gemm_mp_get_tile_stats(self.plan, which, rows, cols)
+
     def tile(self, which, ti, tj, cls):
         return B.gemm_mp_get_tile(self.plan, which, ti, tj, cls, self.desc.nb)
 

@@ -85,6 +85,7 @@ def lib():
             "gemm_mp_get_tile": [vp, ct.c_char, i64, i64, i32, vp, ct.POINTER(ct.c_size_t),
                                  ct.POINTER(ct.c_int16)],
             "gemm_mp_get_stats": [vp, ct.POINTER(gmp_stats_t)],
+            "gemm_mp_get_tile_stats": [vp, ct.c_char, vp, vp, vp],
             "gemm_mp_nccl_unique_id": [vp],
             "gemm_mp_nccl_comm_create": [vp, ct.c_int, ct.c_int, ct.POINTER(vp)],
             "gemm_mp_nccl_comm_destroy": [vp],
@@ -190,6 +191,15 @@ def gemm_mp_get_tile(plan, which, ti, tj, cls, nb):
     _check(lib().gemm_mp_get_tile(plan, which.encode() if isinstance(which, str) else which, ti, tj, cls,
                                   buf.ctypes.data, ct.byref(n), ct.byref(sc)))
     return buf[:n.value].copy(), sc.value
+
+
+def gemm_mp_get_tile_stats(plan, which, rows, cols):
+    """global per-tile (S, maxabs, finite) of 'A' / 'B' / 'C' as rows x cols grids"""
+    import numpy as np
+    S = np.zeros((rows, cols)); M = np.zeros((rows, cols)); F = np.zeros((rows, cols), np.uint8)
+    _check(lib().gemm_mp_get_tile_stats(plan, which.encode() if isinstance(which, str) else which,
+                                        S.ctypes.data, M.ctypes.data, F.ctypes.data))
+    return S, M, F
 
 
 def gemm_mp_get_stats(plan):

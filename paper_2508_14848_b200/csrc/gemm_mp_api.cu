@@ -198,6 +198,10 @@ struct gmp_plan_s {
   // global maps (identical on every rank)
   std::vector<uint8_t> codeA, codeB, codeC;
   std::vector<int16_t> sA5, sB5, sCin, sCout;
+  // global per-tile statistics as the map kernel saw them (A | B | C): S (canonical
+  // sum of squares), then maxabs; finite flags (gemm_mp_get_tile_stats)
+  std::vector<double> statS;
+  std::vector<uint8_t> statF;
   // local tiles (global indices), C local position
   std::vector<int64_t> locA, locB, locC;
   // slots: [global tile][class] -> slot in that class's arena, -1 if absent
@@ -239,6 +243,7 @@ struct gmp_plan_s {
   uint8_t* ws = nullptr;
   bool converted = false;
   bool executed = false;
+  bool host_only = false;   // gemm_mp_plan_host: no operands, no statistics, no communicators
   gmp_stats_t st{};
 };
 
@@ -911,10 +916,14 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
   // ---- multi-GPU: every tile's stats owned by exactly one rank -> sum-allreduce is exact ----
   if (G > 1) {
     pl->world = (ncclComm_t)nccl_comm;
-    GMP_NCCL(ncclGroupStart());
-    GMP_NCCL(ncclAllReduce(S, S, 2 * n, ncclFloat64, ncclSum, pl->world, stream));
-    GMP_NCCL(ncclAllReduce(F, F, n, ncclUint8, ncclSum, pl->world, stream));
-    GMP_NCCL(ncclGroupEnd());
+    ncclResult_t r = ncclGroupStart();
+    if (r == ncclSuccess) {
+      r = ncclAllReduce(S, S, 2 * n, ncclFloat64, ncclSum, pl->world, stream);
+      if (r == ncclSuccess) r = ncclAllReduce(F, F, n, ncclUint8, ncclSum, pl->world, stream);
+      const ncclResult_t e = ncclGroupEnd();   // always close the group
+      if (r == ncclSuccess) r = e;
+    }
+    if (r != ncclSuccess) return fail(GMP_ERR_NCCL, std::string("tile statistics all-reduce: ") + ncclGetErrorString(r));
   }
   // ---- S2: map finalize ----
   uint8_t* codes = sc + L.codes;
@@ -949,7 +958,8 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
     // codes, scales and status -> mapped host memory by a kernel, then the sync
     const int64_t nall = pl->nA + pl->nB + pl->nC;
     const int64_t o_s5 = align_up(nall, 16), o_scin = o_s5 + align_up((pl->nA + pl->nB) * NC * 2, 16),
-                  o_st = o_scin + align_up(pl->nC * 2, 16), total = o_st + 16;
+                  o_st = o_scin + align_up(pl->nC * 2, 16), o_S = o_st + 16, o_F = o_S + 2 * nall * 8,
+                  total = o_F + align_up(nall, 16);
     Stage* st = stage_acquire((size_t)total);
     if (!st) return fail(GMP_ERR_CUDA, "pinned staging buffer allocation failed");
     k_xfer<<<xfer_grid(nall), 256, 0, stream>>>(codes, st->d, nall);
@@ -957,6 +967,9 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
                                                                  (pl->nA + pl->nB) * NC * 2);
     k_xfer<<<xfer_grid(pl->nC * 2), 256, 0, stream>>>((const uint8_t*)scin, st->d + o_scin, pl->nC * 2);
     k_xfer<<<1, 32, 0, stream>>>((const uint8_t*)status, st->d + o_st, (int64_t)sizeof(int));
+    // the global tile statistics (S, maxabs, finite) too: gemm_mp_get_tile_stats
+    k_xfer<<<xfer_grid(2 * nall * 8), 256, 0, stream>>>((const uint8_t*)S, st->d + o_S, 2 * nall * 8);
+    k_xfer<<<xfer_grid(nall), 256, 0, stream>>>(F, st->d + o_F, nall);
     const cudaError_t e1 = cudaGetLastError();
     const cudaError_t e2 = cudaStreamSynchronize(stream);
     if (e1 == cudaSuccess && e2 == cudaSuccess) {
@@ -967,6 +980,10 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
       std::memcpy(pl->sB5.data(), st->h + o_s5 + pl->nA * NC * 2, pl->nB * NC * 2);
       std::memcpy(pl->sCin.data(), st->h + o_scin, pl->nC * 2);
       std::memcpy(&h_status, st->h + o_st, sizeof(int));
+      pl->statS.resize(2 * nall);
+      pl->statF.resize(nall);
+      std::memcpy(pl->statS.data(), st->h + o_S, 2 * nall * 8);
+      std::memcpy(pl->statF.data(), st->h + o_F, nall);
     }
     stage_release(st, stream);
     GMP_CUDA(e1);
@@ -1018,6 +1035,7 @@ extern "C" gmp_status_t gemm_mp_plan_host(const gmp_desc_t* desc, const uint8_t*
   pl->sCout.assign(pl->nC, 0);
   local_tiles(pl);
   build_tables(pl);
+  pl->host_only = true;
   *out = guard.release();
   return GMP_OK;
 }
@@ -1083,11 +1101,20 @@ static int grid_for(int64_t n_elems, int per_thread) {
 // step_ev[s] gates the step's class launches on the compute stream.
 static gmp_status_t issue_comm_step(gmp_plan_s* pl, uint8_t* ws, int s) {
   const int64_t nb = pl->d.nb;
-  GMP_NCCL(ncclGroupStart());
-  for (const Bcast& b : pl->bcast_step[s])
-    GMP_NCCL(ncclBroadcast(ws + b.off, ws + b.off, (size_t)b.bytes, ncclUint8, b.root,
-                           b.which == 0 ? pl->rowc : pl->colc, pl->comm_stream));
-  GMP_NCCL(ncclGroupEnd());
+  {
+    // the group is always closed, also when a broadcast fails: a thread left inside
+    // ncclGroupStart would silently defer every later NCCL call
+    ncclResult_t r = ncclGroupStart();
+    if (r != ncclSuccess) return fail(GMP_ERR_NCCL, std::string("ncclGroupStart: ") + ncclGetErrorString(r));
+    for (const Bcast& b : pl->bcast_step[s]) {
+      r = ncclBroadcast(ws + b.off, ws + b.off, (size_t)b.bytes, ncclUint8, b.root, b.which == 0 ? pl->rowc : pl->colc,
+                        pl->comm_stream);
+      if (r != ncclSuccess) break;
+    }
+    const ncclResult_t e = ncclGroupEnd();
+    if (r == ncclSuccess) r = e;
+    if (r != ncclSuccess) return fail(GMP_ERR_NCCL, std::string("SUMMA broadcast: ") + ncclGetErrorString(r));
+  }
   GMP_TRY(launch_shadows((const ShadowJob*)(ws + pl->off_shadow) + pl->shadow_step_off[s], pl->shadow_step[s], ws,
                          (int)nb, pl->comm_stream));
   if (!pl->split_step[s].empty()) {
@@ -1106,6 +1133,7 @@ static gmp_status_t issue_comm_step(gmp_plan_s* pl, uint8_t* ws, int s) {
 
 extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_bytes, void* stream_) {
   if (!pl) return fail(GMP_ERR_ARG, "plan is NULL");
+  if (pl->host_only) return fail(GMP_ERR_STATE, "host-built plan (gemm_mp_plan_host): no operands to convert");
   if (!ws_ || (int64_t)ws_bytes < pl->ws_bytes) return fail(GMP_ERR_WORKSPACE, "workspace too small");
   if ((uintptr_t)ws_ & 1023) return fail(GMP_ERR_ARG, "workspace must be 1024-byte aligned");
   cudaStream_t stream = (cudaStream_t)stream_;
@@ -1167,6 +1195,7 @@ extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_byte
 
 extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ldc, void* stream_) {
   if (!pl) return fail(GMP_ERR_ARG, "plan is NULL");
+  if (pl->host_only) return fail(GMP_ERR_STATE, "host-built plan (gemm_mp_plan_host) cannot execute");
   if (!pl->converted) return fail(GMP_ERR_STATE, "execute before convert");
   const int64_t nb = pl->d.nb, nb2 = nb * nb;
   const int64_t nCl = (int64_t)pl->locC.size();
@@ -1310,6 +1339,22 @@ extern "C" gmp_status_t gemm_mp_get_maps(gmp_plan_t pl, uint8_t* a, uint8_t* b, 
       for (size_t k = 0; k < tmp.size(); ++k) cs[pl->locC[k]] = tmp[k];
     }
   }
+  return GMP_OK;
+}
+
+extern "C" gmp_status_t gemm_mp_get_tile_stats(gmp_plan_t pl, char which, double* S, double* maxabs,
+                                               uint8_t* finite) {
+  if (!pl) return fail(GMP_ERR_ARG, "plan is NULL");
+  if (pl->statS.empty()) return fail(GMP_ERR_STATE, "no statistics (host-built plan)");
+  const int64_t nall = pl->nA + pl->nB + pl->nC;
+  int64_t off = 0, n = 0;
+  if (which == 'A') { off = 0; n = pl->nA; }
+  else if (which == 'B') { off = pl->nA; n = pl->nB; }
+  else if (which == 'C') { off = pl->nA + pl->nB; n = pl->nC; }
+  else return fail(GMP_ERR_ARG, "which must be A, B or C");
+  if (S) std::memcpy(S, pl->statS.data() + off, n * 8);
+  if (maxabs) std::memcpy(maxabs, pl->statS.data() + nall + off, n * 8);
+  if (finite) std::memcpy(finite, pl->statF.data() + off, n);
   return GMP_OK;
 }
 

@@ -187,24 +187,27 @@ __global__ void __launch_bounds__(1024) k_map_finalize(FinalizeArgs a) {
   for (int64_t ct = t; ct < nC; ct += nthr) {
     const int64_t i = ct / a.nt, j = ct - (ct / a.nt) * a.nt;
     int chosen = 0;
+    double RA = 0.0, QB = 0.0;
+    for (int64_t l = 0; l < a.kt; ++l) RA = __dadd_rn(RA, a.SA[i * a.kt + l]);
+    for (int64_t l = 0; l < a.kt; ++l) QB = __dadd_rn(QB, a.SB[l * a.nt + j]);
+    RA = __dsqrt_rn(RA);
+    QB = __dsqrt_rn(QB);
+    const double sc = hasC ? a.SC[ct] : 0.0;
+    const double nhat = __dadd_rn(__dmul_rn(__dmul_rn(aa, RA), QB), __dmul_rn(ab, __dsqrt_rn(sc)));
     if (a.explicit_c) {
       chosen = a.mapC[ct];
       if (chosen >= GMP_NCLASS || !(mask & (1u << chosen))) chosen = 0;
     } else {
-      double RA = 0.0, QB = 0.0;
-      for (int64_t l = 0; l < a.kt; ++l) RA = __dadd_rn(RA, a.SA[i * a.kt + l]);
-      for (int64_t l = 0; l < a.kt; ++l) QB = __dadd_rn(QB, a.SB[l * a.nt + j]);
-      RA = __dsqrt_rn(RA);
-      QB = __dsqrt_rn(QB);
-      const double sc = hasC ? a.SC[ct] : 0.0;
-      const double nhat = __dadd_rn(__dmul_rn(__dmul_rn(aa, RA), QB), __dmul_rn(ab, __dsqrt_rn(sc)));
       for (int k = GMP_NCLASS - 1; k >= 1; --k) {
         if (!(mask & (1u << k))) continue;
         const double dC = __dadd_rn(__dadd_rn(class_u(k), __dmul_rn(sqkt, 0x1p-24)),
                                     __ddiv_rn(__dmul_rn((double)a.nb, class_eta(k)), class_omega(k)));
         if (__dmul_rn(dC, nhat) <= rhsC) { chosen = k; break; }
       }
-      // R23: FP32 accumulator range guards
+    }
+    {
+      // R23: FP32 accumulator range guards -- explicit codes included (a binary32 W
+      // cannot hold an output or a fold factor outside its range)
       if (chosen != 0) {
         bool ok = nhat <= 0x1p100;
         if (a.beta != 0.0) {

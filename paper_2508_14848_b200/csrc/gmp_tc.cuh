@@ -208,6 +208,10 @@ __device__ __forceinline__ void tc_epilogue(const WorkItem* __restrict__ items, 
       // binary64 W with BN = 256: read-modify-write per pair (the host prefers
       // BN = 128 for launches that hold binary64 accumulators)
       double* wrow = reinterpret_cast<double*>(ws + ct.w_off) + rowoff;
+      if (w.pad & 1) {   // first tile-GEMM launch of this C tile: W0 from C_in (O9)
+#pragma unroll 1
+        for (int v = 0; v < HC; ++v) wrow[v] = w0_f64(ct, ws, rowoff + v, beta);
+      }
       for (int pi = 0; pi < w.pcnt; ++pi) {
         const PairDesc pd = pairs[w.pbeg + pi];
         const double f64 = ldexp_fast(alpha, pd.fexp);

@@ -122,3 +122,39 @@ def rn32(x: Fraction) -> np.float32:
 
 def gamma(n, u):
     return n * u / (1 - n * u)
+
+
+def nearest_even_vec(bits, vals, x):
+    """Vectorised round-to-nearest-even of the binary64 probes x (finite, |x| <= max
+    representable) over the enumerated value set: the same rule as NearestEven, fast
+    enough for an exhaustive probe set.  The neighbours lo <= |x| <= hi come from a
+    binary search; the distances |x| - lo and hi - |x| are exact in binary64 wherever
+    Sterbenz's lemma applies (lo <= |x| <= 2 lo, |x| <= hi <= 2|x|) -- every probe
+    near a tie; the others are decided by a margin far above rounding error and, if
+    not, by exact rationals.  Returns the bit patterns with the sign bit of x at
+    `sign_shift`."""
+    fin = np.isfinite(vals) & (vals >= 0)
+    v, b = vals[fin], bits[fin].astype(np.int64)
+    order = np.lexsort((b, v))             # ascending value, then the smaller pattern (+0 before -0)
+    v, b = v[order], b[order]
+    keep = np.concatenate([[True], v[1:] != v[:-1]])
+    v, b = v[keep], b[keep]
+    a = np.abs(x)
+    i = np.searchsorted(v, a, side="left")
+    exact_hit = (i < v.size) & (v[np.minimum(i, v.size - 1)] == a)
+    i = np.clip(i, 1, v.size - 1)
+    lo, hi = v[i - 1], v[i]
+    d1, d2 = a - lo, hi - a
+    sterbenz = ((lo == 0) | (a <= 2 * lo)) & (hi <= 2 * a)
+    far = (np.maximum(d1, d2) > 1.01 * np.minimum(d1, d2))
+    pick_hi = (d2 < d1) | ((d1 == d2) & (b[i - 1] % 2 == 1))
+    out = np.where(pick_hi, b[i], b[i - 1])
+    out = np.where(exact_hit, b[np.searchsorted(v, a, side="left").clip(0, v.size - 1)], out)
+    slow = ~exact_hit & ~sterbenz & ~far
+    for k in np.nonzero(slow)[0]:            # exact rationals (rare)
+        fa, flo, fhi = Fraction(float(a[k])), Fraction(float(lo[k])), Fraction(float(hi[k]))
+        if fa - flo < fhi - fa or (fa - flo == fhi - fa and b[i[k] - 1] % 2 == 0):
+            out[k] = b[i[k] - 1]
+        else:
+            out[k] = b[i[k]]
+    return out, int(slow.sum())

@@ -46,31 +46,75 @@ def tol_metric(Cmp, A, Bm, C, alpha, beta):
 
 U_CLASS = [2.0 ** -53, 2.0 ** -24, 2.0 ** -11, 2.0 ** -8, 2.0 ** -4, 2.0 ** -3]
 ETA_CLASS = [2.0 ** -1074, 2.0 ** -149, 2.0 ** -24, 2.0 ** -133, 2.0 ** -9, 2.0 ** -16]
+U32 = 2.0 ** -24
+# a sub-FP32 C element may differ from the oracle's only where W_gpu and W_oracle straddle a
+# rounding boundary of C's class; expected rate ~ |dW| / spacing <~ 0.5 % for FP16
+MAX_FLIP_RATE = 0.02
+
+
+def tile_bound(o, i, j, K):
+    """SURVEY C6 / DESIGN.md 4: 1e-13 when the C tile and every pair folded into it are FP64,
+    else 4 u32 sqrt(K) (relative Frobenius, per C tile)"""
+    allfp64 = o["ccode"][i, j] == 0 and (o["acode"][i, :] == 0).all() and (o["bcode"][:, j] == 0).all()
+    return 1e-13 if allfp64 else 4 * U32 * np.sqrt(K)
+
+
+def gpu_w_tile(g, i, j, code, nb):
+    raw, _ = g.tile("W", i, j, code)
+    return raw.view(np.float64 if code == 0 else np.float32).astype(np.float64).reshape(nb, nb)
+
+
+def w_and_finalize_parity(g, o, Cg, nb, K, bitwise=False):
+    """Per C tile: (1) the GPU's W accumulator vs the oracle's exported W -- bitwise on the
+    SIMT path, else within tile_bound; (2) the GPU's packed C_out, its scale and the user C
+    tile are EXACTLY the oracle's finalize (O9) of the GPU's own W.  Returns the worst
+    relative W error."""
+    worst = 0.0
+    mt, nt = o["ccode"].shape
+    for i in range(mt):
+        for j in range(nt):
+            code = int(o["ccode"][i, j])
+            sl = (slice(i * nb, (i + 1) * nb), slice(j * nb, (j + 1) * nb))
+            Wg, Wo = gpu_w_tile(g, i, j, code, nb), o["W"][sl]
+            if bitwise:
+                assert np.array_equal(Wg, Wo), ("W", i, j)
+            else:
+                den = np.linalg.norm(Wo)
+                rel = np.linalg.norm(Wg - Wo) / den if den > 0 else float(np.abs(Wg).max())
+                assert rel <= tile_bound(o, i, j, K), ("W", i, j, code, rel)
+                worst = max(worst, rel)
+            pay, user, e = oracle.finalize(Wg, code)
+            got, sc = g.tile("C", i, j, code)
+            assert sc == e, ("C scale", i, j, sc, e)
+            assert np.array_equal(got, pay.view(np.uint8)), ("C_out bytes", i, j)
+            assert np.array_equal(Cg[sl], user), ("user C", i, j)
+    return worst
 
 
 def c_parity(Cg, Co, ccode, cscale, nb, K, allfp64):
-    """DESIGN.md section 4 / SURVEY C6: W-level agreement within 1e-13 (all-FP64) or
-    4 u32 sqrt(K) (relative Frobenius) on tiles stored in FP64/FP32; tiles stored
-    below FP32 may in addition differ by the final rounding into C's class: at most
-    one step of that class's grid per element.  Returns (ok, worst relative error)."""
-    bound = 1e-13 if allfp64 else 4 * 2.0 ** -24 * np.sqrt(K)
+    """User C vs the oracle's C per tile (DESIGN.md 4 / SURVEY C6).  Tiles stored in FP64 /
+    FP32: relative Frobenius error <= 1e-13 (all-FP64 runs) or 4 u32 sqrt(K), per tile.
+    Tiles stored below FP32: equal except where the final RN into C's class flips -- at
+    most MAX_FLIP_RATE of the tile's elements, each by one step of that class's grid.
+    Returns (ok, worst relative error of the FP64/FP32 tiles)."""
+    bound = 1e-13 if allfp64 else 4 * U32 * np.sqrt(K)
     mt, nt = ccode.shape
-    num = den = 0.0
-    ok = True
+    ok, worst = True, 0.0
     for i in range(mt):
         for j in range(nt):
             sl = (slice(i * nb, (i + 1) * nb), slice(j * nb, (j + 1) * nb))
             g, o = Cg[sl], Co[sl]
             c = int(ccode[i, j])
             if c <= 1:
-                num += float(((g - o) ** 2).sum())
-                den += float((o ** 2).sum())
+                den = np.linalg.norm(o)
+                rel = np.linalg.norm(g - o) / den if den > 0 else float(np.abs(g).max())
+                worst = max(worst, rel)
+                ok = ok and rel <= bound
             else:
-                # one class step at this magnitude + the W-level tolerance
-                step = 2 * U_CLASS[c] * np.maximum(np.abs(g), np.abs(o)) + ETA_CLASS[c] * 2.0 ** (-int(cscale[i, j]))
-                w_tol = bound * np.linalg.norm(o) + 1e-300
-                excess = np.maximum(np.abs(g - o) - step, 0.0)
-                if np.linalg.norm(excess) > w_tol:
+                diff = g != o
+                if diff.mean() > MAX_FLIP_RATE:
                     ok = False
-    rel = np.sqrt(num / den) if den > 0 else 0.0
-    return ok and rel <= bound, rel
+                step = 2 * U_CLASS[c] * np.maximum(np.abs(g), np.abs(o)) + ETA_CLASS[c] * 2.0 ** (-int(cscale[i, j]))
+                if (np.abs(g - o)[diff] > step[diff]).any():
+                    ok = False
+    return ok, worst

@@ -95,3 +95,24 @@ def test_fused_tensor_launch_plan():
     assert sep["pairs"][:3] == fus["pairs"][:3] == [t * t, 2 * t * t, t * t]
     assert fus["launches_execute"] == sep["launches_execute"] - 1          # one step, FP32 + FP16 fused
     assert list(fus["class_launches"][:3]) == list(sep["class_launches"][:3]) == [1, 1, 1]
+
+
+def test_host_plan_cannot_convert_or_execute():
+    """a gemm_mp_plan_host plan holds no operands / statistics / communicators: convert,
+    execute and the statistics export fail with GMP_ERR_STATE before touching a device
+    (also on a P*Q > 1 grid, where convert would otherwise reach NCCL)"""
+    import numpy as np
+    for P, Q in ((1, 1), (2, 2)):
+        d = B.make_desc(512, 512, 512, 128, 1e-6, P=P, Q=Q, rank=0)
+        c = np.zeros((4, 4), np.uint8)
+        z = np.zeros((4, 4, 6), np.int16)
+        pl = B.gemm_mp_plan_host(d, c, c, c, z, z)
+        try:
+            for call in (lambda: B.gemm_mp_convert(pl, 1024, 1 << 40, None),
+                         lambda: B.gemm_mp_execute(pl, 1024, 512, None),
+                         lambda: B.gemm_mp_get_tile_stats(pl, "A", 4, 4)):
+                with pytest.raises(B.GmpError) as e:
+                    call()
+                assert "GMP_ERR_STATE" in str(e.value)
+        finally:
+            B.gemm_mp_destroy(pl)

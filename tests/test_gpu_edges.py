@@ -225,3 +225,16 @@ def test_extreme_exponents_match_oracle():
     allfp64 = (o["bcode"] == 0).all() and (o["ccode"] == 0).all()
     ok, rel = c_parity(out, o["C"], o["ccode"], o["cscale"], nb, 384, allfp64)
     assert ok, rel
+
+
+def test_explicit_fp32_c_map_at_extreme_scales():
+    """an explicit FP32 c_map on outputs beyond 2^100 (R23) is demoted to FP64
+    on the GPU exactly as in the oracle -- no binary32 overflow in the epilogue"""
+    nb = 128
+    A = np.full((256, 256), 2.0 ** 60); Bm = np.full((256, 256), 2.0 ** 60)
+    maps = (None, None, np.ones((2, 2), np.uint8))
+    o = run_oracle(A, Bm, None, nb, 1e-2, 1.0, 0.0, 0b01111, maps=maps)
+    g, (out,) = run_gpu(A, Bm, None, nb, 1e-2, 1.0, 0.0, 0b01111, maps=maps)
+    assert (o["ccode"] == 0).all() and np.array_equal(g.maps()["ccode"], o["ccode"])
+    assert np.isfinite(out).all()
+    assert np.linalg.norm(out - o["C"]) / np.linalg.norm(o["C"]) <= 1e-13

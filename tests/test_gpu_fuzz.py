@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import gmp_inputs
-from gpu_harness import c_parity, run_gpu, run_oracle, tol_metric
+from gpu_harness import c_parity, run_gpu, run_oracle, tol_metric, w_and_finalize_parity
 from paper_2508_14848_b200 import binding as B
 
 pytestmark = pytest.mark.gpu
@@ -48,3 +48,9 @@ def test_fuzz_parity(seed):
     ok, rel = c_parity(Cg, o["C"], o["ccode"], o["cscale"], w.nb, w.K, allfp64)
     assert ok, (seed, rel)
     assert tol_metric(Cg, A, Bm, Cin, w.alpha, w.beta) <= w.tol, seed
+    # S1 export bitwise (CNORM order), W per tile and the exact finalize of the GPU's W
+    for which, So in (("A", o["SA"]), ("B", o["SB"])):
+        S, _, _ = g.tile_stats(which)
+        assert np.array_equal(S.view(np.uint64), So.view(np.uint64)), (seed, which)
+    w_and_finalize_parity(g, o, Cg, w.nb, w.K)
+    w_and_finalize_parity(gs, o, Cs, w.nb, w.K, bitwise=True)

@@ -8,7 +8,7 @@ import pytest
 
 import gmp_inputs
 import oracle
-from gpu_harness import c_parity, run_gpu, run_oracle, tol_metric
+from gpu_harness import c_parity, run_gpu, run_oracle, tol_metric, w_and_finalize_parity
 from paper_2508_14848_b200 import binding as B
 
 pytestmark = pytest.mark.gpu
@@ -95,7 +95,7 @@ def test_packed_bytes_bitwise(case):
                 assert sc == s5[ti, tj, code]
                 assert np.array_equal(got, stored.view(np.uint8)), (which, ti, tj, code)
                 checked += 1
-                for c in range(code + 1, 5):
+                for c in range(code + 1, B.NCLS):
                     try:
                         got, sc = g.tile(which, ti, tj, c)
                     except B.GmpError:
@@ -105,6 +105,33 @@ def test_packed_bytes_bitwise(case):
                     assert np.array_equal(got, sh.view(np.uint8)), (which, ti, tj, code, c)
                     checked += 1
     assert checked > 0
+
+
+def test_tile_stats_bitwise(case):
+    """S1 debug export: every tile's canonical sum of squares (CNORM, O4), maxabs and
+    finite flag as the GPU map kernel computed them == the oracle's, bitwise"""
+    o, g, w = case["orc"], case["g"], case["w"]
+    for which, So, Mo in (("A", o["SA"], o["MA"]), ("B", o["SB"], o["MB"]), ("C", o["SC"], o["MC"])):
+        S, M, F = g.tile_stats(which)
+        if which == "C" and w.beta == 0.0:
+            assert not S.any() and not M.any()
+            continue
+        assert np.array_equal(S.view(np.uint64), So.view(np.uint64)), which
+        assert np.array_equal(M, Mo), which
+        assert F.all(), which
+
+
+def test_w_and_finalize_product_path(case):
+    """per C tile: GPU W accumulator within the parity bound of the oracle's W, and packed
+    C_out / scale / user C exactly the oracle finalize of the GPU's W"""
+    o, w = case["orc"], case["w"]
+    w_and_finalize_parity(case["g"], o, case["Cg"], w.nb, w.K)
+
+
+def test_w_and_finalize_simt_path_bitwise(case):
+    """SIMT kernels (per-thread sequential k): W is the oracle's, bit for bit"""
+    o, w = case["orc"], case["w"]
+    w_and_finalize_parity(case["gs"], o, case["Cs"], w.nb, w.K, bitwise=True)
 
 
 def test_c_bitwise_on_simt_path(case):

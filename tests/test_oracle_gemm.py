@@ -233,3 +233,64 @@ def test_c_map_closed_form_equal_tiles(k, mask):
             assert (o["ccode"] == k).all(), (k, tol, o["ccode"])
         else:
             assert (o["ccode"] < k).all(), (k, tol, o["ccode"])
+
+
+def test_w_export_consistent_with_finalize():
+    """The W debug export is the accumulator the finalize consumed:
+    re-finalizing each exported tile reproduces the oracle's C tile and scale bitwise,
+    W of a binary32-accumulated tile holds binary32 values, and W of an FP64 C tile is C."""
+    w = gmp_inputs.small_workload(192, 256, 320, 64, 1e-3, mode="random", E=30, beta=0.5,
+                                  class_mask=0b111111, seed=21)
+    A, B, C = w.matrices()
+    o = oracle.gemm_mp(A, B, C, w.nb, w.tol, w.alpha, w.beta, w.class_mask)
+    nb = w.nb
+    assert len(set(np.unique(o["ccode"]))) >= 2
+    for i in range(o["ccode"].shape[0]):
+        for j in range(o["ccode"].shape[1]):
+            code = int(o["ccode"][i, j])
+            sl = (slice(i * nb, (i + 1) * nb), slice(j * nb, (j + 1) * nb))
+            Wt = o["W"][sl]
+            _, user, e = oracle.finalize(Wt, code)
+            assert e == o["cscale"][i, j]
+            assert np.array_equal(user, o["C"][sl])
+            if code == 0:
+                assert np.array_equal(Wt, o["C"][sl])
+            else:
+                assert np.array_equal(Wt.astype(np.float32).astype(np.float64), Wt)
+
+
+@pytest.mark.parametrize("cls", [FP64, FP32, FP16, BF16, E4M3, E5M2])
+def test_w_export_vs_exact_product(cls):
+    """W (before the final rounding into C's class) of one-class explicit maps on
+    non-negative data is alpha A B + beta C within the storage error of A, B, C_in
+    (<= u_cls each) plus binary32 (or binary64) accumulation over K -- independent of
+    the oracle: the reference is numpy's binary64 GEMM."""
+    nb = 32
+    w = gmp_inputs.small_workload(96, 64, 128, nb, 1e-6, mode="uniform", E=0, beta=0.5, seed=12)
+    A, B, C = (np.abs(x) for x in w.matrices())
+    mt, nt, kt = 3, 2, 4
+    maps = dict(a_map=np.full((mt, kt), cls, np.uint8), b_map=np.full((kt, nt), cls, np.uint8),
+                c_map=np.full((mt, nt), cls, np.uint8))
+    o = oracle.gemm_mp(A, B, C, nb, 1e-6, 1.0, 0.5, 0b111111, **maps)
+    ref = A @ B + 0.5 * C
+    u = [2.0 ** -53, 2.0 ** -24, 2.0 ** -11, 2.0 ** -8, 2.0 ** -4, 2.0 ** -3][cls]
+    uacc = 2.0 ** -53 if cls == FP64 else 2.0 ** -24
+    err = np.abs(o["W"] - ref) / ref
+    assert err.max() <= 3 * u + 130 * uacc, err.max()
+
+
+def test_explicit_c_map_keeps_r23_guard():
+    """R23 holds for explicit C codes too: an explicit FP32 c_map on a tile
+    whose output estimate exceeds 2^100 is demoted to FP64 (W = binary64), so the
+    result is not a binary32 overflow"""
+    nb = 32
+    A = np.full((64, 64), 2.0 ** 60); B = np.full((64, 64), 2.0 ** 60)
+    cmap = np.ones((2, 2), np.uint8)
+    o = oracle.gemm_mp(A, B, None, nb, 1e-2, 1.0, 0.0, 0b01111, c_map=cmap)
+    assert (o["ccode"] == 0).all()
+    assert np.isfinite(o["C"]).all()
+    ref = A @ B
+    assert np.linalg.norm(o["C"] - ref) / np.linalg.norm(ref) <= 1e-2
+    # an ordinary explicit FP32 c_map is honoured
+    o2 = oracle.gemm_mp(A / 2.0 ** 60, B / 2.0 ** 60, None, nb, 1e-2, 1.0, 0.0, 0b01111, c_map=cmap)
+    assert (o2["ccode"] == 1).all()
