@@ -93,6 +93,16 @@ typedef enum {
                                  receiver would make); otherwise the stored payload is sent.  Maps,
                                  packed bytes and C are bit-identical to the default receiver-side
                                  mode; only the bytes on NVLink (stats.recv_bytes_local) change.     */
+#define GMP_FLAG_LOOPBACK 256u /* TEST ONLY: the P*Q > 1 exchanges run through an in-process loopback
+                                 transport (gemm_mp_loopback_create) instead of NCCL, so that one process
+                                 can drive all P*Q rank plans of a grid on ONE GPU, one host thread per
+                                 rank (the calls of different ranks meet at host barriers inside plan
+                                 and convert, so they must run concurrently).  The statistics all-reduce
+                                 becomes a rank-order sum of the G contributions (exact: one owner per
+                                 entry) and each SUMMA broadcast one
+                                 device-to-device copy per receiving rank from the root plan's payload
+                                 slot.  Everything else -- maps, slots, receiver-side shadows and
+                                 splits, step events, fold order -- is the NCCL path's code.         */
 
 typedef struct {
   int64_t M, N, K;     /* global GEMM shape                                                    */
@@ -228,6 +238,12 @@ gmp_status_t gemm_mp_get_schedule(gmp_plan_t plan, int32_t step, int64_t *entrie
 gmp_status_t gemm_mp_nccl_unique_id(void *out128);
 gmp_status_t gemm_mp_nccl_comm_create(const void *id128, int nranks, int rank, void **comm);
 gmp_status_t gemm_mp_nccl_comm_destroy(void *comm);
+/* TEST ONLY (GMP_FLAG_LOOPBACK): an in-process transport for nranks (2..16) plans on one
+ * GPU.  Pass it as gemm_mp_plan's nccl_comm with GMP_FLAG_LOOPBACK set in desc.flags.
+ * The caller destroys it after every plan on it is destroyed.  GMP_ERR_ARG for a bad
+ * nranks, GMP_ERR_CUDA if its events cannot be created. */
+gmp_status_t gemm_mp_loopback_create(int nranks, void **comm);
+gmp_status_t gemm_mp_loopback_destroy(void *comm);
 
 /* N1 synthetic generator (benchmark inputs): fills
  * the local block-cyclic part of a rows x cols global matrix.  mode 0 uniform,

@@ -25,6 +25,7 @@ GMP_FLAG_SENDER_SIDE = 16
 GMP_FLAG_TC_PAIR = 32
 GMP_FLAG_TC_MCAST = 64
 GMP_FLAG_TC_FUSED = 128
+GMP_FLAG_LOOPBACK = 256
 STATUS = ["GMP_OK", "GMP_ERR_ARG", "GMP_ERR_NOT_DIVISIBLE", "GMP_ERR_MAP_SHAPE", "GMP_ERR_NONFINITE",
           "GMP_ERR_GRID", "GMP_ERR_WORKSPACE", "GMP_ERR_STATE", "GMP_ERR_CUDA", "GMP_ERR_NCCL",
           "GMP_ERR_UNSUPPORTED"]
@@ -89,6 +90,8 @@ def lib():
             "gemm_mp_nccl_unique_id": [vp],
             "gemm_mp_nccl_comm_create": [vp, ct.c_int, ct.c_int, ct.POINTER(vp)],
             "gemm_mp_nccl_comm_destroy": [vp],
+            "gemm_mp_loopback_create": [ct.c_int, ct.POINTER(vp)],
+            "gemm_mp_loopback_destroy": [vp],
             "gemm_mp_synth": [vp, i64, i64, i64, i32, i32, i32, i32, i32, u64, u64, i32, i32, i32, vp],
             "gemm_mp_plan_host": [ct.POINTER(gmp_desc_t), vp, vp, vp, vp, vp, vp, ct.POINTER(vp)],
             "gemm_mp_get_schedule": [vp, i32, vp, i64, ct.POINTER(i64)],
@@ -223,6 +226,16 @@ def gemm_mp_nccl_comm_create(uid, nranks, rank):
 
 def gemm_mp_nccl_comm_destroy(comm):
     _check(lib().gemm_mp_nccl_comm_destroy(comm))
+
+
+def gemm_mp_loopback_create(nranks):
+    out = ct.c_void_p()
+    _check(lib().gemm_mp_loopback_create(nranks, ct.byref(out)))
+    return out.value
+
+
+def gemm_mp_loopback_destroy(comm):
+    _check(lib().gemm_mp_loopback_destroy(comm))
 
 
 def gemm_mp_synth(out, ld, rows, cols, nb, P, Q, p, q, seed, tau, mode, E, s, stream=None):

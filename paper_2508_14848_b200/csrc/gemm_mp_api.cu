@@ -9,6 +9,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <condition_variable>
 #include <cmath>
 #include <memory>
 #include <mutex>
@@ -244,10 +245,123 @@ struct gmp_plan_s {
   bool converted = false;
   bool executed = false;
   bool host_only = false;   // gemm_mp_plan_host: no operands, no statistics, no communicators
+  struct Loopback* lb = nullptr;   // GMP_FLAG_LOOPBACK: in-process transport (tests only)
   gmp_stats_t st{};
 };
 
 extern "C" const char* gemm_mp_last_error(void) { return g_err.c_str(); }
+
+// ---------------------------------------------------------------------------
+// in-process loopback transport (GMP_FLAG_LOOPBACK; tests only)
+// ---------------------------------------------------------------------------
+// One process drives the P x Q plans of a grid on ONE GPU, one host thread per
+// rank, through the same per-rank calls as the NCCL path.  The two exchanges of
+// the method become: (1) plan's tile-statistics all-reduce -> every rank sums
+// the G contributions in rank order (each entry has one owner, so the sum is
+// exact, as with ncclAllReduce); (2) a SUMMA broadcast of panel tile t at step
+// s -> one cudaMemcpyAsync per receiver, from the root plan's payload slot into
+// the receiver's slot, on the receiver's comm stream after the root's
+// packed event.  Host barriers order the event records before the waits; no
+// kernel ever waits on another, so the G plans cannot deadlock on one device.
+struct Loopback {
+  int G = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  std::vector<gmp_plan_s*> plans;        // by world rank, registered by gemm_mp_plan
+  std::vector<const double*> S;          // all-reduce contributions
+  std::vector<const uint8_t*> F;
+  std::vector<cudaEvent_t> ev, done;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t g = gen;
+    if (++arrived == G) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
+namespace {
+constexpr int LB_MAX = 16;
+struct LbSrc {
+  const double* s[LB_MAX];
+  const uint8_t* f[LB_MAX];
+  int G;
+};
+// sum of the G contributions, rank order (exact: one non-zero term per entry)
+__global__ void k_lb_sum(LbSrc src, double* __restrict__ S, int64_t nS, uint8_t* __restrict__ F, int64_t nF) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = t; i < nS; i += stride) {
+    double a = src.s[0][i];
+    for (int k = 1; k < src.G; ++k) a = __dadd_rn(a, src.s[k][i]);
+    S[i] = a;
+  }
+  for (int64_t i = t; i < nF; i += stride) {
+    unsigned a = 0;
+    for (int k = 0; k < src.G; ++k) a += src.f[k][i];
+    F[i] = (uint8_t)a;
+  }
+}
+}  // namespace
+
+extern "C" gmp_status_t gemm_mp_loopback_create(int nranks, void** comm) {
+  if (!comm || nranks < 2 || nranks > LB_MAX) return fail(GMP_ERR_ARG, "loopback: 2 <= nranks <= 16");
+  auto lb = new Loopback();
+  lb->G = nranks;
+  lb->plans.assign(nranks, nullptr);
+  lb->S.assign(nranks, nullptr);
+  lb->F.assign(nranks, nullptr);
+  lb->ev.assign(nranks, nullptr);
+  lb->done.assign(nranks, nullptr);
+  for (int r = 0; r < nranks; ++r) {
+    if (cudaEventCreateWithFlags(&lb->ev[r], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&lb->done[r], cudaEventDisableTiming) != cudaSuccess) {
+      delete lb;
+      return fail(GMP_ERR_CUDA, "loopback: event creation failed");
+    }
+  }
+  *comm = lb;
+  return GMP_OK;
+}
+
+extern "C" gmp_status_t gemm_mp_loopback_destroy(void* comm) {
+  auto lb = (Loopback*)comm;
+  if (!lb) return GMP_OK;
+  for (auto e : lb->ev) if (e) cudaEventDestroy(e);
+  for (auto e : lb->done) if (e) cudaEventDestroy(e);
+  delete lb;
+  return GMP_OK;
+}
+
+// plan's all-reduce of the tile statistics (S: nS doubles, F: nF bytes), in place
+static gmp_status_t lb_allreduce(Loopback* lb, int rank, double* S, int64_t nS, uint8_t* F, int64_t nF,
+                                 cudaStream_t stream) {
+  lb->S[rank] = S;
+  lb->F[rank] = F;
+  GMP_CUDA(cudaEventRecord(lb->ev[rank], stream));
+  lb->barrier();                                   // every contribution's event is recorded
+  for (int k = 0; k < lb->G; ++k) GMP_CUDA(cudaStreamWaitEvent(stream, lb->ev[k], 0));
+  void* tmp = nullptr;
+  GMP_CUDA(cudaMallocAsync(&tmp, (size_t)(nS * 8 + nF), stream));
+  LbSrc src{};
+  src.G = lb->G;
+  for (int k = 0; k < lb->G; ++k) { src.s[k] = lb->S[k]; src.f[k] = lb->F[k]; }
+  k_lb_sum<<<148, 256, 0, stream>>>(src, (double*)tmp, nS, (uint8_t*)tmp + nS * 8, nF);
+  GMP_CUDA(cudaGetLastError());
+  GMP_CUDA(cudaEventRecord(lb->done[rank], stream));
+  lb->barrier();                                   // every rank has read every contribution
+  for (int k = 0; k < lb->G; ++k) GMP_CUDA(cudaStreamWaitEvent(stream, lb->done[k], 0));
+  GMP_CUDA(cudaMemcpyAsync(S, tmp, (size_t)(nS * 8), cudaMemcpyDeviceToDevice, stream));
+  GMP_CUDA(cudaMemcpyAsync(F, (uint8_t*)tmp + nS * 8, (size_t)nF, cudaMemcpyDeviceToDevice, stream));
+  GMP_CUDA(cudaFreeAsync(tmp, stream));
+  lb->barrier();                                   // events may be re-recorded by a later call
+  return GMP_OK;
+}
 
 // Row / column communicators are split once per (world communicator, grid) and
 // reused by every plan on it (ncclCommSplit is a collective costing milliseconds);
@@ -393,6 +507,9 @@ static void build_tables(gmp_plan_s* pl) {
     if (!root && pl->wireA[g] != (1u << pl->codeA[g]))
       for (int c = 0; c < NC; ++c) needA[g * NC + c] = 0;
     for (int c = 0; c < NC; ++c) if (pl->wireA[g] >> c & 1) needA[g * NC + c] = 1;
+    // the owner packs its stored payload (and makes the wire shadows from it) even when
+    // none of its own tile-GEMMs uses the stored class (e.g. a rank without C tiles)
+    if (root) needA[g * NC + pl->codeA[g]] = 1;
   }
   for (int64_t g = 0; g < pl->nB; ++g) {
     if ((g % nt) % Q != q) continue;
@@ -400,6 +517,7 @@ static void build_tables(gmp_plan_s* pl) {
     if (!root && pl->wireB[g] != (1u << pl->codeB[g]))
       for (int c = 0; c < NC; ++c) needB[g * NC + c] = 0;
     for (int c = 0; c < NC; ++c) if (pl->wireB[g] >> c & 1) needB[g * NC + c] = 1;
+    if (root) needB[g * NC + pl->codeB[g]] = 1;
   }
 
   // ---- arena slots ----
@@ -914,7 +1032,12 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
     GMP_CUDA(cudaGetLastError());
   }
   // ---- multi-GPU: every tile's stats owned by exactly one rank -> sum-allreduce is exact ----
-  if (G > 1) {
+  const bool loop = (d.flags & GMP_FLAG_LOOPBACK) != 0;
+  if (loop && G > 1) {
+    pl->lb = (Loopback*)nccl_comm;
+    if (pl->lb->G != G) return fail(GMP_ERR_GRID, "loopback transport size != P*Q");
+    GMP_TRY(lb_allreduce(pl->lb, d.rank, S, 2 * n, F, n, stream));
+  } else if (G > 1) {
     pl->world = (ncclComm_t)nccl_comm;
     ncclResult_t r = ncclGroupStart();
     if (r == ncclSuccess) {
@@ -990,7 +1113,9 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
     GMP_CUDA(e2);
   }
   if (h_status == 4) return fail(GMP_ERR_NONFINITE, "A, B or C holds a NaN or an infinity");
-  if (G > 1) {
+  if (pl->lb) {
+    GMP_CUDA(cudaStreamCreateWithFlags(&pl->comm_stream, cudaStreamNonBlocking));   // owned by the plan
+  } else if (G > 1) {
     GridComms gc{};
     GMP_TRY(grid_comms(pl->world, d.P, d.Q, pl->p, pl->q, &gc));
     pl->rowc = gc.rowc;
@@ -1003,6 +1128,10 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
   if (d.flags & GMP_FLAG_TIMING) {
     pl->launch_ev.resize(2 * pl->launches.size());
     for (auto& e : pl->launch_ev) GMP_CUDA(cudaEventCreate(&e));
+  }
+  if (pl->lb) {
+    std::lock_guard<std::mutex> lk(pl->lb->mu);
+    pl->lb->plans[d.rank] = pl;
   }
   *out = guard.release();
   return GMP_OK;
@@ -1101,7 +1230,22 @@ static int grid_for(int64_t n_elems, int per_thread) {
 // step_ev[s] gates the step's class launches on the compute stream.
 static gmp_status_t issue_comm_step(gmp_plan_s* pl, uint8_t* ws, int s) {
   const int64_t nb = pl->d.nb;
-  {
+  if (pl->lb) {
+    // loopback: each receiver copies the root's payload slot (the root sends nothing)
+    int last_root = -1;
+    for (const Bcast& b : pl->bcast_step[s]) {
+      const int root = b.which == 0 ? pl->p * pl->Q + b.root : b.root * pl->Q + pl->q;
+      if (root == pl->d.rank) continue;
+      const gmp_plan_s* rp = pl->lb->plans[root];
+      if (!rp || !rp->ws || !rp->packed_ev) return fail(GMP_ERR_STATE, "loopback: root plan not converted");
+      const int32_t slot = (b.which == 0 ? rp->slotA5 : rp->slotB5)[b.tile * NC + b.cls];
+      if (slot < 0) return fail(GMP_ERR_STATE, "loopback: root holds no slot for a broadcast tile");
+      if (root != last_root) GMP_CUDA(cudaStreamWaitEvent(pl->comm_stream, rp->packed_ev, 0));
+      last_root = root;
+      const uint8_t* src = rp->ws + rp->arena_off[b.cls] + (int64_t)slot * rp->slot_bytes[b.cls];
+      GMP_CUDA(cudaMemcpyAsync(ws + b.off, src, (size_t)b.bytes, cudaMemcpyDeviceToDevice, pl->comm_stream));
+    }
+  } else {
     // the group is always closed, also when a broadcast fails: a thread left inside
     // ncclGroupStart would silently defer every later NCCL call
     ncclResult_t r = ncclGroupStart();
@@ -1175,6 +1319,7 @@ extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_byte
   if (pl->P * pl->Q > 1 && pl->st.steps > 0) {
     if (!pl->packed_ev) GMP_CUDA(cudaEventCreateWithFlags(&pl->packed_ev, cudaEventDisableTiming));
     GMP_CUDA(cudaEventRecord(pl->packed_ev, stream));
+    if (pl->lb) pl->lb->barrier();   // every root's packed event is recorded before any receiver waits
     GMP_CUDA(cudaStreamWaitEvent(pl->comm_stream, pl->packed_ev, 0));
     GMP_TRY(issue_comm_step(pl, ws, 0));
     pl->step0_issued = true;
@@ -1481,5 +1626,12 @@ extern "C" void gemm_mp_destroy(gmp_plan_t pl) {
   if (pl->packed_ev) cudaEventDestroy(pl->packed_ev);
   for (auto& e : pl->launch_ev) if (e) cudaEventDestroy(e);
   tc_release(pl->tc);
+  if (pl->lb) {
+    {
+      std::lock_guard<std::mutex> lk(pl->lb->mu);
+      if (pl->lb->plans[pl->d.rank] == pl) pl->lb->plans[pl->d.rank] = nullptr;
+    }
+    if (pl->comm_stream) cudaStreamDestroy(pl->comm_stream);
+  }
   delete pl;
 }

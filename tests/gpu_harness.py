@@ -94,8 +94,14 @@ def w_and_finalize_parity(g, o, Cg, nb, K, bitwise=False):
 def c_parity(Cg, Co, ccode, cscale, nb, K, allfp64):
     """User C vs the oracle's C per tile (DESIGN.md 4 / SURVEY C6).  Tiles stored in FP64 /
     FP32: relative Frobenius error <= 1e-13 (all-FP64 runs) or 4 u32 sqrt(K), per tile.
-    Tiles stored below FP32: equal except where the final RN into C's class flips -- at
-    most MAX_FLIP_RATE of the tile's elements, each by one step of that class's grid.
+    Tiles stored below FP32 (class c, scale e): C = RN_c(W 2^e) 2^-e on both sides, so
+    ||C_g - C_o|| <= ||C_g - W_g|| + ||W_g - W_o|| + ||W_o - C_o||
+                 <= (4 u32 sqrt(K) + 2 u_c) ||C_o|| + nb eta_c 2^-e   (per tile),
+    and the final RN may flip at most MAX_FLIP_RATE of the tile's elements.  (SURVEY C6's
+    "<= 1 ulp of C's class per element" does not hold for an element whose W cancels to
+    far below the tile's magnitude: there |dW| alone exceeds that element's ulp; DESIGN.md
+    reading R29.  Each GPU C element is checked exactly against the finalize of the GPU's
+    own W in w_and_finalize_parity.)
     Returns (ok, worst relative error of the FP64/FP32 tiles)."""
     bound = 1e-13 if allfp64 else 4 * U32 * np.sqrt(K)
     mt, nt = ccode.shape
@@ -105,16 +111,16 @@ def c_parity(Cg, Co, ccode, cscale, nb, K, allfp64):
             sl = (slice(i * nb, (i + 1) * nb), slice(j * nb, (j + 1) * nb))
             g, o = Cg[sl], Co[sl]
             c = int(ccode[i, j])
+            den = np.linalg.norm(o)
+            err = np.linalg.norm(g - o)
             if c <= 1:
-                den = np.linalg.norm(o)
-                rel = np.linalg.norm(g - o) / den if den > 0 else float(np.abs(g).max())
+                rel = err / den if den > 0 else float(np.abs(g).max())
                 worst = max(worst, rel)
                 ok = ok and rel <= bound
             else:
-                diff = g != o
-                if diff.mean() > MAX_FLIP_RATE:
+                if (g != o).mean() > MAX_FLIP_RATE:
                     ok = False
-                step = 2 * U_CLASS[c] * np.maximum(np.abs(g), np.abs(o)) + ETA_CLASS[c] * 2.0 ** (-int(cscale[i, j]))
-                if (np.abs(g - o)[diff] > step[diff]).any():
+                lim = (bound + 2 * U_CLASS[c]) * (1 + 2 * U_CLASS[c]) * den + nb * ETA_CLASS[c] * 2.0 ** (-int(cscale[i, j]))
+                if err > lim:
                     ok = False
     return ok, worst
