@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--no-peaks", action="store_true", help="skip the in-run library peak measurement")
     ap.add_argument("--no-fp64-baseline", action="store_true", help="skip the all-FP64 (100D:0S) leg")
     ap.add_argument("--cpu-threads", type=int, default=0, help="oracle threads (0: min(16, cores))")
+    ap.add_argument("--flags", type=int, default=0, help="extra GMP_FLAG_* bits (A/B runs)")
     ap.add_argument("--size", type=int, default=0, help="override M=N=K (keeps the config's recipe)")
     ap.add_argument("--sender", action="store_true",
                     help="GMP_FLAG_SENDER_SIDE: hybrid sender-side conversion of SUMMA panels (NEXT-2)")
@@ -542,7 +543,7 @@ def main():
     ldc = Cout.stride(0)
     torch.cuda.synchronize()
 
-    flags = B.GMP_FLAG_TIMING | (B.GMP_FLAG_SENDER_SIDE if a.sender else 0)
+    flags = B.GMP_FLAG_TIMING | (B.GMP_FLAG_SENDER_SIDE if a.sender else 0) | a.flags
     desc = B.make_desc(w.M, w.N, w.K, w.nb, w.tol, w.alpha, w.beta, w.class_mask, flags, P, Q, rank)
     nscr = B.gemm_mp_scratch_size(desc)
     scratch = torch.empty(nscr, dtype=torch.uint8, device=dev)

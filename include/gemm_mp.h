@@ -69,10 +69,14 @@ typedef enum {
                                  per element, 28 tcgen05 kind::i8 MMAs) instead of DMMA (default)    */
 #define GMP_FLAG_FP32_FFMA 4u /* FP32 class on the FP32 pipe (packed FFMA2, bitwise O8) instead of the
                                  default tensor-pipe path (exact BF16x3 split, nine BF16 MMAs per block) */
-#define GMP_FLAG_TC_PAIR 32u /* FP16/BF16/E4M3 launches whose C tiles fold into binary32 W and whose
-                                 nb is a multiple of 256 run on SM pairs (tcgen05 cta_group::2, 256 x 256
-                                 sub-tiles, half the B bytes per SM).  Opt-in: under the board power
-                                 cap it measured 4-8 % slower than the 1-SM kernel    */
+#define GMP_FLAG_TC_PAIR 32u /* opt-in: FP16/BF16/E4M3/E5M2 launches whose C tiles fold into binary32 W
+                                 and whose nb is a multiple of 256 run on SM pairs (tcgen05 cta_group::2,
+                                 256 x 256 sub-tiles, half the B bytes per SM), rastered by C tile row
+                                 bands.  Faster alone (all-BF16 32768^3: 1107 vs 1035 TF/s under the
+                                 power cap) but slower inside the cfg3 step (702 vs 790 TF/s: the
+                                 later FP32-class launches run at a lower clock), DESIGN.md 7.       */
+#define GMP_FLAG_TC_SINGLE 512u /* the 1-SM 128 x 256 kernel for those launches (the default; the flag
+                                 makes the choice explicit and overrides GMP_FLAG_TC_PAIR)          */
 #define GMP_FLAG_TC_MCAST 64u /* same launches as GMP_FLAG_TC_PAIR, but each SM keeps its own 1-SM MMA
                                  (M = 128) and only the B box is split and multicast across a 2-CTA
                                  cluster (a third fewer L2->SM bytes, no cross-SM operand reads)     */

@@ -151,6 +151,13 @@ struct Upload {
 // FP16/BF16/E4M3 payloads are K-major (A row-major, B column-major) for the
 // tcgen05 descriptors.  role 0 = A, 1 = B.  Returns 1 if element (r,c) of the
 // tile is stored at c*nb + r.
+// 16/8-bit classes folding into binary32 W on 256-multiple tiles run on SM pairs
+// (k_tc2_class, cta_group::2) under GMP_FLAG_TC_PAIR (opt-in: slower than the 1-SM
+// kernel in the power-capped cfg3 step)
+static inline bool pair_default(uint32_t flags) {
+  return (flags & GMP_FLAG_TC_PAIR) && !(flags & GMP_FLAG_TC_SINGLE);
+}
+
 static inline int16_t layout_transposed(int role, int cls) {
   const bool mn = cls <= 1;
   return (int16_t)(role == 0 ? mn : !mn);
@@ -167,6 +174,7 @@ struct Launch {
                         // launch (k_tc_fused; cls = 1, the classes are in `present`)
   int64_t ibeg, icount;
   int bn;  // N of the class kernel's CTA tile
+  int64_t obeg = -1;     // kind 5: first entry of the launch's raster order (gmp_plan_s::order), -1: none
   unsigned present = 0;  // kind 7: bit c set for each class c with pairs in the launch
   double share[GMP_NCLASS] = {};  // kind 7: estimated share of the launch time per class
                                   // (MMA issue cycles; GMP_FLAG_TIMING attribution)
@@ -231,12 +239,14 @@ struct gmp_plan_s {
   std::vector<CTileDesc> ctd;
   std::vector<WorkItem> items;
   std::vector<PairDesc> pairs;
+  std::vector<int32_t> order;            // raster orders of the SM-pair launches (flat -> item * S + sub)
   std::vector<Launch> launches;
   std::vector<int32_t> acc_init_idx;      // local C tiles whose W0 k_acc_init writes (the others: their
                                           // first tile-GEMM launch, WorkItem.pad bit 0)
   int64_t off_accinit = 0;
   std::vector<int64_t> shadow_step_off;   // element offset of each step's shadow jobs
   // workspace layout (byte offsets)
+  int64_t off_order = 0;
   int64_t off_pack = 0, off_shadow = 0, off_ctd = 0, off_items = 0, off_pairs = 0, off_maxbits = 0,
           off_cscale = 0, off_tc = 0, ws_bytes = 0;
   TcTables tc;
@@ -558,6 +568,7 @@ static void build_tables(gmp_plan_s* pl) {
   pl->pairs.clear();
   pl->items.clear();
   pl->launches.clear();
+  pl->order.clear();
   const int steps = (int)((kt + GMP_STEP_DEPTH - 1) / GMP_STEP_DEPTH);
   // arena offsets are needed before the pairs: finish the layout first
   int64_t o = 0;
@@ -591,6 +602,8 @@ static void build_tables(gmp_plan_s* pl) {
   pl->off_ctd = o; o = align_up(o + nCl * (int64_t)sizeof(CTileDesc), 1024);
   pl->off_items = o; o = align_up(o + n_items * (int64_t)sizeof(WorkItem), 1024);
   pl->off_pairs = o; o = align_up(o + n_pairs * (int64_t)sizeof(PairDesc), 1024);
+  // raster orders of SM-pair launches: at most one entry per (item, 256 x 256 sub-tile)
+  pl->off_order = o; o = align_up(o + n_items * (nb / 128) * (nb / 128) * 4, 1024);
   pl->off_maxbits = o; o = align_up(o + nCl * 8, 1024);
   pl->off_accinit = o; o = align_up(o + nCl * 4, 1024);
   pl->off_cscale = o; o = align_up(o + nCl * 2, 1024);
@@ -788,8 +801,41 @@ static void build_tables(gmp_plan_s* pl) {
         pd.b_off = pl->arena_off[GMP_AR_SPLIT] + (int64_t)pd.b_slot * pl->slot_bytes[GMP_AR_SPLIT];
       }
       pd.cls = c;
+#ifdef GMP_EXPERIMENTS   // power experiments only (exp/ builds): every pair reads the same operand slots
+      if (getenv("GMP_EXP_SAME_SLOT")) { pd.a_slot = 0; pd.b_slot = 0; }
+#endif
       pl->pairs.push_back(pd);
     }
+  };
+  // L2 raster of a tensor-core launch: C tile row bands in turn (snaking),
+  // inside a band the sub-columns of its C tiles left to right, each top to bottom, so
+  // the CTAs running at one time share one A row band and a window of about one B tile
+  // per pair l.  Appends the launch's flat -> (item * S + sub) table to pl->order and
+  // returns its first entry (sub = r * nsub_n + c, the kernels' expand_item numbering);
+  // -1 when off.  Used by the SM-pair launches (+5 % there); the 1-SM launches keep their
+  // item-major order unless GMP_RASTER=1 (measured neutral for BF16 and 7 % slower for the
+  // FP32 split kernel in the cfg3 step).
+  static const int raster_env = getenv("GMP_RASTER") ? atoi(getenv("GMP_RASTER")) : -1;
+  auto raster = [&](const std::vector<WorkItem>& its, int nsub_m, int nsub_n, bool pair_launch) -> int64_t {
+    if (raster_env == 0 || (raster_env < 0 && !pair_launch)) return -1;
+    const int S = nsub_m * nsub_n;
+    std::vector<int32_t> qs(its.size());
+    for (size_t q = 0; q < qs.size(); ++q) qs[q] = (int32_t)q;
+    auto band = [&](int32_t q) { return (uint32_t)pl->ctd[its[q].ctile].pad >> 16; };
+    auto col = [&](int32_t q) { return pl->ctd[its[q].ctile].pad & 0xFFFF; };
+    std::stable_sort(qs.begin(), qs.end(), [&](int32_t a, int32_t b) {
+      if (band(a) != band(b)) return band(a) < band(b);
+      return (band(a) & 1) ? col(a) > col(b) : col(a) < col(b);
+    });
+    const int64_t obeg = (int64_t)pl->order.size();
+    for (int32_t q : qs) {
+      const bool rev = band(q) & 1;
+      for (int c0 = 0; c0 < nsub_n; ++c0) {
+        const int c = rev ? nsub_n - 1 - c0 : c0;
+        for (int r = 0; r < nsub_m; ++r) pl->order.push_back(q * S + r * nsub_n + c);
+      }
+    }
+    return obeg;
   };
   const bool tc_on = kTcAvailable && !(d.flags & GMP_FLAG_SIMT_ONLY);
   for (int s = 0; s < steps; ++s) {
@@ -863,7 +909,14 @@ static void build_tables(gmp_plan_s* pl) {
         its.push_back(WorkItem{(int32_t)k, 0, 0, (int32_t)pbeg, (int32_t)pcnt, 0});
       }
       if (its.empty()) continue;
-      std::stable_sort(its.begin(), its.end(), [](const WorkItem& a, const WorkItem& b) { return a.pcnt > b.pcnt; });
+      // SM-pair launches (below) are rastered by C tile row bands instead
+      bool w64i = false;
+      for (const WorkItem& wi : its) w64i = w64i || pl->ctd[wi.ctile].code == 0;
+      const bool rastered = tc_on && c >= 1 &&
+                            (raster_env > 0 || (raster_env < 0 && c >= 2 && !w64i && nb % 256 == 0 &&
+                                                pair_default(d.flags)));
+      if (!rastered)
+        std::stable_sort(its.begin(), its.end(), [](const WorkItem& a, const WorkItem& b) { return a.pcnt > b.pcnt; });
       pl->items.insert(pl->items.end(), its.begin(), its.end());
       const bool split = (c == 1 && pl->fp32_tc), ozaki = (c == 0 && pl->fp64_tc);
       const int kind = ozaki ? 4 : split ? 3 : tc ? 1 : (c == 0 && (d.flags & GMP_FLAG_SIMT_ONLY)) ? 2 : 0;
@@ -874,16 +927,19 @@ static void build_tables(gmp_plan_s* pl) {
       const int tcbn = (w64 ? 128 : tc_bn((int)nb));
       // GMP_FLAG_TC_PAIR: 16-bit / 8-bit classes folding into binary32 W on
       // 256-multiple tiles run on SM pairs (k_tc2_class, cta_group::2)
-      const bool pair = tc && !w64 && c >= 2 && (nb % 256 == 0) && (d.flags & GMP_FLAG_TC_PAIR);
+      const bool pair = tc && !w64 && c >= 2 && (nb % 256 == 0) && pair_default(d.flags);
       const bool mcast = tc && !w64 && c >= 2 && (nb % 256 == 0) && (d.flags & GMP_FLAG_TC_MCAST) && !pair;
       if (pair || mcast) {
-        pl->launches.push_back(Launch{s, c, pair ? 5 : 6, ibeg, (int64_t)its.size() * tc2_subtiles_per_item((int)nb),
-                                      TC2_BN});
+        Launch L{s, c, pair ? 5 : 6, ibeg, (int64_t)its.size() * tc2_subtiles_per_item((int)nb), TC2_BN};
+        if (pair) L.obeg = raster(its, (int)(nb / 256), (int)(nb / 256), true);
+        pl->launches.push_back(L);
         continue;
       }
       // flat launch size: items x sub-tiles of the class kernel's CTA tile
       const int bn = ozaki ? OZ_BN : split ? 128 : tc ? tcbn : (c == 0 && kind == 0) ? DMMA_BN : mn_bn(c);
-      pl->launches.push_back(Launch{s, c, kind, ibeg, (int64_t)its.size() * subtiles_per_item((int)nb, bn), bn});
+      Launch L{s, c, kind, ibeg, (int64_t)its.size() * subtiles_per_item((int)nb, bn), bn};
+      if (kind == 1 || kind == 3) L.obeg = raster(its, (int)(nb / 128), (int)(nb / bn), false);
+      pl->launches.push_back(L);
     }
   }
 
@@ -898,7 +954,7 @@ static void build_tables(gmp_plan_s* pl) {
       const Launch& L = pl->launches[li];
       if (L.step != 0) break;
       const int64_t iend = li + 1 < pl->launches.size() ? pl->launches[li + 1].ibeg : (int64_t)pl->items.size();
-      const bool can = L.kind == 1 || L.kind == 3 || L.kind == 7;
+      const bool can = L.kind == 1 || L.kind == 3 || L.kind == 5 || L.kind == 7;
       for (int64_t q = L.ibeg; q < iend; ++q) {
         WorkItem& wi = pl->items[q];
         if (done[wi.ctile]) continue;
@@ -1298,6 +1354,7 @@ extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_byte
   tables.add(ws + pl->off_shadow, allsh.data(), (int64_t)(allsh.size() * sizeof(ShadowJob)));
   tables.add(ws + pl->off_items, pl->items.data(), (int64_t)(pl->items.size() * sizeof(WorkItem)));
   tables.add(ws + pl->off_pairs, pl->pairs.data(), (int64_t)(pl->pairs.size() * sizeof(PairDesc)));
+  tables.add(ws + pl->off_order, (const uint8_t*)pl->order.data(), (int64_t)(pl->order.size() * 4));
   tables.add(ws + pl->off_split, allsp.data(), (int64_t)(allsp.size() * sizeof(SplitJob)));
   tables.add(ws + pl->off_slice, allsl.data(), (int64_t)(allsl.size() * sizeof(SliceJob)));
   GMP_TRY(tables.run(stream));
@@ -1403,14 +1460,15 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
         const cudaError_t e = oz_launch(pl->oz, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, pl->off_oexp, stream);
         if (e != cudaSuccess) return fail(GMP_ERR_CUDA, std::string("k_tc_fp64 launch: ") + cudaGetErrorString(e));
       } else if (L.kind == 5) {
-        GMP_TRY(tc2_launch(pl->tc, L.cls, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, stream));
+        GMP_TRY(tc2_launch(pl->tc, L.cls, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, pl->d.beta,
+                           L.obeg >= 0 ? (const int32_t*)(ws + pl->off_order) + L.obeg : nullptr, stream));
       } else if (L.kind == 6) {
         GMP_TRY(tcmc_launch(pl->tc, L.cls, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, stream));
       } else if (L.kind == 7) {
         GMP_TRY(tcf_launch(pl->tc, L.present, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, pl->d.beta, stream));
       } else if (L.kind == 1 || L.kind == 3) {
         GMP_TRY(tc_launch(pl->tc, L.kind == 3 ? TC_SPLIT : L.cls, L.bn, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha,
-                          pl->d.beta, stream));
+                          pl->d.beta, L.obeg >= 0 ? (const int32_t*)(ws + pl->off_order) + L.obeg : nullptr, stream));
       } else {
         switch (L.cls) {
           case 0:

@@ -35,8 +35,10 @@ struct WorkItem {
 // The host lists one WorkItem per (C tile, pair list); a launch covers
 // items x S sub-tiles (S = (nb/128) * (nb/bn)).  Flat index -> item + sub-tile,
 // consecutive flat indices walk the n-blocks of one 128-row band (A panel reuse).
-__device__ __forceinline__ WorkItem expand_item(const WorkItem* __restrict__ items, int64_t flat, int nb, int bn) {
+__device__ __forceinline__ WorkItem expand_item(const WorkItem* __restrict__ items, int64_t flat, int nb, int bn,
+                                                const int32_t* __restrict__ order = nullptr) {
   const int nbn = nb / bn, S = (nb / 128) * nbn;
+  if (order) flat = order[flat];   // host raster (C tile row bands, sub-columns)
   const int64_t idx = flat / S;
   const int sub = (int)(flat - idx * S);
   WorkItem w = items[idx];

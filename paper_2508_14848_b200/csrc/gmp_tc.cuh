@@ -118,7 +118,7 @@ __device__ __forceinline__ void tc_epilogue(const WorkItem* __restrict__ items, 
                                             const PairDesc* __restrict__ pairs, const CTileDesc* __restrict__ ctiles,
                                             uint8_t* __restrict__ ws, int nb, double alpha, double beta,
                                             uint32_t tmem_base, uint64_t* tfull, uint64_t* tempty, int warp,
-                                            int lane) {
+                                            int lane, const int32_t* __restrict__ order = nullptr) {
   // epilogue: 8 warps; warp w reads TMEM lanes 32*(w%4)..+31 (= tile rows) and
   // half (w-2)/4 of the BN columns.  binary32 W: the W row segment lives in
   // registers for the whole item (one read + one write per item instead of
@@ -129,7 +129,7 @@ __device__ __forceinline__ void tc_epilogue(const WorkItem* __restrict__ items, 
   int acc = 0;
   uint32_t acc_phase = 0;
   for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
-    const WorkItem w = expand_item(items, it, nb, BN);
+    const WorkItem w = expand_item(items, it, nb, BN, order);
     const CTileDesc ct = ctiles[w.ctile];
     const int64_t rowoff = (int64_t)(w.m0 + rloc) * nb + w.n0 + half * HC;
     if (ct.code != 0) {
@@ -153,11 +153,15 @@ __device__ __forceinline__ void tc_epilogue(const WorkItem* __restrict__ items, 
         const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + half * HC);
 #pragma unroll
         for (int ch = 0; ch < HC / 16; ++ch) {
+#ifdef GMP_EXP_NOEPI   // power experiments only (exp/ builds): no TMEM read, no fold
+          if (f32 == 12345.0f) accr[ch] += 1.0f;
+#else
           uint32_t r[16];
           tmem_ld16_nowait(tbase + ch * 16, r);
           tmem_wait_ld();
 #pragma unroll
           for (int v = 0; v < 16; ++v) accr[ch * 16 + v] = __fmaf_rn(f32, __uint_as_float(r[v]), accr[ch * 16 + v]);
+#endif
         }
         tc_fence_before();
         __syncwarp();
@@ -259,7 +263,8 @@ template <int C, int BN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const WorkItem* __restrict__ items, int64_t nitems, const PairDesc* __restrict__ pairs,
-           const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha, double beta) {
+           const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha, double beta,
+           const int32_t* __restrict__ order) {
   constexpr int NP = tc_np<C>(), ST = tc_stages<C>();
   constexpr int ESZ = (C == 4 || C == 5) ? 1 : 2;
   constexpr int BK = 128 / ESZ;            // elements per 128-byte K block
@@ -300,7 +305,7 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
-        const WorkItem w = expand_item(items, it, nb, BN);
+        const WorkItem w = expand_item(items, it, nb, BN, order);
         for (int pi = 0; pi < w.pcnt; ++pi) {
           const PairDesc pd = pairs[w.pbeg + pi];
           for (int kb = 0; kb < kblocks; ++kb) {
@@ -323,7 +328,7 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
       for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
-        const WorkItem w = expand_item(items, it, nb, BN);
+        const WorkItem w = expand_item(items, it, nb, BN, order);
         for (int pi = 0; pi < w.pcnt; ++pi) {
           mbar_wait(&tempty[acc], acc_phase ^ 1);
           tc_fence_after();
@@ -352,7 +357,7 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
       }
     }
   } else {
-    tc_epilogue<BN>(items, nitems, pairs, ctiles, ws, nb, alpha, beta, tmem_base, tfull, tempty, warp, lane);
+    tc_epilogue<BN>(items, nitems, pairs, ctiles, ws, nb, alpha, beta, tmem_base, tfull, tempty, warp, lane, order);
   }
   tc_fence_before();
   __syncthreads();
@@ -434,7 +439,7 @@ inline gmp_status_t tc_prepare(TcTables& t, uint8_t* ws, const int64_t* arena_of
 
 template <int C, int BN>
 inline gmp_status_t tc_launch_t(TcTables& t, const WorkItem* it, int64_t n, const PairDesc* pd, const CTileDesc* ct,
-                                uint8_t* ws, int nb, double alpha, double beta, cudaStream_t s) {
+                                uint8_t* ws, int nb, double alpha, double beta, const int32_t* order, cudaStream_t s) {
   constexpr int smem = tc_smem_bytes<C, BN>();
   if (ensure_max_smem(k_tc_class<C, BN>, smem) != cudaSuccess) return GMP_ERR_CUDA;
   int dev = 0, sms = 148;
@@ -443,23 +448,24 @@ inline gmp_status_t tc_launch_t(TcTables& t, const WorkItem* it, int64_t n, cons
   const int grid = (int)std::min<int64_t>(n, sms);
   constexpr int mi = tc_map_index<C>();
   k_tc_class<C, BN><<<grid, TC_THREADS, smem, s>>>(t.mapA[mi], BN == 128 ? t.mapB128[mi] : t.mapB[mi], it, n, pd, ct,
-                                                    ws, nb, alpha, beta);
+                                                    ws, nb, alpha, beta, order);
   return cudaGetLastError() == cudaSuccess ? GMP_OK : GMP_ERR_CUDA;
 }
 
 // cls: 2..5 for the 16/8-bit classes, TC_SPLIT for the FP32 class on the tensor
 // pipe; bn: 256 or 128 (128 when the launch folds into binary64 W)
 inline gmp_status_t tc_launch(TcTables& t, int cls, int bn, const WorkItem* it, int64_t n, const PairDesc* pd,
-                              const CTileDesc* ct, uint8_t* ws, int nb, double alpha, double beta, cudaStream_t s) {
+                              const CTileDesc* ct, uint8_t* ws, int nb, double alpha, double beta, const int32_t* order,
+                              cudaStream_t s) {
   const int mi = (cls == TC_SPLIT) ? GMP_AR_SPLIT : cls;
   if (!((cls >= 2 && cls <= 5) || cls == TC_SPLIT) || !t.ready[mi]) return GMP_ERR_STATE;
   const bool wide = bn == 256;
   switch (cls) {
-    case 2: return wide ? tc_launch_t<2, 256>(t, it, n, pd, ct, ws, nb, alpha, beta, s) : tc_launch_t<2, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, s);
-    case 3: return wide ? tc_launch_t<3, 256>(t, it, n, pd, ct, ws, nb, alpha, beta, s) : tc_launch_t<3, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, s);
-    case 4: return wide ? tc_launch_t<4, 256>(t, it, n, pd, ct, ws, nb, alpha, beta, s) : tc_launch_t<4, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, s);
-    case 5: return wide ? tc_launch_t<5, 256>(t, it, n, pd, ct, ws, nb, alpha, beta, s) : tc_launch_t<5, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, s);
-    default: return tc_launch_t<TC_SPLIT, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, s);
+    case 2: return wide ? tc_launch_t<2, 256>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s) : tc_launch_t<2, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s);
+    case 3: return wide ? tc_launch_t<3, 256>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s) : tc_launch_t<3, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s);
+    case 4: return wide ? tc_launch_t<4, 256>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s) : tc_launch_t<4, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s);
+    case 5: return wide ? tc_launch_t<5, 256>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s) : tc_launch_t<5, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s);
+    default: return tc_launch_t<TC_SPLIT, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s);
   }
 }
 

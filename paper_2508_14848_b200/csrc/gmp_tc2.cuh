@@ -44,6 +44,25 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
       "l"(map), "r"(c0), "r"(c1), "r"(bar0)
       : "memory");
 }
+// the same with an L2 cache-policy operand (createpolicy)
+__device__ __forceinline__ void tma_load_2d_pair_hint(void* dst, const CUtensorMap* map, int c0, int c1,
+                                                      uint32_t bar0, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+      "[%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(bar0), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ void tc2_commit_both(uint64_t* b) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
@@ -81,7 +100,8 @@ template <int C>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 k_tc2_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
             const WorkItem* __restrict__ items, int64_t nitems, const PairDesc* __restrict__ pairs,
-            const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha) {
+            const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha, double beta,
+            const int32_t* __restrict__ order, uint32_t hints) {
   constexpr int ESZ = (C == 4 || C == 5) ? 1 : 2;
   constexpr int BK = 128 / ESZ;                  // elements per 128-byte K block
   constexpr int NMMA = 4;                        // 32-byte K per tcgen05.mma
@@ -121,10 +141,13 @@ k_tc2_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   const int64_t cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
   const int nsub = nb / 256;
 
+  // flat index -> (item, 256 x 256 sub-tile): the host's raster order when given
+  // (C tile row bands, sub-columns), else item-major row by row
   auto item_at = [&](int64_t flat) {
     const int S = nsub * nsub;
-    const int64_t idx = flat / S;
-    const int sub = (int)(flat - idx * S);
+    const int64_t v = order ? (int64_t)order[flat] : flat;
+    const int64_t idx = v / S;
+    const int sub = (int)(v - idx * S);
     WorkItem w = items[idx];
     w.m0 = (sub / nsub) * 256;
     w.n0 = (sub - (sub / nsub) * nsub) * 256;
@@ -136,6 +159,8 @@ k_tc2_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       int stage = 0;
       uint32_t phase = 0;
       const uint32_t full0 = smem_u32(full) & TC2_PEER_MASK;
+      // the A panel of the running row band stays in L2 across its C tiles; B streams
+      const uint64_t polA = l2_policy_evict_last(), polB = l2_policy_evict_first();
       for (int64_t it = cluster; it < nitems; it += nclusters) {
         const WorkItem w = item_at(it);
         for (int pi = 0; pi < w.pcnt; ++pi) {
@@ -145,8 +170,14 @@ k_tc2_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             uint8_t* sa = smem + stage * STAGE_BYTES;
             if (rank == 0) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
             const uint32_t fb = full0 + (uint32_t)(stage * 8);
-            tma_load_2d_pair(sa, &tmA, kb * BK, pd.a_slot * nb + w.m0 + 128 * (int)rank, fb);
-            tma_load_2d_pair(sa + A_BYTES, &tmB, kb * BK, pd.b_slot * nb + w.n0 + 128 * (int)rank, fb);
+            if (hints & 1)
+              tma_load_2d_pair_hint(sa, &tmA, kb * BK, pd.a_slot * nb + w.m0 + 128 * (int)rank, fb, polA);
+            else
+              tma_load_2d_pair(sa, &tmA, kb * BK, pd.a_slot * nb + w.m0 + 128 * (int)rank, fb);
+            if (hints & 2)
+              tma_load_2d_pair_hint(sa + A_BYTES, &tmB, kb * BK, pd.b_slot * nb + w.n0 + 128 * (int)rank, fb, polB);
+            else
+              tma_load_2d_pair(sa + A_BYTES, &tmB, kb * BK, pd.b_slot * nb + w.n0 + 128 * (int)rank, fb);
             if (++stage == ST) { stage = 0; phase ^= 1; }
           }
         }
@@ -188,12 +219,18 @@ k_tc2_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     for (int64_t it = cluster; it < nitems; it += nclusters) {
       const WorkItem w = item_at(it);
       const CTileDesc ct = ctiles[w.ctile];
-      float* wrow = reinterpret_cast<float*>(ws + ct.w_off) + (int64_t)(w.m0 + rloc) * nb + w.n0 + half * HC;
+      const int64_t rowoff = (int64_t)(w.m0 + rloc) * nb + w.n0 + half * HC;
+      float* wrow = reinterpret_cast<float*>(ws + ct.w_off) + rowoff;
       float accr[HC];
+      if (w.pad & 1) {   // first tile-GEMM launch of this C tile: W0 from C_in (O9)
 #pragma unroll
-      for (int v = 0; v < HC / 4; ++v) {
-        const float4 x = reinterpret_cast<const float4*>(wrow)[v];
-        accr[4 * v] = x.x; accr[4 * v + 1] = x.y; accr[4 * v + 2] = x.z; accr[4 * v + 3] = x.w;
+        for (int v = 0; v < HC; ++v) accr[v] = w0_f32(ct, ws, rowoff + v, beta);
+      } else {
+#pragma unroll
+        for (int v = 0; v < HC / 4; ++v) {
+          const float4 x = reinterpret_cast<const float4*>(wrow)[v];
+          accr[4 * v] = x.x; accr[4 * v + 1] = x.y; accr[4 * v + 2] = x.z; accr[4 * v + 3] = x.w;
+        }
       }
       for (int pi = 0; pi < w.pcnt; ++pi) {
         const PairDesc pd = pairs[w.pbeg + pi];
@@ -426,9 +463,19 @@ inline gmp_status_t tcmc_launch(TcTables& t, int cls, const WorkItem* it, int64_
 
 constexpr int tc2_smem_bytes() { return TC2_STAGES * (128 * 128 * 2) + 1024 /*align*/ + 256 /*barriers*/; }
 
+// L2 cache hints of the pair kernel's TMA loads (bit 0: A evict_last, bit 1: B
+// evict_first); GMP_TC2_HINTS overrides the default (A/B measurements)
+inline uint32_t tc2_hints() {
+  static const uint32_t h = [] {
+    const char* e = getenv("GMP_TC2_HINTS");
+    return (uint32_t)(e ? atoi(e) : 0);
+  }();
+  return h;
+}
+
 template <int C>
 inline gmp_status_t tc2_launch_t(TcTables& t, const WorkItem* it, int64_t n, const PairDesc* pd, const CTileDesc* ct,
-                                 uint8_t* ws, int nb, double alpha, cudaStream_t s) {
+                                 uint8_t* ws, int nb, double alpha, double beta, const int32_t* order, cudaStream_t s) {
   constexpr int smem = tc2_smem_bytes();
   if (ensure_max_smem(k_tc2_class<C>, smem) != cudaSuccess) return GMP_ERR_CUDA;
   int dev = 0, sms = 148;
@@ -436,19 +483,20 @@ inline gmp_status_t tc2_launch_t(TcTables& t, const WorkItem* it, int64_t n, con
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t clusters = std::min<int64_t>(n, sms / 2);
   k_tc2_class<C><<<(unsigned)(2 * clusters), TC_THREADS, smem, s>>>(t.mapA[C], t.mapB128[C], it, n, pd, ct, ws, nb,
-                                                                    alpha);
+                                                                    alpha, beta, order, tc2_hints());
   return cudaGetLastError() == cudaSuccess ? GMP_OK : GMP_ERR_CUDA;
 }
 
-// cls: 2..4; n = items x tc2_subtiles_per_item(nb)
+// cls: 2..5; n = items x tc2_subtiles_per_item(nb); order: raster (n entries) or NULL
 inline gmp_status_t tc2_launch(TcTables& t, int cls, const WorkItem* it, int64_t n, const PairDesc* pd,
-                               const CTileDesc* ct, uint8_t* ws, int nb, double alpha, cudaStream_t s) {
+                               const CTileDesc* ct, uint8_t* ws, int nb, double alpha, double beta,
+                               const int32_t* order, cudaStream_t s) {
   if (cls < 2 || cls > 5 || !t.ready[cls]) return GMP_ERR_STATE;
   switch (cls) {
-    case 2: return tc2_launch_t<2>(t, it, n, pd, ct, ws, nb, alpha, s);
-    case 3: return tc2_launch_t<3>(t, it, n, pd, ct, ws, nb, alpha, s);
-    case 4: return tc2_launch_t<4>(t, it, n, pd, ct, ws, nb, alpha, s);
-    default: return tc2_launch_t<5>(t, it, n, pd, ct, ws, nb, alpha, s);
+    case 2: return tc2_launch_t<2>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s);
+    case 3: return tc2_launch_t<3>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s);
+    case 4: return tc2_launch_t<4>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s);
+    default: return tc2_launch_t<5>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s);
   }
 }
 

@@ -35,12 +35,16 @@ def _cases():
                                                class_mask=0b111111, seed=46)),
         ("e5m2_nb256", gmp_inputs.small_workload(768, 512, 1024, 256, 2e-2, mode="random", E=40, beta=0.0,
                                                  class_mask=0b111111, seed=47)),
-        # nb = 512 with GMP_FLAG_TC_PAIR: 2 x 2 sub-tiles of 256 x 256 per C tile on the
-        # SM-pair kernel (k_tc2_class); the plain nb = 512 run covers the 1-SM kernel
+        # nb = 512 with GMP_FLAG_TC_PAIR: 2 x 2 sub-tiles of 256 x 256 per C tile on the SM-pair
+        # kernel (k_tc2_class), rastered by C tile row bands; the plain nb = 512 run covers the 1-SM kernel
         ("pairs_nb512", gmp_inputs.small_workload(1024, 1536, 1536, 512, 1e-2, mode="random", E=24, beta=0.75,
                                                   class_mask=0b11111, seed=45), B.GMP_FLAG_TC_PAIR),
         ("nb512", gmp_inputs.small_workload(1024, 1536, 1536, 512, 1e-2, mode="random", E=24, beta=0.75,
                                             class_mask=0b11111, seed=45)),
+        # GMP_FLAG_TC_SINGLE (explicit 1-SM choice) with the raster of the 1-SM launches (GMP_RASTER=1
+        # is process-wide, so here the flag only pins the default)
+        ("single_nb512", gmp_inputs.small_workload(1024, 1536, 1536, 512, 1e-2, mode="random", E=24, beta=0.75,
+                                                   class_mask=0b11111, seed=45), B.GMP_FLAG_TC_SINGLE),
         ("mcast_nb512", gmp_inputs.small_workload(1024, 1536, 1536, 512, 1e-2, mode="random", E=24, beta=0.75,
                                                   class_mask=0b11111, seed=45), B.GMP_FLAG_TC_MCAST),
         ("pairs_e5m2_nb512", gmp_inputs.small_workload(1024, 1024, 1536, 512, 5e-2, mode="random", E=32,
