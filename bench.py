@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--cpu-threads", type=int, default=0, help="oracle threads (0: min(16, cores))")
     ap.add_argument("--flags", type=int, default=0, help="extra GMP_FLAG_* bits (A/B runs)")
     ap.add_argument("--size", type=int, default=0, help="override M=N=K (keeps the config's recipe)")
+    ap.add_argument("--balance", action="store_true",
+                    help="N > 1: precision-aware tile ownership from gemm_mp_balance (NEXT-3) instead of "
+                         "block-cyclic; chosen once from a block-cyclic plan's maps, outside the timed region")
     ap.add_argument("--sender", action="store_true",
                     help="GMP_FLAG_SENDER_SIDE: hybrid sender-side conversion of SUMMA panels (NEXT-2)")
     return ap.parse_args()
@@ -400,7 +403,7 @@ def run_e2e(a, hA, hB, hC, ref_rows, out_shape, G, dev, desc, comm, w, ws_bytes,
             "result_matches_device_run": ok}
 
 
-def fp64_baseline(a, w, A, Bm, C, dev, stream, P, Q, p, q, comm, G):
+def fp64_baseline(a, w, A, Bm, C, dev, stream, P, Q, p, q, comm, G, ro=None, co=None):
     """The paper's comparison point 100D:0S: the same data with
     class_mask = FP64 only, same library, same step.  When the full-size all-FP64
     workspace does not fit next to the inputs (N = 65536 on one GPU: 3 x 32 GB of
@@ -427,7 +430,7 @@ def fp64_baseline(a, w, A, Bm, C, dev, stream, P, Q, p, q, comm, G):
     Csub = None if C is None else (C if not sub else C[:n, :n])
     out = torch.empty((Asub.shape[0], Bsub.shape[1]), dtype=torch.float64, device=dev)
     desc = B.make_desc(n, n if sub else w.N, n if sub else w.K, w.nb, w.tol, w.alpha, w.beta, 0b1, 0, P, Q,
-                       p * Q + q)
+                       p * Q + q, row_owner=None if sub else ro, col_owner=None if sub else co)
     nscr = B.gemm_mp_scratch_size(desc)
     scratch = torch.empty(nscr, dtype=torch.uint8, device=dev)
     ws = None
@@ -534,17 +537,35 @@ def main():
         dist.broadcast(t, 0)
         comm = B.gemm_mp_nccl_comm_create(bytes(t.cpu().numpy()), G, rank)
 
-    # ---- inputs: local block-cyclic parts, generated on the device (N1) ----
-    A = api.synth(w.M, w.K, w.nb, w.a, P, Q, p, q, device=dev)
-    Bm = api.synth(w.K, w.N, w.nb, w.b, P, Q, p, q, device=dev)
-    C = api.synth(w.M, w.N, w.nb, w.c, P, Q, p, q, device=dev) if w.beta != 0 else None
-    lr, lc = api.local_shape(w.M, w.N, w.nb, P, Q, p, q)
+    flags = B.GMP_FLAG_TIMING | (B.GMP_FLAG_SENDER_SIDE if a.sender else 0) | a.flags
+    # ---- NEXT-3: tile ownership.  Block-cyclic unless --balance: then the
+    # owners come from gemm_mp_balance on the global maps of one block-cyclic plan (the same
+    # on every rank), and the inputs are generated directly in that layout ----
+    ro = co = None
+    balance = None
+    if G > 1 and a.balance:
+        A0, B0, C0 = api.synth_operands(w, P, Q, p, q, device=dev)
+        d0 = B.make_desc(w.M, w.N, w.K, w.nb, w.tol, w.alpha, w.beta, w.class_mask, flags, P, Q, rank)
+        g0 = api.GemmMP(d0, A0, B0, C0, nccl_comm=comm, device=dev)
+        m0 = g0.maps()
+        g0.close()
+        del g0, A0, B0, C0
+        torch.cuda.empty_cache()
+        t0 = time.perf_counter()
+        ro, co, imb = B.gemm_mp_balance(d0, m0["acode"], m0["bcode"])
+        balance = {"imbalance_model_block_cyclic": imb[0], "imbalance_model_balanced": imb[1],
+                   "host_ms": (time.perf_counter() - t0) * 1e3,
+                   "rows_per_process_row": [int((ro == x).sum()) for x in range(P)],
+                   "cols_per_process_col": [int((co == x).sum()) for x in range(Q)]}
+    # ---- inputs: local parts, generated on the device (N1) ----
+    A, Bm, C = api.synth_operands(w, P, Q, p, q, ro, co, device=dev)
+    lr, lc = api.local_c_shape(w, P, Q, p, q, ro, co)
     Cout = torch.empty((max(lr, 1), max(lc, 2)), dtype=torch.float64, device=dev)
     ldc = Cout.stride(0)
     torch.cuda.synchronize()
 
-    flags = B.GMP_FLAG_TIMING | (B.GMP_FLAG_SENDER_SIDE if a.sender else 0) | a.flags
-    desc = B.make_desc(w.M, w.N, w.K, w.nb, w.tol, w.alpha, w.beta, w.class_mask, flags, P, Q, rank)
+    desc = B.make_desc(w.M, w.N, w.K, w.nb, w.tol, w.alpha, w.beta, w.class_mask, flags, P, Q, rank,
+                       row_owner=ro, col_owner=co)
     nscr = B.gemm_mp_scratch_size(desc)
     scratch = torch.empty(nscr, dtype=torch.uint8, device=dev)
     ws_holder = {"t": None, "bytes": 0}
@@ -638,7 +659,7 @@ def main():
     fp64 = None
     if not a.no_fp64_baseline:
         try:
-            fp64 = fp64_baseline(a, w, A, Bm, C, dev, stream, P, Q, p, q, comm, G)
+            fp64 = fp64_baseline(a, w, A, Bm, C, dev, stream, P, Q, p, q, comm, G, ro, co)
         except Exception as ex:
             fp64 = {"error": f"{type(ex).__name__}: {str(ex)[:200]}"}
     # ---- NVLink: measured NCCL broadcast bandwidth (N > 1) ----
@@ -724,7 +745,9 @@ def main():
                        "alpha": w.alpha, "beta": w.beta, "grid": f"{P}x{Q}", "parallelism": f"summa{P}x{Q}",
                        "l2": "inputs (2+ GB per matrix) > 126 MB L2, no flush needed",
                        "step": "plan+convert+execute (S1-S7)",
-                       "conversion": "sender-side hybrid (NEXT-2)" if a.sender else "receiver-side (PAPER.md:148)"},
+                       "conversion": "sender-side hybrid (NEXT-2)" if a.sender else "receiver-side (PAPER.md:148)",
+                       "ownership": "balanced (gemm_mp_balance, NEXT-3)" if ro is not None else "2D block-cyclic"},
+            "balance": balance,
             "nvlink_recv_bytes_rank0": st["recv_bytes_local"],
             "phases_ms": {"plan": statistics.median(ph[0] for ph in phase),
                           "convert": statistics.median(ph[1] for ph in phase), "execute": exec_ms},

@@ -24,11 +24,15 @@
  *   - Pointers named A, B, C, scratch, ws are DEVICE pointers; pointers named
  *     host_* or the optional maps in gmp_desc_t are HOST pointers.
  *   - Operand layout: binary64, row-major, leading dimension in elements.  On a
- *     P x Q grid each rank passes ITS LOCAL tiles only, packed block-cyclically:
- *     rank (p, q) = rank p*Q + q holds the tiles (i, l) of A with i = p mod P,
- *     l = q mod Q at local tile position (i div P, l div Q); B tiles (l, j) with
- *     l = p mod P, j = q mod Q; C tiles (i, j) with i = p mod P, j = q mod Q.
- *     P = Q = 1 is the ordinary single-GPU layout.
+ *     P x Q grid each rank passes ITS LOCAL tiles only.  Default: 2D block-cyclic
+ *     (PAPER.md:179): rank (p, q) = rank p*Q + q holds the tiles (i, l) of A with
+ *     i = p mod P, l = q mod Q at local tile position (i div P, l div Q); B tiles
+ *     (l, j) with l = p mod P, j = q mod Q; C tiles (i, j) with i = p mod P,
+ *     j = q mod Q.  With desc.row_owner / col_owner (NEXT-3, gemm_mp_balance) tile
+ *     row i of A and C lives on process row row_owner[i] and tile column j of B
+ *     and C on process column col_owner[j] (K stays block-cyclic: A column l on
+ *     process column l mod Q, B row l on process row l mod P); a rank's local
+ *     tiles keep increasing global order.  P = Q = 1 is the single-GPU layout.
  *   - Asynchronous calls enqueue work on the given stream; asynchronous CUDA or
  *     NCCL failures surface at the next call or at gemm_mp_sync.
  */
@@ -120,6 +124,12 @@ typedef struct {
   /* optional explicit per-tile codes (host, row-major global tile grids: mt x kt, kt x nt,
    * mt x nt) -- the paper's own "aD:bS" experiment mode.  NULL = criterion. */
   const uint8_t *a_map, *b_map, *c_map;
+  /* optional tile ownership (host arrays, NEXT-3): row_owner[i] in [0, P) for each of
+   * the M/nb tile rows, col_owner[j] in [0, Q) for each of the N/nb tile columns;
+   * NULL = block-cyclic (i mod P, j mod Q).  Every rank must pass the same arrays
+   * (gemm_mp_balance computes them identically on every rank).  Read during
+   * gemm_mp_plan / gemm_mp_plan_host only.  GMP_ERR_GRID for an entry out of range. */
+  const int32_t *row_owner, *col_owner;
 } gmp_desc_t;
 
 typedef struct gmp_plan_s *gmp_plan_t;
@@ -255,6 +265,35 @@ gmp_status_t gemm_mp_loopback_destroy(void *comm);
 gmp_status_t gemm_mp_synth(double *out, int64_t ld, int64_t rows, int64_t cols, int32_t nb,
                            int32_t P, int32_t Q, int32_t p, int32_t q, uint64_t seed,
                            uint64_t tau, int32_t mode, int32_t E, int32_t s, void *stream);
+
+/* The same generator for any ownership: local tile (il, jl) of `out` (nrt x nct
+ * tiles, row-major, ld >= nct*nb) is global tile (row_tiles[il], col_tiles[jl]).
+ * row_tiles / col_tiles are HOST arrays (copied before return).  GMP_ERR_ARG for a
+ * tile index out of range.  Async.                                             */
+gmp_status_t gemm_mp_synth_tiles(double *out, int64_t ld, int64_t rows, int64_t cols, int32_t nb,
+                                 const int32_t *row_tiles, int64_t nrt, const int32_t *col_tiles,
+                                 int64_t nct, uint64_t seed, uint64_t tau, int32_t mode, int32_t E,
+                                 int32_t s, void *stream);
+
+/* NEXT-3, precision-aware load balancing (PaRSEC's dynamic scheduling
+ * absorbs "the imbalanced workload introduced by the adaptive tile-centric
+ * mixed-precision algorithm").  Host-only.  From the GLOBAL maps acode (mt x kt)
+ * and bcode (kt x nt) -- e.g. gemm_mp_get_maps of a first, block-cyclic plan --
+ * chooses tile-row owners row_owner[mt] in [0, P) and tile-column owners
+ * col_owner[nt] in [0, Q) (desc->P, desc->Q) that minimise the largest per-rank
+ * cost = sum over the rank's C tiles (i, j) of sum_l cost[max(codeA(i,l),
+ * codeB(l,j))] + cost[6] x (A + B + C tiles it owns), by alternating row / column
+ * local search (moves and swaps) from the block-cyclic start (R30).
+ * cost: 7 doubles (relative per-pair time of classes 0..5, per-owned-tile time) or
+ * NULL for the built-in B200 model.  Deterministic: every rank gets the same
+ * owners from the same maps.  imbalance (may be NULL): {max/mean rank cost of the
+ * block-cyclic layout, of the returned layout} -- never worse than block-cyclic.
+ * Pass the owners as desc.row_owner / col_owner to gemm_mp_plan; the caller
+ * places its local tiles accordingly (gemm_mp_synth_tiles for synthetic inputs).
+ * C is bitwise the same for every ownership (the fold order is fixed, R15).     */
+gmp_status_t gemm_mp_balance(const gmp_desc_t *desc, const uint8_t *acode, const uint8_t *bcode,
+                             const double *cost, int32_t *row_owner, int32_t *col_owner,
+                             double *imbalance);
 
 /* Frees the plan's host metadata (NULL-safe).                                  */
 void gemm_mp_destroy(gmp_plan_t plan);

@@ -24,6 +24,20 @@ def local_shape(rows, cols, nb, P, Q, p, q):
     return nloc(rows // nb, P, p) * nb, nloc(cols // nb, Q, q) * nb
 
 
+def owned_tiles(n_tiles, P, p, owner=None):
+    """global tile indices of one dimension held by process row/column p, increasing:
+    block-cyclic (t mod P == p) or owner[t] == p (gemm_mp_balance, NEXT-3)"""
+    return [t for t in range(n_tiles) if (t % P if owner is None else int(owner[t])) == p]
+
+
+def local_tiles(M, N, K, nb, P, Q, p, q, row_owner=None, col_owner=None):
+    """(row tiles, column tiles) of this rank's local A, B and C (gemm_mp.h layout)"""
+    mt, nt, kt = M // nb, N // nb, K // nb
+    rows = owned_tiles(mt, P, p, row_owner)
+    cols = owned_tiles(nt, Q, q, col_owner)
+    return dict(A=(rows, owned_tiles(kt, Q, q)), B=(owned_tiles(kt, P, p), cols), C=(rows, cols))
+
+
 class GemmMP:
     """One planned GEMM on this rank's device."""
 
@@ -91,6 +105,44 @@ def synth(rows, cols, nb, recipe, P=1, Q=1, p=0, q=0, device="cuda", stream=None
                         MODE[recipe.mode], recipe.E, recipe.s,
                         stream or torch.cuda.current_stream(device))
     return out
+
+
+def synth_tiles(rows, cols, nb, recipe, row_tiles, col_tiles, device="cuda", stream=None):
+    """Local part of a synthetic matrix holding the given global tiles (any ownership)."""
+    lr, lc = len(row_tiles) * nb, len(col_tiles) * nb
+    out = torch.empty((max(lr, 1), max(lc, 2)), dtype=torch.float64, device=device)[:lr, :lc] \
+        if lr * lc == 0 else torch.empty((lr, lc), dtype=torch.float64, device=device)
+    if lr * lc:
+        B.gemm_mp_synth_tiles(out, out.stride(0), rows, cols, nb, row_tiles, col_tiles, recipe.seed,
+                              recipe.tau, MODE[recipe.mode], recipe.E, recipe.s,
+                              stream or torch.cuda.current_stream(device))
+    return out
+
+
+def synth_operands(w, P=1, Q=1, p=0, q=0, row_owner=None, col_owner=None, device="cuda", stream=None):
+    """This rank's local A, B (and C if beta != 0) of a gmp_inputs workload, in the
+    gemm_mp.h layout for the given ownership (block-cyclic when the owners are None)."""
+    lt = local_tiles(w.M, w.N, w.K, w.nb, P, Q, p, q, row_owner, col_owner)
+    A = synth_tiles(w.M, w.K, w.nb, w.a, *lt["A"], device=device, stream=stream)
+    Bm = synth_tiles(w.K, w.N, w.nb, w.b, *lt["B"], device=device, stream=stream)
+    C = synth_tiles(w.M, w.N, w.nb, w.c, *lt["C"], device=device, stream=stream) if w.beta != 0 else None
+    return A, Bm, C
+
+
+def local_c_shape(w, P=1, Q=1, p=0, q=0, row_owner=None, col_owner=None):
+    rows, cols = local_tiles(w.M, w.N, w.K, w.nb, P, Q, p, q, row_owner, col_owner)["C"]
+    return len(rows) * w.nb, len(cols) * w.nb
+
+
+def place_local_c(full, loc, w, P, Q, p, q, row_owner=None, col_owner=None):
+    """writes rank (p, q)'s local C (numpy) into the global numpy matrix `full`"""
+    import numpy as np
+    nb = w.nb
+    rows, cols = local_tiles(w.M, w.N, w.K, nb, P, Q, p, q, row_owner, col_owner)["C"]
+    rr = (np.asarray(rows, np.int64)[:, None] * nb + np.arange(nb)[None, :]).ravel()
+    cc = (np.asarray(cols, np.int64)[:, None] * nb + np.arange(nb)[None, :]).ravel()
+    full[np.ix_(rr, cc)] = loc
+    return rr, cc
 
 
 def gemm_mp(A, B_, C=None, nb=128, tol=1e-6, alpha=1.0, beta=0.0, class_mask=0b01111, flags=0,

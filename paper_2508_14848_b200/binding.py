@@ -43,7 +43,8 @@ class gmp_desc_t(ct.Structure):
                 ("tol", ct.c_double), ("alpha", ct.c_double), ("beta", ct.c_double),
                 ("class_mask", ct.c_uint32), ("flags", ct.c_uint32),
                 ("P", ct.c_int32), ("Q", ct.c_int32), ("rank", ct.c_int32),
-                ("a_map", ct.c_void_p), ("b_map", ct.c_void_p), ("c_map", ct.c_void_p)]
+                ("a_map", ct.c_void_p), ("b_map", ct.c_void_p), ("c_map", ct.c_void_p),
+                ("row_owner", ct.c_void_p), ("col_owner", ct.c_void_p)]
 
 
 class gmp_stats_t(ct.Structure):
@@ -94,6 +95,8 @@ def lib():
             "gemm_mp_loopback_create": [ct.c_int, ct.POINTER(vp)],
             "gemm_mp_loopback_destroy": [vp],
             "gemm_mp_synth": [vp, i64, i64, i64, i32, i32, i32, i32, i32, u64, u64, i32, i32, i32, vp],
+            "gemm_mp_synth_tiles": [vp, i64, i64, i64, i32, vp, i64, vp, i64, u64, u64, i32, i32, i32, vp],
+            "gemm_mp_balance": [ct.POINTER(gmp_desc_t), vp, vp, vp, vp, vp, vp],
             "gemm_mp_plan_host": [ct.POINTER(gmp_desc_t), vp, vp, vp, vp, vp, vp, ct.POINTER(vp)],
             "gemm_mp_get_schedule": [vp, i32, vp, i64, ct.POINTER(i64)],
         }
@@ -137,13 +140,15 @@ def _stream(s):
 
 
 def make_desc(M, N, K, nb, tol, alpha=1.0, beta=0.0, class_mask=0b01111, flags=0, P=1, Q=1, rank=0,
-              a_map=None, b_map=None, c_map=None):
-    """gmp_desc_t; explicit maps are numpy uint8 arrays kept alive on the struct."""
+              a_map=None, b_map=None, c_map=None, row_owner=None, col_owner=None):
+    """gmp_desc_t; explicit maps (uint8) and owners (int32) are numpy arrays kept alive on
+    the struct."""
     import numpy as np
     maps = [None if m is None else np.ascontiguousarray(m, dtype=np.uint8) for m in (a_map, b_map, c_map)]
+    owners = [None if o is None else np.ascontiguousarray(o, dtype=np.int32) for o in (row_owner, col_owner)]
     d = gmp_desc_t(M, N, K, nb, tol, alpha, beta, class_mask, flags, P, Q, rank,
-                   *[None if m is None else m.ctypes.data for m in maps])
-    d._keep = maps
+                   *[None if m is None else m.ctypes.data for m in maps + owners])
+    d._keep = maps + owners
     return d
 
 
@@ -242,6 +247,32 @@ def gemm_mp_loopback_destroy(comm):
 def gemm_mp_synth(out, ld, rows, cols, nb, P, Q, p, q, seed, tau, mode, E, s, stream=None):
     _check(lib().gemm_mp_synth(_ptr(out), ld, rows, cols, nb, P, Q, p, q, seed, tau, mode, E, s,
                                _stream(stream)))
+
+
+def gemm_mp_synth_tiles(out, ld, rows, cols, nb, row_tiles, col_tiles, seed, tau, mode, E, s, stream=None):
+    import numpy as np
+    rt = np.ascontiguousarray(row_tiles, np.int32)
+    ctl = np.ascontiguousarray(col_tiles, np.int32)
+    _check(lib().gemm_mp_synth_tiles(_ptr(out), ld, rows, cols, nb, rt.ctypes.data, rt.size, ctl.ctypes.data,
+                                     ctl.size, seed, tau, mode, E, s, _stream(stream)))
+
+
+def gemm_mp_balance(desc, acode, bcode, cost=None):
+    """-> (row_owner int32[mt], col_owner int32[nt], (imbalance block-cyclic, balanced))"""
+    import numpy as np
+    a = np.ascontiguousarray(acode, np.uint8)
+    b = np.ascontiguousarray(bcode, np.uint8)
+    mt, nt = desc.M // desc.nb, desc.N // desc.nb
+    if a.size != mt * (desc.K // desc.nb) or b.size != (desc.K // desc.nb) * nt:
+        raise ValueError("acode / bcode shapes do not match desc")
+    c = None if cost is None else np.ascontiguousarray(cost, np.float64)
+    if c is not None and c.size != NCLS + 1:
+        raise ValueError(f"cost must hold {NCLS + 1} doubles")
+    ro = np.zeros(mt, np.int32); co = np.zeros(nt, np.int32); imb = np.zeros(2)
+    _check(lib().gemm_mp_balance(ct.byref(desc), a.ctypes.data, b.ctypes.data,
+                                 None if c is None else c.ctypes.data, ro.ctypes.data, co.ctypes.data,
+                                 imb.ctypes.data))
+    return ro, co, (float(imb[0]), float(imb[1]))
 
 
 def gemm_mp_plan_host(desc, acode, bcode, ccode, ascale5, bscale5, cin_scale=None):

@@ -26,6 +26,7 @@
 #include "gmp_ozaki.cuh"
 #include "gmp_tc2.cuh"
 #include "gmp_tcf.cuh"
+#include "gmp_layout.h"
 
 using namespace gmp;
 
@@ -193,6 +194,7 @@ struct gmp_plan_s {
   gmp_desc_t d{};
   int64_t mt = 0, nt = 0, kt = 0, nA = 0, nB = 0, nC = 0;
   int P = 1, Q = 1, p = 0, q = 0;
+  Layout lay;   // tile-row / tile-column owners (block-cyclic unless desc.row_owner / col_owner)
   const double *A = nullptr, *B = nullptr, *C = nullptr;
   int64_t lda = 0, ldb = 0, ldc = 0;
   ncclComm_t world = nullptr, rowc = nullptr, colc = nullptr;
@@ -451,6 +453,8 @@ static void build_tables(gmp_plan_s* pl) {
   const gmp_desc_t& d = pl->d;
   const int64_t nb = d.nb, nb2 = nb * nb, mt = pl->mt, nt = pl->nt, kt = pl->kt;
   const int P = pl->P, Q = pl->Q, p = pl->p, q = pl->q;
+  const std::vector<int32_t>& rowP = pl->lay.rowP;
+  const std::vector<int32_t>& colQ = pl->lay.colQ;
   const bool hasC = d.beta != 0.0;
   for (int c = 0; c < NC; ++c) pl->slot_bytes[c] = nb2 * class_bytes(c);
   pl->slot_bytes[GMP_AR_SPLIT] = 3 * nb2 * 2;
@@ -467,7 +471,7 @@ static void build_tables(gmp_plan_s* pl) {
       for (int64_t l = 0; l < kt; ++l) {
         const int ca = pl->codeA[i * kt + l], cb = pl->codeB[l * nt + j], c = std::max(ca, cb);
         pairs_cls[c]++;
-        if (i % P != p || j % Q != q) continue;
+        if (rowP[i] != p || colQ[j] != q) continue;
         pairs_loc[c]++;
         needA[(i * kt + l) * NC + ca] = 1;
         needA[(i * kt + l) * NC + c] = 1;
@@ -486,24 +490,24 @@ static void build_tables(gmp_plan_s* pl) {
   pl->wireB.assign(pl->nB, 0);
   for (int64_t g = 0; g < pl->nA; ++g) {
     const int64_t i = g / kt, l = g % kt;
-    if (i % P != p) continue;
+    if (rowP[i] != p) continue;
     const int code = pl->codeA[g];
     uint8_t set = 0;
     if (sender)
       for (int64_t j = 0; j < nt; ++j)
-        if ((int)(j % Q) != (int)(l % Q)) set |= (uint8_t)(1u << std::max(code, (int)pl->codeB[l * nt + j]));
+        if ((int)colQ[j] != (int)(l % Q)) set |= (uint8_t)(1u << std::max(code, (int)pl->codeB[l * nt + j]));
     int64_t sb = 0;
     for (int c = 0; c < NC; ++c) if (set >> c & 1) sb += pl->slot_bytes[c];
     pl->wireA[g] = (set && sb < pl->slot_bytes[code]) ? set : (uint8_t)(1u << code);
   }
   for (int64_t g = 0; g < pl->nB; ++g) {
     const int64_t l = g / nt, j = g % nt;
-    if (j % Q != q) continue;
+    if (colQ[j] != q) continue;
     const int code = pl->codeB[g];
     uint8_t set = 0;
     if (sender)
       for (int64_t i = 0; i < mt; ++i)
-        if ((int)(i % P) != (int)(l % P)) set |= (uint8_t)(1u << std::max(code, (int)pl->codeA[i * kt + l]));
+        if ((int)rowP[i] != (int)(l % P)) set |= (uint8_t)(1u << std::max(code, (int)pl->codeA[i * kt + l]));
     int64_t sb = 0;
     for (int c = 0; c < NC; ++c) if (set >> c & 1) sb += pl->slot_bytes[c];
     pl->wireB[g] = (set && sb < pl->slot_bytes[code]) ? set : (uint8_t)(1u << code);
@@ -512,7 +516,7 @@ static void build_tables(gmp_plan_s* pl) {
   // classes (roots send them, the others receive); a receiver of a tile sent
   // sender-side gets every class it needs on the wire and keeps no stored copy
   for (int64_t g = 0; g < pl->nA; ++g) {
-    if ((g / kt) % P != p) continue;
+    if (rowP[g / kt] != p) continue;
     const bool root = (int)((g % kt) % Q) == q;
     if (!root && pl->wireA[g] != (1u << pl->codeA[g]))
       for (int c = 0; c < NC; ++c) needA[g * NC + c] = 0;
@@ -522,7 +526,7 @@ static void build_tables(gmp_plan_s* pl) {
     if (root) needA[g * NC + pl->codeA[g]] = 1;
   }
   for (int64_t g = 0; g < pl->nB; ++g) {
-    if ((g % nt) % Q != q) continue;
+    if (colQ[g % nt] != q) continue;
     const bool root = (int)((g / nt) % P) == p;
     if (!root && pl->wireB[g] != (1u << pl->codeB[g]))
       for (int c = 0; c < NC; ++c) needB[g * NC + c] = 0;
@@ -631,13 +635,13 @@ static void build_tables(gmp_plan_s* pl) {
     else { t.cout_off = o; o = align_up(o + nb2 * class_bytes(t.code), 1024); }
     const int64_t i = g / nt, j = g % nt;
     t.user_off = -1;  // set at execute (depends on ldc)
-    t.pad = (int32_t)(((i / P) << 16) | (j / Q));  // local tile coordinates (il, jl)
+    t.pad = (int32_t)((pl->lay.rowL[i] << 16) | pl->lay.colL[j]);  // local tile coordinates (il, jl)
   }
   pl->ws_bytes = o;
 
   // ---- pack jobs ----
   for (int64_t g : pl->locA) {
-    const int64_t i = g / kt, l = g % kt, il = i / P, ll = l / Q;
+    const int64_t i = g / kt, l = g % kt, il = pl->lay.rowL[i], ll = l / Q;
     PackJob pj{};
     pj.src = pl->A + il * nb * pl->lda + ll * nb;
     pj.ld = pl->lda;
@@ -648,7 +652,7 @@ static void build_tables(gmp_plan_s* pl) {
     pl->pack.push_back(pj);
   }
   for (int64_t g : pl->locB) {
-    const int64_t l = g / nt, j = g % nt, ll = l / P, jl = j / Q;
+    const int64_t l = g / nt, j = g % nt, ll = l / P, jl = pl->lay.colL[j];
     PackJob pj{};
     pj.src = pl->B + ll * nb * pl->ldb + jl * nb;
     pj.ld = pl->ldb;
@@ -662,7 +666,7 @@ static void build_tables(gmp_plan_s* pl) {
     for (int64_t k = 0; k < nCl; ++k) {
       const int64_t g = pl->locC[k], i = g / nt, j = g % nt;
       PackJob pj{};
-      pj.src = pl->C + (i / P) * nb * pl->ldc + (j / Q) * nb;
+      pj.src = pl->C + pl->lay.rowL[i] * nb * pl->ldc + pl->lay.colL[j] * nb;
       pj.ld = pl->ldc;
       pj.cls = pl->codeC[g];
       pj.scale = pl->sCin[g];
@@ -753,7 +757,8 @@ static void build_tables(gmp_plan_s* pl) {
   if (P * Q > 1) {
     for (int64_t l = 0; l < kt; ++l) {
       const int s = (int)(l / GMP_STEP_DEPTH);
-      for (int64_t i = p; i < mt; i += P) {       // A(i,l) along process row p, root column l % Q
+      for (int64_t i = 0; i < mt; ++i) {          // A(i,l) along process row p, root column l % Q
+        if (rowP[i] != p) continue;
         const int64_t g = i * kt + l;
         for (int c = 0; c < NC; ++c) {
           if (!(pl->wireA[g] >> c & 1)) continue;
@@ -762,7 +767,8 @@ static void build_tables(gmp_plan_s* pl) {
           if ((int)(l % Q) != q) recv_bytes += b.bytes;
         }
       }
-      for (int64_t j = q; j < nt; j += Q) {       // B(l,j) along process column q, root row l % P
+      for (int64_t j = 0; j < nt; ++j) {          // B(l,j) along process column q, root row l % P
+        if (colQ[j] != q) continue;
         const int64_t g = l * nt + j;
         for (int c = 0; c < NC; ++c) {
           if (!(pl->wireB[g] >> c & 1)) continue;
@@ -1006,16 +1012,33 @@ static void build_tables(gmp_plan_s* pl) {
   }
 }
 
-// 2D block-cyclic ownership: tile (i, j) of a grid lives on rank (i mod P, j mod Q)
-static void local_tiles(gmp_plan_s* pl) {
+// Ownership (gmp_layout.h): 2D block-cyclic by default -- tile (i, j)
+// on rank (i mod P, j mod Q) -- or the caller's tile-row / tile-column owners
+// (desc.row_owner / col_owner, NEXT-3); K stays block-cyclic.  Local tiles in
+// increasing global order.
+static gmp_status_t local_tiles(gmp_plan_s* pl) {
   const int P = pl->P, Q = pl->Q;
+  if (!make_layout(pl->mt, pl->nt, P, Q, pl->d.row_owner, pl->d.col_owner, &pl->lay))
+    return fail(GMP_ERR_GRID, "row_owner / col_owner entry outside [0, P) / [0, Q)");
+  pl->d.row_owner = pl->d.col_owner = nullptr;   // host arrays of the caller: not kept
+  const std::vector<int32_t>& rowP = pl->lay.rowP;
+  const std::vector<int32_t>& colQ = pl->lay.colQ;
   pl->locA.clear(); pl->locB.clear(); pl->locC.clear();
-  for (int64_t i = pl->p; i < pl->mt; i += P)
-    for (int64_t l = pl->q; l < pl->kt; l += Q) pl->locA.push_back(i * pl->kt + l);
+  for (int64_t i = 0; i < pl->mt; ++i)
+    if (rowP[i] == pl->p)
+      for (int64_t l = pl->q; l < pl->kt; l += Q) pl->locA.push_back(i * pl->kt + l);
   for (int64_t l = pl->p; l < pl->kt; l += P)
-    for (int64_t j = pl->q; j < pl->nt; j += Q) pl->locB.push_back(l * pl->nt + j);
-  for (int64_t i = pl->p; i < pl->mt; i += P)
-    for (int64_t j = pl->q; j < pl->nt; j += Q) pl->locC.push_back(i * pl->nt + j);
+    for (int64_t j = 0; j < pl->nt; ++j)
+      if (colQ[j] == pl->q) pl->locB.push_back(l * pl->nt + j);
+  for (int64_t i = 0; i < pl->mt; ++i)
+    if (rowP[i] == pl->p)
+      for (int64_t j = 0; j < pl->nt; ++j)
+        if (colQ[j] == pl->q) pl->locC.push_back(i * pl->nt + j);
+  return GMP_OK;
+}
+
+static int64_t count_owned(const std::vector<int32_t>& own, int who) {
+  return (int64_t)std::count(own.begin(), own.end(), who);
 }
 
 extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, int64_t lda, const double* B,
@@ -1040,8 +1063,9 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
   pl->P = d.P; pl->Q = d.Q; pl->p = d.rank / d.Q; pl->q = d.rank % d.Q;
   pl->A = A; pl->B = B; pl->C = C; pl->lda = lda; pl->ldb = ldb; pl->ldc = ldc;
   const bool hasC = d.beta != 0.0;
-  const int64_t mtl = nloc(pl->mt, d.P, pl->p), ktlA = nloc(pl->kt, d.Q, pl->q);
-  const int64_t ktlB = nloc(pl->kt, d.P, pl->p), ntl = nloc(pl->nt, d.Q, pl->q);
+  GMP_TRY(local_tiles(pl));
+  const int64_t mtl = count_owned(pl->lay.rowP, pl->p), ktlA = nloc(pl->kt, d.Q, pl->q);
+  const int64_t ktlB = nloc(pl->kt, d.P, pl->p), ntl = count_owned(pl->lay.colQ, pl->q);
   if ((mtl * ktlA > 0 && (!A || lda < ktlA * nb)) || (ktlB * ntl > 0 && (!B || ldb < ntl * nb)) ||
       (hasC && mtl * ntl > 0 && (!C || ldc < ntl * nb)))
     return fail(GMP_ERR_ARG, "operand pointer NULL or leading dimension too small");
@@ -1055,8 +1079,6 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
   if (!chk_map(d.a_map, pl->nA) || !chk_map(d.b_map, pl->nB) || !chk_map(d.c_map, pl->nC))
     return fail(GMP_ERR_MAP_SHAPE, "explicit map holds a code > 5");
 
-  local_tiles(pl);
-
   // ---- S1: stats of local tiles, written at their global index ----
   uint8_t* sc = (uint8_t*)scratch;
   const int64_t n = pl->nA + pl->nB + pl->nC;
@@ -1068,16 +1090,16 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
   std::vector<StatsJob> jobs;
   for (int64_t g : pl->locA) {
     const int64_t i = g / pl->kt, l = g % pl->kt;
-    jobs.push_back(StatsJob{A + (i / d.P) * nb * lda + (l / d.Q) * nb, lda, (int32_t)g});
+    jobs.push_back(StatsJob{A + pl->lay.rowL[i] * nb * lda + (l / d.Q) * nb, lda, (int32_t)g});
   }
   for (int64_t g : pl->locB) {
     const int64_t l = g / pl->nt, j = g % pl->nt;
-    jobs.push_back(StatsJob{B + (l / d.P) * nb * ldb + (j / d.Q) * nb, ldb, (int32_t)(pl->nA + g)});
+    jobs.push_back(StatsJob{B + (l / d.P) * nb * ldb + pl->lay.colL[j] * nb, ldb, (int32_t)(pl->nA + g)});
   }
   if (hasC)
     for (int64_t g : pl->locC) {
       const int64_t i = g / pl->nt, j = g % pl->nt;
-      jobs.push_back(StatsJob{C + (i / d.P) * nb * ldc + (j / d.Q) * nb, ldc, (int32_t)(pl->nA + pl->nB + g)});
+      jobs.push_back(StatsJob{C + pl->lay.rowL[i] * nb * ldc + pl->lay.colL[j] * nb, ldc, (int32_t)(pl->nA + pl->nB + g)});
     }
   StatsJob* djobs = (StatsJob*)(sc + L.jobs);
   if (!jobs.empty()) {
@@ -1218,7 +1240,7 @@ extern "C" gmp_status_t gemm_mp_plan_host(const gmp_desc_t* desc, const uint8_t*
   pl->sCin.assign(pl->nC, 0);
   if (cin_scale) pl->sCin.assign(cin_scale, cin_scale + pl->nC);
   pl->sCout.assign(pl->nC, 0);
-  local_tiles(pl);
+  GMP_TRY(local_tiles(pl));
   build_tables(pl);
   pl->host_only = true;
   *out = guard.release();
@@ -1401,7 +1423,7 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
   if (!pl->converted) return fail(GMP_ERR_STATE, "execute before convert");
   const int64_t nb = pl->d.nb, nb2 = nb * nb;
   const int64_t nCl = (int64_t)pl->locC.size();
-  const int64_t ntl = nloc(pl->nt, pl->Q, pl->q);
+  const int64_t ntl = count_owned(pl->lay.colQ, pl->q);
   if (nCl > 0 && (!Cuser || ldc < ntl * nb)) return fail(GMP_ERR_ARG, "C NULL or ldc too small");
   cudaStream_t stream = (cudaStream_t)stream_;
   uint8_t* ws = pl->ws;
@@ -1663,18 +1685,89 @@ extern "C" gmp_status_t gemm_mp_nccl_comm_destroy(void* comm) {
   return GMP_OK;
 }
 
+extern "C" gmp_status_t gemm_mp_synth_tiles(double* out, int64_t ld, int64_t rows, int64_t cols, int32_t nb,
+                                            const int32_t* row_tiles, int64_t nrt, const int32_t* col_tiles,
+                                            int64_t nct, uint64_t seed, uint64_t tau, int32_t mode, int32_t E,
+                                            int32_t s, void* stream_) {
+  if (!out || nb <= 0 || rows % nb || cols % nb || nrt < 0 || nct < 0 || (nrt && !row_tiles) || (nct && !col_tiles))
+    return fail(GMP_ERR_ARG, "bad synth arguments");
+  if (ld < nct * nb) return fail(GMP_ERR_ARG, "ld too small");
+  for (int64_t t = 0; t < nrt; ++t)
+    if (row_tiles[t] < 0 || row_tiles[t] >= rows / nb) return fail(GMP_ERR_ARG, "row tile out of range");
+  for (int64_t t = 0; t < nct; ++t)
+    if (col_tiles[t] < 0 || col_tiles[t] >= cols / nb) return fail(GMP_ERR_ARG, "column tile out of range");
+  if (nrt * nct == 0) return GMP_OK;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  SynthArgs a{};
+  a.out = out; a.ld = ld;
+  a.lrows = nrt * nb; a.lcols = nct * nb;
+  a.grows = rows; a.gcols = cols; a.nb = nb;
+  a.seed = seed; a.tau = tau; a.mode = mode; a.E = E; a.s = s;
+  int32_t* tab = nullptr;
+  const int64_t co = align_up(nrt, 4);   // k_xfer destinations are 16-byte aligned
+  GMP_CUDA(cudaMallocAsync(&tab, (size_t)(co + nct) * 4, stream));
+  Upload up;
+  up.add((uint8_t*)tab, row_tiles, nrt * 4);
+  up.add((uint8_t*)(tab + co), col_tiles, nct * 4);
+  const gmp_status_t st = up.run(stream);
+  if (st == GMP_OK) {
+    a.trow = tab; a.tcol = tab + co;
+    k_synth<<<148 * 8, 256, 0, stream>>>(a);
+  }
+  const cudaError_t e = cudaGetLastError();
+  GMP_CUDA(cudaFreeAsync(tab, stream));
+  if (st != GMP_OK) return st;
+  GMP_CUDA(e);
+  return GMP_OK;
+}
+
 extern "C" gmp_status_t gemm_mp_synth(double* out, int64_t ld, int64_t rows, int64_t cols, int32_t nb, int32_t P,
                                       int32_t Q, int32_t p, int32_t q, uint64_t seed, uint64_t tau, int32_t mode,
                                       int32_t E, int32_t s, void* stream) {
-  if (!out || nb <= 0 || rows % nb || cols % nb || P < 1 || Q < 1) return fail(GMP_ERR_ARG, "bad synth arguments");
-  SynthArgs a{};
-  a.out = out; a.ld = ld;
-  a.lrows = nloc(rows / nb, P, p) * nb; a.lcols = nloc(cols / nb, Q, q) * nb;
-  a.grows = rows; a.gcols = cols; a.nb = nb; a.P = P; a.Q = Q; a.p0 = p; a.q0 = q;
-  a.seed = seed; a.tau = tau; a.mode = mode; a.E = E; a.s = s;
-  if (a.lrows * a.lcols == 0) return GMP_OK;
-  k_synth<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(a);
-  GMP_CUDA(cudaGetLastError());
+  if (!out || nb <= 0 || rows % nb || cols % nb || P < 1 || Q < 1 || p < 0 || p >= P || q < 0 || q >= Q)
+    return fail(GMP_ERR_ARG, "bad synth arguments");
+  std::vector<int32_t> rt, ct;
+  for (int64_t t = p; t < rows / nb; t += P) rt.push_back((int32_t)t);
+  for (int64_t t = q; t < cols / nb; t += Q) ct.push_back((int32_t)t);
+  return gemm_mp_synth_tiles(out, ld, rows, cols, nb, rt.data(), (int64_t)rt.size(), ct.data(), (int64_t)ct.size(),
+                             seed, tau, mode, E, s, stream);
+}
+
+// Precision-aware ownership (NEXT-3, gmp_layout.h): default per-pair cost of class c =
+// 2 nb^3 / (library peak of c, TF/s, profiles/peaks_r01.json and the bench's sustained
+// measurements: DGEMM 35.5, BF16x9 155, FP16 1323, BF16 1397, E4M3 / E5M2 2628), per owned
+// tile 20 nb^2 bytes at 6 TB/s (stats read + pack read / write + finalize).
+extern "C" gmp_status_t gemm_mp_balance(const gmp_desc_t* desc, const uint8_t* acode, const uint8_t* bcode,
+                                        const double* cost, int32_t* row_owner, int32_t* col_owner,
+                                        double* imbalance) {
+  GMP_TRY(check_desc(desc));
+  if (!acode || !bcode || !row_owner || !col_owner) return fail(GMP_ERR_ARG, "NULL argument");
+  const int64_t nb = desc->nb, mt = desc->M / nb, nt = desc->N / nb, kt = desc->K / nb;
+  for (int64_t t = 0; t < mt * kt; ++t) if (acode[t] >= NC) return fail(GMP_ERR_MAP_SHAPE, "code > 5");
+  for (int64_t t = 0; t < kt * nt; ++t) if (bcode[t] >= NC) return fail(GMP_ERR_MAP_SHAPE, "code > 5");
+  double cst[NC + 1];
+  if (cost) {
+    for (int c = 0; c <= NC; ++c) {
+      if (!(cost[c] >= 0.0) || !std::isfinite(cost[c])) return fail(GMP_ERR_ARG, "cost must be finite and >= 0");
+      cst[c] = cost[c];
+    }
+  } else {
+    const double peak[NC] = {35.5, 155.0, 1323.0, 1397.0, 2628.0, 2628.0};
+    const double f = 2.0 * (double)nb * nb * nb;
+    for (int c = 0; c < NC; ++c) cst[c] = f / (peak[c] * 1e12);
+    cst[NC] = 20.0 * (double)nb * nb / 6.0e12;
+  }
+  BalanceModel M(mt, nt, kt, desc->P, desc->Q, acode, bcode, cst);
+  std::vector<int32_t> rowP, colQ;
+  balance_layout(M, rowP, colQ);
+  std::vector<int32_t> r0(mt), c0(nt);
+  for (int64_t i = 0; i < mt; ++i) r0[i] = (int32_t)(i % desc->P);
+  for (int64_t j = 0; j < nt; ++j) c0[j] = (int32_t)(j % desc->Q);
+  const double imb0 = layout_imbalance(M, r0, c0), imb1 = layout_imbalance(M, rowP, colQ);
+  if (imb1 > imb0) { rowP = r0; colQ = c0; }   // never worse than block-cyclic
+  std::copy(rowP.begin(), rowP.end(), row_owner);
+  std::copy(colQ.begin(), colQ.end(), col_owner);
+  if (imbalance) { imbalance[0] = imb0; imbalance[1] = std::min(imb0, imb1); }
   return GMP_OK;
 }
 

@@ -364,8 +364,8 @@ __global__ void __launch_bounds__(256) k_c_finalize(const CTileDesc* __restrict_
 
 // ---------------------------------------------------------------------------
 // N1 synthetic generator (benchmark input only):
-// x(r,c) = v(r,c) 2^(s - e(r/nb, c/nb)); a local block-cyclic matrix holds the
-// global tiles (p0 + il*P, q0 + jl*Q).
+// x(r,c) = v(r,c) 2^(s - e(r/nb, c/nb)); local tile (il, jl) of the output is the
+// global tile (trow[il], tcol[jl]) (block-cyclic or the caller's ownership).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -377,7 +377,8 @@ struct SynthArgs {
   double* out;
   int64_t ld, lrows, lcols;        // local matrix (lrows x lcols)
   int64_t grows, gcols;            // global matrix
-  int nb, P, Q, p0, q0;
+  int nb;
+  const int32_t *trow, *tcol;      // global tile row / column of each local tile row / column
   uint64_t seed, tau;
   int mode, E, s;
 };
@@ -388,7 +389,7 @@ __global__ void __launch_bounds__(256) k_synth(SynthArgs a) {
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t lr = idx / a.lcols, lc = idx - (idx / a.lcols) * a.lcols;
-    const int64_t ti = a.p0 + (lr / a.nb) * a.P, tj = a.q0 + (lc / a.nb) * a.Q;
+    const int64_t ti = a.trow[lr / a.nb], tj = a.tcol[lc / a.nb];
     const int64_t gr = ti * a.nb + lr % a.nb, gc = tj * a.nb + lc % a.nb;
     const uint64_t u = mix64(a.seed + ((uint64_t)(gr * a.gcols + gc) + 1ull) * 0x9E3779B97F4A7C15ull);
     const double v = ((double)(u >> 11) * 0x1p-53) * 2.0 - 1.0;

@@ -31,17 +31,18 @@ pytestmark = pytest.mark.gpu
 BYTES = [8, 4, 2, 2, 1, 1]
 
 
-def closed_form_recv(acode, bcode, nb, P, Q, p, q):
-    """sum over i = p (P), l != q (Q) of bytes(A_il) + over j = q (Q), l != p (P)
-    of bytes(B_lj) -- every remote panel tile reaches each consumer rank once"""
+def closed_form_recv(acode, bcode, nb, P, Q, p, q, ro=None, co=None):
+    """sum over owned tile rows i, l != q (Q) of bytes(A_il) + over owned tile
+    columns j, l != p (P) of bytes(B_lj) -- every remote panel tile reaches each consumer
+    rank once (owned = i mod P == p block-cyclic, or ro[i] == p under NEXT-3 ownership)"""
     mt, kt = acode.shape
     nt = bcode.shape[1]
     tot = 0
-    for i in range(p, mt, P):
+    for i in api.owned_tiles(mt, P, p, ro):
         for l in range(kt):
             if l % Q != q:
                 tot += nb * nb * BYTES[acode[i, l]]
-    for j in range(q, nt, Q):
+    for j in api.owned_tiles(nt, Q, q, co):
         for l in range(kt):
             if l % P != p:
                 tot += nb * nb * BYTES[bcode[l, j]]
@@ -76,19 +77,17 @@ def run_single(w, flags=0):
     return res
 
 
-def run_grid(w, P, Q, flags=0, executes=2):
+def run_grid(w, P, Q, flags=0, executes=2, ro=None, co=None):
     """all P*Q ranks on cuda:0, one thread and one stream per rank; returns per-rank
-    (p, q, local C, maps, stats)"""
+    (p, q, local C, maps, stats); ro / co: tile-row / tile-column owners (NEXT-3)"""
     dev = torch.device("cuda:0")
     G = P * Q
     lb = B.gemm_mp_loopback_create(G)
     ranks = []
     for r in range(G):
         p, q = r // Q, r % Q
-        A = api.synth(w.M, w.K, w.nb, w.a, P, Q, p, q, device=dev)
-        Bm = api.synth(w.K, w.N, w.nb, w.b, P, Q, p, q, device=dev)
-        C = api.synth(w.M, w.N, w.nb, w.c, P, Q, p, q, device=dev) if w.beta != 0 else None
-        lr, lc = api.local_shape(w.M, w.N, w.nb, P, Q, p, q)
+        A, Bm, C = api.synth_operands(w, P, Q, p, q, ro, co, device=dev)
+        lr, lc = api.local_c_shape(w, P, Q, p, q, ro, co)
         out = torch.full((lr, lc), float("nan"), dtype=torch.float64, device=dev)
         ranks.append(dict(p=p, q=q, A=A, B=Bm, C=C, out=out, stream=torch.cuda.Stream(dev)))
     torch.cuda.synchronize()
@@ -99,7 +98,7 @@ def run_grid(w, P, Q, flags=0, executes=2):
         try:
             torch.cuda.set_device(dev)
             desc = B.make_desc(w.M, w.N, w.K, w.nb, w.tol, w.alpha, w.beta, w.class_mask,
-                               flags | B.GMP_FLAG_LOOPBACK, P, Q, r)
+                               flags | B.GMP_FLAG_LOOPBACK, P, Q, r, row_owner=ro, col_owner=co)
             g = api.GemmMP(desc, d["A"], d["B"], d["C"], nccl_comm=lb, stream=d["stream"], device=dev)
             g.convert()
             for _ in range(executes):   # the second execute reuses the received panels
@@ -129,15 +128,10 @@ def run_grid(w, P, Q, flags=0, executes=2):
     return res
 
 
-def gather(w, res, P, Q):
-    nb = w.nb
+def gather(w, res, P, Q, ro=None, co=None):
     Cfull = np.full((w.M, w.N), np.nan)
     for (p, q, loc, _, _) in res:
-        ti = np.arange(p, w.M // nb, P)
-        tj = np.arange(q, w.N // nb, Q)
-        rr = (ti[:, None] * nb + np.arange(nb)[None, :]).ravel()
-        cc = (tj[:, None] * nb + np.arange(nb)[None, :]).ravel()
-        Cfull[np.ix_(rr, cc)] = loc
+        api.place_local_c(Cfull, loc, w, P, Q, p, q, ro, co)
     return Cfull
 
 
@@ -194,3 +188,41 @@ def test_loopback_simt_bitwise_vs_oracle(grid):
         assert np.array_equal(maps["ccode"], o["ccode"])
     assert np.array_equal(gather(w, res, P, Q), o["C"])
 
+
+
+@pytest.mark.parametrize("kind", ["small", "uneven"])
+@pytest.mark.parametrize("sender", [False, True], ids=["receiver", "sender"])
+@pytest.mark.parametrize("grid", [(2, 2), (2, 4), (1, 4)], ids=["2x2", "2x4", "1x4"])
+def test_loopback_balanced_ownership_bitwise(grid, sender, kind):
+    """NEXT-3: tile-row / tile-column owners from gemm_mp_balance (computed from the global
+    maps, as every rank does); C gathered through the owners is BITWISE the 1-GPU C, the
+    received bytes follow the closed form with the owners, and the model imbalance never
+    exceeds block-cyclic's"""
+    P, Q = grid
+    w = _workload(kind)
+    C1, m1 = single(kind)
+    d = B.make_desc(w.M, w.N, w.K, w.nb, w.tol, w.alpha, w.beta, w.class_mask, 0, P, Q, 0)
+    ro, co, (imb0, imb1) = B.gemm_mp_balance(d, m1["acode"], m1["bcode"])
+    assert imb1 <= imb0
+    res = run_grid(w, P, Q, B.GMP_FLAG_SENDER_SIDE if sender else 0, ro=ro, co=co)
+    for (p, q, loc, maps, st) in res:
+        for k in ["acode", "bcode", "ccode", "ascale", "bscale"]:
+            assert np.array_equal(m1[k], maps[k]), (p, q, k)
+        want = closed_form_recv(maps["acode"], maps["bcode"], w.nb, P, Q, p, q, ro, co)
+        if sender:
+            assert st["recv_bytes_local"] <= want
+        else:
+            assert st["recv_bytes_local"] == want, (p, q, st["recv_bytes_local"], want)
+    Cg = gather(w, res, P, Q, ro, co)
+    assert np.array_equal(Cg, C1), float(np.nanmax(np.abs(Cg - C1)))
+
+
+def test_loopback_explicit_uneven_owners_bitwise():
+    """an arbitrary (unbalanced, non-cyclic) ownership with an empty process row: rows
+    {0, 1, 2, 4} on process row 0, nothing else but row 3 on process row 1 -- C still bitwise"""
+    w = _workload("uneven")   # 5 x 3 x 7 tiles
+    C1, m1 = single("uneven")
+    ro = np.array([0, 0, 0, 1, 0], np.int32)
+    co = np.array([1, 1, 0], np.int32)
+    res = run_grid(w, 2, 2, 0, ro=ro, co=co)
+    assert np.array_equal(gather(w, res, 2, 2, ro, co), C1)

@@ -2,7 +2,8 @@
 runs tools/multi_gpu_check.py under torchrun on 2 (and 4) GPUs -- maps identical
 to the 1-GPU run, C bitwise identical to the 1-GPU C, received bytes equal to the
 closed form; with GMP_FLAG_SENDER_SIDE (hybrid conversion, NEXT-2)
-the same bitwise C with fewer bytes on NVLink."""
+the same bitwise C with fewer bytes on NVLink; with --balance (NEXT-3) the rank owners come from
+gemm_mp_balance and C is still bitwise the 1-GPU C."""
 import json
 import os
 import socket
@@ -25,17 +26,19 @@ def _port():
 
 
 # grids 1x4 / 4x1: a 4-member row (column) communicator, as in the 2x4 grid of 8 GPUs
-@pytest.mark.parametrize("G,sender,cfg,grid", [(2, False, "small", None), (2, True, "small", None),
-                                               (4, False, "small", None), (4, True, "small", None),
-                                               (2, False, "uneven", None), (4, True, "uneven", None),
-                                               (4, False, "small", "1x4"), (4, True, "uneven", "4x1")])
-def test_summa_bitwise_vs_single_gpu(G, sender, cfg, grid):
+@pytest.mark.parametrize("G,sender,cfg,grid,balance", [
+    (2, False, "small", None, False), (2, True, "small", None, False),
+    (4, False, "small", None, False), (4, True, "small", None, False),
+    (2, False, "uneven", None, False), (4, True, "uneven", None, False),
+    (4, False, "small", "1x4", False), (4, True, "uneven", "4x1", False),
+    (2, False, "small", None, True), (4, True, "small", None, True), (4, False, "uneven", None, True)])
+def test_summa_bitwise_vs_single_gpu(G, sender, cfg, grid, balance):
     if torch.cuda.device_count() < G:
         pytest.skip(f"needs {G} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={G}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
            os.path.join(ROOT, "tools", "multi_gpu_check.py"), "--cfg", cfg] + (["--sender"] if sender else []) + \
-        (["--grid", grid] if grid else [])
+        (["--grid", grid] if grid else []) + (["--balance"] if balance else [])
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]

@@ -36,7 +36,7 @@ def _wire(code, partner_codes):
     return S if S and sum(BY[c] for c in S) < BY[code] else {code}
 
 
-def _worker(rank, G, port, q_out, sender=False):
+def _worker(rank, G, port, q_out, sender=False, balanced=False):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
@@ -57,7 +57,16 @@ def _worker(rank, G, port, q_out, sender=False):
         P, Q = api.default_grid(G)
         p, q = rank // Q, rank % Q
         flags = B.GMP_FLAG_SENDER_SIDE if sender else 0
-        desc = B.make_desc(w.M, w.N, w.K, nb, w.tol, w.alpha, 0.0, w.class_mask, flags, P, Q, rank)
+        ro = co = None
+        if balanced:   # NEXT-3: every rank computes the same owners from the same global maps
+            d0 = B.make_desc(w.M, w.N, w.K, nb, w.tol, w.alpha, 0.0, w.class_mask, flags, P, Q, rank)
+            ro, co, _ = B.gemm_mp_balance(d0, o["acode"], o["bcode"])
+        rows_own = api.owned_tiles(mt, P, p, ro)
+        cols_own = api.owned_tiles(nt, Q, q, co)
+        rowP = [i % P if ro is None else int(ro[i]) for i in range(mt)]
+        colQ = [j % Q if co is None else int(co[j]) for j in range(nt)]
+        desc = B.make_desc(w.M, w.N, w.K, nb, w.tol, w.alpha, 0.0, w.class_mask, flags, P, Q, rank,
+                           row_owner=ro, col_owner=co)
         plan = B.gemm_mp_plan_host(desc, o["acode"], o["bcode"], o["ccode"], o["ascale5"], o["bscale5"])
         st = B.gemm_mp_get_stats(plan)
         rows = [dist.new_group([pp * Q + qq for qq in range(Q)]) for pp in range(P)]
@@ -108,8 +117,8 @@ def _worker(rank, G, port, q_out, sender=False):
         # every operand of every local tile-GEMM is present: its pair class, or the
         # stored class (receiver-side conversion)
         pairs_local = 0
-        for i in range(p, mt, P):
-            for j in range(q, nt, Q):
+        for i in rows_own:
+            for j in cols_own:
                 for l in range(kt):
                     pairs_local += 1
                     ca, cb = int(o["acode"][i, l]), int(o["bcode"][l, j])
@@ -119,16 +128,16 @@ def _worker(rank, G, port, q_out, sender=False):
                         errs.append(f"missing operand for C({i},{j}) l={l}")
         if sender:
             closed = sum(nb * nb * sum(BY[c] for c in _wire(int(o["acode"][i, l]),
-                                                            [o["bcode"][l, j] for j in range(nt) if j % Q != l % Q]))
-                         for i in range(p, mt, P) for l in range(kt) if l % Q != q) + \
+                                                            [o["bcode"][l, j] for j in range(nt) if colQ[j] != l % Q]))
+                         for i in rows_own for l in range(kt) if l % Q != q) + \
                 sum(nb * nb * sum(BY[c] for c in _wire(int(o["bcode"][l, j]),
-                                                       [o["acode"][i, l] for i in range(mt) if i % P != l % P]))
-                    for j in range(q, nt, Q) for l in range(kt) if l % P != p)
+                                                       [o["acode"][i, l] for i in range(mt) if rowP[i] != l % P]))
+                    for j in cols_own for l in range(kt) if l % P != p)
         else:
-            closed = sum(nb * nb * BY[o["acode"][i, l]] for i in range(p, mt, P) for l in range(kt) if l % Q != q) + \
-                sum(nb * nb * BY[o["bcode"][l, j]] for j in range(q, nt, Q) for l in range(kt) if l % P != p)
-        stored_bytes = sum(nb * nb * BY[o["acode"][i, l]] for i in range(p, mt, P) for l in range(kt) if l % Q != q) + \
-            sum(nb * nb * BY[o["bcode"][l, j]] for j in range(q, nt, Q) for l in range(kt) if l % P != p)
+            closed = sum(nb * nb * BY[o["acode"][i, l]] for i in rows_own for l in range(kt) if l % Q != q) + \
+                sum(nb * nb * BY[o["bcode"][l, j]] for j in cols_own for l in range(kt) if l % P != p)
+        stored_bytes = sum(nb * nb * BY[o["acode"][i, l]] for i in rows_own for l in range(kt) if l % Q != q) + \
+            sum(nb * nb * BY[o["bcode"][l, j]] for j in cols_own for l in range(kt) if l % P != p)
         q_out.put(dict(rank=rank, errs=errs, recv=recv, recv_lib=st["recv_bytes_local"], closed=closed,
                        stored_bytes=stored_bytes,
                        pairs_local=sum(st["pairs_local"]), pairs_count=pairs_local, pairs_total=sum(st["pairs"]),
@@ -138,12 +147,14 @@ def _worker(rank, G, port, q_out, sender=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("G,sender", [(2, False), (4, False), (2, True), (4, True), (8, False)])
-def test_summa_schedule_over_gloo(G, sender):
+@pytest.mark.parametrize("G,sender,balanced", [(2, False, False), (4, False, False), (2, True, False),
+                                               (4, True, False), (8, False, False), (4, True, True),
+                                               (8, False, True)])
+def test_summa_schedule_over_gloo(G, sender, balanced):
     ctx = mp.get_context("spawn")
     qo = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, G, port, qo, sender)) for r in range(G)]
+    procs = [ctx.Process(target=_worker, args=(r, G, port, qo, sender, balanced)) for r in range(G)]
     for pr in procs:
         pr.start()
     res = [qo.get(timeout=300) for _ in range(G)]

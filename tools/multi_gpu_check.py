@@ -19,16 +19,16 @@ from paper_2508_14848_b200 import api  # noqa: E402
 from paper_2508_14848_b200 import binding as B  # noqa: E402
 
 
-def closed_form_recv(acode, bcode, nb, P, Q, p, q):
+def closed_form_recv(acode, bcode, nb, P, Q, p, q, row_owner=None, col_owner=None):
     mt, kt = acode.shape
     nt = bcode.shape[1]
     by = [8, 4, 2, 2, 1, 1]
     tot = 0
-    for i in range(p, mt, P):
+    for i in api.owned_tiles(mt, P, p, row_owner):
         for l in range(kt):
             if l % Q != q:
                 tot += nb * nb * by[acode[i, l]]
-    for j in range(q, nt, Q):
+    for j in api.owned_tiles(nt, Q, q, col_owner):
         for l in range(kt):
             if l % P != p:
                 tot += nb * nb * by[bcode[l, j]]
@@ -41,6 +41,8 @@ def main():
     ap.add_argument("--cfg", default="small")
     ap.add_argument("--sender", action="store_true", help="GMP_FLAG_SENDER_SIDE (hybrid conversion, NEXT-2)")
     ap.add_argument("--grid", default=None, help="PxQ process grid (default: api.default_grid)")
+    ap.add_argument("--balance", action="store_true",
+                    help="NEXT-3: owners from gemm_mp_balance on the maps of a block-cyclic plan")
     a = ap.parse_args()
     rank, G = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     lr_ = int(os.environ.get("LOCAL_RANK", rank))
@@ -63,16 +65,23 @@ def main():
     dist.broadcast(t, 0)
     comm = B.gemm_mp_nccl_comm_create(bytes(t.cpu().numpy()), G, rank)
 
-    A = api.synth(w.M, w.K, w.nb, w.a, P, Q, p, q, device=dev)
-    Bm = api.synth(w.K, w.N, w.nb, w.b, P, Q, p, q, device=dev)
-    C = api.synth(w.M, w.N, w.nb, w.c, P, Q, p, q, device=dev) if w.beta != 0 else None
     flags = B.GMP_FLAG_SENDER_SIDE if a.sender else 0
-    desc = B.make_desc(w.M, w.N, w.K, w.nb, w.tol, w.alpha, w.beta, w.class_mask, flags, P, Q, rank)
-    g = api.GemmMP.__new__(api.GemmMP)
-    # distributed plan (GemmMP handles buffers; pass the comm)
-    g.__init__(desc, A, Bm, C, nccl_comm=comm, device=dev)
+    ro = co = None
+    imb = None
+    if a.balance:   # a block-cyclic plan gives the global maps; every rank balances them the same way
+        A0, B0, C0 = api.synth_operands(w, P, Q, p, q, device=dev)
+        d0 = B.make_desc(w.M, w.N, w.K, w.nb, w.tol, w.alpha, w.beta, w.class_mask, flags, P, Q, rank)
+        g0 = api.GemmMP(d0, A0, B0, C0, nccl_comm=comm, device=dev)
+        m0 = g0.maps()
+        g0.close()
+        del A0, B0, C0
+        ro, co, imb = B.gemm_mp_balance(d0, m0["acode"], m0["bcode"])
+    A, Bm, C = api.synth_operands(w, P, Q, p, q, ro, co, device=dev)
+    desc = B.make_desc(w.M, w.N, w.K, w.nb, w.tol, w.alpha, w.beta, w.class_mask, flags, P, Q, rank,
+                       row_owner=ro, col_owner=co)
+    g = api.GemmMP(desc, A, Bm, C, nccl_comm=comm, device=dev)
     g.convert()
-    lr, lc = api.local_shape(w.M, w.N, w.nb, P, Q, p, q)
+    lr, lc = api.local_c_shape(w, P, Q, p, q, ro, co)
     out = torch.full((lr, lc), float("nan"), dtype=torch.float64, device=dev)
     g.execute(out)
     g.execute(out)  # twice: receive slots are refilled every execute
@@ -81,7 +90,7 @@ def main():
     st = g.stats()
     ok = True
     msgs = []
-    want_recv = closed_form_recv(maps["acode"], maps["bcode"], w.nb, P, Q, p, q)
+    want_recv = closed_form_recv(maps["acode"], maps["bcode"], w.nb, P, Q, p, q, ro, co)
     if a.sender:   # hybrid: never more than the stored bytes (the gloo test checks the exact rule)
         if st["recv_bytes_local"] > want_recv:
             ok = False
@@ -96,9 +105,7 @@ def main():
     dist.all_gather_object(outs, (p, q, out.cpu().numpy()))
     if rank == 0:
         # reference: the same library on one GPU (G = 1)
-        Af = api.synth(w.M, w.K, w.nb, w.a, device=dev)
-        Bf = api.synth(w.K, w.N, w.nb, w.b, device=dev)
-        Cf = api.synth(w.M, w.N, w.nb, w.c, device=dev) if w.beta != 0 else None
+        Af, Bf, Cf = api.synth_operands(w, device=dev)
         d1 = B.make_desc(w.M, w.N, w.K, w.nb, w.tol, w.alpha, w.beta, w.class_mask)
         g1 = api.GemmMP(d1, Af, Bf, Cf, device=dev)
         g1.convert()
@@ -112,17 +119,21 @@ def main():
                 msgs.append(f"map {k} differs from 1-GPU")
         F = full.cpu().numpy()
         nb = w.nb
+        Cg = np.full_like(F, np.nan)
         for (pp, qq, loc) in outs:
-            ti = np.arange(pp, w.M // nb, P)
-            tj = np.arange(qq, w.N // nb, Q)
-            rr = (ti[:, None] * nb + np.arange(nb)[None, :]).ravel()
-            cc = (tj[:, None] * nb + np.arange(nb)[None, :]).ravel()
+            rr, cc = api.place_local_c(Cg, loc, w, P, Q, pp, qq, ro, co)
             if not np.array_equal(F[np.ix_(rr, cc)], loc):
                 ok = False
                 diff = np.nanmax(np.abs(F[np.ix_(rr, cc)] - loc))
                 msgs.append(f"C of rank ({pp},{qq}) differs from 1-GPU (max |d| {diff})")
+        if np.isnan(Cg).any():
+            ok = False
+            msgs.append("the ranks' local C tiles do not cover C")
         print(json.dumps({"ok": ok, "G": G, "grid": f"{P}x{Q}", "workload": w.name, "msgs": msgs,
                           "mode": "sender-side (hybrid)" if a.sender else "receiver-side",
+                          "ownership": "balanced (gemm_mp_balance)" if a.balance else "block-cyclic",
+                          "imbalance_model": imb,
+                          "covered": bool(not np.isnan(Cg).any()),
                           "recv_bytes_rank0": st["recv_bytes_local"], "recv_bytes_all": sum(r[0] for r in recv_all),
                           "stored_bytes_all": sum(r[1] for r in recv_all), "pairs": st["pairs"]}), flush=True)
     flag = torch.tensor([0 if ok else 1], device=dev)
