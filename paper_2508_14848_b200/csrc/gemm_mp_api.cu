@@ -8,7 +8,10 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <algorithm>
+#include <chrono>
 #include <condition_variable>
 #include <cmath>
 #include <memory>
@@ -16,6 +19,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "gmp_common.cuh"
@@ -29,6 +33,22 @@
 #include "gmp_layout.h"
 
 using namespace gmp;
+
+// NVTX ranges (per phase, SUMMA step and class launch).  Header-only NVTX v3:
+// a no-op unless a tool (nsys, ncu --nvtx) injects itself.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  NvtxRange(const char* what, int step, int cls) {
+    static const char* names[] = {"FP64", "FP32", "FP16", "BF16", "E4M3", "E5M2"};
+    char buf[64];
+    if (cls >= 0) snprintf(buf, sizeof buf, "gmp:%s step %d class %s", what, step, names[cls % 6]);
+    else snprintf(buf, sizeof buf, "gmp:%s step %d", what, step);
+    nvtxRangePushA(buf);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // ---------------------------------------------------------------------------
 // error handling
@@ -257,6 +277,9 @@ struct gmp_plan_s {
   bool converted = false;
   bool executed = false;
   bool host_only = false;   // gemm_mp_plan_host: no operands, no statistics, no communicators
+  bool aborted = false;     // the watchdog aborted this plan's row / column communicators
+  cudaEvent_t done_ev = nullptr;   // recorded at the end of convert / execute (watchdog polls it)
+  bool done_rec = false;
   struct Loopback* lb = nullptr;   // GMP_FLAG_LOOPBACK: in-process transport (tests only)
   gmp_stats_t st{};
 };
@@ -1047,6 +1070,7 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
   GMP_TRY(check_desc(desc));
   if (!out) return fail(GMP_ERR_ARG, "out is NULL");
   *out = nullptr;
+  NvtxRange nv_plan("gmp:plan");
   const gmp_desc_t& d = *desc;
   const int G = d.P * d.Q;
   if ((G > 1) != (nccl_comm != nullptr)) return fail(GMP_ERR_GRID, "nccl_comm must be non-NULL iff P*Q > 1");
@@ -1203,6 +1227,7 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
   build_tables(pl);
   pl->step_ev.resize(pl->st.steps);
   for (auto& e : pl->step_ev) GMP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  GMP_CUDA(cudaEventCreateWithFlags(&pl->done_ev, cudaEventDisableTiming));
   if (d.flags & GMP_FLAG_TIMING) {
     pl->launch_ev.resize(2 * pl->launches.size());
     for (auto& e : pl->launch_ev) GMP_CUDA(cudaEventCreate(&e));
@@ -1308,6 +1333,7 @@ static int grid_for(int64_t n_elems, int per_thread) {
 // step_ev[s] gates the step's class launches on the compute stream.
 static gmp_status_t issue_comm_step(gmp_plan_s* pl, uint8_t* ws, int s) {
   const int64_t nb = pl->d.nb;
+  NvtxRange nv("SUMMA broadcast", s, -1);
   if (pl->lb) {
     // loopback: each receiver copies the root's payload slot (the root sends nothing)
     int last_root = -1;
@@ -1353,9 +1379,76 @@ static gmp_status_t issue_comm_step(gmp_plan_s* pl, uint8_t* ws, int s) {
   return GMP_OK;
 }
 
+// ---------------------------------------------------------------------------
+// NCCL watchdog (failure detection).  convert / execute record done_ev at
+// their end; gemm_mp_sync on a multi-GPU plan polls it together with
+// ncclCommGetAsyncError of the world, row and column communicators instead of
+// blocking in cudaDeviceSynchronize.  An asynchronous NCCL error, or no progress
+// within GMP_WATCHDOG_S seconds (default 900; 0 = wait forever), aborts the
+// library-owned row / column communicators (ncclCommAbort: their pending
+// broadcasts return, so the streams drain) and returns GMP_ERR_NCCL; the plan then
+// refuses convert / execute.  The world communicator is the caller's to abort.
+// ---------------------------------------------------------------------------
+static gmp_status_t record_done(gmp_plan_s* pl, cudaStream_t stream) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  GMP_CUDA(cudaStreamIsCapturing(stream, &cs));
+  if (cs != cudaStreamCaptureStatusNone) return GMP_OK;   // graph capture: nothing to poll
+  GMP_CUDA(cudaEventRecord(pl->done_ev, stream));
+  pl->done_rec = true;
+  return GMP_OK;
+}
+
+static double watchdog_seconds() {
+  const char* e = getenv("GMP_WATCHDOG_S");
+  return e ? atof(e) : 900.0;
+}
+
+static gmp_status_t abort_grid(gmp_plan_s* pl, const std::string& why) {
+  {
+    std::lock_guard<std::mutex> lk(g_grid_mu);
+    for (size_t k = 0; k < g_grid_comms.size();) {
+      GridComms& g = g_grid_comms[k];
+      if (g.world == pl->world) {
+        ncclCommAbort(g.rowc);
+        ncclCommAbort(g.colc);
+        g_grid_comms.erase(g_grid_comms.begin() + k);   // the comm stream is left to the process
+      } else {
+        ++k;
+      }
+    }
+  }
+  pl->rowc = pl->colc = nullptr;
+  pl->aborted = true;
+  return fail(GMP_ERR_NCCL, why + " -- row/column communicators aborted; abort the world communicator too");
+}
+
+static gmp_status_t watchdog_wait(gmp_plan_s* pl) {
+  const double limit = watchdog_seconds();
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaEventQuery(pl->done_ev);
+    if (q == cudaSuccess) return GMP_OK;
+    if (q != cudaErrorNotReady) GMP_CUDA(q);
+    for (ncclComm_t c : {pl->world, pl->rowc, pl->colc}) {
+      if (!c) continue;
+      ncclResult_t ar = ncclSuccess;
+      if (ncclCommGetAsyncError(c, &ar) != ncclSuccess) continue;
+      if (ar != ncclSuccess && ar != ncclInProgress)
+        return abort_grid(pl, std::string("watchdog: asynchronous NCCL error: ") + ncclGetErrorString(ar));
+    }
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (limit > 0 && el > limit)
+      return abort_grid(pl, "watchdog: convert/execute did not complete within " + std::to_string(limit) +
+                                " s (GMP_WATCHDOG_S)");
+    std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
+}
+
 extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_bytes, void* stream_) {
   if (!pl) return fail(GMP_ERR_ARG, "plan is NULL");
   if (pl->host_only) return fail(GMP_ERR_STATE, "host-built plan (gemm_mp_plan_host): no operands to convert");
+  if (pl->aborted) return fail(GMP_ERR_STATE, "the watchdog aborted this plan's communicators");
+  NvtxRange nv_conv("gmp:convert");
   if (!ws_ || (int64_t)ws_bytes < pl->ws_bytes) return fail(GMP_ERR_WORKSPACE, "workspace too small");
   if ((uintptr_t)ws_ & 1023) return fail(GMP_ERR_ARG, "workspace must be 1024-byte aligned");
   cudaStream_t stream = (cudaStream_t)stream_;
@@ -1413,6 +1506,7 @@ extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_byte
         (const SliceJob*)(ws + pl->off_slice), ws, (int)nb);
     GMP_CUDA(cudaGetLastError());
   }
+  GMP_TRY(record_done(pl, stream));
   pl->converted = true;
   return GMP_OK;
 }
@@ -1421,6 +1515,8 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
   if (!pl) return fail(GMP_ERR_ARG, "plan is NULL");
   if (pl->host_only) return fail(GMP_ERR_STATE, "host-built plan (gemm_mp_plan_host) cannot execute");
   if (!pl->converted) return fail(GMP_ERR_STATE, "execute before convert");
+  if (pl->aborted) return fail(GMP_ERR_STATE, "the watchdog aborted this plan's communicators");
+  NvtxRange nv_exec("gmp:execute");
   const int64_t nb = pl->d.nb, nb2 = nb * nb;
   const int64_t nCl = (int64_t)pl->locC.size();
   const int64_t ntl = count_owned(pl->lay.colQ, pl->q);
@@ -1472,9 +1568,11 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
   }
   size_t li = 0;
   for (int s = 0; s < steps; ++s) {
+    NvtxRange nv_step("execute", s, -1);
     if (multi) GMP_CUDA(cudaStreamWaitEvent(stream, pl->step_ev[s], 0));
     for (; li < pl->launches.size() && pl->launches[li].step == s; ++li) {
       const Launch& L = pl->launches[li];
+      NvtxRange nv_cls("tile-GEMMs", s, L.cls);
       const WorkItem* it = (const WorkItem*)(ws + pl->off_items) + L.ibeg;
       const PairDesc* pd = (const PairDesc*)(ws + pl->off_pairs);
       if (!pl->launch_ev.empty()) GMP_CUDA(cudaEventRecord(pl->launch_ev[2 * li], stream));
@@ -1531,12 +1629,14 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
         dct, ws, mb, (int16_t*)(ws + pl->off_cscale), Cuser, ldc, (int)nb);
     GMP_CUDA(cudaGetLastError());
   }
+  GMP_TRY(record_done(pl, stream));
   pl->executed = true;
   return GMP_OK;
 }
 
 extern "C" gmp_status_t gemm_mp_sync(gmp_plan_t pl) {
   if (!pl) return fail(GMP_ERR_ARG, "plan is NULL");
+  if (pl->world && pl->done_rec) GMP_TRY(watchdog_wait(pl));
   GMP_CUDA(cudaDeviceSynchronize());
   GMP_CUDA(cudaGetLastError());
   if (pl->world) {
@@ -1775,6 +1875,7 @@ extern "C" void gemm_mp_destroy(gmp_plan_t pl) {
   if (!pl) return;
   for (auto& e : pl->step_ev) if (e) cudaEventDestroy(e);
   if (pl->packed_ev) cudaEventDestroy(pl->packed_ev);
+  if (pl->done_ev) cudaEventDestroy(pl->done_ev);
   for (auto& e : pl->launch_ev) if (e) cudaEventDestroy(e);
   tc_release(pl->tc);
   if (pl->lb) {

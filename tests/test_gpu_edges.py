@@ -104,6 +104,39 @@ def test_fp32_split_parts_are_exact():
     assert checked > 0
 
 
+def test_fp32_split_wide_dynamic_range_limit():
+    """The exactness limit of the BF16x3 split (FP32 class): BF16 has
+    FP32's exponent range, so x2 = x - x0 - x1 is representable only down to the BF16
+    subnormal quantum 2^-133.  With FP32 tiles scaled to max <= 1 (R10), elements with
+    |x| >= 2^-110 split EXACTLY; below that the parts differ from x by at most 2^-134
+    (half the BF16 subnormal quantum).  Checked on tiles whose elements span 2^0 .. 2^-140."""
+    nb = 128
+    rng = np.random.default_rng(5)
+    A = rng.uniform(0.5, 1.0, (256, 256)) * rng.choice([-1, 1], (256, 256)) * \
+        2.0 ** -rng.integers(0, 141, (256, 256)).astype(np.float64)
+    A[0, 0] = 1.0   # tile max 1: scale 0 (the payload IS x)
+    Bm = A.T.copy()
+    fp32 = (np.ones((2, 2), np.uint8), np.ones((2, 2), np.uint8), np.zeros((2, 2), np.uint8))
+    g, _ = run_gpu(A, Bm, None, nb, 1e-6, 1.0, 0.0, 0b00011, maps=fp32)
+    small = exact = 0
+    for which, X in (("A", A), ("B", Bm)):
+        for ti in range(2):
+            for tj in range(2):
+                parts, sc = g.tile(which, ti, tj, B.TILE_SPLIT)
+                stored, sc32 = g.tile(which, ti, tj, 1)
+                v = oracle.payload_values(stored.view(np.uint32), 1).reshape(nb, nb)   # MN-major payload
+                want = v.T
+                pv = [oracle.decode(parts.view(np.uint16)[k * nb * nb:(k + 1) * nb * nb].astype(np.uint32), 3)
+                      .reshape(nb, nb) for k in range(3)]
+                got = pv[0] + pv[1] + pv[2]            # exact in binary64 (disjoint bit ranges)
+                big = np.abs(want) >= 2.0 ** -110
+                assert np.array_equal(got[big], want[big])
+                assert np.all(np.abs(got[~big] - want[~big]) <= 2.0 ** -134)
+                exact += int(big.sum())
+                small += int((~big & (want != 0)).sum())
+    assert small > 1000 and exact > 1000, (small, exact)
+
+
 def test_rectangular_many_tiles_sampled_vs_oracle():
     """cfg5-shaped (K >> M, N) at reduced size: sampled C tiles vs the oracle"""
     w = gmp_inputs.small_workload(512, 512, 4096, 128, 1e-4, mode="random", E=16, beta=0.0, seed=7)
