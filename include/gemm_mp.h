@@ -49,14 +49,16 @@ extern "C" {
 /* Precision classes, ordered by unit roundoff; the class
  * of a tile-GEMM is max(code_A, code_B) = the lower of its operands' precisions
  * (north_star; R6). */
-typedef enum { GMP_FP64 = 0, GMP_FP32 = 1, GMP_FP16 = 2, GMP_BF16 = 3, GMP_E4M3 = 4, GMP_E5M2 = 5 } gmp_class_t;
-#define GMP_NCLASS_ABI 6   /* classes; ordered by unit roundoff, so a pair's class is max(code_A, code_B) */
+typedef enum { GMP_FP64 = 0, GMP_FP32 = 1, GMP_FP16 = 2, GMP_BF16 = 3, GMP_E4M3 = 4, GMP_E5M2 = 5,
+               GMP_MXFP4 = 6 /* OCP MXFP4: E2M1 + E8M0 scale per 32 K-elements; A/B only (R31) */
+} gmp_class_t;
+#define GMP_NCLASS_ABI 7   /* classes; ordered by unit roundoff, so a pair's class is max(code_A, code_B) */
 
 typedef enum {
   GMP_OK = 0,
   GMP_ERR_ARG = 1,           /* null/invalid argument, tol <= 0 or not finite, ld too small */
   GMP_ERR_NOT_DIVISIBLE = 2, /* nb does not divide M, N or K, or nb is not a multiple of 128 */
-  GMP_ERR_MAP_SHAPE = 3,     /* explicit map holds a code > 5                                  */
+  GMP_ERR_MAP_SHAPE = 3,     /* explicit map holds a code > 6                                  */
   GMP_ERR_NONFINITE = 4,     /* A, B (or C with beta != 0) holds a NaN or an infinity          */
   GMP_ERR_GRID = 5,          /* P*Q, rank and communicator are inconsistent                    */
   GMP_ERR_WORKSPACE = 6,     /* scratch or workspace smaller than the size query returned      */
@@ -117,8 +119,8 @@ typedef struct {
   int32_t nb;          /* tile edge; multiple of 128 dividing M, N, K (PAPER.md:179 uses 1024/2048) */
   double tol;          /* accuracy tolerance: ||C - C_fp64||_F <= tol (|a| ||A|| ||B|| + |b| ||C||) */
   double alpha, beta;  /* GEMM scalars; beta == 0 means C is not read (BLAS convention)          */
-  uint32_t class_mask; /* bit c enables class c (gmp_class_t); FP64 always on; E4M3/E5M2 opt-in;
-                          bits above 5 are ignored                                           */
+  uint32_t class_mask; /* bit c enables class c (gmp_class_t); FP64 always on; E4M3/E5M2/MXFP4 opt-in;
+                          bits above 6 are ignored                                           */
   uint32_t flags;      /* GMP_FLAG_*                                                           */
   int32_t P, Q, rank;  /* process grid and this rank (= p*Q + q); 1, 1, 0 on one GPU            */
   /* optional explicit per-tile codes (host, row-major global tile grids: mt x kt, kt x nt,
@@ -137,20 +139,20 @@ typedef struct gmp_plan_s *gmp_plan_t;
 /* Run statistics (gemm_mp_get_stats). Counts are global (identical on every rank)
  * except the *_local fields. */
 typedef struct {
-  int64_t tiles_a[6], tiles_b[6], tiles_c[6]; /* tiles per stored class                  */
-  int64_t pairs[6];                           /* tile-GEMMs per pair class (global)      */
-  double flops[6];                            /* 2 nb^3 x pairs[c]                       */
-  int64_t pairs_local[6];                     /* tile-GEMMs this rank computes            */
-  int64_t shadows_local[6];                   /* shadow tiles this rank materialises      */
+  int64_t tiles_a[7], tiles_b[7], tiles_c[7]; /* tiles per stored class                  */
+  int64_t pairs[7];                           /* tile-GEMMs per pair class (global)      */
+  double flops[7];                            /* 2 nb^3 x pairs[c]                       */
+  int64_t pairs_local[7];                     /* tile-GEMMs this rank computes            */
+  int64_t shadows_local[7];                   /* shadow tiles this rank materialises      */
   int64_t packed_bytes_local;                 /* packed A/B payload bytes stored locally  */
   int64_t recv_bytes_local;                   /* SUMMA panel bytes this rank receives     */
   int64_t workspace_bytes;
   int32_t steps;                              /* SUMMA steps (K tiles / step depth)        */
   int32_t launches_execute;                   /* kernels one gemm_mp_execute launches      */
   int32_t launches_plan, launches_convert;    /* kernels of gemm_mp_plan / gemm_mp_convert */
-  double class_ms[6];                         /* GMP_FLAG_TIMING: device ms of the class-c tile-GEMM
+  double class_ms[7];                         /* GMP_FLAG_TIMING: device ms of the class-c tile-GEMM
                                                  launches of the last execute (waits for them) */
-  int32_t class_launches[6];                  /* launches per class in one execute             */
+  int32_t class_launches[7];                  /* launches per class in one execute             */
 } gmp_stats_t;
 
 /* Device scratch needed by gemm_mp_plan (tile statistics + maps; KB-sized).     */
@@ -226,7 +228,7 @@ gmp_status_t gemm_mp_get_tile_stats(gmp_plan_t plan, char which, double *S, doub
 
 /* Host-only plan from given maps (no device work): the same tile lists, arena
  * layout, work lists and SUMMA schedule as gemm_mp_plan builds after its map
- * kernels.  acode/bcode/ccode: global code grids; ascale5/bscale5: [tile][6]
+ * kernels.  acode/bcode/ccode: global code grids; ascale5/bscale5: [tile][7]
  * class-c scales; cin_scale may be NULL.  For inspecting the schedule and the
  * multi-rank bookkeeping without a GPU: it holds no operands, statistics or
  * communicators, so gemm_mp_convert / gemm_mp_execute / gemm_mp_get_tile_stats
@@ -282,9 +284,9 @@ gmp_status_t gemm_mp_synth_tiles(double *out, int64_t ld, int64_t rows, int64_t 
  * chooses tile-row owners row_owner[mt] in [0, P) and tile-column owners
  * col_owner[nt] in [0, Q) (desc->P, desc->Q) that minimise the largest per-rank
  * cost = sum over the rank's C tiles (i, j) of sum_l cost[max(codeA(i,l),
- * codeB(l,j))] + cost[6] x (A + B + C tiles it owns), by alternating row / column
+ * codeB(l,j))] + cost[7] x (A + B + C tiles it owns), by alternating row / column
  * local search (moves and swaps) from the block-cyclic start (R30).
- * cost: 7 doubles (relative per-pair time of classes 0..5, per-owned-tile time) or
+ * cost: 8 doubles (relative per-pair time of classes 0..6, per-owned-tile time) or
  * NULL for the built-in B200 model.  Deterministic: every rank gets the same
  * owners from the same maps.  imbalance (may be NULL): {max/mean rank cost of the
  * block-cyclic layout, of the returned layout} -- never worse than block-cyclic.

@@ -64,6 +64,10 @@ def lib():
         L.orc_gemm_mp.argtypes = [vp, vp, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp]
         L.orc_max_threads.restype = ct.c_int
         L.orc_class_bytes.restype = ct.c_int; L.orc_class_bytes.argtypes = [ct.c_int]
+        L.orc_payload_bytes.restype = i64; L.orc_payload_bytes.argtypes = [ct.c_int, i32]
+        L.orc_mx_block_exp.restype = ct.c_int; L.orc_mx_block_exp.argtypes = [dbl]
+        L.orc_mx_encode.argtypes = [vp, i32, vp]
+        L.orc_payload_value.restype = dbl; L.orc_payload_value.argtypes = [vp, i32, i64, ct.c_int]
         _lib = L
     return _lib
 
@@ -72,9 +76,15 @@ def _p(a):
     return a.ctypes.data_as(ct.c_void_p) if a is not None else None
 
 
-PAYLOAD_DTYPE = {0: np.uint64, 1: np.uint32, 2: np.uint16, 3: np.uint16, 4: np.uint8, 5: np.uint8}
-CLASS_NAMES = ["FP64", "FP32", "FP16", "BF16", "E4M3", "E5M2"]
+PAYLOAD_DTYPE = {0: np.uint64, 1: np.uint32, 2: np.uint16, 3: np.uint16, 4: np.uint8, 5: np.uint8, 6: np.uint8}
+CLASS_NAMES = ["FP64", "FP32", "FP16", "BF16", "E4M3", "E5M2", "MX4"]
 NCLS = len(CLASS_NAMES)
+MX = 6   # MXFP4: E2M1 elements + one E8M0 scale per 32 K-elements (R31)
+
+
+def payload_len(cls, nb):
+    """elements of the payload array (PAYLOAD_DTYPE[cls]) of one nb x nb tile"""
+    return int(lib().orc_payload_bytes(cls, nb)) if cls == MX else nb * nb
 
 
 # ---- O1 generator -----------------------------------------------------------
@@ -152,22 +162,43 @@ def pack_tile(tile, cls, scale, transpose=False, role=None):
     nb = t.shape[0]
     if role is not None:
         transpose = layout_transposed(role, cls)
-    out = np.empty(nb * nb, dtype=PAYLOAD_DTYPE[cls])
+    out = np.empty(payload_len(cls, nb), dtype=PAYLOAD_DTYPE[cls])
     lib().orc_pack_tile(_p(t), nb, nb, cls, scale, int(transpose), _p(out))
     return out
 
 
 def shadow_tile(payload, nb, frm, frm_scale, to, role="A"):
-    out = np.empty(nb * nb, dtype=PAYLOAD_DTYPE[to])
+    out = np.empty(payload_len(to, nb), dtype=PAYLOAD_DTYPE[to])
     p = np.ascontiguousarray(payload)
     e = lib().orc_shadow_tile(_p(p), nb, ROLE.get(role, role), frm, frm_scale, to, _p(out))
     return out, int(e)
 
 
-def payload_values(payload, cls):
+def payload_values(payload, cls, nb=None):
+    """exact values (scaled units) in payload-index order; MXFP4 needs nb"""
     if cls == 0:
         return np.ascontiguousarray(payload).view(np.float64).copy()
+    if cls == MX:
+        p = np.ascontiguousarray(payload, np.uint8)
+        n = nb * nb
+        q = np.empty(n, np.uint32)
+        q[0::2] = p[:n // 2] & 15
+        q[1::2] = p[:n // 2] >> 4
+        s = p[n // 2:n // 2 + n // 32].astype(np.int64) - 127
+        return decode(q, MX) * np.ldexp(1.0, np.repeat(s, 32))
     return decode(payload.astype(np.uint32), cls)
+
+
+def mx_block_exp(amax):
+    return int(lib().orc_mx_block_exp(float(amax)))
+
+
+def mx_encode(y, nb):
+    """O6 MXFP4 block encoding of values y (scaled units, payload-index order)"""
+    y = np.ascontiguousarray(y, np.float64).ravel()
+    out = np.empty(payload_len(MX, nb), np.uint8)
+    lib().orc_mx_encode(_p(y), nb, _p(out))
+    return out
 
 
 # ---- O8 / O9 ----------------------------------------------------------------

@@ -104,7 +104,8 @@ typedef struct {
     int bytes;
 } orc_fmt_t;
 
-#define ORC_NCLS 6
+#define ORC_NCLS 7
+#define ORC_MX 6   /* MXFP4 (OCP MX: E2M1 elements, one E8M0 scale per 32 K-elements), R31 */
 static const orc_fmt_t ORC_FMT[ORC_NCLS] = {
     /* FP64 */ {52, 11, 1023, -1022, 0x1.fffffffffffffp+1023, 0, 0x1p-53, 0x1p-1074, 0.0, 8},
     /* FP32 */ {23, 8, 127, -126, 0x1.fffffep+127, 0, 0x1p-24, 0x1p-149, 1.0, 4},
@@ -112,9 +113,17 @@ static const orc_fmt_t ORC_FMT[ORC_NCLS] = {
     /* BF16 */ {7, 8, 127, -126, 0x1.fep+127, 0, 0x1p-8, 0x1p-133, 1.0, 2},
     /* E4M3 */ {3, 4, 7, -6, 448.0, 1, 0x1p-4, 0x1p-9, 448.0, 1},
     /* E5M2 */ {2, 5, 15, -14, 57344.0, 0, 0x1p-3, 0x1p-16, 57344.0, 1},
+    /* MXFP4 element E2M1: no inf/NaN, max 6, subnormal 0.5; bytes: see orc_payload_bytes */
+    /* MX4  */ {1, 2, 1, 0, 6.0, 1, 0x1p-2, 0.5, 1.0, 0},
 };
 
 int orc_class_bytes(int cls) { return ORC_FMT[cls].bytes; }
+/* bytes of one nb x nb payload: nb^2 x bytes, or for MXFP4 nb^2/2 element bytes (two
+ * E2M1 codes per byte) followed by nb^2/32 E8M0 scale bytes (R31) */
+int64_t orc_payload_bytes(int cls, int32_t nb) {
+    int64_t n = (int64_t)nb * nb;
+    return cls == ORC_MX ? n / 2 + n / 32 : n * ORC_FMT[cls].bytes;
+}
 double orc_class_u(int cls) { return ORC_FMT[cls].u; }
 double orc_class_eta(int cls) { return ORC_FMT[cls].eta; }
 double orc_class_omega_scale(int cls) { return ORC_FMT[cls].omega_s; }
@@ -135,10 +144,10 @@ static double orc_rne_abs(double a, const orc_fmt_t *f) {
     return ldexp(fl, q);          /* exact: fl has at most p+2 bits            */
 }
 
-/* Encode binary64 x into class cls (1..4) with one RNE rounding; bits in the
+/* Encode binary64 x into class cls (1..6) with one RNE rounding; bits in the
  * low bytes of the return value. NaN -> canonical NaN; overflow -> inf (FP32,
- * FP16, BF16) or saturate to +-448 (E4M3, "satfinite"; unreachable after the
- * per-tile scaling of DESIGN.md R10). */
+ * FP16, BF16, E5M2) or saturate to +-448 (E4M3, "satfinite") / +-6 (E2M1, the MXFP4
+ * element, which has no inf/NaN); both unreachable after the scaling of R10 / R31. */
 uint32_t orc_encode(double x, int cls) {
     const orc_fmt_t *f = &ORC_FMT[cls];
     uint32_t sign = signbit(x) ? 1u : 0u;
@@ -180,7 +189,7 @@ double orc_decode(uint32_t bits, int cls) {
     uint32_t mant = bits & ((1u << f->p) - 1u);
     double v;
     if (cls == 4 && biased == expmax && mant == 7u) v = NAN;
-    else if (cls != 4 && biased == expmax) v = mant ? NAN : INFINITY;
+    else if (cls != 4 && cls != ORC_MX && biased == expmax) v = mant ? NAN : INFINITY;
     else if (biased == 0) v = ldexp((double)mant, f->emin - f->p);
     else v = ldexp((double)(mant + (1u << f->p)), (int)biased - f->bias - f->p);
     return sign ? -v : v;
@@ -202,6 +211,42 @@ int orc_scale_exp(double maxabs, int cls) {
     while (!(ldexp(maxabs, e) <= ORC_FMT[cls].omega_s)) --e;
     while (ldexp(maxabs, e + 1) <= ORC_FMT[cls].omega_s) ++e;
     return e;
+}
+
+/* O3 for the MXFP4 block scale (reading R31): the smallest integer s >= -127 with
+ * amax <= 6 * 2^s (6 = largest E2M1 value), so no element of the block saturates;
+ * amax == 0 -> -127.  Stored as the E8M0 byte s + 127. */
+int orc_mx_block_exp(double amax) {
+    if (amax == 0.0) return -127;
+    int E;
+    (void)frexp(amax, &E);
+    int s = E - 2;
+    while (s > -127 && ldexp(6.0, s - 1) >= amax) --s;
+    while (ldexp(6.0, s) < amax) ++s;
+    return s < -127 ? -127 : s;
+}
+
+/* O6 for MXFP4: y[idx] (scaled units, payload-index order idx = mn*nb + k, K-major)
+ * -> payload: block b = idx / 32 (32 consecutive K-elements of one row) gets
+ * s_b = orc_mx_block_exp(max |y| over the block); element code q = RN_E2M1(y 2^-s_b)
+ * in nibble idx (byte idx/2, low nibble for even idx); E8M0 byte s_b + 127 at
+ * offset nb^2/2 + b. */
+void orc_mx_encode(const double *y, int32_t nb, uint8_t *payload) {
+    int64_t n = (int64_t)nb * nb;
+    for (int64_t b = 0; b < n / 32; ++b) {
+        double amax = 0.0;
+        for (int v = 0; v < 32; ++v) {
+            double a = fabs(y[b * 32 + v]);
+            if (a > amax) amax = a;
+        }
+        int sb = orc_mx_block_exp(amax);
+        payload[n / 2 + b] = (uint8_t)(sb + 127);
+        for (int v = 0; v < 32; v += 2) {
+            uint32_t q0 = orc_encode(ldexp(y[b * 32 + v], -sb), ORC_MX);
+            uint32_t q1 = orc_encode(ldexp(y[b * 32 + v + 1], -sb), ORC_MX);
+            payload[(b * 32 + v) / 2] = (uint8_t)((q0 & 15u) | ((q1 & 15u) << 4));
+        }
+    }
 }
 
 /* ------------------------------------------------------------------------- */
@@ -259,10 +304,10 @@ void orc_tile_stats(const double *X, int64_t ld, int64_t mt, int64_t nt, int32_t
 
 /* ------------------------------------------------------------------------- */
 /* O5. Precision map for an input matrix A or B (O5, readings R1-R5, */
-/*     R13, R14).  Ladder: E5M2, E4M3, BF16, FP16, FP32, FP64 (enabled classes;  */
-/*     lowest precision first); first eligible wins.                           */
+/*     R13, R14, R31).  Ladder: MXFP4, E5M2, E4M3, BF16, FP16, FP32, FP64        */
+/*     (enabled classes; lowest precision first); first eligible wins.         */
 /* ------------------------------------------------------------------------- */
-static const int ORC_LADDER[ORC_NCLS] = {5, 4, 3, 2, 1, 0};
+static const int ORC_LADDER[ORC_NCLS] = {6, 5, 4, 3, 2, 1, 0};
 
 /* delta_k = u_k + sqrt(nb) * u_acc(k); u_acc = u64 for FP64, u32 otherwise */
 double orc_delta(int cls, int32_t nb) {
@@ -293,8 +338,12 @@ int orc_map_input(int64_t mt, int64_t nt, int32_t nb, double tol, uint32_t class
                 if (k == 0) { chosen = 0; break; }
                 if (maxabs[t] == 0.0) { chosen = k; break; }
                 int e = orc_scale_exp(maxabs[t], k);
+                /* underflow term: nb x half the subnormal quantum of the tile's scaled
+                 * grid; for MXFP4 the quantum of the block holding the tile's max
+                 * (every block's scale is <= it; R31) */
+                int qe = k == ORC_MX ? orc_mx_block_exp(ldexp(maxabs[t], e)) : 0;
                 double lhs = orc_delta(k, nb) * sqrt(S[t]) +
-                             (double)nb * ldexp(ORC_FMT[k].eta, -e - 1);
+                             (double)nb * ldexp(ORC_FMT[k].eta, qe - e - 1);
                 if (lhs <= rhs) { chosen = k; break; }
             }
         }
@@ -307,7 +356,7 @@ int orc_map_input(int64_t mt, int64_t nt, int32_t nb, double tol, uint32_t class
 /* ------------------------------------------------------------------------- */
 /* O6. Packing and receiver-side shadows (O6, R7).     */
 /* ------------------------------------------------------------------------- */
-static void orc_store_elem(void *payload, int64_t idx, int cls, double x) {
+static void orc_store_elem(void *payload, int64_t idx, int cls, double x) {   /* cls != MX */
     if (cls == 0) { ((double *)payload)[idx] = x; return; }
     uint32_t b = orc_encode(x, cls);
     if (cls == 1) ((uint32_t *)payload)[idx] = b;
@@ -315,9 +364,16 @@ static void orc_store_elem(void *payload, int64_t idx, int cls, double x) {
     else ((uint16_t *)payload)[idx] = (uint16_t)b;
 }
 
-/* exact binary64 value of payload element idx (scaled units) */
-double orc_payload_value(const void *payload, int64_t idx, int cls) {
+/* exact binary64 value of payload element idx (scaled units); nb locates the
+ * MXFP4 scale bytes (value = E2M1(q) x 2^s_b) */
+double orc_payload_value(const void *payload, int32_t nb, int64_t idx, int cls) {
     if (cls == 0) return ((const double *)payload)[idx];
+    if (cls == ORC_MX) {
+        const uint8_t *p = (const uint8_t *)payload;
+        uint32_t q = (p[idx / 2] >> (4 * (idx & 1))) & 15u;
+        int sb = (int)p[(int64_t)nb * nb / 2 + idx / 32] - 127;
+        return ldexp(orc_decode(q, ORC_MX), sb);
+    }
     uint32_t b;
     if (cls == 1) b = ((const uint32_t *)payload)[idx];
     else if (cls >= 4) b = ((const uint8_t *)payload)[idx];
@@ -338,9 +394,19 @@ int orc_layout_transposed(int role, int cls) {
 }
 
 /* Stored payload of one tile: element (r,c) of the tile is RN_cls(x(r,c) 2^scale),
- * written at the index given by `transpose` (see orc_layout_transposed). */
+ * written at the index given by `transpose` (see orc_layout_transposed); MXFP4:
+ * y = x 2^scale block-encoded by orc_mx_encode. */
 void orc_pack_tile(const double *X, int64_t ld, int32_t nb, int cls, int scale,
                    int transpose, void *payload) {
+    if (cls == ORC_MX) {
+        double *y = (double *)malloc(sizeof(double) * nb * nb);
+        for (int32_t r = 0; r < nb; ++r)
+            for (int32_t c = 0; c < nb; ++c)
+                y[transpose ? (int64_t)c * nb + r : (int64_t)r * nb + c] = ldexp(X[(int64_t)r * ld + c], scale);
+        orc_mx_encode(y, nb, (uint8_t *)payload);
+        free(y);
+        return;
+    }
     for (int32_t r = 0; r < nb; ++r)
         for (int32_t c = 0; c < nb; ++c) {
             double x = X[(int64_t)r * ld + c];
@@ -358,19 +424,23 @@ int orc_shadow_tile(const void *payload, int32_t nb, int role, int from, int fro
     int64_t n = (int64_t)nb * nb;
     double m = 0.0;
     for (int64_t i = 0; i < n; ++i) {
-        double a = fabs(orc_payload_value(payload, i, from));
+        double a = fabs(orc_payload_value(payload, nb, i, from));
         if (a > m) m = a;
     }
     /* decoded tile = w * 2^-from_scale; its scale for class `to` is
      * orc_scale_exp(m * 2^-from_scale, to) = from_scale + orc_scale_exp(m, to)  */
     int d = orc_scale_exp(m, to);
     int tf = orc_layout_transposed(role, from), tt = orc_layout_transposed(role, to);
+    double *y = to == ORC_MX ? (double *)malloc(sizeof(double) * n) : NULL;
     for (int32_t r = 0; r < nb; ++r)
         for (int32_t c = 0; c < nb; ++c) {
             int64_t src = tf ? (int64_t)c * nb + r : (int64_t)r * nb + c;
             int64_t dst = tt ? (int64_t)c * nb + r : (int64_t)r * nb + c;
-            orc_store_elem(out, dst, to, ldexp(orc_payload_value(payload, src, from), d));
+            double v = ldexp(orc_payload_value(payload, nb, src, from), d);
+            if (y) y[dst] = v;
+            else orc_store_elem(out, dst, to, v);
         }
+    if (y) { orc_mx_encode(y, nb, (uint8_t *)out); free(y); }
     return from_scale + d;
 }
 
@@ -412,11 +482,11 @@ int orc_map_c(int64_t mt, int64_t nt, int64_t kt, int32_t nb, double tol, double
             int chosen = 0;
             if (cmap) {                   /* explicit map (R19): the code, if enabled */
                 chosen = cmap[i * nt + j];
-                if (!(mask & (1u << chosen))) chosen = 0;
+                if (!(mask & (1u << chosen)) || chosen == ORC_MX) chosen = 0;
             } else {
                 for (int li = 0; li < ORC_NCLS; ++li) {
                     int k = ORC_LADDER[li];
-                    if (!(mask & (1u << k))) continue;
+                    if (!(mask & (1u << k)) || k == ORC_MX) continue;   /* MX: operands only (R31) */
                     if (k == 0) { chosen = 0; break; }
                     double dC = (ORC_FMT[k].u + sqkt * 0x1p-24) +
                                 ((double)nb * ORC_FMT[k].eta) / ORC_FMT[k].omega_s;
@@ -452,7 +522,8 @@ int orc_map_c(int64_t mt, int64_t nt, int64_t kt, int32_t nb, double tol, double
 /*   orc_layout_transposed (read as a[r][p] and b[p][col]).                   */
 /*   P[r][col] = sum_p a[r][p] b[p][col], sequential p = 0..nb-1, from +0:    */
 /*     c = 0: binary64 fma;  c = 1: binary32 fmaf;                            */
-/*     c >= 2: binary32 acc + a*b (the product is exact in binary32).         */
+/*     c >= 2: binary32 acc + RN32(a*b) (the product is exact in binary32 for  */
+/*     c = 2..5; for MXFP4, c = 6, when the two block scales sum below -149). */
 /*   P is returned as binary64 (exact copies of the binary32 values if c>=1). */
 /* ------------------------------------------------------------------------- */
 void orc_tile_gemm(int cls, const void *a, const void *b, int32_t nb, double *P) {
@@ -463,9 +534,9 @@ void orc_tile_gemm(int cls, const void *a, const void *b, int32_t nb, double *P)
     for (int32_t r = 0; r < nb; ++r)         /* av[r*nb + p] = A(r,p), bv[col*nb + p] = B(p,col) */
         for (int32_t p = 0; p < nb; ++p) {
             av[(int64_t)r * nb + p] =
-                orc_payload_value(a, ta ? (int64_t)p * nb + r : (int64_t)r * nb + p, cls);
+                orc_payload_value(a, nb, ta ? (int64_t)p * nb + r : (int64_t)r * nb + p, cls);
             bv[(int64_t)r * nb + p] =
-                orc_payload_value(b, tb ? (int64_t)r * nb + p : (int64_t)p * nb + r, cls);
+                orc_payload_value(b, nb, tb ? (int64_t)r * nb + p : (int64_t)p * nb + r, cls);
         }
     for (int32_t r = 0; r < nb; ++r) {
         for (int32_t col = 0; col < nb; ++col) {
@@ -506,7 +577,7 @@ void orc_acc_init(int32_t nb, int code_c, double beta, const void *cin_payload,
     int64_t n = (int64_t)nb * nb;
     for (int64_t i = 0; i < n; ++i) {
         if (beta == 0.0) { acc[i] = 0.0; continue; }
-        double x = ldexp(orc_payload_value(cin_payload, i, code_c), -cin_scale);
+        double x = ldexp(orc_payload_value(cin_payload, nb, i, code_c), -cin_scale);
         if (code_c == 0) acc[i] = beta * x;
         else acc[i] = (double)(float)((double)(float)beta * x);
     }
@@ -537,7 +608,7 @@ int orc_finalize(int32_t nb, int code_c, const double *acc, void *payload, doubl
     for (int64_t i = 0; i < n; ++i) {
         double y = (code_c == 0) ? acc[i] : ldexp(acc[i], e);
         orc_store_elem(payload, i, code_c, y);
-        double back = orc_payload_value(payload, i, code_c);
+        double back = orc_payload_value(payload, nb, i, code_c);
         cuser[(i / nb) * ldc + (i % nb)] = (code_c == 0) ? back : ldexp(back, -e);
     }
     return e;
@@ -570,7 +641,7 @@ typedef struct {
 
 /* Apply an explicit map (R19, NEXT-1): codes given, scales from the rule. */
 static void orc_explicit_map(int64_t ntiles, const uint8_t *map, uint32_t class_mask,
-                             const double *maxabs, uint8_t *code, int16_t *scale) {
+                             const double *maxabs, uint8_t *code, int16_t *scale) {   /* A and B */
     for (int64_t t = 0; t < ntiles; ++t) {
         int c = map[t];
         if (!((class_mask | 1u) & (1u << c))) c = 0;
@@ -642,10 +713,10 @@ int orc_gemm_mp(const orc_desc_t *d, const double *A, int64_t lda, const double 
         void *tmp = malloc((size_t)tsz * 8);
         for (int c = 0; c < ORC_NCLS; ++c) s5[c] = 0;
         s5[code] = isB ? sb[tt] : sa[tt];
-        pp[code] = malloc((size_t)tsz * ORC_FMT[code].bytes);
+        pp[code] = malloc((size_t)orc_payload_bytes(code, nb));
         orc_pack_tile(tp, ld, nb, code, s5[code], orc_layout_transposed(isB, code), pp[code]);
         for (int c = code + 1; c < ORC_NCLS; ++c) {
-            void *dst = keep ? malloc((size_t)tsz * ORC_FMT[c].bytes) : tmp;
+            void *dst = keep ? malloc((size_t)orc_payload_bytes(c, nb)) : tmp;
             s5[c] = (int16_t)orc_shadow_tile(pp[code], nb, isB, code, s5[code], c, dst);
             if (keep) pp[c] = dst;
         }

@@ -12,11 +12,16 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GMP_LIB_PATH") or os.path.join(_HERE, "libgemm_mp.so")   # override: A/B builds
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "gemm_mp.h")
 
-GMP_FP64, GMP_FP32, GMP_FP16, GMP_BF16, GMP_E4M3, GMP_E5M2 = range(6)
-CLASS_NAMES = ["FP64", "FP32", "FP16", "BF16", "E4M3", "E5M2"]
+GMP_FP64, GMP_FP32, GMP_FP16, GMP_BF16, GMP_E4M3, GMP_E5M2, GMP_MXFP4 = range(7)
+CLASS_NAMES = ["FP64", "FP32", "FP16", "BF16", "E4M3", "E5M2", "MX4"]
 NCLS = len(CLASS_NAMES)
 TILE_SPLIT, TILE_DIGITS = NCLS, NCLS + 1   # gemm_mp_get_tile cls of the FP32 splits / FP64 digit planes
-CLASS_BYTES = [8, 4, 2, 2, 1]
+CLASS_BYTES = [8, 4, 2, 2, 1, 1]
+
+
+def slot_bytes(cls, nb):
+    """bytes of one nb x nb payload slot (MXFP4: nb^2/2 element bytes + nb^2/32 scale bytes)"""
+    return nb * nb // 2 + nb * nb // 32 if cls == GMP_MXFP4 else nb * nb * CLASS_BYTES[cls]
 GMP_FLAG_SIMT_ONLY = 1
 GMP_FLAG_TIMING = 2
 GMP_FLAG_FP32_FFMA = 4
@@ -48,13 +53,13 @@ class gmp_desc_t(ct.Structure):
 
 
 class gmp_stats_t(ct.Structure):
-    _fields_ = [("tiles_a", ct.c_int64 * 6), ("tiles_b", ct.c_int64 * 6), ("tiles_c", ct.c_int64 * 6),
-                ("pairs", ct.c_int64 * 6), ("flops", ct.c_double * 6), ("pairs_local", ct.c_int64 * 6),
-                ("shadows_local", ct.c_int64 * 6), ("packed_bytes_local", ct.c_int64),
+    _fields_ = [("tiles_a", ct.c_int64 * 7), ("tiles_b", ct.c_int64 * 7), ("tiles_c", ct.c_int64 * 7),
+                ("pairs", ct.c_int64 * 7), ("flops", ct.c_double * 7), ("pairs_local", ct.c_int64 * 7),
+                ("shadows_local", ct.c_int64 * 7), ("packed_bytes_local", ct.c_int64),
                 ("recv_bytes_local", ct.c_int64), ("workspace_bytes", ct.c_int64),
                 ("steps", ct.c_int32), ("launches_execute", ct.c_int32),
                 ("launches_plan", ct.c_int32), ("launches_convert", ct.c_int32),
-                ("class_ms", ct.c_double * 6), ("class_launches", ct.c_int32 * 6)]
+                ("class_ms", ct.c_double * 7), ("class_launches", ct.c_int32 * 7)]
 
     def as_dict(self):
         d = {}

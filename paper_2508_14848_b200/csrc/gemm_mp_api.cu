@@ -78,7 +78,7 @@ static gmp_status_t fail(gmp_status_t s, const std::string& msg) {
   } while (0)
 
 static inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
-constexpr int NC = GMP_NCLASS;   // precision classes 0..5 (gmp_class_t)
+constexpr int NC = GMP_NCLASS;   // precision classes 0..6 (gmp_class_t)
 
 // ---------------------------------------------------------------------------
 // metadata transfers without the copy engines
@@ -257,6 +257,10 @@ struct gmp_plan_s {
   std::vector<PackJob> pack;
   std::vector<ShadowJob> shadow_local;
   std::vector<std::vector<ShadowJob>> shadow_step;   // receiver-side shadows per step
+  std::vector<MxJob> mx_local;                       // MXFP4 packs and local shadows into MXFP4 (k_mx)
+  std::vector<std::vector<MxJob>> mx_step;           // shadows of received tiles into MXFP4, per step
+  std::vector<int64_t> mx_step_off;
+  int64_t off_mx = 0;
   std::vector<std::vector<Bcast>> bcast_step;
   std::vector<CTileDesc> ctd;
   std::vector<WorkItem> items;
@@ -479,7 +483,7 @@ static void build_tables(gmp_plan_s* pl) {
   const std::vector<int32_t>& rowP = pl->lay.rowP;
   const std::vector<int32_t>& colQ = pl->lay.colQ;
   const bool hasC = d.beta != 0.0;
-  for (int c = 0; c < NC; ++c) pl->slot_bytes[c] = nb2 * class_bytes(c);
+  for (int c = 0; c < NC; ++c) pl->slot_bytes[c] = slot_bytes_of(c, (int)nb);
   pl->slot_bytes[GMP_AR_SPLIT] = 3 * nb2 * 2;
   pl->slot_bytes[GMP_AR_SLICE] = OZ_NS * nb2;
   pl->fp32_tc = kTcAvailable && !(d.flags & (GMP_FLAG_SIMT_ONLY | GMP_FLAG_FP32_FFMA));
@@ -626,6 +630,8 @@ static void build_tables(gmp_plan_s* pl) {
   pl->off_slice = o; o = align_up(o + nslice * (int64_t)sizeof(SliceJob), 1024);
   pl->off_oexp = o; o = align_up(o + nslice * nb * 2, 1024);
   pl->off_shadow = o; o = align_up(o + (n_shadow_local + n_shadow_recv) * (int64_t)sizeof(ShadowJob), 1024);
+  // MXFP4 jobs: packs of MXFP4 tiles and shadows into MXFP4 (bounded by packs + shadows)
+  pl->off_mx = o; o = align_up(o + (n_pack + n_shadow_local + n_shadow_recv) * (int64_t)sizeof(MxJob), 1024);
   pl->off_ctd = o; o = align_up(o + nCl * (int64_t)sizeof(CTileDesc), 1024);
   pl->off_items = o; o = align_up(o + n_items * (int64_t)sizeof(WorkItem), 1024);
   pl->off_pairs = o; o = align_up(o + n_pairs * (int64_t)sizeof(PairDesc), 1024);
@@ -663,8 +669,15 @@ static void build_tables(gmp_plan_s* pl) {
   pl->ws_bytes = o;
 
   // ---- pack jobs ----
+  pl->mx_local.clear();
+  pl->mx_step.assign(steps, {});
   for (int64_t g : pl->locA) {
     const int64_t i = g / kt, l = g % kt, il = pl->lay.rowL[i], ll = l / Q;
+    if (pl->codeA[g] == GMP_MX) {   // MXFP4: K-major payload rows = tile rows (not transposed)
+      pl->mx_local.push_back(MxJob{(const uint8_t*)(pl->A + il * nb * pl->lda + ll * nb), 0, pl->lda,
+                                   arena(GMP_MX, pl->slotA5[g * NC + GMP_MX]), -1, pl->sA5[g * NC + GMP_MX], 0, 0});
+      continue;
+    }
     PackJob pj{};
     pj.src = pl->A + il * nb * pl->lda + ll * nb;
     pj.ld = pl->lda;
@@ -676,6 +689,11 @@ static void build_tables(gmp_plan_s* pl) {
   }
   for (int64_t g : pl->locB) {
     const int64_t l = g / nt, j = g % nt, ll = l / P, jl = pl->lay.colL[j];
+    if (pl->codeB[g] == GMP_MX) {   // MXFP4: K-major payload rows = tile columns (transposed read)
+      pl->mx_local.push_back(MxJob{(const uint8_t*)(pl->B + ll * nb * pl->ldb + jl * nb), 0, pl->ldb,
+                                   arena(GMP_MX, pl->slotB5[g * NC + GMP_MX]), -1, pl->sB5[g * NC + GMP_MX], 1, 0});
+      continue;
+    }
     PackJob pj{};
     pj.src = pl->B + ll * nb * pl->ldb + jl * nb;
     pj.ld = pl->ldb;
@@ -711,6 +729,13 @@ static void build_tables(gmp_plan_s* pl) {
     if (!local && wire && wire != (1u << code)) return;   // every needed class arrives on the wire
     for (int c = code + 1; c < NC; ++c) {
       if (sl[c] < 0) continue;
+      if (c == GMP_MX) {   // into MXFP4 (k_mx): MN-major sources (FP64/FP32) are read transposed
+        MxJob mj{nullptr, arena(code, sl[code]), nb, arena(c, sl[c]), (int16_t)code, (int16_t)(s5[c] - s5[code]),
+                 (int16_t)(code <= 1), 0};
+        if (local) pl->mx_local.push_back(mj);
+        else pl->mx_step[l / GMP_STEP_DEPTH].push_back(mj);
+        continue;
+      }
       ShadowJob sj{};
       sj.src_off = arena(code, sl[code]);
       sj.dst_off = arena(c, sl[c]);
@@ -772,6 +797,11 @@ static void build_tables(gmp_plan_s* pl) {
   {
     int64_t acc = (int64_t)pl->shadow_local.size();
     for (int s = 0; s < steps; ++s) { pl->shadow_step_off[s] = acc; acc += (int64_t)pl->shadow_step[s].size(); }
+  }
+  pl->mx_step_off.assign(steps, 0);
+  {
+    int64_t acc = (int64_t)pl->mx_local.size();
+    for (int s = 0; s < steps; ++s) { pl->mx_step_off[s] = acc; acc += (int64_t)pl->mx_step[s].size(); }
   }
 
   // ---- SUMMA broadcasts per step (stored bytes) ----
@@ -885,6 +915,9 @@ static void build_tables(gmp_plan_s* pl) {
           w64c[c] = w64c[c] || pl->ctd[k].code == 0;
         }
       }
+      // MXFP4 pairs fold first in the step (class order 6 -> 0) and run on their own kernel:
+      // a step holding any keeps the per-class launches
+      if (present >> GMP_MX & 1) fuse = false;
       present &= 0x3Eu;   // classes 1..5
       int ncls = 0;
       for (int c = 1; c < NC; ++c) {
@@ -900,7 +933,7 @@ static void build_tables(gmp_plan_s* pl) {
       std::vector<int64_t> cost;
       for (int64_t k = 0; k < nCl; ++k) {
         const int64_t pbeg = (int64_t)pl->pairs.size();
-        for (int c = NC - 1; c >= 1; --c) add_pairs(s, c, k);
+        for (int c = 5; c >= 1; --c) add_pairs(s, c, k);   // MXFP4 (6) keeps its own launch
         const int64_t pcnt = (int64_t)pl->pairs.size() - pbeg;
         if (!pcnt) continue;
         int64_t w = 0;   // MMA issue cycles per K: BF16x9 36, 16-bit 4, 8-bit 1 (half the blocks, twice the rate)
@@ -926,8 +959,9 @@ static void build_tables(gmp_plan_s* pl) {
       pl->launches.push_back(L);
     }
     for (int c = NC - 1; c >= 0; --c) {
-      if (fuse && c >= 1) continue;
-      const bool tc = tc_on && (c >= 2);
+      if (fuse && c >= 1 && c <= 5) continue;   // MXFP4 pairs keep their own launch
+      // MXFP4 on tcgen05 needs whole 256-element (128-byte) K blocks: nb = 128 runs on the SIMT kernel
+      const bool tc = tc_on && (c >= 2) && (c != GMP_MX || nb % 256 == 0);
       const int64_t ibeg = (int64_t)pl->items.size();
       std::vector<WorkItem> its;
       for (int64_t k = 0; k < nCl; ++k) {
@@ -942,7 +976,7 @@ static void build_tables(gmp_plan_s* pl) {
       bool w64i = false;
       for (const WorkItem& wi : its) w64i = w64i || pl->ctd[wi.ctile].code == 0;
       const bool rastered = tc_on && c >= 1 &&
-                            (raster_env > 0 || (raster_env < 0 && c >= 2 && !w64i && nb % 256 == 0 &&
+                            (raster_env > 0 || (raster_env < 0 && c >= 2 && c <= 5 && !w64i && nb % 256 == 0 &&
                                                 pair_default(d.flags)));
       if (!rastered)
         std::stable_sort(its.begin(), its.end(), [](const WorkItem& a, const WorkItem& b) { return a.pcnt > b.pcnt; });
@@ -953,11 +987,11 @@ static void build_tables(gmp_plan_s* pl) {
       // registers, which needs BN = 128
       bool w64 = false;
       for (const WorkItem& wi : its) w64 = w64 || pl->ctd[wi.ctile].code == 0;
-      const int tcbn = (w64 ? 128 : tc_bn((int)nb));
+      const int tcbn = (w64 || c == GMP_MX) ? 128 : tc_bn((int)nb);   // MXFP4: 128 (TMEM budget)
       // GMP_FLAG_TC_PAIR: 16-bit / 8-bit classes folding into binary32 W on
       // 256-multiple tiles run on SM pairs (k_tc2_class, cta_group::2)
-      const bool pair = tc && !w64 && c >= 2 && (nb % 256 == 0) && pair_default(d.flags);
-      const bool mcast = tc && !w64 && c >= 2 && (nb % 256 == 0) && (d.flags & GMP_FLAG_TC_MCAST) && !pair;
+      const bool pair = tc && !w64 && c >= 2 && c <= 5 && (nb % 256 == 0) && pair_default(d.flags);
+      const bool mcast = tc && !w64 && c >= 2 && c <= 5 && (nb % 256 == 0) && (d.flags & GMP_FLAG_TC_MCAST) && !pair;
       if (pair || mcast) {
         Launch L{s, c, pair ? 5 : 6, ibeg, (int64_t)its.size() * tc2_subtiles_per_item((int)nb), TC2_BN};
         if (pair) L.obeg = raster(its, (int)(nb / 256), (int)(nb / 256), true);
@@ -1101,7 +1135,7 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
     return true;
   };
   if (!chk_map(d.a_map, pl->nA) || !chk_map(d.b_map, pl->nB) || !chk_map(d.c_map, pl->nC))
-    return fail(GMP_ERR_MAP_SHAPE, "explicit map holds a code > 5");
+    return fail(GMP_ERR_MAP_SHAPE, "explicit map holds a code > 6");
 
   // ---- S1: stats of local tiles, written at their global index ----
   uint8_t* sc = (uint8_t*)scratch;
@@ -1254,9 +1288,9 @@ extern "C" gmp_status_t gemm_mp_plan_host(const gmp_desc_t* desc, const uint8_t*
   pl->mt = d.M / d.nb; pl->nt = d.N / d.nb; pl->kt = d.K / d.nb;
   pl->nA = pl->mt * pl->kt; pl->nB = pl->kt * pl->nt; pl->nC = pl->mt * pl->nt;
   pl->P = d.P; pl->Q = d.Q; pl->p = d.rank / d.Q; pl->q = d.rank % d.Q;
-  for (int64_t t = 0; t < pl->nA; ++t) if (acode[t] >= NC) return fail(GMP_ERR_MAP_SHAPE, "code > 5");
-  for (int64_t t = 0; t < pl->nB; ++t) if (bcode[t] >= NC) return fail(GMP_ERR_MAP_SHAPE, "code > 5");
-  for (int64_t t = 0; t < pl->nC; ++t) if (ccode[t] >= NC) return fail(GMP_ERR_MAP_SHAPE, "code > 5");
+  for (int64_t t = 0; t < pl->nA; ++t) if (acode[t] >= NC) return fail(GMP_ERR_MAP_SHAPE, "code > 6");
+  for (int64_t t = 0; t < pl->nB; ++t) if (bcode[t] >= NC) return fail(GMP_ERR_MAP_SHAPE, "code > 6");
+  for (int64_t t = 0; t < pl->nC; ++t) if (ccode[t] >= NC) return fail(GMP_ERR_MAP_SHAPE, "code > 6");
   pl->codeA.assign(acode, acode + pl->nA);
   pl->codeB.assign(bcode, bcode + pl->nB);
   pl->codeC.assign(ccode, ccode + pl->nC);
@@ -1317,6 +1351,13 @@ static gmp_status_t launch_shadows(const ShadowJob* djobs, const std::vector<Sha
   return GMP_OK;
 }
 
+static gmp_status_t launch_mx(const MxJob* djobs, int64_t n, uint8_t* ws, int nb, cudaStream_t s) {
+  if (n <= 0) return GMP_OK;
+  k_mx<<<dim3((unsigned)((nb / 32) * (nb / 128)), (unsigned)n), 256, 0, s>>>(djobs, ws, nb);
+  GMP_CUDA(cudaGetLastError());
+  return GMP_OK;
+}
+
 template <typename K>
 static gmp_status_t set_smem_once(K kernel, int bytes) {
   GMP_CUDA(ensure_max_smem(kernel, bytes));
@@ -1365,6 +1406,8 @@ static gmp_status_t issue_comm_step(gmp_plan_s* pl, uint8_t* ws, int s) {
   }
   GMP_TRY(launch_shadows((const ShadowJob*)(ws + pl->off_shadow) + pl->shadow_step_off[s], pl->shadow_step[s], ws,
                          (int)nb, pl->comm_stream));
+  GMP_TRY(launch_mx((const MxJob*)(ws + pl->off_mx) + pl->mx_step_off[s], (int64_t)pl->mx_step[s].size(), ws, (int)nb,
+                    pl->comm_stream));
   if (!pl->split_step[s].empty()) {
     k_split<<<dim3((unsigned)((nb / 64) * (nb / 64)), (unsigned)pl->split_step[s].size()), 256, 0,
               pl->comm_stream>>>((const SplitJob*)(ws + pl->off_split) + pl->split_step_off[s], ws, (int)nb);
@@ -1467,6 +1510,9 @@ extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_byte
   tables.add(ws + pl->off_pack, pl->pack.data(), (int64_t)(pl->pack.size() * sizeof(PackJob)));
   tables.add(ws + pl->off_accinit, (const uint8_t*)pl->acc_init_idx.data(), (int64_t)(pl->acc_init_idx.size() * 4));
   tables.add(ws + pl->off_shadow, allsh.data(), (int64_t)(allsh.size() * sizeof(ShadowJob)));
+  std::vector<MxJob> allmx = pl->mx_local;
+  for (auto& v : pl->mx_step) allmx.insert(allmx.end(), v.begin(), v.end());
+  tables.add(ws + pl->off_mx, allmx.data(), (int64_t)(allmx.size() * sizeof(MxJob)));
   tables.add(ws + pl->off_items, pl->items.data(), (int64_t)(pl->items.size() * sizeof(WorkItem)));
   tables.add(ws + pl->off_pairs, pl->pairs.data(), (int64_t)(pl->pairs.size() * sizeof(PairDesc)));
   tables.add(ws + pl->off_order, (const uint8_t*)pl->order.data(), (int64_t)(pl->order.size() * 4));
@@ -1484,6 +1530,8 @@ extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_byte
   }
   // S5 shadows of local tiles
   GMP_TRY(launch_shadows((const ShadowJob*)(ws + pl->off_shadow), pl->shadow_local, ws, (int)nb, stream));
+  // MXFP4: packs of MXFP4 tiles and local shadows into MXFP4 (after k_pack: shadows read stored payloads)
+  GMP_TRY(launch_mx((const MxJob*)(ws + pl->off_mx), (int64_t)pl->mx_local.size(), ws, (int)nb, stream));
   // multi-GPU: SUMMA step 0 starts as soon as this rank's panel tiles are packed,
   // overlapping the rest of convert (splits, digit slices) and the accumulator init
   pl->step0_issued = false;
@@ -1612,7 +1660,8 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
           case 2: k_simt_class<2><<<(unsigned)L.icount, 256, 0, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha); break;
           case 3: k_simt_class<3><<<(unsigned)L.icount, 256, 0, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha); break;
           case 4: k_simt_class<4><<<(unsigned)L.icount, 256, 0, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha); break;
-          default: k_simt_class<5><<<(unsigned)L.icount, 256, 0, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha); break;
+          case 5: k_simt_class<5><<<(unsigned)L.icount, 256, 0, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha); break;
+          default: k_simt_class<GMP_MX><<<(unsigned)L.icount, 256, 0, stream>>>(it, pd, dct, ws, (int)nb, pl->d.alpha); break;
         }
         GMP_CUDA(cudaGetLastError());
       }
@@ -1725,6 +1774,15 @@ extern "C" gmp_status_t gemm_mp_get_tile(gmp_plan_t pl, char which, int64_t ti, 
   if ((int64_t)*bytes < nbytes) return fail(GMP_ERR_ARG, "host buffer too small");
   GMP_CUDA(cudaDeviceSynchronize());
   GMP_CUDA(cudaMemcpy(dst, pl->ws + off, nbytes, cudaMemcpyDeviceToHost));
+  if ((which == 'A' || which == 'B') && cls == GMP_MX) {
+    // export the MXFP4 scale bytes in plain order (row m, block b at nb^2/2 + m*nb/32 + b),
+    // the oracle's layout, instead of the tcgen05 chunk layout held in the workspace
+    const int nb = pl->d.nb;
+    uint8_t* h = (uint8_t*)dst;
+    std::vector<uint8_t> sf(h + nb2 / 2, h + nb2 / 2 + nb2 / 32);
+    for (int m = 0; m < nb; ++m)
+      for (int b = 0; b < nb / 32; ++b) h[nb2 / 2 + (int64_t)m * (nb / 32) + b] = sf[mx_sf_offset(nb, m, b) - nb2 / 2];
+  }
   *bytes = (size_t)nbytes;
   if (scale) *scale = sc;
   return GMP_OK;
@@ -1843,8 +1901,8 @@ extern "C" gmp_status_t gemm_mp_balance(const gmp_desc_t* desc, const uint8_t* a
   GMP_TRY(check_desc(desc));
   if (!acode || !bcode || !row_owner || !col_owner) return fail(GMP_ERR_ARG, "NULL argument");
   const int64_t nb = desc->nb, mt = desc->M / nb, nt = desc->N / nb, kt = desc->K / nb;
-  for (int64_t t = 0; t < mt * kt; ++t) if (acode[t] >= NC) return fail(GMP_ERR_MAP_SHAPE, "code > 5");
-  for (int64_t t = 0; t < kt * nt; ++t) if (bcode[t] >= NC) return fail(GMP_ERR_MAP_SHAPE, "code > 5");
+  for (int64_t t = 0; t < mt * kt; ++t) if (acode[t] >= NC) return fail(GMP_ERR_MAP_SHAPE, "code > 6");
+  for (int64_t t = 0; t < kt * nt; ++t) if (bcode[t] >= NC) return fail(GMP_ERR_MAP_SHAPE, "code > 6");
   double cst[NC + 1];
   if (cost) {
     for (int c = 0; c <= NC; ++c) {
@@ -1852,7 +1910,7 @@ extern "C" gmp_status_t gemm_mp_balance(const gmp_desc_t* desc, const uint8_t* a
       cst[c] = cost[c];
     }
   } else {
-    const double peak[NC] = {35.5, 155.0, 1323.0, 1397.0, 2628.0, 2628.0};
+    const double peak[NC] = {35.5, 155.0, 1323.0, 1397.0, 2628.0, 2628.0, 5588.0};   // MXFP4: 4 x BF16 (nominal)
     const double f = 2.0 * (double)nb * nb * nb;
     for (int c = 0; c < NC; ++c) cst[c] = f / (peak[c] * 1e12);
     cst[NC] = 20.0 * (double)nb * nb / 6.0e12;

@@ -2,7 +2,8 @@
 // tile-centric mixed-precision GEMM (arxiv 2508.14848).  sm_100a only.
 //
 // Class codes: 0 FP64, 1 FP32, 2 FP16, 3 BF16, 4 E4M3 (OCP FN),
-// 5 E5M2 (OCP).  Ordered by unit roundoff: pair class = max.
+// 5 E5M2 (OCP), 6 MXFP4 (OCP MX: E2M1 elements, one E8M0 scale
+// per 32 K-elements; NEXT-4, R31).  Ordered by unit roundoff: pair class = max.
 // Every conversion from binary64 is ONE round-to-nearest-even (PAPER.md:148
 // receiver-side conversion; R11): hardware cvt.rn for FP32/FP16/BF16,
 // round-to-odd into binary32 followed by cvt.rn.satfinite for E4M3 / E5M2 (the
@@ -17,7 +18,8 @@
 #include <utility>
 #include <vector>
 
-#define GMP_NCLASS 6
+#define GMP_NCLASS 7
+#define GMP_MX 6   // MXFP4 class (operands only: A/B tiles, never C)
 // workspace arenas: one per class, then the FP32 BF16x3 splits and the FP64 int8 digits
 #define GMP_AR_SPLIT (GMP_NCLASS)
 #define GMP_AR_SLICE (GMP_NCLASS + 1)
@@ -26,18 +28,37 @@
 
 namespace gmp {
 
-__host__ __device__ constexpr int class_bytes(int c) {
+__host__ __device__ constexpr int class_bytes(int c) {   // per element; MXFP4: see mx_slot_bytes
   return c == 0 ? 8 : c == 1 ? 4 : c >= 4 ? 1 : 2;
+}
+
+// MXFP4 slot (O6/R31): nb*nb/2 element bytes -- K-major payload row m (A: tile
+// row, B: tile column), element k in byte m*nb/2 + k/2, low nibble for even k -- then
+// nb*nb/32 E8M0 scale bytes (s + 127 of block k/32 of row m) in the tcgen05 scale-factor
+// layout: per 128-row group g and per 4 blocks c a 512-byte chunk, byte
+// (m%32)*16 + ((m%128)/32)*4 + blk%4 (the smem image tcgen05.cp 32x128b.warpx4 copies to
+// TMEM; tools/microbench/mxf4_probe.cu).
+__host__ __device__ inline int64_t mx_slot_bytes(int nb) { return (int64_t)nb * nb / 2 + (int64_t)nb * nb / 32; }
+__host__ __device__ inline int64_t mx_sf_offset(int nb, int m, int blk) {
+  const int g = m >> 7, mm = m & 127;
+  return (int64_t)nb * nb / 2 + ((int64_t)g * (nb >> 7) + (blk >> 2)) * 512 + (mm & 31) * 16 + (mm >> 5) * 4 + (blk & 3);
+}
+// bytes of one nb x nb payload slot of class c
+__host__ __device__ inline int64_t slot_bytes_of(int c, int nb) {
+  return c == GMP_MX ? mx_slot_bytes(nb) : (int64_t)nb * nb * class_bytes(c);
 }
 
 // unit roundoff u_k, smallest subnormal eta_k, scale target Omega'_k (R10)
 __host__ __device__ inline double class_u(int c) {
-  return c == 0 ? 0x1p-53 : c == 1 ? 0x1p-24 : c == 2 ? 0x1p-11 : c == 3 ? 0x1p-8 : c == 4 ? 0x1p-4 : 0x1p-3;
+  return c == 0 ? 0x1p-53 : c == 1 ? 0x1p-24 : c == 2 ? 0x1p-11 : c == 3 ? 0x1p-8 : c == 4 ? 0x1p-4
+       : c == 5 ? 0x1p-3 : 0x1p-2;
 }
+// MXFP4: eta is the E2M1 subnormal quantum in block units (0.5 x 2^s_b)
 __host__ __device__ inline double class_eta(int c) {
-  return c == 0 ? 0x1p-1074 : c == 1 ? 0x1p-149 : c == 2 ? 0x1p-24 : c == 3 ? 0x1p-133 : c == 4 ? 0x1p-9 : 0x1p-16;
+  return c == 0 ? 0x1p-1074 : c == 1 ? 0x1p-149 : c == 2 ? 0x1p-24 : c == 3 ? 0x1p-133 : c == 4 ? 0x1p-9
+       : c == 5 ? 0x1p-16 : 0.5;
 }
-__host__ __device__ inline double class_omega(int c) {
+__host__ __device__ inline double class_omega(int c) {   // MXFP4: the tile max is scaled to <= 1 too
   return c == 2 ? 65504.0 : c == 4 ? 448.0 : c == 5 ? 57344.0 : 1.0;
 }
 
@@ -82,6 +103,35 @@ __device__ __forceinline__ uint16_t cvt_e5m2x2_rn(double lo, double hi) {
 }
 __device__ __forceinline__ uint8_t cvt_e5m2_rn(double x) {
   return (uint8_t)(cvt_e5m2x2_rn(x, 0.0) & 0xFF);
+}
+
+// MXFP4 block scale (R31): the smallest s >= -127 with amax <= 6 * 2^s (no element of the
+// block saturates); amax = m 2^E (frexp), 6 = 0.75 * 2^3: s = E - 3 if m <= 0.75 else E - 2.
+__host__ __device__ inline int mx_block_exp(double amax) {
+  if (amax == 0.0) return -127;
+  int E;
+  const double m = frexp(amax, &E);
+  const int s = (m <= 0.75) ? E - 3 : E - 2;
+  return s < -127 ? -127 : s;
+}
+// two E2M1 codes (lo in bits 0-3) from binary64 values already divided by the block
+// scale (|x| <= 6): round-to-odd into binary32, then RNE (exact: 24 >= 2 + 2 bits)
+__device__ __forceinline__ uint32_t cvt_e2m1x2_rn(double lo, double hi) {
+  uint16_t r;
+  const float flo = rto_f32(lo), fhi = rto_f32(hi);
+  asm("{.reg .b8 t; cvt.rn.satfinite.e2m1x2.f32 t, %1, %2; cvt.u16.u8 %0, t;}" : "=h"(r) : "f"(fhi), "f"(flo));
+  return (uint32_t)r & 0xFFu;
+}
+__host__ __device__ inline float e2m1_value(uint32_t q) {
+  const float v = (q & 7u) < 2u ? 0.5f * (float)(q & 7u)
+                : (float)(((q & 1u) + 2u) << ((q & 7u) >> 1)) * 0.25f;
+  return (q & 8u) ? -v : v;
+}
+// exact value (scaled units) of element (m, k) of an MXFP4 slot: E2M1(q) x 2^(s_b)
+__device__ __forceinline__ float mx_value(const uint8_t* slot, int nb, int m, int k) {
+  const uint32_t q = (slot[(int64_t)m * (nb >> 1) + (k >> 1)] >> (4 * (k & 1))) & 15u;
+  const int s = (int)slot[mx_sf_offset(nb, m, k >> 5)] - 127;
+  return (float)ldexp((double)e2m1_value(q), s);
 }
 
 // ---- class bits -> exact binary64 / binary32 ----------------------------------

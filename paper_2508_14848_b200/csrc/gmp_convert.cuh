@@ -219,6 +219,71 @@ __global__ void __launch_bounds__(256) k_shadow_t(const ShadowJob* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------
+// MXFP4 encode (S3 pack of an MXFP4 tile and S5 shadows INTO MXFP4; O6, R31):
+//   y = x 2^scale (pack: x = binary64 user element) or y = decode_from(stored) 2^d
+//   (shadow, receiver-side from the stored payload); per block of 32 consecutive
+//   K-elements of a K-major payload row: s_b = mx_block_exp(max |y|), q = RN_E2M1(y 2^-s_b).
+// One CTA = 32 payload rows x 128 K-elements (128 blocks, one per thread), staged
+// through shared memory so the loads are coalesced in either source orientation:
+//   transpose = 0: element (m, k) at src[m * ld + k]; 1: at src[k * ld + m].
+// ---------------------------------------------------------------------------
+struct MxJob {
+  const uint8_t* src;   // pack: the binary64 tile, top-left (from = -1)
+  int64_t src_off;      // shadow: byte offset of the stored payload in the workspace
+  int64_t ld;           // elements
+  int64_t dst_off;      // byte offset of the MXFP4 slot in the workspace
+  int16_t from;         // -1: binary64 user matrix; else the stored class of the payload
+  int16_t scale;        // pack: per-tile scale e; shadow: d
+  int16_t transpose;
+  int16_t pad;
+};
+
+__device__ __forceinline__ double mx_src_value(const MxJob& j, const uint8_t* ws, int64_t idx) {
+  if (j.from < 0) return reinterpret_cast<const double*>(j.src)[idx];
+  return payload_f64(ws + j.src_off, idx, j.from);
+}
+
+__global__ void __launch_bounds__(256) k_mx(const MxJob* __restrict__ jobs, uint8_t* ws, int nb) {
+  __shared__ double sm[32][129];
+  const MxJob j = jobs[blockIdx.y];
+  const int per = nb / 128;                       // 128-K chunks per row group
+  const int m0 = (blockIdx.x / per) * 32, k0 = (blockIdx.x % per) * 128;
+  const int t = threadIdx.x;
+#pragma unroll 4
+  for (int u = 0; u < 16; ++u) {
+    const int idx = t + u * 256;                  // 4096 elements of the 32 x 128 region
+    int m, k;
+    if (!j.transpose) { m = idx >> 7; k = idx & 127; }
+    else { k = idx >> 5; m = idx & 31; }
+    const int64_t si = j.transpose ? (int64_t)(k0 + k) * j.ld + m0 + m : (int64_t)(m0 + m) * j.ld + k0 + k;
+    sm[m][k] = ldexp_fast(mx_src_value(j, ws, si), j.scale);
+  }
+  __syncthreads();
+  if (t < 128) {
+    const int m = t >> 2, b = t & 3;              // payload row m0 + m, block (k0 / 32) + b
+    double amax = 0.0;
+#pragma unroll 8
+    for (int v = 0; v < 32; ++v) amax = fmax(amax, fabs(sm[m][b * 32 + v]));
+    const int sb = mx_block_exp(amax);
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t x = 0;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int e = b * 32 + q * 8 + 2 * v;
+        x |= cvt_e2m1x2_rn(ldexp_fast(sm[m][e], -sb), ldexp_fast(sm[m][e + 1], -sb)) << (8 * v);
+      }
+      w[q] = x;
+    }
+    uint8_t* slot = ws + j.dst_off;
+    *reinterpret_cast<uint4*>(slot + (int64_t)(m0 + m) * (nb >> 1) + ((k0 + b * 32) >> 1)) =
+        make_uint4(w[0], w[1], w[2], w[3]);
+    slot[mx_sf_offset(nb, m0 + m, (k0 >> 5) + b)] = (uint8_t)(sb + 127);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // FP32 class on the tensor pipe: exact 3-way BF16 split of an FP32 payload
 // (MN-major) into three K-major BF16 parts, x = x0 + x1 + x2 with
 // x0 = RN_bf16(x), x1 = RN_bf16(x - x0), x2 = x - x0 - x1 (both differences

@@ -26,6 +26,8 @@
 #include <cstdint>
 #include <vector>
 
+#include "gmp_common.cuh"
+
 namespace gmp {
 
 struct Layout {
@@ -53,7 +55,7 @@ inline bool make_layout(int64_t mt, int64_t nt, int P, int Q, const int32_t* row
 }
 
 // Per-rank cost model of the balancer, in the units of `cost` (relative times).
-//   cost[c], c = 0..5: one tile-GEMM of pair class c; cost[6]: per owned A, B or
+//   cost[c], c = 0..GMP_NCLASS-1: one tile-GEMM of pair class c; cost[GMP_NCLASS]: per owned A, B or
 //   C tile (stats + pack + W init / finalize, HBM-bound).
 struct BalanceModel {
   int64_t mt, nt, kt;
@@ -64,7 +66,7 @@ struct BalanceModel {
 
   BalanceModel(int64_t mt_, int64_t nt_, int64_t kt_, int P_, int Q_, const uint8_t* acode,
                const uint8_t* bcode, const double* cost)
-      : mt(mt_), nt(nt_), kt(kt_), P(P_), Q(Q_), w(mt_ * nt_, 0.0), tile_cost(cost[6]), kq(Q_, 0), kp(P_, 0) {
+      : mt(mt_), nt(nt_), kt(kt_), P(P_), Q(Q_), w(mt_ * nt_, 0.0), tile_cost(cost[GMP_NCLASS]), kq(Q_, 0), kp(P_, 0) {
     for (int64_t i = 0; i < mt; ++i)
       for (int64_t j = 0; j < nt; ++j) {
         double s = 0.0;

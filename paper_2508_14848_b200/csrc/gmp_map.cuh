@@ -164,12 +164,15 @@ __global__ void __launch_bounds__(1024) k_map_finalize(FinalizeArgs a) {
       if (chosen >= GMP_NCLASS || !(mask & (1u << chosen))) chosen = 0;
     } else if (!isinf(SX)) {
       const double rhs = __ddiv_rn(__dmul_rn(eps, __dsqrt_rn(SX)), __dsqrt_rn(ntiles));
-      for (int kk = GMP_NCLASS - 1; kk >= 1; --kk) {   // ladder E5M2, E4M3, BF16, FP16, FP32 (then FP64)
+      for (int kk = GMP_NCLASS - 1; kk >= 1; --kk) {   // ladder MXFP4, E5M2, E4M3, BF16, FP16, FP32 (then FP64)
         if (!(mask & (1u << kk))) continue;
         if (M == 0.0) { chosen = kk; break; }
         const int e = scale_exp(M, kk);
+        // underflow term: nb x half the subnormal quantum of the scaled grid; MXFP4: of the
+        // block holding the tile max (every block scale is <= it; R31)
+        const int qe = (kk == GMP_MX) ? mx_block_exp(ldexp_fast(M, e)) : 0;
         const double lhs = __dadd_rn(__dmul_rn(delta_in(kk, a.nb), __dsqrt_rn(S)),
-                                     __dmul_rn((double)a.nb, ldexp_fast(class_eta(kk), -e - 1)));
+                                     __dmul_rn((double)a.nb, ldexp_fast(class_eta(kk), qe - e - 1)));
         if (lhs <= rhs) { chosen = kk; break; }
       }
     }
@@ -194,12 +197,12 @@ __global__ void __launch_bounds__(1024) k_map_finalize(FinalizeArgs a) {
     QB = __dsqrt_rn(QB);
     const double sc = hasC ? a.SC[ct] : 0.0;
     const double nhat = __dadd_rn(__dmul_rn(__dmul_rn(aa, RA), QB), __dmul_rn(ab, __dsqrt_rn(sc)));
-    if (a.explicit_c) {
+    if (a.explicit_c) {   // MXFP4 is an operand class only (R31): never a C class
       chosen = a.mapC[ct];
-      if (chosen >= GMP_NCLASS || !(mask & (1u << chosen))) chosen = 0;
+      if (chosen >= GMP_NCLASS || chosen == GMP_MX || !(mask & (1u << chosen))) chosen = 0;
     } else {
       for (int k = GMP_NCLASS - 1; k >= 1; --k) {
-        if (!(mask & (1u << k))) continue;
+        if (!(mask & (1u << k)) || k == GMP_MX) continue;
         const double dC = __dadd_rn(__dadd_rn(class_u(k), __dmul_rn(sqkt, 0x1p-24)),
                                     __ddiv_rn(__dmul_rn((double)a.nb, class_eta(k)), class_omega(k)));
         if (__dmul_rn(dC, nhat) <= rhsC) { chosen = k; break; }

@@ -140,8 +140,25 @@ k_simt_class(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pa
       for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
 
     T ra[EA], rb[EBn];
-    ldn<C, T, EA>(Ag, ra);
-    ldn<C, T, EBn>(Bg, rb);
+    // MXFP4 (class 6): nibbles + block scales, element (row, k) through mx_value
+    auto loadA = [&](int sl, T* r) {
+      if constexpr (C == GMP_MX) {
+#pragma unroll
+        for (int e = 0; e < EA; ++e) r[e] = mx_value(ws + pd.a_off, nb, it.m0 + lrA, sl * BK + lkA + e);
+      } else {
+        ldn<C, T, EA>(Ag + (int64_t)sl * BK * EB, r);
+      }
+    };
+    auto loadB = [&](int sl, T* r) {
+      if constexpr (C == GMP_MX) {
+#pragma unroll
+        for (int e = 0; e < EBn; ++e) r[e] = mx_value(ws + pd.b_off, nb, it.n0 + lrB, sl * BK + lkB + e);
+      } else {
+        ldn<C, T, EBn>(Bg + (int64_t)sl * BK * EB, r);
+      }
+    };
+    loadA(0, ra);
+    loadB(0, rb);
 #pragma unroll
     for (int e = 0; e < EA; ++e) As[0][lkA + e][lrA] = ra[e];
 #pragma unroll
@@ -151,8 +168,8 @@ k_simt_class(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pa
     for (int s = 0; s < nsl; ++s) {
       const int buf = s & 1;
       if (s + 1 < nsl) {
-        ldn<C, T, EA>(Ag + (int64_t)(s + 1) * BK * EB, ra);
-        ldn<C, T, EBn>(Bg + (int64_t)(s + 1) * BK * EB, rb);
+        loadA(s + 1, ra);
+        loadB(s + 1, rb);
       }
 #pragma unroll
       for (int k = 0; k < BK; ++k) {
@@ -167,7 +184,12 @@ k_simt_class(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pa
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
-          for (int j = 0; j < TN; ++j) acc[i][j] = fma_rn(a[i], b[j], acc[i][j]);
+          for (int j = 0; j < TN; ++j) {
+            // O8: acc + RN32(a b); the product is exact for classes 2..5 (one fmaf), not
+            // always for MXFP4 (block scales summing below 2^-149)
+            if constexpr (C == GMP_MX) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(a[i], b[j]));
+            else acc[i][j] = fma_rn(a[i], b[j], acc[i][j]);
+          }
       }
       if (s + 1 < nsl) {
 #pragma unroll

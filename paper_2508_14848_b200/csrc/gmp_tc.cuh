@@ -69,6 +69,20 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+// plain bulk copy global -> shared (16-byte aligned, size a multiple of 16)
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(uint64_t* b) {
@@ -86,6 +100,31 @@ template <int C, int BN>
 __host__ __device__ constexpr uint32_t tc_idesc() {
   constexpr uint32_t ab = (C == 3 || C == 5) ? 1u : 0u;   // kind::f16: F16 0, BF16 1; kind::f8f6f4: E4M3 0, E5M2 1
   return (1u << 4) | (ab << 7) | (ab << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
+}
+// MXFP4 (kind::mxf4.block_scale, E2M1 x E2M1, E8M0 scales per 32 K): block-scaled
+// instruction descriptor -- a/b format E2M1 (1) at bits 7/10, N>>3 at 17, scale format
+// E8M0 (bit 23), M>>4 at 24; the scale-factor ids (byte of the 32-bit TMEM column) are
+// OR-ed in per instruction at bits 4-5 (B) and 29-30 (A)
+template <int BN>
+__host__ __device__ constexpr uint32_t mx_idesc() {
+  return (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | (1u << 23) | ((uint32_t)(TC_BM >> 4) << 24);
+}
+__device__ __forceinline__ uint32_t mx_sf_id(uint32_t id) { return (id << 4) | (id << 29); }
+__device__ __forceinline__ void tc_mma_mx(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate, uint32_t tsfa, uint32_t tsfb) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(tsfa), "r"(tsfb));
+}
+// scale factors smem -> TMEM: one 512-byte chunk (32 x 16 B, no swizzle, 8-row core
+// matrices 128 B apart) into 4 TMEM columns, broadcast to the 4 lane quarters
+__device__ __forceinline__ uint64_t sdesc_sf(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(512 >> 4) << 16) | ((uint64_t)(128 >> 4) << 32) |
+         ((uint64_t)1 << 46);
+}
+__device__ __forceinline__ void tc_cp_sf(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(sdesc));
 }
 template <int C>
 __device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -266,12 +305,16 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
            const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha, double beta,
            const int32_t* __restrict__ order) {
   constexpr int NP = tc_np<C>(), ST = tc_stages<C>();
+  constexpr bool MX = (C == GMP_MX);       // MXFP4: 4-bit elements + scale-factor chunks per stage
+  static_assert(!MX || BN == 128, "MXFP4 runs at BN = 128 (TMEM: 2 x 128 accumulator + scale columns)");
   constexpr int ESZ = (C == 4 || C == 5) ? 1 : 2;
-  constexpr int BK = 128 / ESZ;            // elements per 128-byte K block
+  constexpr int BK = MX ? 256 : 128 / ESZ; // elements per 128-byte K block
   constexpr int NMMA = 4;                  // 32-byte K per tcgen05.mma
-  constexpr int A_BYTES = TC_BM * 128, B_BYTES = BN * 128, STAGE_BYTES = NP * (A_BYTES + B_BYTES);
-  constexpr uint32_t TMEM_COLS = 2 * BN;
-  constexpr uint32_t IDESC = tc_idesc<(C == TC_SPLIT ? 3 : C), BN>();
+  constexpr int A_BYTES = TC_BM * 128, B_BYTES = BN * 128;
+  constexpr int SF_BYTES = MX ? 1024 : 0;  // per operand: 128 rows x 8 scales = 2 chunks of 512 B
+  constexpr int STAGE_BYTES = NP * (A_BYTES + B_BYTES) + 2 * SF_BYTES;
+  constexpr uint32_t TMEM_COLS = MX ? 512 : 2 * BN;
+  constexpr uint32_t IDESC = MX ? mx_idesc<BN>() : tc_idesc<(C == TC_SPLIT || C == GMP_MX ? 3 : C), BN>();
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -312,11 +355,21 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
             mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* sa = smem + stage * STAGE_BYTES;
             mbar_expect_tx(&full[stage], STAGE_BYTES);
+            if constexpr (MX) {
+              // elements: 3-D maps (byte in row, row, slot); scales: the two 512-byte chunks
+              // of this 128-row group and K block, contiguous in the slot (mx_sf_offset)
+              tma_load_3d(sa, &tmA, kb * 128, w.m0, pd.a_slot, &full[stage]);
+              tma_load_3d(sa + A_BYTES, &tmB, kb * 128, w.n0, pd.b_slot, &full[stage]);
+              const int64_t sfa = mx_sf_offset(nb, w.m0, kb * 8), sfb = mx_sf_offset(nb, w.n0, kb * 8);
+              bulk_load(sa + A_BYTES + B_BYTES, ws + pd.a_off + sfa, SF_BYTES, &full[stage]);
+              bulk_load(sa + A_BYTES + B_BYTES + SF_BYTES, ws + pd.b_off + sfb, SF_BYTES, &full[stage]);
+            } else {
 #pragma unroll
-            for (int p = 0; p < NP; ++p) {
-              tma_load_2d(sa + p * A_BYTES, &tmA, kb * BK, (pd.a_slot * NP + p) * nb + w.m0, &full[stage]);
-              tma_load_2d(sa + NP * A_BYTES + p * B_BYTES, &tmB, kb * BK, (pd.b_slot * NP + p) * nb + w.n0,
-                          &full[stage]);
+              for (int p = 0; p < NP; ++p) {
+                tma_load_2d(sa + p * A_BYTES, &tmA, kb * BK, (pd.a_slot * NP + p) * nb + w.m0, &full[stage]);
+                tma_load_2d(sa + NP * A_BYTES + p * B_BYTES, &tmB, kb * BK, (pd.b_slot * NP + p) * nb + w.n0,
+                            &full[stage]);
+              }
             }
             if (++stage == ST) { stage = 0; phase ^= 1; }
           }
@@ -337,6 +390,23 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
             mbar_wait(&full[stage], phase);
             tc_fence_after();
             const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+            if constexpr (MX) {
+              // scales of this K block -> TMEM (in issue order with the MMAs: the previous
+              // block's MMAs have read the same columns before these copies land), then
+              // 4 MMAs of K = 64; MMA k reads chunk k/2 at byte 2 (k%2) of each column
+              const uint32_t tsfa = tmem_base + 2 * BN, tsfb = tsfa + 8;
+              const uint32_t ssf = sa + A_BYTES + B_BYTES;
+#pragma unroll
+              for (int c = 0; c < 2; ++c) {
+                tc_cp_sf(tsfa + 4 * c, sdesc_sf(ssf + 512 * c));
+                tc_cp_sf(tsfb + 4 * c, sdesc_sf(ssf + SF_BYTES + 512 * c));
+              }
+              const uint64_t ad = sdesc_k_sw128(sa), bd = sdesc_k_sw128(sa + A_BYTES);
+#pragma unroll
+              for (int k = 0; k < NMMA; ++k)
+                tc_mma_mx(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), IDESC | mx_sf_id(2 * (k & 1)),
+                          (kb | k) != 0, tsfa + 4 * (k >> 1), tsfb + 4 * (k >> 1));
+            } else {
 #pragma unroll
             for (int t = 0; t < NP * NP; ++t) {
               // terms (i, j) by decreasing i + j: the smallest part products first
@@ -347,6 +417,7 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
 #pragma unroll
               for (int k = 0; k < NMMA; ++k)
                 tc_mma<C>(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), IDESC, (kb | t | k) != 0);
+            }
             }
             tc_commit(&empty[stage]);
             if (++stage == ST) { stage = 0; phase ^= 1; }
@@ -368,7 +439,8 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
 
 template <int C, int BN>
 constexpr int tc_smem_bytes() {
-  return tc_stages<C>() * tc_np<C>() * (TC_BM * 128 + BN * 128) + 1024 /*align*/ + 256 /*barriers*/;
+  return tc_stages<C>() * (tc_np<C>() * (TC_BM * 128 + BN * 128) + (C == GMP_MX ? 2048 : 0)) + 1024 /*align*/ +
+         256 /*barriers*/;
 }
 
 // ---------------------------------------------------------------------------
@@ -409,6 +481,23 @@ inline gmp_status_t tc_prepare(TcTables& t, uint8_t* ws, const int64_t* arena_of
     PFN_encodeTiled enc = get_encode_tiled();
     if (!enc) return GMP_ERR_CUDA;
     const bool split = c == GMP_AR_SPLIT;
+    if (c == GMP_MX) {
+      // MXFP4 slots hold nb rows of nb/2 element bytes, then the scale bytes: 3-D map
+      // (byte in row, row, slot), 128-byte x 128-row boxes
+      cuuint64_t dims[3] = {(cuuint64_t)(nb / 2), (cuuint64_t)nb, (cuuint64_t)arena_slots[c]};
+      cuuint64_t strides[2] = {(cuuint64_t)(nb / 2), (cuuint64_t)mx_slot_bytes(nb)};
+      cuuint32_t box[3] = {128u, 128u, 1u};
+      cuuint32_t estr[3] = {1, 1, 1};
+      void* base = ws + arena_off[c];
+      if (enc(&t.mapA[c], CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return GMP_ERR_CUDA;
+      t.mapB[c] = t.mapA[c];
+      t.mapB128[c] = t.mapA[c];
+      t.ready[c] = true;
+      continue;
+    }
     const int esz = (c == 4 || c == 5) ? 1 : 2;
     const int64_t rows = arena_slots[c] * (split ? 3 : 1) * nb;
     cuuint64_t dims[2] = {(cuuint64_t)nb, (cuuint64_t)rows};
@@ -458,9 +547,11 @@ inline gmp_status_t tc_launch(TcTables& t, int cls, int bn, const WorkItem* it, 
                               const CTileDesc* ct, uint8_t* ws, int nb, double alpha, double beta, const int32_t* order,
                               cudaStream_t s) {
   const int mi = (cls == TC_SPLIT) ? GMP_AR_SPLIT : cls;
-  if (!((cls >= 2 && cls <= 5) || cls == TC_SPLIT) || !t.ready[mi]) return GMP_ERR_STATE;
+  if (!((cls >= 2 && cls <= GMP_MX) || cls == TC_SPLIT) || !t.ready[mi]) return GMP_ERR_STATE;
+  if (cls == GMP_MX && bn != 128) return GMP_ERR_STATE;
   const bool wide = bn == 256;
   switch (cls) {
+    case GMP_MX: return tc_launch_t<GMP_MX, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s);
     case 2: return wide ? tc_launch_t<2, 256>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s) : tc_launch_t<2, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s);
     case 3: return wide ? tc_launch_t<3, 256>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s) : tc_launch_t<3, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s);
     case 4: return wide ? tc_launch_t<4, 256>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s) : tc_launch_t<4, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s);

@@ -54,8 +54,8 @@ def test_empty_or_negative_shapes_rejected(kw):
 def test_host_plan_rejects_bad_codes():
     import numpy as np
     d = B.make_desc(256, 256, 256, 128, 1e-6)
-    bad = np.full((2, 2), 7, np.uint8)
-    z = np.zeros((2, 2, 6), np.int16)
+    bad = np.full((2, 2), 7, np.uint8)   # code 7: beyond MXFP4 (6)
+    z = np.zeros((2, 2, B.NCLS), np.int16)
     with pytest.raises(B.GmpError) as e:
         B.gemm_mp_plan_host(d, bad, bad, bad, z, z)
     assert "GMP_ERR_MAP_SHAPE" in str(e.value)
@@ -68,8 +68,8 @@ def test_host_plan_checks_scale_array_sizes():
     d = B.make_desc(256, 256, 256, 128, 1e-6)
     c = np.zeros((2, 2), np.uint8)
     with pytest.raises(ValueError):
-        B.gemm_mp_plan_host(d, c, c, c, np.zeros((2, 2, 5), np.int16), np.zeros((2, 2, 6), np.int16))
-    pl = B.gemm_mp_plan_host(d, c, c, c, np.zeros((2, 2, 6), np.int16), np.zeros((2, 2, 6), np.int16))
+        B.gemm_mp_plan_host(d, c, c, c, np.zeros((2, 2, B.NCLS - 1), np.int16), np.zeros((2, 2, B.NCLS), np.int16))
+    pl = B.gemm_mp_plan_host(d, c, c, c, np.zeros((2, 2, B.NCLS), np.int16), np.zeros((2, 2, B.NCLS), np.int16))
     B.gemm_mp_destroy(pl)
 
 
@@ -85,7 +85,7 @@ def test_fused_tensor_launch_plan():
     bc = np.zeros((t, t), np.uint8)
     bc[1:, :] = 1
     cc = np.zeros((t, t), np.uint8)
-    z = np.zeros((t, t, 6), np.int16)
+    z = np.zeros((t, t, B.NCLS), np.int16)
     st = []
     for d in (d0, d1):
         pl = B.gemm_mp_plan_host(d, ac, bc, cc, z, z)
@@ -105,7 +105,7 @@ def test_host_plan_cannot_convert_or_execute():
     for P, Q in ((1, 1), (2, 2)):
         d = B.make_desc(512, 512, 512, 128, 1e-6, P=P, Q=Q, rank=0)
         c = np.zeros((4, 4), np.uint8)
-        z = np.zeros((4, 4, 6), np.int16)
+        z = np.zeros((4, 4, B.NCLS), np.int16)
         pl = B.gemm_mp_plan_host(d, c, c, c, z, z)
         try:
             for call in (lambda: B.gemm_mp_convert(pl, 1024, 1 << 40, None),

@@ -25,7 +25,7 @@ from paper_2508_14848_b200 import api
 from paper_2508_14848_b200 import binding as B
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-PEAK = np.array([35.5, 155.0, 1323.0, 1397.0, 2628.0, 2628.0])   # the library's default model (TF/s)
+PEAK = np.array([35.5, 155.0, 1323.0, 1397.0, 2628.0, 2628.0, 5588.0])   # the library's default model (TF/s)
 
 
 def golden_maps(cfg):
@@ -46,7 +46,7 @@ def rank_costs(a, b, rowP, colQ, P, Q, cost):
     mt, kt = a.shape
     nt = b.shape[1]
     pc = np.maximum(a[:, :, None], b[None, :, :])            # (i, l, j) pair classes
-    w = cost[:6][pc].sum(axis=1)                              # (i, j) tile-GEMM cost
+    w = cost[:7][pc].sum(axis=1)                              # (i, j) tile-GEMM cost
     rowP, colQ = np.asarray(rowP), np.asarray(colQ)
     out = np.zeros((P, Q))
     for p in range(P):
@@ -54,7 +54,7 @@ def rank_costs(a, b, rowP, colQ, P, Q, cost):
             nr, nc = int((rowP == p).sum()), int((colQ == q).sum())
             kq = len(range(q, kt, Q)); kp = len(range(p, kt, P))
             blk = w[np.ix_(rowP == p, colQ == q)].sum()
-            out[p, q] = blk + cost[6] * (nr * kq + kp * nc + nr * nc)
+            out[p, q] = blk + cost[7] * (nr * kq + kp * nc + nr * nc)
     return out
 
 
@@ -120,7 +120,7 @@ def test_owner_out_of_range_refused():
     d = B.make_desc(4 * nb, 4 * nb, 4 * nb, nb, 1e-4, P=2, Q=2, rank=0, row_owner=[0, 1, 2, 0],
                     col_owner=[0, 1, 0, 1])
     z = np.zeros((4, 4), np.uint8)
-    s5 = np.zeros((4, 4, 6), np.int16)
+    s5 = np.zeros((4, 4, B.NCLS), np.int16)
     with pytest.raises(B.GmpError) as e:
         B.gemm_mp_plan_host(d, z, z, z, s5, s5)
     assert e.value.code == 5
@@ -155,7 +155,7 @@ def _worker(rank, G, port, q_out):
         for name, (r_, c_) in (("cyclic", (None, None)), ("balanced", (ro, co))):
             d = B.make_desc(N, N, N, nb, 1e-4, P=P, Q=Q, rank=rank, row_owner=r_, col_owner=c_)
             z = np.zeros((N // nb, N // nb), np.uint8)
-            s5 = np.zeros((N // nb, N // nb, 6), np.int16)
+            s5 = np.zeros((N // nb, N // nb, B.NCLS), np.int16)
             pl = B.gemm_mp_plan_host(d, a, b, z, s5, s5)
             st = B.gemm_mp_get_stats(pl)
             B.gemm_mp_destroy(pl)

@@ -74,6 +74,35 @@ def test_explicit_maps_match_oracle():
     assert np.linalg.norm(out3 - o["C"]) / np.linalg.norm(o["C"]) <= 4 * 2.0 ** -24 * np.sqrt(512)
 
 
+@pytest.mark.parametrize("flags", [0, B.GMP_FLAG_SIMT_ONLY], ids=["tcgen05", "simt"])
+def test_explicit_all_mxfp4_operands(flags):
+    """NEXT-4: every A and B tile forced to MXFP4 (explicit maps, R19), C in FP32 / FP64:
+    stored MXFP4 bytes (nibbles + block scales) bitwise, C bitwise vs the oracle on the SIMT
+    kernel and within 4 u32 sqrt(K) on tcgen05 kind::mxf4.block_scale (3 x 2 x 4 tiles of 256,
+    several K blocks, both W precisions)"""
+    nb = 256
+    w = gmp_inputs.small_workload(3 * nb, 2 * nb, 4 * nb, nb, 1e-2, mode="random", E=20, beta=0.5,
+                                  class_mask=0b1111111, seed=61)
+    A, Bm, C = w.matrices()
+    maps = (np.full((3, 4), 6, np.uint8), np.full((4, 2), 6, np.uint8),
+            np.array([[1, 0], [0, 1], [1, 1]], np.uint8))
+    o = run_oracle(A, Bm, C, nb, w.tol, w.alpha, w.beta, w.class_mask, maps=maps)
+    assert o["rc"] == 0 and (o["acode"] == 6).all() and (o["bcode"] == 6).all()
+    g, (out,) = run_gpu(A, Bm, C, nb, w.tol, w.alpha, w.beta, w.class_mask, flags=flags, maps=maps)
+    for which, X, codes, s5 in (("A", A, o["acode"], o["ascale5"]), ("B", Bm, o["bcode"], o["bscale5"])):
+        for ti in range(codes.shape[0]):
+            for tj in range(codes.shape[1]):
+                tile = X[ti * nb:(ti + 1) * nb, tj * nb:(tj + 1) * nb]
+                want = oracle.pack_tile(tile, 6, int(s5[ti, tj, 6]), role=which)
+                got, sc = g.tile(which, ti, tj, 6)
+                assert sc == s5[ti, tj, 6] and np.array_equal(got, want), (which, ti, tj)
+    if flags & B.GMP_FLAG_SIMT_ONLY:
+        assert np.array_equal(out, o["C"])
+    else:
+        ok, rel = c_parity(out, o["C"], o["ccode"], o["cscale"], nb, w.K, False)
+        assert ok, rel
+
+
 def test_fp32_split_parts_are_exact():
     """The tensor-pipe FP32 class consumes x = x0 + x1 + x2 (three BF16 parts,
     K-major): the parts must reproduce every FP32 operand value exactly."""

@@ -105,7 +105,7 @@ def test_n65536_fullsize_properties(cfg):
     m = g.maps()
     st = g.stats()
     assert sum(st["pairs"]) == mt * nt * kt
-    enabled = {c for c in range(6) if (w.class_mask | 1) >> c & 1}
+    enabled = {c for c in range(7) if (w.class_mask | 1) >> c & 1}
     assert set(np.unique(m["acode"])) <= enabled and set(np.unique(m["bcode"])) <= enabled
     rng = np.random.default_rng(cfg)
     tiles = [(int(rng.integers(mt)), int(rng.integers(kt))) for _ in range(12)]

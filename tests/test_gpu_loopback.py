@@ -28,7 +28,7 @@ from paper_2508_14848_b200 import binding as B
 
 pytestmark = pytest.mark.gpu
 
-BYTES = [8, 4, 2, 2, 1, 1]
+BYTES = [8, 4, 2, 2, 1, 1, 17 / 32]   # per element; MXFP4: E2M1 nibbles + one scale byte per 32
 
 
 def closed_form_recv(acode, bcode, nb, P, Q, p, q, ro=None, co=None):
@@ -41,11 +41,11 @@ def closed_form_recv(acode, bcode, nb, P, Q, p, q, ro=None, co=None):
     for i in api.owned_tiles(mt, P, p, ro):
         for l in range(kt):
             if l % Q != q:
-                tot += nb * nb * BYTES[acode[i, l]]
+                tot += B.slot_bytes(int(acode[i, l]), nb)
     for j in api.owned_tiles(nt, Q, q, co):
         for l in range(kt):
             if l % P != p:
-                tot += nb * nb * BYTES[bcode[l, j]]
+                tot += B.slot_bytes(int(bcode[l, j]), nb)
     return tot
 
 
@@ -56,6 +56,9 @@ def _workload(kind):
     if kind == "uneven":  # 5 x 3 x 7 tiles: no grid divides them
         return gmp_inputs.small_workload(1280, 768, 1792, 256, 1e-3, mode="graded", E=24, beta=-0.5, seed=6,
                                          class_mask=0b111111)
+    if kind == "mx4":  # MXFP4 enabled: MXFP4 payloads (and sender-side MXFP4 shadows) on the wire
+        return gmp_inputs.small_workload(1024, 768, 1280, 256, 1e-2, mode="random", E=40, beta=0.5, seed=53,
+                                         class_mask=0b1111111)
     if kind == "tiny_nb128":  # 3 x 5 x 9 tiles of 128, beta = 0, FP32-heavy
         return gmp_inputs.small_workload(384, 640, 1152, 128, 1e-6, mode="random", E=20, beta=0.0, seed=7)
     raise ValueError(kind)
@@ -148,7 +151,7 @@ def single(kind, flags=0):
 GRIDS = [(1, 2), (2, 1), (2, 2), (1, 4), (4, 1), (2, 4)]
 
 
-@pytest.mark.parametrize("kind", ["small", "uneven", "tiny_nb128"])
+@pytest.mark.parametrize("kind", ["small", "uneven", "tiny_nb128", "mx4"])
 @pytest.mark.parametrize("sender", [False, True], ids=["receiver", "sender"])
 @pytest.mark.parametrize("grid", GRIDS, ids=[f"{p}x{q}" for p, q in GRIDS])
 def test_loopback_summa_bitwise_vs_single_gpu(grid, sender, kind):

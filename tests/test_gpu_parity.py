@@ -50,6 +50,14 @@ def _cases():
         ("pairs_e5m2_nb512", gmp_inputs.small_workload(1024, 1024, 1536, 512, 5e-2, mode="random", E=32,
                                                        beta=0.0, class_mask=0b111111, seed=48),
          B.GMP_FLAG_TC_PAIR),
+        # MXFP4 enabled (NEXT-4, R31): MXFP4 tiles (E2M1 nibbles + E8M0 block scales),
+        # MXFP4 shadows of every other class (k_mx), MXFP4 pairs on tcgen05 kind::mxf4.block_scale
+        ("mx4_mix", gmp_inputs.small_workload(512, 384, 640, 128, 1e-2, mode="random", E=40, beta=0.5,
+                                              class_mask=0b1111111, seed=41)),
+        ("mx4_nb256", gmp_inputs.small_workload(768, 512, 1024, 256, 2e-2, mode="random", E=40, beta=0.0,
+                                                class_mask=0b1111111, seed=50)),
+        ("mx4_fine", gmp_inputs.small_workload(512, 384, 640, 128, 1e-3, mode="random", E=40, beta=-0.75,
+                                               class_mask=0b1111111, seed=52)),
     ]
 
 

@@ -19,7 +19,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-BY = [8, 4, 2, 2, 1, 1]
+BY = [8, 4, 2, 2, 1, 1, 17 / 32]   # bytes per element; MXFP4: nibbles + one scale byte per 32
 
 
 def _free_port():
@@ -188,7 +188,7 @@ def test_spec_closed_form_128_bytes():
         for rank in range(2):
             d = B.make_desc(2 * nb, 2 * nb, 2 * nb, nb, 1e-6, 1.0, 0.0, 0b00011, 0, 2, 1, rank)
             ac = np.zeros((2, 2), np.uint8); bc = np.full((2, 2), bcls, np.uint8); cc = np.zeros((2, 2), np.uint8)
-            z = np.zeros((2, 2, 6), np.int16)
+            z = np.zeros((2, 2, B.NCLS), np.int16)
             pl = B.gemm_mp_plan_host(d, ac, bc, cc, z, z)
             s += B.gemm_mp_get_stats(pl)["recv_bytes_local"]
             B.gemm_mp_destroy(pl)

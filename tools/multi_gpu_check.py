@@ -22,7 +22,7 @@ from paper_2508_14848_b200 import binding as B  # noqa: E402
 def closed_form_recv(acode, bcode, nb, P, Q, p, q, row_owner=None, col_owner=None):
     mt, kt = acode.shape
     nt = bcode.shape[1]
-    by = [8, 4, 2, 2, 1, 1]
+    by = [8, 4, 2, 2, 1, 1, 17 / 32]
     tot = 0
     for i in api.owned_tiles(mt, P, p, row_owner):
         for l in range(kt):
