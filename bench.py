@@ -72,7 +72,7 @@ def load_peaks():
             "fallback (B200_PROFILING.md)"
 
 
-NCLS = 6   # FP64, FP32, FP16, BF16, E4M3, E5M2 (include/gemm_mp.h gmp_class_t)
+NCLS = 7   # FP64, FP32, FP16, BF16, E4M3, E5M2, MXFP4 (include/gemm_mp.h gmp_class_t)
 
 
 def class_peaks(measured, driver_peaks, sustained, fp32_on_tensor=True):
@@ -106,6 +106,10 @@ def class_peaks(measured, driver_peaks, sustained, fp32_on_tensor=True):
     put(4, m.get("e4m3" + suf), f"measured cuBLASLt E4M3 ({tag})", 2 * bf16_drv, "MEASURED_PEAKS.json BF16 x 2")
     put(5, m.get("e4m3" + suf), f"measured cuBLASLt E4M3 ({tag}; E5M2 same kind::f8f6f4 rate)",
         2 * bf16_drv, "MEASURED_PEAKS.json BF16 x 2")
+    e4 = m.get("e4m3" + suf)
+    put(6, m.get("mxfp4" + suf), f"measured cuBLASLt MXFP4 via torch._scaled_mm ({tag})",
+        2 * e4 if e4 else 4 * bf16_drv,
+        f"measured cuBLASLt E4M3 ({tag}) x 2 (nominal FP4/FP8 ratio)" if e4 else "MEASURED_PEAKS.json BF16 x 4")
     return pk, src
 
 
@@ -170,7 +174,7 @@ class Clocks:
 # CPU oracle baseline (rank 0, N = 1; and the --impl reference arm)
 # ---------------------------------------------------------------------------
 def gmp_class_name(c):
-    return ["FP64", "FP32", "FP16", "BF16", "E4M3", "E5M2"][c]
+    return ["FP64", "FP32", "FP16", "BF16", "E4M3", "E5M2", "MX4"][c]
 
 
 def cpu_model():
@@ -697,7 +701,7 @@ def main():
     # DRAM traffic per launch of the dominant kernel from the committed ncu capture
     traffic, traffic_src = None, None
     kpref = {0: "k_dmma<", 1: "k_tc_class<9,", 2: "k_tc_class<2,", 3: "k_tc_class<3,", 4: "k_tc_class<4,",
-             5: "k_tc_class<5,"}[dom]
+             5: "k_tc_class<5,", 6: "k_tc_class<6,"}[dom]
     for tf in ("traffic_r02.json", "traffic_r01.json"):
         try:
             with open(os.path.join(ROOT, "profiles", tf)) as f:
@@ -739,7 +743,8 @@ def main():
             # the paper's metric is speedup vs 100D:0S; BASELINE configs[1]
             # (cfg2) is quoted "vs all-FP64 baseline" on the same data
             "vs_baseline": vs_fp64 if a.config == 2 else None,
-            "dtype": "f64/f32/f16/bf16" + ("/e4m3" if w.class_mask & 16 else "") + " (per-tile classes)",
+            "dtype": "f64/f32/f16/bf16" + ("/e4m3" if w.class_mask & 16 else "") + ("/e5m2" if w.class_mask & 32 else "")
+                     + ("/mxfp4" if w.class_mask & 64 else "") + " (per-tile classes)",
             "data": "synthetic (counter-based SplitMix64, per-tile norm spread; DESIGN.md Input recipe)",
             "config": {"workload": w.name, "M": w.M, "N": w.N, "K": w.K, "nb": w.nb, "tol": w.tol,
                        "alpha": w.alpha, "beta": w.beta, "grid": f"{P}x{Q}", "parallelism": f"summa{P}x{Q}",

@@ -109,6 +109,7 @@ class Workload:
 
 NO_E4M3 = 0b01111
 WITH_E4M3 = 0b11111
+WITH_MX4 = 0b1000000   # class 6, MXFP4 (R31)
 
 
 def _rec(cfg, k, mode, E, s=0):
@@ -128,8 +129,11 @@ def workload(cfg, variant=None):
         return Workload("cfg3_N65536_nb2048_tol1e-4", 65536, 65536, 65536, 2048, 1e-4, 1.0, 0.0, NO_E4M3,
                         _rec(3, 1, "random", 32), _rec(3, 2, "random", 32), _rec(3, 3, "random", 32))
     if cfg == 4:
-        return Workload("cfg4_N65536_nb2048_tol1e-2_e4m3", 65536, 65536, 65536, 2048, 1e-2, 1.0, 0.0,
-                        WITH_E4M3, _rec(4, 1, "random", 40), _rec(4, 2, "random", 40), _rec(4, 3, "random", 40))
+        # variant "mx4": the same data with MXFP4 (class 6, NEXT-4) enabled as well
+        mx = variant == "mx4"
+        return Workload("cfg4_N65536_nb2048_tol1e-2_e4m3" + ("_mx4" if mx else ""), 65536, 65536, 65536, 2048,
+                        1e-2, 1.0, 0.0, WITH_E4M3 | (WITH_MX4 if mx else 0),
+                        _rec(4, 1, "random", 40), _rec(4, 2, "random", 40), _rec(4, 3, "random", 40))
     if cfg == 5:
         E = 0 if variant in (None, "uniform", "uniform_1e-2") else int(variant[1:])
         mode = "uniform" if E == 0 else "random"

@@ -31,19 +31,20 @@ def needs_build():
     return any(os.path.getmtime(s) > t for s in sources())
 
 
-def build(force=False, verbose=False):
-    if not force and not needs_build():
+def build(force=False, verbose=False, out=None, defines=()):
+    """out / defines: experiment builds (A/B runs load them through GMP_LIB_PATH)"""
+    if out is None and not force and not needs_build():
         return LIB
     inc, libdir = nccl_dirs()
     cmd = ["nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
            "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr",
            "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc,
-           os.path.join(CSRC, "gemm_mp_api.cu"), "-o", LIB,
-           "-L", libdir, "-l:libnccl.so.2", f"-Xlinker=-rpath={libdir}"]
+           os.path.join(CSRC, "gemm_mp_api.cu"), "-o", out or LIB,
+           "-L", libdir, "-l:libnccl.so.2", f"-Xlinker=-rpath={libdir}"] + [f"-D{d}" for d in defines]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)
-    return LIB
+    return out or LIB
 
 
 if __name__ == "__main__":

@@ -1353,7 +1353,10 @@ static gmp_status_t launch_shadows(const ShadowJob* djobs, const std::vector<Sha
 
 static gmp_status_t launch_mx(const MxJob* djobs, int64_t n, uint8_t* ws, int nb, cudaStream_t s) {
   if (n <= 0) return GMP_OK;
-  k_mx<<<dim3((unsigned)((nb / 32) * (nb / 128)), (unsigned)n), 256, 0, s>>>(djobs, ws, nb);
+  // one grid serves both orientations: nb*nb/128 warp units (rows x 128 K) = (nb/32)^2 x 2 (32 x 32 blocks) / 2
+  const int64_t units = std::max<int64_t>((int64_t)nb * (nb / 128), (int64_t)(nb / 32) * (nb / 32));
+  const unsigned grid = (unsigned)((units + 8 * MX_UNITS_PER_WARP - 1) / (8 * MX_UNITS_PER_WARP));
+  k_mx<<<dim3(grid, (unsigned)n), 256, 0, s>>>(djobs, ws, nb);
   GMP_CUDA(cudaGetLastError());
   return GMP_OK;
 }

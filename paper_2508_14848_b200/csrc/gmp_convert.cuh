@@ -223,8 +223,6 @@ __global__ void __launch_bounds__(256) k_shadow_t(const ShadowJob* __restrict__ 
 //   y = x 2^scale (pack: x = binary64 user element) or y = decode_from(stored) 2^d
 //   (shadow, receiver-side from the stored payload); per block of 32 consecutive
 //   K-elements of a K-major payload row: s_b = mx_block_exp(max |y|), q = RN_E2M1(y 2^-s_b).
-// One CTA = 32 payload rows x 128 K-elements (128 blocks, one per thread), staged
-// through shared memory so the loads are coalesced in either source orientation:
 //   transpose = 0: element (m, k) at src[m * ld + k]; 1: at src[k * ld + m].
 // ---------------------------------------------------------------------------
 struct MxJob {
@@ -238,48 +236,93 @@ struct MxJob {
   int16_t pad;
 };
 
-__device__ __forceinline__ double mx_src_value(const MxJob& j, const uint8_t* ws, int64_t idx) {
-  if (j.from < 0) return reinterpret_cast<const double*>(j.src)[idx];
-  return payload_f64(ws + j.src_off, idx, j.from);
-}
 
-__global__ void __launch_bounds__(256) k_mx(const MxJob* __restrict__ jobs, uint8_t* ws, int nb) {
-  __shared__ double sm[32][129];
+// Warp-per-unit, no shared memory.  transpose = 0 (payload row = source row): a unit is one
+// payload row x 128 K; lane l holds elements 4l..4l+3 (one 32-byte coalesced load per
+// lane), the 8 lanes of a block reduce max|y| by shuffles, every lane writes its 2 bytes of
+// nibbles and lane 8b the scale byte.  transpose = 1 (payload row = source column): a unit
+// is 32 payload rows x 32 K; lane l owns payload row m0 + l, the warp reads 32 source rows of
+// 32 consecutive elements (coalesced), each lane keeps its block in registers and writes
+// 16 bytes of nibbles and its scale byte.
+// Values are held as round-to-odd binary32 images of the exact binary64 y: RTO keeps every
+// comparison with a binary32 threshold (the block-scale test amax <= 6 * 2^s, the binade of
+// amax) and the final RNE onto the 2-bit E2M1 significand exact (>= 20 bits kept even for
+// binary32-subnormal y), at half the registers of binary64.
+constexpr int MX_UNITS_PER_WARP = 8;
+__device__ __forceinline__ uint32_t mx_enc2f(float a, float b) {   // two scaled values -> one byte
+  uint16_t r;
+  asm("{.reg .b8 t; cvt.rn.satfinite.e2m1x2.f32 t, %1, %2; cvt.u16.u8 %0, t;}" : "=h"(r) : "f"(b), "f"(a));
+  return (uint32_t)r & 0xFFu;
+}
+__device__ __forceinline__ uint32_t mx_enc4f(const float* v, float inv) {   // 4 values -> 2 bytes
+  return mx_enc2f(v[0] * inv, v[1] * inv) | (mx_enc2f(v[2] * inv, v[3] * inv) << 8);
+}
+__device__ __forceinline__ float mx_inv_scale(int sb) { return __int_as_float((127 - sb) << 23); }   // 2^-sb, sb in [-127, 125]
+__device__ __forceinline__ float mx_load(const MxJob& j, const uint8_t* base, int64_t idx) {
+  const double x = j.from < 0 ? __ldg(reinterpret_cast<const double*>(base) + idx) : payload_f64(base, idx, j.from);
+  return rto_f32(ldexp_fast(x, j.scale));
+}
+__global__ void __launch_bounds__(256, 4) k_mx(const MxJob* __restrict__ jobs, uint8_t* ws, int nb) {
   const MxJob j = jobs[blockIdx.y];
-  const int per = nb / 128;                       // 128-K chunks per row group
-  const int m0 = (blockIdx.x / per) * 32, k0 = (blockIdx.x % per) * 128;
-  const int t = threadIdx.x;
-#pragma unroll 4
-  for (int u = 0; u < 16; ++u) {
-    const int idx = t + u * 256;                  // 4096 elements of the 32 x 128 region
-    int m, k;
-    if (!j.transpose) { m = idx >> 7; k = idx & 127; }
-    else { k = idx >> 5; m = idx & 31; }
-    const int64_t si = j.transpose ? (int64_t)(k0 + k) * j.ld + m0 + m : (int64_t)(m0 + m) * j.ld + k0 + k;
-    sm[m][k] = ldexp_fast(mx_src_value(j, ws, si), j.scale);
-  }
-  __syncthreads();
-  if (t < 128) {
-    const int m = t >> 2, b = t & 3;              // payload row m0 + m, block (k0 / 32) + b
-    double amax = 0.0;
-#pragma unroll 8
-    for (int v = 0; v < 32; ++v) amax = fmax(amax, fabs(sm[m][b * 32 + v]));
-    const int sb = mx_block_exp(amax);
-    uint32_t w[4];
+  const uint8_t* base = j.from < 0 ? j.src : ws + j.src_off;
+  uint8_t* slot = ws + j.dst_off;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * MX_UNITS_PER_WARP;
+  if (!j.transpose) {
+    const int per = nb / 128;   // units per payload row
+    // four units per round: their loads are all in flight before any reduction
+    for (int u0 = 0; u0 < MX_UNITS_PER_WARP; u0 += 4) {
+      float v[4][4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint32_t x = 0;
+      for (int q = 0; q < 4; ++q) {
+        const int64_t unit = warp0 + u0 + q;
+        const int m = (int)(unit / per), k0 = (int)(unit % per) * 128 + 4 * lane;
+        if (unit >= (int64_t)nb * per) { v[q][0] = v[q][1] = v[q][2] = v[q][3] = 0.f; continue; }
+        if (j.from < 0) {
+          const double2* p = reinterpret_cast<const double2*>(reinterpret_cast<const double*>(base) + (int64_t)m * j.ld + k0);
+          const double2 a = __ldg(p), b = __ldg(p + 1);
+          v[q][0] = rto_f32(ldexp_fast(a.x, j.scale)); v[q][1] = rto_f32(ldexp_fast(a.y, j.scale));
+          v[q][2] = rto_f32(ldexp_fast(b.x, j.scale)); v[q][3] = rto_f32(ldexp_fast(b.y, j.scale));
+        } else {
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int e = b * 32 + q * 8 + 2 * v;
-        x |= cvt_e2m1x2_rn(ldexp_fast(sm[m][e], -sb), ldexp_fast(sm[m][e + 1], -sb)) << (8 * v);
+          for (int e = 0; e < 4; ++e) v[q][e] = mx_load(j, base, (int64_t)m * j.ld + k0 + e);
+        }
       }
-      w[q] = x;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t unit = warp0 + u0 + q;
+        if (unit >= (int64_t)nb * per) break;
+        const int m = (int)(unit / per), k0 = (int)(unit % per) * 128 + 4 * lane;
+        float amax = fmaxf(fmaxf(fabsf(v[q][0]), fabsf(v[q][1])), fmaxf(fabsf(v[q][2]), fabsf(v[q][3])));
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 4));
+        const int sb = mx_block_exp((double)amax);
+        *reinterpret_cast<uint16_t*>(slot + (int64_t)m * (nb >> 1) + (k0 >> 1)) = (uint16_t)mx_enc4f(v[q], mx_inv_scale(sb));
+        if ((lane & 7) == 0) slot[mx_sf_offset(nb, m, k0 >> 5)] = (uint8_t)(sb + 127);
+      }
     }
-    uint8_t* slot = ws + j.dst_off;
-    *reinterpret_cast<uint4*>(slot + (int64_t)(m0 + m) * (nb >> 1) + ((k0 + b * 32) >> 1)) =
-        make_uint4(w[0], w[1], w[2], w[3]);
-    slot[mx_sf_offset(nb, m0 + m, (k0 >> 5) + b)] = (uint8_t)(sb + 127);
+  } else {
+    const int per = nb / 32;    // units per 32-row band
+    for (int u = 0; u < MX_UNITS_PER_WARP; ++u) {
+      const int64_t unit = warp0 + u;
+      if (unit >= (int64_t)per * per) break;
+      const int m = (int)(unit / per) * 32 + lane, kb = (int)(unit % per);
+      float v[32];
+      float amax = 0.f;
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        v[e] = mx_load(j, base, (int64_t)(kb * 32 + e) * j.ld + m);
+        amax = fmaxf(amax, fabsf(v[e]));
+      }
+      const int sb = mx_block_exp((double)amax);
+      const float inv = mx_inv_scale(sb);
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) w[q] = mx_enc4f(v + 8 * q, inv) | (mx_enc4f(v + 8 * q + 4, inv) << 16);
+      *reinterpret_cast<uint4*>(slot + (int64_t)m * (nb >> 1) + kb * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+      slot[mx_sf_offset(nb, m, kb)] = (uint8_t)(sb + 127);
+    }
   }
 }
 

@@ -1,0 +1,4 @@
+set -x
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_edges.py tests/test_gpu_loopback.py -x -q -k "mx4 or mxfp4" > gpurun_out/mx_tests.log 2>&1; echo t=$?
+A="--config 4 --variant mx4 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-peaks --no-fp64-baseline"
+timeout 600 python bench.py $A > gpurun_out/bench_cfg4_mx4.log 2>&1; echo b=$?

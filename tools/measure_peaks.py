@@ -69,6 +69,18 @@ def measure(sustain_s=2.0, N=8192, dev="cuda", hbm=False):
             del a, b
         except Exception as ex:  # noqa
             out["e4m3_error"] = repr(ex)[:200]
+        try:   # MXFP4 (E2M1 x E2M1, E8M0 scale per 32 K) through torch._scaled_mm (cuBLASLt block scaling)
+            a = torch.randint(0, 256, (N, N // 2), device=dev, dtype=torch.uint8).view(torch.float4_e2m1fn_x2)
+            b = torch.randint(0, 256, (N, N // 2), device=dev, dtype=torch.uint8).view(torch.float4_e2m1fn_x2)
+            sa = torch.full((N, N // 32), 127, device=dev, dtype=torch.uint8).view(torch.float8_e8m0fnu)
+            sb = torch.full((N, N // 32), 127, device=dev, dtype=torch.uint8).view(torch.float8_e8m0fnu)
+            burst, sus = _bench(lambda: torch._scaled_mm(a, b.t(), scale_a=sa, scale_b=sb, out_dtype=torch.bfloat16),
+                                fl, sustain_s=sustain_s)
+            out["mxfp4_tflops"] = round(burst, 1)
+            out["mxfp4_tflops_sustained"] = round(sus, 1)
+            del a, b, sa, sb
+        except Exception as ex:  # noqa
+            out["mxfp4_error"] = repr(ex)[:200]
         if hbm:
             x = torch.empty(1 << 30, device=dev, dtype=torch.bfloat16)
             y = torch.empty_like(x)
