@@ -75,12 +75,13 @@ def load_peaks():
 NCLS = 7   # FP64, FP32, FP16, BF16, E4M3, E5M2, MXFP4 (include/gemm_mp.h gmp_class_t)
 
 
-def class_peaks(measured, driver_peaks, sustained, fp32_on_tensor=True):
+def class_peaks(measured, driver_peaks, sustained, fp32_on_tensor=True, fp32_terms=6):
     """Peak of the hardware path each class runs on, from the
     library GEMMs measured in this run (tools/measure_peaks.py) -- the sustained
     figure when the timed region ran power-capped, else the burst one:
       FP64: cuBLAS DGEMM (the DMMA pipe);  FP32: the default path is nine BF16 MMAs
-      per product (BF16x9 on tcgen05), so cuBLASLt BF16 / 9 (the FFMA path's
+      per product by default (BF16x6 on tcgen05; nine with GMP_FLAG_FP32_X9), so cuBLASLt
+      BF16 / 6 (or / 9) (the FFMA path's
       library figure, cuBLAS SGEMM, is reported beside it);  FP16 / BF16: cuBLASLt;
       E4M3 and E5M2 (same tcgen05 kind::f8f6f4 rate): cuBLASLt E4M3.
     Falls back to MEASURED_PEAKS.json's BF16 x nominal ratios (FP64: 148 SMs x 64
@@ -97,8 +98,9 @@ def class_peaks(measured, driver_peaks, sustained, fp32_on_tensor=True):
     tag = "sustained" if sustained else "burst"
     put(0, m.get("fp64" + suf), f"measured cuBLAS DGEMM ({tag})", ALU_PEAK_TFLOPS[0], "derived 148x64x2x1965MHz")
     if fp32_on_tensor:
-        put(1, bf16 / 9.0 if bf16 else None, f"measured cuBLASLt BF16 ({tag}) / 9 (BF16x9)",
-            bf16_drv / 9.0, "MEASURED_PEAKS.json BF16 / 9")
+        put(1, bf16 / fp32_terms if bf16 else None,
+            f"measured cuBLASLt BF16 ({tag}) / {fp32_terms} (BF16x{fp32_terms})",
+            bf16_drv / fp32_terms, f"MEASURED_PEAKS.json BF16 / {fp32_terms}")
     else:
         put(1, m.get("fp32" + suf), f"measured cuBLAS SGEMM ({tag})", ALU_PEAK_TFLOPS[1], "derived FFMA")
     put(2, m.get("fp16" + suf), f"measured cuBLASLt FP16 ({tag})", bf16_drv, "MEASURED_PEAKS.json BF16")
@@ -679,7 +681,9 @@ def main():
     # burst peaks when the step ran at >= 90 % of max SM clock, else the sustained
     # (power-capped) ones -- the guide's rule for short vs long kernels
     hot = bool(clk and clk.get("sm_mhz") and clk.get("sm_max_mhz") and clk["sm_mhz"] >= 0.9 * clk["sm_max_mhz"])
-    cpk, csrc = class_peaks(measured if measured and "error" not in measured else None, peaks, sustained=not hot)
+    cpk, csrc = class_peaks(measured if measured and "error" not in measured else None, peaks, sustained=not hot,
+                            fp32_on_tensor=not (flags & (B.GMP_FLAG_FP32_FFMA | B.GMP_FLAG_SIMT_ONLY)),
+                            fp32_terms=9 if flags & B.GMP_FLAG_FP32_X9 else 6)
     dom = max(range(NCLS), key=lambda c: class_ms[c])
     # precision-induced load imbalance: per-rank tile-GEMM device time
     busy = [sum(class_ms)]

@@ -74,7 +74,10 @@ typedef enum {
 #define GMP_FLAG_FP64_INT8 8u /* experimental: FP64 class on the INT8 tensor pipe (7 exact int8 digits
                                  per element, 28 tcgen05 kind::i8 MMAs) instead of DMMA (default)    */
 #define GMP_FLAG_FP32_FFMA 4u /* FP32 class on the FP32 pipe (packed FFMA2, bitwise O8) instead of the
-                                 default tensor-pipe path (exact BF16x3 split, nine BF16 MMAs per block) */
+                                 default tensor-pipe path (exact BF16x3 split, six BF16 MMAs per block) */
+#define GMP_FLAG_FP32_X9 1024u /* FP32 class on the tensor pipe with all nine BF16 part products (exact
+                                 products, BF16x9) instead of the default six with i + j <= 2 (BF16x6: the
+                                 three dropped terms are below 2^-26 of each product; R32)  */
 #define GMP_FLAG_TC_PAIR 32u /* opt-in: FP16/BF16/E4M3/E5M2 launches whose C tiles fold into binary32 W
                                  and whose nb is a multiple of 256 run on SM pairs (tcgen05 cta_group::2,
                                  256 x 256 sub-tiles, half the B bytes per SM), rastered by C tile row

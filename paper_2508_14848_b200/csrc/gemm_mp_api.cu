@@ -179,6 +179,11 @@ static inline bool pair_default(uint32_t flags) {
   return (flags & GMP_FLAG_TC_PAIR) && !(flags & GMP_FLAG_TC_SINGLE);
 }
 
+// FP32 class on the tensor pipe: BF16x6 (the six part products x_i y_j with i + j <= 2;
+// products accurate to ~2^-26 relative, R32) unless GMP_FLAG_FP32_X9 asks for all
+// nine (exact products)
+static inline int split_t0(uint32_t flags) { return (flags & GMP_FLAG_FP32_X9) ? 0 : 3; }
+
 static inline int16_t layout_transposed(int role, int cls) {
   const bool mn = cls <= 1;
   return (int16_t)(role == 0 ? mn : !mn);
@@ -1636,10 +1641,12 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
       } else if (L.kind == 6) {
         GMP_TRY(tcmc_launch(pl->tc, L.cls, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, stream));
       } else if (L.kind == 7) {
-        GMP_TRY(tcf_launch(pl->tc, L.present, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, pl->d.beta, stream));
+        GMP_TRY(tcf_launch(pl->tc, L.present, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, pl->d.beta, stream,
+                           split_t0(pl->d.flags)));
       } else if (L.kind == 1 || L.kind == 3) {
-        GMP_TRY(tc_launch(pl->tc, L.kind == 3 ? TC_SPLIT : L.cls, L.bn, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha,
-                          pl->d.beta, L.obeg >= 0 ? (const int32_t*)(ws + pl->off_order) + L.obeg : nullptr, stream));
+        GMP_TRY(tc_launch(pl->tc, L.kind == 3 ? (split_t0(pl->d.flags) ? TC_SPLIT6 : TC_SPLIT) : L.cls, L.bn, it,
+                          L.icount, pd, dct, ws, (int)nb, pl->d.alpha, pl->d.beta,
+                          L.obeg >= 0 ? (const int32_t*)(ws + pl->off_order) + L.obeg : nullptr, stream));
       } else {
         switch (L.cls) {
           case 0:

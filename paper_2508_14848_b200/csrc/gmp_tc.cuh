@@ -293,14 +293,17 @@ __device__ __forceinline__ void tc_epilogue(const WorkItem* __restrict__ items, 
 // from the stored FP32 payload), NP = 3, and all nine part products -- each
 // exact in the FP32 accumulator's inputs -- are accumulated per K block,
 // smallest terms first; binary32 inputs, exact products, binary32 accumulation.
-constexpr int TC_SPLIT = 9;   // template id of the FP32-class (BF16x9) kernel; its maps are arena GMP_AR_SPLIT
-template <int C> constexpr int tc_np() { return C == TC_SPLIT ? 3 : 1; }
+constexpr int TC_SPLIT = 9;    // template id of the FP32-class kernel, all nine part products (BF16x9, exact)
+constexpr int TC_SPLIT6 = 10;  // the six part products x_i y_j with i + j <= 2 (BF16x6, the default; R32)
+template <int C> constexpr bool tc_is_split() { return C == TC_SPLIT || C == TC_SPLIT6; }
+template <int C> constexpr int tc_np() { return tc_is_split<C>() ? 3 : 1; }
+template <int C> constexpr int tc_t0() { return C == TC_SPLIT6 ? 3 : 0; }   // first part product (smallest first)
 // MXFP4: 4 stages of 34 KB (6 measured 13 % slower in the cfg4-mx4 step)
 #ifndef GMP_MX_STAGES
 #define GMP_MX_STAGES 4
 #endif
-template <int C> constexpr int tc_stages() { return C == TC_SPLIT ? 2 : C == GMP_MX ? GMP_MX_STAGES : TC_STAGES; }
-template <int C> constexpr int tc_map_index() { return C == TC_SPLIT ? GMP_AR_SPLIT : C; }
+template <int C> constexpr int tc_stages() { return tc_is_split<C>() ? 2 : C == GMP_MX ? GMP_MX_STAGES : TC_STAGES; }
+template <int C> constexpr int tc_map_index() { return tc_is_split<C>() ? GMP_AR_SPLIT : C; }
 
 template <int C, int BN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -318,7 +321,7 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
   constexpr int SF_BYTES = MX ? 1024 : 0;  // per operand: 128 rows x 8 scales = 2 chunks of 512 B
   constexpr int STAGE_BYTES = NP * (A_BYTES + B_BYTES) + 2 * SF_BYTES;
   constexpr uint32_t TMEM_COLS = MX ? 512 : 2 * BN;
-  constexpr uint32_t IDESC = MX ? mx_idesc<BN>() : tc_idesc<(C == TC_SPLIT || C == GMP_MX ? 3 : C), BN>();
+  constexpr uint32_t IDESC = MX ? mx_idesc<BN>() : tc_idesc<(tc_is_split<C>() || C == GMP_MX ? 3 : C), BN>();
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -411,8 +414,9 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
                 tc_mma_mx(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), IDESC | mx_sf_id(2 * (k & 1)),
                           (kb | k) != 0, tsfa + 4 * (k >> 1), tsfb + 4 * (k >> 1));
             } else {
+            constexpr int t0 = tc_t0<C>();
 #pragma unroll
-            for (int t = 0; t < NP * NP; ++t) {
+            for (int t = t0; t < NP * NP; ++t) {
               // terms (i, j) by decreasing i + j: the smallest part products first
               constexpr int TI[9] = {2, 2, 1, 2, 1, 0, 1, 0, 0}, TJ[9] = {2, 1, 2, 0, 1, 2, 0, 1, 0};
               const int ti = (NP == 1) ? 0 : TI[t], tj = (NP == 1) ? 0 : TJ[t];
@@ -420,7 +424,7 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
               const uint64_t bd = sdesc_k_sw128(sa + NP * A_BYTES + tj * B_BYTES);
 #pragma unroll
               for (int k = 0; k < NMMA; ++k)
-                tc_mma<C>(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), IDESC, (kb | t | k) != 0);
+                tc_mma<C>(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), IDESC, (kb | (t - t0) | k) != 0);
             }
             }
             tc_commit(&empty[stage]);
@@ -550,8 +554,8 @@ inline gmp_status_t tc_launch_t(TcTables& t, const WorkItem* it, int64_t n, cons
 inline gmp_status_t tc_launch(TcTables& t, int cls, int bn, const WorkItem* it, int64_t n, const PairDesc* pd,
                               const CTileDesc* ct, uint8_t* ws, int nb, double alpha, double beta, const int32_t* order,
                               cudaStream_t s) {
-  const int mi = (cls == TC_SPLIT) ? GMP_AR_SPLIT : cls;
-  if (!((cls >= 2 && cls <= GMP_MX) || cls == TC_SPLIT) || !t.ready[mi]) return GMP_ERR_STATE;
+  const int mi = (cls == TC_SPLIT || cls == TC_SPLIT6) ? GMP_AR_SPLIT : cls;
+  if (!((cls >= 2 && cls <= GMP_MX) || cls == TC_SPLIT || cls == TC_SPLIT6) || !t.ready[mi]) return GMP_ERR_STATE;
   if (cls == GMP_MX && bn != 128) return GMP_ERR_STATE;
   const bool wide = bn == 256;
   switch (cls) {
@@ -560,6 +564,7 @@ inline gmp_status_t tc_launch(TcTables& t, int cls, int bn, const WorkItem* it, 
     case 3: return wide ? tc_launch_t<3, 256>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s) : tc_launch_t<3, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s);
     case 4: return wide ? tc_launch_t<4, 256>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s) : tc_launch_t<4, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s);
     case 5: return wide ? tc_launch_t<5, 256>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s) : tc_launch_t<5, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s);
+    case TC_SPLIT6: return tc_launch_t<TC_SPLIT6, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s);
     default: return tc_launch_t<TC_SPLIT, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s);
   }
 }

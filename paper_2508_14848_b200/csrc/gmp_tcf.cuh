@@ -53,6 +53,8 @@ struct TcfRing {
   }
 };
 
+// T0: first FP32-split part product (3: BF16x6, the default; 0: BF16x9), as k_tc_class
+template <int T0>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_tc_fused(const __grid_constant__ TcfMaps maps, const WorkItem* __restrict__ items, int64_t nitems,
            const PairDesc* __restrict__ pairs, const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb,
@@ -135,14 +137,16 @@ k_tc_fused(const __grid_constant__ TcfMaps maps, const WorkItem* __restrict__ it
             tc_fence_after();
             if (np == 3) {
 #pragma unroll
-              for (int t = 0; t < 9; ++t) {
-                // terms (i, j) by decreasing i + j: the smallest part products first (as k_tc_class)
+              for (int t = T0; t < 9; ++t) {
+                // terms (i, j) by decreasing i + j: the smallest part products first (as k_tc_class;
+                // split_t0 = 3: BF16x6, 0: BF16x9)
                 constexpr int TI[9] = {2, 2, 1, 2, 1, 0, 1, 0, 0}, TJ[9] = {2, 1, 2, 0, 1, 2, 0, 1, 0};
                 const uint64_t ad = sdesc_k_sw128(sl[TI[t]]);
                 const uint64_t bd = sdesc_k_sw128(sl[TJ[t]] + TCF_SLOT_A);
 #pragma unroll
                 for (int k = 0; k < NMMA; ++k)
-                  tc_mma<3>(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, (kb | t | k) != 0);
+                  tc_mma<3>(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc,
+                            (kb | (t - T0) | k) != 0);
               }
             } else {
               const uint64_t ad = sdesc_k_sw128(sl[0]);
@@ -181,7 +185,8 @@ constexpr int tcf_smem_bytes() { return TCF_SLOTS * TCF_SLOT + 1024 /*align*/ + 
 
 // cls_present: bit c set when the launch holds class-c pairs (c = 1 means the split arena)
 inline gmp_status_t tcf_launch(TcTables& t, unsigned cls_present, const WorkItem* it, int64_t n, const PairDesc* pd,
-                               const CTileDesc* ct, uint8_t* ws, int nb, double alpha, double beta, cudaStream_t s) {
+                               const CTileDesc* ct, uint8_t* ws, int nb, double alpha, double beta, cudaStream_t s,
+                               int split_t0 = 3) {
   TcfMaps m;
   std::memset(&m, 0, sizeof m);
   for (int c = 1; c <= 5; ++c) {
@@ -192,12 +197,14 @@ inline gmp_status_t tcf_launch(TcTables& t, unsigned cls_present, const WorkItem
     m.b[tcf_index(c)] = t.mapB128[ar];
   }
   constexpr int smem = tcf_smem_bytes();
-  if (ensure_max_smem(k_tc_fused, smem) != cudaSuccess) return GMP_ERR_CUDA;
+  if (ensure_max_smem(k_tc_fused<0>, smem) != cudaSuccess || ensure_max_smem(k_tc_fused<3>, smem) != cudaSuccess)
+    return GMP_ERR_CUDA;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)std::min<int64_t>(n, sms);
-  k_tc_fused<<<grid, TC_THREADS, smem, s>>>(m, it, n, pd, ct, ws, nb, alpha, beta);
+  if (split_t0) k_tc_fused<3><<<grid, TC_THREADS, smem, s>>>(m, it, n, pd, ct, ws, nb, alpha, beta);
+  else k_tc_fused<0><<<grid, TC_THREADS, smem, s>>>(m, it, n, pd, ct, ws, nb, alpha, beta);
   return cudaGetLastError() == cudaSuccess ? GMP_OK : GMP_ERR_CUDA;
 }
 
