@@ -76,6 +76,12 @@ static gmp_status_t fail(gmp_status_t s, const std::string& msg) {
     gmp_status_t s_ = (call);         \
     if (s_ != GMP_OK) return s_;      \
   } while (0)
+// kernel launchers of the gmp_*.cuh headers return bare codes: attach a message
+#define GMP_LAUNCH(call, what)                                                                    \
+  do {                                                                                            \
+    gmp_status_t s_ = (call);                                                                     \
+    if (s_ != GMP_OK) return fail(s_, std::string(what) + ": arena not prepared or launch failed"); \
+  } while (0)
 
 static inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 constexpr int NC = GMP_NCLASS;   // precision classes 0..6 (gmp_class_t)
@@ -963,15 +969,29 @@ static void build_tables(gmp_plan_s* pl) {
       for (int c = 0; c < NC; ++c) L.share[c] = tot > 0 ? L.share[c] / tot : 0.0;
       pl->launches.push_back(L);
     }
+    // FP16 and BF16 pairs of a step share one k_tc_class<3> launch (default): per item the
+    // BF16 pairs, then the FP16 pairs -- the fold order O9 -- so W is read and written once
+    // for both and the short FP16 lists ride on the BF16 items (GMP_FLAG_SPLIT16: one launch
+    // per class; the SM-pair / multicast kernels keep per-class launches)
+    const bool merge16 = tc_on && !fuse && !(d.flags & GMP_FLAG_SPLIT16) && !pair_default(d.flags) &&
+                         !(d.flags & GMP_FLAG_TC_MCAST);
     for (int c = NC - 1; c >= 0; --c) {
       if (fuse && c >= 1 && c <= 5) continue;   // MXFP4 pairs keep their own launch
+      if (merge16 && c == 2) continue;          // carried by the class-3 launch
       // MXFP4 on tcgen05 needs whole 256-element (128-byte) K blocks: nb = 128 runs on the SIMT kernel
       const bool tc = tc_on && (c >= 2) && (c != GMP_MX || nb % 256 == 0);
       const int64_t ibeg = (int64_t)pl->items.size();
       std::vector<WorkItem> its;
+      int64_t npair[NC] = {0};
       for (int64_t k = 0; k < nCl; ++k) {
         const int64_t pbeg = (int64_t)pl->pairs.size();
         add_pairs(s, c, k);
+        npair[c] += (int64_t)pl->pairs.size() - pbeg;
+        if (merge16 && c == 3) {
+          const int64_t p2 = (int64_t)pl->pairs.size();
+          add_pairs(s, 2, k);
+          npair[2] += (int64_t)pl->pairs.size() - p2;
+        }
         const int64_t pcnt = (int64_t)pl->pairs.size() - pbeg;
         if (!pcnt) continue;
         its.push_back(WorkItem{(int32_t)k, 0, 0, (int32_t)pbeg, (int32_t)pcnt, 0});
@@ -988,6 +1008,7 @@ static void build_tables(gmp_plan_s* pl) {
       pl->items.insert(pl->items.end(), its.begin(), its.end());
       const bool split = (c == 1 && pl->fp32_tc), ozaki = (c == 0 && pl->fp64_tc);
       const int kind = ozaki ? 4 : split ? 3 : tc ? 1 : (c == 0 && (d.flags & GMP_FLAG_SIMT_ONLY)) ? 2 : 0;
+      const bool merged = merge16 && c == 3 && npair[2] > 0;
       // tcgen05 launches that fold into binary64 W keep the accumulator rows in
       // registers, which needs BN = 128
       bool w64 = false;
@@ -1007,6 +1028,12 @@ static void build_tables(gmp_plan_s* pl) {
       const int bn = ozaki ? OZ_BN : split ? 128 : tc ? tcbn : (c == 0 && kind == 0) ? DMMA_BN : mn_bn(c);
       Launch L{s, c, kind, ibeg, (int64_t)its.size() * subtiles_per_item((int)nb, bn), bn};
       if (kind == 1 || kind == 3) L.obeg = raster(its, (int)(nb / 128), (int)(nb / bn), false);
+      if (merged) {   // GMP_FLAG_TIMING: FP16 and BF16 MMAs run at the same rate -> share by pairs
+        L.present = (1u << 2) | (1u << 3);
+        const double tot = (double)(npair[2] + npair[3]);
+        L.share[2] = npair[2] / tot;
+        L.share[3] = npair[3] / tot;
+      }
       pl->launches.push_back(L);
     }
   }
@@ -1636,17 +1663,19 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
         const cudaError_t e = oz_launch(pl->oz, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, pl->off_oexp, stream);
         if (e != cudaSuccess) return fail(GMP_ERR_CUDA, std::string("k_tc_fp64 launch: ") + cudaGetErrorString(e));
       } else if (L.kind == 5) {
-        GMP_TRY(tc2_launch(pl->tc, L.cls, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, pl->d.beta,
-                           L.obeg >= 0 ? (const int32_t*)(ws + pl->off_order) + L.obeg : nullptr, stream));
+        GMP_LAUNCH(tc2_launch(pl->tc, L.cls, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, pl->d.beta,
+                           L.obeg >= 0 ? (const int32_t*)(ws + pl->off_order) + L.obeg : nullptr, stream),
+                   "k_tc2_class");
       } else if (L.kind == 6) {
-        GMP_TRY(tcmc_launch(pl->tc, L.cls, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, stream));
+        GMP_LAUNCH(tcmc_launch(pl->tc, L.cls, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, stream), "k_tcmc_class");
       } else if (L.kind == 7) {
-        GMP_TRY(tcf_launch(pl->tc, L.present, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, pl->d.beta, stream,
-                           split_t0(pl->d.flags)));
+        GMP_LAUNCH(tcf_launch(pl->tc, L.present, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, pl->d.beta, stream,
+                           split_t0(pl->d.flags)), "k_tc_fused");
       } else if (L.kind == 1 || L.kind == 3) {
-        GMP_TRY(tc_launch(pl->tc, L.kind == 3 ? (split_t0(pl->d.flags) ? TC_SPLIT6 : TC_SPLIT) : L.cls, L.bn, it,
+        GMP_LAUNCH(tc_launch(pl->tc, L.kind == 3 ? (split_t0(pl->d.flags) ? TC_SPLIT6 : TC_SPLIT) : L.cls, L.bn, it,
                           L.icount, pd, dct, ws, (int)nb, pl->d.alpha, pl->d.beta,
-                          L.obeg >= 0 ? (const int32_t*)(ws + pl->off_order) + L.obeg : nullptr, stream));
+                          L.obeg >= 0 ? (const int32_t*)(ws + pl->off_order) + L.obeg : nullptr, stream),
+                   "k_tc_class");
       } else {
         switch (L.cls) {
           case 0:
@@ -1807,7 +1836,7 @@ extern "C" gmp_status_t gemm_mp_get_stats(gmp_plan_t pl, gmp_stats_t* out) {
       GMP_CUDA(cudaEventSynchronize(pl->launch_ev[2 * li + 1]));
       GMP_CUDA(cudaEventElapsedTime(&ms, pl->launch_ev[2 * li], pl->launch_ev[2 * li + 1]));
       const Launch& L = pl->launches[li];
-      if (L.kind == 7) {
+      if (L.kind == 7 || L.present) {   // fused / merged launches: split by the classes' shares
         for (int c = 0; c < NC; ++c) pl->st.class_ms[c] += ms * L.share[c];
       } else {
         pl->st.class_ms[L.cls] += ms;

@@ -308,6 +308,7 @@ template <int C> constexpr int tc_map_index() { return tc_is_split<C>() ? GMP_AR
 template <int C, int BN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+           const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
            const WorkItem* __restrict__ items, int64_t nitems, const PairDesc* __restrict__ pairs,
            const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha, double beta,
            const int32_t* __restrict__ order) {
@@ -338,6 +339,10 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    if (C == 3) {   // merged 16-bit launch: FP16 pairs read the FP16 arena (tmA2 / tmB2)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA2) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB2) : "memory");
+    }
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -371,10 +376,15 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
               bulk_load(sa + A_BYTES + B_BYTES, ws + pd.a_off + sfa, SF_BYTES, &full[stage]);
               bulk_load(sa + A_BYTES + B_BYTES + SF_BYTES, ws + pd.b_off + sfb, SF_BYTES, &full[stage]);
             } else {
+              // C = 3 launches may carry FP16 pairs too (BF16 pairs first, then FP16, per item:
+              // the fold order of DESIGN.md O9); same element size, the FP16 arena's maps
+              const bool f16 = (C == 3) && pd.cls == 2;
+              const CUtensorMap* ma = f16 ? &tmA2 : &tmA;
+              const CUtensorMap* mb = f16 ? &tmB2 : &tmB;
 #pragma unroll
               for (int p = 0; p < NP; ++p) {
-                tma_load_2d(sa + p * A_BYTES, &tmA, kb * BK, (pd.a_slot * NP + p) * nb + w.m0, &full[stage]);
-                tma_load_2d(sa + NP * A_BYTES + p * B_BYTES, &tmB, kb * BK, (pd.b_slot * NP + p) * nb + w.n0,
+                tma_load_2d(sa + p * A_BYTES, ma, kb * BK, (pd.a_slot * NP + p) * nb + w.m0, &full[stage]);
+                tma_load_2d(sa + NP * A_BYTES + p * B_BYTES, mb, kb * BK, (pd.b_slot * NP + p) * nb + w.n0,
                             &full[stage]);
               }
             }
@@ -390,6 +400,7 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
       for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
         const WorkItem w = expand_item(items, it, nb, BN, order);
         for (int pi = 0; pi < w.pcnt; ++pi) {
+          const uint32_t idesc = (C == 3 && pairs[w.pbeg + pi].cls == 2) ? tc_idesc<2, BN>() : IDESC;
           mbar_wait(&tempty[acc], acc_phase ^ 1);
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
@@ -424,7 +435,7 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
               const uint64_t bd = sdesc_k_sw128(sa + NP * A_BYTES + tj * B_BYTES);
 #pragma unroll
               for (int k = 0; k < NMMA; ++k)
-                tc_mma<C>(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), IDESC, (kb | (t - t0) | k) != 0);
+                tc_mma<C>(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, (kb | (t - t0) | k) != 0);
             }
             }
             tc_commit(&empty[stage]);
@@ -543,8 +554,11 @@ inline gmp_status_t tc_launch_t(TcTables& t, const WorkItem* it, int64_t n, cons
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)std::min<int64_t>(n, sms);
-  constexpr int mi = tc_map_index<C>();
-  k_tc_class<C, BN><<<grid, TC_THREADS, smem, s>>>(t.mapA[mi], BN == 128 ? t.mapB128[mi] : t.mapB[mi], it, n, pd, ct,
+  // a merged 16-bit launch (C = 3) may hold FP16 pairs only: then the BF16 arena is empty
+  const int mi = (C == 3 && !t.ready[3]) ? 2 : tc_map_index<C>();
+  const int m2 = (C == 3 && t.ready[2]) ? 2 : mi;   // FP16 arena for merged 16-bit launches
+  k_tc_class<C, BN><<<grid, TC_THREADS, smem, s>>>(t.mapA[mi], BN == 128 ? t.mapB128[mi] : t.mapB[mi], t.mapA[m2],
+                                                    BN == 128 ? t.mapB128[m2] : t.mapB[m2], it, n, pd, ct,
                                                     ws, nb, alpha, beta, order);
   return cudaGetLastError() == cudaSuccess ? GMP_OK : GMP_ERR_CUDA;
 }
@@ -555,7 +569,8 @@ inline gmp_status_t tc_launch(TcTables& t, int cls, int bn, const WorkItem* it, 
                               const CTileDesc* ct, uint8_t* ws, int nb, double alpha, double beta, const int32_t* order,
                               cudaStream_t s) {
   const int mi = (cls == TC_SPLIT || cls == TC_SPLIT6) ? GMP_AR_SPLIT : cls;
-  if (!((cls >= 2 && cls <= GMP_MX) || cls == TC_SPLIT || cls == TC_SPLIT6) || !t.ready[mi]) return GMP_ERR_STATE;
+  const bool ok = t.ready[mi] || (cls == 3 && t.ready[2]);   // merged 16-bit launch with FP16 pairs only
+  if (!((cls >= 2 && cls <= GMP_MX) || cls == TC_SPLIT || cls == TC_SPLIT6) || !ok) return GMP_ERR_STATE;
   if (cls == GMP_MX && bn != 128) return GMP_ERR_STATE;
   const bool wide = bn == 256;
   switch (cls) {

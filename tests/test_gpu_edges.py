@@ -103,6 +103,24 @@ def test_explicit_all_mxfp4_operands(flags):
         assert ok, rel
 
 
+@pytest.mark.parametrize("nb,beta,seed", [(256, 0.0, 42), (128, 0.5, 44), (512, 1.0, 44)])
+def test_merged_16bit_launch_bitwise_vs_per_class(nb, beta, seed):
+    """the default plan runs the FP16 pairs of a step on the BF16 launch (per item BF16 then FP16,
+    the O9 fold order); GMP_FLAG_SPLIT16 runs one launch per class: same pairs, same arithmetic,
+    same order -> C bit-identical, fewer launches, and C within the parity bound of the oracle"""
+    w = gmp_inputs.small_workload(3 * nb, 2 * nb, 4 * nb, nb, 1e-4, mode="random", E=28, beta=beta, seed=seed)
+    A, Bm, C = w.matrices()
+    g, (out,) = run_gpu(A, Bm, C, nb, w.tol, w.alpha, w.beta, w.class_mask)
+    g2, (out2,) = run_gpu(A, Bm, C, nb, w.tol, w.alpha, w.beta, w.class_mask, flags=B.GMP_FLAG_SPLIT16)
+    st, st2 = g.stats(), g2.stats()
+    assert st["pairs"][2] > 0 and st["pairs"][3] > 0
+    assert st["launches_execute"] < st2["launches_execute"]
+    assert np.array_equal(out, out2)
+    o = run_oracle(A, Bm, C, nb, w.tol, w.alpha, w.beta, w.class_mask)
+    ok, rel = c_parity(out, o["C"], o["ccode"], o["cscale"], nb, w.K, False)
+    assert ok, rel
+
+
 def test_fp32_split_parts_are_exact():
     """The tensor-pipe FP32 class consumes x = x0 + x1 + x2 (three BF16 parts,
     K-major): the parts must reproduce every FP32 operand value exactly."""
