@@ -198,7 +198,8 @@ gmp_status_t gemm_mp_convert(gmp_plan_t plan, void *ws, size_t ws_bytes, void *s
  * called repeatedly after one convert (a repeated execute reuses the received
  * panels: no SUMMA traffic).  The C tile descriptors are uploaded only when ldc
  * or the workspace changed, so on one GPU a repeated execute with the same
- * arguments issues kernels only and may be captured into a CUDA graph.         */
+ * arguments issues kernels only and may be captured into a CUDA graph.
+ * C: 16-byte aligned, ldc even (GMP_ERR_ARG otherwise; C-finalize writes 16-byte vectors). */
 gmp_status_t gemm_mp_execute(gmp_plan_t plan, double *C, int64_t ldc, void *stream);
 
 /* Waits for the plan's streams; returns the first asynchronous error.          */

@@ -1604,6 +1604,8 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
   const int64_t nCl = (int64_t)pl->locC.size();
   const int64_t ntl = count_owned(pl->lay.colQ, pl->q);
   if (nCl > 0 && (!Cuser || ldc < ntl * nb)) return fail(GMP_ERR_ARG, "C NULL or ldc too small");
+  if (nCl > 0 && (((uintptr_t)Cuser & 15) || (ldc & 1)))
+    return fail(GMP_ERR_ARG, "C must be 16-byte aligned with an even leading dimension");
   cudaStream_t stream = (cudaStream_t)stream_;
   uint8_t* ws = pl->ws;
   // C tile descriptors (user offsets depend on ldc).  Uploaded only when ldc or the

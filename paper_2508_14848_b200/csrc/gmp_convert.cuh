@@ -445,6 +445,58 @@ __global__ void __launch_bounds__(256) k_c_maxabs(const CTileDesc* __restrict__ 
 // stores).  FP64 C tiles: the packed C_out IS the binary64 W (plan aliases
 // cout_off = w_off), so only the user's C is written.
 constexpr int FIN_ROWS = 4;
+// 4 consecutive W values of a binary32-W tile -> packed class-C payload (one RN each) and
+// the decoded binary64 user values; rounded values stay in registers (no payload read-back)
+template <int C>
+__device__ __forceinline__ void fin4(const float4 w, int e, uint8_t* pay, int64_t i, double* u) {
+  const double y[4] = {ldexp_fast((double)w.x, e), ldexp_fast((double)w.y, e), ldexp_fast((double)w.z, e),
+                       ldexp_fast((double)w.w, e)};
+  double r[4];
+  if constexpr (C == 1) {
+    uint32_t b[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) { b[v] = cvt_f32_rn(y[v]); r[v] = (double)__uint_as_float(b[v]); }
+    *reinterpret_cast<uint4*>(pay + i * 4) = make_uint4(b[0], b[1], b[2], b[3]);
+  } else if constexpr (C == 2 || C == 3) {
+    uint16_t h[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      h[v] = (C == 2) ? cvt_f16_rn(y[v]) : cvt_bf16_rn(y[v]);
+      r[v] = (double)((C == 2) ? f16_to_f32(h[v]) : bf16_to_f32(h[v]));
+    }
+    *reinterpret_cast<uint2*>(pay + i * 2) =
+        make_uint2((uint32_t)h[0] | ((uint32_t)h[1] << 16), (uint32_t)h[2] | ((uint32_t)h[3] << 16));
+  } else {
+    const uint32_t lo = (C == 4) ? cvt_e4m3x2_rn(y[0], y[1]) : cvt_e5m2x2_rn(y[0], y[1]);
+    const uint32_t hi = (C == 4) ? cvt_e4m3x2_rn(y[2], y[3]) : cvt_e5m2x2_rn(y[2], y[3]);
+    const uint32_t b = lo | (hi << 16);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const uint8_t q = (uint8_t)(b >> (8 * v));
+      r[v] = (double)((C == 4) ? e4m3_to_f32(q) : e5m2_to_f32(q));
+    }
+    *reinterpret_cast<uint32_t*>(pay + i) = b;
+  }
+#pragma unroll
+  for (int v = 0; v < 4; ++v) u[v] = ldexp_fast(r[v], -e);
+}
+
+template <int C>
+__device__ __forceinline__ void fin_rows(const CTileDesc& c, uint8_t* ws, int e, double* cuser, int64_t ldc, int nb) {
+  uint8_t* pay = ws + c.cout_off;
+  for (int rr = 0; rr < FIN_ROWS; ++rr) {
+    const int64_t r = (int64_t)blockIdx.x * FIN_ROWS + rr;
+    double* urow = cuser + c.user_off + r * ldc;
+    const float4* wrow = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(ws + c.w_off) + r * nb);
+    for (int q = threadIdx.x; q < nb / 4; q += blockDim.x) {
+      double u[4];
+      fin4<C>(wrow[q], e, pay, r * nb + 4 * q, u);
+      reinterpret_cast<double2*>(urow + 4 * q)[0] = make_double2(u[0], u[1]);
+      reinterpret_cast<double2*>(urow + 4 * q)[1] = make_double2(u[2], u[3]);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_c_finalize(const CTileDesc* __restrict__ ct, uint8_t* ws,
                                                     const unsigned long long* maxbits, int16_t* cscale,
                                                     double* cuser, int64_t ldc, int nb) {
@@ -452,21 +504,20 @@ __global__ void __launch_bounds__(256) k_c_finalize(const CTileDesc* __restrict_
   const double m = __longlong_as_double((long long)maxbits[blockIdx.y]);
   const int e = scale_exp(m, c.code);
   if (blockIdx.x == 0 && threadIdx.x == 0) cscale[blockIdx.y] = (int16_t)e;
-  uint8_t* pay = ws + c.cout_off;
-  for (int rr = 0; rr < FIN_ROWS; ++rr) {
-    const int64_t r = (int64_t)blockIdx.x * FIN_ROWS + rr;
-    double* urow = cuser + c.user_off + r * ldc;
-    if (c.code == 0) {
-      const double* wrow = reinterpret_cast<const double*>(ws + c.w_off) + r * nb;
-      for (int col = threadIdx.x; col < nb; col += blockDim.x) urow[col] = wrow[col];
-    } else {
-      const float* wrow = reinterpret_cast<const float*>(ws + c.w_off) + r * nb;
-      for (int col = threadIdx.x; col < nb; col += blockDim.x) {
-        const int64_t i = r * nb + col;
-        payload_store(pay, i, c.code, ldexp_fast((double)wrow[col], e));
-        urow[col] = ldexp_fast(payload_f64(pay, i, c.code), -e);
+  switch (c.code) {
+    case 0:
+      for (int rr = 0; rr < FIN_ROWS; ++rr) {
+        const int64_t r = (int64_t)blockIdx.x * FIN_ROWS + rr;
+        double* urow = cuser + c.user_off + r * ldc;
+        const double2* wrow = reinterpret_cast<const double2*>(reinterpret_cast<const double*>(ws + c.w_off) + r * nb);
+        for (int q = threadIdx.x; q < nb / 2; q += blockDim.x) reinterpret_cast<double2*>(urow)[q] = wrow[q];
       }
-    }
+      break;
+    case 1: fin_rows<1>(c, ws, e, cuser, ldc, nb); break;
+    case 2: fin_rows<2>(c, ws, e, cuser, ldc, nb); break;
+    case 3: fin_rows<3>(c, ws, e, cuser, ldc, nb); break;
+    case 4: fin_rows<4>(c, ws, e, cuser, ldc, nb); break;
+    default: fin_rows<5>(c, ws, e, cuser, ldc, nb); break;
   }
 }
 

@@ -77,25 +77,39 @@ def traffic(rep, out, workload, n_gpus):
 
 
 def launches(path, out):
+    """per kernel: launches, total device ms (gpu__time_duration.sum) and share; DRAM bytes
+    per launch when the list also holds dram__bytes_read/write.sum"""
     rows = [r for r in csv.reader(open(path)) if len(r) > 5]
     hdr = rows[0]
-    ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
-    agg, order = {}, []
+    ki, mi, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    idi = hdr.index("ID")
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+             "ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "nsecond": 1e-6, "ms": 1.0, "msecond": 1.0}
+    agg, order, seen = {}, [], set()
     for r in rows[1:]:
         name = re.sub(r"\(.*", "", r[ki])
-        v = float(r[vi].replace(",", ""))
+        v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
         if name not in agg:
-            agg[name] = [0, 0.0]
+            agg[name] = {"n": 0, "ms": 0.0, "dram": 0.0}
             order.append(name)
-        agg[name][0] += 1
-        agg[name][1] += v
-    tot = sum(v[1] for v in agg.values())
-    lines = [f"# ncu launch list (gpu__time_duration.sum, --clock-control none): {path}", "",
-             "| kernel | launches | total ms | share |", "|---|---|---|---|"]
+        a = agg[name]
+        if r[mi] == "gpu__time_duration.sum":
+            a["ms"] += v if r[ui] in scale else v / 1e6
+            if r[idi] not in seen:
+                seen.add(r[idi])
+                a["n"] += 1
+        elif r[mi].startswith("dram__bytes"):
+            a["dram"] += v
+    tot = sum(a["ms"] for a in agg.values())
+    lines = [f"# ncu launch list (--clock-control none): {path}", "",
+             "| kernel | launches | total ms | share | DRAM GB per launch | GB/s |", "|---|---|---|---|---|---|"]
     for n in order:
-        c, t = agg[n]
-        lines.append(f"| {n} | {c} | {t / 1e6:.3f} | {t / tot:.1%} |")
-    lines.append(f"| total | {sum(v[0] for v in agg.values())} | {tot / 1e6:.3f} | |")
+        a = agg[n]
+        gb = a["dram"] / a["n"] / 1e9 if a["n"] and a["dram"] else None
+        bw = a["dram"] / (a["ms"] * 1e-3) / 1e9 if a["ms"] and a["dram"] else None
+        lines.append(f"| {n} | {a['n']} | {a['ms']:.3f} | {a['ms'] / tot:.1%} | "
+                     f"{'' if gb is None else f'{gb:.2f}'} | {'' if bw is None else f'{bw:.0f}'} |")
+    lines.append(f"| total | {sum(a['n'] for a in agg.values())} | {tot:.3f} | | | |")
     open(out, "w").write("\n".join(lines) + "\n")
 
 
