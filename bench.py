@@ -758,6 +758,7 @@ def main():
                        "ownership": "balanced (gemm_mp_balance, NEXT-3)" if ro is not None else "2D block-cyclic"},
             "balance": balance,
             "nvlink_recv_bytes_rank0": st["recv_bytes_local"],
+            "steps_ms": [[round(x, 2) for x in ph] for ph in phase],   # plan, convert, execute per step
             "phases_ms": {"plan": statistics.median(ph[0] for ph in phase),
                           "convert": statistics.median(ph[1] for ph in phase), "execute": exec_ms},
             "execute_tflops": w.flops / (exec_ms * 1e-3) / 1e12,

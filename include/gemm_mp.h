@@ -81,6 +81,10 @@ typedef enum {
 #define GMP_FLAG_SPLIT16 2048u /* one launch per 16-bit class; default: the FP16 pairs of a SUMMA step ride
                                  on the BF16 launch (k_tc_class<3>, per item BF16 then FP16 pairs in the
                                  fold order, one W read/write for both; C bit-identical)             */
+#define GMP_FLAG_NCCL_BCAST 4096u /* SUMMA panels through ncclBroadcast on the row / column communicators
+                                 (the round-1 transport) instead of the default copy-engine pulls:
+                                 each receiver copies the tiles it needs straight from the root's
+                                 payload slot over NVLink (workspaces mapped with CUDA IPC, no SMs) */
 #define GMP_FLAG_TC_PAIR 32u /* opt-in: FP16/BF16/E4M3/E5M2 launches whose C tiles fold into binary32 W
                                  and whose nb is a multiple of 256 run on SM pairs (tcgen05 cta_group::2,
                                  256 x 256 sub-tiles, half the B bytes per SM), rastered by C tile row

@@ -221,6 +221,10 @@ struct Bcast {           // one SUMMA broadcast of a panel tile payload in a ste
   int64_t bytes;
 };
 
+struct CeState;   // copy-engine pull transport state (below)
+struct gmp_plan_s;
+static gmp_status_t ce_exchange_tables(gmp_plan_s* pl, cudaStream_t stream);
+
 struct gmp_plan_s {
   gmp_desc_t d{};
   int64_t mt = 0, nt = 0, kt = 0, nA = 0, nB = 0, nC = 0;
@@ -296,6 +300,9 @@ struct gmp_plan_s {
   cudaEvent_t done_ev = nullptr;   // recorded at the end of convert / execute (watchdog polls it)
   bool done_rec = false;
   struct Loopback* lb = nullptr;   // GMP_FLAG_LOOPBACK: in-process transport (tests only)
+  CeState* ce = nullptr;           // copy-engine pull transport (default for NCCL grids)
+  std::vector<std::vector<int32_t>> peer_slotA5, peer_slotB5;   // [world rank] its slot tables
+  std::vector<std::vector<int64_t>> peer_arena_off;             // [world rank] its arena offsets
   gmp_stats_t st{};
 };
 
@@ -416,11 +423,29 @@ static gmp_status_t lb_allreduce(Loopback* lb, int rank, double* S, int64_t nS, 
 // Row / column communicators are split once per (world communicator, grid) and
 // reused by every plan on it (ncclCommSplit is a collective costing milliseconds);
 // they are released by gemm_mp_nccl_comm_destroy of the world communicator.
+// Copy-engine pull transport (default SUMMA transport over NCCL communicators):
+// every rank maps the other ranks' workspaces (CUDA IPC), and a receiver copies each panel
+// tile it needs straight from the root's payload slot with cudaMemcpyAsync on its comm
+// stream -- NVLink copy engines, no SMs, so the transfers overlap the persistent tensor
+// kernels, which leave no room for NCCL's broadcast CTAs.  NCCL carries only the
+// statistics all-reduce, the one-time table / handle exchanges and two 4-byte barriers per
+// convert (previous pulls done; every rank packed).
+struct CeState {
+  std::vector<uint8_t*> peer_ws;                         // [world rank] mapped workspace (own: own ws)
+  const uint8_t* ws_for = nullptr;                       // local workspace the mapping was built for
+  std::vector<std::pair<std::string, void*>> opened;     // IPC handle bytes -> mapped base (cache)
+  cudaEvent_t comm_done = nullptr;                       // end of the last execute's pulls
+  bool comm_done_rec = false;
+  int* dummy = nullptr;                                  // 1 int, barrier all-reduces
+  uint8_t* xbuf = nullptr;                               // device buffer of the host all-gathers (kept:
+  size_t xcap = 0;                                       // stream-ordered allocations stalled plans)
+};
 struct GridComms {
   ncclComm_t world;
   int P, Q;
   ncclComm_t rowc, colc;
   cudaStream_t comm_stream;
+  CeState* ce;
 };
 static std::vector<GridComms> g_grid_comms;
 static std::mutex g_grid_mu;   // plans may be built from several host threads
@@ -429,13 +454,16 @@ static gmp_status_t grid_comms(ncclComm_t world, int P, int Q, int p, int q, Gri
   std::lock_guard<std::mutex> lk(g_grid_mu);
   for (auto& g : g_grid_comms)
     if (g.world == world && g.P == P && g.Q == Q) { *out = g; return GMP_OK; }
-  GridComms g{world, P, Q, nullptr, nullptr, nullptr};
+  GridComms g{world, P, Q, nullptr, nullptr, nullptr, new CeState()};
   ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
   if (const char* e = getenv("GMP_NCCL_MAX_CTAS")) cfg.maxCTAs = atoi(e);
   if (const char* e = getenv("GMP_NCCL_CTA_POLICY")) cfg.CTAPolicy = atoi(e);
   GMP_NCCL(ncclCommSplit(world, p, q, &g.rowc, &cfg));
   GMP_NCCL(ncclCommSplit(world, q, p, &g.colc, &cfg));
   GMP_CUDA(cudaStreamCreateWithFlags(&g.comm_stream, cudaStreamNonBlocking));
+  GMP_CUDA(cudaEventCreateWithFlags(&g.ce->comm_done, cudaEventDisableTiming));
+  GMP_CUDA(cudaMalloc(&g.ce->dummy, 16));
+  GMP_CUDA(cudaMemset(g.ce->dummy, 0, 16));
   g_grid_comms.push_back(g);
   *out = g;
   return GMP_OK;
@@ -1289,8 +1317,10 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
     pl->rowc = gc.rowc;
     pl->colc = gc.colc;
     pl->comm_stream = gc.comm_stream;
+    if (!(d.flags & GMP_FLAG_NCCL_BCAST)) pl->ce = gc.ce;
   }
   build_tables(pl);
+  if (pl->ce) GMP_TRY(ce_exchange_tables(pl, stream));
   pl->step_ev.resize(pl->st.steps);
   for (auto& e : pl->step_ev) GMP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   GMP_CUDA(cudaEventCreateWithFlags(&pl->done_ev, cudaEventDisableTiming));
@@ -1407,10 +1437,134 @@ static int grid_for(int64_t n_elems, int per_thread) {
 // SUMMA step s on the comm stream: grouped broadcasts of the step's panel tiles,
 // then the receiver-side shadows / splits / digit slices of the received tiles;
 // step_ev[s] gates the step's class launches on the compute stream.
+// ---- copy-engine pull transport helpers ----
+// all-gather `bytes` host bytes from every rank of `comm` (NCCL on `stream`, then a sync)
+static gmp_status_t allgather_host(CeState* ce, ncclComm_t comm, const void* mine, size_t bytes, int G,
+                                   std::vector<uint8_t>& all, cudaStream_t stream) {
+  const size_t b16 = (size_t)align_up((int64_t)bytes, 16);
+  if (ce->xcap < b16 * (G + 1)) {
+    GMP_CUDA(cudaStreamSynchronize(stream));
+    if (ce->xbuf) GMP_CUDA(cudaFree(ce->xbuf));
+    ce->xbuf = nullptr;
+    ce->xcap = 0;
+    GMP_CUDA(cudaMalloc(&ce->xbuf, b16 * (G + 1)));
+    ce->xcap = b16 * (G + 1);
+  }
+  uint8_t* d = ce->xbuf;
+  Upload up;
+  up.add(d, mine, (int64_t)bytes);
+  gmp_status_t st = up.run(stream);
+  ncclResult_t r = ncclSuccess;
+  if (st == GMP_OK) r = ncclAllGather(d, d + b16, b16, ncclUint8, comm, stream);
+  Stage* sg = (st == GMP_OK && r == ncclSuccess) ? stage_acquire(b16 * G) : nullptr;
+  if (sg) k_xfer<<<xfer_grid((int64_t)(b16 * G)), 256, 0, stream>>>(d + b16, sg->d, (int64_t)(b16 * G));
+  const cudaError_t e = cudaStreamSynchronize(stream);
+  if (sg && e == cudaSuccess) {
+    all.resize(b16 * G);
+    std::memcpy(all.data(), sg->h, b16 * G);
+  }
+  if (sg) stage_release(sg, stream);
+  if (st != GMP_OK) return st;
+  if (r != ncclSuccess) return fail(GMP_ERR_NCCL, std::string("table all-gather: ") + ncclGetErrorString(r));
+  if (!sg) return fail(GMP_ERR_CUDA, "pinned staging buffer allocation failed");
+  GMP_CUDA(e);
+  return GMP_OK;
+}
+
+// every rank's slot tables and arena offsets (plan time: the receivers address the roots'
+// payload slots directly)
+static gmp_status_t ce_exchange_tables(gmp_plan_s* pl, cudaStream_t stream) {
+  const int G = pl->P * pl->Q;
+  const size_t nA5 = (size_t)pl->nA * NC, nB5 = (size_t)pl->nB * NC;
+  const size_t bytes = 8 * GMP_NARENA + 4 * (nA5 + nB5);
+  std::vector<uint8_t> mine(bytes);
+  std::memcpy(mine.data(), pl->arena_off, 8 * GMP_NARENA);
+  std::memcpy(mine.data() + 8 * GMP_NARENA, pl->slotA5.data(), 4 * nA5);
+  std::memcpy(mine.data() + 8 * GMP_NARENA + 4 * nA5, pl->slotB5.data(), 4 * nB5);
+  std::vector<uint8_t> all;
+  GMP_TRY(allgather_host(pl->ce, pl->world, mine.data(), bytes, G, all, stream));
+  const size_t b16 = (size_t)align_up((int64_t)bytes, 16);
+  pl->peer_arena_off.assign(G, {});
+  pl->peer_slotA5.assign(G, {});
+  pl->peer_slotB5.assign(G, {});
+  for (int r = 0; r < G; ++r) {
+    const uint8_t* b = all.data() + r * b16;
+    pl->peer_arena_off[r].assign(GMP_NARENA, 0);
+    std::memcpy(pl->peer_arena_off[r].data(), b, 8 * GMP_NARENA);
+    pl->peer_slotA5[r].resize(nA5);
+    std::memcpy(pl->peer_slotA5[r].data(), b + 8 * GMP_NARENA, 4 * nA5);
+    pl->peer_slotB5[r].resize(nB5);
+    std::memcpy(pl->peer_slotB5[r].data(), b + 8 * GMP_NARENA + 4 * nA5, 4 * nB5);
+  }
+  return GMP_OK;
+}
+
+typedef CUresult (*PFN_memGetAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+// map every peer's workspace into this process (CUDA IPC) when the local workspace changed
+static gmp_status_t ce_map_peers(gmp_plan_s* pl, uint8_t* ws, cudaStream_t stream) {
+  CeState* ce = pl->ce;
+  if (ce->ws_for == ws && (int)ce->peer_ws.size() == pl->P * pl->Q) return GMP_OK;
+  static PFN_memGetAddressRange range = nullptr;
+  if (!range) {
+    void* fp = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fp, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return fail(GMP_ERR_CUDA, "cuMemGetAddressRange not available");
+    range = reinterpret_cast<PFN_memGetAddressRange>(fp);
+  }
+  CUdeviceptr base = 0;
+  size_t sz = 0;
+  if (range(&base, &sz, (CUdeviceptr)(uintptr_t)ws) != CUDA_SUCCESS) return fail(GMP_ERR_CUDA, "cuMemGetAddressRange");
+  struct Rec { cudaIpcMemHandle_t h; int64_t off; int64_t pad; } rec{};
+  GMP_CUDA(cudaIpcGetMemHandle(&rec.h, (void*)(uintptr_t)base));
+  rec.off = (int64_t)((uintptr_t)ws - (uintptr_t)base);
+  const int G = pl->P * pl->Q;
+  std::vector<uint8_t> all;
+  GMP_TRY(allgather_host(pl->ce, pl->world, &rec, sizeof rec, G, all, stream));
+  const size_t b16 = (size_t)align_up((int64_t)sizeof(Rec), 16);
+  ce->peer_ws.assign(G, nullptr);
+  for (int r = 0; r < G; ++r) {
+    Rec pr;
+    std::memcpy(&pr, all.data() + r * b16, sizeof pr);
+    if (r == pl->d.rank) { ce->peer_ws[r] = ws; continue; }
+    const std::string key(reinterpret_cast<const char*>(&pr.h), sizeof pr.h);
+    void* mapped = nullptr;
+    for (auto& o : ce->opened)
+      if (o.first == key) mapped = o.second;
+    if (!mapped) {
+      GMP_CUDA(cudaIpcOpenMemHandle(&mapped, pr.h, cudaIpcMemLazyEnablePeerAccess));
+      ce->opened.emplace_back(key, mapped);
+    }
+    ce->peer_ws[r] = (uint8_t*)mapped + pr.off;
+  }
+  ce->ws_for = ws;
+  return GMP_OK;
+}
+
+// 4-byte all-reduce on `stream`: a device-ordered barrier of the world communicator
+static gmp_status_t ce_barrier(gmp_plan_s* pl, cudaStream_t stream) {
+  const ncclResult_t r = ncclAllReduce(pl->ce->dummy, pl->ce->dummy, 1, ncclInt32, ncclSum, pl->world, stream);
+  if (r != ncclSuccess) return fail(GMP_ERR_NCCL, std::string("barrier all-reduce: ") + ncclGetErrorString(r));
+  return GMP_OK;
+}
+
 static gmp_status_t issue_comm_step(gmp_plan_s* pl, uint8_t* ws, int s) {
   const int64_t nb = pl->d.nb;
   NvtxRange nv("SUMMA broadcast", s, -1);
-  if (pl->lb) {
+  if (pl->ce) {
+    // copy-engine pull: each receiver copies the root's payload slot over NVLink (the root
+    // sends nothing; every root packed before the convert barrier that precedes step 0)
+    for (const Bcast& b : pl->bcast_step[s]) {
+      const int root = b.which == 0 ? pl->p * pl->Q + b.root : b.root * pl->Q + pl->q;
+      if (root == pl->d.rank) continue;
+      const int32_t slot = (b.which == 0 ? pl->peer_slotA5 : pl->peer_slotB5)[root][b.tile * NC + b.cls];
+      if (slot < 0) return fail(GMP_ERR_STATE, "root holds no slot for a broadcast tile");
+      const uint8_t* src = pl->ce->peer_ws[root] + pl->peer_arena_off[root][b.cls] + (int64_t)slot * pl->slot_bytes[b.cls];
+      GMP_CUDA(cudaMemcpyAsync(ws + b.off, src, (size_t)b.bytes, cudaMemcpyDeviceToDevice, pl->comm_stream));
+    }
+  } else if (pl->lb) {
     // loopback: each receiver copies the root's payload slot (the root sends nothing)
     int last_root = -1;
     for (const Bcast& b : pl->bcast_step[s]) {
@@ -1557,6 +1711,13 @@ extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_byte
   if (oz_prepare(pl->oz, ws, pl->arena_off[GMP_AR_SLICE], pl->arena_slots[GMP_AR_SLICE], (int)nb) != GMP_OK)
     return fail(GMP_ERR_CUDA, "cuTensorMapEncodeTiled (digit arena) failed");
   GMP_TRY(tc_prepare(pl->tc, ws, pl->arena_off, pl->arena_slots, (int)nb));
+  if (pl->ce) {
+    GMP_TRY(ce_map_peers(pl, ws, stream));
+    // the previous executes' pulls from this workspace have completed on every rank
+    // before the packs below overwrite the payload slots
+    if (pl->ce->comm_done_rec) GMP_CUDA(cudaStreamWaitEvent(stream, pl->ce->comm_done, 0));
+    GMP_TRY(ce_barrier(pl, stream));
+  }
   // S3 pack
   if (!pl->pack.empty()) {
     dim3 grid((unsigned)((nb / 64) * (nb / 64)), (unsigned)pl->pack.size());
@@ -1573,6 +1734,7 @@ extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_byte
   pl->panels_valid = false;
   if (pl->P * pl->Q > 1 && pl->st.steps > 0) {
     if (!pl->packed_ev) GMP_CUDA(cudaEventCreateWithFlags(&pl->packed_ev, cudaEventDisableTiming));
+    if (pl->ce) GMP_TRY(ce_barrier(pl, stream));   // every rank's stored payloads are packed
     GMP_CUDA(cudaEventRecord(pl->packed_ev, stream));
     if (pl->lb) pl->lb->barrier();   // every root's packed event is recorded before any receiver waits
     GMP_CUDA(cudaStreamWaitEvent(pl->comm_stream, pl->packed_ev, 0));
@@ -1646,6 +1808,10 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
       GMP_CUDA(cudaStreamWaitEvent(pl->comm_stream, ready, 0));
     }
     for (int s = s0; s < steps; ++s) GMP_TRY(issue_comm_step(pl, ws, s));
+    if (pl->ce) {   // the next convert on any rank waits for these pulls (ce_barrier)
+      GMP_CUDA(cudaEventRecord(pl->ce->comm_done, pl->comm_stream));
+      pl->ce->comm_done_rec = true;
+    }
     // A and B payloads are fixed after convert and every remote tile owns its
     // receive slot, so a repeated execute reuses the received panels (no SUMMA
     // traffic); the step events below are the ones of this issuance
@@ -1872,8 +2038,16 @@ extern "C" gmp_status_t gemm_mp_nccl_comm_destroy(void* comm) {
   for (size_t k = 0; k < g_grid_comms.size();) {
     GridComms& g = g_grid_comms[k];
     if (g.world == (ncclComm_t)comm) {
+      cudaStreamSynchronize(g.comm_stream);
       ncclCommDestroy(g.rowc);
       ncclCommDestroy(g.colc);
+      if (g.ce) {
+        for (auto& o : g.ce->opened) cudaIpcCloseMemHandle(o.second);
+        if (g.ce->comm_done) cudaEventDestroy(g.ce->comm_done);
+        if (g.ce->dummy) cudaFree(g.ce->dummy);
+        if (g.ce->xbuf) cudaFree(g.ce->xbuf);
+        delete g.ce;
+      }
       cudaStreamDestroy(g.comm_stream);
       g_grid_comms.erase(g_grid_comms.begin() + k);
     } else {

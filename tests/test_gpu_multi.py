@@ -26,19 +26,23 @@ def _port():
 
 
 # grids 1x4 / 4x1: a 4-member row (column) communicator, as in the 2x4 grid of 8 GPUs
-@pytest.mark.parametrize("G,sender,cfg,grid,balance", [
-    (2, False, "small", None, False), (2, True, "small", None, False),
-    (4, False, "small", None, False), (4, True, "small", None, False),
-    (2, False, "uneven", None, False), (4, True, "uneven", None, False),
-    (4, False, "small", "1x4", False), (4, True, "uneven", "4x1", False),
-    (2, False, "small", None, True), (4, True, "small", None, True), (4, False, "uneven", None, True)])
-def test_summa_bitwise_vs_single_gpu(G, sender, cfg, grid, balance):
+@pytest.mark.parametrize("G,sender,cfg,grid,balance,nccl", [
+    (2, False, "small", None, False, False), (2, True, "small", None, False, False),
+    (4, False, "small", None, False, False), (4, True, "small", None, False, False),
+    (2, False, "uneven", None, False, False), (4, True, "uneven", None, False, False),
+    (4, False, "small", "1x4", False, False), (4, True, "uneven", "4x1", False, False),
+    (2, False, "small", None, True, False), (4, True, "small", None, True, False),
+    (4, False, "uneven", None, True, False),
+    # the NCCL-broadcast transport (GMP_FLAG_NCCL_BCAST)
+    (2, False, "small", None, False, True), (4, True, "uneven", None, False, True),
+    (4, False, "small", "1x4", True, True)])
+def test_summa_bitwise_vs_single_gpu(G, sender, cfg, grid, balance, nccl):
     if torch.cuda.device_count() < G:
         pytest.skip(f"needs {G} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={G}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
            os.path.join(ROOT, "tools", "multi_gpu_check.py"), "--cfg", cfg] + (["--sender"] if sender else []) + \
-        (["--grid", grid] if grid else []) + (["--balance"] if balance else [])
+        (["--grid", grid] if grid else []) + (["--balance"] if balance else []) + (["--nccl"] if nccl else [])
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]

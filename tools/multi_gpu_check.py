@@ -41,6 +41,7 @@ def main():
     ap.add_argument("--cfg", default="small")
     ap.add_argument("--sender", action="store_true", help="GMP_FLAG_SENDER_SIDE (hybrid conversion, NEXT-2)")
     ap.add_argument("--grid", default=None, help="PxQ process grid (default: api.default_grid)")
+    ap.add_argument("--nccl", action="store_true", help="GMP_FLAG_NCCL_BCAST: NCCL broadcasts instead of CE pulls")
     ap.add_argument("--balance", action="store_true",
                     help="NEXT-3: owners from gemm_mp_balance on the maps of a block-cyclic plan")
     a = ap.parse_args()
@@ -65,7 +66,7 @@ def main():
     dist.broadcast(t, 0)
     comm = B.gemm_mp_nccl_comm_create(bytes(t.cpu().numpy()), G, rank)
 
-    flags = B.GMP_FLAG_SENDER_SIDE if a.sender else 0
+    flags = (B.GMP_FLAG_SENDER_SIDE if a.sender else 0) | (B.GMP_FLAG_NCCL_BCAST if a.nccl else 0)
     ro = co = None
     imb = None
     if a.balance:   # a block-cyclic plan gives the global maps; every rank balances them the same way
@@ -132,6 +133,7 @@ def main():
         print(json.dumps({"ok": ok, "G": G, "grid": f"{P}x{Q}", "workload": w.name, "msgs": msgs,
                           "mode": "sender-side (hybrid)" if a.sender else "receiver-side",
                           "ownership": "balanced (gemm_mp_balance)" if a.balance else "block-cyclic",
+                          "transport": "ncclBroadcast" if a.nccl else "copy-engine pulls (CUDA IPC)",
                           "imbalance_model": imb,
                           "covered": bool(not np.isnan(Cg).any()),
                           "recv_bytes_rank0": st["recv_bytes_local"], "recv_bytes_all": sum(r[0] for r in recv_all),
