@@ -79,7 +79,7 @@ def test_fused_tensor_launch_plan():
     own; the per-class launch counts still name every class present"""
     import numpy as np
     nb, t = 128, 4
-    d0 = B.make_desc(t * nb, t * nb, t * nb, nb, 1e-6, 1.0, 0.0, 0b00111)
+    d0 = B.make_desc(t * nb, t * nb, t * nb, nb, 1e-6, 1.0, 0.0, 0b00111, B.GMP_FLAG_SPLIT16)   # one launch per class
     d1 = B.make_desc(t * nb, t * nb, t * nb, nb, 1e-6, 1.0, 0.0, 0b00111, B.GMP_FLAG_TC_FUSED)
     ac = np.array([[0, 1, 2, 1]] * t, np.uint8)     # per l: FP64, FP32, FP16, FP32 pairs
     bc = np.zeros((t, t), np.uint8)
