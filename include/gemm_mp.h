@@ -188,7 +188,10 @@ gmp_status_t gemm_mp_workspace_size(gmp_plan_t plan, size_t *bytes);
  * DESIGN.md O3/O6), then the receiver-side shadows needed by local tile-GEMMs
  * (and, under GMP_FLAG_SENDER_SIDE, the shadows this rank sends).  Host tables
  * reach the device through pinned staging read by a kernel, never through a
- * copy engine.  ws must be 1024-byte aligned.  Async on `stream`.  After
+ * copy engine.  ws must be 1024-byte aligned.  On a P*Q > 1 grid (default
+ * copy-engine transport) the workspaces are mapped into the peers with CUDA IPC
+ * when they change: every rank must switch to a new workspace at the same
+ * convert (one all-gather of the handles).  Async on `stream`.  After
  * completion A and B may be freed.  ws stays owned by the caller and must
  * outlive every execute of this plan.                                          */
 gmp_status_t gemm_mp_convert(gmp_plan_t plan, void *ws, size_t ws_bytes, void *stream);
