@@ -668,6 +668,9 @@ def main():
             fp64 = fp64_baseline(a, w, A, Bm, C, dev, stream, P, Q, p, q, comm, G, ro, co)
         except Exception as ex:
             fp64 = {"error": f"{type(ex).__name__}: {str(ex)[:200]}"}
+        if G > 1:   # every rank has destroyed its plans (unmapping the peers' workspaces) before
+            dist.barrier()   # anyone allocates the next leg's buffers
+        torch.cuda.empty_cache()
     # ---- NVLink: measured NCCL broadcast bandwidth (N > 1) ----
     link_gbs, link_src = 900.0, "datasheet NVLink 5 (900 GB/s per direction)"
     if G > 1:

@@ -437,6 +437,11 @@ struct CeState {
   cudaEvent_t comm_done = nullptr;                       // end of the last execute's pulls
   bool comm_done_rec = false;
   int* dummy = nullptr;                                  // 1 int, barrier all-reduces
+  int live_plans = 0;                                    // plans using this state; at 0 the IPC mappings
+                                                         // are closed (an imported allocation stays
+                                                         // resident on its owner until every importer
+                                                         // closes it)
+  cudaStream_t comm_stream = nullptr;
   uint8_t* xbuf = nullptr;                               // device buffer of the host all-gathers (kept:
   size_t xcap = 0;                                       // stream-ordered allocations stalled plans)
 };
@@ -462,6 +467,7 @@ static gmp_status_t grid_comms(ncclComm_t world, int P, int Q, int p, int q, Gri
   GMP_NCCL(ncclCommSplit(world, q, p, &g.colc, &cfg));
   GMP_CUDA(cudaStreamCreateWithFlags(&g.comm_stream, cudaStreamNonBlocking));
   GMP_CUDA(cudaEventCreateWithFlags(&g.ce->comm_done, cudaEventDisableTiming));
+  g.ce->comm_stream = g.comm_stream;
   GMP_CUDA(cudaMalloc(&g.ce->dummy, 16));
   GMP_CUDA(cudaMemset(g.ce->dummy, 0, 16));
   g_grid_comms.push_back(g);
@@ -1317,7 +1323,11 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
     pl->rowc = gc.rowc;
     pl->colc = gc.colc;
     pl->comm_stream = gc.comm_stream;
-    if (!(d.flags & GMP_FLAG_NCCL_BCAST)) pl->ce = gc.ce;
+    if (!(d.flags & GMP_FLAG_NCCL_BCAST)) {
+      pl->ce = gc.ce;
+      std::lock_guard<std::mutex> lk(g_grid_mu);
+      pl->ce->live_plans++;
+    }
   }
   build_tables(pl);
   if (pl->ce) GMP_TRY(ce_exchange_tables(pl, stream));
@@ -2146,6 +2156,18 @@ extern "C" gmp_status_t gemm_mp_balance(const gmp_desc_t* desc, const uint8_t* a
 
 extern "C" void gemm_mp_destroy(gmp_plan_t pl) {
   if (!pl) return;
+  if (pl->ce) {
+    std::lock_guard<std::mutex> lk(g_grid_mu);
+    if (--pl->ce->live_plans == 0) {
+      // no plan left: let our pulls finish, then unmap the peers' workspaces so their
+      // owners can really free them (the next convert maps again)
+      cudaStreamSynchronize(pl->ce->comm_stream);
+      for (auto& o : pl->ce->opened) cudaIpcCloseMemHandle(o.second);
+      pl->ce->opened.clear();
+      pl->ce->peer_ws.clear();
+      pl->ce->ws_for = nullptr;
+    }
+  }
   for (auto& e : pl->step_ev) if (e) cudaEventDestroy(e);
   if (pl->packed_ev) cudaEventDestroy(pl->packed_ev);
   if (pl->done_ev) cudaEventDestroy(pl->done_ev);

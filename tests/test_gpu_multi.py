@@ -39,11 +39,14 @@ def _port():
 def test_summa_bitwise_vs_single_gpu(G, sender, cfg, grid, balance, nccl):
     if torch.cuda.device_count() < G:
         pytest.skip(f"needs {G} GPUs")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={G}",
-           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(ROOT, "tools", "multi_gpu_check.py"), "--cfg", cfg] + (["--sender"] if sender else []) + \
-        (["--grid", grid] if grid else []) + (["--balance"] if balance else []) + (["--nccl"] if nccl else [])
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    for attempt in range(3):   # a free port can be taken between probing and binding: retry
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={G}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+               os.path.join(ROOT, "tools", "multi_gpu_check.py"), "--cfg", cfg] + (["--sender"] if sender else []) + \
+            (["--grid", grid] if grid else []) + (["--balance"] if balance else []) + (["--nccl"] if nccl else [])
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+        if r.returncode == 0 or "EADDRINUSE" not in r.stderr:
+            break
     assert r.returncode == 0, r.stderr[-2000:]
     line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
     res = json.loads(line)
