@@ -121,6 +121,17 @@ def test_merged_16bit_launch_bitwise_vs_per_class(nb, beta, seed):
     assert ok, rel
 
 
+def test_cnorm_sentinels_gpu_bitwise():
+    """the O4 reduction order on the GPU map kernel: sentinel tiles whose sum of squares
+    depends on the order (tests/test_oracle_map.py) give the oracle's S bit for bit"""
+    from test_oracle_map import _cnorm_order, _sentinels
+    for t in _sentinels(128):
+        A = np.ascontiguousarray(t)
+        g, _ = run_gpu(A, np.ones((128, 128)), None, 128, 1e-6, 1.0, 0.0, 0b01111)
+        S, M, F = g.tile_stats("A")
+        assert S[0, 0] == oracle.cnorm(A) == _cnorm_order(A)
+
+
 def test_fp32_split_parts_are_exact():
     """The tensor-pipe FP32 class consumes x = x0 + x1 + x2 (three BF16 parts,
     K-major): the parts must reproduce every FP32 operand value exactly."""

@@ -34,6 +34,74 @@ def test_cnorm_within_rational_bound(nb):
     assert abs(got - exact) <= Fraction(nb * nb) * Fraction(2.0 ** -53) * exact
 
 
+def _rn(x: Fraction) -> float:
+    return float(x)          # Fraction -> float rounds to nearest, ties to even
+
+
+def _cnorm_order(tile, order="O4"):
+    """DESIGN.md O4 written out with exact rationals and one rounding per operation:
+    256 lanes x 2 slots, lane t slot s runs an fma chain over q = 2t + s + 512w (w = 0, 1, ...);
+    t = a0 + a1; butterfly t <- t + t[lane ^ off] inside each 32-lane warp for off = 16, 8, 4, 2, 1;
+    S = ((w0 + w1) + ...) + w7.  `order` selects a plausible wrong variant (to show the
+    sentinel tiles below can tell them apart): "slot256" (q = t + 256 s + 512 w), "bfly1"
+    (offsets 1, 2, 4, 8, 16), "warptree" (pairwise sum of the warp results)."""
+    x = [Fraction(float(v)) for v in np.asarray(tile, np.float64).ravel()]
+    n = len(x)
+    acc = [[Fraction(0), Fraction(0)] for _ in range(256)]
+    for base in range(0, n, 512):
+        for t in range(256):
+            for sl in range(2):
+                q = base + (t + 256 * sl if order == "slot256" else 2 * t + sl)
+                acc[t][sl] = Fraction(_rn(x[q] * x[q] + acc[t][sl]))
+    lane = [Fraction(_rn(a[0] + a[1])) for a in acc]
+    offs = (1, 2, 4, 8, 16) if order == "bfly1" else (16, 8, 4, 2, 1)
+    for off in offs:
+        lane = [Fraction(_rn(lane[t] + lane[t ^ off])) for t in range(256)]
+    w = [lane[32 * k] for k in range(8)]
+    if order == "warptree":
+        while len(w) > 1:
+            w = [Fraction(_rn(w[2 * i] + w[2 * i + 1])) for i in range(len(w) // 2)]
+        return float(w[0])
+    S = w[0]
+    for k in range(1, 8):
+        S = Fraction(_rn(S + w[k]))
+    return float(S)
+
+
+def _sentinels(nb=64):
+    """tiles whose CNORM depends on the reduction order: a big element and tiny ones whose
+    squares (each below half an ulp of the big square) survive only if they meet each other
+    before they meet the big one"""
+    out = []
+    tiny = 2.0 ** -27 * 0.75 ** 0.5   # tiny^2 = 0.75 * 2^-54
+    for big_q, tiny_qs in [(0, [1, 513, 1025]),            # slot 1 of lane 0 vs slot 0
+                           (0, [2, 64, 514]),             # lanes 1 and 32 (another warp)
+                           (0, [32, 256 + 32, 96]),       # lane 16 / 48 (butterfly offset 16)
+                           (0, [64 * 2 * 8, 130, 258]),   # warps 4, lane 65, lane 129
+                           (512, [0, 2, 4])]:             # the big one later in a chain
+        t = np.zeros(nb * nb)
+        t[big_q] = 1.0
+        for q in tiny_qs:
+            t[q] = tiny
+        out.append(t.reshape(nb, nb))
+    return out
+
+
+def test_cnorm_order_written_out():
+    """O4's reduction order, pinned: the oracle's CNORM equals the order written out above
+    on sentinel tiles (where plausible other orders give other results) and on tiles with
+    a wide dynamic range"""
+    tiles = _sentinels()
+    rng = np.random.default_rng(11)
+    for nb in (32, 64):
+        tiles.append(rng.standard_normal((nb, nb)) * np.exp2(rng.integers(-30, 30, (nb, nb))))
+    for t in tiles:
+        assert oracle.cnorm(t) == _cnorm_order(t)
+    # the sentinels really separate the plausible variants from O4
+    for variant in ("slot256", "bfly1", "warptree"):
+        assert any(_cnorm_order(t, variant) != _cnorm_order(t) for t in tiles), variant
+
+
 def test_cnorm_reads_ld_not_contiguity():
     rng = np.random.default_rng(5)
     big = rng.standard_normal((64, 96))
