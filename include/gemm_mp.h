@@ -85,6 +85,10 @@ typedef enum {
                                  (the round-1 transport) instead of the default copy-engine pulls:
                                  each receiver copies the tiles it needs straight from the root's
                                  payload slot over NVLink (workspaces mapped with CUDA IPC, no SMs) */
+#define GMP_FLAG_DYN_SCHED 8192u /* tcgen05 class launches take their next item from a device counter
+                                 when the TMA producer needs it (CTAs stay on a narrow window of items)
+                                 instead of the default static walk (CTA b: items b, b + grid, ...).
+                                 Measured at cfg3: 834-841 vs 858-860 TF/s, DRAM bytes unchanged.   */
 #define GMP_FLAG_TC_PAIR 32u /* opt-in: FP16/BF16/E4M3/E5M2 launches whose C tiles fold into binary32 W
                                  and whose nb is a multiple of 256 run on SM pairs (tcgen05 cta_group::2,
                                  256 x 256 sub-tiles, half the B bytes per SM), rastered by C tile row

@@ -35,6 +35,7 @@ GMP_FLAG_TC_SINGLE = 512
 GMP_FLAG_FP32_X9 = 1024
 GMP_FLAG_SPLIT16 = 2048
 GMP_FLAG_NCCL_BCAST = 4096
+GMP_FLAG_DYN_SCHED = 8192
 STATUS = ["GMP_OK", "GMP_ERR_ARG", "GMP_ERR_NOT_DIVISIBLE", "GMP_ERR_MAP_SHAPE", "GMP_ERR_NONFINITE",
           "GMP_ERR_GRID", "GMP_ERR_WORKSPACE", "GMP_ERR_STATE", "GMP_ERR_CUDA", "GMP_ERR_NCCL",
           "GMP_ERR_UNSUPPORTED"]

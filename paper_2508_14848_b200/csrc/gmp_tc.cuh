@@ -150,6 +150,45 @@ __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t* r) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// Work distribution of a persistent launch.  Static (default): CTA b takes items b, b + grid, ...
+// Dynamic (GMP_FLAG_DYN_SCHED): the TMA producer takes the next item from a global
+// atomic counter when it is about to load it, so the CTAs stay on a narrow window of
+// consecutive items (sub-tiles of ~1 C tile sharing the same operand tiles in L2) instead
+// of drifting apart when items differ in length; it hands each index to the MMA warp and
+// the epilogue warps through a small shared-memory ring (mbarrier full / empty).
+constexpr int TC_RING = 4;
+struct TcSched {
+  int* counter = nullptr;          // device counter (zeroed before the launch); null: static
+  int64_t* ring = nullptr;         // [TC_RING] item indices (shared memory)
+  uint64_t* rfull = nullptr;       // [TC_RING]
+  uint64_t* rempty = nullptr;      // [TC_RING], MMA warp + epilogue warps arrive
+  int64_t nitems = 0;
+  // producer: k-th item of this CTA (>= nitems: done)
+  __device__ __forceinline__ int64_t produce(int k) const {
+    int64_t it;
+    if (counter) it = (int64_t)atomicAdd(counter, 1);
+    else it = (int64_t)blockIdx.x + (int64_t)k * gridDim.x;
+    if (ring) {
+      const int r = k % TC_RING;
+      mbar_wait(&rempty[r], ((k / TC_RING) & 1) ^ 1);
+      ring[r] = it;
+      mbar_arrive(&rfull[r]);
+    }
+    return it;
+  }
+  // consumers: k-th item; whole_warp = all 32 lanes call it (the epilogue warps: lane 0
+  // releases the slot after the warp has read it), else a single thread (the MMA issuer)
+  __device__ __forceinline__ int64_t consume(int k, int lane, bool whole_warp) const {
+    if (!ring) return (int64_t)blockIdx.x + (int64_t)k * gridDim.x;
+    const int r = k % TC_RING;
+    mbar_wait(&rfull[r], (k / TC_RING) & 1);
+    const int64_t it = *(volatile int64_t*)&ring[r];
+    if (whole_warp) __syncwarp();
+    if (lane == 0) mbar_arrive(&rempty[r]);
+    return it;
+  }
+};
+
 // Epilogue warps 2..9 of the 1-SM tcgen05 kernels (k_tc_class, k_tc_fused): per
 // pair, read the FP32 product from TMEM and fold it into W (O9).
 template <int BN>
@@ -157,7 +196,8 @@ __device__ __forceinline__ void tc_epilogue(const WorkItem* __restrict__ items, 
                                             const PairDesc* __restrict__ pairs, const CTileDesc* __restrict__ ctiles,
                                             uint8_t* __restrict__ ws, int nb, double alpha, double beta,
                                             uint32_t tmem_base, uint64_t* tfull, uint64_t* tempty, int warp,
-                                            int lane, const int32_t* __restrict__ order = nullptr) {
+                                            int lane, const int32_t* __restrict__ order = nullptr,
+                                            const TcSched sc = TcSched()) {
   // epilogue: 8 warps; warp w reads TMEM lanes 32*(w%4)..+31 (= tile rows) and
   // half (w-2)/4 of the BN columns.  binary32 W: the W row segment lives in
   // registers for the whole item (one read + one write per item instead of
@@ -167,7 +207,9 @@ __device__ __forceinline__ void tc_epilogue(const WorkItem* __restrict__ items, 
   const int rloc = quarter * 32 + lane;
   int acc = 0;
   uint32_t acc_phase = 0;
-  for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+  for (int k = 0;; ++k) {
+    const int64_t it = sc.consume(k, lane, true);
+    if (it >= nitems) break;
     const WorkItem w = expand_item(items, it, nb, BN, order);
     const CTileDesc ct = ctiles[w.ctile];
     const int64_t rowoff = (int64_t)(w.m0 + rloc) * nb + w.n0 + half * HC;
@@ -311,7 +353,7 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
            const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
            const WorkItem* __restrict__ items, int64_t nitems, const PairDesc* __restrict__ pairs,
            const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha, double beta,
-           const int32_t* __restrict__ order) {
+           const int32_t* __restrict__ order, int* __restrict__ sched_counter) {
   constexpr int NP = tc_np<C>(), ST = tc_stages<C>();
   constexpr bool MX = (C == GMP_MX);       // MXFP4: 4-bit elements + scale-factor chunks per stage
   static_assert(!MX || BN == 128, "MXFP4 runs at BN = 128 (TMEM: 2 x 128 accumulator + scale columns)");
@@ -330,12 +372,19 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
   uint64_t* empty = full + ST;
   uint64_t* tfull = empty + ST;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rfull = tempty + 2;
+  uint64_t* rempty = rfull + TC_RING;
+  int64_t* ring = reinterpret_cast<int64_t*>(rempty + TC_RING);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + TC_RING);
+  TcSched sc;
+  sc.nitems = nitems;
+  if (sched_counter) { sc.counter = sched_counter; sc.ring = ring; sc.rfull = rfull; sc.rempty = rempty; }
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < ST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], TC_EPI_WARPS); }
+    for (int s = 0; s < TC_RING; ++s) { mbar_init(&rfull[s], 1); mbar_init(&rempty[s], 1 + TC_EPI_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
@@ -359,7 +408,9 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+      for (int kk = 0;; ++kk) {
+        const int64_t it = sc.produce(kk);
+        if (it >= nitems) break;
         const WorkItem w = expand_item(items, it, nb, BN, order);
         for (int pi = 0; pi < w.pcnt; ++pi) {
           const PairDesc pd = pairs[w.pbeg + pi];
@@ -397,7 +448,9 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
     if (lane == 0) {
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
-      for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+      for (int kk = 0;; ++kk) {
+        const int64_t it = sc.consume(kk, 0, false);
+        if (it >= nitems) break;
         const WorkItem w = expand_item(items, it, nb, BN, order);
         for (int pi = 0; pi < w.pcnt; ++pi) {
           const uint32_t idesc = (C == 3 && pairs[w.pbeg + pi].cls == 2) ? tc_idesc<2, BN>() : IDESC;
@@ -447,7 +500,8 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
       }
     }
   } else {
-    tc_epilogue<BN>(items, nitems, pairs, ctiles, ws, nb, alpha, beta, tmem_base, tfull, tempty, warp, lane, order);
+    tc_epilogue<BN>(items, nitems, pairs, ctiles, ws, nb, alpha, beta, tmem_base, tfull, tempty, warp, lane, order,
+                    sc);
   }
   tc_fence_before();
   __syncthreads();
@@ -459,13 +513,15 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
 template <int C, int BN>
 constexpr int tc_smem_bytes() {
   return tc_stages<C>() * (tc_np<C>() * (TC_BM * 128 + BN * 128) + (C == GMP_MX ? 2048 : 0)) + 1024 /*align*/ +
-         256 /*barriers*/;
+         512 /*barriers, scheduler ring*/;
 }
 
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 struct TcTables {
+  int* counters = nullptr;   // device counters of the dynamic scheduler (one per launch of an execute)
+  int ncounters = 0;
   CUtensorMap mapA[GMP_NARENA], mapB[GMP_NARENA];   // classes 2..5 and GMP_AR_SPLIT (FP32 BF16 parts);
                                                     // B box rows = tc_bn(nb)
   CUtensorMap mapB128[GMP_NARENA];                  // B box of 128 rows (launches with binary64 W)
@@ -547,7 +603,8 @@ inline gmp_status_t tc_prepare(TcTables& t, uint8_t* ws, const int64_t* arena_of
 
 template <int C, int BN>
 inline gmp_status_t tc_launch_t(TcTables& t, const WorkItem* it, int64_t n, const PairDesc* pd, const CTileDesc* ct,
-                                uint8_t* ws, int nb, double alpha, double beta, const int32_t* order, cudaStream_t s) {
+                                uint8_t* ws, int nb, double alpha, double beta, const int32_t* order, cudaStream_t s,
+                                int* counter) {
   constexpr int smem = tc_smem_bytes<C, BN>();
   if (ensure_max_smem(k_tc_class<C, BN>, smem) != cudaSuccess) return GMP_ERR_CUDA;
   int dev = 0, sms = 148;
@@ -559,29 +616,33 @@ inline gmp_status_t tc_launch_t(TcTables& t, const WorkItem* it, int64_t n, cons
   const int m2 = (C == 3 && t.ready[2]) ? 2 : mi;   // FP16 arena for merged 16-bit launches
   k_tc_class<C, BN><<<grid, TC_THREADS, smem, s>>>(t.mapA[mi], BN == 128 ? t.mapB128[mi] : t.mapB[mi], t.mapA[m2],
                                                     BN == 128 ? t.mapB128[m2] : t.mapB[m2], it, n, pd, ct,
-                                                    ws, nb, alpha, beta, order);
+                                                    ws, nb, alpha, beta, order, counter);
   return cudaGetLastError() == cudaSuccess ? GMP_OK : GMP_ERR_CUDA;
 }
 
 // cls: 2..5 for the 16/8-bit classes, TC_SPLIT for the FP32 class on the tensor
 // pipe; bn: 256 or 128 (128 when the launch folds into binary64 W)
+// counter: device int of the dynamic scheduler, zeroed here on the stream; null = static
 inline gmp_status_t tc_launch(TcTables& t, int cls, int bn, const WorkItem* it, int64_t n, const PairDesc* pd,
                               const CTileDesc* ct, uint8_t* ws, int nb, double alpha, double beta, const int32_t* order,
-                              cudaStream_t s) {
+                              cudaStream_t s, int* counter = nullptr) {
   const int mi = (cls == TC_SPLIT || cls == TC_SPLIT6) ? GMP_AR_SPLIT : cls;
   const bool ok = t.ready[mi] || (cls == 3 && t.ready[2]);   // merged 16-bit launch with FP16 pairs only
   if (!((cls >= 2 && cls <= GMP_MX) || cls == TC_SPLIT || cls == TC_SPLIT6) || !ok) return GMP_ERR_STATE;
   if (cls == GMP_MX && bn != 128) return GMP_ERR_STATE;
+  if (counter && cudaMemsetAsync(counter, 0, sizeof(int), s) != cudaSuccess) return GMP_ERR_CUDA;
   const bool wide = bn == 256;
+#define GMP_TCL(C_, BN_) tc_launch_t<C_, BN_>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s, counter)
   switch (cls) {
-    case GMP_MX: return tc_launch_t<GMP_MX, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s);
-    case 2: return wide ? tc_launch_t<2, 256>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s) : tc_launch_t<2, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s);
-    case 3: return wide ? tc_launch_t<3, 256>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s) : tc_launch_t<3, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s);
-    case 4: return wide ? tc_launch_t<4, 256>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s) : tc_launch_t<4, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s);
-    case 5: return wide ? tc_launch_t<5, 256>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s) : tc_launch_t<5, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s);
-    case TC_SPLIT6: return tc_launch_t<TC_SPLIT6, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s);
-    default: return tc_launch_t<TC_SPLIT, 128>(t, it, n, pd, ct, ws, nb, alpha, beta, order, s);
+    case GMP_MX: return GMP_TCL(GMP_MX, 128);
+    case 2: return wide ? GMP_TCL(2, 256) : GMP_TCL(2, 128);
+    case 3: return wide ? GMP_TCL(3, 256) : GMP_TCL(3, 128);
+    case 4: return wide ? GMP_TCL(4, 256) : GMP_TCL(4, 128);
+    case 5: return wide ? GMP_TCL(5, 256) : GMP_TCL(5, 128);
+    case TC_SPLIT6: return GMP_TCL(TC_SPLIT6, 128);
+    default: return GMP_TCL(TC_SPLIT, 128);
   }
+#undef GMP_TCL
 }
 
 inline void tc_release(TcTables&) {}
