@@ -5,7 +5,7 @@ workload on the GPU, runs plan + convert + execute through the C ABI, repeats
 execute, and prints one JSON line per run with the realised mix, the
 per-class device times and the precision-mix roofline
     T_roof = sum_c F_c / Peak_c      (Peak from MEASURED_PEAKS.json, bf16 burst;
-                                      FP64 = DMMA 37.2, FP32 class = BF16 / 9)
+                                      FP64 = DMMA 37.2, FP32 class = BF16 / 6)
 Comparison runs:
   cfg2 all-FP64 (class_mask = FP64)            -- the paper's 100D:0S baseline
   cfg2 cuBLAS DGEMM (torch.matmul float64)     -- the library FP64 GEMM
@@ -29,7 +29,7 @@ import gmp_inputs  # noqa: E402
 from paper_2508_14848_b200 import api  # noqa: E402
 from paper_2508_14848_b200 import binding as B  # noqa: E402
 
-NAMES = ["FP64", "FP32", "FP16", "BF16", "E4M3", "E5M2"]
+NAMES = ["FP64", "FP32", "FP16", "BF16", "E4M3", "E5M2", "MX4"]
 
 
 def peaks():
@@ -38,7 +38,8 @@ def peaks():
     except Exception:
         p = {"bf16_tflops": 1590.0}
     bf16 = p.get("bf16_tflops", 1590.0)
-    return [37.22496, bf16 / 9.0, bf16, bf16, 2 * bf16, 2 * bf16]
+    # FP32 class: BF16x6 on tcgen05 (R32); MXFP4: 2 x E4M3 (nominal)
+    return [37.22496, bf16 / 6.0, bf16, bf16, 2 * bf16, 2 * bf16, 4 * bf16]
 
 
 def run(w, reps, mask=None, flags=0, explicit=None, label=None):
@@ -126,6 +127,7 @@ def main():
         ("cfg3", lambda: run(W(3), a.reps)),
         ("cfg4", lambda: run(W(4), a.reps)),
         ("cfg4_allfp16", lambda: run(W(4), a.reps, explicit=2, label="cfg4_explicit_all_FP16")),
+        ("cfg4_mx4", lambda: run(W(4, "mx4"), a.reps)),
         ("cfg5_uniform", lambda: run(W(5, "uniform"), a.reps)),
         ("cfg5_uniform_1e-2", lambda: run(W(5, "uniform_1e-2"), a.reps)),
         ("cfg5_E8", lambda: run(W(5, "E8"), a.reps)),
