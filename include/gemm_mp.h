@@ -89,6 +89,9 @@ typedef enum {
                                  when the TMA producer needs it (CTAs stay on a narrow window of items)
                                  instead of the default static walk (CTA b: items b, b + grid, ...).
                                  Measured at cfg3: 834-841 vs 858-860 TF/s, DRAM bytes unchanged.   */
+#define GMP_FLAG_SPLIT_BN128 16384u /* FP32 class (BF16x6) always at BN = 128 (128-byte K blocks); default
+                                 BN = 256 with 64-byte K blocks when every W of the launch is binary32
+                                 and nb % 256 == 0 (fewer staged bytes per flop)                       */
 #define GMP_FLAG_TC_PAIR 32u /* opt-in: FP16/BF16/E4M3/E5M2 launches whose C tiles fold into binary32 W
                                  and whose nb is a multiple of 256 run on SM pairs (tcgen05 cta_group::2,
                                  256 x 256 sub-tiles, half the B bytes per SM), rastered by C tile row

@@ -1060,7 +1060,9 @@ static void build_tables(gmp_plan_s* pl) {
         continue;
       }
       // flat launch size: items x sub-tiles of the class kernel's CTA tile
-      const int bn = ozaki ? OZ_BN : split ? 128 : tc ? tcbn : (c == 0 && kind == 0) ? DMMA_BN : mn_bn(c);
+      // FP32 split: BN = 256 (BF16x6, 64-byte K blocks) when every W of the launch is binary32
+      const int split_bn = (!w64 && nb % 256 == 0 && split_t0(d.flags) && !(d.flags & GMP_FLAG_SPLIT_BN128)) ? 256 : 128;
+      const int bn = ozaki ? OZ_BN : split ? split_bn : tc ? tcbn : (c == 0 && kind == 0) ? DMMA_BN : mn_bn(c);
       Launch L{s, c, kind, ibeg, (int64_t)its.size() * subtiles_per_item((int)nb, bn), bn};
       if (kind == 1 || kind == 3) L.obeg = raster(its, (int)(nb / 128), (int)(nb / bn), false);
       if (merged) {   // GMP_FLAG_TIMING: FP16 and BF16 MMAs run at the same rate -> share by pairs
@@ -1855,7 +1857,8 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
         // workspace); default static striding (measured 2 % faster at cfg3, same DRAM bytes)
         int* ctr = (L.obeg < 0 && (pl->d.flags & GMP_FLAG_DYN_SCHED))
                        ? reinterpret_cast<int*>(ws + pl->off_sched) + li : nullptr;
-        GMP_LAUNCH(tc_launch(pl->tc, L.kind == 3 ? (split_t0(pl->d.flags) ? TC_SPLIT6 : TC_SPLIT) : L.cls, L.bn, it,
+        const int tcls = L.kind != 3 ? L.cls : !split_t0(pl->d.flags) ? TC_SPLIT : L.bn == 256 ? TC_SPLIT6W : TC_SPLIT6;
+        GMP_LAUNCH(tc_launch(pl->tc, tcls, L.bn, it,
                           L.icount, pd, dct, ws, (int)nb, pl->d.alpha, pl->d.beta,
                           L.obeg >= 0 ? (const int32_t*)(ws + pl->off_order) + L.obeg : nullptr, stream, ctr),
                    "k_tc_class");

@@ -108,11 +108,7 @@ __global__ void __launch_bounds__(256) k_slice64(const SliceJob* __restrict__ jo
 // product into it (O9).
 // ---------------------------------------------------------------------------
 constexpr int OZ2_BN = 64, OZ2_BK = 64, OZ2_STAGES = 2;
-// K-major SWIZZLE_64B canonical layout: 8-row x 64-byte atoms, SBO = 512 B.
-__device__ __forceinline__ uint64_t sdesc_k_sw64(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
-}
+// (sdesc_k_sw64: K-major SWIZZLE_64B descriptor, gmp_tc.cuh)
 // D = S32 (c_format 2), A/B signed int8 (format 1), K-major, N = 64, M = 128
 constexpr uint32_t oz_idesc() {
   return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ2_BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);

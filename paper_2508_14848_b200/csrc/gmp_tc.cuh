@@ -95,6 +95,11 @@ __device__ __forceinline__ uint64_t sdesc_k_sw128(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
+// K-major SWIZZLE_64B canonical layout: 8-row x 64-byte atoms, SBO = 512 B.
+__device__ __forceinline__ uint64_t sdesc_k_sw64(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+}
 // instruction descriptor: D = F32, A/B format, K-major both, N>>3, M>>4
 template <int C, int BN>
 __host__ __device__ constexpr uint32_t tc_idesc() {
@@ -337,14 +342,20 @@ __device__ __forceinline__ void tc_epilogue(const WorkItem* __restrict__ items, 
 // smallest terms first; binary32 inputs, exact products, binary32 accumulation.
 constexpr int TC_SPLIT = 9;    // template id of the FP32-class kernel, all nine part products (BF16x9, exact)
 constexpr int TC_SPLIT6 = 10;  // the six part products x_i y_j with i + j <= 2 (BF16x6, the default; R32)
-template <int C> constexpr bool tc_is_split() { return C == TC_SPLIT || C == TC_SPLIT6; }
+// BF16x6 at BN = 256 (binary32 W, nb % 256 == 0): 64-byte K blocks (SWIZZLE_64B), 3 stages of
+// 3 x (8 + 16) KB -- 175 instead of 131 flop per staged byte, for a kernel the L2 -> SMEM feed limits
+constexpr int TC_SPLIT6W = 11;
+template <int C> constexpr bool tc_is_split() { return C == TC_SPLIT || C == TC_SPLIT6 || C == TC_SPLIT6W; }
 template <int C> constexpr int tc_np() { return tc_is_split<C>() ? 3 : 1; }
-template <int C> constexpr int tc_t0() { return C == TC_SPLIT6 ? 3 : 0; }   // first part product (smallest first)
+template <int C> constexpr int tc_t0() { return (C == TC_SPLIT6 || C == TC_SPLIT6W) ? 3 : 0; }   // smallest first
+template <int C> constexpr int tc_kbytes() { return C == TC_SPLIT6W ? 64 : 128; }   // bytes of K per stage row
 // MXFP4: 4 stages of 34 KB (6 measured 13 % slower in the cfg4-mx4 step)
 #ifndef GMP_MX_STAGES
 #define GMP_MX_STAGES 4
 #endif
-template <int C> constexpr int tc_stages() { return tc_is_split<C>() ? 2 : C == GMP_MX ? GMP_MX_STAGES : TC_STAGES; }
+template <int C> constexpr int tc_stages() {
+  return C == TC_SPLIT6W ? 3 : tc_is_split<C>() ? 2 : C == GMP_MX ? GMP_MX_STAGES : TC_STAGES;
+}
 template <int C> constexpr int tc_map_index() { return tc_is_split<C>() ? GMP_AR_SPLIT : C; }
 
 template <int C, int BN>
@@ -358,9 +369,10 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
   constexpr bool MX = (C == GMP_MX);       // MXFP4: 4-bit elements + scale-factor chunks per stage
   static_assert(!MX || BN == 128, "MXFP4 runs at BN = 128 (TMEM: 2 x 128 accumulator + scale columns)");
   constexpr int ESZ = (C == 4 || C == 5) ? 1 : 2;
-  constexpr int BK = MX ? 256 : 128 / ESZ; // elements per 128-byte K block
-  constexpr int NMMA = 4;                  // 32-byte K per tcgen05.mma
-  constexpr int A_BYTES = TC_BM * 128, B_BYTES = BN * 128;
+  constexpr int KB = tc_kbytes<C>();       // bytes of K per staged row: 128 (SWIZZLE_128B) or 64 (SWIZZLE_64B)
+  constexpr int BK = MX ? 256 : KB / ESZ;  // elements per K block
+  constexpr int NMMA = KB / 32;            // 32-byte K per tcgen05.mma
+  constexpr int A_BYTES = TC_BM * KB, B_BYTES = BN * KB;
   constexpr int SF_BYTES = MX ? 1024 : 0;  // per operand: 128 rows x 8 scales = 2 chunks of 512 B
   constexpr int STAGE_BYTES = NP * (A_BYTES + B_BYTES) + 2 * SF_BYTES;
   constexpr uint32_t TMEM_COLS = MX ? 512 : 2 * BN;
@@ -484,8 +496,9 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
               // terms (i, j) by decreasing i + j: the smallest part products first
               constexpr int TI[9] = {2, 2, 1, 2, 1, 0, 1, 0, 0}, TJ[9] = {2, 1, 2, 0, 1, 2, 0, 1, 0};
               const int ti = (NP == 1) ? 0 : TI[t], tj = (NP == 1) ? 0 : TJ[t];
-              const uint64_t ad = sdesc_k_sw128(sa + ti * A_BYTES);
-              const uint64_t bd = sdesc_k_sw128(sa + NP * A_BYTES + tj * B_BYTES);
+              const uint64_t ad = (KB == 64) ? sdesc_k_sw64(sa + ti * A_BYTES) : sdesc_k_sw128(sa + ti * A_BYTES);
+              const uint64_t bd = (KB == 64) ? sdesc_k_sw64(sa + NP * A_BYTES + tj * B_BYTES)
+                                             : sdesc_k_sw128(sa + NP * A_BYTES + tj * B_BYTES);
 #pragma unroll
               for (int k = 0; k < NMMA; ++k)
                 tc_mma<C>(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, (kb | (t - t0) | k) != 0);
@@ -512,7 +525,7 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
 
 template <int C, int BN>
 constexpr int tc_smem_bytes() {
-  return tc_stages<C>() * (tc_np<C>() * (TC_BM * 128 + BN * 128) + (C == GMP_MX ? 2048 : 0)) + 1024 /*align*/ +
+  return tc_stages<C>() * (tc_np<C>() * (TC_BM + BN) * tc_kbytes<C>() + (C == GMP_MX ? 2048 : 0)) + 1024 /*align*/ +
          512 /*barriers, scheduler ring*/;
 }
 
@@ -525,6 +538,7 @@ struct TcTables {
   CUtensorMap mapA[GMP_NARENA], mapB[GMP_NARENA];   // classes 2..5 and GMP_AR_SPLIT (FP32 BF16 parts);
                                                     // B box rows = tc_bn(nb)
   CUtensorMap mapB128[GMP_NARENA];                  // B box of 128 rows (launches with binary64 W)
+  CUtensorMap splitA64, splitB64;                   // split arena, 64-byte x {128, 256}-row boxes (SW64)
   bool ready[GMP_NARENA] = {};
   int nb = 0;
 };
@@ -596,6 +610,16 @@ inline gmp_status_t tc_prepare(TcTables& t, uint8_t* ws, const int64_t* arena_of
             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return GMP_ERR_CUDA;
+    if (split && nb % 256 == 0) {   // BF16x6 at BN = 256: 64-byte K boxes, SWIZZLE_64B
+      cuuint32_t a64[2] = {32u, (cuuint32_t)TC_BM}, b64[2] = {32u, 256u};
+      if (enc(&t.splitA64, dt, 2, base, dims, strides, a64, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
+          enc(&t.splitB64, dt, 2, base, dims, strides, b64, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return GMP_ERR_CUDA;
+    }
     t.ready[c] = true;
   }
   return GMP_OK;
@@ -614,7 +638,9 @@ inline gmp_status_t tc_launch_t(TcTables& t, const WorkItem* it, int64_t n, cons
   // a merged 16-bit launch (C = 3) may hold FP16 pairs only: then the BF16 arena is empty
   const int mi = (C == 3 && !t.ready[3]) ? 2 : tc_map_index<C>();
   const int m2 = (C == 3 && t.ready[2]) ? 2 : mi;   // FP16 arena for merged 16-bit launches
-  k_tc_class<C, BN><<<grid, TC_THREADS, smem, s>>>(t.mapA[mi], BN == 128 ? t.mapB128[mi] : t.mapB[mi], t.mapA[m2],
+  const CUtensorMap& ma = (C == TC_SPLIT6W) ? t.splitA64 : t.mapA[mi];
+  const CUtensorMap& mb = (C == TC_SPLIT6W) ? t.splitB64 : (BN == 128 ? t.mapB128[mi] : t.mapB[mi]);
+  k_tc_class<C, BN><<<grid, TC_THREADS, smem, s>>>(ma, mb, t.mapA[m2],
                                                     BN == 128 ? t.mapB128[m2] : t.mapB[m2], it, n, pd, ct,
                                                     ws, nb, alpha, beta, order, counter);
   return cudaGetLastError() == cudaSuccess ? GMP_OK : GMP_ERR_CUDA;
@@ -626,9 +652,11 @@ inline gmp_status_t tc_launch_t(TcTables& t, const WorkItem* it, int64_t n, cons
 inline gmp_status_t tc_launch(TcTables& t, int cls, int bn, const WorkItem* it, int64_t n, const PairDesc* pd,
                               const CTileDesc* ct, uint8_t* ws, int nb, double alpha, double beta, const int32_t* order,
                               cudaStream_t s, int* counter = nullptr) {
-  const int mi = (cls == TC_SPLIT || cls == TC_SPLIT6) ? GMP_AR_SPLIT : cls;
+  const bool split = cls == TC_SPLIT || cls == TC_SPLIT6 || cls == TC_SPLIT6W;
+  const int mi = split ? GMP_AR_SPLIT : cls;
   const bool ok = t.ready[mi] || (cls == 3 && t.ready[2]);   // merged 16-bit launch with FP16 pairs only
-  if (!((cls >= 2 && cls <= GMP_MX) || cls == TC_SPLIT || cls == TC_SPLIT6) || !ok) return GMP_ERR_STATE;
+  if (!((cls >= 2 && cls <= GMP_MX) || split) || !ok) return GMP_ERR_STATE;
+  if (cls == TC_SPLIT6W && (bn != 256 || t.nb % 256)) return GMP_ERR_STATE;
   if (cls == GMP_MX && bn != 128) return GMP_ERR_STATE;
   if (counter && cudaMemsetAsync(counter, 0, sizeof(int), s) != cudaSuccess) return GMP_ERR_CUDA;
   const bool wide = bn == 256;
@@ -640,6 +668,7 @@ inline gmp_status_t tc_launch(TcTables& t, int cls, int bn, const WorkItem* it, 
     case 4: return wide ? GMP_TCL(4, 256) : GMP_TCL(4, 128);
     case 5: return wide ? GMP_TCL(5, 256) : GMP_TCL(5, 128);
     case TC_SPLIT6: return GMP_TCL(TC_SPLIT6, 128);
+    case TC_SPLIT6W: return GMP_TCL(TC_SPLIT6W, 256);
     default: return GMP_TCL(TC_SPLIT, 128);
   }
 #undef GMP_TCL
