@@ -100,18 +100,9 @@ typedef enum {
                                  later FP32-class launches run at a lower clock), DESIGN.md 7.       */
 #define GMP_FLAG_TC_SINGLE 512u /* the 1-SM 128 x 256 kernel for those launches (the default; the flag
                                  makes the choice explicit and overrides GMP_FLAG_TC_PAIR)          */
-#define GMP_FLAG_TC_MCAST 64u /* same launches as GMP_FLAG_TC_PAIR, but each SM keeps its own 1-SM MMA
-                                 (M = 128) and only the B box is split and multicast across a 2-CTA
-                                 cluster (a third fewer L2->SM bytes, no cross-SM operand reads)     */
-#define GMP_FLAG_TC_FUSED 128u /* opt-in: when the FP32 class runs on the tensor pipe and every tensor
-                                 class of a SUMMA step runs 128 x 128 sub-tiles (binary64 W, or nb
-                                 not a multiple of 256), the step's tensor classes share one launch
-                                 (k_tc_fused): per C sub-tile their pairs run in the fold order
-                                 (class 5 .. 1, l increasing) with one W read and write instead of
-                                 one per class; C is bit-identical.  Measured 3-10 % slower than the
-                                 per-class launches on cfg2 (the 16-bit pairs at 128 x 128 are limited
-                                 by their operand feed, not by W traffic).  stats.class_ms
-                                 splits the launch's time by the classes' MMA issue cycles.       */
+/* 64u, 128u: retired (round 2) -- the B-multicast 2-CTA kernel and the all-tensor-classes
+   launch measured slower than the per-class 1-SM kernels; the FP16 / BF16 W
+   sharing they aimed at is the default merged 16-bit launch (R33)                          */
 #define GMP_FLAG_SENDER_SIDE 16u /* SURVEY 8(f) NEXT-2, hybrid conversion (PAPER.md:148 defers it): a
                                  SUMMA panel tile whose receivers in its process row (A) / column (B)
                                  together need a set of classes S whose payloads are smaller than the

@@ -28,8 +28,6 @@ GMP_FLAG_FP32_FFMA = 4
 GMP_FLAG_FP64_INT8 = 8
 GMP_FLAG_SENDER_SIDE = 16
 GMP_FLAG_TC_PAIR = 32
-GMP_FLAG_TC_MCAST = 64
-GMP_FLAG_TC_FUSED = 128
 GMP_FLAG_LOOPBACK = 256
 GMP_FLAG_TC_SINGLE = 512
 GMP_FLAG_FP32_X9 = 1024

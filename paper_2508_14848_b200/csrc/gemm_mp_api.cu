@@ -29,7 +29,6 @@
 #include "gmp_tc.cuh"
 #include "gmp_ozaki.cuh"
 #include "gmp_tc2.cuh"
-#include "gmp_tcf.cuh"
 #include "gmp_layout.h"
 
 using namespace gmp;
@@ -199,17 +198,14 @@ static inline int16_t layout_transposed(int role, int cls) {
 // plan
 // ---------------------------------------------------------------------------
 struct Launch {
-  int step, cls, kind;  // kind 0: SIMT/DMMA kernel, 1: tcgen05, 2: FP64 DFMA cross-check, 3: FP32 on tcgen05
-                        // (BF16x9), 4: FP64 on the INT8 tensor pipe (Ozaki digits), 5: tcgen05 on an SM
-                        // pair (cta_group::2, 256 x 256 sub-tiles), 6: 1-SM tcgen05 with B multicast
-                        // across a 2-CTA cluster, 7: every tensor class of the step in one
-                        // launch (k_tc_fused; cls = 1, the classes are in `present`)
+  int step, cls, kind;  // kind 0: SIMT/DMMA kernel, 1: tcgen05 (cls 3 may carry FP16 pairs, R33), 2: FP64
+                        // DFMA cross-check, 3: FP32 on tcgen05 (BF16x6 / x9), 4: FP64 on the INT8 tensor
+                        // pipe (Ozaki digits), 5: tcgen05 on an SM pair (cta_group::2, 256 x 256 sub-tiles)
   int64_t ibeg, icount;
   int bn;  // N of the class kernel's CTA tile
   int64_t obeg = -1;     // kind 5: first entry of the launch's raster order (gmp_plan_s::order), -1: none
-  unsigned present = 0;  // kind 7: bit c set for each class c with pairs in the launch
-  double share[GMP_NCLASS] = {};  // kind 7: estimated share of the launch time per class
-                                  // (MMA issue cycles; GMP_FLAG_TIMING attribution)
+  unsigned present = 0;  // merged 16-bit launch: bit c set for each class c with pairs in it
+  double share[GMP_NCLASS] = {};  // its share of the launch time per class (GMP_FLAG_TIMING attribution)
 };
 
 struct Bcast {           // one SUMMA broadcast of a panel tile payload in a step
@@ -944,74 +940,12 @@ static void build_tables(gmp_plan_s* pl) {
   };
   const bool tc_on = kTcAvailable && !(d.flags & GMP_FLAG_SIMT_ONLY);
   for (int s = 0; s < steps; ++s) {
-    // GMP_FLAG_TC_FUSED: one launch for every tensor-core class of the step
-    // (k_tc_fused, gmp_tcf.cuh) when the FP32 class runs on the tensor pipe, at
-    // least two tensor classes have pairs, and each of them would run at BN = 128
-    // anyway (binary64 W in the launch, or nb not a multiple of 256): W is then
-    // read and written once per step for all of them instead of once per class.
-    bool fuse = tc_on && pl->fp32_tc && (d.flags & GMP_FLAG_TC_FUSED);
-    unsigned present = 0;
-    if (fuse) {
-      bool w64c[NC] = {};
-      for (int64_t k = 0; k < nCl; ++k) {
-        const int64_t g = pl->locC[k], i = g / nt, j = g % nt;
-        for (int64_t l = (int64_t)s * GMP_STEP_DEPTH; l < std::min<int64_t>(kt, (int64_t)(s + 1) * GMP_STEP_DEPTH); ++l) {
-          const int c = std::max(pl->codeA[i * kt + l], pl->codeB[l * nt + j]);
-          present |= 1u << c;
-          w64c[c] = w64c[c] || pl->ctd[k].code == 0;
-        }
-      }
-      // MXFP4 pairs fold first in the step (class order 6 -> 0) and run on their own kernel:
-      // a step holding any keeps the per-class launches
-      if (present >> GMP_MX & 1) fuse = false;
-      present &= 0x3Eu;   // classes 1..5
-      int ncls = 0;
-      for (int c = 1; c < NC; ++c) {
-        if (!(present >> c & 1)) continue;
-        ++ncls;
-        if (c >= 2 && !w64c[c] && tc_bn((int)nb) != 128) fuse = false;
-      }
-      fuse = fuse && ncls >= 2;
-    }
-    if (fuse) {
-      const int64_t ibeg = (int64_t)pl->items.size();
-      std::vector<WorkItem> its;
-      std::vector<int64_t> cost;
-      for (int64_t k = 0; k < nCl; ++k) {
-        const int64_t pbeg = (int64_t)pl->pairs.size();
-        for (int c = 5; c >= 1; --c) add_pairs(s, c, k);   // MXFP4 (6) keeps its own launch
-        const int64_t pcnt = (int64_t)pl->pairs.size() - pbeg;
-        if (!pcnt) continue;
-        int64_t w = 0;   // MMA issue cycles per K: BF16x9 36, 16-bit 4, 8-bit 1 (half the blocks, twice the rate)
-        for (int64_t q = pbeg; q < pbeg + pcnt; ++q) w += pl->pairs[q].cls == 1 ? 36 : pl->pairs[q].cls >= 4 ? 1 : 4;
-        its.push_back(WorkItem{(int32_t)k, 0, 0, (int32_t)pbeg, (int32_t)pcnt, 0});
-        cost.push_back(w);
-      }
-      std::vector<size_t> ord(its.size());
-      for (size_t q = 0; q < ord.size(); ++q) ord[q] = q;
-      std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return cost[a] > cost[b]; });
-      for (size_t q : ord) pl->items.push_back(its[q]);
-      Launch L{s, 1, 7, ibeg, (int64_t)its.size() * subtiles_per_item((int)nb, TCF_BN), TCF_BN};
-      L.present = present;
-      double tot = 0.0;
-      for (const WorkItem& wi : its)
-        for (int64_t q = wi.pbeg; q < wi.pbeg + wi.pcnt; ++q) {
-          const int c = pl->pairs[q].cls;
-          const double w = c == 1 ? 36.0 : c >= 4 ? 1.0 : 4.0;
-          L.share[c] += w;
-          tot += w;
-        }
-      for (int c = 0; c < NC; ++c) L.share[c] = tot > 0 ? L.share[c] / tot : 0.0;
-      pl->launches.push_back(L);
-    }
     // FP16 and BF16 pairs of a step share one k_tc_class<3> launch (default): per item the
     // BF16 pairs, then the FP16 pairs -- the fold order O9 -- so W is read and written once
     // for both and the short FP16 lists ride on the BF16 items (GMP_FLAG_SPLIT16: one launch
-    // per class; the SM-pair / multicast kernels keep per-class launches)
-    const bool merge16 = tc_on && !fuse && !(d.flags & GMP_FLAG_SPLIT16) && !pair_default(d.flags) &&
-                         !(d.flags & GMP_FLAG_TC_MCAST);
+    // per class; the SM-pair kernel keeps per-class launches)
+    const bool merge16 = tc_on && !(d.flags & GMP_FLAG_SPLIT16) && !pair_default(d.flags);
     for (int c = NC - 1; c >= 0; --c) {
-      if (fuse && c >= 1 && c <= 5) continue;   // MXFP4 pairs keep their own launch
       if (merge16 && c == 2) continue;          // carried by the class-3 launch
       // MXFP4 on tcgen05 needs whole 256-element (128-byte) K blocks: nb = 128 runs on the SIMT kernel
       const bool tc = tc_on && (c >= 2) && (c != GMP_MX || nb % 256 == 0);
@@ -1052,10 +986,9 @@ static void build_tables(gmp_plan_s* pl) {
       // GMP_FLAG_TC_PAIR: 16-bit / 8-bit classes folding into binary32 W on
       // 256-multiple tiles run on SM pairs (k_tc2_class, cta_group::2)
       const bool pair = tc && !w64 && c >= 2 && c <= 5 && (nb % 256 == 0) && pair_default(d.flags);
-      const bool mcast = tc && !w64 && c >= 2 && c <= 5 && (nb % 256 == 0) && (d.flags & GMP_FLAG_TC_MCAST) && !pair;
-      if (pair || mcast) {
-        Launch L{s, c, pair ? 5 : 6, ibeg, (int64_t)its.size() * tc2_subtiles_per_item((int)nb), TC2_BN};
-        if (pair) L.obeg = raster(its, (int)(nb / 256), (int)(nb / 256), true);
+      if (pair) {
+        Launch L{s, c, 5, ibeg, (int64_t)its.size() * tc2_subtiles_per_item((int)nb), TC2_BN};
+        L.obeg = raster(its, (int)(nb / 256), (int)(nb / 256), true);
         pl->launches.push_back(L);
         continue;
       }
@@ -1086,7 +1019,7 @@ static void build_tables(gmp_plan_s* pl) {
       const Launch& L = pl->launches[li];
       if (L.step != 0) break;
       const int64_t iend = li + 1 < pl->launches.size() ? pl->launches[li + 1].ibeg : (int64_t)pl->items.size();
-      const bool can = L.kind == 1 || L.kind == 3 || L.kind == 5 || L.kind == 7;
+      const bool can = L.kind == 1 || L.kind == 3 || L.kind == 5;
       for (int64_t q = L.ibeg; q < iend; ++q) {
         WorkItem& wi = pl->items[q];
         if (done[wi.ctile]) continue;
@@ -1130,7 +1063,7 @@ static void build_tables(gmp_plan_s* pl) {
   st.launches_convert = (pl->pack.empty() ? 0 : 1) + nsh(pl->shadow_local) + (pl->split_local.empty() ? 0 : 1) +
                         (pl->slice_local.empty() ? 0 : 1);
   for (const Launch& L : pl->launches) {
-    if (L.kind == 7) {
+    if (L.present) {
       for (int c = 0; c < NC; ++c) st.class_launches[c] += (int32_t)(L.present >> c & 1);
     } else {
       st.class_launches[L.cls]++;
@@ -1847,11 +1780,6 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
         GMP_LAUNCH(tc2_launch(pl->tc, L.cls, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, pl->d.beta,
                            L.obeg >= 0 ? (const int32_t*)(ws + pl->off_order) + L.obeg : nullptr, stream),
                    "k_tc2_class");
-      } else if (L.kind == 6) {
-        GMP_LAUNCH(tcmc_launch(pl->tc, L.cls, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, stream), "k_tcmc_class");
-      } else if (L.kind == 7) {
-        GMP_LAUNCH(tcf_launch(pl->tc, L.present, it, L.icount, pd, dct, ws, (int)nb, pl->d.alpha, pl->d.beta, stream,
-                           split_t0(pl->d.flags)), "k_tc_fused");
       } else if (L.kind == 1 || L.kind == 3) {
         // GMP_FLAG_DYN_SCHED: dynamic item scheduler (one device counter per launch, in the
         // workspace); default static striding (measured 2 % faster at cfg3, same DRAM bytes)
@@ -2022,7 +1950,7 @@ extern "C" gmp_status_t gemm_mp_get_stats(gmp_plan_t pl, gmp_stats_t* out) {
       GMP_CUDA(cudaEventSynchronize(pl->launch_ev[2 * li + 1]));
       GMP_CUDA(cudaEventElapsedTime(&ms, pl->launch_ev[2 * li], pl->launch_ev[2 * li + 1]));
       const Launch& L = pl->launches[li];
-      if (L.kind == 7 || L.present) {   // fused / merged launches: split by the classes' shares
+      if (L.present) {   // merged 16-bit launches: split by the classes' shares
         for (int c = 0; c < NC; ++c) pl->st.class_ms[c] += ms * L.share[c];
       } else {
         pl->st.class_ms[L.cls] += ms;

@@ -263,203 +263,6 @@ k_tc2_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
 }
 
-// ---------------------------------------------------------------------------
-// 1-SM MMAs with the B operand multicast across a cluster of 2 CTAs
-// (GMP_FLAG_TC_MCAST): CTA r computes rows 128r.. of a 256 x 256 sub-tile with
-// its own tcgen05.mma.cta_group::1 (M = 128, N = 256) from its own shared
-// memory, but each CTA loads only HALF of the B box and multicasts it into both
-// CTAs -- L2->SM bytes per flop drop by a third while every MMA operand stays
-// local (no cross-SM operand reads).  empty[s] counts both CTAs' MMA commits
-// (each multicasts its commit), because a stage is refilled in both CTAs.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
-                                               uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, "
-      "%3}], [%4], %5;" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
-      : "memory");
-}
-__device__ __forceinline__ void tc1_commit_both(uint64_t* b) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          smem_u32(b)),
-      "h"((uint16_t)3)
-      : "memory");
-}
-
-template <int C>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
-k_tcmc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-             const WorkItem* __restrict__ items, int64_t nitems, const PairDesc* __restrict__ pairs,
-             const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha) {
-  constexpr int ESZ = (C == 4 || C == 5) ? 1 : 2;
-  constexpr int BK = 128 / ESZ;
-  constexpr int NMMA = 4;
-  constexpr int BN = TC2_BN;
-  constexpr int A_BYTES = 128 * 128, B_BYTES = BN * 128, STAGE_BYTES = A_BYTES + B_BYTES;
-  constexpr int ST = TC_STAGES;
-  constexpr uint32_t TMEM_COLS = 2 * BN;
-  constexpr uint32_t IDESC = tc_idesc<C, BN>();
-  constexpr int HC = BN / 2;
-
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * STAGE_BYTES);
-  uint64_t* empty = full + ST;
-  uint64_t* tfull = empty + ST;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-
-  const uint32_t rank = cluster_ctarank();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == 0 && lane == 0) {
-    for (int s = 0; s < ST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 2); }
-    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], TC_EPI_WARPS); }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_fence_before();
-  cluster_sync_all();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  const int kblocks = nb / BK;
-  const int64_t cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
-  const int nsub = nb / 256;
-  auto item_at = [&](int64_t flat) {
-    const int S = nsub * nsub;
-    const int64_t idx = flat / S;
-    const int sub = (int)(flat - idx * S);
-    WorkItem w = items[idx];
-    w.m0 = (sub / nsub) * 256 + 128 * (int)rank;
-    w.n0 = (sub - (sub / nsub) * nsub) * 256;
-    return w;
-  };
-
-  if (warp == 0) {
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int64_t it = cluster; it < nitems; it += nclusters) {
-        const WorkItem w = item_at(it);
-        for (int pi = 0; pi < w.pcnt; ++pi) {
-          const PairDesc pd = pairs[w.pbeg + pi];
-          for (int kb = 0; kb < kblocks; ++kb) {
-            mbar_wait(&empty[stage], phase ^ 1);        // both CTAs' MMAs are done with the stage
-            uint8_t* sa = smem + stage * STAGE_BYTES;
-            mbar_expect_tx(&full[stage], STAGE_BYTES);  // own A + both B halves
-            tma_load_2d(sa, &tmA, kb * BK, pd.a_slot * nb + w.m0, &full[stage]);
-            tma_load_2d_mc(sa + A_BYTES + (int)rank * (B_BYTES / 2), &tmB, kb * BK,
-                           pd.b_slot * nb + w.n0 + (BN / 2) * (int)rank, &full[stage], (uint16_t)3);
-            if (++stage == ST) { stage = 0; phase ^= 1; }
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      int stage = 0, acc = 0;
-      uint32_t phase = 0, acc_phase = 0;
-      for (int64_t it = cluster; it < nitems; it += nclusters) {
-        const WorkItem w = item_at(it);
-        for (int pi = 0; pi < w.pcnt; ++pi) {
-          mbar_wait(&tempty[acc], acc_phase ^ 1);
-          tc_fence_after();
-          const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
-          for (int kb = 0; kb < kblocks; ++kb) {
-            mbar_wait(&full[stage], phase);
-            tc_fence_after();
-            const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
-            const uint64_t ad = sdesc_k_sw128(sa), bd = sdesc_k_sw128(sa + A_BYTES);
-#pragma unroll
-            for (int k = 0; k < NMMA; ++k)
-              tc_mma<C>(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), IDESC, (kb | k) != 0);
-            tc1_commit_both(&empty[stage]);
-            if (++stage == ST) { stage = 0; phase ^= 1; }
-          }
-          tc_commit(&tfull[acc]);
-          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-        }
-      }
-    }
-  } else {
-    const int quarter = warp & 3, half = (warp - 2) >> 2;
-    const int rloc = quarter * 32 + lane;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int64_t it = cluster; it < nitems; it += nclusters) {
-      const WorkItem w = item_at(it);
-      const CTileDesc ct = ctiles[w.ctile];
-      float* wrow = reinterpret_cast<float*>(ws + ct.w_off) + (int64_t)(w.m0 + rloc) * nb + w.n0 + half * HC;
-      float accr[HC];
-#pragma unroll
-      for (int v = 0; v < HC / 4; ++v) {
-        const float4 x = reinterpret_cast<const float4*>(wrow)[v];
-        accr[4 * v] = x.x; accr[4 * v + 1] = x.y; accr[4 * v + 2] = x.z; accr[4 * v + 3] = x.w;
-      }
-      for (int pi = 0; pi < w.pcnt; ++pi) {
-        const PairDesc pd = pairs[w.pbeg + pi];
-        const float f32 = __double2float_rn(ldexp_fast(alpha, pd.fexp));
-        mbar_wait(&tfull[acc], acc_phase);
-        tc_fence_after();
-        const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + half * HC);
-#pragma unroll
-        for (int ch = 0; ch < HC / 16; ++ch) {
-          uint32_t r[16];
-          tmem_ld16_nowait(tbase + ch * 16, r);
-          tmem_wait_ld();
-#pragma unroll
-          for (int v = 0; v < 16; ++v) accr[ch * 16 + v] = __fmaf_rn(f32, __uint_as_float(r[v]), accr[ch * 16 + v]);
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-      }
-#pragma unroll
-      for (int v = 0; v < HC / 4; ++v)
-        reinterpret_cast<float4*>(wrow)[v] = make_float4(accr[4 * v], accr[4 * v + 1], accr[4 * v + 2], accr[4 * v + 3]);
-    }
-  }
-  tc_fence_before();
-  cluster_sync_all();
-  tc_fence_after();
-  if (warp == 1)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
-}
-
-constexpr int tcmc_smem_bytes() { return TC_STAGES * (128 * 128 + TC2_BN * 128) + 1024 + 256; }
-
-template <int C>
-inline gmp_status_t tcmc_launch_t(TcTables& t, const WorkItem* it, int64_t n, const PairDesc* pd, const CTileDesc* ct,
-                                  uint8_t* ws, int nb, double alpha, cudaStream_t s) {
-  constexpr int smem = tcmc_smem_bytes();
-  if (ensure_max_smem(k_tcmc_class<C>, smem) != cudaSuccess) return GMP_ERR_CUDA;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t clusters = std::min<int64_t>(n, sms / 2);
-  k_tcmc_class<C><<<(unsigned)(2 * clusters), TC_THREADS, smem, s>>>(t.mapA[C], t.mapB128[C], it, n, pd, ct, ws, nb,
-                                                                     alpha);
-  return cudaGetLastError() == cudaSuccess ? GMP_OK : GMP_ERR_CUDA;
-}
-
-inline gmp_status_t tcmc_launch(TcTables& t, int cls, const WorkItem* it, int64_t n, const PairDesc* pd,
-                                const CTileDesc* ct, uint8_t* ws, int nb, double alpha, cudaStream_t s) {
-  if (cls < 2 || cls > 5 || !t.ready[cls]) return GMP_ERR_STATE;
-  switch (cls) {
-    case 2: return tcmc_launch_t<2>(t, it, n, pd, ct, ws, nb, alpha, s);
-    case 3: return tcmc_launch_t<3>(t, it, n, pd, ct, ws, nb, alpha, s);
-    case 4: return tcmc_launch_t<4>(t, it, n, pd, ct, ws, nb, alpha, s);
-    default: return tcmc_launch_t<5>(t, it, n, pd, ct, ws, nb, alpha, s);
-  }
-}
 
 constexpr int tc2_smem_bytes() { return TC2_STAGES * (128 * 128 * 2) + 1024 /*align*/ + 256 /*barriers*/; }
 

@@ -73,28 +73,27 @@ def test_host_plan_checks_scale_array_sizes():
     B.gemm_mp_destroy(pl)
 
 
-def test_fused_tensor_launch_plan():
-    """GMP_FLAG_TC_FUSED (host plan only): with FP32 and FP16 pairs in each SUMMA step
-    and nb = 128, the step's tensor classes share one launch; the FP64 class keeps its
-    own; the per-class launch counts still name every class present"""
+def test_merged_16bit_launch_plan():
+    """host plan only: with FP16 and BF16 pairs in each SUMMA step the default plan runs them
+    in one k_tc_class<3> launch (R33); GMP_FLAG_SPLIT16 keeps one launch per class; the
+    per-class launch counts still name every class present"""
     import numpy as np
     nb, t = 128, 4
-    d0 = B.make_desc(t * nb, t * nb, t * nb, nb, 1e-6, 1.0, 0.0, 0b00111, B.GMP_FLAG_SPLIT16)   # one launch per class
-    d1 = B.make_desc(t * nb, t * nb, t * nb, nb, 1e-6, 1.0, 0.0, 0b00111, B.GMP_FLAG_TC_FUSED)
-    ac = np.array([[0, 1, 2, 1]] * t, np.uint8)     # per l: FP64, FP32, FP16, FP32 pairs
+    d0 = B.make_desc(t * nb, t * nb, t * nb, nb, 1e-6, 1.0, 0.0, 0b01111, B.GMP_FLAG_SPLIT16)   # one launch per class
+    d1 = B.make_desc(t * nb, t * nb, t * nb, nb, 1e-6, 1.0, 0.0, 0b01111)
+    ac = np.array([[0, 1, 2, 3]] * t, np.uint8)     # per l: FP64, FP32, FP16, BF16 pairs
     bc = np.zeros((t, t), np.uint8)
-    bc[1:, :] = 1
-    cc = np.zeros((t, t), np.uint8)
+    cc = np.ones((t, t), np.uint8)
     z = np.zeros((t, t, B.NCLS), np.int16)
     st = []
     for d in (d0, d1):
         pl = B.gemm_mp_plan_host(d, ac, bc, cc, z, z)
         st.append(B.gemm_mp_get_stats(pl))
         B.gemm_mp_destroy(pl)
-    sep, fus = st
-    assert sep["pairs"][:3] == fus["pairs"][:3] == [t * t, 2 * t * t, t * t]
-    assert fus["launches_execute"] == sep["launches_execute"] - 1          # one step, FP32 + FP16 fused
-    assert list(fus["class_launches"][:3]) == list(sep["class_launches"][:3]) == [1, 1, 1]
+    sep, mer = st
+    assert sep["pairs"][:4] == mer["pairs"][:4] == [t * t] * 4
+    assert mer["launches_execute"] == sep["launches_execute"] - 1          # one step: FP16 rides on BF16
+    assert list(mer["class_launches"][:4]) == list(sep["class_launches"][:4]) == [1, 1, 1, 1]
 
 
 def test_host_plan_cannot_convert_or_execute():

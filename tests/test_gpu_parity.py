@@ -45,8 +45,6 @@ def _cases():
         # is process-wide, so here the flag only pins the default)
         ("single_nb512", gmp_inputs.small_workload(1024, 1536, 1536, 512, 1e-2, mode="random", E=24, beta=0.75,
                                                    class_mask=0b11111, seed=45), B.GMP_FLAG_TC_SINGLE),
-        ("mcast_nb512", gmp_inputs.small_workload(1024, 1536, 1536, 512, 1e-2, mode="random", E=24, beta=0.75,
-                                                  class_mask=0b11111, seed=45), B.GMP_FLAG_TC_MCAST),
         ("pairs_e5m2_nb512", gmp_inputs.small_workload(1024, 1024, 1536, 512, 5e-2, mode="random", E=32,
                                                        beta=0.0, class_mask=0b111111, seed=48),
          B.GMP_FLAG_TC_PAIR),
@@ -74,7 +72,7 @@ def case(request):
     g, (Cg, Cg2) = run_gpu(A, Bm, C, w.nb, w.tol, w.alpha, w.beta, w.class_mask, flags=flags, reps=2)
     gs, (Cs,) = run_gpu(A, Bm, C, w.nb, w.tol, w.alpha, w.beta, w.class_mask, flags=B.GMP_FLAG_SIMT_ONLY)
     gp, (Cp,) = run_gpu(A, Bm, C, w.nb, w.tol, w.alpha, w.beta, w.class_mask,
-                        flags=flags | B.GMP_FLAG_TC_FUSED)
+                        flags=flags | B.GMP_FLAG_SPLIT16)
     return dict(name=name, w=w, A=A, B=Bm, C=C, orc=orc, g=g, Cg=Cg, Cg2=Cg2, gs=gs, Cs=Cs, gp=gp, Cp=Cp)
 
 
@@ -158,10 +156,10 @@ def test_c_parity_product_path(case):
     assert ok, rel
 
 
-def test_fused_launch_equals_per_class_launches(case):
-    """k_tc_fused (GMP_FLAG_TC_FUSED: all tensor classes of a step in one launch) runs the
-    same pairs with the same arithmetic in the same fold order as the default one
-    k_tc_class launch per class: C is bit-identical"""
+def test_merged_16bit_launch_equals_per_class_launches(case):
+    """the default merged FP16 + BF16 launch (R33) runs the same pairs with the same
+    arithmetic in the same fold order as one launch per class (GMP_FLAG_SPLIT16): C is
+    bit-identical"""
     assert np.array_equal(case["Cg"], case["Cp"])
 
 
@@ -196,15 +194,3 @@ def test_mixes_are_mixed():
     g, _ = run_gpu(A, Bm, C, w.nb, w.tol, w.alpha, w.beta, w.class_mask)
     st = g.stats()
     assert st["tiles_a"][0] > 0 and st["tiles_a"][1] > 0 and st["tiles_a"][2] > 0
-
-
-def test_fused_launch_is_used():
-    """cfg1 (nb = 128: every tensor class runs 128 x 128 sub-tiles) has FP32, FP16 and BF16
-    pairs in each step, so GMP_FLAG_TC_FUSED launches fewer kernels than the per-class plan"""
-    w = gmp_inputs.workload(1)
-    A, Bm, C = w.matrices()
-    g, _ = run_gpu(A, Bm, C, w.nb, w.tol, w.alpha, w.beta, w.class_mask, flags=B.GMP_FLAG_TC_FUSED)
-    gp, _ = run_gpu(A, Bm, C, w.nb, w.tol, w.alpha, w.beta, w.class_mask)
-    st, sp = g.stats(), gp.stats()
-    assert sum(1 for c in range(1, 6) if st["pairs"][c]) >= 2
-    assert st["launches_execute"] < sp["launches_execute"]

@@ -41,7 +41,7 @@ def test_host_pipeline_matches_single_runs(beta, nbuf):
         assert np.array_equal(hOut[k].numpy(), want[k]), f"step {k}"
 
 
-@pytest.mark.parametrize("flags", [0, B.GMP_FLAG_TC_FUSED])
+@pytest.mark.parametrize("flags", [0, B.GMP_FLAG_SPLIT16])
 def test_execute_replays_from_a_cuda_graph(flags):
     """after one warm-up execute, gemm_mp_execute issues kernels only (the C tile
     descriptors are already on the device), so a captured execute replays to the

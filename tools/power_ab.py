@@ -41,7 +41,7 @@ def timed(fn, seconds, flops):
                 pj_per_flop=round(c["power_w_median"] / (tf * 1e12) * 1e12, 4) if c["power_w_median"] else None)
 
 
-FLAGS = {"default": 0, "single": B.GMP_FLAG_TC_SINGLE, "pair": B.GMP_FLAG_TC_PAIR, "mcast": B.GMP_FLAG_TC_MCAST, "fused": B.GMP_FLAG_TC_FUSED}
+FLAGS = {"default": 0, "single": B.GMP_FLAG_TC_SINGLE, "pair": B.GMP_FLAG_TC_PAIR}
 
 
 def main():
