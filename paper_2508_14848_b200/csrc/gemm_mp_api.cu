@@ -433,6 +433,7 @@ struct CeState {
   cudaEvent_t comm_done = nullptr;                       // end of the last execute's pulls
   bool comm_done_rec = false;
   int* dummy = nullptr;                                  // 1 int, barrier all-reduces
+  bool disabled = false;                                 // IPC unavailable on some rank: NCCL broadcasts
   int live_plans = 0;                                    // plans using this state; at 0 the IPC mappings
                                                          // are closed (an imported allocation stays
                                                          // resident on its owner until every importer
@@ -1259,7 +1260,7 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
     pl->rowc = gc.rowc;
     pl->colc = gc.colc;
     pl->comm_stream = gc.comm_stream;
-    if (!(d.flags & GMP_FLAG_NCCL_BCAST)) {
+    if (!(d.flags & GMP_FLAG_NCCL_BCAST) && !gc.ce->disabled) {
       pl->ce = gc.ce;
       std::lock_guard<std::mutex> lk(g_grid_mu);
       pl->ce->live_plans++;
@@ -1460,18 +1461,28 @@ static gmp_status_t ce_map_peers(gmp_plan_s* pl, uint8_t* ws, cudaStream_t strea
       return fail(GMP_ERR_CUDA, "cuMemGetAddressRange not available");
     range = reinterpret_cast<PFN_memGetAddressRange>(fp);
   }
+  // every rank takes the same decision: a rank that cannot export or map a workspace turns
+  // the copy-engine transport off on all ranks (two all-gathers of flags), which then fall
+  // back to the NCCL broadcasts for this and every later plan on the grid
   CUdeviceptr base = 0;
   size_t sz = 0;
-  if (range(&base, &sz, (CUdeviceptr)(uintptr_t)ws) != CUDA_SUCCESS) return fail(GMP_ERR_CUDA, "cuMemGetAddressRange");
-  struct Rec { cudaIpcMemHandle_t h; int64_t off; int64_t pad; } rec{};
-  GMP_CUDA(cudaIpcGetMemHandle(&rec.h, (void*)(uintptr_t)base));
+  struct Rec { cudaIpcMemHandle_t h; int64_t off; int32_t ok; int32_t pad; } rec{};
+  rec.ok = range(&base, &sz, (CUdeviceptr)(uintptr_t)ws) == CUDA_SUCCESS &&
+           cudaIpcGetMemHandle(&rec.h, (void*)(uintptr_t)base) == cudaSuccess;
+  (void)cudaGetLastError();
   rec.off = (int64_t)((uintptr_t)ws - (uintptr_t)base);
   const int G = pl->P * pl->Q;
   std::vector<uint8_t> all;
   GMP_TRY(allgather_host(pl->ce, pl->world, &rec, sizeof rec, G, all, stream));
   const size_t b16 = (size_t)align_up((int64_t)sizeof(Rec), 16);
-  ce->peer_ws.assign(G, nullptr);
+  bool ok = true;
   for (int r = 0; r < G; ++r) {
+    Rec pr;
+    std::memcpy(&pr, all.data() + r * b16, sizeof pr);
+    ok = ok && pr.ok;
+  }
+  ce->peer_ws.assign(G, nullptr);
+  for (int r = 0; ok && r < G; ++r) {
     Rec pr;
     std::memcpy(&pr, all.data() + r * b16, sizeof pr);
     if (r == pl->d.rank) { ce->peer_ws[r] = ws; continue; }
@@ -1480,10 +1491,30 @@ static gmp_status_t ce_map_peers(gmp_plan_s* pl, uint8_t* ws, cudaStream_t strea
     for (auto& o : ce->opened)
       if (o.first == key) mapped = o.second;
     if (!mapped) {
-      GMP_CUDA(cudaIpcOpenMemHandle(&mapped, pr.h, cudaIpcMemLazyEnablePeerAccess));
+      if (cudaIpcOpenMemHandle(&mapped, pr.h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        (void)cudaGetLastError();
+        ok = false;
+        break;
+      }
       ce->opened.emplace_back(key, mapped);
     }
     ce->peer_ws[r] = (uint8_t*)mapped + pr.off;
+  }
+  int32_t mine[4] = {ok ? 1 : 0, 0, 0, 0};
+  GMP_TRY(allgather_host(pl->ce, pl->world, mine, sizeof mine, G, all, stream));
+  for (int r = 0; r < G; ++r) ok = ok && reinterpret_cast<const int32_t*>(all.data() + r * 16)[0] != 0;
+  if (!ok) {
+    for (auto& o : ce->opened) cudaIpcCloseMemHandle(o.second);
+    ce->opened.clear();
+    ce->peer_ws.clear();
+    ce->ws_for = nullptr;
+    ce->disabled = true;
+    {
+      std::lock_guard<std::mutex> lk(g_grid_mu);
+      ce->live_plans--;
+    }
+    pl->ce = nullptr;   // this plan: NCCL broadcasts (rowc / colc exist)
+    return GMP_OK;
   }
   ce->ws_for = ws;
   return GMP_OK;
@@ -1657,8 +1688,8 @@ extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_byte
   if (oz_prepare(pl->oz, ws, pl->arena_off[GMP_AR_SLICE], pl->arena_slots[GMP_AR_SLICE], (int)nb) != GMP_OK)
     return fail(GMP_ERR_CUDA, "cuTensorMapEncodeTiled (digit arena) failed");
   GMP_TRY(tc_prepare(pl->tc, ws, pl->arena_off, pl->arena_slots, (int)nb));
+  if (pl->ce) GMP_TRY(ce_map_peers(pl, ws, stream));   // may turn the transport off (all ranks)
   if (pl->ce) {
-    GMP_TRY(ce_map_peers(pl, ws, stream));
     // the previous executes' pulls from this workspace have completed on every rank
     // before the packs below overwrite the payload slots
     if (pl->ce->comm_done_rec) GMP_CUDA(cudaStreamWaitEvent(stream, pl->ce->comm_done, 0));
