@@ -1,4 +1,4 @@
-"""Randomised parity sweep (48 fixed seeds): shapes of 1..6 tiles per dimension, nb in
+"""Randomised parity sweep (48 fixed seeds, plus 24 with MXFP4 enabled): shapes of 1..6 tiles per dimension, nb in
 {128, 256, 384, 512}, tolerances from 1e-12 to 0.5, every class mask with FP8 on or
 off, alpha/beta signs and zeros, graded / random / uniform inputs.  Each case runs
 the CUDA path twice through the C ABI -- the product kernels and the SIMT (bitwise)
@@ -15,12 +15,12 @@ from paper_2508_14848_b200 import binding as B
 pytestmark = pytest.mark.gpu
 
 
-def _case(seed):
-    r = np.random.default_rng(1000 + seed)
+def _case(seed, masks=(0b000001, 0b000011, 0b001111, 0b011111, 0b111111, 0b101111, 0b000111), rng_base=1000):
+    r = np.random.default_rng(rng_base + seed)
     nb = int(r.choice([128, 256, 384, 512]))
     mt, nt, kt = (int(x) for x in r.integers(1, 5 if nb >= 384 else 7, size=3))
     tol = float(10.0 ** r.uniform(-10, np.log10(0.5)))
-    mask = int(r.choice([0b000001, 0b000011, 0b001111, 0b011111, 0b111111, 0b101111, 0b000111]))
+    mask = int(r.choice(list(masks)))
     mode = str(r.choice(["graded", "random", "uniform"]))
     E = int(r.integers(0, 48))
     alpha = float(r.choice([1.0, -0.75, 2.0 ** -20, 3.0]))
@@ -30,9 +30,13 @@ def _case(seed):
     return w
 
 
-@pytest.mark.parametrize("seed", range(48))
+# MXFP4 enabled (class 6, NEXT-4): its own 24 seeds (tolerances up to 0.5 put many tiles there)
+MX_MASKS = (0b1111111, 0b1011111, 0b1000001, 0b1001111, 0b1000011)
+
+
+@pytest.mark.parametrize("seed", list(range(48)) + [f"mx{k}" for k in range(24)])
 def test_fuzz_parity(seed):
-    w = _case(seed)
+    w = _case(int(seed[2:]), MX_MASKS, 5000) if isinstance(seed, str) else _case(seed)
     A, Bm, C = w.matrices()
     Cin = C if w.beta != 0.0 else None
     o = run_oracle(A, Bm, Cin, w.nb, w.tol, w.alpha, w.beta, w.class_mask)

@@ -193,7 +193,7 @@ def test_loopback_simt_bitwise_vs_oracle(grid):
 
 
 
-@pytest.mark.parametrize("kind", ["small", "uneven"])
+@pytest.mark.parametrize("kind", ["small", "uneven", "mx4"])
 @pytest.mark.parametrize("sender", [False, True], ids=["receiver", "sender"])
 @pytest.mark.parametrize("grid", [(2, 2), (2, 4), (1, 4)], ids=["2x2", "2x4", "1x4"])
 def test_loopback_balanced_ownership_bitwise(grid, sender, kind):
