@@ -54,9 +54,12 @@ def parse():
     ap.add_argument("--cpu-threads", type=int, default=0, help="oracle threads (0: min(16, cores))")
     ap.add_argument("--flags", type=int, default=0, help="extra GMP_FLAG_* bits (A/B runs)")
     ap.add_argument("--size", type=int, default=0, help="override M=N=K (keeps the config's recipe)")
-    ap.add_argument("--balance", action="store_true",
-                    help="N > 1: precision-aware tile ownership from gemm_mp_balance (NEXT-3) instead of "
-                         "block-cyclic; chosen once from a block-cyclic plan's maps, outside the timed region")
+    ap.add_argument("--ownership", default="auto", choices=["auto", "cyclic", "balanced"],
+                    help="N > 1: tile ownership. cyclic = 2D block-cyclic (PAPER.md:179); balanced = "
+                         "gemm_mp_balance (NEXT-3); auto (default) = balanced when it lowers the model's "
+                         "largest per-rank cost by >= 2 %% (2x4 at cfg3: 1.045 -> 1.001), else cyclic. Chosen "
+                         "once from a block-cyclic plan's maps, outside the timed region")
+    ap.add_argument("--balance", action="store_true", help="same as --ownership balanced")
     ap.add_argument("--sender", action="store_true",
                     help="GMP_FLAG_SENDER_SIDE: hybrid sender-side conversion of SUMMA panels (NEXT-2)")
     return ap.parse_args()
@@ -544,12 +547,14 @@ def main():
         comm = B.gemm_mp_nccl_comm_create(bytes(t.cpu().numpy()), G, rank)
 
     flags = B.GMP_FLAG_TIMING | (B.GMP_FLAG_SENDER_SIDE if a.sender else 0) | a.flags
-    # ---- NEXT-3: tile ownership.  Block-cyclic unless --balance: then the
-    # owners come from gemm_mp_balance on the global maps of one block-cyclic plan (the same
-    # on every rank), and the inputs are generated directly in that layout ----
+    # ---- NEXT-3: tile ownership (--ownership): the owners come from gemm_mp_balance on the
+    # global maps of one block-cyclic plan (the same on every rank), and the inputs are
+    # generated directly in the chosen layout ----
     ro = co = None
     balance = None
-    if G > 1 and a.balance:
+    if a.balance:
+        a.ownership = "balanced"
+    if G > 1 and a.ownership != "cyclic":
         A0, B0, C0 = api.synth_operands(w, P, Q, p, q, device=dev)
         d0 = B.make_desc(w.M, w.N, w.K, w.nb, w.tol, w.alpha, w.beta, w.class_mask, flags, P, Q, rank)
         g0 = api.GemmMP(d0, A0, B0, C0, nccl_comm=comm, device=dev)
@@ -559,10 +564,14 @@ def main():
         torch.cuda.empty_cache()
         t0 = time.perf_counter()
         ro, co, imb = B.gemm_mp_balance(d0, m0["acode"], m0["bcode"])
-        balance = {"imbalance_model_block_cyclic": imb[0], "imbalance_model_balanced": imb[1],
+        use = a.ownership == "balanced" or imb[0] >= 1.02 * imb[1]
+        balance = {"mode": a.ownership, "used": bool(use),
+                   "imbalance_model_block_cyclic": imb[0], "imbalance_model_balanced": imb[1],
                    "host_ms": (time.perf_counter() - t0) * 1e3,
                    "rows_per_process_row": [int((ro == x).sum()) for x in range(P)],
                    "cols_per_process_col": [int((co == x).sum()) for x in range(Q)]}
+        if not use:
+            ro = co = None
     # ---- inputs: local parts, generated on the device (N1) ----
     A, Bm, C = api.synth_operands(w, P, Q, p, q, ro, co, device=dev)
     lr, lc = api.local_c_shape(w, P, Q, p, q, ro, co)
