@@ -787,6 +787,9 @@ def main():
             "mix": {"tiles_a": st["tiles_a"], "tiles_b": st["tiles_b"], "tiles_c": st["tiles_c"],
                     "pairs": st["pairs"]},
             "class_ms_rank0": class_ms,
+            "exec_other_ms_rank0": {"before_first_class_launch": st["exec_other_ms"][0],
+                                    "between_class_launches": st["exec_other_ms"][1],
+                                    "finalize": st["exec_other_ms"][2]},
             "class_roofline_rank0": {gmp_class_name(c): {"achieved": ach[c], "peak": cpk[c],
                                                         "frac": ach[c] / cpk[c] if cpk[c] else None}
                                      for c in range(NCLS) if class_ms[c] > 0},

@@ -161,6 +161,10 @@ typedef struct {
   double class_ms[7];                         /* GMP_FLAG_TIMING: device ms of the class-c tile-GEMM
                                                  launches of the last execute (waits for them) */
   int32_t class_launches[7];                  /* launches per class in one execute             */
+  double exec_other_ms[3];                    /* GMP_FLAG_TIMING: device ms of the last execute outside
+                                                 the class launches: before the first (W0, uploads),
+                                                 between them (SUMMA waits, gaps), after the last
+                                                 (C-finalize)                                     */
 } gmp_stats_t;
 
 /* Device scratch needed by gemm_mp_plan (tile statistics + maps; KB-sized).     */

@@ -62,7 +62,8 @@ class gmp_stats_t(ct.Structure):
                 ("recv_bytes_local", ct.c_int64), ("workspace_bytes", ct.c_int64),
                 ("steps", ct.c_int32), ("launches_execute", ct.c_int32),
                 ("launches_plan", ct.c_int32), ("launches_convert", ct.c_int32),
-                ("class_ms", ct.c_double * 7), ("class_launches", ct.c_int32 * 7)]
+                ("class_ms", ct.c_double * 7), ("class_launches", ct.c_int32 * 7),
+                ("exec_other_ms", ct.c_double * 3)]
 
     def as_dict(self):
         d = {}

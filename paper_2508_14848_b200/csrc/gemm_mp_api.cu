@@ -1272,7 +1272,7 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
   for (auto& e : pl->step_ev) GMP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   GMP_CUDA(cudaEventCreateWithFlags(&pl->done_ev, cudaEventDisableTiming));
   if (d.flags & GMP_FLAG_TIMING) {
-    pl->launch_ev.resize(2 * pl->launches.size());
+    pl->launch_ev.resize(2 * pl->launches.size() + 2);   // + execute begin, execute end
     for (auto& e : pl->launch_ev) GMP_CUDA(cudaEventCreate(&e));
   }
   if (pl->lb) {
@@ -1763,6 +1763,8 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
     pl->ctd_ws = ws;
   }
   const CTileDesc* dct = (const CTileDesc*)(ws + pl->off_ctd);
+  const size_t nlev = 2 * pl->launches.size();
+  if (!pl->launch_ev.empty()) GMP_CUDA(cudaEventRecord(pl->launch_ev[nlev], stream));   // execute begins
   if (!pl->acc_init_idx.empty()) {
     k_acc_init<<<dim3(grid_for(nb2, 1) / 4 + 1, (unsigned)pl->acc_init_idx.size()), 256, 0, stream>>>(
         dct, (const int32_t*)(ws + pl->off_accinit), ws, nb2, pl->d.beta);
@@ -1862,6 +1864,7 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
         dct, ws, mb, (int16_t*)(ws + pl->off_cscale), Cuser, ldc, (int)nb);
     GMP_CUDA(cudaGetLastError());
   }
+  if (!pl->launch_ev.empty()) GMP_CUDA(cudaEventRecord(pl->launch_ev[nlev + 1], stream));   // execute ends
   GMP_TRY(record_done(pl, stream));
   pl->executed = true;
   return GMP_OK;
@@ -1975,6 +1978,23 @@ extern "C" gmp_status_t gemm_mp_get_tile(gmp_plan_t pl, char which, int64_t ti, 
 extern "C" gmp_status_t gemm_mp_get_stats(gmp_plan_t pl, gmp_stats_t* out) {
   if (!pl || !out) return fail(GMP_ERR_ARG, "NULL argument");
   for (int c = 0; c < NC; ++c) pl->st.class_ms[c] = 0.0;
+  for (int k = 0; k < 3; ++k) pl->st.exec_other_ms[k] = 0.0;
+  if (pl->executed && !pl->launch_ev.empty() && !pl->launches.empty()) {
+    // where execute's time goes outside the class launches: before the first one (W0 /
+    // table uploads), between launches (waits on SUMMA steps, launch gaps), after the last
+    // one (C-finalize)
+    const size_t nl = pl->launches.size(), nlev = 2 * nl;
+    float ms = 0.f;
+    GMP_CUDA(cudaEventSynchronize(pl->launch_ev[nlev + 1]));
+    GMP_CUDA(cudaEventElapsedTime(&ms, pl->launch_ev[nlev], pl->launch_ev[0]));
+    pl->st.exec_other_ms[0] = ms;
+    for (size_t li = 0; li + 1 < nl; ++li) {
+      GMP_CUDA(cudaEventElapsedTime(&ms, pl->launch_ev[2 * li + 1], pl->launch_ev[2 * li + 2]));
+      pl->st.exec_other_ms[1] += ms;
+    }
+    GMP_CUDA(cudaEventElapsedTime(&ms, pl->launch_ev[nlev - 1], pl->launch_ev[nlev + 1]));
+    pl->st.exec_other_ms[2] = ms;
+  }
   if (pl->executed && !pl->launch_ev.empty()) {
     for (size_t li = 0; li < pl->launches.size(); ++li) {
       float ms = 0.f;

@@ -45,7 +45,8 @@ def main():
     out = torch.empty(n, n, dtype=torch.float64, device=dev)
     t = n // nb
     res = {}
-    for flags, tag in [(0, "fp32_tensor_bf16x9"), (B.GMP_FLAG_FP32_FFMA, "fp32_ffma2")]:
+    for flags, tag in [(0, "fp32_tensor_bf16x6"), (B.GMP_FLAG_FP32_X9, "fp32_tensor_bf16x9"),
+                       (B.GMP_FLAG_FP32_FFMA, "fp32_ffma2")]:
         rows = []
         for d in RATIOS:
             maps = pm.paper_maps(t, t, t, d, 5000 + d)
