@@ -2040,10 +2040,17 @@ extern "C" gmp_status_t gemm_mp_nccl_comm_destroy(void* comm) {
       ncclCommDestroy(g.colc);
       if (g.ce) {
         for (auto& o : g.ce->opened) cudaIpcCloseMemHandle(o.second);
-        if (g.ce->comm_done) cudaEventDestroy(g.ce->comm_done);
-        if (g.ce->dummy) cudaFree(g.ce->dummy);
-        if (g.ce->xbuf) cudaFree(g.ce->xbuf);
-        delete g.ce;
+        g.ce->opened.clear();
+        g.ce->peer_ws.clear();
+        g.ce->disabled = true;
+        // plans still alive (destroyed after their communicator) keep a pointer to this
+        // state: it is then left allocated (their destroy only decrements a counter)
+        if (g.ce->live_plans <= 0) {
+          if (g.ce->comm_done) cudaEventDestroy(g.ce->comm_done);
+          if (g.ce->dummy) cudaFree(g.ce->dummy);
+          if (g.ce->xbuf) cudaFree(g.ce->xbuf);
+          delete g.ce;
+        }
       }
       cudaStreamDestroy(g.comm_stream);
       g_grid_comms.erase(g_grid_comms.begin() + k);
