@@ -787,6 +787,8 @@ def main():
             "mix": {"tiles_a": st["tiles_a"], "tiles_b": st["tiles_b"], "tiles_c": st["tiles_c"],
                     "pairs": st["pairs"]},
             "class_ms_rank0": class_ms,
+            "convert_ms_rank0": {"tables_barriers": st["convert_ms"][0], "pack": st["convert_ms"][1],
+                                 "shadows": st["convert_ms"][2], "splits": st["convert_ms"][3]},
             "exec_other_ms_rank0": {"before_first_class_launch": st["exec_other_ms"][0],
                                     "between_class_launches": st["exec_other_ms"][1],
                                     "finalize": st["exec_other_ms"][2]},

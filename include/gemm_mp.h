@@ -165,6 +165,9 @@ typedef struct {
                                                  the class launches: before the first (W0, uploads),
                                                  between them (SUMMA waits, gaps), after the last
                                                  (C-finalize)                                     */
+  double convert_ms[4];                       /* GMP_FLAG_TIMING: device ms of the last convert: table
+                                                 uploads + barriers, pack, shadows (incl. MXFP4 and the
+                                                 step-0 pull issue), FP32 splits / FP64 digit planes */
 } gmp_stats_t;
 
 /* Device scratch needed by gemm_mp_plan (tile statistics + maps; KB-sized).     */

@@ -63,7 +63,7 @@ class gmp_stats_t(ct.Structure):
                 ("steps", ct.c_int32), ("launches_execute", ct.c_int32),
                 ("launches_plan", ct.c_int32), ("launches_convert", ct.c_int32),
                 ("class_ms", ct.c_double * 7), ("class_launches", ct.c_int32 * 7),
-                ("exec_other_ms", ct.c_double * 3)]
+                ("exec_other_ms", ct.c_double * 3), ("convert_ms", ct.c_double * 4)]
 
     def as_dict(self):
         d = {}

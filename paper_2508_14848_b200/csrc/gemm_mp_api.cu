@@ -288,6 +288,7 @@ struct gmp_plan_s {
           off_cscale = 0, off_tc = 0, ws_bytes = 0;
   TcTables tc;
   std::vector<cudaEvent_t> launch_ev;    // GMP_FLAG_TIMING: start/stop per class launch
+  std::vector<cudaEvent_t> conv_ev;      // GMP_FLAG_TIMING: convert begin / tables / pack / shadows / end
   uint8_t* ws = nullptr;
   bool converted = false;
   bool executed = false;
@@ -1274,6 +1275,8 @@ extern "C" gmp_status_t gemm_mp_plan(const gmp_desc_t* desc, const double* A, in
   if (d.flags & GMP_FLAG_TIMING) {
     pl->launch_ev.resize(2 * pl->launches.size() + 2);   // + execute begin, execute end
     for (auto& e : pl->launch_ev) GMP_CUDA(cudaEventCreate(&e));
+    pl->conv_ev.resize(5);
+    for (auto& e : pl->conv_ev) GMP_CUDA(cudaEventCreate(&e));
   }
   if (pl->lb) {
     std::lock_guard<std::mutex> lk(pl->lb->mu);
@@ -1665,6 +1668,11 @@ extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_byte
   pl->ws = ws;
   pl->ctd_ldc = -1;   // the workspace is (re)claimed: execute re-uploads the C tile descriptors
   const int64_t nb = pl->d.nb;
+  auto cev = [&](int k) -> gmp_status_t {
+    if (!pl->conv_ev.empty()) GMP_CUDA(cudaEventRecord(pl->conv_ev[k], stream));
+    return GMP_OK;
+  };
+  GMP_TRY(cev(0));
   // job tables
   Upload tables;
   std::vector<ShadowJob> allsh = pl->shadow_local;
@@ -1695,12 +1703,14 @@ extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_byte
     if (pl->ce->comm_done_rec) GMP_CUDA(cudaStreamWaitEvent(stream, pl->ce->comm_done, 0));
     GMP_TRY(ce_barrier(pl, stream));
   }
+  GMP_TRY(cev(1));
   // S3 pack
   if (!pl->pack.empty()) {
     dim3 grid((unsigned)((nb / 64) * (nb / 64)), (unsigned)pl->pack.size());
     k_pack<<<grid, 256, 0, stream>>>((const PackJob*)(ws + pl->off_pack), ws, (int)nb);
     GMP_CUDA(cudaGetLastError());
   }
+  GMP_TRY(cev(2));
   // S5 shadows of local tiles
   GMP_TRY(launch_shadows((const ShadowJob*)(ws + pl->off_shadow), pl->shadow_local, ws, (int)nb, stream));
   // MXFP4: packs of MXFP4 tiles and local shadows into MXFP4 (after k_pack: shadows read stored payloads)
@@ -1718,6 +1728,7 @@ extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_byte
     GMP_TRY(issue_comm_step(pl, ws, 0));
     pl->step0_issued = true;
   }
+  GMP_TRY(cev(3));
   if (!pl->split_local.empty()) {
     k_split<<<dim3((unsigned)((nb / 64) * (nb / 64)), (unsigned)pl->split_local.size()), 256, 0, stream>>>(
         (const SplitJob*)(ws + pl->off_split), ws, (int)nb);
@@ -1728,6 +1739,7 @@ extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_byte
         (const SliceJob*)(ws + pl->off_slice), ws, (int)nb);
     GMP_CUDA(cudaGetLastError());
   }
+  GMP_TRY(cev(4));
   GMP_TRY(record_done(pl, stream));
   pl->converted = true;
   return GMP_OK;
@@ -1979,6 +1991,15 @@ extern "C" gmp_status_t gemm_mp_get_stats(gmp_plan_t pl, gmp_stats_t* out) {
   if (!pl || !out) return fail(GMP_ERR_ARG, "NULL argument");
   for (int c = 0; c < NC; ++c) pl->st.class_ms[c] = 0.0;
   for (int k = 0; k < 3; ++k) pl->st.exec_other_ms[k] = 0.0;
+  for (int k = 0; k < 4; ++k) pl->st.convert_ms[k] = 0.0;
+  if (pl->converted && pl->conv_ev.size() == 5) {
+    GMP_CUDA(cudaEventSynchronize(pl->conv_ev[4]));
+    for (int k = 0; k < 4; ++k) {
+      float ms = 0.f;
+      GMP_CUDA(cudaEventElapsedTime(&ms, pl->conv_ev[k], pl->conv_ev[k + 1]));
+      pl->st.convert_ms[k] = ms;
+    }
+  }
   if (pl->executed && !pl->launch_ev.empty() && !pl->launches.empty()) {
     // where execute's time goes outside the class launches: before the first one (W0 /
     // table uploads), between launches (waits on SUMMA steps, launch gaps), after the last
@@ -2166,6 +2187,7 @@ extern "C" void gemm_mp_destroy(gmp_plan_t pl) {
   if (pl->packed_ev) cudaEventDestroy(pl->packed_ev);
   if (pl->done_ev) cudaEventDestroy(pl->done_ev);
   for (auto& e : pl->launch_ev) if (e) cudaEventDestroy(e);
+  for (auto& e : pl->conv_ev) if (e) cudaEventDestroy(e);
   tc_release(pl->tc);
   if (pl->lb) {
     {
