@@ -92,6 +92,9 @@ typedef enum {
 #define GMP_FLAG_SPLIT_BN128 16384u /* FP32 class (BF16x6) always at BN = 128 (128-byte K blocks); default
                                  BN = 256 with 64-byte K blocks when every W of the launch is binary32
                                  and nb % 256 == 0 (fewer staged bytes per flop)                       */
+#define GMP_FLAG_SEPARATE_MAXABS 32768u /* max|W| of every binary32-W C tile in k_c_maxabs (one extra W
+                                 read); default: the last 1-SM tcgen05 launch of a tile emits it from
+                                 its registers (same value: max is order-free)                        */
 #define GMP_FLAG_TC_PAIR 32u /* opt-in: FP16/BF16/E4M3/E5M2 launches whose C tiles fold into binary32 W
                                  and whose nb is a multiple of 256 run on SM pairs (tcgen05 cta_group::2,
                                  256 x 256 sub-tiles, half the B bytes per SM), rastered by C tile row

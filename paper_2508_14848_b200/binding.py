@@ -35,6 +35,7 @@ GMP_FLAG_SPLIT16 = 2048
 GMP_FLAG_NCCL_BCAST = 4096
 GMP_FLAG_DYN_SCHED = 8192
 GMP_FLAG_SPLIT_BN128 = 16384
+GMP_FLAG_SEPARATE_MAXABS = 32768
 STATUS = ["GMP_OK", "GMP_ERR_ARG", "GMP_ERR_NOT_DIVISIBLE", "GMP_ERR_MAP_SHAPE", "GMP_ERR_NONFINITE",
           "GMP_ERR_GRID", "GMP_ERR_WORKSPACE", "GMP_ERR_STATE", "GMP_ERR_CUDA", "GMP_ERR_NCCL",
           "GMP_ERR_UNSUPPORTED"]

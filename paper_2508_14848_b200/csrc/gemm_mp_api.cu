@@ -278,6 +278,9 @@ struct gmp_plan_s {
   std::vector<PairDesc> pairs;
   std::vector<int32_t> order;            // raster orders of the SM-pair launches (flat -> item * S + sub)
   std::vector<Launch> launches;
+  std::vector<int32_t> maxabs_idx;        // binary32-W C tiles whose max|W| k_c_maxabs computes (the others:
+                                          // their last tcgen05 launch, WorkItem.pad bit 1)
+  int64_t off_maxidx = 0;
   std::vector<int32_t> acc_init_idx;      // local C tiles whose W0 k_acc_init writes (the others: their
                                           // first tile-GEMM launch, WorkItem.pad bit 0)
   int64_t off_accinit = 0;
@@ -682,6 +685,7 @@ static void build_tables(gmp_plan_s* pl) {
   pl->off_order = o; o = align_up(o + n_items * (nb / 128) * (nb / 128) * 4, 1024);
   pl->off_maxbits = o; o = align_up(o + nCl * 8, 1024);
   pl->off_accinit = o; o = align_up(o + nCl * 4, 1024);
+  pl->off_maxidx = o; o = align_up(o + nCl * 4, 1024);
   pl->off_cscale = o; o = align_up(o + nCl * 2, 1024);
   pl->off_tc = o; o = align_up(o + 1024, 1024);
   pl->off_sched = o; o = align_up(o + 4 * (int64_t)(steps * (NC + 1) + 16), 1024);   // scheduler counters per launch
@@ -1033,6 +1037,28 @@ static void build_tables(gmp_plan_s* pl) {
     for (int64_t k = 0; k < nCl; ++k)
       if (!done[k]) pl->acc_init_idx.push_back((int32_t)k);
   }
+  // ---- max|W| for the C-finalize scale: the LAST launch that touches a binary32-W C tile
+  // emits it from the W rows it holds in registers when that launch is a 1-SM tcgen05
+  // kernel (WorkItem.pad bit 1, atomicMax); k_c_maxabs covers the other tiles ----
+  pl->maxabs_idx.clear();
+  {
+    std::vector<uint8_t> seen(nCl, 0);
+    for (size_t li = pl->launches.size(); li-- > 0;) {
+      const Launch& L = pl->launches[li];
+      const int64_t iend = li + 1 < pl->launches.size() ? pl->launches[li + 1].ibeg : (int64_t)pl->items.size();
+      const bool can = (L.kind == 1 || L.kind == 3) && !(d.flags & GMP_FLAG_SEPARATE_MAXABS);
+      for (int64_t q = L.ibeg; q < iend; ++q) {
+        WorkItem& wi = pl->items[q];
+        if (seen[wi.ctile]) continue;
+        seen[wi.ctile] = 1;
+        if (pl->ctd[wi.ctile].code == 0) continue;            // binary64 W: no scale
+        if (can) wi.pad |= 2;
+        else pl->maxabs_idx.push_back(wi.ctile);
+      }
+    }
+    for (int64_t k = 0; k < nCl; ++k)
+      if (!seen[k] && pl->ctd[k].code != 0) pl->maxabs_idx.push_back((int32_t)k);
+  }
 
   // ---- stats ----
   gmp_stats_t& st = pl->st;
@@ -1052,7 +1078,8 @@ static void build_tables(gmp_plan_s* pl) {
   st.recv_bytes_local = recv_bytes;
   st.workspace_bytes = pl->ws_bytes;
   st.steps = steps;
-  int nl = (pl->acc_init_idx.empty() ? 2 : 3) + (int)pl->launches.size();  // [acc init], tile-GEMMs, maxabs, finalize
+  // [acc init], tile-GEMMs, [maxabs], finalize
+  int nl = (pl->acc_init_idx.empty() ? 1 : 2) + (pl->maxabs_idx.empty() ? 0 : 1) + (int)pl->launches.size();
   auto nsh = [](const std::vector<ShadowJob>& v) {
     int64_t t = 0;
     for (const auto& j : v) t += j.transpose;
@@ -1683,6 +1710,7 @@ extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_byte
   for (auto& v : pl->slice_step) allsl.insert(allsl.end(), v.begin(), v.end());
   tables.add(ws + pl->off_pack, pl->pack.data(), (int64_t)(pl->pack.size() * sizeof(PackJob)));
   tables.add(ws + pl->off_accinit, (const uint8_t*)pl->acc_init_idx.data(), (int64_t)(pl->acc_init_idx.size() * 4));
+  tables.add(ws + pl->off_maxidx, (const uint8_t*)pl->maxabs_idx.data(), (int64_t)(pl->maxabs_idx.size() * 4));
   tables.add(ws + pl->off_shadow, allsh.data(), (int64_t)(allsh.size() * sizeof(ShadowJob)));
   std::vector<MxJob> allmx = pl->mx_local;
   for (auto& v : pl->mx_step) allmx.insert(allmx.end(), v.begin(), v.end());
@@ -1777,6 +1805,10 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
   const CTileDesc* dct = (const CTileDesc*)(ws + pl->off_ctd);
   const size_t nlev = 2 * pl->launches.size();
   if (!pl->launch_ev.empty()) GMP_CUDA(cudaEventRecord(pl->launch_ev[nlev], stream));   // execute begins
+  if (nCl) {   // max|W| bits: atomicMax targets of the last tcgen05 launches and of k_c_maxabs
+    pl->tc.maxbits = (unsigned long long*)(ws + pl->off_maxbits);
+    GMP_CUDA(cudaMemsetAsync(pl->tc.maxbits, 0, nCl * 8, stream));
+  }
   if (!pl->acc_init_idx.empty()) {
     k_acc_init<<<dim3(grid_for(nb2, 1) / 4 + 1, (unsigned)pl->acc_init_idx.size()), 256, 0, stream>>>(
         dct, (const int32_t*)(ws + pl->off_accinit), ws, nb2, pl->d.beta);
@@ -1869,9 +1901,11 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
   if (ready) cudaEventDestroy(ready);
   if (nCl) {
     unsigned long long* mb = (unsigned long long*)(ws + pl->off_maxbits);
-    GMP_CUDA(cudaMemsetAsync(mb, 0, nCl * 8, stream));
-    k_c_maxabs<<<dim3(grid_for(nb2, 4) / 8 + 1, (unsigned)nCl), 256, 0, stream>>>(dct, ws, nb2, mb);
-    GMP_CUDA(cudaGetLastError());
+    if (!pl->maxabs_idx.empty()) {
+      k_c_maxabs<<<dim3(grid_for(nb2, 4) / 8 + 1, (unsigned)pl->maxabs_idx.size()), 256, 0, stream>>>(
+          dct, (const int32_t*)(ws + pl->off_maxidx), ws, nb2, mb);
+      GMP_CUDA(cudaGetLastError());
+    }
     k_c_finalize<<<dim3((unsigned)(nb / FIN_ROWS), (unsigned)nCl), 256, 0, stream>>>(
         dct, ws, mb, (int16_t*)(ws + pl->off_cscale), Cuser, ldc, (int)nb);
     GMP_CUDA(cudaGetLastError());

@@ -426,9 +426,12 @@ __global__ void __launch_bounds__(256) k_acc_init(const CTileDesc* __restrict__ 
 // S7 C-finalize: pass 1 maxabs(W) per tile (bit-pattern atomicMax on |x|),
 // pass 2 encode into the C class with the scale of maxabs, decode to user C.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_c_maxabs(const CTileDesc* __restrict__ ct, const uint8_t* ws,
-                                                  int64_t n, unsigned long long* maxbits) {
-  const CTileDesc c = ct[blockIdx.y];
+// (pass 1 runs over the tiles listed in idx: the ones whose last tile-GEMM launch does not
+// emit max|W| itself, WorkItem.pad bit 1; maxbits is zeroed before the first launch)
+__global__ void __launch_bounds__(256) k_c_maxabs(const CTileDesc* __restrict__ ct, const int32_t* __restrict__ idx,
+                                                  const uint8_t* ws, int64_t n, unsigned long long* maxbits) {
+  const int32_t k = idx[blockIdx.y];
+  const CTileDesc c = ct[k];
   if (c.code == 0) return;                      // FP64 C tiles carry no scale
   float m = 0.f;
   for (int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; e < n;
@@ -438,7 +441,7 @@ __global__ void __launch_bounds__(256) k_c_maxabs(const CTileDesc* __restrict__ 
   }
   for (int off = 16; off >= 1; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
   if ((threadIdx.x & 31) == 0 && m > 0.f)
-    atomicMax(maxbits + blockIdx.y, (unsigned long long)__double_as_longlong((double)m));
+    atomicMax(maxbits + k, (unsigned long long)__double_as_longlong((double)m));
 }
 
 // one CTA per FP_ROWS rows of a C tile, threads along the row (coalesced user C

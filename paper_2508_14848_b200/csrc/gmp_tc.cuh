@@ -202,7 +202,8 @@ __device__ __forceinline__ void tc_epilogue(const WorkItem* __restrict__ items, 
                                             uint8_t* __restrict__ ws, int nb, double alpha, double beta,
                                             uint32_t tmem_base, uint64_t* tfull, uint64_t* tempty, int warp,
                                             int lane, const int32_t* __restrict__ order = nullptr,
-                                            const TcSched sc = TcSched()) {
+                                            const TcSched sc = TcSched(),
+                                            unsigned long long* __restrict__ maxbits = nullptr) {
   // epilogue: 8 warps; warp w reads TMEM lanes 32*(w%4)..+31 (= tile rows) and
   // half (w-2)/4 of the BN columns.  binary32 W: the W row segment lives in
   // registers for the whole item (one read + one write per item instead of
@@ -257,6 +258,13 @@ __device__ __forceinline__ void tc_epilogue(const WorkItem* __restrict__ items, 
 #pragma unroll
       for (int v = 0; v < HC / 4; ++v)
         reinterpret_cast<float4*>(wrow)[v] = make_float4(accr[4 * v], accr[4 * v + 1], accr[4 * v + 2], accr[4 * v + 3]);
+      if (w.pad & 2) {   // last launch of this C tile: max|W| for the finalize scale (S7)
+        float m = 0.f;
+#pragma unroll
+        for (int v = 0; v < HC; ++v) m = fmaxf(m, fabsf(accr[v]));
+        for (int off = 16; off >= 1; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+        if (lane == 0 && m > 0.f) atomicMax(maxbits + w.ctile, (unsigned long long)__double_as_longlong((double)m));
+      }
     } else if constexpr (HC <= 64) {
       // binary64 W, BN <= 128: the W row segment lives in registers for the item
       double* wrow = reinterpret_cast<double*>(ws + ct.w_off) + rowoff;
@@ -364,7 +372,8 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
            const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
            const WorkItem* __restrict__ items, int64_t nitems, const PairDesc* __restrict__ pairs,
            const CTileDesc* __restrict__ ctiles, uint8_t* __restrict__ ws, int nb, double alpha, double beta,
-           const int32_t* __restrict__ order, int* __restrict__ sched_counter) {
+           const int32_t* __restrict__ order, int* __restrict__ sched_counter,
+           unsigned long long* __restrict__ maxbits) {
   constexpr int NP = tc_np<C>(), ST = tc_stages<C>();
   constexpr bool MX = (C == GMP_MX);       // MXFP4: 4-bit elements + scale-factor chunks per stage
   static_assert(!MX || BN == 128, "MXFP4 runs at BN = 128 (TMEM: 2 x 128 accumulator + scale columns)");
@@ -514,7 +523,7 @@ k_tc_class(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
     }
   } else {
     tc_epilogue<BN>(items, nitems, pairs, ctiles, ws, nb, alpha, beta, tmem_base, tfull, tempty, warp, lane, order,
-                    sc);
+                    sc, maxbits);
   }
   tc_fence_before();
   __syncthreads();
@@ -541,6 +550,7 @@ struct TcTables {
   CUtensorMap splitA64, splitB64;                   // split arena, 64-byte x {128, 256}-row boxes (SW64)
   bool ready[GMP_NARENA] = {};
   int nb = 0;
+  unsigned long long* maxbits = nullptr;   // per-C-tile max|W| bits of the current execute (items with pad bit 1)
 };
 
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -642,7 +652,7 @@ inline gmp_status_t tc_launch_t(TcTables& t, const WorkItem* it, int64_t n, cons
   const CUtensorMap& mb = (C == TC_SPLIT6W) ? t.splitB64 : (BN == 128 ? t.mapB128[mi] : t.mapB[mi]);
   k_tc_class<C, BN><<<grid, TC_THREADS, smem, s>>>(ma, mb, t.mapA[m2],
                                                     BN == 128 ? t.mapB128[m2] : t.mapB[m2], it, n, pd, ct,
-                                                    ws, nb, alpha, beta, order, counter);
+                                                    ws, nb, alpha, beta, order, counter, t.maxbits);
   return cudaGetLastError() == cudaSuccess ? GMP_OK : GMP_ERR_CUDA;
 }
 

@@ -329,3 +329,21 @@ def test_explicit_fp32_c_map_at_extreme_scales():
     assert (o["ccode"] == 0).all() and np.array_equal(g.maps()["ccode"], o["ccode"])
     assert np.isfinite(out).all()
     assert np.linalg.norm(out - o["C"]) / np.linalg.norm(o["C"]) <= 1e-13
+
+
+@pytest.mark.parametrize("nb,beta,seed,mask", [(256, 0.5, 42, 0b1111111), (128, 1.0, 45, 0b0111111),
+                                               (256, 0.0, 46, 0b0011111)])
+def test_fused_maxabs_bitwise_vs_separate(nb, beta, seed, mask):
+    """S7 pass 1: max|W| of a binary32-W C tile is emitted by its last tcgen05 launch (atomicMax
+    on the register copy of W); GMP_FLAG_SEPARATE_MAXABS re-reads W in k_c_maxabs.  The max is
+    independent of the order, so C (and its scales) are bit-identical; one launch fewer"""
+    w = gmp_inputs.small_workload(3 * nb, 2 * nb, 4 * nb, nb, 1e-3, mode="random", E=36, beta=beta,
+                                  class_mask=mask, seed=seed)
+    A, Bm, C = w.matrices()
+    g, (out,) = run_gpu(A, Bm, C, nb, w.tol, w.alpha, w.beta, w.class_mask)
+    g2, (out2,) = run_gpu(A, Bm, C, nb, w.tol, w.alpha, w.beta, w.class_mask, flags=B.GMP_FLAG_SEPARATE_MAXABS)
+    assert np.array_equal(out, out2)
+    assert g.stats()["launches_execute"] <= g2.stats()["launches_execute"]
+    o = run_oracle(A, Bm, C, nb, w.tol, w.alpha, w.beta, w.class_mask)
+    ok, rel = c_parity(out, o["C"], o["ccode"], o["cscale"], nb, w.K, False)
+    assert ok, rel
