@@ -431,8 +431,8 @@ k_mn(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
 // 128x64 sub-tile, 8 warps (4 x 2), warp tile 32x32 = 2 m16 x 4 n8 MMA tiles,
 // binary64 accumulation in registers, 2 CTAs per SM; MN-major payloads, BK = 16 k-rows per
 // stage through a 4-stage cp.async ring into As[k][m] / Bs[k][n] rows whose
-// pitch is 32 B mod 128 B, so the fragment loads (per half-warp: 4 k-rows x 4
-// consecutive m) fall in four distinct 32-byte bank groups.
+// pitch is 32 B mod 128 B, so the 16-byte fragment loads (per 8-lane phase: 4 k-rows x
+// 2 consecutive 16-byte chunks) fall in eight distinct 16-byte bank groups.
 // The accumulation order inside a DMMA is the hardware's: the parity bound is
 // the all-FP64 1e-13 relative Frobenius.
 // ---------------------------------------------------------------------------
@@ -532,20 +532,35 @@ k_dmma(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
     const double* As = reinterpret_cast<const double*>(sm + cstage * STAGE);
     const double* Bs = As + BK * AP;
     if (++cstage == ST) cstage = 0;
+    // fragment permutation (bitwise neutral: every output is the same k-ordered DMMA dot
+    // product): MMA rows g / g+8 of an m16 tile are sub-tile rows 2g / 2g+1, MMA column g of
+    // n8 tiles 2J / 2J+1 is column 16J + 2g / 16J + 2g + 1 -- each fragment pair is one
+    // 16-byte LDS.128 (half the shared-load instructions of per-element loads)
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 16) {
       double a[2][8];
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int r = 0; r < 8; ++r) a[i][r] = As[(kk + t + 4 * (r >> 1)) * AP + wm + i * 16 + g + 8 * (r & 1)];
+        for (int q = 0; q < 4; ++q) {
+          const double2 x = *reinterpret_cast<const double2*>(As + (kk + t + 4 * q) * AP + wm + i * 16 + 2 * g);
+          a[i][2 * q] = x.x;
+          a[i][2 * q + 1] = x.y;
+        }
 #pragma unroll
-      for (int j = 0; j < NJ; ++j) {
-        double b[4];
+      for (int J = 0; J < NJ / 2; ++J) {
+        double b0[4], b1[4];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) b[r] = Bs[(kk + t + 4 * r) * BP + wn + j * 8 + g];
+        for (int r = 0; r < 4; ++r) {
+          const double2 x = *reinterpret_cast<const double2*>(Bs + (kk + t + 4 * r) * BP + wn + J * 16 + 2 * g);
+          b0[r] = x.x;
+          b1[r] = x.y;
+        }
 #pragma unroll
-        for (int i = 0; i < 2; ++i) dmma16816(acc[i][j], a[i], b);
+        for (int i = 0; i < 2; ++i) {
+          dmma16816(acc[i][2 * J], a[i], b0);
+          dmma16816(acc[i][2 * J + 1], a[i], b1);
+        }
       }
     }
     if (++cslice == nsl) {
@@ -557,29 +572,38 @@ k_dmma(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
       if (cpair < it.pcnt && pairs[it.pbeg + cpair].fexp == pd.fexp) continue;
       const double f64 = ldexp_fast(alpha, pd.fexp);
       const float f32 = __double2float_rn(f64);
+      // lane (g, t), half hv: sub-tile row wm + 16i + 2g + hv, columns wn + 16J + 4t + 0..3
+      // = {acc[i][2J][2hv], acc[i][2J+1][2hv], acc[i][2J][2hv+1], acc[i][2J+1][2hv+1]}
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int j = 0; j < NJ; ++j)
+        for (int J = 0; J < NJ / 2; ++J)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int r = it.m0 + wm + i * 16 + g + 8 * h;
-            const int64_t e = (int64_t)r * nb + it.n0 + wn + j * 8 + 2 * t;
+          for (int hv = 0; hv < 2; ++hv) {
+            const int r = it.m0 + wm + i * 16 + 2 * g + hv;
+            const int64_t e = (int64_t)r * nb + it.n0 + wn + J * 16 + 4 * t;
+            double* p0 = acc[i][2 * J];
+            double* p1 = acc[i][2 * J + 1];
+            const double x0 = p0[2 * hv], x1 = p1[2 * hv], x2 = p0[2 * hv + 1], x3 = p1[2 * hv + 1];
             if (ct.code == 0) {
               double2* w = reinterpret_cast<double2*>(reinterpret_cast<double*>(ws + ct.w_off) + e);
-              double2 v = *w;
-              v.x = __fma_rn(f64, acc[i][j][2 * h], v.x);
-              v.y = __fma_rn(f64, acc[i][j][2 * h + 1], v.y);
-              *w = v;
+              double2 v = w[0], u = w[1];
+              v.x = __fma_rn(f64, x0, v.x);
+              v.y = __fma_rn(f64, x1, v.y);
+              u.x = __fma_rn(f64, x2, u.x);
+              u.y = __fma_rn(f64, x3, u.y);
+              w[0] = v;
+              w[1] = u;
             } else {
-              float2* w = reinterpret_cast<float2*>(reinterpret_cast<float*>(ws + ct.w_off) + e);
-              float2 v = *w;
-              v.x = __fmaf_rn(f32, __double2float_rn(acc[i][j][2 * h]), v.x);
-              v.y = __fmaf_rn(f32, __double2float_rn(acc[i][j][2 * h + 1]), v.y);
+              float4* w = reinterpret_cast<float4*>(reinterpret_cast<float*>(ws + ct.w_off) + e);
+              float4 v = *w;
+              v.x = __fmaf_rn(f32, __double2float_rn(x0), v.x);
+              v.y = __fmaf_rn(f32, __double2float_rn(x1), v.y);
+              v.z = __fmaf_rn(f32, __double2float_rn(x2), v.z);
+              v.w = __fmaf_rn(f32, __double2float_rn(x3), v.w);
               *w = v;
             }
-            acc[i][j][2 * h] = 0.0;
-            acc[i][j][2 * h + 1] = 0.0;
+            p0[2 * hv] = p1[2 * hv] = p0[2 * hv + 1] = p1[2 * hv + 1] = 0.0;
           }
     }
   }
