@@ -1877,8 +1877,8 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
             } else {
               // BK = 16 x 4 stages (BK 32 x 2 and 16 x 3 measured equal, profiles/dmma_peak_r01.md)
               using V = DmmaProduct;
-              GMP_TRY(set_smem_once(k_dmma<DMMA_WN, 16, 4, DMMA_WGN>, V::SMEM));
-              k_dmma<DMMA_WN, 16, 4, DMMA_WGN><<<(unsigned)L.icount, V::THREADS, V::SMEM, stream>>>(it, pd, dct, ws,
+              GMP_TRY(set_smem_once(k_dmma<DMMA_WN, 16, DMMA_ST, DMMA_WGN>, V::SMEM));
+              k_dmma<DMMA_WN, 16, DMMA_ST, DMMA_WGN><<<(unsigned)L.icount, V::THREADS, V::SMEM, stream>>>(it, pd, dct, ws,
                                                                                                 (int)nb, pl->d.alpha);
             }
             break;

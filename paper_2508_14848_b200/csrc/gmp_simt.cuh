@@ -442,14 +442,20 @@ template <int WN, int BK_ = 16, int ST_ = 4, int WGN_ = 2> struct DmmaCfg {
   static constexpr int BN = WGN * WN;
   static constexpr int THREADS = 4 * WGN * 32;
   static constexpr int AP = 128 + 4, BP = BN + 4;   // row pitches in doubles (= 32 B mod 128 B)
-  static constexpr int SMEM = ST * BK * (AP + BP) * 8;
+  static constexpr int SMEM = ST * BK * (AP + BP) * 8 + 2 * ST * 8;   // stages + full/empty mbarriers
   static constexpr int MINB = (THREADS == 256 && WN == 32) ? 2 : 1;
 };
 // product: 128 x 64 sub-tiles, 8 warps of 32 x 32, 2 CTAs/SM.  Measured alternatives
 // (profiles/dmma_peak_r01.md): 32 x 64 warp tiles at 1 CTA/SM 9 % slower; 128 x 128
 // sub-tiles with 16 warps (WGN = 4) at 1 CTA/SM 8 % slower (one barrier for all warps).
-constexpr int DMMA_WN = 32, DMMA_WGN = 2;
-using DmmaProduct = DmmaCfg<DMMA_WN, 16, 4, DMMA_WGN>;
+#ifndef GMP_DMMA_WGN   // experiment builds override the shape (-DGMP_DMMA_WGN=4 -DGMP_DMMA_ST=6)
+#define GMP_DMMA_WGN 2
+#endif
+#ifndef GMP_DMMA_ST
+#define GMP_DMMA_ST 4
+#endif
+constexpr int DMMA_WN = 32, DMMA_WGN = GMP_DMMA_WGN, DMMA_ST = GMP_DMMA_ST;
+using DmmaProduct = DmmaCfg<DMMA_WN, 16, DMMA_ST, DMMA_WGN>;
 constexpr int DMMA_BN = DmmaProduct::BN;
 
 __device__ __forceinline__ void dmma16816(double (&c)[4], const double (&a)[8], const double (&b)[4]) {
@@ -481,6 +487,22 @@ k_dmma(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
   const int nsl = nb / BK;
   const int total = it.pcnt * nsl;
   const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+#ifndef GMP_DMMA_SYNC
+  // stage hand-off through mbarriers instead of a CTA barrier per stage: full[s] completes
+  // when every thread's cp.async of the fill landed (noinc arrivals), empty[s] when all 8
+  // warps read the stage; a thread refills a buffer only after its previous fill was read,
+  // and issues that refill after computing its current stage, so warps run decoupled
+  // (no lock-step barrier bubble in the DMMA pipe) with ST - 2 stages of load lead
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + ST * STAGE);
+  uint64_t* empty = full + ST;
+  if (tid == 0)
+    for (int s2 = 0; s2 < ST; ++s2) {
+      mbar_init(&full[s2], NT);
+      mbar_init(&empty[s2], NT / 32);
+    }
+  __syncthreads();
+  uint32_t iphase = 0;
+#endif
 
   // producer cursor over the (pair, slice) sequence (no divisions in the loop)
   int ip = 0, is = 0, istage = 0;
@@ -488,6 +510,9 @@ k_dmma(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
   const int64_t slice_bytes = (int64_t)BK * nb * 8;
   auto issue = [&](int gi) {
     if (gi < total) {
+#ifndef GMP_DMMA_SYNC
+      if (gi >= ST) mbar_wait(&empty[istage], iphase ^ 1);   // previous fill of this buffer read by all warps
+#endif
       if (is == 0) {
         const PairDesc pd = pairs[it.pbeg + ip];
         Ag = ws + pd.a_off + (int64_t)it.m0 * 8;
@@ -505,12 +530,22 @@ k_dmma(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
           cp_async16(stg + BK * AP * 8 + k * BP * 8 + ch * 16, Bg + (int64_t)k * nb * 8 + ch * 16);
         }
       }
+#ifndef GMP_DMMA_SYNC
+      cp_async_mbar_arrive_noinc(&full[istage]);
+#endif
       Ag += slice_bytes;
       Bg += slice_bytes;
       if (++is == nsl) { is = 0; ++ip; }
-      if (++istage == ST) istage = 0;
+      if (++istage == ST) {
+        istage = 0;
+#ifndef GMP_DMMA_SYNC
+        iphase ^= 1;
+#endif
+      }
     }
+#ifdef GMP_DMMA_SYNC
     cp_async_commit();
+#endif
   };
 
 #pragma unroll
@@ -525,13 +560,19 @@ k_dmma(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
       for (int v = 0; v < 4; ++v) acc[i][j][v] = 0.0;
 
   int cstage = 0, cslice = 0, cpair = 0;
+#ifndef GMP_DMMA_SYNC
+  uint32_t cphase = 0;
+#endif
   for (int gi = 0; gi < total; ++gi) {
+#ifdef GMP_DMMA_SYNC
     cp_async_wait<ST - 2>();
     __syncthreads();
     issue(gi + ST - 1);
+#else
+    mbar_wait(&full[cstage], cphase);
+#endif
     const double* As = reinterpret_cast<const double*>(sm + cstage * STAGE);
     const double* Bs = As + BK * AP;
-    if (++cstage == ST) cstage = 0;
     // fragment permutation (bitwise neutral: every output is the same k-ordered DMMA dot
     // product): MMA rows g / g+8 of an m16 tile are sub-tile rows 2g / 2g+1, MMA column g of
     // n8 tiles 2J / 2J+1 is column 16J + 2g / 16J + 2g + 1 -- each fragment pair is one
@@ -563,6 +604,14 @@ k_dmma(const WorkItem* __restrict__ items, const PairDesc* __restrict__ pairs,
         }
       }
     }
+#ifdef GMP_DMMA_SYNC
+    if (++cstage == ST) cstage = 0;
+#else
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[cstage]);
+    if (++cstage == ST) { cstage = 0; cphase ^= 1; }
+    issue(gi + ST - 1);
+#endif
     if (++cslice == nsl) {
       cslice = 0;
       // ---- fold (O9, R25): consecutive pairs with the same fold
