@@ -50,7 +50,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg")
     ap.add_argument("--no-peaks", action="store_true", help="skip the in-run library peak measurement")
-    ap.add_argument("--no-fp64-baseline", action="store_true", help="skip the all-FP64 (100D:0S) leg")
+    ap.add_argument("--no-fp64-baseline", action="store_true",
+                    help="skip the all-FP64 (100D:0S) leg (and, at --config 4, the pure-FP16 leg)")
     ap.add_argument("--cpu-threads", type=int, default=0, help="oracle threads (0: min(16, cores))")
     ap.add_argument("--flags", type=int, default=0, help="extra GMP_FLAG_* bits (A/B runs)")
     ap.add_argument("--size", type=int, default=0, help="override M=N=K (keeps the config's recipe)")
@@ -412,12 +413,14 @@ def run_e2e(a, hA, hB, hC, ref_rows, out_shape, G, dev, desc, comm, w, ws_bytes,
             "result_matches_device_run": ok}
 
 
-def fp64_baseline(a, w, A, Bm, C, dev, stream, P, Q, p, q, comm, G, ro=None, co=None):
+def fp64_baseline(a, w, A, Bm, C, dev, stream, P, Q, p, q, comm, G, ro=None, co=None, kind="fp64"):
     """The paper's comparison point 100D:0S: the same data with
     class_mask = FP64 only, same library, same step.  When the full-size all-FP64
     workspace does not fit next to the inputs (N = 65536 on one GPU: 3 x 32 GB of
     binary64 payloads + W), it runs on the leading square block of A and B that does
-    (same data, labelled)."""
+    (same data, labelled).
+    kind = "fp16": SURVEY 8(d)'s cfg4 comparison, the same data with explicit all-FP16 maps
+    for A, B and C (NEXT-1 explicit-map mode; W binary32), i.e. pure FP16 on the tensor pipe."""
     import torch
     import torch.distributed as dist
     from paper_2508_14848_b200 import binding as B
@@ -425,7 +428,10 @@ def fp64_baseline(a, w, A, Bm, C, dev, stream, P, Q, p, q, comm, G, ro=None, co=
     free, _ = torch.cuda.mem_get_info(dev)
     # extra device bytes of the all-FP64 run: binary64 packed A and B, binary64 W (the C_out
     # payload) of the local C tiles, the packed C_in, and its own result buffer
-    full = A.numel() * 8 + Bm.numel() * 8 + 2 * A.shape[0] * Bm.shape[1] * 8 + (C.numel() * 8 if C is not None else 0)
+    fp16 = kind == "fp16"
+    eb = 2 if fp16 else 8
+    full = (A.numel() * eb + Bm.numel() * eb + A.shape[0] * Bm.shape[1] * (8 + (6 if fp16 else 8))
+            + (C.numel() * eb if C is not None else 0))
     room = free - (8 << 30)
     if full > room:
         if G > 1 or not (w.M == w.N == w.K):
@@ -438,8 +444,15 @@ def fp64_baseline(a, w, A, Bm, C, dev, stream, P, Q, p, q, comm, G, ro=None, co=
     Bsub = Bm if not sub else Bm[:n, :n]
     Csub = None if C is None else (C if not sub else C[:n, :n])
     out = torch.empty((Asub.shape[0], Bsub.shape[1]), dtype=torch.float64, device=dev)
-    desc = B.make_desc(n, n if sub else w.N, n if sub else w.K, w.nb, w.tol, w.alpha, w.beta, 0b1, 0, P, Q,
-                       p * Q + q, row_owner=None if sub else ro, col_owner=None if sub else co)
+    maps = {}
+    if fp16:
+        import numpy as np
+        mt, kt, nt = n // w.nb, (n if sub else w.K) // w.nb, (n if sub else w.N) // w.nb
+        maps = dict(a_map=np.full((mt, kt), 2, np.uint8), b_map=np.full((kt, nt), 2, np.uint8),
+                    c_map=np.full((mt, nt), 2, np.uint8))
+    desc = B.make_desc(n, n if sub else w.N, n if sub else w.K, w.nb, w.tol, w.alpha, w.beta,
+                       0b101 if fp16 else 0b1, 0, P, Q, p * Q + q, row_owner=None if sub else ro,
+                       col_owner=None if sub else co, **maps)
     nscr = B.gemm_mp_scratch_size(desc)
     scratch = torch.empty(nscr, dtype=torch.uint8, device=dev)
     ws = None
@@ -477,10 +490,12 @@ def fp64_baseline(a, w, A, Bm, C, dev, stream, P, Q, p, q, comm, G, ro=None, co=
     del ws, scratch, out
     torch.cuda.empty_cache()
     fl = 2.0 * n * (n if sub else w.N) * (n if sub else w.K)
-    assert st["pairs"][0] == sum(st["pairs"]), "all-FP64 run holds non-FP64 pairs"
+    ci = 2 if fp16 else 0
+    assert st["pairs"][ci] == sum(st["pairs"]), f"all-{kind} run holds pairs of other classes"
     return {"value": fl / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms, "steps": steps,
-            "problem": f"{n}x{n}x{n} leading block of the same A, B (full all-FP64 workspace does not fit)"
-            if sub else "the same problem", "class_mask": "FP64 only (100D:0S)"}
+            "problem": f"{n}x{n}x{n} leading block of the same A, B (full all-{kind} workspace does not fit)"
+            if sub else "the same problem",
+            "class_mask": "explicit all-FP16 maps for A, B, C (pure FP16)" if fp16 else "FP64 only (100D:0S)"}
 
 
 def link_bandwidth(dev, G):
@@ -680,6 +695,16 @@ def main():
         if G > 1:   # every rank has destroyed its plans (unmapping the peers' workspaces) before
             dist.barrier()   # anyone allocates the next leg's buffers
         torch.cuda.empty_cache()
+    # ---- cfg4's comparison: the same data as pure FP16 (explicit all-FP16 maps) ----
+    fp16 = None
+    if a.config == 4 and not a.no_fp64_baseline:
+        try:
+            fp16 = fp64_baseline(a, w, A, Bm, C, dev, stream, P, Q, p, q, comm, G, ro, co, kind="fp16")
+        except Exception as ex:
+            fp16 = {"error": f"{type(ex).__name__}: {str(ex)[:200]}"}
+        if G > 1:
+            dist.barrier()
+        torch.cuda.empty_cache()
     # ---- NVLink: measured NCCL broadcast bandwidth (N > 1) ----
     link_gbs, link_src = 900.0, "datasheet NVLink 5 (900 GB/s per direction)"
     if G > 1:
@@ -752,6 +777,7 @@ def main():
 
     if rank == 0:
         vs_fp64 = (value / fp64["value"]) if fp64 and "value" in fp64 else None
+        vs_fp16 = (value / fp16["value"]) if fp16 and "value" in fp16 else None
         out = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": G, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -776,6 +802,7 @@ def main():
             "execute_tflops": w.flops / (exec_ms * 1e-3) / 1e12,
             "all_fp64": fp64,
             "vs_all_fp64": vs_fp64,
+            **({"all_fp16": fp16, "vs_all_fp16": vs_fp16} if fp16 is not None else {}),
             "precision_mix_roofline": {"t_roof_ms": t_roof_ms, "t_compute_ms": t_comp_ms, "t_link_ms": t_link_ms,
                                        "link_gbs": link_gbs, "link_source": link_src,
                                        "recv_bytes_max_rank": recv_max,
