@@ -179,19 +179,41 @@ __device__ __forceinline__ void shadow_t_block(const ShadowJob& j, uint8_t* ws, 
   const int t = threadIdx.x;
   const uint8_t* src = ws + j.src_off;
   uint8_t* dst = ws + j.dst_off;
-  // all 16 loads first: a global load through a generic pointer may alias the
-  // shared block, so interleaving them with the shared stores would serialise
-  double x[16];
+  // all loads first (16-byte vectors: 4 binary32 or 2 binary64 source elements each): a
+  // global load through a generic pointer may alias the shared block, so interleaving them
+  // with the shared stores would serialise.  The swizzle keeps column pairs (c, c+1), c even,
+  // adjacent, so each pair is one 16-byte shared store.
+  if constexpr (F == 1) {
+    float4 x[4];
 #pragma unroll
-  for (int u = 0; u < 16; ++u) {
-    const int unit = t + u * 256;  // 64 rows x 64 cols
-    const int r = unit >> 6, c = unit & 63;
-    x[u] = payload_f64(src, (int64_t)(r0 + r) * nb + c0 + c, F);
-  }
+    for (int u = 0; u < 4; ++u) {
+      const int unit = t + u * 256;  // 64 rows x 16 float4
+      const int r = unit >> 4, c = (unit & 15) * 4;
+      x[u] = __ldg(reinterpret_cast<const float4*>(src + ((int64_t)(r0 + r) * nb + c0 + c) * 4));
+    }
 #pragma unroll
-  for (int u = 0; u < 16; ++u) {
-    const int unit = t + u * 256;
-    sm[sw64(unit >> 6, unit & 63)] = ldexp_fast(x[u], j.d);
+    for (int u = 0; u < 4; ++u) {
+      const int unit = t + u * 256;
+      const int r = unit >> 4, c = (unit & 15) * 4;
+      *reinterpret_cast<double2*>(sm + sw64(r, c)) = make_double2(ldexp_fast(x[u].x, j.d), ldexp_fast(x[u].y, j.d));
+      *reinterpret_cast<double2*>(sm + sw64(r, c + 2)) =
+          make_double2(ldexp_fast(x[u].z, j.d), ldexp_fast(x[u].w, j.d));
+    }
+  } else {
+    static_assert(F == 0, "transposing shadows start from the MN-major binary64 / binary32 classes");
+    double2 x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int unit = t + u * 256;  // 64 rows x 32 double2
+      const int r = unit >> 5, c = (unit & 31) * 2;
+      x[u] = __ldg(reinterpret_cast<const double2*>(src + ((int64_t)(r0 + r) * nb + c0 + c) * 8));
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int unit = t + u * 256;
+      const int r = unit >> 5, c = (unit & 31) * 2;
+      *reinterpret_cast<double2*>(sm + sw64(r, c)) = make_double2(ldexp_fast(x[u].x, j.d), ldexp_fast(x[u].y, j.d));
+    }
   }
   __syncthreads();
 #pragma unroll
