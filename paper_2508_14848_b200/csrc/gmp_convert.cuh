@@ -58,15 +58,8 @@ __device__ __forceinline__ void store8(uint8_t* dst, const double* v) {
   }
 }
 
-// 64x64 binary64 staging block, XOR-swizzled instead of padded: element (r, c)
-// lives at r*64 + (c ^ 2*((r >> 3) & 7)).  Row-wise double2 writes stay
-// contiguous, and the transposed reads (8 row groups x 2 columns per half-warp)
-// hit 16 distinct 8-byte bank pairs.
-__device__ __forceinline__ int sw64(int r, int c) { return r * 64 + (c ^ (((r >> 3) & 7) << 1)); }
-
 template <int C>
-__device__ __forceinline__ void pack_block(const PackJob& j, uint8_t* ws, int nb, int r0, int c0,
-                                           double* sm) {
+__device__ __forceinline__ void pack_block(const PackJob& j, uint8_t* ws, int nb, int r0, int c0) {
   const int t = threadIdx.x;
   constexpr int B = class_bytes(C);
   uint8_t* dst = ws + j.dst_off;
@@ -87,46 +80,37 @@ __device__ __forceinline__ void pack_block(const PackJob& j, uint8_t* ws, int nb
       store8<C>(dst + ((int64_t)(r0 + r) * nb + c0 + g * 8) * B, v);
     }
   } else {
-    // stage the 64x64 block in shared memory, write it transposed (K-major)
+    // transposed (K-major) write, register transpose: warp w takes source rows 8w..8w+7,
+    // lane l the column pair (2l, 2l+1) -- one coalesced 512-byte row per warp load -- and
+    // writes 8 consecutive output elements of each of its two output rows (the next warp
+    // fills the rest of the 32-byte sectors).  No shared memory, no barrier.
+    const int w = t >> 5, c = 2 * (t & 31);
     double2 x[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int unit = t + u * 256;     // 64 rows x 32 double2
-      x[u] = __ldg(reinterpret_cast<const double2*>(j.src + (int64_t)(r0 + (unit >> 5)) * j.ld + c0 + 2 * (unit & 31)));
-    }
+    for (int i = 0; i < 8; ++i)
+      x[i] = __ldg(reinterpret_cast<const double2*>(j.src + (int64_t)(r0 + 8 * w + i) * j.ld + c0 + c));
+    double v0[8], v1[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int unit = t + u * 256;
-      *reinterpret_cast<double2*>(sm + sw64(unit >> 5, 2 * (unit & 31))) = x[u];
+    for (int i = 0; i < 8; ++i) {
+      v0[i] = (C == 0) ? x[i].x : ldexp_fast(x[i].x, j.scale);
+      v1[i] = (C == 0) ? x[i].y : ldexp_fast(x[i].y, j.scale);
     }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      int unit = t + u * 256;           // output row (= source col) x 8-k group
-      int oc = unit >> 3, g = unit & 7;
-      double v[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const double x = sm[sw64(g * 8 + i, oc)];
-        v[i] = (C == 0) ? x : ldexp_fast(x, j.scale);
-      }
-      store8<C>(dst + ((int64_t)(c0 + oc) * nb + r0 + g * 8) * B, v);
-    }
+    store8<C>(dst + ((int64_t)(c0 + c) * nb + r0 + 8 * w) * B, v0);
+    store8<C>(dst + ((int64_t)(c0 + c + 1) * nb + r0 + 8 * w) * B, v1);
   }
 }
 
 __global__ void __launch_bounds__(256) k_pack(const PackJob* __restrict__ jobs, uint8_t* ws, int nb) {
-  __shared__ __align__(16) double sm[64 * 64];
   const PackJob j = jobs[blockIdx.y];
   const int per = nb / 64;
   const int r0 = (blockIdx.x / per) * 64, c0 = (blockIdx.x % per) * 64;
   switch (j.cls) {
-    case 0: pack_block<0>(j, ws, nb, r0, c0, sm); break;
-    case 1: pack_block<1>(j, ws, nb, r0, c0, sm); break;
-    case 2: pack_block<2>(j, ws, nb, r0, c0, sm); break;
-    case 3: pack_block<3>(j, ws, nb, r0, c0, sm); break;
-    case 4: pack_block<4>(j, ws, nb, r0, c0, sm); break;
-    default: pack_block<5>(j, ws, nb, r0, c0, sm); break;
+    case 0: pack_block<0>(j, ws, nb, r0, c0); break;
+    case 1: pack_block<1>(j, ws, nb, r0, c0); break;
+    case 2: pack_block<2>(j, ws, nb, r0, c0); break;
+    case 3: pack_block<3>(j, ws, nb, r0, c0); break;
+    case 4: pack_block<4>(j, ws, nb, r0, c0); break;
+    default: pack_block<5>(j, ws, nb, r0, c0); break;
   }
 }
 
@@ -170,70 +154,48 @@ __global__ void __launch_bounds__(256) k_shadow(const ShadowJob* __restrict__ jo
   }
 }
 
-// Transposing shadow (source MN-major class 0/1 -> target K-major class 2..4):
-// 64x64 blocks staged through shared memory, decoded exactly, scaled, rounded
-// once into the target class and written transposed.
+// Transposing shadow (source MN-major class 0/1 -> target K-major class 2..5): per 64x64
+// block, warp w takes source rows 8w..8w+7 and lane l the column pair (2l, 2l+1) (8- or
+// 16-byte coalesced loads), decodes exactly, scales, rounds once into the target class and
+// writes 8 consecutive elements of each of its two output rows (register transpose).
 template <int F, int T>
-__device__ __forceinline__ void shadow_t_block(const ShadowJob& j, uint8_t* ws, int nb, int r0, int c0,
-                                               double* sm) {
-  const int t = threadIdx.x;
+__device__ __forceinline__ void shadow_t_block(const ShadowJob& j, uint8_t* ws, int nb, int r0, int c0) {
+  static_assert(F == 0 || F == 1, "transposing shadows start from the MN-major binary64 / binary32 classes");
+  const int t = threadIdx.x, w = t >> 5, c = 2 * (t & 31);
   const uint8_t* src = ws + j.src_off;
   uint8_t* dst = ws + j.dst_off;
-  // all loads first (16-byte vectors: 4 binary32 or 2 binary64 source elements each): a
-  // global load through a generic pointer may alias the shared block, so interleaving them
-  // with the shared stores would serialise.  The swizzle keeps column pairs (c, c+1), c even,
-  // adjacent, so each pair is one 16-byte shared store.
+  double v0[8], v1[8];
   if constexpr (F == 1) {
-    float4 x[4];
+    float2 x[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int unit = t + u * 256;  // 64 rows x 16 float4
-      const int r = unit >> 4, c = (unit & 15) * 4;
-      x[u] = __ldg(reinterpret_cast<const float4*>(src + ((int64_t)(r0 + r) * nb + c0 + c) * 4));
-    }
+    for (int i = 0; i < 8; ++i)
+      x[i] = __ldg(reinterpret_cast<const float2*>(src + ((int64_t)(r0 + 8 * w + i) * nb + c0 + c) * 4));
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int unit = t + u * 256;
-      const int r = unit >> 4, c = (unit & 15) * 4;
-      *reinterpret_cast<double2*>(sm + sw64(r, c)) = make_double2(ldexp_fast(x[u].x, j.d), ldexp_fast(x[u].y, j.d));
-      *reinterpret_cast<double2*>(sm + sw64(r, c + 2)) =
-          make_double2(ldexp_fast(x[u].z, j.d), ldexp_fast(x[u].w, j.d));
+    for (int i = 0; i < 8; ++i) {
+      v0[i] = ldexp_fast((double)x[i].x, j.d);
+      v1[i] = ldexp_fast((double)x[i].y, j.d);
     }
   } else {
-    static_assert(F == 0, "transposing shadows start from the MN-major binary64 / binary32 classes");
     double2 x[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int unit = t + u * 256;  // 64 rows x 32 double2
-      const int r = unit >> 5, c = (unit & 31) * 2;
-      x[u] = __ldg(reinterpret_cast<const double2*>(src + ((int64_t)(r0 + r) * nb + c0 + c) * 8));
-    }
+    for (int i = 0; i < 8; ++i)
+      x[i] = __ldg(reinterpret_cast<const double2*>(src + ((int64_t)(r0 + 8 * w + i) * nb + c0 + c) * 8));
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int unit = t + u * 256;
-      const int r = unit >> 5, c = (unit & 31) * 2;
-      *reinterpret_cast<double2*>(sm + sw64(r, c)) = make_double2(ldexp_fast(x[u].x, j.d), ldexp_fast(x[u].y, j.d));
+    for (int i = 0; i < 8; ++i) {
+      v0[i] = ldexp_fast(x[i].x, j.d);
+      v1[i] = ldexp_fast(x[i].y, j.d);
     }
   }
-  __syncthreads();
-#pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const int unit = t + u * 256;  // output row (= source col) x 8-element group
-    const int oc = unit >> 3, gq = unit & 7;
-    double v[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = sm[sw64(gq * 8 + i, oc)];
-    store8<T>(dst + ((int64_t)(c0 + oc) * nb + r0 + gq * 8) * class_bytes(T), v);
-  }
+  store8<T>(dst + ((int64_t)(c0 + c) * nb + r0 + 8 * w) * class_bytes(T), v0);
+  store8<T>(dst + ((int64_t)(c0 + c + 1) * nb + r0 + 8 * w) * class_bytes(T), v1);
 }
 
 __global__ void __launch_bounds__(256) k_shadow_t(const ShadowJob* __restrict__ jobs, uint8_t* ws, int nb) {
-  __shared__ __align__(16) double sm[64 * 64];
   const ShadowJob j = jobs[blockIdx.y];
   const int per = nb / 64;
   const int r0 = (blockIdx.x / per) * 64, c0 = (blockIdx.x % per) * 64;
   switch (j.from * 8 + j.to) {
-#define GMP_ST(F, T) case F * 8 + T: shadow_t_block<F, T>(j, ws, nb, r0, c0, sm); break;
+#define GMP_ST(F, T) case F * 8 + T: shadow_t_block<F, T>(j, ws, nb, r0, c0); break;
     GMP_ST(0, 2) GMP_ST(0, 3) GMP_ST(0, 4) GMP_ST(0, 5) GMP_ST(1, 2) GMP_ST(1, 3) GMP_ST(1, 4) GMP_ST(1, 5)
 #undef GMP_ST
     default: break;
