@@ -392,9 +392,15 @@ def run_e2e(a, hA, hB, hC, ref_rows, out_shape, G, dev, desc, comm, w, ws_bytes,
     s0.record(pipe.compute)
     pipe.h2d.wait_stream(pipe.compute)
     pipe.d2h.wait_stream(pipe.compute)
+    pipe.record_timeline = bool(os.environ.get("GMP_E2E_TIMELINE"))   # diagnostics: per-step events
     pipe.run([hA] * K, [hB] * K, [hC] * K, [hOut] * K)
     s1.record(pipe.compute)
     torch.cuda.synchronize()
+    if pipe.record_timeline and int(os.environ.get("RANK", 0)) == 0:
+        print(f"e2e timeline (nbuf={nbuf}, {K} steps; ms after start: h2d_done convert_done exec_done d2h_done)",
+              file=sys.stderr)
+        for k in range(K):
+            print(k, *[round(s0.elapsed_time(e[k]), 1) for e in pipe.timeline], file=sys.stderr)
     pipe.close()
     e2e_ms = s0.elapsed_time(s1) / K
     if G > 1:

@@ -217,6 +217,14 @@ gmp_status_t gemm_mp_convert(gmp_plan_t plan, void *ws, size_t ws_bytes, void *s
  * C: 16-byte aligned, ldc even (GMP_ERR_ARG otherwise; C-finalize writes 16-byte vectors). */
 gmp_status_t gemm_mp_execute(gmp_plan_t plan, double *C, int64_t ldc, void *stream);
 
+/* gemm_mp_execute whose C-finalize (the only step that writes C) first waits for the CUDA
+ * event c_free_event (a cudaEvent_t; NULL = gemm_mp_execute): a caller streaming results
+ * out of C (e.g. a device->host copy of the previous GEMM's C on another stream) overlaps
+ * that copy with this execute's tile-GEMMs instead of serialising the whole execute behind
+ * it.  The event is waited on at the finalize launch; it must have been recorded (or never
+ * recorded) when this call is made.                                                       */
+gmp_status_t gemm_mp_execute_after(gmp_plan_t plan, double *C, int64_t ldc, void *stream, void *c_free_event);
+
 /* Waits for the plan's streams; returns the first asynchronous error.          */
 gmp_status_t gemm_mp_sync(gmp_plan_t plan);
 

@@ -253,9 +253,10 @@ class HostPipeline:
                     self._ensure_ws(nws)
             B.gemm_mp_convert(pl, self.ws, nws, self.compute)
             convert_done[k].record(self.compute)
-            if k >= nbuf:
-                self.compute.wait_event(d2h_done[k - nbuf])     # result buffer b read back
-            B.gemm_mp_execute(pl, self.dOut[b], self.dOut[b].stride(0), self.compute)
+            # result buffer b is free once step k-nbuf was read back: only the C-finalize waits
+            # for that copy, the tile-GEMMs overlap it
+            B.gemm_mp_execute_after(pl, self.dOut[b], self.dOut[b].stride(0), self.compute,
+                                    d2h_done[k - nbuf] if k >= nbuf else None)
             exec_done[k].record(self.compute)
             with torch.cuda.stream(self.d2h):
                 self.d2h.wait_event(exec_done[k])

@@ -93,6 +93,7 @@ def lib():
             "gemm_mp_workspace_size": [vp, ct.POINTER(ct.c_size_t)],
             "gemm_mp_convert": [vp, vp, ct.c_size_t, vp],
             "gemm_mp_execute": [vp, vp, i64, vp],
+            "gemm_mp_execute_after": [vp, vp, i64, vp, vp],
             "gemm_mp_sync": [vp],
             "gemm_mp_get_maps": [vp, vp, vp, vp, vp, vp, vp],
             "gemm_mp_get_tile": [vp, ct.c_char, i64, i64, i32, vp, ct.POINTER(ct.c_size_t),
@@ -187,6 +188,14 @@ def gemm_mp_convert(plan, ws, ws_bytes, stream=None):
 
 def gemm_mp_execute(plan, C, ldc, stream=None):
     _check(lib().gemm_mp_execute(plan, _ptr(C), ldc, _stream(stream)))
+
+
+def gemm_mp_execute_after(plan, C, ldc, stream=None, c_free_event=None):
+    """c_free_event: a torch.cuda.Event (or raw cudaEvent_t int) the C-finalize waits for"""
+    ev = c_free_event
+    if ev is not None and not isinstance(ev, int):
+        ev = ev.cuda_event
+    _check(lib().gemm_mp_execute_after(plan, _ptr(C), ldc, _stream(stream), ev or None))
 
 
 def gemm_mp_sync(plan):

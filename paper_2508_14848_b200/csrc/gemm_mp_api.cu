@@ -1773,7 +1773,7 @@ extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_byte
   return GMP_OK;
 }
 
-extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ldc, void* stream_) {
+static gmp_status_t execute_impl(gmp_plan_t pl, double* Cuser, int64_t ldc, void* stream_, cudaEvent_t c_free) {
   if (!pl) return fail(GMP_ERR_ARG, "plan is NULL");
   if (pl->host_only) return fail(GMP_ERR_STATE, "host-built plan (gemm_mp_plan_host) cannot execute");
   if (!pl->converted) return fail(GMP_ERR_STATE, "execute before convert");
@@ -1906,6 +1906,9 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
           dct, (const int32_t*)(ws + pl->off_maxidx), ws, nb2, mb);
       GMP_CUDA(cudaGetLastError());
     }
+    // the only writer of the user's C: a caller still reading the previous result out of C
+    // (gemm_mp_execute_after) holds back this launch alone, not the tile-GEMMs
+    if (c_free) GMP_CUDA(cudaStreamWaitEvent(stream, c_free, 0));
     k_c_finalize<<<dim3((unsigned)(nb / FIN_ROWS), (unsigned)nCl), 256, 0, stream>>>(
         dct, ws, mb, (int16_t*)(ws + pl->off_cscale), Cuser, ldc, (int)nb);
     GMP_CUDA(cudaGetLastError());
@@ -1914,6 +1917,16 @@ extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ld
   GMP_TRY(record_done(pl, stream));
   pl->executed = true;
   return GMP_OK;
+}
+
+
+extern "C" gmp_status_t gemm_mp_execute(gmp_plan_t pl, double* Cuser, int64_t ldc, void* stream) {
+  return execute_impl(pl, Cuser, ldc, stream, nullptr);
+}
+
+extern "C" gmp_status_t gemm_mp_execute_after(gmp_plan_t pl, double* Cuser, int64_t ldc, void* stream,
+                                              void* c_free_event) {
+  return execute_impl(pl, Cuser, ldc, stream, (cudaEvent_t)c_free_event);
 }
 
 extern "C" gmp_status_t gemm_mp_sync(gmp_plan_t pl) {

@@ -15,7 +15,7 @@ from paper_2508_14848_b200 import binding as B
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("beta,nbuf", [(0.0, 3), (0.5, 3), (0.5, 2)])
+@pytest.mark.parametrize("beta,nbuf", [(0.0, 3), (0.5, 3), (0.5, 2), (0.0, 1), (0.5, 1)])
 def test_host_pipeline_matches_single_runs(beta, nbuf):
     M, N, K, nb = 768, 512, 1024, 128
     steps = 6
@@ -39,6 +39,35 @@ def test_host_pipeline_matches_single_runs(beta, nbuf):
     pipe.close()
     for k in range(steps):
         assert np.array_equal(hOut[k].numpy(), want[k]), f"step {k}"
+
+
+def test_execute_after_holds_back_only_the_finalize():
+    """gemm_mp_execute_after: the C-finalize waits for the caller's event.  A side stream
+    sleeps, then overwrites C with NaN and records the event; the execute's result must land
+    after that write (C finite and equal to a plain execute's), so C is never written before
+    the event."""
+    w = gmp_inputs.small_workload(512, 512, 768, 128, 1e-5, mode="random", E=24, beta=0.0, seed=78,
+                                  class_mask=0b11111)
+    A, Bm, _ = w.matrices()
+    dev = torch.device("cuda:0")
+    desc = B.make_desc(w.M, w.N, w.K, w.nb, w.tol, w.alpha, w.beta, w.class_mask)
+    g = api.GemmMP(desc, torch.from_numpy(A).to(dev), torch.from_numpy(Bm).to(dev), None)
+    g.convert()
+    ref = torch.empty(w.M, w.N, dtype=torch.float64, device=dev)
+    g.execute(ref)
+    g.sync()
+    out = torch.zeros(w.M, w.N, dtype=torch.float64, device=dev)
+    side = torch.cuda.Stream(dev)
+    ev = torch.cuda.Event()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(side):
+        torch.cuda._sleep(200_000_000)            # ~0.1 s
+        out.fill_(float("nan"))
+        ev.record(side)
+    cur = torch.cuda.current_stream(dev)
+    B.gemm_mp_execute_after(g.plan, out, out.stride(0), cur, ev)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
 
 
 @pytest.mark.parametrize("flags", [0, B.GMP_FLAG_SPLIT16])
