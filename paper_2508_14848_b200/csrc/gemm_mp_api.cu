@@ -1015,8 +1015,8 @@ static void build_tables(gmp_plan_s* pl) {
   }
 
   // ---- W0 (O9): the first launch of SUMMA step 0 that touches a local C tile starts
-  // its W from C_in when its kernel can (k_tc_class incl. the FP32 split, k_tc_fused:
-  // the W rows are loaded once per item there); the other tiles get W0 from
+  // its W from C_in when its kernel can (k_tc_class incl. the FP32 split, and the SM-pair
+  // kernel: the W rows are loaded once per item there); the other tiles get W0 from
   // k_acc_init ----
   pl->acc_init_idx.clear();
   {

@@ -53,7 +53,7 @@ struct PairDesc {
   int32_t fexp;          // -(eA + eB): fold factor alpha * 2^fexp
   int32_t l;             // global reduction tile index (bookkeeping)
   int32_t a_slot, b_slot;  // slot indices in the class arena (TMA row = slot * nb)
-  int32_t cls;             // pair class (k_tc_fused: selects the operand arena and the MMA kind)
+  int32_t cls;             // pair class (the merged FP16+BF16 launch selects the operand map and the MMA kind by it)
   int32_t pad;
 };
 

@@ -175,7 +175,7 @@ struct TcSched {
   }
 };
 
-// Epilogue warps 2..9 of the 1-SM tcgen05 kernels (k_tc_class, k_tc_fused): per
+// Epilogue warps 2..9 of the 1-SM tcgen05 kernel (k_tc_class): per
 // pair, read the FP32 product from TMEM and fold it into W (O9).
 template <int BN>
 __device__ __forceinline__ void tc_epilogue(const WorkItem* __restrict__ items, int64_t nitems,
