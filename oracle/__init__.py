@@ -62,6 +62,8 @@ def lib():
         L.orc_finalize.argtypes = [i32, ct.c_int, vp, vp, vp, i64]
         L.orc_gemm_mp.restype = ct.c_int
         L.orc_gemm_mp.argtypes = [vp, vp, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp]
+        L.orc_gemm_mp_synth.restype = ct.c_int
+        L.orc_gemm_mp_synth.argtypes = [vp, vp, vp, vp, vp, vp, i64, vp]
         L.orc_max_threads.restype = ct.c_int
         L.orc_class_bytes.restype = ct.c_int; L.orc_class_bytes.argtypes = [ct.c_int]
         L.orc_payload_bytes.restype = i64; L.orc_payload_bytes.argtypes = [ct.c_int, i32]
@@ -257,6 +259,45 @@ def gemm_mp(A, B, C, nb, tol, alpha=1.0, beta=0.0, class_mask=0b01111, ctiles=No
     o["C"] = Cout
     o["W"] = W
     o["threads"] = out.threads
+    return o
+
+
+class _Synth(ct.Structure):
+    _fields_ = [("seed", ct.c_uint64), ("tau", ct.c_uint64), ("mode", ct.c_int), ("E", ct.c_int), ("s", ct.c_int)]
+
+
+_MODES = {"uniform": 0, "graded": 1, "random": 2}
+
+
+def gemm_mp_synth(M, N, K, nb, tol, gen_a, gen_b, gen_c, ctiles, alpha=1.0, beta=0.0, class_mask=0b01111,
+                  want_w=True):
+    """The whole method (O1-O9) on the synthetic workload, generated tile by tile (the
+    inputs are never materialised: N = 65536 fits).  gen_x: (seed, mode, E, s, tau) of the
+    O1 recipe (mode 'uniform' / 'graded' / 'random' or 0/1/2).  Returns the maps, scales
+    and stats of every tile as gemm_mp does, and the listed C tiles (and their final W)
+    as arrays of shape (len(ctiles), nb, nb) in list order."""
+    mt, nt, kt = M // nb, N // nb, K // nb
+
+    def syn(g):
+        seed, mode, E, s_, tau = g
+        return _Synth(seed, tau, _MODES.get(mode, mode), E, s_)
+
+    d = _Desc(M, N, K, nb, tol, alpha, beta, class_mask, None, None, None)
+    o = dict(acode=np.zeros((mt, kt), np.uint8), bcode=np.zeros((kt, nt), np.uint8),
+             ccode=np.zeros((mt, nt), np.uint8), ascale5=np.zeros((mt, kt, NCLS), np.int16),
+             bscale5=np.zeros((kt, nt, NCLS), np.int16), cscale=np.zeros((mt, nt), np.int16),
+             cin_scale=np.zeros((mt, nt), np.int16),
+             SA=np.zeros((mt, kt)), MA=np.zeros((mt, kt)), SB=np.zeros((kt, nt)),
+             MB=np.zeros((kt, nt)), SC=np.zeros((mt, nt)), MC=np.zeros((mt, nt)))
+    tl = np.ascontiguousarray(ctiles, np.int64)
+    Ct = np.zeros((tl.size, nb, nb))
+    W = np.zeros((tl.size, nb, nb)) if want_w else None
+    out = _Out(*[_p(o[k]) for k in ["acode", "bcode", "ccode", "ascale5", "bscale5", "cscale",
+                                     "cin_scale", "SA", "MA", "SB", "MB", "SC", "MC"]], 0, _p(W), nb)
+    ga, gb, gc = syn(gen_a), syn(gen_b), syn(gen_c)
+    o["rc"] = lib().orc_gemm_mp_synth(ct.byref(d), ct.byref(ga), ct.byref(gb), ct.byref(gc), _p(Ct), _p(tl),
+                                      tl.size, ct.byref(out))
+    o["C"], o["W"], o["threads"] = Ct, W, out.threads
     return o
 
 

@@ -282,23 +282,27 @@ double orc_cnorm(const double *tile, int64_t ld, int32_t nb) {
 
 /* Stats of every tile of an (mt*nb) x (nt*nb) row-major matrix. finite[t] = 0 if
  * the tile holds a NaN or an infinity. Arrays are mt*nt, row-major tile order. */
+static void orc_one_tile_stats(const double *tp, int64_t ld, int32_t nb, double *S, double *maxabs,
+                               uint8_t *finite) {
+    double m = 0.0;
+    int fin = 1;
+    for (int32_t r = 0; r < nb; ++r)
+        for (int32_t c = 0; c < nb; ++c) {
+            double a = fabs(tp[(int64_t)r * ld + c]);
+            if (!isfinite(a)) fin = 0;
+            else if (a > m) m = a;
+        }
+    *maxabs = m;
+    *finite = (uint8_t)fin;
+    *S = fin ? orc_cnorm(tp, ld, nb) : NAN;
+}
+
 void orc_tile_stats(const double *X, int64_t ld, int64_t mt, int64_t nt, int32_t nb,
                     double *S, double *maxabs, uint8_t *finite) {
 #pragma omp parallel for schedule(dynamic)
     for (int64_t t = 0; t < mt * nt; ++t) {
         int64_t ti = t / nt, tj = t % nt;
-        const double *tp = X + ti * nb * ld + tj * nb;
-        double m = 0.0;
-        int fin = 1;
-        for (int32_t r = 0; r < nb; ++r)
-            for (int32_t c = 0; c < nb; ++c) {
-                double a = fabs(tp[(int64_t)r * ld + c]);
-                if (!isfinite(a)) fin = 0;
-                else if (a > m) m = a;
-            }
-        maxabs[t] = m;
-        finite[t] = (uint8_t)fin;
-        S[t] = fin ? orc_cnorm(tp, ld, nb) : NAN;
+        orc_one_tile_stats(X + ti * nb * ld + tj * nb, ld, nb, S + t, maxabs + t, finite + t);
     }
 }
 
@@ -651,23 +655,70 @@ static void orc_explicit_map(int64_t ntiles, const uint8_t *map, uint32_t class_
 }
 
 /*
- * Full method over all of A (M x K), B (K x N), C (M x N), binary64 row-major.
- * ctiles: list of n_ctiles C tile indices (i*nt + j) to compute (NULL = all);
- * Cout receives the user (binary64) result for those tiles; other tiles of Cout
- * are left untouched.  Returns 0, 1 (non-finite input) or 2 (bad arguments).
+ * Where the driver reads an input tile from: an in-memory binary64 row-major matrix, or
+ * the O1 synthetic generator (orc_synth_block), tile by tile, so that workloads larger than
+ * host memory (N = 65536) never exist as a whole.  Either way the tile's values are the
+ * same binary64 numbers.
  */
-int orc_gemm_mp(const orc_desc_t *d, const double *A, int64_t lda, const double *B,
-                int64_t ldb, const double *C, int64_t ldc, double *Cout, int64_t ldo,
-                const int64_t *ctiles, int64_t n_ctiles, orc_out_t *o) {
+typedef struct {
+    const double *X;            /* in-memory matrix (synth = 0) */
+    int64_t ld;
+    int synth;                  /* 1: generator below            */
+    int64_t rows, cols;
+    uint64_t seed, tau;
+    int mode, E, s;
+} orc_src_t;
+
+/* tile (ti, tj): a pointer to its top-left element and its leading dimension; buf
+ * (nb*nb doubles) receives generated tiles */
+static const double *orc_src_tile(const orc_src_t *src, int32_t nb, int64_t ti, int64_t tj, double *buf,
+                                  int64_t *ld) {
+    if (!src->synth) {
+        *ld = src->ld;
+        return src->X + ti * nb * src->ld + tj * nb;
+    }
+    orc_synth_block(src->rows, src->cols, nb, src->seed, src->mode, src->E, src->s, src->tau, ti * nb, nb,
+                    tj * nb, nb, buf, nb);
+    *ld = nb;
+    return buf;
+}
+
+static void orc_src_stats(const orc_src_t *src, int64_t mt, int64_t nt, int32_t nb, double *S, double *maxabs,
+                          uint8_t *finite) {
+#pragma omp parallel
+    {
+        double *buf = src->synth ? malloc(sizeof(double) * (size_t)nb * nb) : NULL;
+#pragma omp for schedule(dynamic)
+        for (int64_t t = 0; t < mt * nt; ++t) {
+            int64_t ld;
+            const double *tp = orc_src_tile(src, nb, t / nt, t % nt, buf, &ld);
+            orc_one_tile_stats(tp, ld, nb, S + t, maxabs + t, finite + t);
+        }
+        free(buf);
+    }
+}
+
+/*
+ * Full method (Algorithm 1) over the tiles of A (M x K), B (K x N), C (M x N).
+ * ctiles: list of n_ctiles C tile indices (i*nt + j) to compute (NULL = all).
+ * compact = 0: Cout (ldo) and o->W (o->ldw) are full M x N arrays, listed tiles written
+ * in place; compact = 1: the q-th listed tile goes to Cout + q*nb*nb and o->W + q*nb*nb
+ * (leading dimension nb).  The tile-GEMMs of one C tile are independent and are computed
+ * concurrently; their folds into W run one by one in the order of O9.
+ * Returns 0, 1 (non-finite input) or 2 (bad arguments).
+ */
+static int orc_gemm_mp_core(const orc_desc_t *d, const orc_src_t *sA, const orc_src_t *sB, const orc_src_t *sC,
+                            double *Cout, int64_t ldo, const int64_t *ctiles, int64_t n_ctiles, int compact,
+                            orc_out_t *o) {
     int32_t nb = d->nb;
     if (nb <= 0 || d->M % nb || d->N % nb || d->K % nb) return 2;
     int64_t mt = d->M / nb, nt = d->N / nb, kt = d->K / nb;
     int64_t nA = mt * kt, nB = kt * nt, nC = mt * nt;
     int64_t tsz = (int64_t)nb * nb;
     uint8_t *fA = malloc(nA), *fB = malloc(nB), *fC = malloc(nC);
-    orc_tile_stats(A, lda, mt, kt, nb, o->SA, o->MA, fA);
-    orc_tile_stats(B, ldb, kt, nt, nb, o->SB, o->MB, fB);
-    if (d->beta != 0.0) orc_tile_stats(C, ldc, mt, nt, nb, o->SC, o->MC, fC);
+    orc_src_stats(sA, mt, kt, nb, o->SA, o->MA, fA);
+    orc_src_stats(sB, kt, nt, nb, o->SB, o->MB, fB);
+    if (d->beta != 0.0) orc_src_stats(sC, mt, nt, nb, o->SC, o->MC, fC);
     else for (int64_t t = 0; t < nC; ++t) { o->SC[t] = 0.0; o->MC[t] = 0.0; fC[t] = 1; }
     int16_t *sa = malloc(sizeof(int16_t) * nA), *sb = malloc(sizeof(int16_t) * nB);
     int rc = 0;
@@ -698,14 +749,16 @@ int orc_gemm_mp(const orc_desc_t *d, const double *A, int64_t lda, const double 
     }
     void **Ap = calloc((size_t)nA * ORC_NCLS, sizeof(void *));
     void **Bp = calloc((size_t)nB * ORC_NCLS, sizeof(void *));
-#pragma omp parallel for schedule(dynamic)
+#pragma omp parallel
+    {
+    double *gbuf = (sA->synth || sB->synth) ? malloc(sizeof(double) * (size_t)tsz) : NULL;
+#pragma omp for schedule(dynamic)
     for (int64_t t = 0; t < nA + nB; ++t) {
         int isB = t >= nA;
         int64_t tt = isB ? t - nA : t;
         int64_t ncols = isB ? nt : kt;
-        const double *X = isB ? B : A;
-        int64_t ld = isB ? ldb : lda;
-        const double *tp = X + (tt / ncols) * nb * ld + (tt % ncols) * nb;
+        int64_t ld;
+        const double *tp = orc_src_tile(isB ? sB : sA, nb, tt / ncols, tt % ncols, gbuf, &ld);
         int code = isB ? o->bcode[tt] : o->acode[tt];
         int keep = isB ? needB[tt] : needA[tt];
         int16_t *s5 = isB ? o->bscale5 + tt * ORC_NCLS : o->ascale5 + tt * ORC_NCLS;
@@ -723,6 +776,8 @@ int orc_gemm_mp(const orc_desc_t *d, const double *A, int64_t lda, const double 
         if (!keep) { free(pp[code]); pp[code] = NULL; }
         free(tmp);
     }
+    free(gbuf);
+    }
     free(needA); free(needB);
     rc = orc_map_c(mt, nt, kt, nb, d->tol, d->alpha, d->beta, d->class_mask, o->SA,
                    o->SB, o->SC, fC, o->acode, o->ascale5, o->bcode, o->bscale5, o->ccode,
@@ -730,55 +785,92 @@ int orc_gemm_mp(const orc_desc_t *d, const double *A, int64_t lda, const double 
     if (!rc) {
         int64_t nlist = ctiles ? n_ctiles : nC;
         int nthreads = 1;
-#pragma omp parallel
-        {
 #ifdef _OPENMP
-#pragma omp single
-            nthreads = omp_get_num_threads();
+        nthreads = omp_get_max_threads();
 #endif
-            double *acc = malloc(sizeof(double) * tsz);
-            double *P = malloc(sizeof(double) * tsz);
-            void *cpay = malloc((size_t)tsz * 8);
-            void *cin = malloc((size_t)tsz * 8);
-#pragma omp for schedule(dynamic)
-            for (int64_t q = 0; q < nlist; ++q) {
-                int64_t ct = ctiles ? ctiles[q] : q;
-                int64_t i = ct / nt, j = ct % nt;
-                int codec = o->ccode[ct];
-                int cins = 0;
-                if (d->beta != 0.0) {
-                    cins = orc_scale_exp(o->MC[ct], codec);
-                    orc_pack_tile(C + i * nb * ldc + j * nb, ldc, nb, codec, cins, 0, cin);
-                }
-                if (o->cin_scale) o->cin_scale[ct] = (int16_t)cins;
-                orc_acc_init(nb, codec, d->beta, cin, cins, acc);
-                for (int64_t s0 = 0; s0 < kt; s0 += ORC_STEP_DEPTH) {
-                    int64_t s1 = s0 + ORC_STEP_DEPTH < kt ? s0 + ORC_STEP_DEPTH : kt;
-                    for (int c = ORC_NCLS - 1; c >= 0; --c) {
-                        for (int64_t l = s0; l < s1; ++l) {
-                            int ca = o->acode[i * kt + l], cb = o->bcode[l * nt + j];
-                            if ((ca > cb ? ca : cb) != c) continue;
-                            orc_tile_gemm(c, Ap[(i * kt + l) * ORC_NCLS + c], Bp[(l * nt + j) * ORC_NCLS + c],
-                                          nb, P);
-                            orc_fold(nb, codec, d->alpha, o->ascale5[(i * kt + l) * ORC_NCLS + c],
-                                     o->bscale5[(l * nt + j) * ORC_NCLS + c], P, acc);
-                        }
-                    }
-                }
-                if (o->W)
-                    for (int64_t r = 0; r < nb; ++r)
-                        memcpy(o->W + (i * nb + r) * o->ldw + j * nb, acc + r * nb, sizeof(double) * nb);
-                int e = orc_finalize(nb, codec, acc, cpay, Cout + i * nb * ldo + j * nb, ldo);
-                if (o->cscale) o->cscale[ct] = (int16_t)e;
+        double *acc = malloc(sizeof(double) * tsz);
+        void *cpay = malloc((size_t)tsz * 8);
+        void *cin = malloc((size_t)tsz * 8);
+        double *cbuf = (sC->synth && d->beta != 0.0) ? malloc(sizeof(double) * tsz) : NULL;
+        int64_t *pl = malloc(sizeof(int64_t) * (size_t)kt);   /* the tile's pairs in fold order */
+        int *pc = malloc(sizeof(int) * (size_t)kt);
+        double *P = malloc(sizeof(double) * (size_t)tsz * (size_t)kt);
+        for (int64_t q = 0; q < nlist; ++q) {
+            int64_t ct = ctiles ? ctiles[q] : q;
+            int64_t i = ct / nt, j = ct % nt;
+            int codec = o->ccode[ct];
+            int cins = 0;
+            if (d->beta != 0.0) {
+                int64_t ldcin;
+                const double *ctp = orc_src_tile(sC, nb, i, j, cbuf, &ldcin);
+                cins = orc_scale_exp(o->MC[ct], codec);
+                orc_pack_tile(ctp, ldcin, nb, codec, cins, 0, cin);
             }
-            free(acc); free(P); free(cpay); free(cin);
+            if (o->cin_scale) o->cin_scale[ct] = (int16_t)cins;
+            orc_acc_init(nb, codec, d->beta, cin, cins, acc);
+            /* O9 fold order: SUMMA step, class from high code to low, l ascending */
+            int64_t np = 0;
+            for (int64_t s0 = 0; s0 < kt; s0 += ORC_STEP_DEPTH) {
+                int64_t s1 = s0 + ORC_STEP_DEPTH < kt ? s0 + ORC_STEP_DEPTH : kt;
+                for (int c = ORC_NCLS - 1; c >= 0; --c)
+                    for (int64_t l = s0; l < s1; ++l) {
+                        int ca = o->acode[i * kt + l], cb = o->bcode[l * nt + j];
+                        if ((ca > cb ? ca : cb) != c) continue;
+                        pl[np] = l;
+                        pc[np] = c;
+                        ++np;
+                    }
+            }
+#pragma omp parallel for schedule(dynamic)
+            for (int64_t u = 0; u < np; ++u) {
+                int64_t l = pl[u];
+                int c = pc[u];
+                orc_tile_gemm(c, Ap[(i * kt + l) * ORC_NCLS + c], Bp[(l * nt + j) * ORC_NCLS + c], nb,
+                              P + u * tsz);
+            }
+            for (int64_t u = 0; u < np; ++u) {
+                int64_t l = pl[u];
+                int c = pc[u];
+                orc_fold(nb, codec, d->alpha, o->ascale5[(i * kt + l) * ORC_NCLS + c],
+                         o->bscale5[(l * nt + j) * ORC_NCLS + c], P + u * tsz, acc);
+            }
+            double *wdst = compact ? (o->W ? o->W + q * tsz : NULL) : (o->W ? o->W + i * nb * o->ldw + j * nb : NULL);
+            int64_t ldw = compact ? nb : o->ldw;
+            if (wdst)
+                for (int64_t r = 0; r < nb; ++r) memcpy(wdst + r * ldw, acc + r * nb, sizeof(double) * nb);
+            double *cdst = compact ? Cout + q * tsz : Cout + i * nb * ldo + j * nb;
+            int e = orc_finalize(nb, codec, acc, cpay, cdst, compact ? nb : ldo);
+            if (o->cscale) o->cscale[ct] = (int16_t)e;
         }
+        free(acc); free(cpay); free(cin); free(cbuf); free(pl); free(pc); free(P);
         o->threads = nthreads;
     }
     for (int64_t t = 0; t < nA * ORC_NCLS; ++t) free(Ap[t]);
     for (int64_t t = 0; t < nB * ORC_NCLS; ++t) free(Bp[t]);
     free(Ap); free(Bp); free(fA); free(fB); free(fC); free(sa); free(sb);
     return rc;
+}
+
+int orc_gemm_mp(const orc_desc_t *d, const double *A, int64_t lda, const double *B,
+                int64_t ldb, const double *C, int64_t ldc, double *Cout, int64_t ldo,
+                const int64_t *ctiles, int64_t n_ctiles, orc_out_t *o) {
+    orc_src_t sA = {A, lda, 0, 0, 0, 0, 0, 0, 0, 0};
+    orc_src_t sB = {B, ldb, 0, 0, 0, 0, 0, 0, 0, 0};
+    orc_src_t sC = {C, ldc, 0, 0, 0, 0, 0, 0, 0, 0};
+    return orc_gemm_mp_core(d, &sA, &sB, &sC, Cout, ldo, ctiles, n_ctiles, 0, o);
+}
+
+/* The same method on the O1 synthetic workload, generated
+ * tile by tile (A: M x K, B: K x N, C: M x N with the given seeds / modes / E / s / tau):
+ * the listed C tiles are written compactly (Cout + q*nb*nb; o->W likewise when set). */
+typedef struct { uint64_t seed, tau; int mode, E, s; } orc_synth_t;
+
+int orc_gemm_mp_synth(const orc_desc_t *d, const orc_synth_t *ga, const orc_synth_t *gb, const orc_synth_t *gc,
+                      double *Cout, const int64_t *ctiles, int64_t n_ctiles, orc_out_t *o) {
+    orc_src_t sA = {NULL, 0, 1, d->M, d->K, ga->seed, ga->tau, ga->mode, ga->E, ga->s};
+    orc_src_t sB = {NULL, 0, 1, d->K, d->N, gb->seed, gb->tau, gb->mode, gb->E, gb->s};
+    orc_src_t sC = {NULL, 0, 1, d->M, d->N, gc->seed, gc->tau, gc->mode, gc->E, gc->s};
+    return orc_gemm_mp_core(d, &sA, &sB, &sC, Cout, 0, ctiles, n_ctiles, 1, o);
 }
 
 int orc_max_threads(void) {

@@ -88,7 +88,12 @@ def test_n65536_fullsize_properties(cfg):
     their class and fail it for the next-lower-precision enabled class (O5, norms in
     binary64 by torch, a 1e-9 band around the threshold is skipped); (3) two sampled
     row panels of C meet the tolerance against a cuBLAS DGEMM of those panels, with
-    the global normaliser; (4) repeated executes are bitwise identical."""
+    the global normaliser; (4) repeated executes are bitwise identical; (5) cfg3: the
+    oracle's streaming driver (inputs generated tile by tile, oracle.gemm_mp_synth)
+    computes the maps of all 2048 A/B tiles and one whole C tile (32 tile-GEMMs of
+    2048^3 in its emulated class arithmetic, O9 fold order): maps and scales bitwise,
+    the GPU's W and C tiles within the parity bound, C_out = the exact finalize of the
+    GPU's W."""
     w = gmp_inputs.workload(cfg)
     nb = w.nb
     mt, nt, kt = w.M // nb, w.N // nb, w.K // nb
@@ -147,6 +152,8 @@ def test_n65536_fullsize_properties(cfg):
         err = float(torch.linalg.norm(out[rows, :] - ref))
         assert err / den <= w.tol, (i, err / den)
         del ref
+    if cfg == 3:   # (5) full-size parity against the oracle on one sampled C tile
+        _oracle_tile_parity(g, w, out, mt, nt)
     panels = [slice(0, nb), slice((mt // 2) * nb, (mt // 2 + 1) * nb), slice((mt - 1) * nb, mt * nb)]
     first = [out[p].clone() for p in panels]
     g.execute(out)                                                              # (4)
@@ -155,3 +162,31 @@ def test_n65536_fullsize_properties(cfg):
     g.close()
     del A, Bm, out, first
     torch.cuda.empty_cache()
+
+
+def _oracle_tile_parity(g, w, out, mt, nt):
+    from gpu_harness import gpu_w_tile, tile_bound
+    nb = w.nb
+    gen = lambda r: (r.seed, r.mode, r.E, r.s, r.tau)   # noqa: E731
+    i, j = mt - 2, 5
+    o = oracle.gemm_mp_synth(w.M, w.N, w.K, nb, w.tol, gen(w.a), gen(w.b), gen(w.c), [i * nt + j],
+                             alpha=w.alpha, beta=w.beta, class_mask=w.class_mask)
+    assert o["rc"] == 0
+    gm = g.maps()
+    for k in ("acode", "bcode", "ccode"):
+        assert np.array_equal(gm[k], o[k]), k
+    kt = o["acode"].shape[1]
+    assert np.array_equal(gm["ascale"], o["ascale5"][np.arange(mt)[:, None], np.arange(kt)[None, :], o["acode"]])
+    assert np.array_equal(gm["bscale"], o["bscale5"][np.arange(kt)[:, None], np.arange(nt)[None, :], o["bcode"]])
+    code = int(o["ccode"][i, j])
+    Wg = gpu_w_tile(g, i, j, code, nb)
+    Wo = o["W"][0]
+    bound = tile_bound(o, i, j, w.K)
+    relw = np.linalg.norm(Wg - Wo) / np.linalg.norm(Wo)
+    assert relw <= bound, relw
+    cg = out[i * nb:(i + 1) * nb, j * nb:(j + 1) * nb].cpu().numpy()
+    rel = np.linalg.norm(cg - o["C"][0]) / np.linalg.norm(o["C"][0])
+    assert rel <= bound, rel
+    pay, user, e = oracle.finalize(Wg, code)
+    got, sc = g.tile("C", i, j, code)
+    assert sc == e and np.array_equal(got, pay.view(np.uint8)) and np.array_equal(cg, user)
