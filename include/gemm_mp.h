@@ -217,7 +217,9 @@ gmp_status_t gemm_mp_convert(gmp_plan_t plan, void *ws, size_t ws_bytes, void *s
  * C: 16-byte aligned, ldc even (GMP_ERR_ARG otherwise; C-finalize writes 16-byte vectors). */
 gmp_status_t gemm_mp_execute(gmp_plan_t plan, double *C, int64_t ldc, void *stream);
 
-/* gemm_mp_execute whose C-finalize (the only step that writes C) first waits for the CUDA
+/* S7 of SURVEY 8(a) (C-finalize, north_star "accumulating into C at C's tile precision"),
+ * with the C lifetime of SURVEY 8(b) ("C is written at execute") narrowed to the finalize:
+ * gemm_mp_execute whose C-finalize (the only step that writes C) first waits for the CUDA
  * event c_free_event (a cudaEvent_t; NULL = gemm_mp_execute): a caller streaming results
  * out of C (e.g. a device->host copy of the previous GEMM's C on another stream) overlaps
  * that copy with this execute's tile-GEMMs instead of serialising the whole execute behind
