@@ -2180,8 +2180,15 @@ extern "C" gmp_status_t gemm_mp_synth(double* out, int64_t ld, int64_t rows, int
 
 // Precision-aware ownership (NEXT-3, gmp_layout.h): default per-pair cost of class c =
 // 2 nb^3 / (library peak of c, TF/s, profiles/peaks_r01.json and the bench's sustained
-// measurements: DGEMM 35.5, BF16x9 155, FP16 1323, BF16 1397, E4M3 / E5M2 2628), per owned
-// tile 20 nb^2 bytes at 6 TB/s (stats read + pack read / write + finalize).
+// measurements: DGEMM 35.5, FP16 1323, BF16 1397, E4M3 / E5M2 2628), per owned tile
+// 20 nb^2 bytes at 6 TB/s (stats read + pack read / write + finalize).  The FP32 class
+// follows the kernel desc->flags select (R32): BF16x6 (default) BF16 / 6 = 233, BF16x9
+// (GMP_FLAG_FP32_X9) BF16 / 9 = 155, FFMA2 (GMP_FLAG_FP32_FFMA) the SGEMM rate 64.
+static double balance_fp32_peak(uint32_t flags) {
+  if (flags & GMP_FLAG_FP32_FFMA) return 64.0;
+  if (flags & GMP_FLAG_FP32_X9) return 1397.0 / 9.0;
+  return 1397.0 / 6.0;
+}
 extern "C" gmp_status_t gemm_mp_balance(const gmp_desc_t* desc, const uint8_t* acode, const uint8_t* bcode,
                                         const double* cost, int32_t* row_owner, int32_t* col_owner,
                                         double* imbalance) {
@@ -2197,7 +2204,8 @@ extern "C" gmp_status_t gemm_mp_balance(const gmp_desc_t* desc, const uint8_t* a
       cst[c] = cost[c];
     }
   } else {
-    const double peak[NC] = {35.5, 155.0, 1323.0, 1397.0, 2628.0, 2628.0, 5588.0};   // MXFP4: 4 x BF16 (nominal)
+    const double peak[NC] = {35.5, balance_fp32_peak(desc->flags), 1323.0, 1397.0, 2628.0, 2628.0,
+                             5588.0};   // MXFP4: 4 x BF16 (nominal)
     const double f = 2.0 * (double)nb * nb * nb;
     for (int c = 0; c < NC; ++c) cst[c] = f / (peak[c] * 1e12);
     cst[NC] = 20.0 * (double)nb * nb / 6.0e12;

@@ -215,16 +215,16 @@ inline void local_search(const BalanceModel& M, std::vector<int32_t>& rowP, std:
   }
 }
 
-// Alternating row / column local search from two starts (block-cyclic and LPT);
-// the better result (lexicographic max, sum of squares) wins, ties to block-cyclic.
+// Alternating row / column local search from several starts -- block-cyclic, LPT and
+// GMP_BALANCE_RESTARTS block-cyclic layouts with their tile rows / columns shuffled by a
+// fixed-seed SplitMix64 (deterministic: every rank gets the same owners) -- the best result
+// (lexicographic max, sum of squares) wins, ties to the earlier start.
+constexpr int GMP_BALANCE_RESTARTS = 8;
 inline void balance_layout(const BalanceModel& M, std::vector<int32_t>& rowP, std::vector<int32_t>& colQ) {
   rowP.resize(M.mt); colQ.resize(M.nt);
   for (int64_t i = 0; i < M.mt; ++i) rowP[i] = (int32_t)(i % M.P);
   for (int64_t j = 0; j < M.nt; ++j) colQ[j] = (int32_t)(j % M.Q);
   local_search(M, rowP, colQ);
-  std::vector<int32_t> r2, c2;
-  lpt_start(M, r2, c2);
-  local_search(M, r2, c2);
   auto obj = [&](const std::vector<int32_t>& r, const std::vector<int32_t>& c, double* mx, double* ss) {
     std::vector<double> Bk;
     M.blocks(r, c, Bk);
@@ -234,10 +234,34 @@ inline void balance_layout(const BalanceModel& M, std::vector<int32_t>& rowP, st
     double sum;
     M.objective(Bk, nr, nc, mx, ss, &sum);
   };
-  double m1, s1, m2, s2;
+  double m1, s1;
   obj(rowP, colQ, &m1, &s1);
-  obj(r2, c2, &m2, &s2);
-  if (obj_less(m2, s2, m1, s1)) { rowP = r2; colQ = c2; }
+  auto consider = [&](std::vector<int32_t>& r2, std::vector<int32_t>& c2) {
+    local_search(M, r2, c2);
+    double m2, s2;
+    obj(r2, c2, &m2, &s2);
+    if (obj_less(m2, s2, m1, s1)) { rowP = r2; colQ = c2; m1 = m2; s1 = s2; }
+  };
+  std::vector<int32_t> r2, c2;
+  lpt_start(M, r2, c2);
+  consider(r2, c2);
+  uint64_t st = 0x9E3779B97F4A7C15ull;
+  auto next = [&]() {   // SplitMix64
+    uint64_t z = (st += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  };
+  auto shuffled_cyclic = [&](int64_t n, int bins, std::vector<int32_t>& own) {
+    own.resize(n);
+    for (int64_t t = 0; t < n; ++t) own[t] = (int32_t)(t % bins);
+    for (int64_t t = n - 1; t > 0; --t) std::swap(own[t], own[(int64_t)(next() % (uint64_t)(t + 1))]);
+  };
+  for (int k = 0; k < GMP_BALANCE_RESTARTS; ++k) {
+    shuffled_cyclic(M.mt, M.P, r2);
+    shuffled_cyclic(M.nt, M.Q, c2);
+    consider(r2, c2);
+  }
 }
 
 }  // namespace gmp

@@ -25,7 +25,8 @@ from paper_2508_14848_b200 import api
 from paper_2508_14848_b200 import binding as B
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-PEAK = np.array([35.5, 155.0, 1323.0, 1397.0, 2628.0, 2628.0, 5588.0])   # the library's default model (TF/s)
+# the library's default model (TF/s); FP32 = BF16 / 6 for the default BF16x6 kernel (R32)
+PEAK = np.array([35.5, 1397.0 / 6.0, 1323.0, 1397.0, 2628.0, 2628.0, 5588.0])
 
 
 def golden_maps(cfg):
@@ -82,6 +83,25 @@ def test_balance_full_size_oracle_maps(cfg, grid):
     # deterministic
     ro2, co2, _ = B.gemm_mp_balance(d, a, b)
     assert np.array_equal(ro, ro2) and np.array_equal(co, co2)
+
+
+@pytest.mark.parametrize("flags,fp32_peak", [(0, 1397.0 / 6.0), (B.GMP_FLAG_FP32_X9, 1397.0 / 9.0),
+                                             (B.GMP_FLAG_FP32_FFMA, 64.0)])
+def test_balance_fp32_cost_follows_kernel(flags, fp32_peak):
+    """the built-in model prices an FP32 pair at the rate of the FP32-class kernel the flags
+    select (R32: BF16x6 default, BF16x9, FFMA2): the library's imbalance figures equal the
+    numpy evaluation of that model on the oracle's cfg3 maps (2 x 4)"""
+    a, b = golden_maps(3)
+    nb = 2048
+    d = B.make_desc(65536, 65536, 65536, nb, 1e-4, flags=flags, P=2, Q=4)
+    ro, co, (imb0, imb1) = B.gemm_mp_balance(d, a, b)
+    peak = PEAK.copy()
+    peak[1] = fp32_peak
+    f = 2.0 * nb ** 3
+    cost = np.concatenate([f / (peak * 1e12), [20.0 * nb * nb / 6.0e12]])
+    cyc = rank_costs(a, b, [i % 2 for i in range(a.shape[0])], [j % 4 for j in range(b.shape[1])], 2, 4, cost)
+    assert imb0 == pytest.approx(imbalance(cyc), rel=1e-12)
+    assert imb1 == pytest.approx(imbalance(rank_costs(a, b, ro, co, 2, 4, cost)), rel=1e-12)
 
 
 def test_balance_vs_brute_force_tiny():
