@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--ownership", default="auto", choices=["auto", "cyclic", "balanced"],
                     help="N > 1: tile ownership. cyclic = 2D block-cyclic (PAPER.md:179); balanced = "
                          "gemm_mp_balance (NEXT-3); auto (default) = balanced when it lowers the model's "
-                         "largest per-rank cost by >= 2 %% (2x4 at cfg3: 1.045 -> 1.001), else cyclic. Chosen "
+                         "largest per-rank cost by >= 2 %% (2x4 at cfg3: 1.031 -> 1.0006), else cyclic. Chosen "
                          "once from a block-cyclic plan's maps, outside the timed region")
     ap.add_argument("--balance", action="store_true", help="same as --ownership balanced")
     ap.add_argument("--sender", action="store_true",
