@@ -1694,6 +1694,7 @@ extern "C" gmp_status_t gemm_mp_convert(gmp_plan_t pl, void* ws_, size_t ws_byte
   uint8_t* ws = (uint8_t*)ws_;
   pl->ws = ws;
   pl->ctd_ldc = -1;   // the workspace is (re)claimed: execute re-uploads the C tile descriptors
+  pl->converted = false;   // a convert that fails part-way leaves no executable payloads
   const int64_t nb = pl->d.nb;
   auto cev = [&](int k) -> gmp_status_t {
     if (!pl->conv_ev.empty()) GMP_CUDA(cudaEventRecord(pl->conv_ev[k], stream));
@@ -1817,6 +1818,10 @@ static gmp_status_t execute_impl(gmp_plan_t pl, double* Cuser, int64_t ldc, void
   const int steps = pl->st.steps;
   const bool multi = pl->P * pl->Q > 1;
   cudaEvent_t ready = nullptr;
+  struct EventGuard {   // released on every return path (CUDA defers the destruction past its waits)
+    cudaEvent_t& e;
+    ~EventGuard() { if (e) cudaEventDestroy(e); }
+  } ready_guard{ready};
   if (multi && !pl->panels_valid) {
     int s0 = 0;
     if (pl->step0_issued) {
@@ -1898,7 +1903,6 @@ static gmp_status_t execute_impl(gmp_plan_t pl, double* Cuser, int64_t ldc, void
       if (!pl->launch_ev.empty()) GMP_CUDA(cudaEventRecord(pl->launch_ev[2 * li + 1], stream));
     }
   }
-  if (ready) cudaEventDestroy(ready);
   if (nCl) {
     unsigned long long* mb = (unsigned long long*)(ws + pl->off_maxbits);
     if (!pl->maxabs_idx.empty()) {
