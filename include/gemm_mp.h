@@ -319,7 +319,9 @@ gmp_status_t gemm_mp_synth_tiles(double *out, int64_t ld, int64_t rows, int64_t 
  * codeB(l,j))] + cost[7] x (A + B + C tiles it owns), by alternating row / column
  * local search (moves and swaps) from the block-cyclic start (R30).
  * cost: 8 doubles (relative per-pair time of classes 0..6, per-owned-tile time) or
- * NULL for the built-in B200 model.  Deterministic: every rank gets the same
+ * NULL for the built-in B200 model (per pair 2 nb^3 / library peak of the class; the
+ * FP32 entry follows the FP32-class kernel desc->flags select: BF16x6 by default,
+ * GMP_FLAG_FP32_X9, GMP_FLAG_FP32_FFMA).  Deterministic: every rank gets the same
  * owners from the same maps.  imbalance (may be NULL): {max/mean rank cost of the
  * block-cyclic layout, of the returned layout} -- never worse than block-cyclic.
  * Pass the owners as desc.row_owner / col_owner to gemm_mp_plan; the caller
